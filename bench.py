@@ -1,0 +1,366 @@
+#!/usr/bin/env python
+"""Benchmark: ParIS+ exact 1-NN queries/s on B200 (BASELINE.json metric, config 4 by default).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
+
+One step = one paris_knn_exact call answering the config's whole query batch (rows
+a3-a8 of SURVEY §8: query PAA, BSF seed, LB pass, candidate order, refinement,
+finalize) over a device-resident collection + SAX array.  Summarization (rows a1-a2)
+is timed in the same run as its own line item ("summarize").  Inputs are larger than
+L2 (config 4: SAX 1.6 GB, raw 102.4 GB vs 126 MB L2), so no flush is needed.
+
+Multi-GPU (torchrun): weak scaling -- every rank holds its own collection of the
+config's size and answers its own queries (queries are independent problems); no
+data-path collective; the only NCCL calls are the timing barrier/max.
+--impl reference: the CPU oracle (oracle/, single thread) timed on a bounded sample of
+the same workload, scaled to queries/s over the full collection.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    1: dict(n=100_000, len=256, nq=100, k=1, queries="fresh", desc="C1: 1e5 x 256 fp32 RW, 100 fresh RW queries, exact 1-NN"),
+    2: dict(n=1_000_000, len=256, nq=1000, k=1, queries="noise0.05", desc="C2: 1e6 x 256 fp32 RW, 1000 member+N(0,0.05^2) queries, exact 1-NN"),
+    3: dict(n=10_000_000, len=128, nq=1000, k=1, queries="fresh", batch=8, desc="C3: 1e7 x 128 fp32 RW, 1000 fresh RW queries, exact 1-NN"),
+    4: dict(n=100_000_000, len=256, nq=100, k=1, queries="fresh", desc="C4: 1e8 x 256 fp32 RW (102.4 GB raw + 1.6 GB SAX in HBM), 100 fresh RW queries, exact 1-NN"),
+    5: dict(n=20_000_000, len=256, nq=200, k=1, queries="noise0.05", desc="C5: 2e7 x 256 fp32 RW, 200 member+N(0,0.05^2) queries, exact 1-NN"),
+}
+W, CARD = 16, 256
+
+
+def log(*a):
+    print("[bench]", *a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms while running."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy R+W)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kernel: str, config: int):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    return d.get(f"C{config}", {}).get(kernel)
+
+
+# --------------------------------------------------------------------------- CPU oracle arm
+def oracle_sample(raw_dev, queries_dev, k, n_sample, nq_sample):
+    """Time the oracle's LB-pruned exact search (its own SAX) on the first n_sample series
+    for nq_sample queries; returns (seconds per query on the sample, threads)."""
+    import numpy as np
+    import oracle
+    x = raw_dev[:n_sample].cpu().numpy()
+    q = queries_dev[:nq_sample].cpu().numpy()
+    sax = oracle.summarize(x, W, CARD)
+    t0 = time.perf_counter()
+    oracle.knn_pruned(x, sax, q, k, W, CARD)
+    dt = time.perf_counter() - t0
+    del x, sax
+    _ = np
+    return dt / nq_sample
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import torch
+    from datagen import gpu as dg
+    cfg = CONFIGS[args.config]
+    n, length, nq, k = cfg["n"], cfg["len"], cfg["nq"], cfg["k"]
+    dev = torch.device("cuda:0") if torch.cuda.is_available() else None
+    n_sample = min(n, args.ref_sample)
+    log(f"reference arm: oracle on {n_sample} of {n} series")
+    if dev is not None:
+        ds, qs = __import__("datagen").config_seeds(args.config)
+        raw = dg.walks(n_sample, length, ds, device=dev)
+        queries = dg.walks(max(2, args.ref_queries), length, qs, device=dev)
+    else:
+        import datagen
+        ds, qs = datagen.config_seeds(args.config)
+        raw = torch.from_numpy(datagen.random_walks(n_sample, length, ds))
+        queries = torch.from_numpy(datagen.random_walks(max(2, args.ref_queries), length, qs))
+    per_q = []
+    for i in range(args.warmup + args.steps):
+        t = oracle_sample(raw, queries, k, n_sample, args.ref_queries)
+        if i >= args.warmup:
+            per_q.append(t * (n / n_sample))  # scaled to the full collection (linear in n)
+    sec_per_query = statistics.mean(per_q)
+    value = 1.0 / sec_per_query
+    sample = (f"oracle_knn_pruned (single thread, fp64) over the first {n_sample} series of {cfg['desc']}, "
+              f"{args.ref_queries} queries per step, time scaled x{n / n_sample:.0f} to n={n}")
+    line = {"impl": "reference", "metric": "exact 1-NN queries/sec", "value": value, "unit": "queries/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": sec_per_query * nq * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["desc"], "n": n, "len": length, "w": W, "card": CARD, "nq": nq, "k": k},
+            "cpu_baseline": {"value": value, "unit": "queries/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- GPU arm
+def run_gpu(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2009_00166_b200 as P
+    from datagen import gpu as dg
+    import datagen
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = CONFIGS[args.config]
+    n, length, nq, k = cfg["n"], cfg["len"], cfg["nq"], cfg["k"]
+    if args.n:
+        n = args.n
+    if args.nq:
+        nq = args.nq
+    batch = args.batch or cfg.get("batch", 8)
+    ds, qs = datagen.config_seeds(args.config)
+    ds += 7919 * rank  # weak scaling: every rank owns a distinct collection
+    qs += 7919 * rank
+
+    t0 = time.time()
+    raw = dg.walks(n, length, ds, device=dev)
+    if cfg["queries"] == "fresh":
+        queries = dg.walks(nq, length, qs, device=dev)
+    else:
+        queries, _ = dg.noisy_members(raw, nq, float(cfg["queries"][5:]), qs)
+    sax = torch.empty((W, n), dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+    log(f"rank {rank}: generated n={n} len={length} nq={nq} in {time.time() - t0:.1f}s")
+    st = torch.cuda.current_stream()
+    kcfg = P.KnnConfig(batch=batch)
+
+    # ---- summarize (rows a1-a2): warmup + timed
+    for _ in range(args.warmup):
+        P.summarize(raw, W, CARD, out=sax)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(args.steps):
+        P.summarize(raw, W, CARD, out=sax)
+    e1.record(st)
+    torch.cuda.synchronize()
+    sum_ms = e0.elapsed_time(e1) / args.steps
+
+    # ---- query step: warmup (also collects stats once)
+    out_idx = torch.empty((nq, k), dtype=torch.int64, device=dev)
+    out_dist = torch.empty((nq, k), dtype=torch.float32, device=dev)
+    _, _, stats = P.knn_exact(raw, sax, queries, k=k, w=W, card=CARD, out_idx=out_idx,
+                              out_dist=out_dist, config=kcfg, stats=True)
+    for _ in range(max(0, args.warmup - 1)):
+        P.knn_exact(raw, sax, queries, k=k, w=W, card=CARD, out_idx=out_idx, out_dist=out_dist, config=kcfg)
+    torch.cuda.synchronize()
+
+    # ---- timed region (device events, max over ranks); per-kernel events via libparis profiling
+    P.profile_reset()
+    P.profile_enable(True)
+    launches0 = P.launch_count()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        e0.record(st)
+        for _ in range(args.steps):
+            P.knn_exact(raw, sax, queries, k=k, w=W, card=CARD, out_idx=out_idx, out_dist=out_dist, config=kcfg)
+        e1.record(st)
+        torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    launches = P.launch_count() - launches0
+    P.profile_enable(False)
+    prof = P.profile_read()
+    step_ms = e0.elapsed_time(e1) / args.steps
+    t_max = torch.tensor([step_ms], device=dev)
+    if ws > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    step_ms_max = float(t_max.item())
+    value = nq * ws / (step_ms_max / 1e3)
+
+    # ---- e2e through the same ABI call with HOST (pinned) buffers
+    hq = queries.cpu().pin_memory()
+    hidx = torch.empty((nq, k), dtype=torch.int64).pin_memory()
+    hdist = torch.empty((nq, k), dtype=torch.float32).pin_memory()
+    P.knn_exact(raw, sax, hq, k=k, w=W, card=CARD, out_idx=hidx, out_dist=hdist, config=kcfg)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(args.steps):
+        P.knn_exact(raw, sax, hq, k=k, w=W, card=CARD, out_idx=hidx, out_dist=hdist, config=kcfg)
+    e1.record(st)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+    t_e2e = torch.tensor([e2e_ms], device=dev)
+    if ws > 1:
+        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+    e2e_value = nq * ws / (float(t_e2e.item()) / 1e3)
+    assert torch.equal(hidx, out_idx.cpu()), "host-buffer path disagrees with device path"
+
+    # ---- roofline of the dominant kernel (algorithmic bytes / event-timed duration)
+    peak, peak_src = measured_peaks()
+    cand = stats["candidates"].numpy().astype(np.float64)
+    refined = stats["refined"].numpy().astype(np.float64)
+    kern = {}
+    for name, (cnt, ms) in prof.items():
+        kern[name] = {"launches": cnt, "ms_per_step": ms / args.steps, "share": None}
+    tot = sum(v["ms_per_step"] for v in kern.values()) or 1.0
+    for v in kern.values():
+        v["share"] = v["ms_per_step"] / tot
+    nbatches = (nq + batch - 1) // batch
+    alg = {
+        # SAX bytes per pass + 8 B per candidate written
+        "lb_pass": (nbatches * n * W + 8.0 * cand.sum()) / nbatches,
+        # raw bytes per refined series (K6)
+        "refine": 4.0 * length * refined.sum() / nbatches,
+    }
+    dom = max(kern, key=lambda s: kern[s]["ms_per_step"]) if kern else None
+    roof = None
+    if dom:
+        per_launch_ms = kern[dom]["ms_per_step"] * args.steps / prof[dom][0]
+        by = alg.get(dom)
+        for name, v in kern.items():
+            if name in alg:
+                pl = v["ms_per_step"] * args.steps / prof[name][0]
+                v["achieved_gbs"] = alg[name] / (pl / 1e3) / 1e9
+        if by is not None:
+            ach = by / (per_launch_ms / 1e3) / 1e9
+            roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                    "frac": ach / peak, "traffic": ncu_traffic(dom, args.config),
+                    "algorithmic_bytes_per_launch": by, "launch_ms": per_launch_ms, "peak_source": peak_src}
+    sum_bytes = n * (4.0 * length + W)
+    summarize = {"series_per_s": n / (sum_ms / 1e3), "ms": sum_ms, "unit": "series/s",
+                 "roofline": {"kernel": "summarize", "bound": "hbm", "achieved": sum_bytes / (sum_ms / 1e3) / 1e9,
+                              "peak": peak, "unit": "GB/s", "frac": sum_bytes / (sum_ms / 1e3) / 1e9 / peak,
+                              "traffic": ncu_traffic("summarize", args.config),
+                              "algorithmic_bytes_per_launch": sum_bytes}}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        n_sample = min(n, args.ref_sample)
+        t_q = oracle_sample(raw, queries, k, n_sample, args.ref_queries)
+        cpu = {"value": 1.0 / (t_q * n / n_sample), "unit": "queries/s", "cores": 1, "kind": "oracle",
+               "sample": f"oracle_knn_pruned (1 thread, fp64) over the first {n_sample} series, "
+                         f"{args.ref_queries} queries, time scaled x{n / n_sample:.0f} to n={n}"}
+
+    if rank == 0:
+        line = {
+            "metric": "exact 1-NN queries/sec", "value": value, "unit": "queries/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms_max,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded Philox random walks, z-normalized; no dataset on the box)",
+            "config": {"workload": cfg["desc"], "n": n, "len": length, "w": W, "card": CARD, "nq": nq, "k": k,
+                       "batch": batch, "parallelism": f"weak x{ws} (independent collections + queries per GPU)",
+                       "l2": "inputs larger than L2 (no flush)"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": nq * length * 4,
+                    "d2h_bytes_per_step": nq * k * 12},
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "summarize": summarize,
+            "kernels": kern,
+            "pruning": {"candidates_mean": float(cand.mean()), "refined_mean": float(refined.mean()),
+                        "pruning_ratio": float(1.0 - refined.mean() / n),
+                        "tau_seed_mean": float(stats["tau_seed"].mean())},
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="paris", choices=["paris", "reference"])
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--n", type=int, default=0, help="override n (debug only)")
+    ap.add_argument("--nq", type=int, default=0, help="override query count (debug only)")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-sample", type=int, default=2_000_000)
+    ap.add_argument("--ref-queries", type=int, default=4)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "paris" else args.warmup
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,141 @@
+/*
+ * paris.h -- C ABI of libparis: the B200 (sm_100a) hot path of ParIS+ exact
+ * whole-series k-NN search over an in-HBM iSAX summary array.
+ *
+ * Paper: Peng, Fatourou, Palpanas, "ParIS+: Data Series Indexing on Multi-Core
+ * Architectures" (arXiv 2009.00166).  "P:N" cites line N of its LaTeX source
+ * (PAPER.md); "S:N" a line of SPEC.md; readings (R#) are listed in DESIGN.md.
+ *
+ * Conventions for every entry point
+ *   - raw / queries: fp32, row-major [count][len], 16-byte aligned, finite values
+ *     (non-finite input is the caller's responsibility).
+ *   - sax: uint8 structure-of-arrays [w][n]: the symbol of segment s of series i
+ *     is sax[s*n + i], in [0, card).  (The paper's SAX[p] array holds the word of
+ *     series p at position p; it is stored segment-major here so a
+ *     warp reads one segment of 128 consecutive series with one 128-byte request.)
+ *   - Unless stated otherwise pointers are DEVICE pointers owned by the caller
+ *     (e.g. torch tensors); the library never frees or retains them.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Work is ordered
+ *     on it; see each call for when results are valid.
+ *   - Return 0 on success or a negative PARIS_E* code; paris_last_error() gives a
+ *     thread-local message.  On error nothing is promised about the outputs.
+ *   - Supported: 1 <= n < 2^31 series, len % 4 == 0, 4 <= len <= 4096, w | len,
+ *     1 <= w <= 64, card a power of two in [2, 256] (8-bit symbols P:294).
+ *     Fast paths: len % 128 == 0 with (len/w) % 4 == 0 and len/w <= 128 for
+ *     summarize; n % 16 == 0 for the SAX scans (other n run a byte-granular tail).
+ */
+#ifndef PARIS_H_
+#define PARIS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PARIS_OK 0
+#define PARIS_EINVAL (-1)  /* null pointer, n < 1, nq < 0, k < 1, k > n, k > PARIS_MAX_K */
+#define PARIS_ECONFIG (-2) /* unsupported (len, w, card) -- see the list above */
+#define PARIS_ECUDA (-3)   /* a CUDA launch/runtime error; details in paris_last_error() */
+#define PARIS_ENOMEM (-4)  /* scratch allocation failed */
+
+#define PARIS_MAX_K 1024
+
+/*
+ * paris_summarize -- ConvertToSAX over a whole collection (IndexBulkLoading,
+ * Alg2 line al2:cover): for every series i,
+ *   PAA  paa[s] = mean of points [s*len/w, (s+1)*len/w)
+ *   iSAX out_sax[s*n + i] = #{k in 1..card-1 : cut_k <= paa[s]},
+ *        cut_k = Phi^-1(k/card) (N(0,1) equiprobable breakpoints, R2;
+ *        a value on a cut goes to the upper region, R3).
+ * The symbol is decided as if PAA were computed exactly: an fp32 PAA whose
+ * rounding-error bound straddles a cut is recomputed in fp64.
+ *   raw      device [n][len] fp32
+ *   out_sax  device [w][n] uint8 (caller-allocated, n*w bytes)
+ * Asynchronous: returns after enqueueing; results valid once `stream` completes.
+ */
+int paris_summarize(const float* raw, int64_t n, int32_t len, int32_t w, int32_t card,
+                    uint8_t* out_sax, void* stream);
+
+/*
+ * paris_knn_exact -- exact k-NN under Euclidean distance (k-NN per
+ * S:406-414) following ParIS+ ExactSearch (Alg9):
+ *   1. BSF seed (approximate search analog, R8): the lower bound over
+ *      a sample of the SAX array ranks seed series; their true distances give an
+ *      upper bound tau_seed on the k-th NN distance.
+ *   2. LBC pass (Alg10): MINDIST_PAA_iSAX (R1) for every
+ *      series' word; a series is a candidate iff its (rigorous, round-down fp32)
+ *      LB^2 <= tau_seed^2 (rounded up).  Candidates are compacted per query.
+ *   3. RDC pass (Alg11): candidates are refined in two waves -- the
+ *      ~lowest-LB ones first, then the rest -- each re-checked against the live
+ *      BSF before its raw series is read; true squared ED with early abandoning;
+ *      the BSF (k-th best) is shared through atomics.
+ *   4. Result: ascending (distance, id); ties go to the lower id (R6).
+ *   raw       device [n][len] fp32           sax  device [w][n] uint8 (paris_summarize)
+ *   queries   [nq][len] fp32                 -- device OR host memory
+ *   out_idx   [nq][k] int64 series ids       -- device OR host memory
+ *   out_dist  [nq][k] fp32 Euclidean (rooted) distance -- device OR host memory
+ * queries/out_idx/out_dist may be host pointers (pageable or pinned): the library
+ * then stages them through device memory on `stream`.
+ * Synchronizes `stream` once per call (to check per-query candidate-buffer
+ * overflow; an overflowed query is re-scanned with an exact-size buffer), so on
+ * return the outputs are final.  nq == 0 is a no-op.
+ */
+int paris_knn_exact(const float* raw, const uint8_t* sax, int64_t n, const float* queries,
+                    int32_t nq, int32_t k, int64_t* out_idx, float* out_dist, int32_t len,
+                    int32_t w, int32_t card, void* stream);
+
+/* Tunables for paris_knn_exact_ex (0 = library default). */
+typedef struct paris_knn_config {
+  int32_t batch;        /* queries per SAX pass (1..8); default 8 */
+  int32_t seed_div;     /* seed sample = n / seed_div series (default 16) */
+  int32_t wave_a;       /* candidates refined in the first (lowest-LB) wave: max(wave_a, 2k) */
+  int32_t reserved[5];
+} paris_knn_config;
+
+/* Per-query counters (host memory, arrays of nq), filled by paris_knn_exact_ex. */
+typedef struct paris_knn_stats {
+  int64_t* candidates;  /* series whose LB passed tau_seed (Alg10 list length)       */
+  int64_t* refined;     /* raw series read and distance computed (Alg11 line al9:rcal) */
+  float* tau_seed;      /* seed BSF distance (rooted)                                 */
+} paris_knn_stats;
+
+/* Same as paris_knn_exact with tunables and optional stats (either may be NULL). */
+int paris_knn_exact_ex(const float* raw, const uint8_t* sax, int64_t n, const float* queries,
+                       int32_t nq, int32_t k, int64_t* out_idx, float* out_dist, int32_t len,
+                       int32_t w, int32_t card, void* stream, const paris_knn_config* config,
+                       paris_knn_stats* stats);
+
+/* Thread-local text of the last failure (never NULL). */
+const char* paris_last_error(void);
+
+/* ABI version (major*100 + minor). */
+int32_t paris_version(void);
+
+/* Test hook: the library's own fp64 breakpoints cut_1..cut_{card-1} (R2) into
+ * out[0..card-2] (host memory).  PARIS_ECONFIG for a bad card. */
+int paris_debug_cuts(int32_t card, double* out);
+
+/*
+ * Launch accounting / per-kernel device time (for benchmarks).
+ *   paris_profile_enable(1): every kernel launch is bracketed by CUDA events on its
+ *   stream; paris_profile_read() synchronizes on those events and returns, per
+ *   kernel name, the launch count and the summed device milliseconds.
+ *   paris_launch_count() counts every kernel launched by the library (always on).
+ */
+typedef struct paris_kernel_profile {
+  char name[48];
+  int64_t launches;
+  double total_ms;
+} paris_kernel_profile;
+
+void paris_profile_enable(int32_t on);
+void paris_profile_reset(void);
+int32_t paris_profile_read(paris_kernel_profile* out, int32_t max_entries);
+int64_t paris_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PARIS_H_ */

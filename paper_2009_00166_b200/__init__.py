@@ -1,0 +1,17 @@
+"""paper_2009_00166_b200 -- B200-native hot path of ParIS+ exact k-NN search.
+
+Thin Python binding (argument marshalling only) over the C ABI of
+``libparis.so`` declared in ``include/paris.h``: every step of the path runs in
+the library's CUDA kernels (sm_100a).  PyTorch provides device memory and
+streams.  There is no CPU fallback: if the extension is missing or no CUDA
+device is present, every call raises.
+
+    sax = summarize(raw, w=16, card=256)                    # [w][n] uint8
+    idx, dist = knn_exact(raw, sax, queries, k=1, w=16, card=256)
+"""
+from ._binding import (  # noqa: F401
+    PARIS_EINVAL, PARIS_ECONFIG, PARIS_ECUDA, PARIS_ENOMEM, PARIS_MAX_K,
+    ParisError, KnnConfig, library_path, load, summarize, knn_exact, last_error,
+    profile_enable, profile_reset, profile_read, launch_count, version, debug_cuts,
+    symbols,
+)

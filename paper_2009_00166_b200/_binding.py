@@ -1,0 +1,217 @@
+"""ctypes binding for libparis.so (include/paris.h).  Marshalling only."""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+import threading
+from dataclasses import dataclass
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_ROOT = os.path.dirname(_PKG)
+_LIBPATH = os.path.join(_PKG, "libparis.so")
+_HEADER = os.path.join(_ROOT, "include", "paris.h")
+
+PARIS_EINVAL = -1
+PARIS_ECONFIG = -2
+PARIS_ECUDA = -3
+PARIS_ENOMEM = -4
+PARIS_MAX_K = 1024
+
+_lock = threading.Lock()
+_lib = None
+
+
+class ParisError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"libparis error {code}: {msg}")
+        self.code = code
+
+
+class _Config(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int32), ("seed_div", ctypes.c_int32),
+                ("wave_a", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [("candidates", ctypes.c_void_p), ("refined", ctypes.c_void_p),
+                ("tau_seed", ctypes.c_void_p)]
+
+
+class _KProf(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 48), ("launches", ctypes.c_int64),
+                ("total_ms", ctypes.c_double)]
+
+
+@dataclass
+class KnnConfig:
+    batch: int = 0      # queries per SAX pass (1..8), 0 = default (8)
+    seed_div: int = 0   # seed sample = n / seed_div (0 = 16)
+    wave_a: int = 0     # first refinement wave size (0 = 256)
+
+
+def library_path() -> str:
+    return _LIBPATH
+
+
+def load():
+    """Load libparis.so (must have been built: __graft_entry__.build()).  Raises if missing."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(_LIBPATH):
+            raise ParisError(PARIS_ECUDA, f"CUDA extension not built: {_LIBPATH} is missing "
+                             "(run python -c 'import __graft_entry__ as g; g.build()')")
+        lib = ctypes.CDLL(_LIBPATH)
+        P, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
+        lib.paris_summarize.argtypes = [P, i64, i32, i32, i32, P, P]
+        lib.paris_summarize.restype = ctypes.c_int
+        lib.paris_knn_exact.argtypes = [P, P, i64, P, i32, i32, P, P, i32, i32, i32, P]
+        lib.paris_knn_exact.restype = ctypes.c_int
+        lib.paris_knn_exact_ex.argtypes = [P, P, i64, P, i32, i32, P, P, i32, i32, i32, P,
+                                           ctypes.POINTER(_Config), ctypes.POINTER(_Stats)]
+        lib.paris_knn_exact_ex.restype = ctypes.c_int
+        lib.paris_last_error.restype = ctypes.c_char_p
+        lib.paris_version.restype = i32
+        lib.paris_profile_enable.argtypes = [i32]
+        lib.paris_profile_read.argtypes = [ctypes.POINTER(_KProf), i32]
+        lib.paris_profile_read.restype = i32
+        lib.paris_launch_count.restype = i64
+        lib.paris_debug_cuts.argtypes = [i32, P]
+        lib.paris_debug_cuts.restype = ctypes.c_int
+        _lib = lib
+        return lib
+
+
+def symbols():
+    """Function names declared in include/paris.h."""
+    txt = open(_HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(paris_\w+)\s*\(", txt)))
+
+
+def last_error() -> str:
+    return load().paris_last_error().decode()
+
+
+def version() -> int:
+    return int(load().paris_version())
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise ParisError(rc, last_error())
+
+
+def _stream(stream):
+    if stream is None:
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, torch.cuda.Stream):
+        return ctypes.c_void_p(stream.cuda_stream)
+    return ctypes.c_void_p(int(stream))
+
+
+def _need_cuda(t: torch.Tensor, name: str):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (the index lives in HBM)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+def summarize(raw: torch.Tensor, w: int = 16, card: int = 256, out: torch.Tensor | None = None,
+              stream=None) -> torch.Tensor:
+    """PAA + iSAX of every row of raw ([n][len] fp32, CUDA) -> uint8 [w][n] (segment-major)."""
+    lib = load()
+    _need_cuda(raw, "raw")
+    if raw.dtype != torch.float32 or raw.dim() != 2:
+        raise ValueError("raw must be [n][len] float32")
+    n, length = raw.shape
+    if out is None:
+        out = torch.empty((w, n), dtype=torch.uint8, device=raw.device)
+    _need_cuda(out, "out")
+    if out.dtype != torch.uint8 or out.numel() != n * w:
+        raise ValueError("out must be uint8 with n*w elements")
+    _check(lib.paris_summarize(raw.data_ptr(), n, length, w, card, out.data_ptr(), _stream(stream)))
+    return out
+
+
+def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: int = 1,
+              w: int = 16, card: int = 256, out_idx: torch.Tensor | None = None,
+              out_dist: torch.Tensor | None = None, stream=None,
+              config: KnnConfig | None = None, stats: bool = False):
+    """Exact k-NN of every query (rows of `queries`, CUDA or host) over raw/sax (CUDA).
+
+    Returns (idx int64 [nq][k], dist float32 [nq][k]) on the device of `queries`
+    (or the given out tensors); with stats=True also a dict of per-query counters.
+    """
+    lib = load()
+    _need_cuda(raw, "raw")
+    _need_cuda(sax, "sax")
+    if not queries.is_contiguous():
+        queries = queries.contiguous()
+    if queries.dtype != torch.float32:
+        raise ValueError("queries must be float32")
+    if queries.dim() == 1:
+        queries = queries.unsqueeze(0)
+    n, length = raw.shape
+    nq = queries.shape[0]
+    if queries.shape[1] != length:
+        raise ValueError("query length differs from series length")
+    if sax.dtype != torch.uint8 or sax.numel() != n * w:
+        raise ValueError("sax must be uint8 [w][n]")
+    dev = queries.device
+    pin = (not queries.is_cuda) and torch.cuda.is_available()
+    if out_idx is None:
+        out_idx = torch.empty((nq, k), dtype=torch.int64, device=dev, pin_memory=pin)
+    if out_dist is None:
+        out_dist = torch.empty((nq, k), dtype=torch.float32, device=dev, pin_memory=pin)
+    cfg = None
+    if config is not None:
+        cfg = _Config(config.batch, config.seed_div, config.wave_a)
+    st = None
+    arrays = None
+    if stats:
+        arrays = (torch.zeros(nq, dtype=torch.int64), torch.zeros(nq, dtype=torch.int64),
+                  torch.zeros(nq, dtype=torch.float32))
+        st = _Stats(arrays[0].data_ptr(), arrays[1].data_ptr(), arrays[2].data_ptr())
+    rc = lib.paris_knn_exact_ex(raw.data_ptr(), sax.data_ptr(), n, queries.data_ptr(), nq, k,
+                                out_idx.data_ptr(), out_dist.data_ptr(), length, w, card,
+                                _stream(stream), ctypes.byref(cfg) if cfg else None,
+                                ctypes.byref(st) if st else None)
+    _check(rc)
+    if stats:
+        return out_idx, out_dist, {"candidates": arrays[0], "refined": arrays[1],
+                                   "tau_seed": arrays[2]}
+    return out_idx, out_dist
+
+
+def profile_enable(on: bool = True):
+    load().paris_profile_enable(1 if on else 0)
+
+
+def profile_reset():
+    load().paris_profile_reset()
+
+
+def profile_read() -> dict:
+    """{kernel name: (launches, total device ms)} since the last reset (synchronizes)."""
+    lib = load()
+    n = lib.paris_profile_read(None, 0)
+    buf = (_KProf * max(1, n))()
+    n = lib.paris_profile_read(buf, n)
+    return {buf[i].name.decode(): (int(buf[i].launches), float(buf[i].total_ms)) for i in range(n)}
+
+
+def launch_count() -> int:
+    return int(load().paris_launch_count())
+
+
+def debug_cuts(card: int):
+    """The library's own N(0,1) breakpoints (fp64) -- for tests."""
+    import numpy as np
+    out = np.zeros(256, dtype=np.float64)
+    _check(load().paris_debug_cuts(card, out.ctypes.data))
+    return out[: card - 1].copy()

@@ -1,0 +1,81 @@
+"""Build libparis.so (the C-ABI library) and the harness datagen library in-tree.
+
+nvcc -gencode arch=compute_100a,code=sm_100a (B200 only; no other targets).
+Each .cu is compiled to an object in parallel, then linked with -shared.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIB = os.path.join(PKG, "libparis.so")
+DATAGEN_SRC = os.path.join(ROOT, "datagen", "datagen.cu")
+DATAGEN_LIB = os.path.join(ROOT, "datagen", "libparis_datagen.so")
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+         "-Xptxas", "-warn-spills"]
+SOURCES = ["runtime.cu", "summarize.cu", "knn.cu"]
+HEADERS = ["runtime.cuh"]
+
+
+def _newer(target: str, deps) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _run(cmd):
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("command failed: " + " ".join(cmd) + "\n" + r.stdout + r.stderr)
+    return r.stdout + r.stderr
+
+
+def build_paris(force: bool = False, verbose: bool = False) -> str:
+    srcs = [os.path.join(CSRC, s) for s in SOURCES]
+    deps = srcs + [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "paris.h")]
+    if not force and not _newer(LIB, deps + [__file__]):
+        return LIB
+    objdir = os.path.join(PKG, "build")
+    os.makedirs(objdir, exist_ok=True)
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        extra = ["-Xptxas", "-v"] if verbose else []
+        out = _run([NVCC, *ARCH, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj])
+        return obj, out
+
+    with cf.ThreadPoolExecutor(max_workers=len(srcs)) as ex:
+        results = list(ex.map(compile_one, srcs))
+    if verbose:
+        for _, out in results:
+            sys.stdout.write(out)
+    tmp = LIB + f".tmp{os.getpid()}"
+    _run([NVCC, *ARCH, "-shared", "-o", tmp, *[o for o, _ in results], "-lcudart"])
+    os.replace(tmp, LIB)
+    return LIB
+
+
+def build_datagen(force: bool = False) -> str:
+    if not force and not _newer(DATAGEN_LIB, [DATAGEN_SRC, __file__]):
+        return DATAGEN_LIB
+    tmp = DATAGEN_LIB + f".tmp{os.getpid()}"
+    _run([NVCC, *ARCH, *FLAGS, "-shared", "-o", tmp, DATAGEN_SRC, "-lcudart"])
+    os.replace(tmp, DATAGEN_LIB)
+    return DATAGEN_LIB
+
+
+def build_all(force: bool = False, verbose: bool = False):
+    return build_paris(force, verbose), build_datagen(force)
+
+
+if __name__ == "__main__":
+    print(build_all(force="--force" in sys.argv, verbose="-v" in sys.argv))

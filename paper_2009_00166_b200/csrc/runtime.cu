@@ -1,0 +1,241 @@
+// libparis runtime: errors, launch accounting / per-kernel device time, and the
+// N(0,1) breakpoint tables (reading R2: cut_k = Phi^-1(k/card)).
+#include "runtime.cuh"
+
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+#include <mutex>
+#include <vector>
+
+namespace paris {
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err = "no error";
+
+void set_error(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+int cuda_error(cudaError_t e, const char* what) {
+  set_error("%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+  return PARIS_ECUDA;
+}
+
+// ------------------------------------------------------------------ launch accounting
+static std::atomic<int64_t> g_launches{0};
+static std::atomic<int> g_profile_on{0};
+
+struct ProfRec {
+  std::string name;
+  cudaEvent_t ev0, ev1;
+};
+static std::mutex g_prof_mu;
+static std::vector<ProfRec> g_prof;          // pending (unread) launches
+static std::vector<cudaEvent_t> g_ev_pool;   // recycled events
+struct ProfAgg {
+  std::string name;
+  int64_t launches;
+  double ms;
+};
+static std::vector<ProfAgg> g_agg;
+
+static cudaEvent_t get_event() {
+  if (!g_ev_pool.empty()) {
+    cudaEvent_t e = g_ev_pool.back();
+    g_ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+LaunchScope::LaunchScope(const char* name, cudaStream_t st) : name_(name), st_(st), slot_(-1) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (g_profile_on.load(std::memory_order_relaxed)) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    ProfRec r{name, get_event(), get_event()};
+    cudaEventRecord(r.ev0, st);
+    g_prof.push_back(r);
+    slot_ = (int)g_prof.size() - 1;
+  }
+}
+
+LaunchScope::~LaunchScope() {
+  if (slot_ >= 0) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (slot_ < (int)g_prof.size()) cudaEventRecord(g_prof[slot_].ev1, st_);
+  }
+}
+
+static void drain_locked() {
+  for (auto& r : g_prof) {
+    float ms = 0.f;
+    cudaEventSynchronize(r.ev1);
+    cudaEventElapsedTime(&ms, r.ev0, r.ev1);
+    bool found = false;
+    for (auto& a : g_agg)
+      if (a.name == r.name) { a.launches++; a.ms += ms; found = true; break; }
+    if (!found) g_agg.push_back({r.name, 1, (double)ms});
+    g_ev_pool.push_back(r.ev0);
+    g_ev_pool.push_back(r.ev1);
+  }
+  g_prof.clear();
+}
+
+// ------------------------------------------------------------------ breakpoints
+// Phi^-1 by Acklam's rational approximation (relative error < 1.2e-9) refined
+// by two Halley steps on the lower-tail CDF 0.5*erfc(-x/sqrt2); the upper half
+// uses the symmetry Phi^-1(p) = -Phi^-1(1-p) (1-p is exact for p = k/card).
+static double inv_phi_lower(double p) {  // p in (0, 0.5]
+  static const double a[6] = {-3.969683028665376e+01, 2.209460984245205e+02,
+                              -2.759285104469687e+02, 1.383577518672690e+02,
+                              -3.066479806614716e+01, 2.506628277459239e+00};
+  static const double b[5] = {-5.447609879822406e+01, 1.615858368580409e+02,
+                              -1.556989798598866e+02, 6.680131188771972e+01,
+                              -1.328068155288572e+01};
+  static const double c[6] = {-7.784894002430293e-03, -3.223964580411365e-01,
+                              -2.400758277161838e+00, -2.549732539343734e+00,
+                              4.374664141464968e+00, 2.938163982698783e+00};
+  static const double d[4] = {7.784695709041462e-03, 3.224671290700398e-01,
+                              2.445134137142996e+00, 3.754408661907416e+00};
+  double x;
+  if (p < 0.02425) {
+    double q = sqrt(-2.0 * log(p));
+    x = (((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+        ((((d[0] * q + d[1]) * q + d[2]) * q + d[3]) * q + 1.0);
+  } else {
+    double q = p - 0.5, r = q * q;
+    x = (((((a[0] * r + a[1]) * r + a[2]) * r + a[3]) * r + a[4]) * r + a[5]) * q /
+        (((((b[0] * r + b[1]) * r + b[2]) * r + b[3]) * r + b[4]) * r + 1.0);
+  }
+  if (p == 0.5) return 0.0;
+  for (int it = 0; it < 2; ++it) {
+    double e = 0.5 * erfc(-x / sqrt(2.0)) - p;
+    double u = e * sqrt(2.0 * M_PI) * exp(0.5 * x * x);
+    x = x - u / (1.0 + 0.5 * x * u);
+  }
+  return x;
+}
+
+void host_cuts(int card, double* cuts) {
+  for (int k = 1; k < card; ++k) {
+    if (2 * k <= card)
+      cuts[k - 1] = inv_phi_lower((double)k / card);
+    else
+      cuts[k - 1] = -inv_phi_lower((double)(card - k) / card);
+  }
+}
+
+static float round_down_f(double v) {
+  float f = (float)v;
+  if ((double)f > v) f = nextafterf(f, -INFINITY);
+  return f;
+}
+static float round_up_f(double v) {
+  float f = (float)v;
+  if ((double)f < v) f = nextafterf(f, INFINITY);
+  return f;
+}
+
+static std::mutex g_tab_mu;
+static CardTables* g_tables[64] = {nullptr};  // per device
+
+const CardTables* device_tables(int card) {
+  if (card < 2 || card > 256 || (card & (card - 1))) {
+    set_error("card must be a power of two in [2, 256] (got %d)", card);
+    return nullptr;
+  }
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess || dev < 0 || dev >= 64) {
+    cuda_error(e, "cudaGetDevice");
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lk(g_tab_mu);
+  if (!g_tables[dev]) {
+    std::vector<CardTables> h(kNumCards);
+    for (int ci = 0; ci < kNumCards; ++ci) {
+      int cd = 2 << ci;
+      double cuts[kMaxCard];
+      host_cuts(cd, cuts);
+      CardTables& t = h[ci];
+      for (int c = 0; c < kMaxCard; ++c) {
+        t.cuts_d[c] = (c < cd - 1) ? cuts[c] : INFINITY;
+        t.cuts_f[c] = (c < cd - 1) ? (float)cuts[c] : INFINITY;
+        float lo = (c == 0) ? -INFINITY : (c < cd ? round_down_f(cuts[c - 1]) : INFINITY);
+        float hi = (c >= cd - 1) ? INFINITY : round_up_f(cuts[c]);
+        t.lu[c] = make_float2(lo, hi);
+      }
+    }
+    CardTables* d = nullptr;
+    e = cudaMalloc(&d, sizeof(CardTables) * kNumCards);
+    if (e != cudaSuccess) {
+      cuda_error(e, "cudaMalloc(tables)");
+      return nullptr;
+    }
+    e = cudaMemcpy(d, h.data(), sizeof(CardTables) * kNumCards, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      cudaFree(d);
+      cuda_error(e, "cudaMemcpy(tables)");
+      return nullptr;
+    }
+    g_tables[dev] = d;
+  }
+  int ci = 0;
+  while ((2 << ci) != card) ++ci;
+  return g_tables[dev] + ci;
+}
+
+}  // namespace paris
+
+// ------------------------------------------------------------------ C ABI (misc)
+extern "C" {
+
+const char* paris_last_error(void) { return paris::g_err.c_str(); }
+
+int32_t paris_version(void) { return 100; }
+
+void paris_profile_enable(int32_t on) { paris::g_profile_on.store(on ? 1 : 0); }
+
+void paris_profile_reset(void) {
+  std::lock_guard<std::mutex> lk(paris::g_prof_mu);
+  paris::drain_locked();
+  paris::g_agg.clear();
+}
+
+int32_t paris_profile_read(paris_kernel_profile* out, int32_t max_entries) {
+  std::lock_guard<std::mutex> lk(paris::g_prof_mu);
+  paris::drain_locked();
+  int32_t n = 0;
+  for (auto& a : paris::g_agg) {
+    if (out && n < max_entries) {
+      memset(out[n].name, 0, sizeof out[n].name);
+      strncpy(out[n].name, a.name.c_str(), sizeof out[n].name - 1);
+      out[n].launches = a.launches;
+      out[n].total_ms = a.ms;
+    }
+    ++n;
+  }
+  return n;
+}
+
+int64_t paris_launch_count(void) { return paris::g_launches.load(); }
+
+// Test hook: the library's own breakpoints (fp64), card-1 values.
+int paris_debug_cuts(int32_t card, double* out) {
+  if (card < 2 || card > 256 || (card & (card - 1)) || !out) return PARIS_ECONFIG;
+  paris::host_cuts(card, out);
+  return 0;
+}
+
+}  // extern "C"

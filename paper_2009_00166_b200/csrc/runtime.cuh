@@ -1,0 +1,67 @@
+// libparis internal runtime: error reporting, launch accounting/profiling,
+// breakpoint tables.  Product code (sm_100a); shares nothing with oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/paris.h"
+
+namespace paris {
+
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+constexpr int kMaxCard = 256;
+constexpr int kNumCards = 8;  // 2, 4, ..., 256
+
+// Per-cardinality breakpoint tables (device resident, built once per device).
+//   cuts_f[c]  fp32 round-to-nearest of cut_{c+1} = Phi^-1((c+1)/card), c < card-1;
+//              +inf for c >= card-1 (pads the binary search to 256 entries)
+//   cuts_d[c]  same in fp64
+//   lu[c]      region bounds of symbol c as fp32 {L rounded down, U rounded up}:
+//              L = cut_c (-inf for c = 0), U = cut_{c+1} (+inf for c = card-1);
+//              outward rounding makes the fp32 region contain the exact one, so
+//              the fp32 lower bound never exceeds the exact one.
+struct CardTables {
+  float cuts_f[kMaxCard];
+  double cuts_d[kMaxCard];
+  float2 lu[kMaxCard];
+};
+
+// Returns the device table for `card` (power of two in [2,256]) on the current
+// device, building all eight on first use.  nullptr + error set on failure.
+const CardTables* device_tables(int card);
+
+// Host copy (for tests/debug): fills cuts (card-1 doubles).
+void host_cuts(int card, double* cuts);
+
+// ---- errors
+void set_error(const char* fmt, ...);
+int cuda_error(cudaError_t e, const char* what);
+
+// ---- launch accounting
+struct LaunchScope {
+  LaunchScope(const char* name, cudaStream_t st);
+  ~LaunchScope();
+  const char* name_;
+  cudaStream_t st_;
+  int slot_;
+};
+
+}  // namespace paris
+
+// Launch a kernel with accounting; evaluates to the cudaError_t of the launch.
+#define PARIS_LAUNCH(name, kernel, grid, block, smem, stream, ...)            \
+  ([&]() -> cudaError_t {                                                     \
+    ::paris::LaunchScope _scope(name, stream);                                \
+    kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);               \
+    return cudaGetLastError();                                                \
+  }())
+
+#define PARIS_CHECK_LAUNCH(call, what)                   \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return ::paris::cuda_error(_e, what); \
+  } while (0)
