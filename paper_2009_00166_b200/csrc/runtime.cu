@@ -5,6 +5,7 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <atomic>
@@ -70,10 +71,26 @@ LaunchScope::LaunchScope(const char* name, cudaStream_t st) : name_(name), st_(s
   }
 }
 
+static int sync_debug() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PARIS_SYNC_DEBUG");
+    v = (e && *e && *e != '0') ? 1 : 0;
+  }
+  return v;
+}
+
 LaunchScope::~LaunchScope() {
   if (slot_ >= 0) {
     std::lock_guard<std::mutex> lk(g_prof_mu);
     if (slot_ < (int)g_prof.size()) cudaEventRecord(g_prof[slot_].ev1, st_);
+  }
+  if (sync_debug()) {  // debugging aid: name each launch, wait for it
+    fprintf(stderr, "[paris] launch %s\n", name_);
+    fflush(stderr);
+    cudaError_t e = cudaStreamSynchronize(st_);
+    fprintf(stderr, "[paris] done %s: %s\n", name_, cudaGetErrorString(e));
+    fflush(stderr);
   }
 }
 
