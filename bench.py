@@ -32,11 +32,12 @@ sys.path.insert(0, ROOT)
 CONFIGS = {
     1: dict(n=100_000, len=256, nq=100, k=1, queries="fresh", desc="C1: 1e5 x 256 fp32 RW, 100 fresh RW queries, exact 1-NN"),
     2: dict(n=1_000_000, len=256, nq=1000, k=1, queries="noise0.05", desc="C2: 1e6 x 256 fp32 RW, 1000 member+N(0,0.05^2) queries, exact 1-NN"),
-    3: dict(n=10_000_000, len=128, nq=1000, k=1, queries="fresh", batch=8, desc="C3: 1e7 x 128 fp32 RW, 1000 fresh RW queries, exact 1-NN"),
+    3: dict(n=10_000_000, len=128, nq=1000, k=1, queries="fresh", call=64, desc="C3: 1e7 x 128 fp32 RW, 1000 fresh RW queries in calls of 64, exact 1-NN"),
     4: dict(n=100_000_000, len=256, nq=100, k=1, queries="fresh", desc="C4: 1e8 x 256 fp32 RW (102.4 GB raw + 1.6 GB SAX in HBM), 100 fresh RW queries, exact 1-NN"),
     5: dict(n=20_000_000, len=256, nq=200, k=1, queries="noise0.05", desc="C5: 2e7 x 256 fp32 RW, 200 member+N(0,0.05^2) queries, exact 1-NN"),
 }
 W, CARD = 16, 256
+ALU_CLOCK_GHZ = 1.965  # B200 clocks.max.sm (B200_PROFILING.md)
 
 
 def log(*a):
@@ -188,7 +189,8 @@ def run_gpu(args):
         n = args.n
     if args.nq:
         nq = args.nq
-    batch = args.batch or cfg.get("batch", 8)
+    batch = args.batch or 16
+    call_q = cfg.get("call", nq)  # queries per paris_knn_exact call (C3: batches of 64)
     ds, qs = datagen.config_seeds(args.config)
     ds += 7919 * rank  # weak scaling: every rank owns a distinct collection
     qs += 7919 * rank
@@ -217,13 +219,21 @@ def run_gpu(args):
     torch.cuda.synchronize()
     sum_ms = e0.elapsed_time(e1) / args.steps
 
-    # ---- query step: warmup (also collects stats once)
+    # ---- query step = every query of the config through paris_knn_exact (calls of call_q)
     out_idx = torch.empty((nq, k), dtype=torch.int64, device=dev)
     out_dist = torch.empty((nq, k), dtype=torch.float32, device=dev)
+
+    def step(qsrc, oi, od, cfg_=None):
+        cfg_ = cfg_ or kcfg
+        for c0 in range(0, nq, call_q):
+            c1 = min(nq, c0 + call_q)
+            P.knn_exact(raw, sax, qsrc[c0:c1], k=k, w=W, card=CARD, out_idx=oi[c0:c1], out_dist=od[c0:c1],
+                        config=cfg_)
+
     _, _, stats = P.knn_exact(raw, sax, queries, k=k, w=W, card=CARD, out_idx=out_idx,
                               out_dist=out_dist, config=kcfg, stats=True)
     for _ in range(max(0, args.warmup - 1)):
-        P.knn_exact(raw, sax, queries, k=k, w=W, card=CARD, out_idx=out_idx, out_dist=out_dist, config=kcfg)
+        step(queries, out_idx, out_dist)
     torch.cuda.synchronize()
 
     # ---- timed region (device events, max over ranks); per-kernel events via libparis profiling
@@ -236,7 +246,7 @@ def run_gpu(args):
     with ClockSampler(local) as clocks:
         e0.record(st)
         for _ in range(args.steps):
-            P.knn_exact(raw, sax, queries, k=k, w=W, card=CARD, out_idx=out_idx, out_dist=out_dist, config=kcfg)
+            step(queries, out_idx, out_dist)
         e1.record(st)
         torch.cuda.synchronize()
     if ws > 1:
@@ -255,11 +265,11 @@ def run_gpu(args):
     hq = queries.cpu().pin_memory()
     hidx = torch.empty((nq, k), dtype=torch.int64).pin_memory()
     hdist = torch.empty((nq, k), dtype=torch.float32).pin_memory()
-    P.knn_exact(raw, sax, hq, k=k, w=W, card=CARD, out_idx=hidx, out_dist=hdist, config=kcfg)
+    step(hq, hidx, hdist)
     torch.cuda.synchronize()
     e0.record(st)
     for _ in range(args.steps):
-        P.knn_exact(raw, sax, hq, k=k, w=W, card=CARD, out_idx=hidx, out_dist=hdist, config=kcfg)
+        step(hq, hidx, hdist)
     e1.record(st)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / args.steps
@@ -279,27 +289,68 @@ def run_gpu(args):
     tot = sum(v["ms_per_step"] for v in kern.values()) or 1.0
     for v in kern.values():
         v["share"] = v["ms_per_step"] / tot
-    nbatches = (nq + batch - 1) // batch
+    ncalls = (nq + call_q - 1) // call_q
+    nbatches = sum((min(call_q, nq - c0) + batch - 1) // batch for c0 in range(0, nq, call_q))
+    q_per_pass = nq / nbatches
     alg = {
         # SAX bytes per pass + 8 B per candidate written
         "lb_pass": (nbatches * n * W + 8.0 * cand.sum()) / nbatches,
         # raw bytes per refined series (K6)
         "refine": 4.0 * length * refined.sum() / nbatches,
     }
+    for name, v in kern.items():
+        if name in alg:
+            pl = v["ms_per_step"] * args.steps / prof[name][0]
+            v["launch_ms"] = pl
+            v["achieved_gbs"] = alg[name] / (pl / 1e3) / 1e9
     dom = max(kern, key=lambda s: kern[s]["ms_per_step"]) if kern else None
     roof = None
     if dom:
         per_launch_ms = kern[dom]["ms_per_step"] * args.steps / prof[dom][0]
-        by = alg.get(dom)
-        for name, v in kern.items():
-            if name in alg:
-                pl = v["ms_per_step"] * args.steps / prof[name][0]
-                v["achieved_gbs"] = alg[name] / (pl / 1e3) / 1e9
-        if by is not None:
-            ach = by / (per_launch_ms / 1e3) / 1e9
+        if dom == "lb_pass" and q_per_pass > 1.5:
+            # batched fp16x2 LB: bound by the FMA pipe, not HBM: 3 half-precision
+            # FMA-pipe ops per (series, segment, query); peak = 148 SMs x 64 lanes/clk x 2 halves
+            # x sm clock (B300_MICROARCH.md: FFMA/HFMA2 reciprocal throughput 2 per SMSP).
+            ops = 3.0 * n * W * q_per_pass
+            ach = ops / (per_launch_ms / 1e3) / 1e12
+            pk = 148 * 64 * 2 * ALU_CLOCK_GHZ * 1e9 / 1e12
+            roof = {"kernel": dom, "bound": "alu", "achieved": ach, "peak": pk, "unit": "Tops/s (fp16x2 half-ops)",
+                    "frac": ach / pk, "traffic": ncu_traffic(dom, args.config),
+                    "algorithmic_ops_per_launch": ops, "launch_ms": per_launch_ms,
+                    "peak_source": f"derived: 148 SM x 64 FMA lanes/clk x 2 (f16x2) x {ALU_CLOCK_GHZ} GHz",
+                    "hbm_achieved_gbs": alg[dom] / (per_launch_ms / 1e3) / 1e9, "hbm_peak_gbs": peak,
+                    "queries_per_pass": q_per_pass}
+        elif dom in alg:
+            ach = alg[dom] / (per_launch_ms / 1e3) / 1e9
             roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                     "frac": ach / peak, "traffic": ncu_traffic(dom, args.config),
-                    "algorithmic_bytes_per_launch": by, "launch_ms": per_launch_ms, "peak_source": peak_src}
+                    "algorithmic_bytes_per_launch": alg[dom], "launch_ms": per_launch_ms, "peak_source": peak_src}
+
+    # ---- LB pass at one query per SAX read: the HBM-roofline configuration of K4 (SURVEY §7 hard part 1)
+    lb1 = None
+    if not args.no_b1:
+        nq1 = min(nq, 8)
+        cfg1 = P.KnnConfig(batch=1)
+        P.knn_exact(raw, sax, queries[:nq1], k=k, w=W, card=CARD, config=cfg1)
+        torch.cuda.synchronize()
+        P.profile_reset()
+        P.profile_enable(True)
+        _, _, st1 = P.knn_exact(raw, sax, queries[:nq1], k=k, w=W, card=CARD, config=cfg1, stats=True)
+        P.profile_enable(False)
+        pr1 = P.profile_read()
+        if "lb_pass" in pr1:
+            c1, ms1 = pr1["lb_pass"]
+            by1 = n * W + 8.0 * float(st1["candidates"].double().mean())
+            a1 = by1 / (ms1 / c1 / 1e3) / 1e9
+            lb1 = {"kernel": "lb_pass", "bound": "hbm", "queries_per_pass": 1, "launch_ms": ms1 / c1,
+                   "algorithmic_bytes_per_launch": by1, "achieved": a1, "peak": peak, "unit": "GB/s",
+                   "frac": a1 / peak, "queries": nq1}
+        if "refine" in pr1:
+            c1, ms1 = pr1["refine"]
+            by1 = 4.0 * length * float(st1["refined"].double().mean())
+            lb1 = lb1 or {}
+            lb1["refine_batch1"] = {"launch_ms": ms1 / c1, "algorithmic_bytes_per_launch": by1,
+                                    "achieved": by1 / (ms1 / c1 / 1e3) / 1e9, "peak": peak, "unit": "GB/s"}
     sum_bytes = n * (4.0 * length + W)
     summarize = {"series_per_s": n / (sum_ms / 1e3), "ms": sum_ms, "unit": "series/s",
                  "roofline": {"kernel": "summarize", "bound": "hbm", "achieved": sum_bytes / (sum_ms / 1e3) / 1e9,
@@ -325,6 +376,7 @@ def run_gpu(args):
                        "batch": batch, "parallelism": f"weak x{ws} (independent collections + queries per GPU)",
                        "l2": "inputs larger than L2 (no flush)"},
             "roofline": roof,
+            "lb_batch1": lb1,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": nq * length * 4,
                     "d2h_bytes_per_step": nq * k * 12},
@@ -353,6 +405,7 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="override n (debug only)")
     ap.add_argument("--nq", type=int, default=0, help="override query count (debug only)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-b1", action="store_true", help="skip the batch-1 LB roofline measurement")
     ap.add_argument("--ref-sample", type=int, default=2_000_000)
     ap.add_argument("--ref-queries", type=int, default=4)
     args = ap.parse_args()

@@ -64,12 +64,13 @@ int paris_summarize(const float* raw, int64_t n, int32_t len, int32_t w, int32_t
  *      a sample of the SAX array ranks seed series; their true distances give an
  *      upper bound tau_seed on the k-th NN distance.
  *   2. LBC pass (Alg10): MINDIST_PAA_iSAX (R1) for every
- *      series' word; a series is a candidate iff its (rigorous, round-down fp32)
- *      LB^2 <= tau_seed^2 (rounded up).  Candidates are compacted per query.
- *   3. RDC pass (Alg11): candidates are refined in two waves -- the
- *      ~lowest-LB ones first, then the rest -- each re-checked against the live
- *      BSF before its raw series is read; true squared ED with early abandoning;
- *      the BSF (k-th best) is shared through atomics.
+ *      series' word, up to 16 queries per read of the SAX array (packed fp16 with
+ *      a rigorous error budget as a filter); a series is a candidate iff its
+ *      rigorous (round-down fp32) LB^2 <= tau_seed^2 (rounded up).  Candidates
+ *      are compacted per query.
+ *   3. RDC pass (Alg11): candidates are refined in LB order, each
+ *      re-checked against the live BSF before its raw series is read; true squared
+ *      ED with early abandoning; the BSF (k-th best) is shared through atomics.
  *   4. Result: ascending (distance, id); ties go to the lower id (R6).
  *   raw       device [n][len] fp32           sax  device [w][n] uint8 (paris_summarize)
  *   queries   [nq][len] fp32                 -- device OR host memory
@@ -77,6 +78,9 @@ int paris_summarize(const float* raw, int64_t n, int32_t len, int32_t w, int32_t
  *   out_dist  [nq][k] fp32 Euclidean (rooted) distance -- device OR host memory
  * queries/out_idx/out_dist may be host pointers (pageable or pinned): the library
  * then stages them through device memory on `stream`.
+ * Scratch (candidate lists, up to 16 * 2 * 8 * max(65536, n/32) bytes) is
+ * allocated stream-ordered from the device's default memory pool; the library
+ * raises that pool's release threshold so repeated calls reuse the mapping.
  * Synchronizes `stream` once per call (to check per-query candidate-buffer
  * overflow; an overflowed query is re-scanned with an exact-size buffer), so on
  * return the outputs are final.  nq == 0 is a no-op.
@@ -87,10 +91,10 @@ int paris_knn_exact(const float* raw, const uint8_t* sax, int64_t n, const float
 
 /* Tunables for paris_knn_exact_ex (0 = library default). */
 typedef struct paris_knn_config {
-  int32_t batch;        /* queries per SAX pass (1..8); default 8 */
+  int32_t batch;        /* queries per SAX pass (1..16); default 16 */
   int32_t seed_div;     /* seed sample = n / seed_div series (default 16) */
-  int32_t wave_a;       /* candidates refined in the first (lowest-LB) wave: max(wave_a, 2k) */
-  int32_t reserved[5];
+  int32_t wave_a;       /* reserved (0) */
+  int32_t reserved[5];  /* reserved[0] = 1: test hook forcing the direct-load LB kernels */
 } paris_knn_config;
 
 /* Per-query counters (host memory, arrays of nq), filled by paris_knn_exact_ex. */
@@ -115,6 +119,10 @@ int32_t paris_version(void);
 /* Test hook: the library's own fp64 breakpoints cut_1..cut_{card-1} (R2) into
  * out[0..card-2] (host memory).  PARIS_ECONFIG for a bad card. */
 int paris_debug_cuts(int32_t card, double* out);
+
+/* Test hook: IEEE binary16 bits of v rounded toward -inf (dir < 0) or +inf
+ * (dir > 0) -- the directed rounding behind the batched fp16 lower bound. */
+uint16_t paris_debug_half_dir(double v, int32_t dir);
 
 /*
  * Launch accounting / per-kernel device time (for benchmarks).

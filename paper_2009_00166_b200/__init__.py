@@ -12,6 +12,6 @@ device is present, every call raises.
 from ._binding import (  # noqa: F401
     PARIS_EINVAL, PARIS_ECONFIG, PARIS_ECUDA, PARIS_ENOMEM, PARIS_MAX_K,
     ParisError, KnnConfig, library_path, load, summarize, knn_exact, last_error,
-    profile_enable, profile_reset, profile_read, launch_count, version, debug_cuts,
+    profile_enable, profile_reset, profile_read, launch_count, version, debug_cuts, debug_half_dir,
     symbols,
 )

@@ -47,9 +47,10 @@ class _KProf(ctypes.Structure):
 
 @dataclass
 class KnnConfig:
-    batch: int = 0      # queries per SAX pass (1..8), 0 = default (8)
+    batch: int = 0      # queries per SAX pass (1..16), 0 = default (16)
     seed_div: int = 0   # seed sample = n / seed_div (0 = 16)
-    wave_a: int = 0     # first refinement wave size (0 = 256)
+    wave_a: int = 0     # reserved
+    force_direct: bool = False  # test hook: use the direct-load LB kernels even where the TMA-tiled ones apply
 
 
 def library_path() -> str:
@@ -82,6 +83,8 @@ def load():
         lib.paris_launch_count.restype = i64
         lib.paris_debug_cuts.argtypes = [i32, P]
         lib.paris_debug_cuts.restype = ctypes.c_int
+        lib.paris_debug_half_dir.argtypes = [ctypes.c_double, i32]
+        lib.paris_debug_half_dir.restype = ctypes.c_uint16
         _lib = lib
         return lib
 
@@ -171,6 +174,7 @@ def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: in
     cfg = None
     if config is not None:
         cfg = _Config(config.batch, config.seed_div, config.wave_a)
+        cfg.reserved[0] = 1 if config.force_direct else 0
     st = None
     arrays = None
     if stats:
@@ -207,6 +211,11 @@ def profile_read() -> dict:
 
 def launch_count() -> int:
     return int(load().paris_launch_count())
+
+
+def debug_half_dir(v: float, direction: int) -> int:
+    """IEEE binary16 bits of v rounded down (direction < 0) or up (> 0) -- for tests."""
+    return int(load().paris_debug_half_dir(float(v), int(direction)))
 
 
 def debug_cuts(card: int):

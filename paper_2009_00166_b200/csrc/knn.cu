@@ -1,26 +1,32 @@
 // K2-K7 -- paris_knn_exact: ParIS+ ExactSearch (Alg9) on one B200.
 //
-//   k_seed        (K2+K3a) query PAA (fp64) -> outward-rounded fp32 pair per
-//                 segment; lower bound over a SAX sample, per-warp best (LB,id)
-//                 = the approximate-search analog (reading R8)
+//   k_seed        (K2+K3a) query PAA (fp64) -> fp32 interval + packed fp16 pairs;
+//                 batched fp16 lower bound over a prefix sample of the SAX array,
+//                 per-warp LB-best series = the approximate-search analog
+//                 (reading R8)
 //   k_seed_ed     (K3b) true distance of each seed series
-//   k_seed_select (K3c) tau_seed^2 = k-th best seed d^2, rounded up
+//   k_seed_select (K3c) tau_seed^2 = k-th best seed d^2 (rounded up)
 //   k_lb          (K4) LBC pass (Alg10): MINDIST_PAA_iSAX
-//                  of every word for B queries at once; candidates
-//                 (LB^2 bits << 32 | id) compacted per query + LB histogram
+//                  of every word for up to 16 queries per SAX read,
+//                 in packed fp16x2 (two queries per instruction); a series that
+//                 passes the fp16 test gets a rigorous fp32 LB and is compacted
+//                 as (LB^2 bits << 32 | id) + a 256-bin LB histogram
 //   k_scatter     (K5) candidates bucket-sorted by LB (256 bins over [0, tau^2])
-//   k_refine      (K6) RDC pass (Alg11): warp per candidate in LB
-//                 order, LB re-checked against the live BSF, true ED
-//                 with early abandoning, BSF = k-th best shared via atomicMin
-//   k_finalize    (K7) merge per-CTA top-k lists -> ascending (d^2, id), sqrt
+//   k_refine1     (K6, k = 1) RDC pass (Alg11): warp per candidate in
+//                 LB order, LB re-checked against the live BSF, true ED
+//                 with early abandoning, BSF = 64-bit atomicMin on (d^2 bits, id)
+//   k_refine_topk (K6, k > 1) same, in CTA-synchronous rounds that merge the
+//                 round's admitted series into a CTA top-k; BSF = k-th best
+//                 shared through atomicMin on float bits
+//   k_finalize*   (K7) result rows ascending (d^2, id), sqrt
 //
-// Exactness: every LB is a rigorous lower bound of the
-// exact MINDIST (outward-rounded region bounds, round-down arithmetic), every
-// pruning threshold a rigorous upper bound of a real series' distance (fp32 d^2
-// scaled by 1 + 2^-19 > its summation error bound), so pruning never drops a
-// series that belongs in the exact answer; ranking among refined series uses
-// fp32 d^2 with the lower id breaking exact ties.
+// Exactness: every LB is a rigorous lower bound of the exact
+// MINDIST (outward-rounded bounds, directed rounding, fp16 error budget), every
+// pruning threshold a rigorous upper bound of a real series' exact d^2 (fp32
+// d^2 scaled by d2up), so pruning never drops a series of the exact answer.
 #include "runtime.cuh"
+
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <vector>
@@ -33,13 +39,16 @@ namespace {
 
 constexpr int kMaxW = 64;
 constexpr int kNB = 256;            // LB histogram bins per query
-constexpr int kMaxB = 8;            // queries per SAX pass
+constexpr int kMaxB = 16;           // queries per SAX pass
 constexpr int kLBThreads = 256;
 constexpr int kRefThreads = 256;
-constexpr int kRefAThreads = 1024;
+constexpr int kRefWarps = kRefThreads / 32;
+constexpr int kU = 4;               // candidates in flight per warp (refine)
 constexpr int kSortP = 4096;        // finalize / seed-select sort buffer
 constexpr int kMaxSeed = 4096;      // seed entries per query
 constexpr uint64_t kNoKey = ~0ull;
+constexpr uint32_t kHalf2One = 0x3C003C00u;
+constexpr uint32_t kHalfNeg1 = 0xBC00u;
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float r;
@@ -69,30 +78,51 @@ __device__ __forceinline__ float bin_scale(float thr) {
   return (thr > 0.f && thr < INFINITY) ? (float)kNB / thr : 0.f;
 }
 
-__device__ __forceinline__ float ld_volatile_f(const unsigned* p) {
-  return __uint_as_float(*(const volatile unsigned*)p);
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
 }
 
-// ---------------------------------------------------------------- lower bound
-// One SAX word row (4 consecutive series' symbols of segment s) against B
-// queries.  MINDIST branches: ABOVE q-U, BELOW L-q, IN 0 -- the
-// paper's 3 masked SIMD branches become one 3-input max.  All arithmetic rounds
-// toward -inf on outward-rounded bounds, so acc <= exact sum of delta^2.
-template <int B>
-__device__ __forceinline__ void lb_row(uint32_t word, const float2* __restrict__ q,
-                                       const float2* __restrict__ s_lu, float (&acc)[4][B]) {
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const float2 lu = s_lu[(word >> (8 * j)) & 0xFFu];
-#pragma unroll
-    for (int b = 0; b < B; ++b) {
-      const float above = __fsub_rd(q[b].x, lu.y);  // q_lo - U_up  <= q - U
-      const float below = __fsub_rd(lu.x, q[b].y);  // L_dn - q_hi  <= L - q
-      const float delta = fmax3(above, below, 0.f);
-      acc[j][b] = __fmaf_rd(delta, delta, acc[j][b]);
-    }
-  }
+// ---------------------------------------------------------------- packed fp16 ops
+__device__ __forceinline__ uint32_t h2_fma_relu(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("fma.rn.relu.f16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
 }
+__device__ __forceinline__ uint32_t h2_max(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("max.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t h2_min(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("min.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t h2_fma(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+// bit 0: low half a <= b; bit 1: high half a <= b
+__device__ __forceinline__ uint32_t h2_le_bits(uint32_t a, uint32_t b) {
+  const unsigned m = __hle2_mask(*reinterpret_cast<const __half2*>(&a), *reinterpret_cast<const __half2*>(&b));
+  return (m & 1u) | ((m >> 15) & 2u);
+}
+__device__ __forceinline__ float h_lo_f(uint32_t v) { return __half2float(__ushort_as_half((unsigned short)(v & 0xFFFFu))); }
+__device__ __forceinline__ float h_hi_f(uint32_t v) { return __half2float(__ushort_as_half((unsigned short)(v >> 16))); }
 
 template <bool AL>
 __device__ __forceinline__ uint32_t load_word(const uint8_t* __restrict__ sax, int64_t n, int s,
@@ -106,63 +136,94 @@ __device__ __forceinline__ uint32_t load_word(const uint8_t* __restrict__ sax, i
   return v;
 }
 
-// acc[j][b] = sum_s delta^2 for series i0+j (4 consecutive series) and query b.
-// WT = compile-time w (words preloaded for memory-level parallelism) or 0 (runtime w).
-template <int B, int WT, bool AL>
-__device__ __forceinline__ void lb_group(const uint8_t* __restrict__ sax, int64_t n, int w,
-                                         int64_t i0, const float2* __restrict__ s_q,
-                                         const float2* __restrict__ s_lu, float (&acc)[4][B]) {
+// ---------------------------------------------------------------- lower bounds
+// Batched fp16 MINDIST: for 4 series (the bytes of `word`) and P
+// query pairs, one segment.  Branches ABOVE / BELOW / IN (the paper's three
+// masked SIMD branches) become relu(q_lo - U), relu(L - q_hi) and their max:
+//   a = relu(q_lo16 - U16), b = relu(L16 - q_hi16), delta = max(a, b),
+//   acc += delta^2                          (3 fp16x2 FMA-pipe ops per 2 queries)
+// q_lo16 <= q, q_hi16 >= q, L16 <= L, U16 >= U, so the exact-arithmetic value is
+// <= the exact delta; round-to-nearest error is bounded in k_lb (T16).
+template <int P>
+__device__ __forceinline__ void lb16_seg(uint32_t word, const uint2* __restrict__ q16s,
+                                         const uint2* __restrict__ s_lu16, uint32_t (&acc)[4][P]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint2 t = s_lu16[(word >> (8 * j)) & 0xFFu];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const uint2 q = q16s[p];
+      const uint32_t a = h2_fma_relu(q.x, kHalf2One, t.x);
+      const uint32_t b = h2_fma_relu(q.y, kHalf2One, t.y);
+      const uint32_t d = h2_max(a, b);
+      acc[j][p] = h2_fma(d, d, acc[j][p]);
+    }
+  }
+}
+
+// fp16 accumulators of 4 consecutive series i0..i0+3 against P pairs.
+// WT: compile-time w (all words loaded up front) or 0 (runtime w).
+template <int P, int WT, bool AL>
+__device__ __forceinline__ void lb16_group(const uint8_t* __restrict__ sax, int64_t n, int w,
+                                           int64_t i0, const uint2* __restrict__ s_q16,
+                                           const uint2* __restrict__ s_lu16, uint32_t (&acc)[4][P]) {
 #pragma unroll
   for (int j = 0; j < 4; ++j)
 #pragma unroll
-    for (int b = 0; b < B; ++b) acc[j][b] = 0.f;
+    for (int p = 0; p < P; ++p) acc[j][p] = 0u;
   if (WT > 0) {
     uint32_t wd[WT > 0 ? WT : 1];
 #pragma unroll
     for (int s = 0; s < WT; ++s) wd[s] = load_word<AL>(sax, n, s, i0);
 #pragma unroll
-    for (int s = 0; s < WT; ++s) {
-      float2 q[B];
-#pragma unroll
-      for (int b = 0; b < B; ++b) q[b] = s_q[b * kMaxW + s];
-      lb_row<B>(wd[s], q, s_lu, acc);
-    }
+    for (int s = 0; s < WT; ++s) lb16_seg<P>(wd[s], s_q16 + s * P, s_lu16, acc);
   } else {
     uint32_t nxt = load_word<AL>(sax, n, 0, i0);
     for (int s = 0; s < w; ++s) {
       const uint32_t cur = nxt;
       if (s + 1 < w) nxt = load_word<AL>(sax, n, s + 1, i0);
-      float2 q[B];
-#pragma unroll
-      for (int b = 0; b < B; ++b) q[b] = s_q[b * kMaxW + s];
-      lb_row<B>(cur, q, s_lu, acc);
+      lb16_seg<P>(cur, s_q16 + s * P, s_lu16, acc);
     }
+  }
+  if (i0 + 3 >= n) {  // tail: absent series are +inf
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (i0 + j >= n)
+#pragma unroll
+        for (int p = 0; p < P; ++p) acc[j][p] = 0x7C007C00u;
   }
 }
 
-// Shared prologue: region bounds for the card, query pairs for the batch.
-template <int B>
-__device__ __forceinline__ void load_lu_q(const CardTables* __restrict__ tab,
-                                          const float2* __restrict__ qlh, int w, float2* s_lu,
-                                          float2* s_q) {
-  for (int i = threadIdx.x; i < kMaxCard; i += blockDim.x) s_lu[i] = tab->lu[i];
-  for (int i = threadIdx.x; i < B * kMaxW; i += blockDim.x) s_q[i] = qlh[i];
+// Rigorous fp32 LB^2 sum (without the len/w factor) of series i (byte j of the
+// words at i0) for one query interval q[s] = {q_lo, q_hi}: outward-rounded
+// region bounds, every operation rounded toward -inf, so the result is <= the
+// exact sum of delta^2 of the exact query PAA.
+template <bool AL>
+__device__ float lb32_series(const uint8_t* __restrict__ sax, int64_t n, int w, int64_t i0, int j,
+                             const float2* __restrict__ q, const float2* __restrict__ s_lu) {
+  float acc = 0.f;
+  for (int s = 0; s < w; ++s) {
+    const uint32_t word = load_word<AL>(sax, n, s, i0);
+    const float2 lu = s_lu[(word >> (8 * j)) & 0xFFu];
+    const float above = __fsub_rd(q[s].x, lu.y);  // q_lo - U_up <= q - U
+    const float below = __fsub_rd(lu.x, q[s].y);  // L_dn - q_hi <= L - q
+    const float delta = fmax3(above, below, 0.f);
+    acc = __fmaf_rd(delta, delta, acc);
+  }
+  return acc;
 }
 
-// ---------------------------------------------------------------- K2+K3a seed LB
-// Query PAA in fp64 (segment means), stored as {round-down,
-// round-up} fp32 -> qlh[b][s].  Then the LB over the sample [0, ns): every warp
-// keeps its best (LB^2, id) per query -> seed_ids[b][warp].
-template <int B, int WT, bool AL>
-__global__ void __launch_bounds__(kLBThreads)
-k_seed(const uint8_t* __restrict__ sax, int64_t n, int64_t ns, const float* __restrict__ queries,
-       int nb, int len, int w, const CardTables* __restrict__ tab, float2* __restrict__ qlh,
-       int* __restrict__ seed_ids, int S) {
-  __shared__ float2 s_lu[kMaxCard];
-  __shared__ float2 s_q[B * kMaxW];
+// Query PAA in fp64 (segment means) for the B = 2P slots of a batch:
+// s_q[b*kMaxW + s] = {round-down, round-up} fp32 of the PAA, and the packed fp16
+// pairs s_q16[s*P + p] = {half2(q_lo16[2p], q_lo16[2p+1]), half2(-q_hi16[2p], -q_hi16[2p+1])}
+// with q_lo16 = fp16 round-down of q_lo and q_hi16 = round-up of q_hi, both
+// clamped into [-60000, 60000] (a clamp only shrinks delta, so it stays sound).
+// Slots b >= nb are dummies.  Optionally mirrored to global (block 0).
+template <int P>
+__device__ void query_prep(const float* __restrict__ queries, int nb, int len, int w,
+                           float2* s_q, uint2* s_q16, float2* g_q, uint2* g_q16) {
   const int seglen = len / w;
-  for (int i = threadIdx.x; i < kMaxCard; i += blockDim.x) s_lu[i] = tab->lu[i];
-  for (int i = threadIdx.x; i < B * kMaxW; i += blockDim.x) {
+  for (int i = threadIdx.x; i < 2 * P * kMaxW; i += blockDim.x) {
     const int b = i / kMaxW, s = i % kMaxW;
     float2 v = make_float2(0.f, 0.f);
     if (b < nb && s < w) {
@@ -173,32 +234,68 @@ k_seed(const uint8_t* __restrict__ sax, int64_t n, int64_t ns, const float* __re
       v = make_float2(__double2float_rd(paa), __double2float_ru(paa));
     }
     s_q[i] = v;
-    if (blockIdx.x == 0) qlh[i] = v;
+    if (g_q) g_q[i] = v;
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  float best[B];
-  uint32_t bid[B];
+  for (int i = threadIdx.x; i < P * kMaxW; i += blockDim.x) {
+    const int s = i / P, p = i % P;
+    uint32_t lo2 = 0, nhi2 = 0;
+    if (s < w) {
 #pragma unroll
-  for (int b = 0; b < B; ++b) { best[b] = INFINITY; bid[b] = 0xFFFFFFFFu; }
+      for (int h = 0; h < 2; ++h) {
+        const float2 v = s_q[(2 * p + h) * kMaxW + s];
+        const float lo = fminf(fmaxf(v.x, -60000.f), 60000.f);
+        const float hi = fminf(fmaxf(v.y, -60000.f), 60000.f);
+        const unsigned short l16 = __half_as_ushort(__float2half_rd(lo));
+        const unsigned short h16 = __half_as_ushort(__float2half_ru(hi)) ^ 0x8000u;  // -q_hi16
+        lo2 |= (uint32_t)l16 << (16 * h);
+        nhi2 |= (uint32_t)h16 << (16 * h);
+      }
+    }
+    s_q16[i] = make_uint2(lo2, nhi2);
+    if (g_q16) g_q16[i] = make_uint2(lo2, nhi2);
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- K2+K3a seed LB
+// Every warp keeps its LB-best (LB, id) per query over the sample [0, ns).
+template <int P, int WT, bool AL>
+__global__ void __launch_bounds__(kLBThreads)
+k_seed(const uint8_t* __restrict__ sax, int64_t n, int64_t ns, const float* __restrict__ queries,
+       int nb, int len, int w, const CardTables* __restrict__ tab, float2* __restrict__ g_q,
+       uint2* __restrict__ g_q16, int* __restrict__ seed_ids, int S) {
+  __shared__ uint2 s_lu16[kMaxCard];
+  __shared__ float2 s_q[2 * P * kMaxW];
+  __shared__ uint2 s_q16[P * kMaxW];
+  for (int i = threadIdx.x; i < kMaxCard; i += blockDim.x) s_lu16[i] = tab->lu16[i];
+  query_prep<P>(queries, nb, len, w, s_q, s_q16, blockIdx.x == 0 ? g_q : nullptr,
+                blockIdx.x == 0 ? g_q16 : nullptr);
+  const int lane = threadIdx.x & 31;
+  float best[2 * P];
+  uint32_t bid[2 * P];
+#pragma unroll
+  for (int b = 0; b < 2 * P; ++b) { best[b] = INFINITY; bid[b] = 0xFFFFFFFFu; }
   const int64_t ngroups = (ns + 3) / 4;
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ngroups;
        g += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i0 = 4 * g;
-    float acc[4][B];
-    lb_group<B, WT, AL>(sax, n, w, i0, s_q, s_lu, acc);
+    uint32_t acc[4][P];
+    lb16_group<P, WT, AL>(sax, n, w, i0, s_q16, s_lu16, acc);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       if (i0 + j >= ns) break;
 #pragma unroll
-      for (int b = 0; b < B; ++b)
-        if (acc[j][b] < best[b]) { best[b] = acc[j][b]; bid[b] = (uint32_t)(i0 + j); }
+      for (int p = 0; p < P; ++p) {
+        const float lo = h_lo_f(acc[j][p]), hi = h_hi_f(acc[j][p]);
+        if (lo < best[2 * p]) { best[2 * p] = lo; bid[2 * p] = (uint32_t)(i0 + j); }
+        if (hi < best[2 * p + 1]) { best[2 * p + 1] = hi; bid[2 * p + 1] = (uint32_t)(i0 + j); }
+      }
     }
   }
-  // warp argmin of (LB, id) per query
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
 #pragma unroll
-  for (int b = 0; b < B; ++b) {
+  for (int b = 0; b < 2 * P; ++b) {
     float v = best[b];
     uint32_t id = bid[b];
 #pragma unroll
@@ -212,36 +309,25 @@ k_seed(const uint8_t* __restrict__ sax, int64_t n, int64_t ns, const float* __re
 }
 
 // ---------------------------------------------------------------- distance
-// d^2 between raw[id] and the query held in shared memory (warp-cooperative,
-// one float4 per lane per 128-point chunk).  Early abandoning (north_star;
-// S:159-167): after each chunk but the last, if the partial sum already exceeds
-// `limit` the rest is not read and +inf is returned (*abandoned = true).
-// Summation: <= len/128 sequential fma per lane, then a 5-level xor tree, so
+// d^2 between raw[id] and the query in shared memory (warp-cooperative, one
+// float4 per lane per 128-point chunk), no abandoning (seed pass).
+// Summation: <= len/32 sequential fma per lane, then a 5-level xor tree, so
 // |fp32 - exact| <= (len/32 + 8) * 2^-24 * d^2 (d2up in the host code covers it).
 __device__ __forceinline__ float warp_ed2(const float* __restrict__ raw, uint32_t id, int len,
-                                          const float4* __restrict__ s_qv, float limit,
-                                          bool* abandoned) {
+                                          const float4* __restrict__ s_qv) {
   const int lane = threadIdx.x & 31;
   const int nf = len >> 2;
   const float4* row = reinterpret_cast<const float4*>(raw + (size_t)id * len);
   float acc = 0.f;
-  for (int c0 = 0; c0 < nf; c0 += 32) {
-    const int f = c0 + lane;
-    if (f < nf) {
-      const float4 x = __ldg(row + f);
-      const float4 q = s_qv[f];
-      float d;
-      d = x.x - q.x; acc = fmaf(d, d, acc);
-      d = x.y - q.y; acc = fmaf(d, d, acc);
-      d = x.z - q.z; acc = fmaf(d, d, acc);
-      d = x.w - q.w; acc = fmaf(d, d, acc);
-    }
-    if (c0 + 32 < nf && limit < INFINITY) {
-      const float part = warp_sum(acc);
-      if (part > limit) { *abandoned = true; return INFINITY; }
-    }
+  for (int f = lane; f < nf; f += 32) {
+    const float4 x = ld_stream(row + f);
+    const float4 q = s_qv[f];
+    float d;
+    d = x.x - q.x; acc = fmaf(d, d, acc);
+    d = x.y - q.y; acc = fmaf(d, d, acc);
+    d = x.z - q.z; acc = fmaf(d, d, acc);
+    d = x.w - q.w; acc = fmaf(d, d, acc);
   }
-  *abandoned = false;
   return warp_sum(acc);
 }
 
@@ -259,11 +345,7 @@ k_seed_ed(const float* __restrict__ raw, int len, const float* __restrict__ quer
   for (int j = blockIdx.x * nw + warp; j < S; j += gridDim.x * nw) {
     const int id = seed_ids[b * S + j];
     uint64_t key = kNoKey;
-    if (id >= 0) {
-      bool ab;
-      const float d2 = warp_ed2(raw, (uint32_t)id, len, s_qv, INFINITY, &ab);
-      key = make_key(d2, (uint32_t)id);
-    }
+    if (id >= 0) key = make_key(warp_ed2(raw, (uint32_t)id, len, s_qv), (uint32_t)id);
     if (lane == 0) seed_keys[b * S + j] = key;
   }
 }
@@ -284,97 +366,548 @@ __device__ void bitonic_sort(uint64_t* buf, int P) {
   }
 }
 
+// 32 keys, one per lane, sorted ascending across the warp (lane i gets the i-th).
+__device__ __forceinline__ uint64_t warp_sort32(uint64_t v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const uint64_t o = __shfl_xor_sync(0xffffffffu, v, stride);
+      const bool up = ((lane & size) == 0);
+      const bool low = ((lane & stride) == 0);
+      v = (low == up) ? (v < o ? v : o) : (v < o ? o : v);
+    }
+  }
+  return v;
+}
+
 // ---------------------------------------------------------------- K3c seed select
-// tau_seed^2 = k-th smallest seed d^2 (upper bound of the k-th NN distance,
-// R8), rounded up by the fp32 summation error bound; +inf if < k seeds.
+// tau_seed^2 = k-th smallest seed d^2 (an upper bound of the k-th NN distance,
+// R8), rounded up by the fp32 error bound; +inf if < k seeds.  For k = 1 the best
+// seed key also initializes the BSF (best[b]).
 __global__ void __launch_bounds__(1024)
 k_seed_select(const uint64_t* __restrict__ seed_keys, int S, int k, float d2up,
-              unsigned* __restrict__ thr, unsigned* __restrict__ thr_seed, float* __restrict__ tau_out,
-              int q0) {
+              unsigned* __restrict__ thr, unsigned* __restrict__ thr_seed,
+              unsigned long long* __restrict__ best, float* __restrict__ tau_out, int q0) {
   __shared__ uint64_t buf[kSortP];
+  __shared__ uint64_t s_red[32];
   const int b = blockIdx.x;
-  for (int i = threadIdx.x; i < kSortP; i += blockDim.x) buf[i] = (i < S) ? seed_keys[b * S + i] : kNoKey;
-  __syncthreads();
-  bitonic_sort(buf, kSortP);
+  uint64_t kth;
+  if (k == 1) {
+    uint64_t m = kNoKey;
+    for (int i = threadIdx.x; i < S; i += blockDim.x) m = min(m, (uint64_t)seed_keys[b * S + i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = min(m, (uint64_t)__shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      m = (threadIdx.x < (blockDim.x >> 5)) ? s_red[threadIdx.x] : kNoKey;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = min(m, (uint64_t)__shfl_xor_sync(0xffffffffu, m, o));
+    }
+    kth = m;
+  } else {
+    for (int i = threadIdx.x; i < kSortP; i += blockDim.x) buf[i] = (i < S) ? seed_keys[b * S + i] : kNoKey;
+    __syncthreads();
+    bitonic_sort(buf, kSortP);
+    kth = buf[k - 1];
+  }
   if (threadIdx.x == 0) {
-    const uint64_t kth = buf[k - 1];
     const float t = (kth == kNoKey) ? INFINITY : __fmul_ru(key_val(kth), d2up);
     thr[b] = __float_as_uint(t);
     thr_seed[b] = __float_as_uint(t);
+    if (k == 1) best[b] = kth;
     if (tau_out) tau_out[q0 + b] = (kth == kNoKey) ? INFINITY : sqrtf(key_val(kth));
   }
 }
 
 // ---------------------------------------------------------------- K4 LBC pass
-// Alg10: for every word, LB^2 < BSF^2 -> append (LB, position).
-// Here: LB^2 <= tau_seed^2 (rigorous bounds on both sides), B queries per SAX
-// read; warp-aggregated atomics reserve slots; a 256-bin LB histogram per
-// query drives the ordering (K5).  count[b] keeps counting past `cap` so an
-// overflow is detected exactly.
-template <int B, int WT, bool AL>
-__global__ void __launch_bounds__(kLBThreads)
-k_lb(const uint8_t* __restrict__ sax, int64_t n, int w, float seglen_f,
-     const CardTables* __restrict__ tab, const float2* __restrict__ qlh, int nb,
-     const unsigned* __restrict__ thr, unsigned* __restrict__ count, unsigned* __restrict__ hist,
-     uint64_t* __restrict__ cand, int64_t cap) {
-  __shared__ float2 s_lu[kMaxCard];
-  __shared__ float2 s_q[B * kMaxW];
-  __shared__ float s_thr[B], s_scale[B];
-  load_lu_q<B>(tab, qlh, w, s_lu, s_q);
-  if (threadIdx.x < B) {
-    const float t = (threadIdx.x < nb) ? __uint_as_float(thr[threadIdx.x]) : -1.f;
-    s_thr[threadIdx.x] = t;
-    s_scale[threadIdx.x] = bin_scale(t);
+// Alg10: for every word, LB < BSF -> append (LB, position).
+// Here: up to 2P queries per SAX read, in packed fp16; warp-aggregated atomics
+// reserve slots; count[b] keeps counting past `cap` (overflow detection).
+//
+// fp16 error budget: with u = 2^-11, a delta rounded once (relu-FMA) and squared
+// into a running sum by w round-to-nearest FMAs is within (1+u)^(w+2) of its
+// exact-input value (non-negative terms; relu keeps signs), plus at most w*2^-24
+// of subnormal slack; the single-query form adds one fp32 add and one fp16
+// round-up.  So, with G = (1+u)^(w+4):
+//   LB16 <= LBexact_sum * G + w*2^-24                  (sum over s of delta^2).
+// Hence (a) a series can only be a candidate if
+//   LB16 <= T16 := tau^2/(len/w) * G + w*2^-24   (rounded up to fp16;
+// above 64000 it is replaced by +inf: an fp16 overflow needs a sum >= 65520), and
+// (b) LB^2 >= (LB16 - w*2^-24) * (len/w) / G is a rigorous lower bound,
+// computed with round-down fp32 -- it is the LB stored in the candidate key.
+struct LbArgs {
+  const uint8_t* sax;
+  int64_t n;
+  int w;
+  float seglen_f;
+  const CardTables* tab;
+  const float2* g_q;     // [2P][kMaxW]   fp32 query PAA intervals
+  const uint2* g_q16;    // [kMaxW][P]    packed fp16 pairs
+  int nb;
+  const unsigned* thr;   // tau_seed^2 (float bits) per query
+  unsigned* count;
+  unsigned* hist;
+  uint64_t* cand;
+  int64_t cap;
+};
+
+struct LbConsts {
+  uint32_t T16[kMaxB / 2];   // fp16 thresholds, packed per pair
+  float thr[kMaxB];          // tau^2 (rounded up), -1 for dummy slots
+  float scale[kMaxB];        // histogram bin scale
+  float lbconv;              // (len/w) / (1+u)^(w+3), rounded down
+  float wabs;                // w * 2^-24
+};
+
+__device__ void lb_consts_init(const LbArgs& a, int nslots, LbConsts* c) {
+  if (threadIdx.x < nslots) {
+    const int b = threadIdx.x;
+    const float t = (b < a.nb) ? __uint_as_float(a.thr[b]) : -1.f;
+    c->thr[b] = t;
+    c->scale[b] = bin_scale(t);
+  }
+  if (threadIdx.x == 0) {
+    const double grow = pow(1.0 + 1.0 / 2048.0, (double)(a.w + 4)) * (1.0 + 1e-12);
+    c->lbconv = __double2float_rd((double)a.seglen_f / grow);
+    c->wabs = (float)a.w * 5.9604644775390625e-08f;
   }
   __syncthreads();
+  if (threadIdx.x < (nslots + 1) / 2) {
+    uint32_t t2 = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int b = 2 * threadIdx.x + h;
+      const float t = (b < nslots) ? c->thr[b] : -1.f;
+      unsigned short hb;
+      if (t < 0.f) {
+        hb = (unsigned short)kHalfNeg1;  // dummy slot: never passes
+      } else {
+        const double grow = pow(1.0 + 1.0 / 2048.0, (double)(a.w + 4)) * (1.0 + 1e-12);
+        const double T = (double)t / (double)a.seglen_f * grow + (double)a.w * 5.9604644775390625e-08;
+        hb = (T > 64000.0) ? (unsigned short)0x7C00u
+                           : __half_as_ushort(__float2half_ru(__double2float_ru(T)));
+      }
+      t2 |= (uint32_t)hb << (16 * h);
+    }
+    c->T16[threadIdx.x] = t2;
+  }
+  __syncthreads();
+}
+
+// Candidate emission for 4 series i0..i0+3 (nvalid of them real) and 2P query
+// slots whose fp16 sums are acc[j][p] (slot 2p low half, 2p+1 high half).
+// Whole warp must call it (warp-aggregated atomics).
+template <int P>
+__device__ __forceinline__ void lb_emit(const uint32_t (&acc)[4][P], int64_t i0, int nvalid,
+                                        const LbConsts& c, const LbArgs& a) {
   const int lane = threadIdx.x & 31;
+  uint32_t qm = 0;
+  if (nvalid > 0) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const uint32_t mn = h2_min(h2_min(acc[0][p], acc[1][p]), h2_min(acc[2][p], acc[3][p]));
+      qm |= h2_le_bits(mn, c.T16[p]) << (2 * p);
+    }
+  }
+  if (!__any_sync(0xffffffffu, qm != 0)) return;
+  uint32_t wq = __reduce_or_sync(0xffffffffu, qm);
+  while (wq) {
+    const int b = __ffs(wq) - 1;
+    wq &= wq - 1;
+    unsigned m = 0;
+    float lbv[4];
+    if ((qm >> b) & 1u) {
+      const uint32_t T = c.T16[b >> 1];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int p = 0; p < P; ++p)
+          if (p == (b >> 1)) v = acc[j][p];
+        const uint32_t pass = (h2_le_bits(v, T) >> (b & 1)) & 1u;
+        const float h = (b & 1) ? h_hi_f(v) : h_lo_f(v);
+        lbv[j] = __fmul_rd(fmaxf(__fsub_rd(h, c.wabs), 0.f), c.lbconv);
+        if (pass && j < nvalid && lbv[j] <= c.thr[b]) m |= 1u << j;
+      }
+    }
+    const int cnt = __popc(m);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) continue;
+    unsigned base = 0;
+    if (lane == 31) base = atomicAdd(&a.count[b], (unsigned)total);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    uint64_t pos = (uint64_t)base + (unsigned)(incl - cnt);
+    const float sc = c.scale[b];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (m & (1u << j)) {
+        if (pos < (uint64_t)a.cap) a.cand[(size_t)b * a.cap + pos] = make_key(lbv[j], (uint32_t)(i0 + j));
+        atomicAdd(&a.hist[b * kNB + lb_bin(lbv[j], sc)], 1u);
+        ++pos;
+      }
+    }
+  }
+}
+
+// Warp-private candidate staging in shared memory (tiled kernel): a warp appends
+// its candidates (key + query slot) with shared-memory atomics only; when the
+// buffer would overflow (and at the end) the warp flushes it: one global
+// atomicAdd per query slot reserves the slots of all its entries at once.
+constexpr int kWB = 128;
+struct WarpBuf {
+  uint64_t key[kWB];
+  uint8_t slot[kWB];
+  unsigned cnt[kMaxB];   // entries per slot
+  unsigned cur[kMaxB];   // flush cursors
+  int n;
+};
+
+__device__ void wb_flush(WarpBuf& wb, int nslots, const LbConsts& c, const LbArgs& a) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  const int m = wb.n;
+  if (m == 0) return;
+  if (lane < nslots) {
+    const unsigned k = wb.cnt[lane];
+    wb.cur[lane] = k ? atomicAdd(&a.count[lane], k) : 0u;
+    wb.cnt[lane] = 0;
+  }
+  __syncwarp();
+  for (int e = lane; e < m; e += 32) {
+    const int b = wb.slot[e];
+    const uint64_t key = wb.key[e];
+    const unsigned pos = atomicAdd(&wb.cur[b], 1u);
+    if ((int64_t)pos < a.cap) a.cand[(size_t)b * a.cap + pos] = key;
+    atomicAdd(&a.hist[b * kNB + lb_bin(key_val(key), c.scale[b])], 1u);
+  }
+  __syncwarp();
+  if (lane == 0) wb.n = 0;
+  __syncwarp();
+}
+
+template <int P>
+__device__ __forceinline__ void lb_emit_wb(const uint32_t (&acc)[4][P], int64_t i0, int nvalid, int nslots,
+                                           const LbConsts& c, const LbArgs& a, WarpBuf& wb) {
+  const int lane = threadIdx.x & 31;
+  uint32_t qm = 0;
+  if (nvalid > 0) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const uint32_t mn = h2_min(h2_min(acc[0][p], acc[1][p]), h2_min(acc[2][p], acc[3][p]));
+      qm |= h2_le_bits(mn, c.T16[p]) << (2 * p);
+    }
+  }
+  if (!__any_sync(0xffffffffu, qm != 0)) return;
+  // pass 1: this lane's candidate count; pass 2 writes (lane-local loops over set bits)
+  int cntl = 0;
+  for (uint32_t r = qm; r; r &= r - 1) {
+    const int b = __ffs(r) - 1;
+    const uint32_t T = c.T16[b >> 1];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint32_t v = 0;
+#pragma unroll
+      for (int p = 0; p < P; ++p)
+        if (p == (b >> 1)) v = acc[j][p];
+      const float h = (b & 1) ? h_hi_f(v) : h_lo_f(v);
+      const float lb = __fmul_rd(fmaxf(__fsub_rd(h, c.wabs), 0.f), c.lbconv);
+      if (((h2_le_bits(v, T) >> (b & 1)) & 1u) && j < nvalid && lb <= c.thr[b]) ++cntl;
+    }
+  }
+  int incl = cntl;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  if (total == 0) return;
+  if (wb.n + total > kWB) wb_flush(wb, nslots, c, a);
+  if (total > kWB) {  // degenerate (e.g. tau = inf): straight to global memory
+    lb_emit<P>(acc, i0, nvalid, c, a);
+    return;
+  }
+  int pos = wb.n + incl - cntl;
+  for (uint32_t r = qm; r; r &= r - 1) {
+    const int b = __ffs(r) - 1;
+    const uint32_t T = c.T16[b >> 1];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint32_t v = 0;
+#pragma unroll
+      for (int p = 0; p < P; ++p)
+        if (p == (b >> 1)) v = acc[j][p];
+      const float h = (b & 1) ? h_hi_f(v) : h_lo_f(v);
+      const float lb = __fmul_rd(fmaxf(__fsub_rd(h, c.wabs), 0.f), c.lbconv);
+      if (((h2_le_bits(v, T) >> (b & 1)) & 1u) && j < nvalid && lb <= c.thr[b]) {
+        wb.key[pos] = make_key(lb, (uint32_t)(i0 + j));
+        wb.slot[pos] = (uint8_t)b;
+        atomicAdd(&wb.cnt[b], 1u);
+        ++pos;
+      }
+    }
+  }
+  __syncwarp();
+  if (lane == 31) wb.n += total;
+  __syncwarp();
+}
+
+// Direct-load variant (any n, any w <= 64): a thread loads the 4-series words of
+// every segment row straight from global memory.
+template <int P, int WT, bool AL>
+__global__ void __launch_bounds__(kLBThreads)
+k_lb(LbArgs a) {
+  __shared__ uint2 s_lu16[kMaxCard];
+  __shared__ uint2 s_q16[P * kMaxW];
+  __shared__ LbConsts s_c;
+  for (int i = threadIdx.x; i < kMaxCard; i += blockDim.x) s_lu16[i] = a.tab->lu16[i];
+  for (int i = threadIdx.x; i < P * kMaxW; i += blockDim.x) s_q16[i] = a.g_q16[i];
+  lb_consts_init(a, 2 * P, &s_c);
+  const int lane = threadIdx.x & 31;
+  const int64_t n = a.n;
   const int64_t ngroups = (n + 3) / 4;
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g - lane < ngroups;
        g += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i0 = 4 * g;
-    float acc[4][B];
+    uint32_t acc[4][P];
+    int nvalid = 0;
     if (g < ngroups) {
-      lb_group<B, WT, AL>(sax, n, w, i0, s_q, s_lu, acc);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int b = 0; b < B; ++b) acc[j][b] = INFINITY;
+      lb16_group<P, WT, AL>(a.sax, n, a.w, i0, s_q16, s_lu16, acc);
+      nvalid = (int)imin64(4, n - i0);
     }
+    lb_emit<P>(acc, i0, nvalid, s_c, a);
+  }
+}
+
+// ---------------------------------------------------------------- K3a/K4 tiled (TMA) variant
+// n % 16 == 0 and w == 16 (every BASELINE config): a persistent CTA per SM streams
+// SAX tiles of kTS series x 16 segment rows into a kStages-deep shared-memory ring
+// with cp.async.bulk (one bulk copy per row, completion on an mbarrier), so HBM
+// reads run ahead of the lookups; the last warp to finish a stage refills it.
+// The region table is replicated 32x in shared memory (entry c of lane l at word
+// c*32 + l) so the per-series lookups are bank-conflict free.
+constexpr int kTS = 2048;
+constexpr int kTThreads = 512;
+constexpr int kTWarps = kTThreads / 32;
+constexpr int kStages = 4;
+constexpr int kTW = 16;
+constexpr size_t kTileBytes = (size_t)kTW * kTS;
+constexpr size_t kTSmem = kStages * kTileBytes + kMaxCard * 32 * 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Pair form for one segment word (4 series) from the replicated table.
+template <int P>
+__device__ __forceinline__ void lbt_seg(uint32_t word, const uint32_t* __restrict__ tabl,
+                                        const uint2* __restrict__ q16s, uint32_t (&acc)[4][P]) {
 #pragma unroll
-    for (int b = 0; b < B; ++b) {
-      const float t = s_thr[b];
-      float lb[4];
-      unsigned m = 0;
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t t = tabl[__byte_perm(word, 0, 0x4440 | j) * 32];  // (-U16, L16)
+    const uint32_t tx = __byte_perm(t, 0, 0x1010);                    // (-U16, -U16)
+    const uint32_t ty = __byte_perm(t, 0, 0x3232);                    // (L16, L16)
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const uint2 q = q16s[p];
+      const uint32_t a = h2_fma_relu(q.x, kHalf2One, tx);
+      const uint32_t b = h2_fma_relu(q.y, kHalf2One, ty);
+      const uint32_t d = h2_max(a, b);
+      acc[j][p] = h2_fma(d, d, acc[j][p]);
+    }
+  }
+}
+
+// Single-query form (B = 1): qd = half2(q_lo16, -q_hi16) against (-U16, L16):
+// one relu-FMA gives (relu(q-U), relu(L-q)), one FMA accumulates both halves
+// (at most one is non-zero); the LB sum is lo + hi at the end.
+__device__ __forceinline__ void lbt_seg1(uint32_t word, const uint32_t* __restrict__ tabl, uint32_t qd,
+                                         uint32_t (&acc)[4]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t t = tabl[__byte_perm(word, 0, 0x4440 | j) * 32];
+    const uint32_t d = h2_fma_relu(qd, kHalf2One, t);
+    acc[j] = h2_fma(d, d, acc[j]);
+  }
+}
+
+// MODE 0: seed (per-warp LB-best series per query over [0, nlim));
+// MODE 1: LB pass with candidate emission over [0, nlim = n).
+// P = 0: single query (slot 0).  nlim % 16 == 0.
+template <int P, int MODE>
+__global__ void __launch_bounds__(kTThreads, 1)
+k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
+  constexpr int PP = P > 0 ? P : 1;
+  extern __shared__ __align__(128) uint8_t dsm[];
+  uint8_t* s_tiles = dsm;
+  uint32_t* s_tab = reinterpret_cast<uint32_t*>(dsm + kStages * kTileBytes);
+  __shared__ __align__(8) uint64_t s_full[kStages];
+  __shared__ unsigned s_cnt[kStages];
+  __shared__ uint2 s_q16[PP * kTW];
+  __shared__ LbConsts s_c;
+  __shared__ WarpBuf s_wb[MODE == 1 ? kTWarps : 1];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t ntiles = (nlim + kTS - 1) / kTS;
+  const int nslots = P > 0 ? 2 * P : 1;
+  WarpBuf& wb = s_wb[MODE == 1 ? (tid >> 5) : 0];
+  if (MODE == 1) {
+    if (lane < kMaxB) wb.cnt[lane] = 0;
+    if (lane == 0) wb.n = 0;
+  }
+
+  auto issue = [&](int64_t tile, int st) {
+    const int64_t base = tile * kTS;
+    const unsigned bytes = (unsigned)imin64(kTS, nlim - base);
+    mbar_expect_tx(&s_full[st], bytes * kTW);
+    uint8_t* dst = s_tiles + (size_t)st * kTileBytes;
+#pragma unroll 1
+    for (int s = 0; s < kTW; ++s)
+      bulk_g2s(dst + (size_t)s * kTS, a.sax + (size_t)s * a.n + base, bytes, &s_full[st]);
+  };
+
+  if (tid == 0) {
+    for (int st = 0; st < kStages; ++st) {
+      mbar_init(&s_full[st], 1);
+      s_cnt[st] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int st = 0; st < kStages; ++st) {
+      const int64_t tile = blockIdx.x + (int64_t)st * gridDim.x;
+      if (tile < ntiles) issue(tile, st);
+    }
+  }
+  for (int i = tid; i < kMaxCard * 32; i += kTThreads) s_tab[i] = a.tab->lu16p[i >> 5];
+  if (P > 0) {
+    for (int i = tid; i < PP * kTW; i += kTThreads) s_q16[i] = a.g_q16[i];
+  } else if (tid < kTW) {
+    // single query: (q_lo16, -q_hi16) of slot 0, repacked from the pair layout (low halves)
+    const uint2 v = a.g_q16[tid];
+    s_q16[tid] = make_uint2((v.x & 0xFFFFu) | (v.y << 16), 0u);
+  }
+  lb_consts_init(a, P > 0 ? 2 * P : 1, &s_c);   // ends with __syncthreads
+  const uint32_t* tabl = s_tab + lane;
+
+  float best[MODE == 0 ? 2 * PP : 1];
+  uint32_t bid[MODE == 0 ? 2 * PP : 1];
+  if (MODE == 0) {
+#pragma unroll
+    for (int b = 0; b < (MODE == 0 ? 2 * PP : 1); ++b) { best[b] = INFINITY; bid[b] = 0xFFFFFFFFu; }
+  }
+
+  for (int64_t it = 0;; ++it) {
+    const int64_t tile = blockIdx.x + it * gridDim.x;
+    if (tile >= ntiles) break;
+    const int st = (int)(it % kStages);
+    mbar_wait(&s_full[st], (unsigned)((it / kStages) & 1));
+    const uint32_t* rows = reinterpret_cast<const uint32_t*>(s_tiles + (size_t)st * kTileBytes);
+    const int64_t i0 = tile * kTS + 4 * tid;
+    const int nvalid = (int)std::max<int64_t>(0, imin64(4, nlim - i0));
+    uint32_t acc[4][PP];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int p = 0; p < PP; ++p) acc[j][p] = 0u;
+    if (P > 0) {
+#pragma unroll 2
+      for (int s = 0; s < kTW; ++s) lbt_seg<PP>(rows[s * (kTS / 4) + tid], tabl, s_q16 + s * PP, acc);
+    } else {
+      uint32_t a1[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int s = 0; s < kTW; ++s) lbt_seg1(rows[s * (kTS / 4) + tid], tabl, s_q16[s].x, a1);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        lb[j] = __fmul_rd(acc[j][b], seglen_f);
-        if (i0 + j < n && lb[j] <= t) m |= 1u << j;
+        // lo + hi (ABOVE and BELOW sums), rounded up to fp16 (inside the G budget);
+        // the unused high slot is +inf so it never passes
+        const float v = h_lo_f(a1[j]) + h_hi_f(a1[j]);
+        const __half hv = __float2half_ru(v);
+        acc[j][0] = (uint32_t)__half_as_ushort(hv) | (0x7C00u << 16);
       }
-      if (__any_sync(0xffffffffu, m != 0)) {
-        const int c = __popc(m);
-        int incl = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int v = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += v;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      // stage consumed by this warp; the last warp refills it with the tile kStages ahead
+      if (atomicAdd(&s_cnt[st], 1u) == kTWarps - 1) {
+        s_cnt[st] = 0;
+        const int64_t next = tile + (int64_t)kStages * gridDim.x;
+        if (next < ntiles) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(next, st);
         }
-        unsigned base = 0;
-        if (lane == 31) base = atomicAdd(&count[b], (unsigned)incl);
-        base = __shfl_sync(0xffffffffu, base, 31);
-        uint64_t pos = (uint64_t)base + (unsigned)(incl - c);
-        const float sc = s_scale[b];
+      }
+    }
+    if (MODE == 1) {
+      lb_emit_wb<PP>(acc, i0, nvalid, nslots, s_c, a, wb);
+    } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (m & (1u << j)) {
-            if (pos < (uint64_t)cap) cand[(size_t)b * cap + pos] = make_key(lb[j], (uint32_t)(i0 + j));
-            atomicAdd(&hist[b * kNB + lb_bin(lb[j], sc)], 1u);
-            ++pos;
-          }
+      for (int j = 0; j < 4; ++j) {
+        if (j >= nvalid) break;
+#pragma unroll
+        for (int p = 0; p < PP; ++p) {
+          const float lo = h_lo_f(acc[j][p]), hi = h_hi_f(acc[j][p]);
+          if (lo < best[2 * p]) { best[2 * p] = lo; bid[2 * p] = (uint32_t)(i0 + j); }
+          if (P > 0 && hi < best[2 * p + 1]) { best[2 * p + 1] = hi; bid[2 * p + 1] = (uint32_t)(i0 + j); }
         }
       }
     }
   }
+  if (MODE == 1) wb_flush(wb, nslots, s_c, a);
+  if (MODE == 0) {
+    const int gwarp = (blockIdx.x * kTThreads + tid) >> 5;
+#pragma unroll
+    for (int b = 0; b < (MODE == 0 ? 2 * PP : 1); ++b) {
+      float v = best[b];
+      uint32_t id = bid[b];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float v2 = __shfl_xor_sync(0xffffffffu, v, o);
+        const uint32_t id2 = __shfl_xor_sync(0xffffffffu, id, o);
+        if (v2 < v || (v2 == v && id2 < id)) { v = v2; id = id2; }
+      }
+      if (lane == 0 && b < a.nb && gwarp < S) seed_ids[b * S + gwarp] = (id == 0xFFFFFFFFu) ? -1 : (int)id;
+    }
+  }
+}
+
+// Query prep alone (for the tiled seed, which has no prologue of its own).
+template <int P>
+__global__ void k_qprep(const float* __restrict__ queries, int nb, int len, int w, float2* __restrict__ g_q,
+                        uint2* __restrict__ g_q16) {
+  __shared__ float2 s_q[2 * P * kMaxW];
+  __shared__ uint2 s_q16[P * kMaxW];
+  query_prep<P>(queries, nb, len, w, s_q, s_q16, g_q, g_q16);
 }
 
 // ---------------------------------------------------------------- K5 bucket order
@@ -387,7 +920,6 @@ k_scatter(const uint64_t* __restrict__ cand, const unsigned* __restrict__ count,
           unsigned* __restrict__ cursor, uint64_t* __restrict__ sorted, int64_t cap) {
   __shared__ unsigned s_off[kNB];
   const int b = blockIdx.y;
-  // exclusive prefix of the histogram (Hillis-Steele over 256 bins)
   unsigned v = hist[b * kNB + threadIdx.x];
   s_off[threadIdx.x] = v;
   __syncthreads();
@@ -413,160 +945,419 @@ k_scatter(const uint64_t* __restrict__ cand, const unsigned* __restrict__ count,
 }
 
 // ---------------------------------------------------------------- K6 RDC pass
-// Alg11: take the next candidate (static interleave over the
-// LB-ordered list instead of a locked cursor), skip it if LB > BSF,
-// else read raw[id] and compute the true distance (early abandoning), and
-// update the BSF.  BSF for k-NN = k-th best: each CTA keeps a
-// top-k list in shared memory; when full, its k-th d^2 (rounded up) is pushed to
-// the query's global threshold with atomicMin on the float bits, which every
-// warp re-reads before each candidate.
-//   wave 0 (k > 1 only): one CTA refines the lowest-LB ~max(M, 2k) candidates so
-//                       that its list fills and tightens the BSF early;
-//   wave 1: all other candidates, many CTAs per query.
+// Alg11: take the next candidate (static interleave of warps over
+// the LB-ordered list instead of a locked cursor), skip it if LB > BSF,
+// else read raw[id], compute the true distance with early abandoning, and lower
+// the BSF.  kU candidates are in flight per warp.
 struct RefineArgs {
   const float* raw;
   int len;
-  const float* queries;  // batch base [nb][len]
+  const float* queries;      // batch base [nb][len]
   const uint64_t* sorted;
   int64_t cap;
   const unsigned* count;
-  const unsigned* hist;
-  unsigned* thr;         // live pruning threshold (float bits), per query
   const unsigned* thr_seed;  // tau_seed^2 (float bits): the binning scale of K4/K5
-  unsigned* wave_end;    // per query: end of wave 0 in the sorted list
-  unsigned* refined;     // per query counter
-  uint64_t* lists;       // [nb][nslots][k]
-  int nslots;
+  unsigned* thr;             // k > 1: live pruning threshold (float bits), per query
+  unsigned long long* best;  // k = 1: (d^2 bits << 32 | id), per query
+  unsigned* refined;         // per query counter
+  uint64_t* lists;           // k > 1: [nb][gridDim.x][k]
   int k;
-  int wave;
-  int wave_m;            // wave-0 size target
-  float d2up;            // 1 + bound on the relative error of an fp32 d^2 (rounding up)
+  float d2up;                // 1 + bound on the relative error of an fp32 d^2 (rounding up)
 };
 
-__global__ void __launch_bounds__(1024)
-k_refine(RefineArgs a) {
-  extern __shared__ float4 s_dyn[];
-  float4* s_qv = s_dyn;                                            // len/4 float4
-  uint64_t* s_keys = reinterpret_cast<uint64_t*>(s_dyn + (a.len >> 2));  // k keys
-  __shared__ int s_lock, s_size, s_maxpos;
-  __shared__ uint64_t s_maxkey;
-  __shared__ float s_kth;          // local k-th d^2 (unscaled) when full, else inf
-  __shared__ float s_thr_local;    // local k-th d^2 rounded up, else inf
-  __shared__ unsigned s_begin, s_end, s_refined;
-  __shared__ float s_scale;
+// One warp step: up to kU candidates (indices i0 + u*stride) against the live
+// threshold `thr`; returns true when the list is exhausted for this warp (index
+// past the end, or a candidate whose LB bin lies wholly above thr: every later
+// candidate in bin order is then above it too).  Distances of survivors go to
+// d2[u] (INFINITY = pruned or abandoned).
+__device__ __forceinline__ bool refine_step(const RefineArgs& a, const uint64_t* __restrict__ list,
+                                            unsigned cnt, unsigned i0, unsigned stride, float thr,
+                                            float scale, const float4* __restrict__ s_qv,
+                                            uint64_t (&key)[kU], float (&d2)[kU], unsigned& nref) {
+  const int lane = threadIdx.x & 31;
+  const int nf = a.len >> 2;
+  bool live[kU];
+  bool stop = false;
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    const unsigned i = i0 + u * stride;
+    key[u] = (i < cnt) ? list[i] : kNoKey;
+    const float lb = key_val(key[u]);
+    live[u] = (i < cnt) && !stop && lb <= thr;
+    if (i >= cnt) stop = true;
+    else if (!live[u] && !stop) {
+      const int bin = lb_bin(lb, scale);
+      if (bin >= 1 && (float)(bin - 1) > thr * scale) stop = true;
+    }
+    d2[u] = INFINITY;
+  }
+  float acc[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) acc[u] = 0.f;
+  for (int c0 = 0; c0 < nf; c0 += 32) {
+    const int f = c0 + lane;
+    float4 x[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (live[u] && f < nf)
+        x[u] = ld_stream(reinterpret_cast<const float4*>(a.raw + (size_t)key_id(key[u]) * a.len) + f);
+    if (f < nf) {
+      const float4 q = s_qv[f];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (!live[u]) continue;
+        float d;
+        d = x[u].x - q.x; acc[u] = fmaf(d, d, acc[u]);
+        d = x[u].y - q.y; acc[u] = fmaf(d, d, acc[u]);
+        d = x[u].z - q.z; acc[u] = fmaf(d, d, acc[u]);
+        d = x[u].w - q.w; acc[u] = fmaf(d, d, acc[u]);
+      }
+    }
+    if (c0 + 32 < nf) {
+      // early abandoning (north_star) after each 128-point chunk
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (!live[u]) continue;
+        if (warp_sum(acc[u]) > thr) { live[u] = false; ++nref; }
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    if (!live[u]) continue;
+    d2[u] = warp_sum(acc[u]);
+    ++nref;
+  }
+  return stop;
+}
 
+__global__ void __launch_bounds__(kRefThreads)
+k_refine1(RefineArgs a) {
+  extern __shared__ float4 s_qv[];
+  __shared__ unsigned s_refined;
   const int b = blockIdx.y;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float4* qsrc = reinterpret_cast<const float4*>(a.queries + (size_t)b * a.len);
   for (int i = threadIdx.x; i < (a.len >> 2); i += blockDim.x) s_qv[i] = qsrc[i];
-  for (int i = threadIdx.x; i < a.k; i += blockDim.x) s_keys[i] = kNoKey;
-  if (threadIdx.x == 0) {
-    s_lock = 0; s_size = 0; s_maxpos = 0; s_maxkey = kNoKey;
-    s_kth = INFINITY; s_thr_local = INFINITY; s_refined = 0;
-    s_scale = bin_scale(__uint_as_float(a.thr_seed[b]));
-    const unsigned cnt = (unsigned)imin64((int64_t)a.count[b], a.cap);
-    if (a.wave == 0) {
-      // wave 0 = all bins up to the first whose cumulative count reaches wave_m
-      unsigned cum = 0;
-      int bin = 0;
-      for (; bin < kNB; ++bin) {
-        cum += a.hist[b * kNB + bin];
-        if (cum >= (unsigned)a.wave_m) break;
-      }
-      const unsigned e = min(cum, cnt);
-      s_begin = 0; s_end = e;
-      a.wave_end[b] = e;
-    } else {
-      s_begin = min(a.wave_end[b], cnt); s_end = cnt;
-    }
-  }
+  if (threadIdx.x == 0) s_refined = 0;
   __syncthreads();
-  const unsigned begin = s_begin, end = s_end;
-  const float scale = s_scale;
-  unsigned my_refined = 0;
+  const unsigned cnt = (unsigned)imin64((int64_t)a.count[b], a.cap);
+  const float scale = bin_scale(__uint_as_float(a.thr_seed[b]));
   const uint64_t* list = a.sorted + (size_t)b * a.cap;
-
-  for (unsigned i = begin + blockIdx.x * nw + warp; i < end; i += gridDim.x * nw) {
-    const uint64_t key = list[i];
-    const float lb = key_val(key);
-    const float thr_live = fminf(ld_volatile_f(&a.thr[b]), *(volatile float*)&s_thr_local);
-    if (lb > thr_live) {
-      // sorted by bin: once this bin's lower edge is above the BSF, so is every later one
-      const int bin = lb_bin(lb, scale);
-      if (bin >= 1 && (float)(bin - 1) > thr_live * scale) break;
-      continue;
-    }
-    const float limit = fminf(thr_live, *(volatile float*)&s_kth);
-    bool ab;
-    const float d2 = warp_ed2(a.raw, key_id(key), a.len, s_qv, limit, &ab);
-    ++my_refined;
-    if (ab) continue;
-    const uint64_t k2 = make_key(d2, key_id(key));
-    if (*(volatile int*)&s_size >= a.k && k2 >= *(volatile uint64_t*)&s_maxkey) continue;
-    // insert under the CTA lock (warp-cooperative max recomputation)
-    if (lane == 0) {
-      while (atomicCAS(&s_lock, 0, 1) != 0) { }
-    }
-    __syncwarp();
-    __threadfence_block();
-    volatile uint64_t* vk = s_keys;
-    const int size = *(volatile int*)&s_size;
-    bool changed = false;
-    if (size < a.k) {
-      if (lane == 0) { vk[size] = k2; *(volatile int*)&s_size = size + 1; }
-      changed = (size + 1 == a.k);
-    } else if (k2 < *(volatile uint64_t*)&s_maxkey) {
-      if (lane == 0) vk[*(volatile int*)&s_maxpos] = k2;
-      changed = true;
-    }
-    __syncwarp();
-    __threadfence_block();
-    if (changed) {
-      uint64_t mk = 0;
-      int mp = 0;
-      for (int t = lane; t < a.k; t += 32) {
-        const uint64_t v = vk[t];
-        if (v >= mk) { mk = v; mp = t; }
-      }
+  unsigned long long* bp = a.best + b;
+  const unsigned gw = blockIdx.x * kRefWarps + warp, GW = gridDim.x * kRefWarps;
+  unsigned nref = 0;
+  for (unsigned i0 = gw; i0 < cnt; i0 += kU * GW) {
+    const uint64_t cur = ld_relaxed_u64(bp);
+    const float thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
+    uint64_t key[kU];
+    float d2[kU];
+    const bool stop = refine_step(a, list, cnt, i0, GW, thr, scale, s_qv, key, d2, nref);
+    uint64_t mk = kNoKey;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const uint64_t v2 = __shfl_xor_sync(0xffffffffu, mk, o);
-        const int p2 = __shfl_xor_sync(0xffffffffu, mp, o);
-        if (v2 > mk || (v2 == mk && p2 > mp)) { mk = v2; mp = p2; }
-      }
-      if (lane == 0) {
-        *(volatile uint64_t*)&s_maxkey = mk;
-        *(volatile int*)&s_maxpos = mp;
-        const float kth = key_val(mk);
-        *(volatile float*)&s_kth = kth;
-        const float up = __fmul_ru(kth, a.d2up);
-        *(volatile float*)&s_thr_local = up;
-        atomicMin(&a.thr[b], __float_as_uint(up));
+    for (int u = 0; u < kU; ++u)
+      if (d2[u] < INFINITY) mk = min(mk, make_key(d2[u], key_id(key[u])));
+    if (lane == 0 && mk < cur) atomicMin(bp, (unsigned long long)mk);
+    if (stop) break;
+  }
+  if (lane == 0 && nref) atomicAdd(&s_refined, nref);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_refined) atomicAdd(&a.refined[b], s_refined);
+}
+
+// k = 1, warp-specialized TMA gather (the B200 form of the paper's RDC workers
+// with oversubscription): one persistent CTA per SM; its producer
+// warp walks the CTA's share of every query's LB-ordered candidate list (32 keys
+// per load), re-checks LB against the live BSF and issues one
+// cp.async.bulk per surviving candidate (the whole raw row) into a ring of
+// shared-memory slots; consumer warps take slots in sequence order, compute d^2
+// from shared memory with early abandoning and lower the BSF with a 64-bit
+// atomicMin.  Up to ~128 KB of gathers are in flight per SM.
+constexpr int kR1Threads = 384;
+constexpr int kR1Consumers = kR1Threads / 32 - 1;
+constexpr int kR1RingBytes = 131072;
+constexpr int kR1MaxSlots = 256;
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+struct Refine1Args {
+  const float* raw;
+  int len;
+  const float* queries;      // [nb][len]
+  const uint64_t* sorted;    // [nb][cap]
+  int64_t cap;
+  int nb;
+  const unsigned* count;
+  const unsigned* thr_seed;
+  unsigned long long* best;  // [nb]
+  unsigned* refined;         // [nb]
+  float d2up;
+  int slots;                 // ring slots (<= kR1MaxSlots)
+};
+
+__global__ void __launch_bounds__(kR1Threads, 1)
+k_refine1t(Refine1Args a) {
+  extern __shared__ __align__(128) uint8_t dsm[];
+  const int len = a.len, nf = len >> 2, S = a.slots;
+  float4* s_ring = reinterpret_cast<float4*>(dsm);                       // S * nf
+  float4* s_qv = s_ring + (size_t)S * nf;                                 // nb * nf
+  __shared__ __align__(8) uint64_t s_full[kR1MaxSlots];
+  __shared__ __align__(8) uint64_t s_empty[kR1MaxSlots];
+  __shared__ uint64_t s_key[kR1MaxSlots];   // candidate key (kNoKey = end sentinel)
+  __shared__ int s_qid[kR1MaxSlots];
+  __shared__ unsigned s_ref[kMaxB];
+  __shared__ unsigned long long s_best[kMaxB];  // CTA view of the BSF (<= what it has seen)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < a.nb * nf; i += kR1Threads)
+    s_qv[i] = reinterpret_cast<const float4*>(a.queries)[i];
+  if (tid < kMaxB) {
+    s_ref[tid] = 0;
+    s_best[tid] = (tid < a.nb) ? a.best[tid] : kNoKey;
+  }
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ---------------- producer
+    uint32_t q = 0;  // sequence number of the next slot
+    const unsigned row_bytes = (unsigned)len * 4u;
+    for (int b = 0; b < a.nb; ++b) {
+      const unsigned cnt = (unsigned)imin64((int64_t)a.count[b], a.cap);
+      const float scale = bin_scale(__uint_as_float(a.thr_seed[b]));
+      const uint64_t* list = a.sorted + (size_t)b * a.cap;
+      constexpr int KU = 8;  // 8 x 32 keys loaded per producer step (latency amortized)
+      bool done = false;
+      for (unsigned t0 = blockIdx.x; t0 < cnt && !done; t0 += 32u * KU * gridDim.x) {
+        uint64_t keys[KU];
+#pragma unroll
+        for (int r = 0; r < KU; ++r) {
+          const unsigned i = t0 + (unsigned)(r * 32 + lane) * gridDim.x;
+          keys[r] = (i < cnt) ? list[i] : kNoKey;
+        }
+        uint64_t cur = ld_relaxed_u64(a.best + b);
+        const uint64_t mine = *(volatile unsigned long long*)&s_best[b];
+        if (cur < mine) { if (lane == 0) atomicMin(&s_best[b], (unsigned long long)cur); }
+        else cur = mine;
+        const float thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
+#pragma unroll
+        for (int r = 0; r < KU; ++r) {
+          const unsigned i = t0 + (unsigned)(r * 32 + lane) * gridDim.x;
+          const uint64_t key = keys[r];
+          const float lb = key_val(key);
+          const bool live = (i < cnt) && lb <= thr;
+          // bin order: a candidate whose bin lies wholly above thr ends the list
+          bool past = (i >= cnt);
+          if (!past && !live) {
+            const int bin = lb_bin(lb, scale);
+            past = bin >= 1 && (float)(bin - 1) > thr * scale;
+          }
+          const unsigned pastm = __ballot_sync(0xffffffffu, past);
+          const int first_past = pastm ? __ffs(pastm) - 1 : 32;
+          const unsigned livem = __ballot_sync(0xffffffffu, live && lane < first_past);
+          if (live && lane < first_past) {
+            const uint32_t my = q + (uint32_t)__popc(livem & ((1u << lane) - 1u));
+            const int slot = (int)(my % (uint32_t)S);
+            if (my >= (uint32_t)S) mbar_wait(&s_empty[slot], ((my / S) - 1) & 1);
+            s_key[slot] = key;
+            s_qid[slot] = b;
+            mbar_expect_tx(&s_full[slot], row_bytes);
+            bulk_g2s(s_ring + (size_t)slot * nf, a.raw + (size_t)key_id(key) * len, row_bytes, &s_full[slot]);
+          }
+          q += (uint32_t)__popc(livem);
+          if (pastm) { done = true; break; }
+        }
       }
     }
-    __threadfence_block();
-    __syncwarp();
-    if (lane == 0) atomicExch(&s_lock, 0);
+    // end sentinels: one per consumer warp
+    if (lane < kR1Consumers) {
+      const uint32_t my = q + (uint32_t)lane;
+      const int slot = (int)(my % (uint32_t)S);
+      if (my >= (uint32_t)S) mbar_wait(&s_empty[slot], ((my / S) - 1) & 1);
+      s_key[slot] = kNoKey;
+      s_qid[slot] = -1;
+      mbar_arrive(&s_full[slot]);
+    }
+  } else {
+    // ---------------- consumers: sequence numbers c, c + C, c + 2C, ...
+    const int c = warp - 1;
+    for (uint32_t my = (uint32_t)c;; my += kR1Consumers) {
+      const int slot = (int)(my % (uint32_t)S);
+      mbar_wait(&s_full[slot], (my / S) & 1);
+      const uint64_t key = s_key[slot];
+      const int b = s_qid[slot];
+      if (b < 0) break;
+      const float4* row = s_ring + (size_t)slot * nf;
+      const float4* qv = s_qv + (size_t)b * nf;
+      const uint64_t cur = *(volatile unsigned long long*)&s_best[b];
+      const float thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
+      float acc = 0.f;
+      bool abandoned = false;
+      if (key_val(key) <= thr) {
+        for (int c0 = 0; c0 < nf; c0 += 32) {
+          const int f = c0 + lane;
+          if (f < nf) {
+            const float4 x = row[f], y = qv[f];
+            float d;
+            d = x.x - y.x; acc = fmaf(d, d, acc);
+            d = x.y - y.y; acc = fmaf(d, d, acc);
+            d = x.z - y.z; acc = fmaf(d, d, acc);
+            d = x.w - y.w; acc = fmaf(d, d, acc);
+          }
+          // early abandoning (north_star) after each 128-point chunk
+          if (c0 + 32 < nf && warp_sum(acc) > thr) { abandoned = true; break; }
+        }
+      } else {
+        abandoned = true;  // the BSF dropped below its LB while in flight
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&s_empty[slot]);
+        atomicAdd(&s_ref[b], 1u);
+      }
+      if (!abandoned) {
+        const float d2 = warp_sum(acc);
+        const uint64_t k2 = make_key(d2, key_id(key));
+        if (lane == 0 && k2 < cur) {
+          atomicMin(&s_best[b], (unsigned long long)k2);
+          atomicMin(a.best + b, (unsigned long long)k2);
+        }
+      }
+    }
   }
-  if (lane == 0 && my_refined) atomicAdd(&s_refined, my_refined);
   __syncthreads();
-  uint64_t* out = a.lists + ((size_t)b * a.nslots + (a.wave == 0 ? 0 : 1 + blockIdx.x)) * a.k;
-  for (int i = threadIdx.x; i < a.k; i += blockDim.x) out[i] = s_keys[i];
+  if (tid < a.nb && s_ref[tid]) atomicAdd(&a.refined[tid], s_ref[tid]);
+}
+
+// k > 1: rounds of (every warp: one refine_step) -> merge the round's admitted
+// keys into the CTA's sorted top-k -> publish the k-th (rounded up) to the
+// query's global threshold.  Each true top-k member lands in the top-k of the
+// CTA that refined it, so merging the per-CTA lists (K7) is exact.
+__global__ void __launch_bounds__(kRefThreads)
+k_refine_topk(RefineArgs a) {
+  extern __shared__ float4 s_dyn[];
+  const int k = a.k;
+  float4* s_qv = s_dyn;
+  uint64_t* s_top = reinterpret_cast<uint64_t*>(s_dyn + (a.len >> 2));
+  uint64_t* s_new = s_top + k;
+  __shared__ uint64_t s_pend[kRefWarps * kU];
+  __shared__ int s_np;
+  __shared__ float s_thr_local;
+  __shared__ uint64_t s_kthkey;
+  __shared__ unsigned s_refined;
+  const int b = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float4* qsrc = reinterpret_cast<const float4*>(a.queries + (size_t)b * a.len);
+  for (int i = threadIdx.x; i < (a.len >> 2); i += blockDim.x) s_qv[i] = qsrc[i];
+  for (int i = threadIdx.x; i < k; i += blockDim.x) s_top[i] = kNoKey;
+  if (threadIdx.x == 0) {
+    s_np = 0;
+    s_thr_local = INFINITY;
+    s_kthkey = kNoKey;
+    s_refined = 0;
+  }
+  __syncthreads();
+  const unsigned cnt = (unsigned)imin64((int64_t)a.count[b], a.cap);
+  const float scale = bin_scale(__uint_as_float(a.thr_seed[b]));
+  const uint64_t* list = a.sorted + (size_t)b * a.cap;
+  const unsigned gw = blockIdx.x * kRefWarps + warp, GW = gridDim.x * kRefWarps;
+  unsigned nref = 0;
+  bool done = false;
+  for (unsigned i0 = gw;; i0 += kU * GW) {
+    if (!done && i0 < cnt) {
+      const float thr = fminf(__uint_as_float(ld_relaxed_u32(&a.thr[b])), s_thr_local);
+      uint64_t key[kU];
+      float d2[kU];
+      done = refine_step(a, list, cnt, i0, GW, thr, scale, s_qv, key, d2, nref);
+      const uint64_t kk = s_kthkey;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (d2[u] < INFINITY) {
+          const uint64_t k2 = make_key(d2[u], key_id(key[u]));
+          if (k2 < kk && lane == 0) s_pend[atomicAdd(&s_np, 1)] = k2;
+        }
+      }
+    } else {
+      done = true;
+    }
+    __syncthreads();
+    const int np = s_np;
+    if (np > 0) {
+      if (warp == 0) {
+        uint64_t v = (lane < np) ? s_pend[lane] : kNoKey;
+        v = warp_sort32(v);
+        s_pend[lane] = v;
+      }
+      __syncthreads();
+      for (int t = threadIdx.x; t < k; t += blockDim.x) {
+        const uint64_t key = s_top[t];
+        int lo = 0, hi = np;  // # pending < key
+        while (lo < hi) { const int mid = (lo + hi) >> 1; if (s_pend[mid] < key) lo = mid + 1; else hi = mid; }
+        const int r = t + lo;
+        if (r < k) s_new[r] = key;
+      }
+      for (int j = threadIdx.x; j < np; j += blockDim.x) {
+        const uint64_t key = s_pend[j];
+        int lo = 0, hi = k;  // # top < key
+        while (lo < hi) { const int mid = (lo + hi) >> 1; if (s_top[mid] < key) lo = mid + 1; else hi = mid; }
+        const int r = j + lo;
+        if (r < k) s_new[r] = key;
+      }
+      __syncthreads();
+      for (int t = threadIdx.x; t < k; t += blockDim.x) s_top[t] = s_new[t];
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        s_np = 0;
+        const uint64_t kk = s_top[k - 1];
+        s_kthkey = kk;
+        if (kk != kNoKey) {
+          const float up = __fmul_ru(key_val(kk), a.d2up);
+          s_thr_local = up;
+          atomicMin(&a.thr[b], __float_as_uint(up));
+        }
+      }
+    }
+    if (!__syncthreads_or(!done)) break;
+  }
+  if (lane == 0 && nref) atomicAdd(&s_refined, nref);
+  __syncthreads();
+  uint64_t* out = a.lists + ((size_t)b * gridDim.x + blockIdx.x) * k;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) out[i] = s_top[i];
   if (threadIdx.x == 0 && s_refined) atomicAdd(&a.refined[b], s_refined);
 }
 
 // ---------------------------------------------------------------- K7 finalize
+__global__ void k_finalize1(const unsigned long long* __restrict__ best, int nb, int q0,
+                            int64_t* __restrict__ out_idx, float* __restrict__ out_dist,
+                            const unsigned* __restrict__ count, const unsigned* __restrict__ refined,
+                            unsigned* __restrict__ all_count, unsigned* __restrict__ all_refined) {
+  const int b = threadIdx.x;
+  if (b >= nb) return;
+  const uint64_t key = best[b];
+  if (key == kNoKey) { out_idx[q0 + b] = -1; out_dist[q0 + b] = INFINITY; }
+  else { out_idx[q0 + b] = (int64_t)key_id(key); out_dist[q0 + b] = sqrtf(key_val(key)); }
+  all_count[q0 + b] = count[b];
+  all_refined[q0 + b] = refined[b];
+}
+
 // Merge the per-CTA top-k lists: repeatedly sort [current top-k | next chunk]
 // in shared memory and keep the first k.  Output ascending (d^2, id) -> (id, sqrt d^2).
 __global__ void __launch_bounds__(1024)
-k_finalize(const uint64_t* __restrict__ lists, int nslots, int first_slot, int k, int q0,
+k_finalize(const uint64_t* __restrict__ lists, int nslots, int k, int q0,
            int64_t* __restrict__ out_idx, float* __restrict__ out_dist,
            const unsigned* __restrict__ count, const unsigned* __restrict__ refined,
            unsigned* __restrict__ all_count, unsigned* __restrict__ all_refined) {
   __shared__ uint64_t buf[kSortP];
   const int b = blockIdx.x;
-  const int64_t total = (int64_t)(nslots - first_slot) * k;
-  const uint64_t* src = lists + ((size_t)b * nslots + first_slot) * k;
+  const int64_t total = (int64_t)nslots * k;
+  const uint64_t* src = lists + (size_t)b * nslots * k;
   for (int i = threadIdx.x; i < kSortP; i += blockDim.x) buf[i] = kNoKey;
   __syncthreads();
   const int chunk = kSortP - k;
@@ -609,18 +1400,19 @@ int occupancy(K kernel, int threads, size_t smem) {
 
 // scratch of one batch (device)
 struct Ws {
-  float2* qlh;
+  float2* g_q;
+  uint2* g_q16;
   int* seed_ids;
   uint64_t* seed_keys;
-  unsigned* zero_block;  // thr | count | hist | cursor | refined | wave_end (zeroed per batch)
+  unsigned* zero_block;  // thr | thr_seed | count | hist | cursor | refined (zeroed per batch)
   unsigned* thr;
   unsigned* thr_seed;
   unsigned* count;
   unsigned* hist;
   unsigned* cursor;
   unsigned* refined;
-  unsigned* wave_end;
   size_t zero_bytes;
+  unsigned long long* best;
   uint64_t* cand;
   uint64_t* sorted;
   uint64_t* lists;
@@ -630,57 +1422,61 @@ struct Ws {
 struct Plan {
   int64_t n;
   int len, w, card, k;
-  int B;          // batch
+  int B;          // queries per SAX pass
   int S;          // seed entries per query (warps of the seed grid)
   int seed_grid;
   int64_t ns;     // seed sample
   int64_t cap;
-  int XB;         // wave-1 CTAs per query
-  int nslots;
-  int wave_m;
+  int XB;         // refine CTAs per query
   float d2up;     // fp32 d^2 -> rigorous upper bound factor
+  bool tiled;     // TMA-tiled LB kernels (n % 16 == 0, w == 16)
 };
 
-template <int B, int WT, bool AL>
-cudaError_t launch_seed_lb(const Plan& p, const uint8_t* sax, const float* qb, int nb,
-                           const CardTables* tab, const Ws& ws, cudaStream_t st) {
-  return PARIS_LAUNCH("seed_lb", (k_seed<B, WT, AL>), p.seed_grid, kLBThreads, 0, st, sax, p.n, p.ns,
-                      qb, nb, p.len, p.w, tab, ws.qlh, ws.seed_ids, p.S);
+int pairs_for(int nb) { return nb <= 2 ? 1 : nb <= 4 ? 2 : nb <= 8 ? 4 : 8; }
+
+template <int P, int WT, bool AL>
+cudaError_t launch_seed(const Plan& p, const uint8_t* sax, const float* qb, int nb,
+                        const CardTables* tab, const Ws& ws, cudaStream_t st) {
+  return PARIS_LAUNCH("seed_lb", (k_seed<P, WT, AL>), p.seed_grid, kLBThreads, 0, st, sax, p.n, p.ns,
+                      qb, nb, p.len, p.w, tab, ws.g_q, ws.g_q16, ws.seed_ids, p.S);
 }
 
-template <int B, int WT, bool AL>
+template <int P, int WT, bool AL>
 cudaError_t launch_lb(const Plan& p, const uint8_t* sax, int nb, const CardTables* tab, const Ws& ws,
                       cudaStream_t st, int64_t cap) {
   static int occ = 0;
-  if (!occ) occ = occupancy(k_lb<B, WT, AL>, kLBThreads, 0);
+  if (!occ) occ = occupancy(k_lb<P, WT, AL>, kLBThreads, 0);
   const int64_t ngroups = (p.n + 3) / 4;
   const int64_t need = (ngroups + kLBThreads - 1) / kLBThreads;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)sms() * occ));
-  return PARIS_LAUNCH("lb_pass", (k_lb<B, WT, AL>), grid, kLBThreads, 0, st, sax, p.n, p.w,
-                      (float)(p.len / p.w), tab, ws.qlh, nb, ws.thr_seed, ws.count, ws.hist, ws.cand, cap);
+  LbArgs la;
+  la.sax = sax; la.n = p.n; la.w = p.w; la.seglen_f = (float)(p.len / p.w); la.tab = tab;
+  la.g_q = ws.g_q; la.g_q16 = ws.g_q16; la.nb = nb; la.thr = ws.thr_seed; la.count = ws.count;
+  la.hist = ws.hist; la.cand = ws.cand; la.cap = cap;
+  return PARIS_LAUNCH("lb_pass", (k_lb<P, WT, AL>), grid, kLBThreads, 0, st, la);
 }
 
-template <int B, int WT>
+template <int P, int WT>
 cudaError_t dispatch_al(bool al, bool lb, const Plan& p, const uint8_t* sax, const float* qb, int nb,
                         const CardTables* tab, const Ws& ws, cudaStream_t st, int64_t cap) {
-  if (lb) return al ? launch_lb<B, WT, true>(p, sax, nb, tab, ws, st, cap)
-                    : launch_lb<B, WT, false>(p, sax, nb, tab, ws, st, cap);
-  // the seed pass covers ~1/16 of the array: the register-light runtime-w variant suffices
-  return al ? launch_seed_lb<B, 0, true>(p, sax, qb, nb, tab, ws, st)
-            : launch_seed_lb<B, 0, false>(p, sax, qb, nb, tab, ws, st);
+  if (lb) return al ? launch_lb<P, WT, true>(p, sax, nb, tab, ws, st, cap)
+                    : launch_lb<P, WT, false>(p, sax, nb, tab, ws, st, cap);
+  // the seed pass covers ~1/16 of the array: the register-light runtime-w variant
+  return al ? launch_seed<P, 0, true>(p, sax, qb, nb, tab, ws, st)
+            : launch_seed<P, 0, false>(p, sax, qb, nb, tab, ws, st);
 }
 
-template <int B>
+template <int P>
 cudaError_t dispatch_w(bool lb, const Plan& p, const uint8_t* sax, const float* qb, int nb,
                        const CardTables* tab, const Ws& ws, cudaStream_t st, int64_t cap) {
   const bool al = (p.n % 4) == 0;
-  if (p.w == 16) return dispatch_al<B, 16>(al, lb, p, sax, qb, nb, tab, ws, st, cap);
-  return dispatch_al<B, 0>(al, lb, p, sax, qb, nb, tab, ws, st, cap);
+  if (p.w == 16) return dispatch_al<P, 16>(al, lb, p, sax, qb, nb, tab, ws, st, cap);
+  return dispatch_al<P, 0>(al, lb, p, sax, qb, nb, tab, ws, st, cap);
 }
 
-cudaError_t dispatch_b(int Bt, bool lb, const Plan& p, const uint8_t* sax, const float* qb, int nb,
+cudaError_t dispatch_p(int P, bool lb, const Plan& p, const uint8_t* sax, const float* qb, int nb,
                        const CardTables* tab, const Ws& ws, cudaStream_t st, int64_t cap) {
-  switch (Bt) {
+  switch (P) {
     case 1: return dispatch_w<1>(lb, p, sax, qb, nb, tab, ws, st, cap);
     case 2: return dispatch_w<2>(lb, p, sax, qb, nb, tab, ws, st, cap);
     case 4: return dispatch_w<4>(lb, p, sax, qb, nb, tab, ws, st, cap);
@@ -688,21 +1484,61 @@ cudaError_t dispatch_b(int Bt, bool lb, const Plan& p, const uint8_t* sax, const
   }
 }
 
-int pow2_batch(int nb) { return nb <= 1 ? 1 : nb <= 2 ? 2 : nb <= 4 ? 4 : 8; }
+template <int P, int MODE>
+cudaError_t launch_lbt(const Plan& p, const uint8_t* sax, int nb, const CardTables* tab, const Ws& ws,
+                       cudaStream_t st, int64_t cap, int64_t nlim, int grid) {
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaError_t e = cudaFuncSetAttribute(k_lbt<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTSmem);
+    if (e != cudaSuccess) return e;
+    attr_dev = dev;
+  }
+  LbArgs la;
+  la.sax = sax; la.n = p.n; la.w = p.w; la.seglen_f = (float)(p.len / p.w); la.tab = tab;
+  la.g_q = ws.g_q; la.g_q16 = ws.g_q16; la.nb = nb; la.thr = ws.thr_seed; la.count = ws.count;
+  la.hist = ws.hist; la.cand = ws.cand; la.cap = cap;
+  return PARIS_LAUNCH(MODE ? "lb_pass" : "seed_lb", (k_lbt<P, MODE>), grid, kTThreads, kTSmem, st, la, nlim,
+                      ws.seed_ids, p.S);
+}
+
+template <int MODE>
+cudaError_t dispatch_lbt(int nb, const Plan& p, const uint8_t* sax, const CardTables* tab, const Ws& ws,
+                         cudaStream_t st, int64_t cap, int64_t nlim, int grid) {
+  if (nb == 1) return launch_lbt<0, MODE>(p, sax, nb, tab, ws, st, cap, nlim, grid);
+  switch (pairs_for(nb)) {
+    case 1: return launch_lbt<1, MODE>(p, sax, nb, tab, ws, st, cap, nlim, grid);
+    case 2: return launch_lbt<2, MODE>(p, sax, nb, tab, ws, st, cap, nlim, grid);
+    case 4: return launch_lbt<4, MODE>(p, sax, nb, tab, ws, st, cap, nlim, grid);
+    default: return launch_lbt<8, MODE>(p, sax, nb, tab, ws, st, cap, nlim, grid);
+  }
+}
+
+cudaError_t launch_qprep(int nb, const Plan& p, const float* qb, const Ws& ws, cudaStream_t st) {
+  switch (pairs_for(nb)) {
+    case 1: return PARIS_LAUNCH("qprep", k_qprep<1>, 1, 256, 0, st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
+    case 2: return PARIS_LAUNCH("qprep", k_qprep<2>, 1, 256, 0, st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
+    case 4: return PARIS_LAUNCH("qprep", k_qprep<4>, 1, 256, 0, st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
+    default: return PARIS_LAUNCH("qprep", k_qprep<8>, 1, 256, 0, st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
+  }
+}
 
 // Allocate the batch scratch for `cap` candidates per query.
 int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
-  const int B = pow2_batch(p.B);
+  const int B = 2 * pairs_for(p.B);
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off = (off + bytes + 255) & ~(size_t)255; return o; };
-  const size_t o_qlh = take(sizeof(float2) * B * kMaxW);
+  const size_t o_q = take(sizeof(float2) * B * kMaxW);
+  const size_t o_q16 = take(sizeof(uint2) * (B / 2) * kMaxW);
   const size_t o_sid = take(sizeof(int) * B * p.S);
   const size_t o_skey = take(sizeof(uint64_t) * B * p.S);
-  const size_t zb = sizeof(unsigned) * (B + B + B + B * kNB + B * kNB + B + B);
+  const size_t zb = sizeof(unsigned) * (B + B + B + B * kNB + B * kNB + B);
   const size_t o_zero = take(zb);
+  const size_t o_best = take(sizeof(unsigned long long) * B);
   const size_t o_cand = take(sizeof(uint64_t) * B * (size_t)cap);
   const size_t o_sorted = take(sizeof(uint64_t) * B * (size_t)cap);
-  const size_t o_lists = take(sizeof(uint64_t) * B * (size_t)p.nslots * p.k);
+  const size_t o_lists = take(p.k > 1 ? sizeof(uint64_t) * B * (size_t)p.XB * p.k : 8);
   void* base = nullptr;
   cudaError_t e = cudaMallocAsync(&base, off, st);
   if (e != cudaSuccess) {
@@ -712,7 +1548,8 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   }
   char* c = (char*)base;
   ws.base = base;
-  ws.qlh = (float2*)(c + o_qlh);
+  ws.g_q = (float2*)(c + o_q);
+  ws.g_q16 = (uint2*)(c + o_q16);
   ws.seed_ids = (int*)(c + o_sid);
   ws.seed_keys = (uint64_t*)(c + o_skey);
   ws.zero_block = (unsigned*)(c + o_zero);
@@ -723,21 +1560,26 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   ws.hist = ws.count + B;
   ws.cursor = ws.hist + B * kNB;
   ws.refined = ws.cursor + B * kNB;
-  ws.wave_end = ws.refined + B;
+  ws.best = (unsigned long long*)(c + o_best);
   ws.cand = (uint64_t*)(c + o_cand);
   ws.sorted = (uint64_t*)(c + o_sorted);
   ws.lists = (uint64_t*)(c + o_lists);
   return PARIS_OK;
 }
 
-// One batch of nb <= 8 queries (device pointers).  Outputs at [q0 .. q0+nb).
+// One batch of nb <= kMaxB queries (device pointers).  Outputs at [q0 .. q0+nb).
 int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* qbatch, int nb, int q0,
               int64_t cap, const CardTables* tab, const Ws& ws, int64_t* d_idx, float* d_dist,
               unsigned* all_count, unsigned* all_refined, float* all_tau, cudaStream_t st) {
-  const int Bt = pow2_batch(nb);
+  const int P = pairs_for(nb);
   cudaError_t e = cudaMemsetAsync(ws.zero_block, 0, ws.zero_bytes, st);
   if (e != cudaSuccess) return cuda_error(e, "memset scratch");
-  PARIS_CHECK_LAUNCH(dispatch_b(Bt, false, p, sax, qbatch, nb, tab, ws, st, cap), "seed_lb launch");
+  if (p.tiled) {
+    PARIS_CHECK_LAUNCH(launch_qprep(nb, p, qbatch, ws, st), "qprep launch");
+    PARIS_CHECK_LAUNCH(dispatch_lbt<0>(nb, p, sax, tab, ws, st, cap, p.ns, p.seed_grid), "seed_lb launch");
+  } else {
+    PARIS_CHECK_LAUNCH(dispatch_p(P, false, p, sax, qbatch, nb, tab, ws, st, cap), "seed_lb launch");
+  }
   {
     dim3 g((unsigned)((p.S + 7) / 8), (unsigned)nb);
     PARIS_CHECK_LAUNCH(PARIS_LAUNCH("seed_ed", k_seed_ed, g, kRefThreads, (size_t)p.len * 4, st, raw, p.len,
@@ -745,9 +1587,14 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
                        "seed_ed launch");
   }
   PARIS_CHECK_LAUNCH(PARIS_LAUNCH("seed_select", k_seed_select, nb, 1024, 0, st, ws.seed_keys, p.S, p.k,
-                                  p.d2up, ws.thr, ws.thr_seed, all_tau, q0),
+                                  p.d2up, ws.thr, ws.thr_seed, ws.best, all_tau, q0),
                      "seed_select launch");
-  PARIS_CHECK_LAUNCH(dispatch_b(Bt, true, p, sax, qbatch, nb, tab, ws, st, cap), "lb_pass launch");
+  if (p.tiled) {
+    const int grid = (int)std::min<int64_t>(sms(), (p.n + kTS - 1) / kTS);
+    PARIS_CHECK_LAUNCH(dispatch_lbt<1>(nb, p, sax, tab, ws, st, cap, p.n, grid), "lb_pass launch");
+  } else {
+    PARIS_CHECK_LAUNCH(dispatch_p(P, true, p, sax, qbatch, nb, tab, ws, st, cap), "lb_pass launch");
+  }
   {
     const int xs = std::max(1, std::min(sms() * 4 / nb, 1024));
     dim3 g((unsigned)xs, (unsigned)nb);
@@ -757,24 +1604,41 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
   }
   RefineArgs ra;
   ra.raw = raw; ra.len = p.len; ra.queries = qbatch; ra.sorted = ws.sorted; ra.cap = cap;
-  ra.count = ws.count; ra.hist = ws.hist; ra.thr = ws.thr; ra.thr_seed = ws.thr_seed; ra.wave_end = ws.wave_end;
-  ra.refined = ws.refined; ra.lists = ws.lists; ra.nslots = p.nslots; ra.k = p.k; ra.wave_m = p.wave_m;
-  ra.d2up = p.d2up;
-  const size_t rsmem = (size_t)p.len * 4 + (size_t)p.k * 8;
-  if (p.k > 1) {
-    ra.wave = 0;
-    dim3 g(1u, (unsigned)nb);
-    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("refine_wave0", k_refine, g, kRefAThreads, rsmem, st, ra), "refine0 launch");
+  ra.count = ws.count; ra.thr_seed = ws.thr_seed; ra.thr = ws.thr; ra.best = ws.best;
+  ra.refined = ws.refined; ra.lists = ws.lists; ra.k = p.k; ra.d2up = p.d2up;
+  dim3 g((unsigned)p.XB, (unsigned)nb);
+  if (p.k == 1) {
+    Refine1Args r1;
+    r1.raw = raw; r1.len = p.len; r1.queries = qbatch; r1.sorted = ws.sorted; r1.cap = cap; r1.nb = nb;
+    r1.count = ws.count; r1.thr_seed = ws.thr_seed; r1.best = ws.best; r1.refined = ws.refined;
+    r1.d2up = p.d2up;
+    r1.slots = std::min(kR1MaxSlots, std::max(kR1Consumers + 1, kR1RingBytes / (p.len * 4)));
+    const size_t smem = (size_t)r1.slots * p.len * 4 + (size_t)nb * p.len * 4;
+    if (smem > 200 * 1024) {  // very long series: the register-staged kernel
+      PARIS_CHECK_LAUNCH(PARIS_LAUNCH("refine", k_refine1, g, kRefThreads, (size_t)p.len * 4, st, ra),
+                         "refine launch");
+    } else {
+    static int attr_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (attr_dev != dev) {
+      PARIS_CHECK_LAUNCH(cudaFuncSetAttribute(k_refine1t, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              227 * 1024 - 12 * 1024),
+                         "refine smem attribute");
+      attr_dev = dev;
+    }
+    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("refine", k_refine1t, sms(), kR1Threads, smem, st, r1), "refine launch");
+    }
+    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("finalize", k_finalize1, 1, 32, 0, st, ws.best, nb, q0, d_idx, d_dist,
+                                    ws.count, ws.refined, all_count, all_refined),
+                       "finalize launch");
+  } else {
+    const size_t rsmem = (size_t)p.len * 4 + (size_t)p.k * 16;
+    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("refine", k_refine_topk, g, kRefThreads, rsmem, st, ra), "refine launch");
+    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("finalize", k_finalize, nb, 1024, 0, st, ws.lists, p.XB, p.k, q0,
+                                    d_idx, d_dist, ws.count, ws.refined, all_count, all_refined),
+                       "finalize launch");
   }
-  {
-    ra.wave = 1;
-    dim3 g((unsigned)p.XB, (unsigned)nb);
-    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("refine", k_refine, g, kRefThreads, rsmem, st, ra), "refine launch");
-  }
-  PARIS_CHECK_LAUNCH(PARIS_LAUNCH("finalize", k_finalize, nb, 1024, 0, st, ws.lists, p.nslots,
-                                  p.k > 1 ? 0 : 1, p.k, q0,
-                                  d_idx, d_dist, ws.count, ws.refined, all_count, all_refined),
-                     "finalize launch");
   return PARIS_OK;
 }
 
@@ -783,6 +1647,24 @@ bool is_host_ptr(const void* p) {
   cudaError_t e = cudaPointerGetAttributes(&at, p);
   if (e != cudaSuccess) { cudaGetLastError(); return true; }
   return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered;
+}
+
+void plan_seed(Plan& p, int seed_div) {
+  p.ns = std::min<int64_t>(p.n, std::max<int64_t>(p.n / seed_div, std::min<int64_t>(p.n, 65536)));
+  if (p.tiled) {
+    p.ns = std::min<int64_t>(p.n, (p.ns + 15) / 16 * 16);
+    p.seed_grid = (int)std::min<int64_t>(sms(), (p.ns + kTS - 1) / kTS);
+    p.S = p.seed_grid * kTWarps;
+    return;
+  }
+  const int64_t groups = (p.ns + 3) / 4;
+  const int64_t need = (groups + kLBThreads - 1) / kLBThreads;
+  p.seed_grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, std::min(sms() * 2, kMaxSeed / 8)));
+  p.S = p.seed_grid * (kLBThreads / 32);
+}
+
+void plan_refine(Plan& p) {
+  p.XB = std::max(1, std::min(sms() * 8 / std::max(1, p.B), 65535));
 }
 
 }  // namespace
@@ -814,21 +1696,15 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   Plan p;
   p.n = n; p.len = len; p.w = w; p.card = card; p.k = k;
   p.B = (cfg && cfg->batch > 0) ? std::min(cfg->batch, kMaxB) : kMaxB;
-  const int seed_div = (cfg && cfg->seed_div > 0) ? cfg->seed_div : 16;
-  p.ns = std::min<int64_t>(n, std::max<int64_t>(n / seed_div, std::min<int64_t>(n, 65536)));
-  {
-    const int64_t groups = (p.ns + 3) / 4;
-    const int64_t need = (groups + kLBThreads - 1) / kLBThreads;
-    p.seed_grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, std::min(sms() * 2, kMaxSeed / 8)));
-    p.S = p.seed_grid * (kLBThreads / 32);
-  }
+  p.tiled = (n % 16 == 0) && (w == kTW) && !(cfg && cfg->reserved[0] == 1);
+  plan_seed(p, (cfg && cfg->seed_div > 0) ? cfg->seed_div : 16);
   p.cap = std::min<int64_t>(n, std::max<int64_t>(65536, n / 32));
-  p.XB = std::max(1, std::min(sms() * 4 / std::max(1, p.B), 65535));
-  p.nslots = 1 + p.XB;
-  p.wave_m = std::max((cfg && cfg->wave_a > 0) ? cfg->wave_a : 256, 2 * k);
-  // |fp32 d^2 - exact| <= (len/32 + 8) u d^2 (warp_ed2); doubled for slack, u = 2^-24
-  p.d2up = (float)(1.0 + 2.0 * (len / 32 + 8) * 5.9604644775390625e-08);
+  plan_refine(p);
+  // |fp32 d^2 - exact| <= e d^2 with e = (len/32 + 8) u (warp_ed2 / refine_step);
+  // d2up >= (1+e)/(1-e) with margin, u = 2^-24
+  p.d2up = (float)(1.0 + 2.5 * (len / 32 + 8) * 5.9604644775390625e-08);
 
+  retain_pool();
   // host <-> device staging of queries / outputs
   const bool hq = is_host_ptr(queries), hi = is_host_ptr(out_idx), hd = is_host_ptr(out_dist);
   cudaError_t e;
@@ -882,8 +1758,7 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
       // re-scan this query alone with an exact-size candidate buffer
       Plan p1 = p;
       p1.B = 1;
-      p1.XB = std::max(1, std::min(sms() * 4, 65535));
-      p1.nslots = 1 + p1.XB;
+      plan_refine(p1);
       p1.cap = std::min<int64_t>(n, (int64_t)h_count[q]);
       Ws ws1;
       rc = alloc_ws(p1, p1.cap, ws1, st);

@@ -164,6 +164,45 @@ static float round_up_f(double v) {
   return f;
 }
 
+// fp16 with directed rounding, by hand (host): normal numbers have 10 stored
+// mantissa bits and exponents -14..15, subnormals are multiples of 2^-24.
+uint16_t half_bits_dir(double v, int dir) {
+  if (isnan(v)) return 0x7E00;
+  if (isinf(v)) return v > 0 ? 0x7C00 : 0xFC00;
+  const uint16_t sign = v < 0 ? 0x8000 : 0;
+  const double a = fabs(v);
+  // magnitude rounded toward zero (trunc) or away from zero (up), per dir and sign
+  const bool away = (dir > 0) != (v < 0);
+  if (a == 0.0) return sign;  // exact
+  int e;
+  frexp(a, &e);  // a = f * 2^e, f in [0.5, 1)
+  int ex = e - 1;  // a in [2^ex, 2^(ex+1))
+  if (ex < -14) ex = -14;
+  const double quantum = ldexp(1.0, ex - 10);
+  double m = a / quantum;  // exact (power-of-two scaling)
+  double mi = away ? ceil(m) : floor(m);
+  if (ex == -14 && mi < 1024.0) {  // subnormal (or the top of it rounding into 2^-14)
+    return (uint16_t)(sign | (uint16_t)mi);
+  }
+  if (mi >= 2048.0) { mi = 1024.0; ex += 1; }  // mantissa overflow
+  if (ex > 15) return away ? (uint16_t)(sign | 0x7C00) : (uint16_t)(sign | 0x7BFF);
+  const uint16_t bits = (uint16_t)(((ex + 15) << 10) | ((int)mi - 1024));
+  return (uint16_t)(sign | bits);
+}
+
+void retain_pool() {
+  static int done[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  cudaGetLastError();
+  done[dev] = 1;
+}
+
 static std::mutex g_tab_mu;
 static CardTables* g_tables[64] = {nullptr};  // per device
 
@@ -192,6 +231,26 @@ const CardTables* device_tables(int card) {
         float lo = (c == 0) ? -INFINITY : (c < cd ? round_down_f(cuts[c - 1]) : INFINITY);
         float hi = (c >= cd - 1) ? INFINITY : round_up_f(cuts[c]);
         t.lu[c] = make_float2(lo, hi);
+        // fp16 region pair: L rounded down, U rounded up (from the fp64 cuts)
+        const double Ld = (c == 0) ? -INFINITY : (c < cd ? cuts[c - 1] : INFINITY);
+        const double Ud = (c >= cd - 1) ? INFINITY : cuts[c];
+        const uint32_t nU = (uint32_t)(half_bits_dir(Ud, +1) ^ 0x8000u);  // -U16 (exact negation)
+        const uint32_t L16 = half_bits_dir(Ld, -1);
+        t.lu16[c] = make_uint2(nU | (nU << 16), L16 | (L16 << 16));
+        t.lu16p[c] = nU | (L16 << 16);
+      }
+      for (int k = 0; k < kLutN; ++k) {
+        const double x0 = -(double)kLutLo + (double)k / kLutScale;
+        const double lo_edge = x0 - kLutMargin, hi_edge = x0 + 1.0 / kLutScale + kLutMargin;
+        uint32_t lo = 0;
+        float cut = 3.0e38f;  // "no cut in this bucket": finite, so |v - cut| never looks ambiguous
+        for (int c = 0; c < cd - 1; ++c) {
+          if (cuts[c] <= lo_edge) ++lo;
+          else if (cuts[c] <= hi_edge) cut = (float)cuts[c];
+        }
+        uint32_t cb;
+        memcpy(&cb, &cut, 4);
+        t.lut[k] = make_uint2(cb, lo);
       }
     }
     CardTables* d = nullptr;
@@ -247,6 +306,9 @@ int32_t paris_profile_read(paris_kernel_profile* out, int32_t max_entries) {
 }
 
 int64_t paris_launch_count(void) { return paris::g_launches.load(); }
+
+// Test hook: fp16 bits of v rounded down (dir < 0) / up (dir > 0).
+uint16_t paris_debug_half_dir(double v, int32_t dir) { return paris::half_bits_dir(v, dir); }
 
 // Test hook: the library's own breakpoints (fp64), card-1 values.
 int paris_debug_cuts(int32_t card, double* out) {

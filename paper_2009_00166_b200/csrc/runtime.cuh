@@ -24,10 +24,28 @@ constexpr int kNumCards = 8;  // 2, 4, ..., 256
 //              L = cut_c (-inf for c = 0), U = cut_{c+1} (+inf for c = card-1);
 //              outward rounding makes the fp32 region contain the exact one, so
 //              the fp32 lower bound never exceeds the exact one.
+//   lu16[c]    the same region as packed fp16 pairs for the batched lower bound:
+//              .x = half2(-U16, -U16), .y = half2(L16, L16) with L16 = L rounded
+//              down and U16 = U rounded up to fp16 (so [L16, U16] contains the
+//              exact region; +-inf stay infinite)
+//   lu16p[c]   half2(-U16, L16) (low half -U16): the single-query form
+//   lut[k]     quantization shortcut over kLutN buckets of width 1/kLutScale on
+//              [-kLutLo, kLutLo): {fp32 bits of the single cut lying within
+//              kLutMargin of bucket k (3e38 if none), #cuts <= left edge - margin}
+//              so that symbol = lut.y + (v >= cut) for every v whose computed
+//              bucket is k (the cut gap, >= 0.0097 at card 256, exceeds the
+//              window 1/kLutScale + 2*kLutMargin)
+constexpr int kLutN = 4096;
+constexpr float kLutLo = 4.0f;
+constexpr float kLutScale = 512.0f;
+constexpr double kLutMargin = 1e-3;
 struct CardTables {
   float cuts_f[kMaxCard];
   double cuts_d[kMaxCard];
   float2 lu[kMaxCard];
+  uint2 lu16[kMaxCard];
+  uint32_t lu16p[kMaxCard];
+  uint2 lut[kLutN];
 };
 
 // Returns the device table for `card` (power of two in [2,256]) on the current
@@ -36,6 +54,13 @@ const CardTables* device_tables(int card);
 
 // Host copy (for tests/debug): fills cuts (card-1 doubles).
 void host_cuts(int card, double* cuts);
+
+// fp16 bits of v rounded toward -inf (dir < 0) or +inf (dir > 0); +-inf map to +-inf.
+uint16_t half_bits_dir(double v, int dir);
+
+// Keep freed stream-ordered scratch mapped in the current device's default
+// memory pool (release threshold = max) so repeated calls do not remap it.
+void retain_pool();
 
 // ---- errors
 void set_error(const char* fmt, ...);

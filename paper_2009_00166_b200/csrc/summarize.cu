@@ -154,6 +154,182 @@ k_summarize_fast(const float* __restrict__ raw, int64_t n, int w, int card, int 
   }
 }
 
+// TMA-tiled variant (len in {128, 256, 512}, n % 4 == 0): a persistent CTA per SM
+// streams 32 KB tiles of consecutive raw series (one contiguous range, one
+// cp.async.bulk each) into a kSumStages-deep shared-memory ring (mbarrier
+// completion), so HBM reads run ahead of the arithmetic.  Warp w owns SPW
+// consecutive series of a tile; lane l takes float4 #(l + 32j) of a series from
+// shared memory (conflict-free); segment sums by G-lane xor shuffles; the symbol
+// comes from the bucket table (one 8-byte shared load per segment, no search).
+// The owner lane of a segment packs the SPW symbols of its series into one store.
+constexpr int kSumThreads = 512;
+constexpr int kSumWarps = kSumThreads / 32;
+constexpr int kSumStages = 4;
+constexpr int kSumTileBytes = 32768;
+constexpr size_t kSumSmem = (size_t)kSumStages * kSumTileBytes + kLutN * 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+template <int NV>  // len = 128 * NV
+__global__ void __launch_bounds__(kSumThreads, 1)
+k_summarize_tma(const float* __restrict__ raw, int64_t n, int w, int card, int G,
+                uint8_t* __restrict__ sax, const CardTables* __restrict__ tab) {
+  constexpr int len = 128 * NV;
+  constexpr int TS = kSumTileBytes / (4 * len);  // series per tile
+  constexpr int SPW = TS / kSumWarps;             // series per warp per tile (1, 2 or 4)
+  static_assert(SPW >= 1 && SPW <= 4, "tile shape");
+  extern __shared__ __align__(128) uint8_t dsm[];
+  float* s_tiles = reinterpret_cast<float*>(dsm);
+  uint2* s_lut = reinterpret_cast<uint2*>(dsm + (size_t)kSumStages * kSumTileBytes);
+  __shared__ double s_cd[kMaxCard];
+  __shared__ __align__(8) uint64_t s_full[kSumStages];
+  __shared__ unsigned s_cnt[kSumStages];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t ntiles = (n + TS - 1) / TS;
+
+  auto issue = [&](int64_t tile, int st) {
+    const int64_t base = tile * TS;
+    const unsigned bytes = (unsigned)(imin64(TS, n - base) * len * 4);
+    mbar_expect_tx(&s_full[st], bytes);
+    bulk_g2s(s_tiles + (size_t)st * (kSumTileBytes / 4), raw + (size_t)base * len, bytes, &s_full[st]);
+  };
+  if (tid == 0) {
+    for (int st = 0; st < kSumStages; ++st) {
+      mbar_init(&s_full[st], 1);
+      s_cnt[st] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int st = 0; st < kSumStages; ++st) {
+      const int64_t tile = blockIdx.x + (int64_t)st * gridDim.x;
+      if (tile < ntiles) issue(tile, st);
+    }
+  }
+  for (int i = tid; i < kLutN; i += kSumThreads) s_lut[i] = tab->lut[i];
+  for (int i = tid; i < kMaxCard; i += kSumThreads) s_cd[i] = tab->cuts_d[i];
+  __syncthreads();
+
+  const int seglen = 4 * G;
+  const float inv_seglen = 1.0f / (float)seglen;
+  const int top = card >> 1;
+  int depth = 2;
+  for (int g = G; g > 1; g >>= 1) ++depth;
+  const float err_scale = (float)(depth + 1) * 5.9604645e-08f * inv_seglen * 1.001f;
+
+  for (int64_t it = 0;; ++it) {
+    const int64_t tile = blockIdx.x + it * gridDim.x;
+    if (tile >= ntiles) break;
+    const int st = (int)(it % kSumStages);
+    mbar_wait(&s_full[st], (unsigned)((it / kSumStages) & 1));
+    const int64_t base = tile * TS + warp * SPW;
+    const int cnt = (int)std::max<int64_t>(0, imin64(SPW, n - base));
+    const float4* tl = reinterpret_cast<const float4*>(s_tiles + (size_t)st * (kSumTileBytes / 4)) +
+                       (size_t)warp * SPW * (len / 4);
+    float4 v[SPW][NV];
+#pragma unroll
+    for (int u = 0; u < SPW; ++u)
+#pragma unroll
+      for (int j = 0; j < NV; ++j) v[u][j] = (u < cnt) ? tl[u * (len / 4) + lane + 32 * j] : make_float4(0, 0, 0, 0);
+    __syncwarp();
+    if (lane == 0) {
+      if (atomicAdd(&s_cnt[st], 1u) == kSumWarps - 1) {
+        s_cnt[st] = 0;
+        const int64_t next = tile + (int64_t)kSumStages * gridDim.x;
+        if (next < ntiles) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(next, st);
+        }
+      }
+    }
+    uint32_t packed[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) packed[j] = 0;
+#pragma unroll
+    for (int u = 0; u < SPW; ++u) {
+      float sum[NV], asum[NV];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        const float4 x = v[u][j];
+        sum[j] = (x.x + x.y) + (x.z + x.w);
+        asum[j] = (fabsf(x.x) + fabsf(x.y)) + (fabsf(x.z) + fabsf(x.w));
+      }
+      for (int o = 1; o < G; o <<= 1) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          sum[j] += __shfl_xor_sync(0xffffffffu, sum[j], o);
+          asum[j] += __shfl_xor_sync(0xffffffffu, asum[j], o);
+        }
+      }
+      int sym[NV];
+      bool amb_any = false, amb[NV];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        const float paa = sum[j] * inv_seglen;
+        int k = __float2int_rd((paa + kLutLo) * kLutScale);
+        k = min(max(k, 0), kLutN - 1);
+        const uint2 e = s_lut[k];
+        const float c = __uint_as_float(e.x);
+        sym[j] = (int)e.y + (paa >= c ? 1 : 0);
+        const float err = asum[j] * err_scale;
+        amb[j] = ((lane % G) == (j % G)) && (fabsf(paa - c) <= err + fabsf(c) * 1.2e-7f + 1e-30f);
+        amb_any |= amb[j];
+      }
+      if (__any_sync(0xffffffffu, amb_any)) {
+        // exact path: fp64 sums and fp64 cuts (binary search), as in k_summarize_fast
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          const float4 x = v[u][j];
+          double d = ((double)x.x + (double)x.y) + ((double)x.z + (double)x.w);
+          for (int o = 1; o < G; o <<= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+          if (amb[j]) sym[j] = upper_bound_pow2(s_cd, d / (double)seglen, top);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < NV; ++j) packed[j] |= (uint32_t)sym[j] << (8 * u);
+    }
+    // owner lane of segment (lane + 32 j) / G stores the SPW symbols of its series
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      if ((lane % G) == (j % G) && cnt > 0) {
+        const int seg = (lane + 32 * j) / G;
+        uint8_t* dst = sax + (size_t)seg * n + base;
+        if (cnt == SPW) {
+          if (SPW == 4) *reinterpret_cast<uint32_t*>(dst) = packed[j];
+          else if (SPW == 2) *reinterpret_cast<uint16_t*>(dst) = (uint16_t)packed[j];
+          else *dst = (uint8_t)packed[j];
+        } else {
+          for (int u = 0; u < cnt; ++u) dst[u] = (uint8_t)(packed[j] >> (8 * u));
+        }
+      }
+    }
+  }
+}
+
 // Generic fallback (any len % w == 0): one thread per series, fp64 segment sums
 // (sequential), fp64 binary search.  Correct for every supported shape; used
 // only when the fast path's shape conditions do not hold.
@@ -206,7 +382,29 @@ int summarize_impl(const float* raw, int64_t n, int len, int w, int card, uint8_
   const int G = seglen / 4;
   const bool fast = (len % 128 == 0) && (seglen % 4 == 0) && G >= 1 && G <= 32 && ((G & (G - 1)) == 0);
   const int sms = sm_count();
-  if (fast) {
+  const bool tma = fast && (n % 4 == 0) && (len == 128 || len == 256 || len == 512);
+  if (tma) {
+    const int64_t tiles = (n + (kSumTileBytes / (4 * len)) - 1) / (kSumTileBytes / (4 * len));
+    const int grid = (int)imin64(tiles, (int64_t)sms);
+    cudaError_t e;
+    static int attr_dev[3] = {-1, -1, -1};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int ai = len == 128 ? 0 : len == 256 ? 1 : 2;
+    if (attr_dev[ai] != dev) {
+      e = (len == 128) ? cudaFuncSetAttribute(k_summarize_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSumSmem)
+        : (len == 256) ? cudaFuncSetAttribute(k_summarize_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSumSmem)
+                       : cudaFuncSetAttribute(k_summarize_tma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSumSmem);
+      PARIS_CHECK_LAUNCH(e, "summarize smem attribute");
+      attr_dev[ai] = dev;
+    }
+    switch (len) {
+      case 128: e = PARIS_LAUNCH("summarize", k_summarize_tma<1>, grid, kSumThreads, kSumSmem, st, raw, n, w, card, G, out_sax, tab); break;
+      case 256: e = PARIS_LAUNCH("summarize", k_summarize_tma<2>, grid, kSumThreads, kSumSmem, st, raw, n, w, card, G, out_sax, tab); break;
+      default: e = PARIS_LAUNCH("summarize", k_summarize_tma<4>, grid, kSumThreads, kSumSmem, st, raw, n, w, card, G, out_sax, tab); break;
+    }
+    PARIS_CHECK_LAUNCH(e, "summarize launch");
+  } else if (fast) {
     const int64_t tiles = (n + kTile - 1) / kTile;
     const int grid = (int)imin64(tiles, (int64_t)sms * 8);
     cudaError_t e;

@@ -77,3 +77,24 @@ def test_missing_extension_fails_loudly(tmp_path, monkeypatch):
     monkeypatch.setattr(b, "_lib", None)
     with pytest.raises(b.ParisError):
         b.load()
+
+
+def test_half_directed_rounding(lib):
+    """The fp16 region bounds of the batched LB are rounded outward: check the library's
+    directed fp16 rounding against numpy's binary16 on random, tiny, huge and exact values."""
+    rng = np.random.default_rng(1)
+    vals = np.concatenate([rng.normal(0, 3, 3000), rng.normal(0, 1e-5, 500),
+                           rng.uniform(-7e4, 7e4, 500), [0.0, 1.0, -1.0, 65504.0, -65504.0,
+                                                         2.0 ** -24, 2.0 ** -14, 6.1e-5, 0.1, -0.1]])
+    for v in vals:
+        dn = np.array([lib.debug_half_dir(v, -1)], dtype=np.uint16).view(np.float16)[0]
+        up = np.array([lib.debug_half_dir(v, +1)], dtype=np.uint16).view(np.float16)[0]
+        assert float(dn) <= v <= float(up), (v, dn, up)
+        if np.isfinite(dn) and np.isfinite(up):
+            # adjacent (or equal when v is representable)
+            if float(dn) == v:
+                assert float(up) == v
+            else:
+                assert np.nextafter(dn, np.float16(np.inf)) == up, (v, dn, up)
+    assert np.isinf(np.array([lib.debug_half_dir(1e6, +1)], np.uint16).view(np.float16)[0])
+    assert np.array([lib.debug_half_dir(1e6, -1)], np.uint16).view(np.float16)[0] == np.float16(65504)

@@ -203,3 +203,20 @@ def test_gpu_datagen_matches_numpy(torch_dev):
     qd, src = gpu.noisy_members(xd, 10, 0.05, 2)
     qn = datagen.noisy_members(xd.cpu().numpy(), src, 0.05, 2)
     assert np.max(np.abs(qd.cpu().numpy() - qn)) < 1e-5
+
+
+@pytest.mark.parametrize("n", [2048, 4096 + 16, 3 * 2048 + 1024 + 48, 40_000])
+@pytest.mark.parametrize("nq", [1, 2, 3, 9, 16, 21])
+def test_knn_tiled_path_parity(P, torch_dev, n, nq):
+    """n % 16 == 0, w == 16: the TMA-tiled LB kernels (ragged last tile, every query-slot
+    layout: single, pairs, dummy slots) against the oracle and the direct-load kernels."""
+    import paper_2009_00166_b200 as p
+    x = datagen.random_walks(n, 256, 900 + n)
+    q = datagen.random_walks(nq, 256, 901 + nq)
+    q[0] = x[n // 2]
+    for k in (1, 10):
+        ri, rd2 = oracle.knn_bruteforce(x, q, k)
+        gi, gd = _knn_case(P, torch_dev, x, q, k)
+        check_knn(x, q, gi, gd, ri, rd2)
+        gi2, gd2 = _knn_case(P, torch_dev, x, q, k, config=p.KnnConfig(force_direct=True))
+        check_knn(x, q, gi2, gd2, ri, rd2)
