@@ -93,7 +93,7 @@ int paris_knn_exact(const float* raw, const uint8_t* sax, int64_t n, const float
 typedef struct paris_knn_config {
   int32_t batch;        /* queries per SAX pass (1..16); default 16 */
   int32_t seed_div;     /* seed sample = n / seed_div series (default 16) */
-  int32_t wave_a;       /* reserved (0) */
+  int32_t wave_a;       /* k = 1: candidates per query refined in the first (lowest-LB) wave; default 2048 */
   int32_t reserved[5];  /* reserved[0] = 1: test hook forcing the direct-load LB kernels */
 } paris_knn_config;
 

@@ -49,7 +49,7 @@ class _KProf(ctypes.Structure):
 class KnnConfig:
     batch: int = 0      # queries per SAX pass (1..16), 0 = default (16)
     seed_div: int = 0   # seed sample = n / seed_div (0 = 16)
-    wave_a: int = 0     # reserved
+    wave_a: int = 0     # k = 1: first refinement wave per query (0 = 2048)
     force_direct: bool = False  # test hook: use the direct-load LB kernels even where the TMA-tiled ones apply
 
 

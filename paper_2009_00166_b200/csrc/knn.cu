@@ -47,6 +47,10 @@ constexpr int kU = 4;               // candidates in flight per warp (refine)
 constexpr int kSortP = 4096;        // finalize / seed-select sort buffer
 constexpr int kMaxSeed = 4096;      // seed entries per query
 constexpr uint64_t kNoKey = ~0ull;
+// Per-query words hammered by every warp of a query (BSF key, k-NN threshold) sit
+// 128 B apart, one L2 line each: 16 queries on one line serialized the refine.
+constexpr int kPadU32 = 32;
+constexpr int kPadU64 = 16;
 constexpr uint32_t kHalf2One = 0x3C003C00u;
 constexpr uint32_t kHalfNeg1 = 0xBC00u;
 
@@ -415,9 +419,9 @@ k_seed_select(const uint64_t* __restrict__ seed_keys, int S, int k, float d2up,
   }
   if (threadIdx.x == 0) {
     const float t = (kth == kNoKey) ? INFINITY : __fmul_ru(key_val(kth), d2up);
-    thr[b] = __float_as_uint(t);
+    thr[b * kPadU32] = __float_as_uint(t);
     thr_seed[b] = __float_as_uint(t);
-    if (k == 1) best[b] = kth;
+    if (k == 1) best[b * kPadU64] = kth;
     if (tau_out) tau_out[q0 + b] = (kth == kNoKey) ? INFINITY : sqrtf(key_val(kth));
   }
 }
@@ -571,7 +575,8 @@ struct WarpBuf {
   int n;
 };
 
-__device__ void wb_flush(WarpBuf& wb, int nslots, const LbConsts& c, const LbArgs& a) {
+// s_hist: the CTA's shared-memory LB histogram [kMaxB][kNB] (flushed at kernel end)
+__device__ void wb_flush(WarpBuf& wb, int nslots, const LbConsts& c, const LbArgs& a, unsigned* s_hist) {
   const int lane = threadIdx.x & 31;
   __syncwarp();
   const int m = wb.n;
@@ -587,7 +592,7 @@ __device__ void wb_flush(WarpBuf& wb, int nslots, const LbConsts& c, const LbArg
     const uint64_t key = wb.key[e];
     const unsigned pos = atomicAdd(&wb.cur[b], 1u);
     if ((int64_t)pos < a.cap) a.cand[(size_t)b * a.cap + pos] = key;
-    atomicAdd(&a.hist[b * kNB + lb_bin(key_val(key), c.scale[b])], 1u);
+    atomicAdd(&s_hist[b * kNB + lb_bin(key_val(key), c.scale[b])], 1u);
   }
   __syncwarp();
   if (lane == 0) wb.n = 0;
@@ -596,7 +601,7 @@ __device__ void wb_flush(WarpBuf& wb, int nslots, const LbConsts& c, const LbArg
 
 template <int P>
 __device__ __forceinline__ void lb_emit_wb(const uint32_t (&acc)[4][P], int64_t i0, int nvalid, int nslots,
-                                           const LbConsts& c, const LbArgs& a, WarpBuf& wb) {
+                                           const LbConsts& c, const LbArgs& a, WarpBuf& wb, unsigned* s_hist) {
   const int lane = threadIdx.x & 31;
   uint32_t qm = 0;
   if (nvalid > 0) {
@@ -631,7 +636,7 @@ __device__ __forceinline__ void lb_emit_wb(const uint32_t (&acc)[4][P], int64_t 
   }
   const int total = __shfl_sync(0xffffffffu, incl, 31);
   if (total == 0) return;
-  if (wb.n + total > kWB) wb_flush(wb, nslots, c, a);
+  if (wb.n + total > kWB) wb_flush(wb, nslots, c, a, s_hist);
   if (total > kWB) {  // degenerate (e.g. tau = inf): straight to global memory
     lb_emit<P>(acc, i0, nvalid, c, a);
     return;
@@ -776,6 +781,7 @@ k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
   __shared__ uint2 s_q16[PP * kTW];
   __shared__ LbConsts s_c;
   __shared__ WarpBuf s_wb[MODE == 1 ? kTWarps : 1];
+  __shared__ unsigned s_hist[MODE == 1 ? kMaxB * kNB : 1];
   const int tid = threadIdx.x, lane = tid & 31;
   const int64_t ntiles = (nlim + kTS - 1) / kTS;
   const int nslots = P > 0 ? 2 * P : 1;
@@ -783,6 +789,7 @@ k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
   if (MODE == 1) {
     if (lane < kMaxB) wb.cnt[lane] = 0;
     if (lane == 0) wb.n = 0;
+    for (int i = tid; i < nslots * kNB; i += kTThreads) s_hist[i] = 0;
   }
 
   auto issue = [&](int64_t tile, int st) {
@@ -869,7 +876,7 @@ k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
       }
     }
     if (MODE == 1) {
-      lb_emit_wb<PP>(acc, i0, nvalid, nslots, s_c, a, wb);
+      lb_emit_wb<PP>(acc, i0, nvalid, nslots, s_c, a, wb, s_hist);
     } else {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -883,7 +890,12 @@ k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
       }
     }
   }
-  if (MODE == 1) wb_flush(wb, nslots, s_c, a);
+  if (MODE == 1) {
+    wb_flush(wb, nslots, s_c, a, s_hist);
+    __syncthreads();
+    for (int i = tid; i < nslots * kNB; i += kTThreads)
+      if (s_hist[i]) atomicAdd(&a.hist[i], s_hist[i]);
+  }
   if (MODE == 0) {
     const int gwarp = (blockIdx.x * kTThreads + tid) >> 5;
 #pragma unroll
@@ -918,10 +930,16 @@ __global__ void __launch_bounds__(256)
 k_scatter(const uint64_t* __restrict__ cand, const unsigned* __restrict__ count,
           const unsigned* __restrict__ hist, const unsigned* __restrict__ thr,
           unsigned* __restrict__ cursor, uint64_t* __restrict__ sorted, int64_t cap) {
+  // Each CTA owns a contiguous chunk of the query's candidates: it counts its
+  // chunk per bin in shared memory, reserves each bin's range with one global
+  // atomic, then scatters with shared-memory cursors (no per-candidate global
+  // atomics on the hot bins near tau).
   __shared__ unsigned s_off[kNB];
+  __shared__ unsigned s_cnt[kNB];
   const int b = blockIdx.y;
   unsigned v = hist[b * kNB + threadIdx.x];
   s_off[threadIdx.x] = v;
+  s_cnt[threadIdx.x] = 0;
   __syncthreads();
   for (int o = 1; o < kNB; o <<= 1) {
     const unsigned t = (threadIdx.x >= o) ? s_off[threadIdx.x - o] : 0u;
@@ -932,14 +950,23 @@ k_scatter(const uint64_t* __restrict__ cand, const unsigned* __restrict__ count,
   const unsigned excl = s_off[threadIdx.x] - v;
   __syncthreads();
   s_off[threadIdx.x] = excl;
-  __syncthreads();
   const float sc = bin_scale(__uint_as_float(thr[b]));
   const int64_t cnt = imin64((int64_t)count[b], cap);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t key = cand[(size_t)b * cap + i];
+  const int64_t per = (cnt + gridDim.x - 1) / gridDim.x;
+  const int64_t c0 = imin64(cnt, (int64_t)blockIdx.x * per), c1 = imin64(cnt, c0 + per);
+  const uint64_t* src = cand + (size_t)b * cap;
+  for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) atomicAdd(&s_cnt[lb_bin(key_val(src[i]), sc)], 1u);
+  __syncthreads();
+  {
+    const unsigned k = s_cnt[threadIdx.x];
+    s_off[threadIdx.x] += k ? atomicAdd(&cursor[b * kNB + threadIdx.x], k) : 0u;
+    s_cnt[threadIdx.x] = 0;
+  }
+  __syncthreads();
+  for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+    const uint64_t key = src[i];
     const int bin = lb_bin(key_val(key), sc);
-    const uint64_t pos = (uint64_t)s_off[bin] + atomicAdd(&cursor[b * kNB + bin], 1u);
+    const uint64_t pos = (uint64_t)s_off[bin] + atomicAdd(&s_cnt[bin], 1u);
     if (pos < (uint64_t)cap) sorted[(size_t)b * cap + pos] = key;
   }
 }
@@ -963,6 +990,7 @@ struct RefineArgs {
   uint64_t* lists;           // k > 1: [nb][gridDim.x][k]
   int k;
   float d2up;                // 1 + bound on the relative error of an fp32 d^2 (rounding up)
+  unsigned lo, hi;           // k = 1: refine list positions [lo, min(hi, count)) (a wave)
 };
 
 // One warp step: up to kU candidates (indices i0 + u*stride) against the live
@@ -1031,209 +1059,108 @@ __device__ __forceinline__ bool refine_step(const RefineArgs& a, const uint64_t*
   return stop;
 }
 
-__global__ void __launch_bounds__(kRefThreads)
-k_refine1(RefineArgs a) {
-  extern __shared__ float4 s_qv[];
-  __shared__ unsigned s_refined;
-  const int b = blockIdx.y;
+// k = 1 (P:1357-1378 with BSF = the best (d^2, id) key): a warp takes U
+// candidates at a time from its interleaved share of the query's LB-ordered list;
+// the live BSF is read (relaxed) in parallel with the keys; surviving rows are
+// loaded whole (lane l: float4 #(l + 32c)), the distance is accumulated chunk by
+// chunk with early abandoning (north_star) after each 128 points, and
+// the BSF is lowered with one 64-bit atomicMin.  Few registers -> 64 warps per SM:
+// the occupancy, not TMA, is what keeps random 1 KB gathers at HBM speed
+// (profiles/r01/micro_gather_1KB_rows.txt: LDG 6.8-7.0 TB/s vs 2.2 TB/s for
+// 1 KB cp.async.bulk copies issued by one warp per SM).
+template <int NC, int U>  // NC = float4 chunks of 32 per lane (len <= 128*NC)
+__global__ void __launch_bounds__(kRefThreads, NC <= 2 ? 8 : 2)
+k_refine1(RefineArgs a, int nb) {
+  // every warp walks its interleaved share of EVERY query's list (balanced work:
+  // a query with 5x the mean candidate count no longer leaves most SMs idle); the
+  // query rows are read through L1 (all warps of a CTA share them)
+  __shared__ unsigned s_refined[kMaxB];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const float4* qsrc = reinterpret_cast<const float4*>(a.queries + (size_t)b * a.len);
-  for (int i = threadIdx.x; i < (a.len >> 2); i += blockDim.x) s_qv[i] = qsrc[i];
-  if (threadIdx.x == 0) s_refined = 0;
+  const int nf = a.len >> 2;
+  if (threadIdx.x < kMaxB) s_refined[threadIdx.x] = 0;
   __syncthreads();
-  const unsigned cnt = (unsigned)imin64((int64_t)a.count[b], a.cap);
-  const float scale = bin_scale(__uint_as_float(a.thr_seed[b]));
-  const uint64_t* list = a.sorted + (size_t)b * a.cap;
-  unsigned long long* bp = a.best + b;
   const unsigned gw = blockIdx.x * kRefWarps + warp, GW = gridDim.x * kRefWarps;
-  unsigned nref = 0;
-  for (unsigned i0 = gw; i0 < cnt; i0 += kU * GW) {
-    const uint64_t cur = ld_relaxed_u64(bp);
-    const float thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
-    uint64_t key[kU];
-    float d2[kU];
-    const bool stop = refine_step(a, list, cnt, i0, GW, thr, scale, s_qv, key, d2, nref);
-    uint64_t mk = kNoKey;
+  for (int b = 0; b < nb; ++b) {
+    const unsigned cnt = (unsigned)imin64(imin64((int64_t)a.count[b], a.cap), (int64_t)a.hi);
+    const float scale = bin_scale(__uint_as_float(a.thr_seed[b]));
+    const uint64_t* list = a.sorted + (size_t)b * a.cap + a.lo;
+    const float4* qv = reinterpret_cast<const float4*>(a.queries + (size_t)b * a.len);
+    unsigned long long* bp = a.best + (size_t)b * kPadU64;
+    unsigned nref = 0;
+    uint64_t cur = kNoKey;  // this warp's view of the BSF: refreshed every 4 steps, lowered by its own finds
+    unsigned step = 0;
+    for (unsigned i0 = gw; a.lo + i0 < cnt; i0 += U * GW, ++step) {
+      uint64_t key[U];
 #pragma unroll
-    for (int u = 0; u < kU; ++u)
-      if (d2[u] < INFINITY) mk = min(mk, make_key(d2[u], key_id(key[u])));
-    if (lane == 0 && mk < cur) atomicMin(bp, (unsigned long long)mk);
-    if (stop) break;
-  }
-  if (lane == 0 && nref) atomicAdd(&s_refined, nref);
-  __syncthreads();
-  if (threadIdx.x == 0 && s_refined) atomicAdd(&a.refined[b], s_refined);
-}
-
-// k = 1, warp-specialized TMA gather (the B200 form of the paper's RDC workers
-// with oversubscription): one persistent CTA per SM; its producer
-// warp walks the CTA's share of every query's LB-ordered candidate list (32 keys
-// per load), re-checks LB against the live BSF and issues one
-// cp.async.bulk per surviving candidate (the whole raw row) into a ring of
-// shared-memory slots; consumer warps take slots in sequence order, compute d^2
-// from shared memory with early abandoning and lower the BSF with a 64-bit
-// atomicMin.  Up to ~128 KB of gathers are in flight per SM.
-constexpr int kR1Threads = 384;
-constexpr int kR1Consumers = kR1Threads / 32 - 1;
-constexpr int kR1RingBytes = 131072;
-constexpr int kR1MaxSlots = 256;
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-struct Refine1Args {
-  const float* raw;
-  int len;
-  const float* queries;      // [nb][len]
-  const uint64_t* sorted;    // [nb][cap]
-  int64_t cap;
-  int nb;
-  const unsigned* count;
-  const unsigned* thr_seed;
-  unsigned long long* best;  // [nb]
-  unsigned* refined;         // [nb]
-  float d2up;
-  int slots;                 // ring slots (<= kR1MaxSlots)
-};
-
-__global__ void __launch_bounds__(kR1Threads, 1)
-k_refine1t(Refine1Args a) {
-  extern __shared__ __align__(128) uint8_t dsm[];
-  const int len = a.len, nf = len >> 2, S = a.slots;
-  float4* s_ring = reinterpret_cast<float4*>(dsm);                       // S * nf
-  float4* s_qv = s_ring + (size_t)S * nf;                                 // nb * nf
-  __shared__ __align__(8) uint64_t s_full[kR1MaxSlots];
-  __shared__ __align__(8) uint64_t s_empty[kR1MaxSlots];
-  __shared__ uint64_t s_key[kR1MaxSlots];   // candidate key (kNoKey = end sentinel)
-  __shared__ int s_qid[kR1MaxSlots];
-  __shared__ unsigned s_ref[kMaxB];
-  __shared__ unsigned long long s_best[kMaxB];  // CTA view of the BSF (<= what it has seen)
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < a.nb * nf; i += kR1Threads)
-    s_qv[i] = reinterpret_cast<const float4*>(a.queries)[i];
-  if (tid < kMaxB) {
-    s_ref[tid] = 0;
-    s_best[tid] = (tid < a.nb) ? a.best[tid] : kNoKey;
-  }
-  if (tid == 0) {
-    for (int i = 0; i < S; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  if (warp == 0) {
-    // ---------------- producer
-    uint32_t q = 0;  // sequence number of the next slot
-    const unsigned row_bytes = (unsigned)len * 4u;
-    for (int b = 0; b < a.nb; ++b) {
-      const unsigned cnt = (unsigned)imin64((int64_t)a.count[b], a.cap);
-      const float scale = bin_scale(__uint_as_float(a.thr_seed[b]));
-      const uint64_t* list = a.sorted + (size_t)b * a.cap;
-      constexpr int KU = 8;  // 8 x 32 keys loaded per producer step (latency amortized)
-      bool done = false;
-      for (unsigned t0 = blockIdx.x; t0 < cnt && !done; t0 += 32u * KU * gridDim.x) {
-        uint64_t keys[KU];
-#pragma unroll
-        for (int r = 0; r < KU; ++r) {
-          const unsigned i = t0 + (unsigned)(r * 32 + lane) * gridDim.x;
-          keys[r] = (i < cnt) ? list[i] : kNoKey;
-        }
-        uint64_t cur = ld_relaxed_u64(a.best + b);
-        const uint64_t mine = *(volatile unsigned long long*)&s_best[b];
-        if (cur < mine) { if (lane == 0) atomicMin(&s_best[b], (unsigned long long)cur); }
-        else cur = mine;
-        const float thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
-#pragma unroll
-        for (int r = 0; r < KU; ++r) {
-          const unsigned i = t0 + (unsigned)(r * 32 + lane) * gridDim.x;
-          const uint64_t key = keys[r];
-          const float lb = key_val(key);
-          const bool live = (i < cnt) && lb <= thr;
-          // bin order: a candidate whose bin lies wholly above thr ends the list
-          bool past = (i >= cnt);
-          if (!past && !live) {
-            const int bin = lb_bin(lb, scale);
-            past = bin >= 1 && (float)(bin - 1) > thr * scale;
-          }
-          const unsigned pastm = __ballot_sync(0xffffffffu, past);
-          const int first_past = pastm ? __ffs(pastm) - 1 : 32;
-          const unsigned livem = __ballot_sync(0xffffffffu, live && lane < first_past);
-          if (live && lane < first_past) {
-            const uint32_t my = q + (uint32_t)__popc(livem & ((1u << lane) - 1u));
-            const int slot = (int)(my % (uint32_t)S);
-            if (my >= (uint32_t)S) mbar_wait(&s_empty[slot], ((my / S) - 1) & 1);
-            s_key[slot] = key;
-            s_qid[slot] = b;
-            mbar_expect_tx(&s_full[slot], row_bytes);
-            bulk_g2s(s_ring + (size_t)slot * nf, a.raw + (size_t)key_id(key) * len, row_bytes, &s_full[slot]);
-          }
-          q += (uint32_t)__popc(livem);
-          if (pastm) { done = true; break; }
-        }
+      for (int u = 0; u < U; ++u) {
+        const unsigned i = i0 + u * GW;
+        key[u] = (a.lo + i < cnt) ? __ldg(list + i) : kNoKey;
       }
-    }
-    // end sentinels: one per consumer warp
-    if (lane < kR1Consumers) {
-      const uint32_t my = q + (uint32_t)lane;
-      const int slot = (int)(my % (uint32_t)S);
-      if (my >= (uint32_t)S) mbar_wait(&s_empty[slot], ((my / S) - 1) & 1);
-      s_key[slot] = kNoKey;
-      s_qid[slot] = -1;
-      mbar_arrive(&s_full[slot]);
-    }
-  } else {
-    // ---------------- consumers: sequence numbers c, c + C, c + 2C, ...
-    const int c = warp - 1;
-    for (uint32_t my = (uint32_t)c;; my += kR1Consumers) {
-      const int slot = (int)(my % (uint32_t)S);
-      mbar_wait(&s_full[slot], (my / S) & 1);
-      const uint64_t key = s_key[slot];
-      const int b = s_qid[slot];
-      if (b < 0) break;
-      const float4* row = s_ring + (size_t)slot * nf;
-      const float4* qv = s_qv + (size_t)b * nf;
-      const uint64_t cur = *(volatile unsigned long long*)&s_best[b];
+      if ((step & 3) == 0) cur = min(cur, ld_relaxed_u64(bp));
       const float thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
-      float acc = 0.f;
-      bool abandoned = false;
-      if (key_val(key) <= thr) {
-        for (int c0 = 0; c0 < nf; c0 += 32) {
-          const int f = c0 + lane;
-          if (f < nf) {
-            const float4 x = row[f], y = qv[f];
-            float d;
-            d = x.x - y.x; acc = fmaf(d, d, acc);
-            d = x.y - y.y; acc = fmaf(d, d, acc);
-            d = x.z - y.z; acc = fmaf(d, d, acc);
-            d = x.w - y.w; acc = fmaf(d, d, acc);
-          }
-          // early abandoning (north_star) after each 128-point chunk
-          if (c0 + 32 < nf && warp_sum(acc) > thr) { abandoned = true; break; }
-        }
-      } else {
-        abandoned = true;  // the BSF dropped below its LB while in flight
-      }
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&s_empty[slot]);
-        atomicAdd(&s_ref[b], 1u);
-      }
-      if (!abandoned) {
-        const float d2 = warp_sum(acc);
-        const uint64_t k2 = make_key(d2, key_id(key));
-        if (lane == 0 && k2 < cur) {
-          atomicMin(&s_best[b], (unsigned long long)k2);
-          atomicMin(a.best + b, (unsigned long long)k2);
+      bool live[U], stop = false;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float lb = key_val(key[u]);
+        live[u] = !stop && (a.lo + i0 + u * GW < cnt) && lb <= thr;
+        if (!live[u] && !stop) {
+          // bin order: past the end, or a bin wholly above thr, ends this warp's share
+          const int bin = lb_bin(lb, scale);
+          stop = (a.lo + i0 + u * GW >= cnt) || (bin >= 1 && (float)(bin - 1) > thr * scale);
         }
       }
+      float4 x[U][NC];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const int f = lane + 32 * c;
+          x[u][c] = (live[u] && f < nf)
+                        ? ld_stream(reinterpret_cast<const float4*>(a.raw + (size_t)key_id(key[u]) * a.len) + f)
+                        : make_float4(0, 0, 0, 0);
+        }
+      float acc[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc[u] = 0.f;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const float4 q = (lane + 32 * c < nf) ? __ldg(qv + lane + 32 * c) : make_float4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          float d;
+          d = x[u][c].x - q.x; acc[u] = fmaf(d, d, acc[u]);
+          d = x[u][c].y - q.y; acc[u] = fmaf(d, d, acc[u]);
+          d = x[u][c].z - q.z; acc[u] = fmaf(d, d, acc[u]);
+          d = x[u][c].w - q.w; acc[u] = fmaf(d, d, acc[u]);
+        }
+        if (c + 1 < NC && 32 * (c + 1) < nf) {
+          // early abandoning after each 128-point chunk (the rest is not accumulated)
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (live[u] && warp_sum(acc[u]) > thr) { live[u] = false; ++nref; }
+          bool any = false;
+#pragma unroll
+          for (int u = 0; u < U; ++u) any |= live[u];
+          if (!any) break;
+        }
+      }
+      uint64_t mk = kNoKey;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (!live[u]) continue;
+        ++nref;
+        mk = min(mk, make_key(warp_sum(acc[u]), key_id(key[u])));
+      }
+      if (mk < cur) {
+        if (lane == 0) atomicMin(bp, (unsigned long long)mk);
+        cur = mk;
+      }
+      if (stop) break;
     }
+    if (lane == 0 && nref) atomicAdd(&s_refined[b], nref);
   }
   __syncthreads();
-  if (tid < a.nb && s_ref[tid]) atomicAdd(&a.refined[tid], s_ref[tid]);
+  if (threadIdx.x < nb && s_refined[threadIdx.x]) atomicAdd(&a.refined[threadIdx.x], s_refined[threadIdx.x]);
 }
 
 // k > 1: rounds of (every warp: one refine_step) -> merge the round's admitted
@@ -1272,7 +1199,7 @@ k_refine_topk(RefineArgs a) {
   bool done = false;
   for (unsigned i0 = gw;; i0 += kU * GW) {
     if (!done && i0 < cnt) {
-      const float thr = fminf(__uint_as_float(ld_relaxed_u32(&a.thr[b])), s_thr_local);
+      const float thr = fminf(__uint_as_float(ld_relaxed_u32(&a.thr[b * kPadU32])), s_thr_local);
       uint64_t key[kU];
       float d2[kU];
       done = refine_step(a, list, cnt, i0, GW, thr, scale, s_qv, key, d2, nref);
@@ -1320,7 +1247,7 @@ k_refine_topk(RefineArgs a) {
         if (kk != kNoKey) {
           const float up = __fmul_ru(key_val(kk), a.d2up);
           s_thr_local = up;
-          atomicMin(&a.thr[b], __float_as_uint(up));
+          atomicMin(&a.thr[b * kPadU32], __float_as_uint(up));
         }
       }
     }
@@ -1340,7 +1267,7 @@ __global__ void k_finalize1(const unsigned long long* __restrict__ best, int nb,
                             unsigned* __restrict__ all_count, unsigned* __restrict__ all_refined) {
   const int b = threadIdx.x;
   if (b >= nb) return;
-  const uint64_t key = best[b];
+  const uint64_t key = best[b * kPadU64];
   if (key == kNoKey) { out_idx[q0 + b] = -1; out_dist[q0 + b] = INFINITY; }
   else { out_idx[q0 + b] = (int64_t)key_id(key); out_dist[q0 + b] = sqrtf(key_val(key)); }
   all_count[q0 + b] = count[b];
@@ -1404,7 +1331,7 @@ struct Ws {
   uint2* g_q16;
   int* seed_ids;
   uint64_t* seed_keys;
-  unsigned* zero_block;  // thr | thr_seed | count | hist | cursor | refined (zeroed per batch)
+  unsigned* zero_block;  // thr_seed | count | hist | cursor | refined (zeroed per batch)
   unsigned* thr;
   unsigned* thr_seed;
   unsigned* count;
@@ -1428,6 +1355,7 @@ struct Plan {
   int64_t ns;     // seed sample
   int64_t cap;
   int XB;         // refine CTAs per query
+  int wave_a;     // k = 1: candidates per query refined in the first wave
   float d2up;     // fp32 d^2 -> rigorous upper bound factor
   bool tiled;     // TMA-tiled LB kernels (n % 16 == 0, w == 16)
 };
@@ -1524,6 +1452,15 @@ cudaError_t launch_qprep(int nb, const Plan& p, const float* qb, const Ws& ws, c
   }
 }
 
+template <int NC, int U>
+cudaError_t launch_refine1(const RefineArgs& ra, int nb, int64_t max_work, cudaStream_t st) {
+  // grid: one full wave of resident CTAs, or fewer when the wave holds less work
+  const int full = sms() * (NC <= 2 ? 8 : 2);
+  const int64_t need = (max_work + (int64_t)kRefWarps * U - 1) / ((int64_t)kRefWarps * U);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(full, need));
+  return PARIS_LAUNCH("refine", (k_refine1<NC, U>), grid, kRefThreads, 0, st, ra, nb);
+}
+
 // Allocate the batch scratch for `cap` candidates per query.
 int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   const int B = 2 * pairs_for(p.B);
@@ -1533,9 +1470,10 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   const size_t o_q16 = take(sizeof(uint2) * (B / 2) * kMaxW);
   const size_t o_sid = take(sizeof(int) * B * p.S);
   const size_t o_skey = take(sizeof(uint64_t) * B * p.S);
-  const size_t zb = sizeof(unsigned) * (B + B + B + B * kNB + B * kNB + B);
+  const size_t zb = sizeof(unsigned) * (B + B + B * kNB + B * kNB + B);
   const size_t o_zero = take(zb);
-  const size_t o_best = take(sizeof(unsigned long long) * B);
+  const size_t o_best = take(sizeof(unsigned long long) * B * kPadU64);
+  const size_t o_thr = take(sizeof(unsigned) * B * kPadU32);
   const size_t o_cand = take(sizeof(uint64_t) * B * (size_t)cap);
   const size_t o_sorted = take(sizeof(uint64_t) * B * (size_t)cap);
   const size_t o_lists = take(p.k > 1 ? sizeof(uint64_t) * B * (size_t)p.XB * p.k : 8);
@@ -1554,8 +1492,8 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   ws.seed_keys = (uint64_t*)(c + o_skey);
   ws.zero_block = (unsigned*)(c + o_zero);
   ws.zero_bytes = zb;
-  ws.thr = ws.zero_block;
-  ws.thr_seed = ws.thr + B;
+  ws.thr = (unsigned*)(c + o_thr);
+  ws.thr_seed = ws.zero_block;
   ws.count = ws.thr_seed + B;
   ws.hist = ws.count + B;
   ws.cursor = ws.hist + B * kNB;
@@ -1606,29 +1544,27 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
   ra.raw = raw; ra.len = p.len; ra.queries = qbatch; ra.sorted = ws.sorted; ra.cap = cap;
   ra.count = ws.count; ra.thr_seed = ws.thr_seed; ra.thr = ws.thr; ra.best = ws.best;
   ra.refined = ws.refined; ra.lists = ws.lists; ra.k = p.k; ra.d2up = p.d2up;
+  ra.lo = 0; ra.hi = 0xFFFFFFFFu;
   dim3 g((unsigned)p.XB, (unsigned)nb);
   if (p.k == 1) {
-    Refine1Args r1;
-    r1.raw = raw; r1.len = p.len; r1.queries = qbatch; r1.sorted = ws.sorted; r1.cap = cap; r1.nb = nb;
-    r1.count = ws.count; r1.thr_seed = ws.thr_seed; r1.best = ws.best; r1.refined = ws.refined;
-    r1.d2up = p.d2up;
-    r1.slots = std::min(kR1MaxSlots, std::max(kR1Consumers + 1, kR1RingBytes / (p.len * 4)));
-    const size_t smem = (size_t)r1.slots * p.len * 4 + (size_t)nb * p.len * 4;
-    if (smem > 200 * 1024) {  // very long series: the register-staged kernel
-      PARIS_CHECK_LAUNCH(PARIS_LAUNCH("refine", k_refine1, g, kRefThreads, (size_t)p.len * 4, st, ra),
-                         "refine launch");
-    } else {
-    static int attr_dev = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (attr_dev != dev) {
-      PARIS_CHECK_LAUNCH(cudaFuncSetAttribute(k_refine1t, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              227 * 1024 - 12 * 1024),
-                         "refine smem attribute");
-      attr_dev = dev;
+    cudaError_t e1 = cudaSuccess;
+    const int NC = p.len <= 128 ? 1 : p.len <= 256 ? 2 : p.len <= 512 ? 4 : p.len <= 1024 ? 8 : 32;
+    // wave A: the lowest-LB wave_a candidates of every query (finds the NN early, so
+    // wave B -- the rest, in LB order -- prunes against a tight BSF)
+    for (int wv = 0; wv < 2 && e1 == cudaSuccess; ++wv) {
+      RefineArgs rb = ra;
+      rb.lo = wv == 0 ? 0u : (unsigned)p.wave_a;
+      rb.hi = wv == 0 ? (unsigned)p.wave_a : 0xFFFFFFFFu;
+      const int64_t work = wv == 0 ? (int64_t)p.wave_a : cap;  // per query, upper bound
+      switch (NC) {
+        case 1: e1 = launch_refine1<1, 2>(rb, nb, work, st); break;
+        case 2: e1 = launch_refine1<2, 1>(rb, nb, work, st); break;
+        case 4: e1 = launch_refine1<4, 1>(rb, nb, work, st); break;
+        case 8: e1 = launch_refine1<8, 1>(rb, nb, work, st); break;
+        default: e1 = launch_refine1<32, 1>(rb, nb, work, st); break;
+      }
     }
-    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("refine", k_refine1t, sms(), kR1Threads, smem, st, r1), "refine launch");
-    }
+    PARIS_CHECK_LAUNCH(e1, "refine launch");
     PARIS_CHECK_LAUNCH(PARIS_LAUNCH("finalize", k_finalize1, 1, 32, 0, st, ws.best, nb, q0, d_idx, d_dist,
                                     ws.count, ws.refined, all_count, all_refined),
                        "finalize launch");
@@ -1700,6 +1636,7 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   plan_seed(p, (cfg && cfg->seed_div > 0) ? cfg->seed_div : 16);
   p.cap = std::min<int64_t>(n, std::max<int64_t>(65536, n / 32));
   plan_refine(p);
+  p.wave_a = (cfg && cfg->wave_a > 0) ? cfg->wave_a : 2048;
   // |fp32 d^2 - exact| <= e d^2 with e = (len/32 + 8) u (warp_ed2 / refine_step);
   // d2up >= (1+e)/(1-e) with margin, u = 2^-24
   p.d2up = (float)(1.0 + 2.5 * (len / 32 + 8) * 5.9604644775390625e-08);

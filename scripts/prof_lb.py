@@ -16,3 +16,7 @@ i1, d1 = P.knn_exact(raw, sax, q[:1], k=1, config=P.KnnConfig(batch=1))
 torch.cuda.synchronize()
 assert int(i16[0, 0]) == int(i1[0, 0])
 print("ok", i16[:4, 0].tolist())
+if os.environ.get("PROF_K10"):
+    i10, d10 = P.knn_exact(raw, sax, q, k=10, config=P.KnnConfig(batch=16))
+    torch.cuda.synchronize()
+    print("k10 ok", i10[0, :3].tolist())
