@@ -95,6 +95,29 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def rank_seeds(config: int, rank: int):
+    """(dataset seed, query seed) of a rank: weak scaling -- every rank owns a distinct
+    collection and query set of the config's size (queries are independent problems)."""
+    import datagen
+    ds, qs = datagen.config_seeds(config)
+    return ds + 7919 * rank, qs + 7919 * rank
+
+
+def reduce_max_ms(ms: float, device, world_size: int) -> float:
+    """Max over ranks of a device-timed duration (the slowest rank defines the step)."""
+    import torch
+    t = torch.tensor([float(ms)], dtype=torch.float64, device=device)
+    if world_size > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def weak_throughput(nq_per_rank: int, world_size: int, max_ms: float) -> float:
+    """Whole-job queries/s: every rank answered nq_per_rank queries within max_ms."""
+    return nq_per_rank * world_size / (max_ms / 1e3)
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -191,9 +214,7 @@ def run_gpu(args):
         nq = args.nq
     batch = args.batch or 16
     call_q = cfg.get("call", nq)  # queries per paris_knn_exact call (C3: batches of 64)
-    ds, qs = datagen.config_seeds(args.config)
-    ds += 7919 * rank  # weak scaling: every rank owns a distinct collection
-    qs += 7919 * rank
+    ds, qs = rank_seeds(args.config, rank)
 
     t0 = time.time()
     raw = dg.walks(n, length, ds, device=dev)
@@ -236,9 +257,7 @@ def run_gpu(args):
         step(queries, out_idx, out_dist)
     torch.cuda.synchronize()
 
-    # ---- timed region (device events, max over ranks); per-kernel events via libparis profiling
-    P.profile_reset()
-    P.profile_enable(True)
+    # ---- timed region (device events, max over ranks)
     launches0 = P.launch_count()
     if ws > 1:
         dist.barrier()
@@ -252,14 +271,19 @@ def run_gpu(args):
     if ws > 1:
         dist.barrier()
     launches = P.launch_count() - launches0
+    step_ms = e0.elapsed_time(e1) / args.steps
+    # ---- the same K steps again with libparis' per-launch CUDA events (on the launching
+    # stream): per-kernel durations for the roofline and the time split (kept out of the
+    # headline timing because the event records add launch overhead on the small configs)
+    P.profile_reset()
+    P.profile_enable(True)
+    for _ in range(args.steps):
+        step(queries, out_idx, out_dist)
+    torch.cuda.synchronize()
     P.profile_enable(False)
     prof = P.profile_read()
-    step_ms = e0.elapsed_time(e1) / args.steps
-    t_max = torch.tensor([step_ms], device=dev)
-    if ws > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    step_ms_max = float(t_max.item())
-    value = nq * ws / (step_ms_max / 1e3)
+    step_ms_max = reduce_max_ms(step_ms, dev, ws)
+    value = weak_throughput(nq, ws, step_ms_max)
 
     # ---- e2e through the same ABI call with HOST (pinned) buffers
     hq = queries.cpu().pin_memory()
@@ -273,10 +297,7 @@ def run_gpu(args):
     e1.record(st)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / args.steps
-    t_e2e = torch.tensor([e2e_ms], device=dev)
-    if ws > 1:
-        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
-    e2e_value = nq * ws / (float(t_e2e.item()) / 1e3)
+    e2e_value = weak_throughput(nq, ws, reduce_max_ms(e2e_ms, dev, ws))
     assert torch.equal(hidx, out_idx.cpu()), "host-buffer path disagrees with device path"
 
     # ---- roofline of the dominant kernel (algorithmic bytes / event-timed duration)
@@ -384,7 +405,9 @@ def run_gpu(args):
             "clocks": clocks.summary(),
             "summarize": summarize,
             "kernels": kern,
-            "pruning": {"candidates_mean": float(cand.mean()), "refined_mean": float(refined.mean()),
+            "pruning": {"candidates_mean": float(cand.mean()), "candidates_p50": float(np.median(cand)),
+                        "candidates_max": float(cand.max()), "refined_mean": float(refined.mean()),
+                        "refined_max": float(refined.max()),
                         "pruning_ratio": float(1.0 - refined.mean() / n),
                         "tau_seed_mean": float(stats["tau_seed"].mean())},
         }

@@ -426,6 +426,24 @@ k_seed_select(const uint64_t* __restrict__ seed_keys, int S, int k, float d2up,
   }
 }
 
+// Re-scan seed (candidate-buffer overflow): the first pass already refined the
+// `cap` candidates it kept, so its result row is a real (and much tighter) BSF:
+// tau^2 = (k-th returned distance)^2 rounded up (the fp32 sqrt/square round trip
+// is covered by a further 2^-20), the k = 1 BSF key restarts from that row.
+__global__ void k_seed_prev(const int64_t* __restrict__ prev_idx, const float* __restrict__ prev_dist, int nb,
+                            int q0, int k, float d2up, unsigned* __restrict__ thr, unsigned* __restrict__ thr_seed,
+                            unsigned long long* __restrict__ best) {
+  const int b = threadIdx.x;
+  if (b >= nb) return;
+  const float d = prev_dist[(size_t)(q0 + b) * k + (k - 1)];
+  const int64_t id = prev_idx[(size_t)(q0 + b) * k + (k - 1)];
+  const bool ok = (id >= 0) && d < INFINITY;
+  const float t = ok ? __fmul_ru(__fmul_ru(__fmul_ru(d, d), 1.00000096f), d2up) : INFINITY;
+  thr[b * kPadU32] = __float_as_uint(t);
+  thr_seed[b] = __float_as_uint(t);
+  if (k == 1) best[b * kPadU64] = ok ? make_key(__fmul_ru(__fmul_ru(d, d), 1.00000096f), (uint32_t)id) : kNoKey;
+}
+
 // ---------------------------------------------------------------- K4 LBC pass
 // Alg10: for every word, LB < BSF -> append (LB, position).
 // Here: up to 2P queries per SAX read, in packed fp16; warp-aggregated atomics
@@ -1264,14 +1282,14 @@ k_refine_topk(RefineArgs a) {
 __global__ void k_finalize1(const unsigned long long* __restrict__ best, int nb, int q0,
                             int64_t* __restrict__ out_idx, float* __restrict__ out_dist,
                             const unsigned* __restrict__ count, const unsigned* __restrict__ refined,
-                            unsigned* __restrict__ all_count, unsigned* __restrict__ all_refined) {
+                            unsigned* __restrict__ all_count, unsigned* __restrict__ all_refined, int accum) {
   const int b = threadIdx.x;
   if (b >= nb) return;
   const uint64_t key = best[b * kPadU64];
   if (key == kNoKey) { out_idx[q0 + b] = -1; out_dist[q0 + b] = INFINITY; }
   else { out_idx[q0 + b] = (int64_t)key_id(key); out_dist[q0 + b] = sqrtf(key_val(key)); }
-  all_count[q0 + b] = count[b];
-  all_refined[q0 + b] = refined[b];
+  all_count[q0 + b] = (accum ? all_count[q0 + b] : 0u) + count[b];
+  all_refined[q0 + b] = (accum ? all_refined[q0 + b] : 0u) + refined[b];
 }
 
 // Merge the per-CTA top-k lists: repeatedly sort [current top-k | next chunk]
@@ -1280,7 +1298,7 @@ __global__ void __launch_bounds__(1024)
 k_finalize(const uint64_t* __restrict__ lists, int nslots, int k, int q0,
            int64_t* __restrict__ out_idx, float* __restrict__ out_dist,
            const unsigned* __restrict__ count, const unsigned* __restrict__ refined,
-           unsigned* __restrict__ all_count, unsigned* __restrict__ all_refined) {
+           unsigned* __restrict__ all_count, unsigned* __restrict__ all_refined, int accum) {
   __shared__ uint64_t buf[kSortP];
   const int b = blockIdx.x;
   const int64_t total = (int64_t)nslots * k;
@@ -1301,8 +1319,8 @@ k_finalize(const uint64_t* __restrict__ lists, int nslots, int k, int q0,
     else { out_idx[o] = (int64_t)key_id(key); out_dist[o] = sqrtf(key_val(key)); }
   }
   if (threadIdx.x == 0) {
-    all_count[q0 + b] = count[b];
-    all_refined[q0 + b] = refined[b];
+    all_count[q0 + b] = (accum ? all_count[q0 + b] : 0u) + count[b];
+    all_refined[q0 + b] = (accum ? all_refined[q0 + b] : 0u) + refined[b];
   }
 }
 
@@ -1508,25 +1526,35 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
 // One batch of nb <= kMaxB queries (device pointers).  Outputs at [q0 .. q0+nb).
 int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* qbatch, int nb, int q0,
               int64_t cap, const CardTables* tab, const Ws& ws, int64_t* d_idx, float* d_dist,
-              unsigned* all_count, unsigned* all_refined, float* all_tau, cudaStream_t st) {
+              unsigned* all_count, unsigned* all_refined, float* all_tau, cudaStream_t st,
+              bool rescan = false) {
   const int P = pairs_for(nb);
   cudaError_t e = cudaMemsetAsync(ws.zero_block, 0, ws.zero_bytes, st);
   if (e != cudaSuccess) return cuda_error(e, "memset scratch");
-  if (p.tiled) {
-    PARIS_CHECK_LAUNCH(launch_qprep(nb, p, qbatch, ws, st), "qprep launch");
-    PARIS_CHECK_LAUNCH(dispatch_lbt<0>(nb, p, sax, tab, ws, st, cap, p.ns, p.seed_grid), "seed_lb launch");
+  if (rescan) {
+    // query PAA (the direct LB kernels compute it in their seed prologue) + BSF from the first pass
+    if (p.tiled) PARIS_CHECK_LAUNCH(launch_qprep(nb, p, qbatch, ws, st), "qprep launch");
+    else PARIS_CHECK_LAUNCH(dispatch_p(P, false, p, sax, qbatch, nb, tab, ws, st, cap), "seed_lb launch");
+    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("seed_select", k_seed_prev, 1, 32, 0, st, d_idx, d_dist, nb, q0, p.k, p.d2up,
+                                    ws.thr, ws.thr_seed, ws.best),
+                       "seed_prev launch");
   } else {
-    PARIS_CHECK_LAUNCH(dispatch_p(P, false, p, sax, qbatch, nb, tab, ws, st, cap), "seed_lb launch");
+    if (p.tiled) {
+      PARIS_CHECK_LAUNCH(launch_qprep(nb, p, qbatch, ws, st), "qprep launch");
+      PARIS_CHECK_LAUNCH(dispatch_lbt<0>(nb, p, sax, tab, ws, st, cap, p.ns, p.seed_grid), "seed_lb launch");
+    } else {
+      PARIS_CHECK_LAUNCH(dispatch_p(P, false, p, sax, qbatch, nb, tab, ws, st, cap), "seed_lb launch");
+    }
+    {
+      dim3 g((unsigned)((p.S + 7) / 8), (unsigned)nb);
+      PARIS_CHECK_LAUNCH(PARIS_LAUNCH("seed_ed", k_seed_ed, g, kRefThreads, (size_t)p.len * 4, st, raw, p.len,
+                                      qbatch, ws.seed_ids, p.S, ws.seed_keys),
+                         "seed_ed launch");
+    }
+    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("seed_select", k_seed_select, nb, 1024, 0, st, ws.seed_keys, p.S, p.k,
+                                    p.d2up, ws.thr, ws.thr_seed, ws.best, all_tau, q0),
+                       "seed_select launch");
   }
-  {
-    dim3 g((unsigned)((p.S + 7) / 8), (unsigned)nb);
-    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("seed_ed", k_seed_ed, g, kRefThreads, (size_t)p.len * 4, st, raw, p.len,
-                                    qbatch, ws.seed_ids, p.S, ws.seed_keys),
-                       "seed_ed launch");
-  }
-  PARIS_CHECK_LAUNCH(PARIS_LAUNCH("seed_select", k_seed_select, nb, 1024, 0, st, ws.seed_keys, p.S, p.k,
-                                  p.d2up, ws.thr, ws.thr_seed, ws.best, all_tau, q0),
-                     "seed_select launch");
   if (p.tiled) {
     const int grid = (int)std::min<int64_t>(sms(), (p.n + kTS - 1) / kTS);
     PARIS_CHECK_LAUNCH(dispatch_lbt<1>(nb, p, sax, tab, ws, st, cap, p.n, grid), "lb_pass launch");
@@ -1566,13 +1594,13 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
     }
     PARIS_CHECK_LAUNCH(e1, "refine launch");
     PARIS_CHECK_LAUNCH(PARIS_LAUNCH("finalize", k_finalize1, 1, 32, 0, st, ws.best, nb, q0, d_idx, d_dist,
-                                    ws.count, ws.refined, all_count, all_refined),
+                                    ws.count, ws.refined, all_count, all_refined, rescan ? 1 : 0),
                        "finalize launch");
   } else {
     const size_t rsmem = (size_t)p.len * 4 + (size_t)p.k * 16;
     PARIS_CHECK_LAUNCH(PARIS_LAUNCH("refine", k_refine_topk, g, kRefThreads, rsmem, st, ra), "refine launch");
     PARIS_CHECK_LAUNCH(PARIS_LAUNCH("finalize", k_finalize, nb, 1024, 0, st, ws.lists, p.XB, p.k, q0,
-                                    d_idx, d_dist, ws.count, ws.refined, all_count, all_refined),
+                                    d_idx, d_dist, ws.count, ws.refined, all_count, all_refined, rescan ? 1 : 0),
                        "finalize launch");
   }
   return PARIS_OK;
@@ -1692,7 +1720,8 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   if (rc == PARIS_OK) {
     for (int q = 0; q < nq && rc == PARIS_OK; ++q) {
       if ((int64_t)h_count[q] <= p.cap) continue;
-      // re-scan this query alone with an exact-size candidate buffer
+      // re-scan this query alone, seeded with its first-pass result (refined over the
+      // `cap` candidates kept) -- its candidates are a subset of the first pass's
       Plan p1 = p;
       p1.B = 1;
       plan_refine(p1);
@@ -1701,7 +1730,7 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
       rc = alloc_ws(p1, p1.cap, ws1, st);
       if (rc) break;
       rc = run_batch(p1, raw, sax, d_q + (size_t)q * len, 1, q, p1.cap, tab, ws1, d_idx, d_dist,
-                     all_count, all_refined, all_tau, st);
+                     all_count, all_refined, all_tau, st, /*rescan=*/true);
       cudaFreeAsync(ws1.base, st);
     }
   }
