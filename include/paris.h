@@ -40,6 +40,7 @@ extern "C" {
 #define PARIS_ENOMEM (-4)  /* scratch allocation failed */
 
 #define PARIS_MAX_K 1024
+#define PARIS_INDEX_BLOCK 128 /* series per envelope block of the index (paris_index_build) */
 
 /*
  * paris_summarize -- ConvertToSAX over a whole collection (IndexBulkLoading,
@@ -89,6 +90,25 @@ int paris_knn_exact(const float* raw, const uint8_t* sax, int64_t n, const float
                     int32_t nq, int32_t k, int64_t* out_idx, float* out_dist, int32_t len,
                     int32_t w, int32_t card, void* stream);
 
+/*
+ * paris_index_build -- GPU-native iSAX organization of a SAX array (SURVEY §8(f)
+ * f1; the data-parallel analog of ParIS+'s index construction, Stage 3,
+ * P:396-402).  Series are ordered the way the iSAX tree groups them (root split
+ * on the first bit of every segment; deeper nodes on further
+ * bits) at uniform cardinality: by the key interleaving bits 7..4 of
+ * the 16 symbols (card < 256: symbols scaled to 8 bits), ties by id.
+ *   sax            device [w][n] uint8 (paris_summarize)
+ *   out_sax_sorted device [w][n] uint8: out_sax_sorted[s*n + j] = sax[s*n + perm[j]]
+ *   out_perm       device [n] uint32: series id at sorted position j
+ *   out_env        device [ceil(n/PARIS_INDEX_BLOCK)][2][w] uint8: per block of
+ *                  PARIS_INDEX_BLOCK consecutive sorted series, the min ([blk][0][s])
+ *                  and max ([blk][1][s]) symbol of segment s (the node envelope)
+ * Requires w == 16, n % 16 == 0 (PARIS_ECONFIG otherwise).  Asynchronous on
+ * `stream`; scratch (~36 bytes per series) is stream-ordered.
+ */
+int paris_index_build(const uint8_t* sax, int64_t n, int32_t w, int32_t card, uint8_t* out_sax_sorted,
+                      uint32_t* out_perm, uint8_t* out_env, void* stream);
+
 /* Tunables for paris_knn_exact_ex (0 = library default). */
 typedef struct paris_knn_config {
   int32_t batch;        /* queries per SAX pass (1..16); default 16 */
@@ -109,6 +129,27 @@ int paris_knn_exact_ex(const float* raw, const uint8_t* sax, int64_t n, const fl
                        int32_t nq, int32_t k, int64_t* out_idx, float* out_dist, int32_t len,
                        int32_t w, int32_t card, void* stream, const paris_knn_config* config,
                        paris_knn_stats* stats);
+
+/*
+ * paris_knn_index -- exact k-NN like paris_knn_exact, over an index built by
+ * paris_index_build (same results; raw stays in its original order):
+ *   1. approximate search: the query's own word is located in the
+ *      sorted array (the leaf it would be inserted into); the true distances of
+ *      the 1024 series around it give tau_seed;
+ *   2. LBC pass over the sorted SAX array: each block's envelope MINDIST (the
+ *      iSAX node bound) is computed first and only the queries the block can hold
+ *      candidates for are evaluated on its series;
+ *   3-4. as paris_knn_exact (candidate ids are the original series ids).
+ * Requires w == 16 and n % 16 == 0.
+ */
+int paris_knn_index(const float* raw, const uint8_t* sax_sorted, const uint32_t* perm, const uint8_t* env,
+                    int64_t n, const float* queries, int32_t nq, int32_t k, int64_t* out_idx, float* out_dist,
+                    int32_t len, int32_t w, int32_t card, void* stream);
+
+int paris_knn_index_ex(const float* raw, const uint8_t* sax_sorted, const uint32_t* perm, const uint8_t* env,
+                       int64_t n, const float* queries, int32_t nq, int32_t k, int64_t* out_idx,
+                       float* out_dist, int32_t len, int32_t w, int32_t card, void* stream,
+                       const paris_knn_config* config, paris_knn_stats* stats);
 
 /* Thread-local text of the last failure (never NULL). */
 const char* paris_last_error(void);

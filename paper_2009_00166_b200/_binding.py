@@ -75,6 +75,13 @@ def load():
         lib.paris_knn_exact_ex.argtypes = [P, P, i64, P, i32, i32, P, P, i32, i32, i32, P,
                                            ctypes.POINTER(_Config), ctypes.POINTER(_Stats)]
         lib.paris_knn_exact_ex.restype = ctypes.c_int
+        lib.paris_index_build.argtypes = [P, i64, i32, i32, P, P, P, P]
+        lib.paris_index_build.restype = ctypes.c_int
+        lib.paris_knn_index_ex.argtypes = [P, P, P, P, i64, P, i32, i32, P, P, i32, i32, i32, P,
+                                           ctypes.POINTER(_Config), ctypes.POINTER(_Stats)]
+        lib.paris_knn_index_ex.restype = ctypes.c_int
+        lib.paris_knn_index.argtypes = [P, P, P, P, i64, P, i32, i32, P, P, i32, i32, i32, P]
+        lib.paris_knn_index.restype = ctypes.c_int
         lib.paris_last_error.restype = ctypes.c_char_p
         lib.paris_version.restype = i32
         lib.paris_profile_enable.argtypes = [i32]
@@ -141,10 +148,47 @@ def summarize(raw: torch.Tensor, w: int = 16, card: int = 256, out: torch.Tensor
     return out
 
 
+PARIS_INDEX_BLOCK = 128
+
+
+@dataclass
+class Index:
+    """iSAX-ordered SAX array (paris_index_build): sorted SoA words, ids, block envelopes."""
+    sax_sorted: torch.Tensor   # uint8 [w][n]
+    perm: torch.Tensor         # int32 [n] (uint32 ids)
+    env: torch.Tensor          # uint8 [ceil(n/128)][2][w]
+    w: int
+    card: int
+
+
+def index_build(sax: torch.Tensor, w: int = 16, card: int = 256, stream=None) -> Index:
+    """Sort the SAX array by its iSAX key and compute block envelopes (CUDA)."""
+    lib = load()
+    _need_cuda(sax, "sax")
+    if sax.dtype != torch.uint8 or sax.dim() != 2 or sax.shape[0] != w:
+        raise ValueError("sax must be uint8 [w][n]")
+    n = sax.shape[1]
+    nblk = (n + PARIS_INDEX_BLOCK - 1) // PARIS_INDEX_BLOCK
+    out = torch.empty_like(sax)
+    perm = torch.empty(n, dtype=torch.int32, device=sax.device)
+    env = torch.empty((nblk, 2, w), dtype=torch.uint8, device=sax.device)
+    _check(lib.paris_index_build(sax.data_ptr(), n, w, card, out.data_ptr(), perm.data_ptr(), env.data_ptr(),
+                                 _stream(stream)))
+    return Index(out, perm, env, w, card)
+
+
+def knn_index(raw: torch.Tensor, index: Index, queries: torch.Tensor, k: int = 1,
+              out_idx: torch.Tensor | None = None, out_dist: torch.Tensor | None = None, stream=None,
+              config: KnnConfig | None = None, stats: bool = False):
+    """Exact k-NN over an Index (paris_knn_index); same results as knn_exact."""
+    return knn_exact(raw, index.sax_sorted, queries, k=k, w=index.w, card=index.card, out_idx=out_idx,
+                     out_dist=out_dist, stream=stream, config=config, stats=stats, _index=index)
+
+
 def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: int = 1,
               w: int = 16, card: int = 256, out_idx: torch.Tensor | None = None,
               out_dist: torch.Tensor | None = None, stream=None,
-              config: KnnConfig | None = None, stats: bool = False):
+              config: KnnConfig | None = None, stats: bool = False, _index: Index | None = None):
     """Exact k-NN of every query (rows of `queries`, CUDA or host) over raw/sax (CUDA).
 
     Returns (idx int64 [nq][k], dist float32 [nq][k]) on the device of `queries`
@@ -181,10 +225,16 @@ def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: in
         arrays = (torch.zeros(nq, dtype=torch.int64), torch.zeros(nq, dtype=torch.int64),
                   torch.zeros(nq, dtype=torch.float32))
         st = _Stats(arrays[0].data_ptr(), arrays[1].data_ptr(), arrays[2].data_ptr())
-    rc = lib.paris_knn_exact_ex(raw.data_ptr(), sax.data_ptr(), n, queries.data_ptr(), nq, k,
-                                out_idx.data_ptr(), out_dist.data_ptr(), length, w, card,
-                                _stream(stream), ctypes.byref(cfg) if cfg else None,
-                                ctypes.byref(st) if st else None)
+    if _index is None:
+        rc = lib.paris_knn_exact_ex(raw.data_ptr(), sax.data_ptr(), n, queries.data_ptr(), nq, k,
+                                    out_idx.data_ptr(), out_dist.data_ptr(), length, w, card,
+                                    _stream(stream), ctypes.byref(cfg) if cfg else None,
+                                    ctypes.byref(st) if st else None)
+    else:
+        rc = lib.paris_knn_index_ex(raw.data_ptr(), sax.data_ptr(), _index.perm.data_ptr(), _index.env.data_ptr(),
+                                    n, queries.data_ptr(), nq, k, out_idx.data_ptr(), out_dist.data_ptr(),
+                                    length, w, card, _stream(stream), ctypes.byref(cfg) if cfg else None,
+                                    ctypes.byref(st) if st else None)
     _check(rc)
     if stats:
         return out_idx, out_dist, {"candidates": arrays[0], "refined": arrays[1],

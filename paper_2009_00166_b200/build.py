@@ -21,7 +21,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills"]
-SOURCES = ["runtime.cu", "summarize.cu", "knn.cu"]
+SOURCES = ["runtime.cu", "summarize.cu", "knn.cu", "index.cu"]
 HEADERS = ["runtime.cuh"]
 
 

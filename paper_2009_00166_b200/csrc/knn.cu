@@ -444,6 +444,49 @@ __global__ void k_seed_prev(const int64_t* __restrict__ prev_idx, const float* _
   if (k == 1) best[b * kPadU64] = ok ? make_key(__fmul_ru(__fmul_ru(d, d), 1.00000096f), (uint32_t)id) : kNoKey;
 }
 
+// Index mode seed = approximate search: the leaf the query's own
+// iSAX word would be inserted into.  One warp per query: the word (symbols of the
+// query PAA midpoints; any word is sound, this one is the closest leaf), its key,
+// a 32-ary search of the sorted array (lane l probes one position per round),
+// then the S series around the insertion point become the seed set.
+__global__ void __launch_bounds__(32)
+k_approx_seed(const uint8_t* __restrict__ sax_sorted, const uint32_t* __restrict__ perm, int64_t n,
+              const float2* __restrict__ g_q, const CardTables* __restrict__ tab, int card,
+              int* __restrict__ seed_ids, int S) {
+  const int b = blockIdx.x, lane = threadIdx.x;
+  int shift = 0;
+  while ((card << shift) < 256) ++shift;
+  // symbol of segment `lane` (lanes 0..15)
+  int sym = 0;
+  if (lane < 16) {
+    const float2 q = g_q[b * kMaxW + lane];
+    const float v = 0.5f * (q.x + q.y);
+    for (int step = card >> 1; step >= 1; step >>= 1)
+      if (tab->cuts_f[sym + step - 1] <= v) sym += step;
+  }
+  uint8_t word[16];
+#pragma unroll
+  for (int s = 0; s < 16; ++s) word[s] = (uint8_t)__shfl_sync(0xffffffffu, sym, s);
+  const uint64_t target = isax_key16(word, shift);
+  // lower_bound of target over keys(0..n-1); invariant: the answer lies in [lo, hi]
+  int64_t lo = 0, hi = n;
+  while (hi - lo > 32) {
+    const int64_t step = (hi - lo) / 32;
+    const int64_t pos = lo + step * (lane + 1) - 1;  // increasing in lane, all < hi
+    uint8_t w2[16];
+#pragma unroll
+    for (int s = 0; s < 16; ++s) w2[s] = sax_sorted[(size_t)s * n + pos];
+    const int c = __popc(__ballot_sync(0xffffffffu, isax_key16(w2, shift) < target));  // a prefix of lanes
+    const int64_t nlo = lo + step * c;
+    hi = (c < 32) ? lo + step * (c + 1) - 1 : hi;
+    lo = nlo;
+  }
+  const int64_t cnt = min((int64_t)S, n);
+  int64_t start = lo - cnt / 2;
+  start = max((int64_t)0, min(start, n - cnt));
+  for (int t = lane; t < S; t += 32) seed_ids[b * S + t] = (t < cnt) ? (int)perm[start + t] : -1;
+}
+
 // ---------------------------------------------------------------- K4 LBC pass
 // Alg10: for every word, LB < BSF -> append (LB, position).
 // Here: up to 2P queries per SAX read, in packed fp16; warp-aggregated atomics
@@ -474,6 +517,8 @@ struct LbArgs {
   unsigned* hist;
   uint64_t* cand;
   int64_t cap;
+  const uint32_t* perm;  // index mode: sorted position -> series id (else nullptr)
+  const uint8_t* env;    // index mode: [n/128 blocks][2][16] min/max symbols (else nullptr)
 };
 
 struct LbConsts {
@@ -524,7 +569,8 @@ __device__ void lb_consts_init(const LbArgs& a, int nslots, LbConsts* c) {
 // Whole warp must call it (warp-aggregated atomics).
 template <int P>
 __device__ __forceinline__ void lb_emit(const uint32_t (&acc)[4][P], int64_t i0, int nvalid,
-                                        const LbConsts& c, const LbArgs& a) {
+                                        const LbConsts& c, const LbArgs& a,
+                                        uint32_t slot_mask = 0xFFFFFFFFu, const uint32_t* perm = nullptr) {
   const int lane = threadIdx.x & 31;
   uint32_t qm = 0;
   if (nvalid > 0) {
@@ -533,6 +579,7 @@ __device__ __forceinline__ void lb_emit(const uint32_t (&acc)[4][P], int64_t i0,
       const uint32_t mn = h2_min(h2_min(acc[0][p], acc[1][p]), h2_min(acc[2][p], acc[3][p]));
       qm |= h2_le_bits(mn, c.T16[p]) << (2 * p);
     }
+    qm &= slot_mask;
   }
   if (!__any_sync(0xffffffffu, qm != 0)) return;
   uint32_t wq = __reduce_or_sync(0xffffffffu, qm);
@@ -572,7 +619,8 @@ __device__ __forceinline__ void lb_emit(const uint32_t (&acc)[4][P], int64_t i0,
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       if (m & (1u << j)) {
-        if (pos < (uint64_t)a.cap) a.cand[(size_t)b * a.cap + pos] = make_key(lbv[j], (uint32_t)(i0 + j));
+        if (pos < (uint64_t)a.cap)
+          a.cand[(size_t)b * a.cap + pos] = make_key(lbv[j], perm ? __ldg(perm + i0 + j) : (uint32_t)(i0 + j));
         atomicAdd(&a.hist[b * kNB + lb_bin(lbv[j], sc)], 1u);
         ++pos;
       }
@@ -617,9 +665,12 @@ __device__ void wb_flush(WarpBuf& wb, int nslots, const LbConsts& c, const LbArg
   __syncwarp();
 }
 
+// slot_mask: query slots this warp's block may hold candidates for (index mode);
+// perm: sorted position -> series id (index mode), nullptr = identity.
 template <int P>
 __device__ __forceinline__ void lb_emit_wb(const uint32_t (&acc)[4][P], int64_t i0, int nvalid, int nslots,
-                                           const LbConsts& c, const LbArgs& a, WarpBuf& wb, unsigned* s_hist) {
+                                           const LbConsts& c, const LbArgs& a, WarpBuf& wb, unsigned* s_hist,
+                                           uint32_t slot_mask = 0xFFFFFFFFu, const uint32_t* perm = nullptr) {
   const int lane = threadIdx.x & 31;
   uint32_t qm = 0;
   if (nvalid > 0) {
@@ -628,6 +679,7 @@ __device__ __forceinline__ void lb_emit_wb(const uint32_t (&acc)[4][P], int64_t 
       const uint32_t mn = h2_min(h2_min(acc[0][p], acc[1][p]), h2_min(acc[2][p], acc[3][p]));
       qm |= h2_le_bits(mn, c.T16[p]) << (2 * p);
     }
+    qm &= slot_mask;
   }
   if (!__any_sync(0xffffffffu, qm != 0)) return;
   // pass 1: this lane's candidate count; pass 2 writes (lane-local loops over set bits)
@@ -656,7 +708,7 @@ __device__ __forceinline__ void lb_emit_wb(const uint32_t (&acc)[4][P], int64_t 
   if (total == 0) return;
   if (wb.n + total > kWB) wb_flush(wb, nslots, c, a, s_hist);
   if (total > kWB) {  // degenerate (e.g. tau = inf): straight to global memory
-    lb_emit<P>(acc, i0, nvalid, c, a);
+    lb_emit<P>(acc, i0, nvalid, c, a, qm, perm);
     return;
   }
   int pos = wb.n + incl - cntl;
@@ -672,7 +724,7 @@ __device__ __forceinline__ void lb_emit_wb(const uint32_t (&acc)[4][P], int64_t 
       const float h = (b & 1) ? h_hi_f(v) : h_lo_f(v);
       const float lb = __fmul_rd(fmaxf(__fsub_rd(h, c.wabs), 0.f), c.lbconv);
       if (((h2_le_bits(v, T) >> (b & 1)) & 1u) && j < nvalid && lb <= c.thr[b]) {
-        wb.key[pos] = make_key(lb, (uint32_t)(i0 + j));
+        wb.key[pos] = make_key(lb, perm ? __ldg(perm + i0 + j) : (uint32_t)(i0 + j));
         wb.slot[pos] = (uint8_t)b;
         atomicAdd(&wb.cnt[b], 1u);
         ++pos;
@@ -771,6 +823,75 @@ __device__ __forceinline__ void lbt_seg(uint32_t word, const uint32_t* __restric
   }
 }
 
+// Same for pairs [G0, G0+GP) of a P-pair accumulator (index mode: only the
+// query pairs whose block bound can pass are computed).
+template <int P, int G0, int GP>
+__device__ __forceinline__ void lbt_seg_g(uint32_t word, const uint32_t* __restrict__ tabl,
+                                          const uint2* __restrict__ q16s, uint32_t (&acc)[4][P]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t t = tabl[__byte_perm(word, 0, 0x4440 | j) * 32];
+    const uint32_t tx = __byte_perm(t, 0, 0x1010);
+    const uint32_t ty = __byte_perm(t, 0, 0x3232);
+#pragma unroll
+    for (int p = G0; p < G0 + GP; ++p) {
+      const uint2 q = q16s[p];
+      const uint32_t a = h2_fma_relu(q.x, kHalf2One, tx);
+      const uint32_t b = h2_fma_relu(q.y, kHalf2One, ty);
+      const uint32_t d = h2_max(a, b);
+      acc[j][p] = h2_fma(d, d, acc[j][p]);
+    }
+  }
+}
+
+template <int P, int G0, int GP>
+__device__ __forceinline__ void lbt_group(uint32_t bm, const uint32_t* __restrict__ rows, int tid,
+                                          const uint32_t* __restrict__ tabl, const uint2* __restrict__ s_q16,
+                                          uint32_t (&acc)[4][P]) {
+  if constexpr (G0 < P) {
+    constexpr uint32_t gm = ((1u << (2 * GP)) - 1u) << (2 * G0);
+    if (bm & gm) {
+#pragma unroll 2
+      for (int s = 0; s < kTW; ++s) lbt_seg_g<P, G0, GP>(rows[s * (kTS / 4) + tid], tabl, s_q16 + s * P, acc);
+    }
+    lbt_group<P, G0 + GP, GP>(bm, rows, tid, tabl, s_q16, acc);
+  }
+}
+
+// Block MINDIST (the iSAX node bound) of this warp's 128-series block for every
+// query slot, from the block's per-segment [min, max] symbols: region
+// [L[min], U[max]] (outward fp32), round-down arithmetic -> bit b set iff the
+// block's LB^2 <= thr[b] (only then can one of its series be a candidate).
+__device__ __forceinline__ uint32_t block_mask(const uint8_t* __restrict__ env, int64_t blk, int nslots,
+                                               const float2* __restrict__ s_q, const float2* __restrict__ s_lu,
+                                               const LbConsts& c, float seglen) {
+  const int lane = threadIdx.x & 31;
+  const int b = lane >> 1, h = lane & 1;
+  float acc = 0.f;
+  if (b < nslots) {
+    const uint2 mn = __ldg(reinterpret_cast<const uint2*>(env + (size_t)blk * 32 + 8 * h));
+    const uint2 mx = __ldg(reinterpret_cast<const uint2*>(env + (size_t)blk * 32 + 16 + 8 * h));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int seg = 8 * h + k;
+      const uint32_t cmin = ((k < 4 ? mn.x : mn.y) >> (8 * (k & 3))) & 0xFFu;
+      const uint32_t cmax = ((k < 4 ? mx.x : mx.y) >> (8 * (k & 3))) & 0xFFu;
+      const float2 q = s_q[b * kMaxW + seg];
+      const float above = __fsub_rd(q.x, s_lu[cmax].y);
+      const float below = __fsub_rd(s_lu[cmin].x, q.y);
+      const float delta = fmax3(above, below, 0.f);
+      acc = __fmaf_rd(delta, delta, acc);
+    }
+  }
+  acc = __fadd_rd(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
+  const bool act = (b < nslots) && h == 0 && __fmul_rd(acc, seglen) <= c.thr[b];
+  const uint32_t m = __ballot_sync(0xffffffffu, act);
+  uint32_t r = 0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) r |= ((m >> (2 * k)) & 1u) << k;
+  return r;
+}
+
 // Single-query form (B = 1): qd = half2(q_lo16, -q_hi16) against (-U16, L16):
 // one relu-FMA gives (relu(q-U), relu(L-q)), one FMA accumulates both halves
 // (at most one is non-zero); the LB sum is lo + hi at the end.
@@ -785,7 +906,10 @@ __device__ __forceinline__ void lbt_seg1(uint32_t word, const uint32_t* __restri
 }
 
 // MODE 0: seed (per-warp LB-best series per query over [0, nlim));
-// MODE 1: LB pass with candidate emission over [0, nlim = n).
+// MODE 1: LB pass with candidate emission over [0, nlim = n);
+// MODE 2: the same over the index-sorted SAX array: each warp first bounds its
+//         128-series block (envelope MINDIST) and computes only the query pairs
+//         the block can hold candidates for; candidate ids go through perm.
 // P = 0: single query (slot 0).  nlim % 16 == 0.
 template <int P, int MODE>
 __global__ void __launch_bounds__(kTThreads, 1)
@@ -798,13 +922,19 @@ k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
   __shared__ unsigned s_cnt[kStages];
   __shared__ uint2 s_q16[PP * kTW];
   __shared__ LbConsts s_c;
-  __shared__ WarpBuf s_wb[MODE == 1 ? kTWarps : 1];
-  __shared__ unsigned s_hist[MODE == 1 ? kMaxB * kNB : 1];
+  __shared__ WarpBuf s_wb[MODE >= 1 ? kTWarps : 1];
+  __shared__ unsigned s_hist[MODE >= 1 ? kMaxB * kNB : 1];
+  __shared__ float2 s_lu[MODE == 2 ? kMaxCard : 1];
+  __shared__ float2 s_qf[MODE == 2 ? 2 * PP * kMaxW : 1];
   const int tid = threadIdx.x, lane = tid & 31;
   const int64_t ntiles = (nlim + kTS - 1) / kTS;
   const int nslots = P > 0 ? 2 * P : 1;
-  WarpBuf& wb = s_wb[MODE == 1 ? (tid >> 5) : 0];
-  if (MODE == 1) {
+  WarpBuf& wb = s_wb[MODE >= 1 ? (tid >> 5) : 0];
+  if (MODE == 2) {
+    for (int i = tid; i < kMaxCard; i += kTThreads) s_lu[i] = a.tab->lu[i];
+    for (int i = tid; i < 2 * PP * kMaxW; i += kTThreads) s_qf[i] = a.g_q[i];
+  }
+  if (MODE >= 1) {
     if (lane < kMaxB) wb.cnt[lane] = 0;
     if (lane == 0) wb.n = 0;
     for (int i = tid; i < nslots * kNB; i += kTThreads) s_hist[i] = 0;
@@ -865,7 +995,14 @@ k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
     for (int j = 0; j < 4; ++j)
 #pragma unroll
       for (int p = 0; p < PP; ++p) acc[j][p] = 0u;
-    if (P > 0) {
+    uint32_t bm = 0xFFFFFFFFu;
+    if (MODE == 2) bm = block_mask(a.env, (tile * kTS) / PARIS_INDEX_BLOCK + (tid >> 5), nslots, s_qf, s_lu, s_c,
+                                   a.seglen_f);
+    if (MODE == 2 && P > 0) {
+      lbt_group<PP, 0, (PP < 2 ? PP : 2)>(bm, rows, tid, tabl, s_q16, acc);
+    } else if (MODE == 2 && bm == 0) {
+      // single query, block pruned: nothing to compute
+    } else if (P > 0) {
 #pragma unroll 2
       for (int s = 0; s < kTW; ++s) lbt_seg<PP>(rows[s * (kTS / 4) + tid], tabl, s_q16 + s * PP, acc);
     } else {
@@ -893,8 +1030,8 @@ k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
         }
       }
     }
-    if (MODE == 1) {
-      lb_emit_wb<PP>(acc, i0, nvalid, nslots, s_c, a, wb, s_hist);
+    if (MODE >= 1) {
+      lb_emit_wb<PP>(acc, i0, nvalid, nslots, s_c, a, wb, s_hist, bm, MODE == 2 ? a.perm : nullptr);
     } else {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -908,7 +1045,7 @@ k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
       }
     }
   }
-  if (MODE == 1) {
+  if (MODE >= 1) {
     wb_flush(wb, nslots, s_c, a, s_hist);
     __syncthreads();
     for (int i = tid; i < nslots * kNB; i += kTThreads)
@@ -1376,6 +1513,8 @@ struct Plan {
   int wave_a;     // k = 1: candidates per query refined in the first wave
   float d2up;     // fp32 d^2 -> rigorous upper bound factor
   bool tiled;     // TMA-tiled LB kernels (n % 16 == 0, w == 16)
+  const uint32_t* perm;  // index mode (paris_knn_index): sorted position -> id
+  const uint8_t* env;    // index mode: block envelopes
 };
 
 int pairs_for(int nb) { return nb <= 2 ? 1 : nb <= 4 ? 2 : nb <= 8 ? 4 : 8; }
@@ -1398,7 +1537,7 @@ cudaError_t launch_lb(const Plan& p, const uint8_t* sax, int nb, const CardTable
   LbArgs la;
   la.sax = sax; la.n = p.n; la.w = p.w; la.seglen_f = (float)(p.len / p.w); la.tab = tab;
   la.g_q = ws.g_q; la.g_q16 = ws.g_q16; la.nb = nb; la.thr = ws.thr_seed; la.count = ws.count;
-  la.hist = ws.hist; la.cand = ws.cand; la.cap = cap;
+  la.hist = ws.hist; la.cand = ws.cand; la.cap = cap; la.perm = nullptr; la.env = nullptr;
   return PARIS_LAUNCH("lb_pass", (k_lb<P, WT, AL>), grid, kLBThreads, 0, st, la);
 }
 
@@ -1444,7 +1583,7 @@ cudaError_t launch_lbt(const Plan& p, const uint8_t* sax, int nb, const CardTabl
   LbArgs la;
   la.sax = sax; la.n = p.n; la.w = p.w; la.seglen_f = (float)(p.len / p.w); la.tab = tab;
   la.g_q = ws.g_q; la.g_q16 = ws.g_q16; la.nb = nb; la.thr = ws.thr_seed; la.count = ws.count;
-  la.hist = ws.hist; la.cand = ws.cand; la.cap = cap;
+  la.hist = ws.hist; la.cand = ws.cand; la.cap = cap; la.perm = p.perm; la.env = p.env;
   return PARIS_LAUNCH(MODE ? "lb_pass" : "seed_lb", (k_lbt<P, MODE>), grid, kTThreads, kTSmem, st, la, nlim,
                       ws.seed_ids, p.S);
 }
@@ -1539,7 +1678,12 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
                                     ws.thr, ws.thr_seed, ws.best),
                        "seed_prev launch");
   } else {
-    if (p.tiled) {
+    if (p.perm) {
+      PARIS_CHECK_LAUNCH(launch_qprep(nb, p, qbatch, ws, st), "qprep launch");
+      PARIS_CHECK_LAUNCH(PARIS_LAUNCH("seed_lb", k_approx_seed, nb, 32, 0, st, sax, p.perm, p.n, ws.g_q, tab, p.card,
+                                      ws.seed_ids, p.S),
+                         "approx seed launch");
+    } else if (p.tiled) {
       PARIS_CHECK_LAUNCH(launch_qprep(nb, p, qbatch, ws, st), "qprep launch");
       PARIS_CHECK_LAUNCH(dispatch_lbt<0>(nb, p, sax, tab, ws, st, cap, p.ns, p.seed_grid), "seed_lb launch");
     } else {
@@ -1557,7 +1701,8 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
   }
   if (p.tiled) {
     const int grid = (int)std::min<int64_t>(sms(), (p.n + kTS - 1) / kTS);
-    PARIS_CHECK_LAUNCH(dispatch_lbt<1>(nb, p, sax, tab, ws, st, cap, p.n, grid), "lb_pass launch");
+    if (p.perm) PARIS_CHECK_LAUNCH(dispatch_lbt<2>(nb, p, sax, tab, ws, st, cap, p.n, grid), "lb_pass launch");
+    else PARIS_CHECK_LAUNCH(dispatch_lbt<1>(nb, p, sax, tab, ws, st, cap, p.n, grid), "lb_pass launch");
   } else {
     PARIS_CHECK_LAUNCH(dispatch_p(P, true, p, sax, qbatch, nb, tab, ws, st, cap), "lb_pass launch");
   }
@@ -1599,6 +1744,30 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
   } else {
     const size_t rsmem = (size_t)p.len * 4 + (size_t)p.k * 16;
     PARIS_CHECK_LAUNCH(PARIS_LAUNCH("refine", k_refine_topk, g, kRefThreads, rsmem, st, ra), "refine launch");
+    if (getenv("PARIS_DEBUG_DUMP")) {  // debugging aid: candidate lists and per-CTA top-k lists
+      cudaStreamSynchronize(st);
+      std::vector<unsigned> hc(nb);
+      cudaMemcpy(hc.data(), ws.count, 4 * nb, cudaMemcpyDeviceToHost);
+      for (int b = 0; b < nb; ++b) {
+        const size_t c = std::min<size_t>(hc[b], cap);
+        std::vector<uint64_t> h(c), hl((size_t)p.XB * p.k);
+        cudaMemcpy(h.data(), ws.sorted + (size_t)b * cap, 8 * c, cudaMemcpyDeviceToHost);
+        cudaMemcpy(hl.data(), ws.lists + (size_t)b * p.XB * p.k, 8 * hl.size(), cudaMemcpyDeviceToHost);
+        std::vector<uint32_t> ids;
+        for (auto k2 : h) ids.push_back((uint32_t)k2);
+        std::sort(ids.begin(), ids.end());
+        const size_t uniq = std::unique(ids.begin(), ids.end()) - ids.begin();
+        std::sort(hl.begin(), hl.end());
+        fprintf(stderr, "[paris dump] b=%d count=%u uniq=%zu lists_min=(%g,%u) (%g,%u)\n", b, hc[b], uniq,
+                (double)__builtin_bit_cast(float, (uint32_t)(hl[0] >> 32)), (uint32_t)hl[0],
+                (double)__builtin_bit_cast(float, (uint32_t)(hl[1] >> 32)), (uint32_t)hl[1]);
+        const char* want = getenv("PARIS_DEBUG_DUMP");
+        const uint32_t wid = (uint32_t)atoi(want);
+        for (size_t i = 0; i < c; ++i)
+          if ((uint32_t)h[i] == wid)
+            fprintf(stderr, "[paris dump]   id %u at %zu lb=%g\n", wid, i, (double)__builtin_bit_cast(float, (uint32_t)(h[i] >> 32)));
+      }
+    }
     PARIS_CHECK_LAUNCH(PARIS_LAUNCH("finalize", k_finalize, nb, 1024, 0, st, ws.lists, p.XB, p.k, q0,
                                     d_idx, d_dist, ws.count, ws.refined, all_count, all_refined, rescan ? 1 : 0),
                        "finalize launch");
@@ -1613,7 +1782,15 @@ bool is_host_ptr(const void* p) {
   return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered;
 }
 
+constexpr int kIdxSeeds = 1024;  // index mode: series around the query's leaf
+
 void plan_seed(Plan& p, int seed_div) {
+  if (p.perm) {
+    p.ns = 0;
+    p.seed_grid = 0;
+    p.S = kIdxSeeds;
+    return;
+  }
   p.ns = std::min<int64_t>(p.n, std::max<int64_t>(p.n / seed_div, std::min<int64_t>(p.n, 65536)));
   if (p.tiled) {
     p.ns = std::min<int64_t>(p.n, (p.ns + 15) / 16 * 16);
@@ -1635,7 +1812,17 @@ void plan_refine(Plan& p) {
 
 int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queries, int nq, int k,
              int64_t* out_idx, float* out_dist, int len, int w, int card, cudaStream_t st,
-             const paris_knn_config* cfg, paris_knn_stats* stats) {
+             const paris_knn_config* cfg, paris_knn_stats* stats, const uint32_t* perm = nullptr,
+             const uint8_t* env = nullptr) {
+  const bool indexed = perm || env;
+  if (indexed && (!perm || !env)) {
+    set_error("paris_knn_index: null perm/env");
+    return PARIS_EINVAL;
+  }
+  if (indexed && (w != kTW || n % 16 != 0)) {
+    set_error("paris_knn_index: the index needs w == 16 and n %% 16 == 0 (w=%d, n=%lld)", w, (long long)n);
+    return PARIS_ECONFIG;
+  }
   if (!raw || !sax || (nq > 0 && (!queries || !out_idx || !out_dist))) {
     set_error("paris_knn_exact: null pointer");
     return PARIS_EINVAL;
@@ -1660,7 +1847,9 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   Plan p;
   p.n = n; p.len = len; p.w = w; p.card = card; p.k = k;
   p.B = (cfg && cfg->batch > 0) ? std::min(cfg->batch, kMaxB) : kMaxB;
-  p.tiled = (n % 16 == 0) && (w == kTW) && !(cfg && cfg->reserved[0] == 1);
+  p.tiled = (n % 16 == 0) && (w == kTW) && (indexed || !(cfg && cfg->reserved[0] == 1));
+  p.perm = perm;
+  p.env = env;
   plan_seed(p, (cfg && cfg->seed_div > 0) ? cfg->seed_div : 16);
   p.cap = std::min<int64_t>(n, std::max<int64_t>(65536, n / 32));
   plan_refine(p);
@@ -1775,6 +1964,21 @@ int paris_knn_exact_ex(const float* raw, const uint8_t* sax, int64_t n, const fl
                        paris_knn_stats* stats) {
   return paris::knn_impl(raw, sax, n, queries, nq, k, out_idx, out_dist, len, w, card,
                          (cudaStream_t)stream, config, stats);
+}
+
+int paris_knn_index(const float* raw, const uint8_t* sax_sorted, const uint32_t* perm, const uint8_t* env,
+                    int64_t n, const float* queries, int32_t nq, int32_t k, int64_t* out_idx, float* out_dist,
+                    int32_t len, int32_t w, int32_t card, void* stream) {
+  return paris::knn_impl(raw, sax_sorted, n, queries, nq, k, out_idx, out_dist, len, w, card,
+                         (cudaStream_t)stream, nullptr, nullptr, perm, env);
+}
+
+int paris_knn_index_ex(const float* raw, const uint8_t* sax_sorted, const uint32_t* perm, const uint8_t* env,
+                       int64_t n, const float* queries, int32_t nq, int32_t k, int64_t* out_idx,
+                       float* out_dist, int32_t len, int32_t w, int32_t card, void* stream,
+                       const paris_knn_config* config, paris_knn_stats* stats) {
+  return paris::knn_impl(raw, sax_sorted, n, queries, nq, k, out_idx, out_dist, len, w, card,
+                         (cudaStream_t)stream, config, stats, perm, env);
 }
 
 }  // extern "C"

@@ -48,6 +48,18 @@ struct CardTables {
   uint2 lut[kLutN];
 };
 
+// Index sort key (f1): 8-bit-normalized symbols (card < 256 shifted up), bits
+// interleaved most significant first -- bit 7 of segments 0..15, then bit 6, ...
+// down to bit 4: the iSAX tree's split order at uniform cardinality.
+__device__ __forceinline__ uint64_t isax_key16(const uint8_t* sym, int shift) {
+  uint64_t key = 0;
+#pragma unroll
+  for (int b = 7; b >= 4; --b)
+#pragma unroll
+    for (int s = 0; s < 16; ++s) key = (key << 1) | (uint64_t)(((sym[s] << shift) >> b) & 1u);
+  return key;
+}
+
 // Returns the device table for `card` (power of two in [2,256]) on the current
 // device, building all eight on first use.  nullptr + error set on failure.
 const CardTables* device_tables(int card);

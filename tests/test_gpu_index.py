@@ -1,0 +1,110 @@
+"""f1 index (paris_index_build / paris_knn_index) through the C ABI vs independent definitions:
+the interleaved iSAX key computed here in numpy from the oracle's SAX words, the sort order
+(key, id), the block envelopes, and exact k-NN against the oracle's brute force."""
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+from tests._parity import check_knn
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import __graft_entry__ as ge
+    ge.build()
+    import paper_2009_00166_b200 as p
+    return p
+
+
+def _keys(words_nw, card):
+    """Definition (include/paris.h): bits 7..4 of the 8-bit-scaled symbols, interleaved
+    most significant first over segments 0..15."""
+    shift = 8 - int(np.log2(card))
+    sym = (words_nw.astype(np.uint64) << np.uint64(shift)) & np.uint64(0xFF)
+    key = np.zeros(words_nw.shape[0], dtype=np.uint64)
+    for b in range(7, 3, -1):
+        for s in range(16):
+            key = (key << np.uint64(1)) | ((sym[:, s] >> np.uint64(b)) & np.uint64(1))
+    return key
+
+
+@pytest.mark.parametrize("n,card", [(16, 256), (2048, 256), (5000 * 16, 256), (4096 + 48, 64), (3000 * 16, 8)])
+def test_index_build_matches_definition(P, n, card):
+    import torch
+    x = datagen.random_walks(n, 256, 300 + n)
+    xd = torch.from_numpy(x).cuda()
+    sax = P.summarize(xd, 16, card)
+    idx = P.index_build(sax, 16, card)
+    words = sax.cpu().numpy().T.copy()                  # [n][16] (GPU SAX is parity-tested elsewhere)
+    keys = _keys(words, card)
+    order = np.lexsort((np.arange(n), keys))            # by (key, id)
+    perm = idx.perm.cpu().numpy().astype(np.int64)
+    np.testing.assert_array_equal(perm, order)
+    np.testing.assert_array_equal(idx.sax_sorted.cpu().numpy(), sax.cpu().numpy()[:, perm])
+    env = idx.env.cpu().numpy()
+    ss = words[perm]
+    for blk in range(env.shape[0]):
+        seg = ss[blk * 128:(blk + 1) * 128]
+        np.testing.assert_array_equal(env[blk, 0], seg.min(0))
+        np.testing.assert_array_equal(env[blk, 1], seg.max(0))
+
+
+@pytest.mark.parametrize("n,nq,k", [(2048, 3, 1), (40_000, 16, 1), (40_000, 5, 10), (100_000, 21, 1),
+                                    (100_000, 9, 100), (6000 * 16, 1, 1)])
+def test_knn_index_parity(P, n, nq, k):
+    import torch
+    x = datagen.random_walks(n, 256, 500 + n)
+    q = datagen.random_walks(nq, 256, 501 + nq)
+    q[0] = x[n // 3]                                    # member query: distance 0
+    xd = torch.from_numpy(x).cuda()
+    sax = P.summarize(xd, 16, 256)
+    idx = P.index_build(sax, 16, 256)
+    gi, gd = P.knn_index(xd, idx, torch.from_numpy(q).cuda(), k=k)
+    ri, rd2 = oracle.knn_bruteforce(x, q, k)
+    check_knn(x, q, gi.cpu().numpy(), gd.cpu().numpy(), ri, rd2)
+    assert gi[0, 0].item() == n // 3 and gd[0, 0].item() == 0.0
+
+
+def test_knn_index_noisy_members_and_ties(P):
+    import torch
+    n = 60_000
+    x = datagen.random_walks(n, 256, 77)
+    x[1000] = x[10]
+    x[59_999] = x[10]
+    src = datagen.member_ids(12, n, 78)
+    q = datagen.noisy_members(x, src, 0.05, 78)
+    q[0] = x[10]
+    xd = torch.from_numpy(x).cuda()
+    sax = P.summarize(xd, 16, 256)
+    idx = P.index_build(sax, 16, 256)
+    for k in (1, 3, 50):
+        gi, gd = P.knn_index(xd, idx, torch.from_numpy(q).cuda(), k=k)
+        ri, rd2 = oracle.knn_bruteforce(x, q, k)
+        check_knn(x, q, gi.cpu().numpy(), gd.cpu().numpy(), ri, rd2)
+    gi, _ = P.knn_index(xd, idx, torch.from_numpy(q[:1]).cuda(), k=3)
+    assert sorted(gi[0].tolist()) == [10, 1000, 59_999]
+
+
+def test_knn_index_same_as_flat(P):
+    """Index and flat scans return the same rows (both exact)."""
+    import torch
+    n = 80_000
+    x = datagen.random_walks(n, 128, 91)
+    q = datagen.random_walks(16, 128, 92)
+    xd = torch.from_numpy(x).cuda()
+    qd = torch.from_numpy(q).cuda()
+    sax = P.summarize(xd, 16, 256)
+    idx = P.index_build(sax, 16, 256)
+    a_i, a_d = P.knn_exact(xd, sax, qd, k=5)
+    b_i, b_d = P.knn_index(xd, idx, qd, k=5)
+    np.testing.assert_allclose(a_d.cpu().numpy(), b_d.cpu().numpy(), rtol=1e-6)
+
+
+def test_index_rejects_bad_shapes(P):
+    import torch
+    sax = torch.zeros((16, 20), dtype=torch.uint8, device="cuda")
+    with pytest.raises(P.ParisError):
+        P.index_build(sax, 16, 256)   # n % 16 != 0
