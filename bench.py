@@ -226,7 +226,7 @@ def run_gpu(args):
     torch.cuda.synchronize()
     log(f"rank {rank}: generated n={n} len={length} nq={nq} in {time.time() - t0:.1f}s")
     st = torch.cuda.current_stream()
-    kcfg = P.KnnConfig(batch=batch)
+    kcfg = P.KnnConfig(batch=batch, index_group1=bool(args.group1), index_seeds=args.index_seeds)
 
     # ---- summarize (rows a1-a2): warmup + timed
     for _ in range(args.warmup):
@@ -240,7 +240,24 @@ def run_gpu(args):
     torch.cuda.synchronize()
     sum_ms = e0.elapsed_time(e1) / args.steps
 
-    # ---- query step = every query of the config through paris_knn_exact (calls of call_q)
+    # ---- index (f1): iSAX-ordered SAX + block envelopes, built once (timed on its own)
+    index = None
+    index_ms = None
+    if args.path == "index":
+        index = P.index_build(sax, W, CARD)
+        torch.cuda.synchronize()
+        e0.record(st)
+        index = P.index_build(sax, W, CARD)
+        e1.record(st)
+        torch.cuda.synchronize()
+        index_ms = e0.elapsed_time(e1)
+
+    def knn(qsrc, **kw):
+        if index is not None:
+            return P.knn_index(raw, index, qsrc, k=k, **kw)
+        return P.knn_exact(raw, sax, qsrc, k=k, w=W, card=CARD, **kw)
+
+    # ---- query step = every query of the config through one ABI call per call_q queries
     out_idx = torch.empty((nq, k), dtype=torch.int64, device=dev)
     out_dist = torch.empty((nq, k), dtype=torch.float32, device=dev)
 
@@ -248,11 +265,9 @@ def run_gpu(args):
         cfg_ = cfg_ or kcfg
         for c0 in range(0, nq, call_q):
             c1 = min(nq, c0 + call_q)
-            P.knn_exact(raw, sax, qsrc[c0:c1], k=k, w=W, card=CARD, out_idx=oi[c0:c1], out_dist=od[c0:c1],
-                        config=cfg_)
+            knn(qsrc[c0:c1], out_idx=oi[c0:c1], out_dist=od[c0:c1], config=cfg_)
 
-    _, _, stats = P.knn_exact(raw, sax, queries, k=k, w=W, card=CARD, out_idx=out_idx,
-                              out_dist=out_dist, config=kcfg, stats=True)
+    _, _, stats = knn(queries, out_idx=out_idx, out_dist=out_dist, config=kcfg, stats=True)
     for _ in range(max(0, args.warmup - 1)):
         step(queries, out_idx, out_dist)
     torch.cuda.synchronize()
@@ -328,7 +343,21 @@ def run_gpu(args):
     roof = None
     if dom:
         per_launch_ms = kern[dom]["ms_per_step"] * args.steps / prof[dom][0]
-        if dom == "lb_pass" and q_per_pass > 1.5:
+        if dom == "lb_pass" and index is not None:
+            # index path: the algorithmic work is the (block, query) pairs whose envelope bound
+            # passed (stats lb_blocks) x 128 series x w segments x 3 FMA-pipe half-ops
+            blocks = stats["lb_blocks"].numpy().astype(np.float64).sum()
+            ops = 3.0 * W * P.PARIS_INDEX_BLOCK * blocks / nbatches
+            ach = ops / (per_launch_ms / 1e3) / 1e12
+            pk = 148 * 64 * 2 * ALU_CLOCK_GHZ * 1e9 / 1e12
+            roof = {"kernel": dom, "bound": "alu", "achieved": ach, "peak": pk, "unit": "Tops/s (fp16x2 half-ops)",
+                    "frac": ach / pk, "traffic": ncu_traffic(dom, args.config),
+                    "algorithmic_ops_per_launch": ops, "launch_ms": per_launch_ms,
+                    "peak_source": f"derived: 148 SM x 64 FMA lanes/clk x 2 (f16x2) x {ALU_CLOCK_GHZ} GHz",
+                    "active_block_frac": blocks / (nq * (n / P.PARIS_INDEX_BLOCK)),
+                    "hbm_achieved_gbs": alg[dom] / (per_launch_ms / 1e3) / 1e9, "hbm_peak_gbs": peak,
+                    "queries_per_pass": q_per_pass}
+        elif dom == "lb_pass" and q_per_pass > 1.5:
             # batched fp16x2 LB: bound by the FMA pipe, not HBM: 3 half-precision
             # FMA-pipe ops per (series, segment, query); peak = 148 SMs x 64 lanes/clk x 2 halves
             # x sm clock (B300_MICROARCH.md: FFMA/HFMA2 reciprocal throughput 2 per SMSP).
@@ -352,11 +381,11 @@ def run_gpu(args):
     if not args.no_b1:
         nq1 = min(nq, 8)
         cfg1 = P.KnnConfig(batch=1)
-        P.knn_exact(raw, sax, queries[:nq1], k=k, w=W, card=CARD, config=cfg1)
+        knn(queries[:nq1], config=cfg1)
         torch.cuda.synchronize()
         P.profile_reset()
         P.profile_enable(True)
-        _, _, st1 = P.knn_exact(raw, sax, queries[:nq1], k=k, w=W, card=CARD, config=cfg1, stats=True)
+        _, _, st1 = knn(queries[:nq1], config=cfg1, stats=True)
         P.profile_enable(False)
         pr1 = P.profile_read()
         if "lb_pass" in pr1:
@@ -394,7 +423,7 @@ def run_gpu(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded Philox random walks, z-normalized; no dataset on the box)",
             "config": {"workload": cfg["desc"], "n": n, "len": length, "w": W, "card": CARD, "nq": nq, "k": k,
-                       "batch": batch, "parallelism": f"weak x{ws} (independent collections + queries per GPU)",
+                       "batch": batch, "path": args.path, "index_build_ms": index_ms, "parallelism": f"weak x{ws} (independent collections + queries per GPU)",
                        "l2": "inputs larger than L2 (no flush)"},
             "roofline": roof,
             "lb_batch1": lb1,
@@ -425,6 +454,11 @@ def main():
     ap.add_argument("--config", type=int, default=4, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="paris", choices=["paris", "reference"])
     ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--group1", type=int, default=0, help="index path: skip granularity one query pair")
+    ap.add_argument("--index-seeds", type=int, default=0, help="index path: seed series around the leaf")
+    ap.add_argument("--path", default="flat", choices=["flat", "index"],
+                    help="flat: paris_knn_exact over the SAX array (ParIS+ Alg9); index: paris_knn_index over "
+                         "the iSAX-ordered array with block envelopes (SURVEY f1)")
     ap.add_argument("--n", type=int, default=0, help="override n (debug only)")
     ap.add_argument("--nq", type=int, default=0, help="override query count (debug only)")
     ap.add_argument("--no-cpu", action="store_true")

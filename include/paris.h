@@ -114,7 +114,9 @@ typedef struct paris_knn_config {
   int32_t batch;        /* queries per SAX pass (1..16); default 16 */
   int32_t seed_div;     /* seed sample = n / seed_div series (default 16) */
   int32_t wave_a;       /* k = 1: candidates per query refined in the first (lowest-LB) wave; default 2048 */
-  int32_t reserved[5];  /* reserved[0] = 1: test hook forcing the direct-load LB kernels */
+  int32_t reserved[5];  /* tuning/test hooks: [0] = 1 forces the direct-load LB kernels;
+                           [1] = 1 index mode skips per query pair (default: per 2 pairs);
+                           [2] index mode seed series around the leaf (0 = 4096) */
 } paris_knn_config;
 
 /* Per-query counters (host memory, arrays of nq), filled by paris_knn_exact_ex. */
@@ -122,6 +124,8 @@ typedef struct paris_knn_stats {
   int64_t* candidates;  /* series whose LB passed tau_seed (Alg10 list length)       */
   int64_t* refined;     /* raw series read and distance computed (Alg11 line al9:rcal) */
   float* tau_seed;      /* seed BSF distance (rooted)                                 */
+  int64_t* lb_blocks;   /* index mode: PARIS_INDEX_BLOCK-series blocks whose envelope
+                           bound passed (their series' LBs were computed); 0 otherwise */
 } paris_knn_stats;
 
 /* Same as paris_knn_exact with tunables and optional stats (either may be NULL). */
@@ -155,7 +159,7 @@ int paris_knn_index_ex(const float* raw, const uint8_t* sax_sorted, const uint32
 const char* paris_last_error(void);
 
 /* ABI version (major*100 + minor). */
-int32_t paris_version(void);
+int32_t paris_version(void);  /* 101: paris_knn_stats.lb_blocks, index API */
 
 /* Test hook: the library's own fp64 breakpoints cut_1..cut_{card-1} (R2) into
  * out[0..card-2] (host memory).  PARIS_ECONFIG for a bad card. */

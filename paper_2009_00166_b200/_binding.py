@@ -37,7 +37,7 @@ class _Config(ctypes.Structure):
 
 class _Stats(ctypes.Structure):
     _fields_ = [("candidates", ctypes.c_void_p), ("refined", ctypes.c_void_p),
-                ("tau_seed", ctypes.c_void_p)]
+                ("tau_seed", ctypes.c_void_p), ("lb_blocks", ctypes.c_void_p)]
 
 
 class _KProf(ctypes.Structure):
@@ -51,6 +51,8 @@ class KnnConfig:
     seed_div: int = 0   # seed sample = n / seed_div (0 = 16)
     wave_a: int = 0     # k = 1: first refinement wave per query (0 = 2048)
     force_direct: bool = False  # test hook: use the direct-load LB kernels even where the TMA-tiled ones apply
+    index_group1: bool = False  # index mode: skip block work per query pair (default per 2 pairs)
+    index_seeds: int = 0        # index mode: seed series around the query's leaf (0 = 4096)
 
 
 def library_path() -> str:
@@ -219,12 +221,14 @@ def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: in
     if config is not None:
         cfg = _Config(config.batch, config.seed_div, config.wave_a)
         cfg.reserved[0] = 1 if config.force_direct else 0
+        cfg.reserved[1] = 1 if config.index_group1 else 0
+        cfg.reserved[2] = int(config.index_seeds)
     st = None
     arrays = None
     if stats:
         arrays = (torch.zeros(nq, dtype=torch.int64), torch.zeros(nq, dtype=torch.int64),
-                  torch.zeros(nq, dtype=torch.float32))
-        st = _Stats(arrays[0].data_ptr(), arrays[1].data_ptr(), arrays[2].data_ptr())
+                  torch.zeros(nq, dtype=torch.float32), torch.zeros(nq, dtype=torch.int64))
+        st = _Stats(arrays[0].data_ptr(), arrays[1].data_ptr(), arrays[2].data_ptr(), arrays[3].data_ptr())
     if _index is None:
         rc = lib.paris_knn_exact_ex(raw.data_ptr(), sax.data_ptr(), n, queries.data_ptr(), nq, k,
                                     out_idx.data_ptr(), out_dist.data_ptr(), length, w, card,
@@ -238,7 +242,7 @@ def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: in
     _check(rc)
     if stats:
         return out_idx, out_dist, {"candidates": arrays[0], "refined": arrays[1],
-                                   "tau_seed": arrays[2]}
+                                   "tau_seed": arrays[2], "lb_blocks": arrays[3]}
     return out_idx, out_dist
 
 

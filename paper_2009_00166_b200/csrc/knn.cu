@@ -519,6 +519,8 @@ struct LbArgs {
   int64_t cap;
   const uint32_t* perm;  // index mode: sorted position -> series id (else nullptr)
   const uint8_t* env;    // index mode: [n/128 blocks][2][16] min/max symbols (else nullptr)
+  int group1;            // index mode: skip granularity 1 query pair (else 2 pairs)
+  unsigned* blocks;      // index mode: per query, blocks whose envelope bound passed
 };
 
 struct LbConsts {
@@ -619,9 +621,10 @@ __device__ __forceinline__ void lb_emit(const uint32_t (&acc)[4][P], int64_t i0,
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       if (m & (1u << j)) {
-        if (pos < (uint64_t)a.cap)
+        if (pos < (uint64_t)a.cap) {
           a.cand[(size_t)b * a.cap + pos] = make_key(lbv[j], perm ? __ldg(perm + i0 + j) : (uint32_t)(i0 + j));
-        atomicAdd(&a.hist[b * kNB + lb_bin(lbv[j], sc)], 1u);
+          atomicAdd(&a.hist[b * kNB + lb_bin(lbv[j], sc)], 1u);
+        }
         ++pos;
       }
     }
@@ -657,8 +660,12 @@ __device__ void wb_flush(WarpBuf& wb, int nslots, const LbConsts& c, const LbArg
     const int b = wb.slot[e];
     const uint64_t key = wb.key[e];
     const unsigned pos = atomicAdd(&wb.cur[b], 1u);
-    if ((int64_t)pos < a.cap) a.cand[(size_t)b * a.cap + pos] = key;
-    atomicAdd(&s_hist[b * kNB + lb_bin(key_val(key), c.scale[b])], 1u);
+    // only stored candidates enter the histogram: on overflow (count > cap) the
+    // bucket offsets must describe exactly the `cap` entries K5 orders
+    if ((int64_t)pos < a.cap) {
+      a.cand[(size_t)b * a.cap + pos] = key;
+      atomicAdd(&s_hist[b * kNB + lb_bin(key_val(key), c.scale[b])], 1u);
+    }
   }
   __syncwarp();
   if (lane == 0) wb.n = 0;
@@ -926,10 +933,12 @@ k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
   __shared__ unsigned s_hist[MODE >= 1 ? kMaxB * kNB : 1];
   __shared__ float2 s_lu[MODE == 2 ? kMaxCard : 1];
   __shared__ float2 s_qf[MODE == 2 ? 2 * PP * kMaxW : 1];
+  __shared__ unsigned s_blk[kMaxB];
   const int tid = threadIdx.x, lane = tid & 31;
   const int64_t ntiles = (nlim + kTS - 1) / kTS;
   const int nslots = P > 0 ? 2 * P : 1;
   WarpBuf& wb = s_wb[MODE >= 1 ? (tid >> 5) : 0];
+  if (tid < kMaxB) s_blk[tid] = 0;
   if (MODE == 2) {
     for (int i = tid; i < kMaxCard; i += kTThreads) s_lu[i] = a.tab->lu[i];
     for (int i = tid; i < 2 * PP * kMaxW; i += kTThreads) s_qf[i] = a.g_q[i];
@@ -996,10 +1005,15 @@ k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
 #pragma unroll
       for (int p = 0; p < PP; ++p) acc[j][p] = 0u;
     uint32_t bm = 0xFFFFFFFFu;
-    if (MODE == 2) bm = block_mask(a.env, (tile * kTS) / PARIS_INDEX_BLOCK + (tid >> 5), nslots, s_qf, s_lu, s_c,
-                                   a.seglen_f);
+    if (MODE == 2) {
+      const int64_t blk = (tile * kTS) / PARIS_INDEX_BLOCK + (tid >> 5);
+      // a ragged last tile: warps past the end have no block (and no envelope)
+      bm = ((int64_t)blk * PARIS_INDEX_BLOCK < nlim) ? block_mask(a.env, blk, nslots, s_qf, s_lu, s_c, a.seglen_f) : 0u;
+      if (lane < nslots && ((bm >> lane) & 1u)) atomicAdd(&s_blk[lane], 1u);
+    }
     if (MODE == 2 && P > 0) {
-      lbt_group<PP, 0, (PP < 2 ? PP : 2)>(bm, rows, tid, tabl, s_q16, acc);
+      if (a.group1) lbt_group<PP, 0, 1>(bm, rows, tid, tabl, s_q16, acc);
+      else lbt_group<PP, 0, (PP < 2 ? PP : 2)>(bm, rows, tid, tabl, s_q16, acc);
     } else if (MODE == 2 && bm == 0) {
       // single query, block pruned: nothing to compute
     } else if (P > 0) {
@@ -1048,6 +1062,7 @@ k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
   if (MODE >= 1) {
     wb_flush(wb, nslots, s_c, a, s_hist);
     __syncthreads();
+    if (MODE == 2 && tid < nslots && s_blk[tid]) atomicAdd(&a.blocks[tid], s_blk[tid]);
     for (int i = tid; i < nslots * kNB; i += kTThreads)
       if (s_hist[i]) atomicAdd(&a.hist[i], s_hist[i]);
   }
@@ -1419,7 +1434,8 @@ k_refine_topk(RefineArgs a) {
 __global__ void k_finalize1(const unsigned long long* __restrict__ best, int nb, int q0,
                             int64_t* __restrict__ out_idx, float* __restrict__ out_dist,
                             const unsigned* __restrict__ count, const unsigned* __restrict__ refined,
-                            unsigned* __restrict__ all_count, unsigned* __restrict__ all_refined, int accum) {
+                            unsigned* __restrict__ all_count, unsigned* __restrict__ all_refined, int accum,
+                            const unsigned* __restrict__ blocks, unsigned* __restrict__ all_blocks) {
   const int b = threadIdx.x;
   if (b >= nb) return;
   const uint64_t key = best[b * kPadU64];
@@ -1427,6 +1443,7 @@ __global__ void k_finalize1(const unsigned long long* __restrict__ best, int nb,
   else { out_idx[q0 + b] = (int64_t)key_id(key); out_dist[q0 + b] = sqrtf(key_val(key)); }
   all_count[q0 + b] = (accum ? all_count[q0 + b] : 0u) + count[b];
   all_refined[q0 + b] = (accum ? all_refined[q0 + b] : 0u) + refined[b];
+  all_blocks[q0 + b] = (accum ? all_blocks[q0 + b] : 0u) + blocks[b];
 }
 
 // Merge the per-CTA top-k lists: repeatedly sort [current top-k | next chunk]
@@ -1435,7 +1452,8 @@ __global__ void __launch_bounds__(1024)
 k_finalize(const uint64_t* __restrict__ lists, int nslots, int k, int q0,
            int64_t* __restrict__ out_idx, float* __restrict__ out_dist,
            const unsigned* __restrict__ count, const unsigned* __restrict__ refined,
-           unsigned* __restrict__ all_count, unsigned* __restrict__ all_refined, int accum) {
+           unsigned* __restrict__ all_count, unsigned* __restrict__ all_refined, int accum,
+           const unsigned* __restrict__ blocks, unsigned* __restrict__ all_blocks) {
   __shared__ uint64_t buf[kSortP];
   const int b = blockIdx.x;
   const int64_t total = (int64_t)nslots * k;
@@ -1458,6 +1476,7 @@ k_finalize(const uint64_t* __restrict__ lists, int nslots, int k, int q0,
   if (threadIdx.x == 0) {
     all_count[q0 + b] = (accum ? all_count[q0 + b] : 0u) + count[b];
     all_refined[q0 + b] = (accum ? all_refined[q0 + b] : 0u) + refined[b];
+    all_blocks[q0 + b] = (accum ? all_blocks[q0 + b] : 0u) + blocks[b];
   }
 }
 
@@ -1493,6 +1512,7 @@ struct Ws {
   unsigned* hist;
   unsigned* cursor;
   unsigned* refined;
+  unsigned* blocks;      // index mode: blocks whose envelope bound passed, per query
   size_t zero_bytes;
   unsigned long long* best;
   uint64_t* cand;
@@ -1515,6 +1535,8 @@ struct Plan {
   bool tiled;     // TMA-tiled LB kernels (n % 16 == 0, w == 16)
   const uint32_t* perm;  // index mode (paris_knn_index): sorted position -> id
   const uint8_t* env;    // index mode: block envelopes
+  int group1;            // index mode: per-pair skip granularity (test/tuning hook)
+  int idx_seeds;         // index mode: series around the query's leaf
 };
 
 int pairs_for(int nb) { return nb <= 2 ? 1 : nb <= 4 ? 2 : nb <= 8 ? 4 : 8; }
@@ -1537,7 +1559,8 @@ cudaError_t launch_lb(const Plan& p, const uint8_t* sax, int nb, const CardTable
   LbArgs la;
   la.sax = sax; la.n = p.n; la.w = p.w; la.seglen_f = (float)(p.len / p.w); la.tab = tab;
   la.g_q = ws.g_q; la.g_q16 = ws.g_q16; la.nb = nb; la.thr = ws.thr_seed; la.count = ws.count;
-  la.hist = ws.hist; la.cand = ws.cand; la.cap = cap; la.perm = nullptr; la.env = nullptr;
+  la.hist = ws.hist; la.cand = ws.cand; la.cap = cap; la.perm = nullptr; la.env = nullptr; la.group1 = 0;
+  la.blocks = ws.blocks;
   return PARIS_LAUNCH("lb_pass", (k_lb<P, WT, AL>), grid, kLBThreads, 0, st, la);
 }
 
@@ -1583,7 +1606,8 @@ cudaError_t launch_lbt(const Plan& p, const uint8_t* sax, int nb, const CardTabl
   LbArgs la;
   la.sax = sax; la.n = p.n; la.w = p.w; la.seglen_f = (float)(p.len / p.w); la.tab = tab;
   la.g_q = ws.g_q; la.g_q16 = ws.g_q16; la.nb = nb; la.thr = ws.thr_seed; la.count = ws.count;
-  la.hist = ws.hist; la.cand = ws.cand; la.cap = cap; la.perm = p.perm; la.env = p.env;
+  la.hist = ws.hist; la.cand = ws.cand; la.cap = cap; la.perm = p.perm; la.env = p.env; la.group1 = p.group1;
+  la.blocks = ws.blocks;
   return PARIS_LAUNCH(MODE ? "lb_pass" : "seed_lb", (k_lbt<P, MODE>), grid, kTThreads, kTSmem, st, la, nlim,
                       ws.seed_ids, p.S);
 }
@@ -1627,7 +1651,7 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   const size_t o_q16 = take(sizeof(uint2) * (B / 2) * kMaxW);
   const size_t o_sid = take(sizeof(int) * B * p.S);
   const size_t o_skey = take(sizeof(uint64_t) * B * p.S);
-  const size_t zb = sizeof(unsigned) * (B + B + B * kNB + B * kNB + B);
+  const size_t zb = sizeof(unsigned) * (B + B + B * kNB + B * kNB + B + B);
   const size_t o_zero = take(zb);
   const size_t o_best = take(sizeof(unsigned long long) * B * kPadU64);
   const size_t o_thr = take(sizeof(unsigned) * B * kPadU32);
@@ -1655,6 +1679,7 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   ws.hist = ws.count + B;
   ws.cursor = ws.hist + B * kNB;
   ws.refined = ws.cursor + B * kNB;
+  ws.blocks = ws.refined + B;
   ws.best = (unsigned long long*)(c + o_best);
   ws.cand = (uint64_t*)(c + o_cand);
   ws.sorted = (uint64_t*)(c + o_sorted);
@@ -1665,8 +1690,8 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
 // One batch of nb <= kMaxB queries (device pointers).  Outputs at [q0 .. q0+nb).
 int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* qbatch, int nb, int q0,
               int64_t cap, const CardTables* tab, const Ws& ws, int64_t* d_idx, float* d_dist,
-              unsigned* all_count, unsigned* all_refined, float* all_tau, cudaStream_t st,
-              bool rescan = false) {
+              unsigned* all_count, unsigned* all_refined, float* all_tau, unsigned* all_blocks,
+              cudaStream_t st, bool rescan = false) {
   const int P = pairs_for(nb);
   cudaError_t e = cudaMemsetAsync(ws.zero_block, 0, ws.zero_bytes, st);
   if (e != cudaSuccess) return cuda_error(e, "memset scratch");
@@ -1739,7 +1764,8 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
     }
     PARIS_CHECK_LAUNCH(e1, "refine launch");
     PARIS_CHECK_LAUNCH(PARIS_LAUNCH("finalize", k_finalize1, 1, 32, 0, st, ws.best, nb, q0, d_idx, d_dist,
-                                    ws.count, ws.refined, all_count, all_refined, rescan ? 1 : 0),
+                                    ws.count, ws.refined, all_count, all_refined, rescan ? 1 : 0,
+                                    ws.blocks, all_blocks),
                        "finalize launch");
   } else {
     const size_t rsmem = (size_t)p.len * 4 + (size_t)p.k * 16;
@@ -1769,7 +1795,8 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
       }
     }
     PARIS_CHECK_LAUNCH(PARIS_LAUNCH("finalize", k_finalize, nb, 1024, 0, st, ws.lists, p.XB, p.k, q0,
-                                    d_idx, d_dist, ws.count, ws.refined, all_count, all_refined, rescan ? 1 : 0),
+                                    d_idx, d_dist, ws.count, ws.refined, all_count, all_refined, rescan ? 1 : 0,
+                                    ws.blocks, all_blocks),
                        "finalize launch");
   }
   return PARIS_OK;
@@ -1782,13 +1809,13 @@ bool is_host_ptr(const void* p) {
   return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered;
 }
 
-constexpr int kIdxSeeds = 1024;  // index mode: series around the query's leaf
+constexpr int kIdxSeeds = 4096;  // index mode: series around the query's leaf (default)
 
 void plan_seed(Plan& p, int seed_div) {
   if (p.perm) {
     p.ns = 0;
     p.seed_grid = 0;
-    p.S = kIdxSeeds;
+    p.S = std::max(p.k, std::min(kMaxSeed, p.idx_seeds > 0 ? p.idx_seeds : kIdxSeeds));
     return;
   }
   p.ns = std::min<int64_t>(p.n, std::max<int64_t>(p.n / seed_div, std::min<int64_t>(p.n, 65536)));
@@ -1850,6 +1877,8 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   p.tiled = (n % 16 == 0) && (w == kTW) && (indexed || !(cfg && cfg->reserved[0] == 1));
   p.perm = perm;
   p.env = env;
+  p.group1 = (cfg && cfg->reserved[1] == 1) ? 1 : 0;
+  p.idx_seeds = cfg ? cfg->reserved[2] : 0;
   plan_seed(p, (cfg && cfg->seed_div > 0) ? cfg->seed_div : 16);
   p.cap = std::min<int64_t>(n, std::max<int64_t>(65536, n / 32));
   plan_refine(p);
@@ -1864,7 +1893,7 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   cudaError_t e;
   char* stage = nullptr;
   const size_t qbytes = (size_t)nq * len * 4, ibytes = (size_t)nq * k * 8, dbytes = (size_t)nq * k * 4;
-  const size_t cbytes = (size_t)nq * 4 * 3;
+  const size_t cbytes = (size_t)nq * 4 * 4;
   e = cudaMallocAsync((void**)&stage, qbytes + ibytes + dbytes + cbytes + 1024, st);
   if (e != cudaSuccess) { cudaGetLastError(); set_error("paris_knn_exact: staging alloc failed"); return PARIS_ENOMEM; }
   const float* d_q = queries;
@@ -1877,6 +1906,7 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   unsigned* all_count = (unsigned*)cur;
   unsigned* all_refined = all_count + nq;
   float* all_tau = (float*)(all_refined + nq);
+  unsigned* all_blocks = (unsigned*)(all_tau + nq);
   if (hq) {
     e = cudaMemcpyAsync(sq, queries, qbytes, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) { cudaFreeAsync(stage, st); return cuda_error(e, "H2D queries"); }
@@ -1896,10 +1926,10 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   for (int q0 = 0; q0 < nq && rc == PARIS_OK; q0 += p.B) {
     const int nb = std::min(p.B, nq - q0);
     rc = run_batch(p, raw, sax, d_q + (size_t)q0 * len, nb, q0, p.cap, tab, ws, d_idx, d_dist,
-                   all_count, all_refined, all_tau, st);
+                   all_count, all_refined, all_tau, all_blocks, st);
   }
   // overflow check: one synchronization per call
-  std::vector<unsigned> h_count(nq), h_ref(nq);
+  std::vector<unsigned> h_count(nq), h_ref(nq), h_blk(nq);
   std::vector<float> h_tau(nq);
   if (rc == PARIS_OK) {
     e = cudaMemcpyAsync(h_count.data(), all_count, (size_t)nq * 4, cudaMemcpyDeviceToHost, st);
@@ -1919,7 +1949,7 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
       rc = alloc_ws(p1, p1.cap, ws1, st);
       if (rc) break;
       rc = run_batch(p1, raw, sax, d_q + (size_t)q * len, 1, q, p1.cap, tab, ws1, d_idx, d_dist,
-                     all_count, all_refined, all_tau, st, /*rescan=*/true);
+                     all_count, all_refined, all_tau, all_blocks, st, /*rescan=*/true);
       cudaFreeAsync(ws1.base, st);
     }
   }
@@ -1931,6 +1961,7 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
       e = cudaMemcpyAsync(h_count.data(), all_count, (size_t)nq * 4, cudaMemcpyDeviceToHost, st);
       if (e == cudaSuccess) e = cudaMemcpyAsync(h_ref.data(), all_refined, (size_t)nq * 4, cudaMemcpyDeviceToHost, st);
       if (e == cudaSuccess) e = cudaMemcpyAsync(h_tau.data(), all_tau, (size_t)nq * 4, cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(h_blk.data(), all_blocks, (size_t)nq * 4, cudaMemcpyDeviceToHost, st);
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) rc = cuda_error(e, "paris_knn_exact D2H");
@@ -1939,6 +1970,7 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
         if (stats->candidates) stats->candidates[q] = h_count[q];
         if (stats->refined) stats->refined[q] = h_ref[q];
         if (stats->tau_seed) stats->tau_seed[q] = h_tau[q];
+        if (stats->lb_blocks) stats->lb_blocks[q] = h_blk[q];
       }
     }
   }

@@ -108,3 +108,21 @@ def test_index_rejects_bad_shapes(P):
     sax = torch.zeros((16, 20), dtype=torch.uint8, device="cuda")
     with pytest.raises(P.ParisError):
         P.index_build(sax, 16, 256)   # n % 16 != 0
+
+
+def test_knn_index_overflow_rescan(P):
+    """A one-series seed and all-zero queries flood the candidate buffer (count > cap): the
+    first pass refines only the stored candidates, the re-scan starts from its result."""
+    import torch
+    n = 100_000 - 96
+    x = datagen.random_walks(n, 128, 41)
+    q = np.zeros((3, 128), dtype=np.float32)
+    q[1] = x[5]
+    xd = torch.from_numpy(x).cuda()
+    sax = P.summarize(xd, 16, 256)
+    idx = P.index_build(sax, 16, 256)
+    for k in (1, 1000):
+        gi, gd, st = P.knn_index(xd, idx, torch.from_numpy(q).cuda(), k=k,
+                                 config=P.KnnConfig(index_seeds=1), stats=True)
+        ri, rd2 = oracle.knn_bruteforce(x, q, k)
+        check_knn(x, q, gi.cpu().numpy(), gd.cpu().numpy(), ri, rd2)
