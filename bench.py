@@ -226,7 +226,7 @@ def run_gpu(args):
     torch.cuda.synchronize()
     log(f"rank {rank}: generated n={n} len={length} nq={nq} in {time.time() - t0:.1f}s")
     st = torch.cuda.current_stream()
-    kcfg = P.KnnConfig(batch=batch, index_group1=bool(args.group1), index_seeds=args.index_seeds)
+    kcfg = P.KnnConfig(batch=batch, index_seeds=args.index_seeds)
 
     # ---- summarize (rows a1-a2): warmup + timed
     for _ in range(args.warmup):
@@ -454,7 +454,6 @@ def main():
     ap.add_argument("--config", type=int, default=4, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="paris", choices=["paris", "reference"])
     ap.add_argument("--batch", type=int, default=0)
-    ap.add_argument("--group1", type=int, default=0, help="index path: skip granularity one query pair")
     ap.add_argument("--index-seeds", type=int, default=0, help="index path: seed series around the leaf")
     ap.add_argument("--path", default="flat", choices=["flat", "index"],
                     help="flat: paris_knn_exact over the SAX array (ParIS+ Alg9); index: paris_knn_index over "

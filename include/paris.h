@@ -41,6 +41,7 @@ extern "C" {
 
 #define PARIS_MAX_K 1024
 #define PARIS_INDEX_BLOCK 128 /* series per envelope block of the index (paris_index_build) */
+#define PARIS_INDEX_TILE 2048 /* series per tile of the index's tile-major sorted SAX array   */
 
 /*
  * paris_summarize -- ConvertToSAX over a whole collection (IndexBulkLoading,
@@ -98,7 +99,9 @@ int paris_knn_exact(const float* raw, const uint8_t* sax, int64_t n, const float
  * bits) at uniform cardinality: by the key interleaving bits 7..4 of
  * the 16 symbols (card < 256: symbols scaled to 8 bits), ties by id.
  *   sax            device [w][n] uint8 (paris_summarize)
- *   out_sax_sorted device [w][n] uint8: out_sax_sorted[s*n + j] = sax[s*n + perm[j]]
+ *   out_sax_sorted device [ceil(n/PARIS_INDEX_TILE)][w][PARIS_INDEX_TILE] uint8 (tile-major
+ *                  SoA; the last tile padded): the symbol of segment s of sorted series j
+ *                  is out_sax_sorted[(j/T)*w*T + s*T + j%T] = sax[s*n + perm[j]], T = PARIS_INDEX_TILE
  *   out_perm       device [n] uint32: series id at sorted position j
  *   out_env        device [ceil(n/PARIS_INDEX_BLOCK)][2][w] uint8: per block of
  *                  PARIS_INDEX_BLOCK consecutive sorted series, the min ([blk][0][s])
@@ -115,8 +118,7 @@ typedef struct paris_knn_config {
   int32_t seed_div;     /* seed sample = n / seed_div series (default 16) */
   int32_t wave_a;       /* k = 1: candidates per query refined in the first (lowest-LB) wave; default 2048 */
   int32_t reserved[5];  /* tuning/test hooks: [0] = 1 forces the direct-load LB kernels;
-                           [1] = 1 index mode skips per query pair (default: per 2 pairs);
-                           [2] index mode seed series around the leaf (0 = 4096) */
+                           [1] unused; [2] index mode: seed series around the leaf (0 = 4096) */
 } paris_knn_config;
 
 /* Per-query counters (host memory, arrays of nq), filled by paris_knn_exact_ex. */

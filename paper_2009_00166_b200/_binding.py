@@ -51,7 +51,6 @@ class KnnConfig:
     seed_div: int = 0   # seed sample = n / seed_div (0 = 16)
     wave_a: int = 0     # k = 1: first refinement wave per query (0 = 2048)
     force_direct: bool = False  # test hook: use the direct-load LB kernels even where the TMA-tiled ones apply
-    index_group1: bool = False  # index mode: skip block work per query pair (default per 2 pairs)
     index_seeds: int = 0        # index mode: seed series around the query's leaf (0 = 4096)
 
 
@@ -151,12 +150,13 @@ def summarize(raw: torch.Tensor, w: int = 16, card: int = 256, out: torch.Tensor
 
 
 PARIS_INDEX_BLOCK = 128
+PARIS_INDEX_TILE = 2048
 
 
 @dataclass
 class Index:
     """iSAX-ordered SAX array (paris_index_build): sorted SoA words, ids, block envelopes."""
-    sax_sorted: torch.Tensor   # uint8 [w][n]
+    sax_sorted: torch.Tensor   # uint8 [ceil(n/2048)][w][2048] tile-major (include/paris.h)
     perm: torch.Tensor         # int32 [n] (uint32 ids)
     env: torch.Tensor          # uint8 [ceil(n/128)][2][w]
     w: int
@@ -171,7 +171,8 @@ def index_build(sax: torch.Tensor, w: int = 16, card: int = 256, stream=None) ->
         raise ValueError("sax must be uint8 [w][n]")
     n = sax.shape[1]
     nblk = (n + PARIS_INDEX_BLOCK - 1) // PARIS_INDEX_BLOCK
-    out = torch.empty_like(sax)
+    ntile = (n + PARIS_INDEX_TILE - 1) // PARIS_INDEX_TILE
+    out = torch.zeros((ntile, w, PARIS_INDEX_TILE), dtype=torch.uint8, device=sax.device)
     perm = torch.empty(n, dtype=torch.int32, device=sax.device)
     env = torch.empty((nblk, 2, w), dtype=torch.uint8, device=sax.device)
     _check(lib.paris_index_build(sax.data_ptr(), n, w, card, out.data_ptr(), perm.data_ptr(), env.data_ptr(),
@@ -209,7 +210,7 @@ def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: in
     nq = queries.shape[0]
     if queries.shape[1] != length:
         raise ValueError("query length differs from series length")
-    if sax.dtype != torch.uint8 or sax.numel() != n * w:
+    if _index is None and (sax.dtype != torch.uint8 or sax.numel() != n * w):
         raise ValueError("sax must be uint8 [w][n]")
     dev = queries.device
     pin = (not queries.is_cuda) and torch.cuda.is_available()
@@ -221,7 +222,6 @@ def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: in
     if config is not None:
         cfg = _Config(config.batch, config.seed_div, config.wave_a)
         cfg.reserved[0] = 1 if config.force_direct else 0
-        cfg.reserved[1] = 1 if config.index_group1 else 0
         cfg.reserved[2] = int(config.index_seeds)
     st = None
     arrays = None

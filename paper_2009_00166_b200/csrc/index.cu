@@ -12,7 +12,12 @@
 //
 //   k_idx_aos    SoA [w][n] -> AoS [n][16] words + 64-bit keys + ids (smem transpose)
 //   (CUB radix sort of (key, id) pairs -- a library sort, off the query path)
-//   k_idx_gather sorted ids -> sorted SoA rows + block envelopes (smem transpose)
+//   k_idx_gather sorted ids -> tile-major sorted SAX + block envelopes (smem transpose)
+//
+// Layout of the sorted array: tile-major SoA, [ceil(n/PARIS_INDEX_TILE)][16][PARIS_INDEX_TILE]:
+// the 16 segment rows of 2048 consecutive sorted series are one contiguous 32 KB
+// range, so the query kernel streams a tile with ONE bulk copy (16 row copies of
+// 2 KB each capped the [w][n] layout's TMA ring near 2.7 TB/s).
 #include "runtime.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
@@ -77,12 +82,11 @@ k_idx_gather(const uint4* __restrict__ aos, const uint32_t* __restrict__ perm, i
     const int cnt = (int)imin64(kIdxTile, n - base);
     for (int t = threadIdx.x; t < kIdxW * (kIdxTile / 4); t += kIdxTile) {
       const int s = t / (kIdxTile / 4), c = t % (kIdxTile / 4);
-      const int64_t i = base + 4 * c;
+      const int64_t i = base + 4 * c;  // whole uint32 stays inside one index tile (2048 % 4 == 0)
       const uint32_t v = reinterpret_cast<const uint32_t*>(tile[s])[c];
-      if (i + 3 < n) *reinterpret_cast<uint32_t*>(sax_sorted + (size_t)s * n + i) = v;
-      else
-        for (int q = 0; q < 4; ++q)
-          if (i + q < n) sax_sorted[(size_t)s * n + i + q] = (uint8_t)(v >> (8 * q));
+      const int64_t T = i / PARIS_INDEX_TILE, r = i % PARIS_INDEX_TILE;
+      if (i < n)  // padding past n is left as is (never a candidate)
+        *reinterpret_cast<uint32_t*>(sax_sorted + (size_t)T * kIdxW * PARIS_INDEX_TILE + (size_t)s * PARIS_INDEX_TILE + r) = v;
     }
     // envelopes: one thread per (block in tile, segment)
     constexpr int kBlocks = kIdxTile / PARIS_INDEX_BLOCK;

@@ -475,7 +475,9 @@ k_approx_seed(const uint8_t* __restrict__ sax_sorted, const uint32_t* __restrict
     const int64_t pos = lo + step * (lane + 1) - 1;  // increasing in lane, all < hi
     uint8_t w2[16];
 #pragma unroll
-    for (int s = 0; s < 16; ++s) w2[s] = sax_sorted[(size_t)s * n + pos];
+    for (int s = 0; s < 16; ++s)  // tile-major sorted SAX (include/paris.h)
+      w2[s] = sax_sorted[(size_t)(pos / PARIS_INDEX_TILE) * 16 * PARIS_INDEX_TILE + (size_t)s * PARIS_INDEX_TILE +
+                         pos % PARIS_INDEX_TILE];
     const int c = __popc(__ballot_sync(0xffffffffu, isax_key16(w2, shift) < target));  // a prefix of lanes
     const int64_t nlo = lo + step * c;
     hi = (c < 32) ? lo + step * (c + 1) - 1 : hi;
@@ -519,7 +521,6 @@ struct LbArgs {
   int64_t cap;
   const uint32_t* perm;  // index mode: sorted position -> series id (else nullptr)
   const uint8_t* env;    // index mode: [n/128 blocks][2][16] min/max symbols (else nullptr)
-  int group1;            // index mode: skip granularity 1 query pair (else 2 pairs)
   unsigned* blocks;      // index mode: per query, blocks whose envelope bound passed
 };
 
@@ -569,17 +570,19 @@ __device__ void lb_consts_init(const LbArgs& a, int nslots, LbConsts* c) {
 // Candidate emission for 4 series i0..i0+3 (nvalid of them real) and 2P query
 // slots whose fp16 sums are acc[j][p] (slot 2p low half, 2p+1 high half).
 // Whole warp must call it (warp-aggregated atomics).
+// slot0: global query slot of local slot 0 (index mode computes one pair at a time)
 template <int P>
 __device__ __forceinline__ void lb_emit(const uint32_t (&acc)[4][P], int64_t i0, int nvalid,
                                         const LbConsts& c, const LbArgs& a,
-                                        uint32_t slot_mask = 0xFFFFFFFFu, const uint32_t* perm = nullptr) {
+                                        uint32_t slot_mask = 0xFFFFFFFFu, const uint32_t* perm = nullptr,
+                                        int slot0 = 0) {
   const int lane = threadIdx.x & 31;
   uint32_t qm = 0;
   if (nvalid > 0) {
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       const uint32_t mn = h2_min(h2_min(acc[0][p], acc[1][p]), h2_min(acc[2][p], acc[3][p]));
-      qm |= h2_le_bits(mn, c.T16[p]) << (2 * p);
+      qm |= h2_le_bits(mn, c.T16[p + (slot0 >> 1)]) << (2 * p);
     }
     qm &= slot_mask;
   }
@@ -591,7 +594,7 @@ __device__ __forceinline__ void lb_emit(const uint32_t (&acc)[4][P], int64_t i0,
     unsigned m = 0;
     float lbv[4];
     if ((qm >> b) & 1u) {
-      const uint32_t T = c.T16[b >> 1];
+      const uint32_t T = c.T16[(b + slot0) >> 1];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         uint32_t v = 0;
@@ -601,7 +604,7 @@ __device__ __forceinline__ void lb_emit(const uint32_t (&acc)[4][P], int64_t i0,
         const uint32_t pass = (h2_le_bits(v, T) >> (b & 1)) & 1u;
         const float h = (b & 1) ? h_hi_f(v) : h_lo_f(v);
         lbv[j] = __fmul_rd(fmaxf(__fsub_rd(h, c.wabs), 0.f), c.lbconv);
-        if (pass && j < nvalid && lbv[j] <= c.thr[b]) m |= 1u << j;
+        if (pass && j < nvalid && lbv[j] <= c.thr[b + slot0]) m |= 1u << j;
       }
     }
     const int cnt = __popc(m);
@@ -614,16 +617,16 @@ __device__ __forceinline__ void lb_emit(const uint32_t (&acc)[4][P], int64_t i0,
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     if (total == 0) continue;
     unsigned base = 0;
-    if (lane == 31) base = atomicAdd(&a.count[b], (unsigned)total);
+    if (lane == 31) base = atomicAdd(&a.count[b + slot0], (unsigned)total);
     base = __shfl_sync(0xffffffffu, base, 31);
     uint64_t pos = (uint64_t)base + (unsigned)(incl - cnt);
-    const float sc = c.scale[b];
+    const float sc = c.scale[b + slot0];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       if (m & (1u << j)) {
         if (pos < (uint64_t)a.cap) {
-          a.cand[(size_t)b * a.cap + pos] = make_key(lbv[j], perm ? __ldg(perm + i0 + j) : (uint32_t)(i0 + j));
-          atomicAdd(&a.hist[b * kNB + lb_bin(lbv[j], sc)], 1u);
+          a.cand[(size_t)(b + slot0) * a.cap + pos] = make_key(lbv[j], perm ? __ldg(perm + i0 + j) : (uint32_t)(i0 + j));
+          atomicAdd(&a.hist[(b + slot0) * kNB + lb_bin(lbv[j], sc)], 1u);
         }
         ++pos;
       }
@@ -677,14 +680,15 @@ __device__ void wb_flush(WarpBuf& wb, int nslots, const LbConsts& c, const LbArg
 template <int P>
 __device__ __forceinline__ void lb_emit_wb(const uint32_t (&acc)[4][P], int64_t i0, int nvalid, int nslots,
                                            const LbConsts& c, const LbArgs& a, WarpBuf& wb, unsigned* s_hist,
-                                           uint32_t slot_mask = 0xFFFFFFFFu, const uint32_t* perm = nullptr) {
+                                           uint32_t slot_mask = 0xFFFFFFFFu, const uint32_t* perm = nullptr,
+                                           int slot0 = 0) {
   const int lane = threadIdx.x & 31;
   uint32_t qm = 0;
   if (nvalid > 0) {
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       const uint32_t mn = h2_min(h2_min(acc[0][p], acc[1][p]), h2_min(acc[2][p], acc[3][p]));
-      qm |= h2_le_bits(mn, c.T16[p]) << (2 * p);
+      qm |= h2_le_bits(mn, c.T16[p + (slot0 >> 1)]) << (2 * p);
     }
     qm &= slot_mask;
   }
@@ -693,7 +697,7 @@ __device__ __forceinline__ void lb_emit_wb(const uint32_t (&acc)[4][P], int64_t 
   int cntl = 0;
   for (uint32_t r = qm; r; r &= r - 1) {
     const int b = __ffs(r) - 1;
-    const uint32_t T = c.T16[b >> 1];
+    const uint32_t T = c.T16[(b + slot0) >> 1];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       uint32_t v = 0;
@@ -702,7 +706,7 @@ __device__ __forceinline__ void lb_emit_wb(const uint32_t (&acc)[4][P], int64_t 
         if (p == (b >> 1)) v = acc[j][p];
       const float h = (b & 1) ? h_hi_f(v) : h_lo_f(v);
       const float lb = __fmul_rd(fmaxf(__fsub_rd(h, c.wabs), 0.f), c.lbconv);
-      if (((h2_le_bits(v, T) >> (b & 1)) & 1u) && j < nvalid && lb <= c.thr[b]) ++cntl;
+      if (((h2_le_bits(v, T) >> (b & 1)) & 1u) && j < nvalid && lb <= c.thr[b + slot0]) ++cntl;
     }
   }
   int incl = cntl;
@@ -715,13 +719,13 @@ __device__ __forceinline__ void lb_emit_wb(const uint32_t (&acc)[4][P], int64_t 
   if (total == 0) return;
   if (wb.n + total > kWB) wb_flush(wb, nslots, c, a, s_hist);
   if (total > kWB) {  // degenerate (e.g. tau = inf): straight to global memory
-    lb_emit<P>(acc, i0, nvalid, c, a, qm, perm);
+    lb_emit<P>(acc, i0, nvalid, c, a, qm, perm, slot0);
     return;
   }
   int pos = wb.n + incl - cntl;
   for (uint32_t r = qm; r; r &= r - 1) {
     const int b = __ffs(r) - 1;
-    const uint32_t T = c.T16[b >> 1];
+    const uint32_t T = c.T16[(b + slot0) >> 1];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       uint32_t v = 0;
@@ -730,10 +734,10 @@ __device__ __forceinline__ void lb_emit_wb(const uint32_t (&acc)[4][P], int64_t 
         if (p == (b >> 1)) v = acc[j][p];
       const float h = (b & 1) ? h_hi_f(v) : h_lo_f(v);
       const float lb = __fmul_rd(fmaxf(__fsub_rd(h, c.wabs), 0.f), c.lbconv);
-      if (((h2_le_bits(v, T) >> (b & 1)) & 1u) && j < nvalid && lb <= c.thr[b]) {
+      if (((h2_le_bits(v, T) >> (b & 1)) & 1u) && j < nvalid && lb <= c.thr[b + slot0]) {
         wb.key[pos] = make_key(lb, perm ? __ldg(perm + i0 + j) : (uint32_t)(i0 + j));
-        wb.slot[pos] = (uint8_t)b;
-        atomicAdd(&wb.cnt[b], 1u);
+        wb.slot[pos] = (uint8_t)(b + slot0);
+        atomicAdd(&wb.cnt[b + slot0], 1u);
         ++pos;
       }
     }
@@ -830,41 +834,6 @@ __device__ __forceinline__ void lbt_seg(uint32_t word, const uint32_t* __restric
   }
 }
 
-// Same for pairs [G0, G0+GP) of a P-pair accumulator (index mode: only the
-// query pairs whose block bound can pass are computed).
-template <int P, int G0, int GP>
-__device__ __forceinline__ void lbt_seg_g(uint32_t word, const uint32_t* __restrict__ tabl,
-                                          const uint2* __restrict__ q16s, uint32_t (&acc)[4][P]) {
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const uint32_t t = tabl[__byte_perm(word, 0, 0x4440 | j) * 32];
-    const uint32_t tx = __byte_perm(t, 0, 0x1010);
-    const uint32_t ty = __byte_perm(t, 0, 0x3232);
-#pragma unroll
-    for (int p = G0; p < G0 + GP; ++p) {
-      const uint2 q = q16s[p];
-      const uint32_t a = h2_fma_relu(q.x, kHalf2One, tx);
-      const uint32_t b = h2_fma_relu(q.y, kHalf2One, ty);
-      const uint32_t d = h2_max(a, b);
-      acc[j][p] = h2_fma(d, d, acc[j][p]);
-    }
-  }
-}
-
-template <int P, int G0, int GP>
-__device__ __forceinline__ void lbt_group(uint32_t bm, const uint32_t* __restrict__ rows, int tid,
-                                          const uint32_t* __restrict__ tabl, const uint2* __restrict__ s_q16,
-                                          uint32_t (&acc)[4][P]) {
-  if constexpr (G0 < P) {
-    constexpr uint32_t gm = ((1u << (2 * GP)) - 1u) << (2 * G0);
-    if (bm & gm) {
-#pragma unroll 2
-      for (int s = 0; s < kTW; ++s) lbt_seg_g<P, G0, GP>(rows[s * (kTS / 4) + tid], tabl, s_q16 + s * P, acc);
-    }
-    lbt_group<P, G0 + GP, GP>(bm, rows, tid, tabl, s_q16, acc);
-  }
-}
-
 // Block MINDIST (the iSAX node bound) of this warp's 128-series block for every
 // query slot, from the block's per-segment [min, max] symbols: region
 // [L[min], U[max]] (outward fp32), round-down arithmetic -> bit b set iff the
@@ -913,10 +882,7 @@ __device__ __forceinline__ void lbt_seg1(uint32_t word, const uint32_t* __restri
 }
 
 // MODE 0: seed (per-warp LB-best series per query over [0, nlim));
-// MODE 1: LB pass with candidate emission over [0, nlim = n);
-// MODE 2: the same over the index-sorted SAX array: each warp first bounds its
-//         128-series block (envelope MINDIST) and computes only the query pairs
-//         the block can hold candidates for; candidate ids go through perm.
+// MODE 1: LB pass with candidate emission over [0, nlim = n).
 // P = 0: single query (slot 0).  nlim % 16 == 0.
 template <int P, int MODE>
 __global__ void __launch_bounds__(kTThreads, 1)
@@ -929,21 +895,13 @@ k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
   __shared__ unsigned s_cnt[kStages];
   __shared__ uint2 s_q16[PP * kTW];
   __shared__ LbConsts s_c;
-  __shared__ WarpBuf s_wb[MODE >= 1 ? kTWarps : 1];
-  __shared__ unsigned s_hist[MODE >= 1 ? kMaxB * kNB : 1];
-  __shared__ float2 s_lu[MODE == 2 ? kMaxCard : 1];
-  __shared__ float2 s_qf[MODE == 2 ? 2 * PP * kMaxW : 1];
-  __shared__ unsigned s_blk[kMaxB];
+  __shared__ WarpBuf s_wb[MODE == 1 ? kTWarps : 1];
+  __shared__ unsigned s_hist[MODE == 1 ? kMaxB * kNB : 1];
   const int tid = threadIdx.x, lane = tid & 31;
   const int64_t ntiles = (nlim + kTS - 1) / kTS;
   const int nslots = P > 0 ? 2 * P : 1;
-  WarpBuf& wb = s_wb[MODE >= 1 ? (tid >> 5) : 0];
-  if (tid < kMaxB) s_blk[tid] = 0;
-  if (MODE == 2) {
-    for (int i = tid; i < kMaxCard; i += kTThreads) s_lu[i] = a.tab->lu[i];
-    for (int i = tid; i < 2 * PP * kMaxW; i += kTThreads) s_qf[i] = a.g_q[i];
-  }
-  if (MODE >= 1) {
+  WarpBuf& wb = s_wb[MODE == 1 ? (tid >> 5) : 0];
+  if (MODE == 1) {
     if (lane < kMaxB) wb.cnt[lane] = 0;
     if (lane == 0) wb.n = 0;
     for (int i = tid; i < nslots * kNB; i += kTThreads) s_hist[i] = 0;
@@ -1004,19 +962,7 @@ k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
     for (int j = 0; j < 4; ++j)
 #pragma unroll
       for (int p = 0; p < PP; ++p) acc[j][p] = 0u;
-    uint32_t bm = 0xFFFFFFFFu;
-    if (MODE == 2) {
-      const int64_t blk = (tile * kTS) / PARIS_INDEX_BLOCK + (tid >> 5);
-      // a ragged last tile: warps past the end have no block (and no envelope)
-      bm = ((int64_t)blk * PARIS_INDEX_BLOCK < nlim) ? block_mask(a.env, blk, nslots, s_qf, s_lu, s_c, a.seglen_f) : 0u;
-      if (lane < nslots && ((bm >> lane) & 1u)) atomicAdd(&s_blk[lane], 1u);
-    }
-    if (MODE == 2 && P > 0) {
-      if (a.group1) lbt_group<PP, 0, 1>(bm, rows, tid, tabl, s_q16, acc);
-      else lbt_group<PP, 0, (PP < 2 ? PP : 2)>(bm, rows, tid, tabl, s_q16, acc);
-    } else if (MODE == 2 && bm == 0) {
-      // single query, block pruned: nothing to compute
-    } else if (P > 0) {
+    if (P > 0) {
 #pragma unroll 2
       for (int s = 0; s < kTW; ++s) lbt_seg<PP>(rows[s * (kTS / 4) + tid], tabl, s_q16 + s * PP, acc);
     } else {
@@ -1044,8 +990,8 @@ k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
         }
       }
     }
-    if (MODE >= 1) {
-      lb_emit_wb<PP>(acc, i0, nvalid, nslots, s_c, a, wb, s_hist, bm, MODE == 2 ? a.perm : nullptr);
+    if (MODE == 1) {
+      lb_emit_wb<PP>(acc, i0, nvalid, nslots, s_c, a, wb, s_hist);
     } else {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -1059,10 +1005,9 @@ k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
       }
     }
   }
-  if (MODE >= 1) {
+  if (MODE == 1) {
     wb_flush(wb, nslots, s_c, a, s_hist);
     __syncthreads();
-    if (MODE == 2 && tid < nslots && s_blk[tid]) atomicAdd(&a.blocks[tid], s_blk[tid]);
     for (int i = tid; i < nslots * kNB; i += kTThreads)
       if (s_hist[i]) atomicAdd(&a.hist[i], s_hist[i]);
   }
@@ -1081,6 +1026,261 @@ k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
       if (lane == 0 && b < a.nb && gwarp < S) seed_ids[b * S + gwarp] = (id == 0xFFFFFFFFu) ? -1 : (int)id;
     }
   }
+}
+
+// ---------------------------------------------------------------- index mode LB (f1)
+// Pass 1 (k_blkmask): the envelope MINDIST of every 128-series block for every
+// query slot (the iSAX node bound): bit b of bmask[blk] = block may hold a
+// candidate of slot b.  A CTA covers the 16 blocks of one SAX tile and appends
+// the tile to a work list when any of its blocks is live.
+// Pass 2 (k_lbi): the TMA ring streams only listed tiles; the live (block, query
+// pair) items of a tile are dealt round-robin to its 16 warps (every warp derives
+// the same item list from the 16 block masks, no CTA barrier), so warps stay
+// balanced however the live blocks are spread.
+// Candidate emission of one index item: 4 series x 2 query slots (sa = low half,
+// sb = high half, sb < 0: none).  Same tests and warp buffer as lb_emit_wb.
+__device__ __forceinline__ uint32_t half_of(uint32_t v, int h) { return (v >> (16 * h)) & 0xFFFFu; }
+
+__device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int sb, int64_t i0, int nvalid,
+                                         int nslots, const LbConsts& c, const LbArgs& a, WarpBuf& wb,
+                                         unsigned* s_hist) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t Tp = half_of(c.T16[sa >> 1], sa & 1) |
+                      ((sb >= 0 ? half_of(c.T16[sb >> 1], sb & 1) : (uint32_t)kHalfNeg1) << 16);
+  uint32_t pm = 0;  // bit 2j+h: series j passes for slot h
+  float lbv[4][2];
+  if (nvalid > 0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t pb = h2_le_bits(acc[j], Tp);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int sl = h ? sb : sa;
+        const float hv = h ? h_hi_f(acc[j]) : h_lo_f(acc[j]);
+        lbv[j][h] = __fmul_rd(fmaxf(__fsub_rd(hv, c.wabs), 0.f), c.lbconv);
+        if (((pb >> h) & 1u) && sl >= 0 && j < nvalid && lbv[j][h] <= c.thr[sl]) pm |= 1u << (2 * j + h);
+      }
+    }
+  }
+  if (!__any_sync(0xffffffffu, pm != 0u)) return;
+  const int cntl = __popc(pm);
+  int incl = cntl;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  if (wb.n + total > kWB) wb_flush(wb, nslots, c, a, s_hist);
+  if (total > kWB) {  // degenerate (e.g. tau = inf): straight to global memory
+    for (uint32_t r = pm; r; r &= r - 1) {
+      const int bit = __ffs(r) - 1, j = bit >> 1, sl = (bit & 1) ? sb : sa;
+      const unsigned pos = atomicAdd(&a.count[sl], 1u);
+      if ((int64_t)pos < a.cap) {
+        a.cand[(size_t)sl * a.cap + pos] = make_key(lbv[j][bit & 1], __ldg(a.perm + i0 + j));
+        atomicAdd(&a.hist[sl * kNB + lb_bin(lbv[j][bit & 1], c.scale[sl])], 1u);
+      }
+    }
+    return;
+  }
+  int pos = wb.n + incl - cntl;
+  for (uint32_t r = pm; r; r &= r - 1) {
+    const int bit = __ffs(r) - 1, j = bit >> 1, sl = (bit & 1) ? sb : sa;
+    wb.key[pos] = make_key(lbv[j][bit & 1], __ldg(a.perm + i0 + j));
+    wb.slot[pos] = (uint8_t)sl;
+    atomicAdd(&wb.cnt[sl], 1u);
+    ++pos;
+  }
+  __syncwarp();
+  if (lane == 31) wb.n += total;
+  __syncwarp();
+}
+
+// One lane per block: lane l of a warp bounds block 32*g + l against every query
+// slot (region [L[min_s], U[max_s]] per segment, outward fp32, round-down sums);
+// a warp covers two whole tiles, so it lists its live tiles itself.
+template <int P>
+__global__ void __launch_bounds__(256)
+k_blkmask(LbArgs a, unsigned* __restrict__ bmask, unsigned* __restrict__ tile_list,
+          unsigned* __restrict__ tile_count, unsigned* __restrict__ blocks) {
+  constexpr int NS = 2 * P;
+  __shared__ float2 s_lu[kMaxCard];
+  __shared__ float2 s_qf[NS * kTW];
+  __shared__ float s_thr[NS];
+  __shared__ unsigned s_blk[kMaxB];
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int i = tid; i < kMaxCard; i += blockDim.x) s_lu[i] = a.tab->lu[i];
+  for (int i = tid; i < NS * kTW; i += blockDim.x) s_qf[i] = a.g_q[(i / kTW) * kMaxW + (i % kTW)];
+  if (tid < NS) s_thr[tid] = (tid < a.nb) ? __uint_as_float(a.thr[tid]) : -1.f;
+  if (tid < kMaxB) s_blk[tid] = 0;
+  __syncthreads();
+  const int64_t nblocks = (a.n + PARIS_INDEX_BLOCK - 1) / PARIS_INDEX_BLOCK;
+  const int64_t ntiles = (a.n + kTS - 1) / kTS;
+  const int64_t ngroups = (ntiles + 1) / 2;  // 32 blocks = 2 tiles per warp step
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + tid) >> 5, GW = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t g = gw; g < ngroups; g += GW) {
+    const int64_t blk = 32 * g + lane;
+    uint32_t bm = 0;
+    if (blk < nblocks) {
+      const uint4 mn = __ldg(reinterpret_cast<const uint4*>(a.env + (size_t)blk * 32));
+      const uint4 mx = __ldg(reinterpret_cast<const uint4*>(a.env + (size_t)blk * 32 + 16));
+      const uint32_t mnw[4] = {mn.x, mn.y, mn.z, mn.w}, mxw[4] = {mx.x, mx.y, mx.z, mx.w};
+      float acc[NS];
+#pragma unroll
+      for (int b = 0; b < NS; ++b) acc[b] = 0.f;
+#pragma unroll
+      for (int seg = 0; seg < kTW; ++seg) {
+        const float Lo = s_lu[(mnw[seg >> 2] >> (8 * (seg & 3))) & 0xFFu].x;  // L of the min symbol (down)
+        const float Up = s_lu[(mxw[seg >> 2] >> (8 * (seg & 3))) & 0xFFu].y;  // U of the max symbol (up)
+#pragma unroll
+        for (int b = 0; b < NS; ++b) {
+          const float2 q = s_qf[b * kTW + seg];
+          const float delta = fmax3(__fsub_rd(q.x, Up), __fsub_rd(Lo, q.y), 0.f);
+          acc[b] = __fmaf_rd(delta, delta, acc[b]);
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < NS; ++b) bm |= (__fmul_rd(acc[b], a.seglen_f) <= s_thr[b] ? 1u : 0u) << b;
+    }
+    const int64_t nbpad = ntiles * kTWarps;
+    if (blk < nbpad) bmask[blk] = bm;
+    const unsigned live = __ballot_sync(0xffffffffu, bm != 0u);
+    if (lane == 0 && (live & 0xFFFFu)) tile_list[atomicAdd(tile_count, 1u)] = (unsigned)(2 * g);
+    if (lane == 16 && (live >> 16) && 2 * g + 1 < ntiles) tile_list[atomicAdd(tile_count, 1u)] = (unsigned)(2 * g + 1);
+#pragma unroll
+    for (int b = 0; b < NS; ++b) {
+      const unsigned m = __ballot_sync(0xffffffffu, (bm >> b) & 1u);
+      if (lane == 0 && m) atomicAdd(&s_blk[b], (unsigned)__popc(m));
+    }
+  }
+  __syncthreads();
+  if (tid < NS && s_blk[tid]) atomicAdd(&blocks[tid], s_blk[tid]);
+}
+
+template <int P>
+__global__ void __launch_bounds__(kTThreads, 1)
+k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__ tile_list,
+      const unsigned* __restrict__ tile_count) {
+  extern __shared__ __align__(128) uint8_t dsm[];
+  uint8_t* s_tiles = dsm;
+  // region table in pair form {(-U16,-U16), (L16,L16)}, 16 copies: entry c of lane l
+  // at uint2 index 16c + (l % 16) -- a 64-bit load is served per half-warp, so the
+  // 16 lanes of each half always hit distinct banks
+  uint2* s_tab = reinterpret_cast<uint2*>(dsm + kStages * kTileBytes);
+  __shared__ __align__(8) uint64_t s_full[kStages];
+  __shared__ unsigned s_cnt[kStages];
+  __shared__ uint32_t s_qs[2 * P][kTW];  // per slot and segment: half2(q_lo16, -q_hi16)
+  __shared__ LbConsts s_c;
+  __shared__ WarpBuf s_wb[kTWarps];
+  __shared__ unsigned s_hist[kMaxB * kNB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nslots = 2 * P;
+  const int64_t nlist = *tile_count;
+  WarpBuf& wb = s_wb[warp];
+  if (lane < kMaxB) wb.cnt[lane] = 0;
+  if (lane == 0) wb.n = 0;
+  for (int i = tid; i < nslots * kNB; i += kTThreads) s_hist[i] = 0;
+
+  static_assert(kTS == PARIS_INDEX_TILE, "index tiles are the LB kernel's tiles");
+  auto issue = [&](int64_t li, int st) {
+    // tile-major sorted SAX: the tile's 16 rows are one contiguous 32 KB range
+    mbar_expect_tx(&s_full[st], (unsigned)kTileBytes);
+    bulk_g2s(s_tiles + (size_t)st * kTileBytes, a.sax + (size_t)tile_list[li] * kTileBytes, (unsigned)kTileBytes,
+             &s_full[st]);
+  };
+  if (tid == 0) {
+    for (int st = 0; st < kStages; ++st) {
+      mbar_init(&s_full[st], 1);
+      s_cnt[st] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int st = 0; st < kStages; ++st) {
+      const int64_t li = blockIdx.x + (int64_t)st * gridDim.x;
+      if (li < nlist) issue(li, st);
+    }
+  }
+  for (int i = tid; i < kMaxCard * 16; i += kTThreads) s_tab[i] = a.tab->lu16[i >> 4];
+  for (int i = tid; i < 2 * P * kTW; i += kTThreads) {
+    const int b = i / kTW, sg = i % kTW;
+    const uint2 v = a.g_q16[sg * P + (b >> 1)];
+    s_qs[b][sg] = half_of(v.x, b & 1) | (half_of(v.y, b & 1) << 16);
+  }
+  lb_consts_init(a, nslots, &s_c);  // ends with __syncthreads
+  const uint2* tabl = s_tab + (lane & 15);
+  int rot = 0;
+
+  for (int64_t it = 0;; ++it) {
+    const int64_t li = blockIdx.x + it * gridDim.x;
+    if (li >= nlist) break;
+    const int st = (int)(it % kStages);
+    const int64_t tile = tile_list[li];
+    // the tile's 16 block masks; a block's live slots are computed two at a time
+    // (consecutive live slots form an item), items dealt round-robin to the warps
+    uint32_t bm = 0;
+    if (lane < kTWarps) bm = __ldg(bmask + tile * kTWarps + lane);
+    const int cnt = (__popc(bm) + 1) >> 1;
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, kTWarps - 1);
+    mbar_wait(&s_full[st], (unsigned)((it / kStages) & 1));
+    const uint32_t* rows = reinterpret_cast<const uint32_t*>(s_tiles + (size_t)st * kTileBytes);
+    // deal items round-robin starting where the previous tile stopped, so no warp
+    // is systematically one item behind (a lagging warp delays the stage refill)
+    const int first = (warp - rot + 2 * kTWarps) % kTWarps;
+    rot = (rot + total) % kTWarps;
+    for (int t = first; t < total; t += kTWarps) {
+      // item t -> (block k, pair p)
+      const int k = __popc(__ballot_sync(0xffffffffu, lane < kTWarps && incl <= t));
+      const int excl = __shfl_sync(0xffffffffu, incl - cnt, k);
+      const uint32_t bmk = __shfl_sync(0xffffffffu, bm, k);
+      const int r = t - excl;
+      const int sa = __fns(bmk, 0, 2 * r + 1);
+      const int sbf = __fns(bmk, 0, 2 * r + 2);
+      const int sb = (sbf >= 0 && sbf < 32) ? sbf : -1;
+      const int sq = sb >= 0 ? sb : sa;  // odd count: duplicate lane, masked in emission
+      uint32_t acc[4] = {0u, 0u, 0u, 0u};
+#pragma unroll 4
+      for (int s = 0; s < kTW; ++s) {
+        const uint32_t word = rows[s * (kTS / 4) + k * 32 + lane];
+        const uint32_t qa = s_qs[sa][s], qb = s_qs[sq][s];
+        const uint32_t qx = __byte_perm(qa, qb, 0x5410);  // (q_lo16[sa], q_lo16[sb])
+        const uint32_t qy = __byte_perm(qa, qb, 0x7632);  // (-q_hi16[sa], -q_hi16[sb])
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint2 tt = tabl[__byte_perm(word, 0, 0x4440 | j) * 16];
+          const uint32_t a1 = h2_fma_relu(qx, kHalf2One, tt.x);
+          const uint32_t b1 = h2_fma_relu(qy, kHalf2One, tt.y);
+          const uint32_t d = h2_max(a1, b1);
+          acc[j] = h2_fma(d, d, acc[j]);
+        }
+      }
+      const int64_t i0 = tile * kTS + k * PARIS_INDEX_BLOCK + 4 * lane;
+      const int nvalid = (int)std::max<int64_t>(0, imin64(4, a.n - i0));
+      lbi_emit(acc, sa, sb, i0, nvalid, nslots, s_c, a, wb, s_hist);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (atomicAdd(&s_cnt[st], 1u) == kTWarps - 1) {
+        s_cnt[st] = 0;
+        const int64_t next = li + (int64_t)kStages * gridDim.x;
+        if (next < nlist) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(next, st);
+        }
+      }
+    }
+  }
+  wb_flush(wb, nslots, s_c, a, s_hist);
+  __syncthreads();
+  for (int i = tid; i < nslots * kNB; i += kTThreads)
+    if (s_hist[i]) atomicAdd(&a.hist[i], s_hist[i]);
 }
 
 // Query prep alone (for the tiled seed, which has no prologue of its own).
@@ -1513,6 +1713,11 @@ struct Ws {
   unsigned* cursor;
   unsigned* refined;
   unsigned* blocks;      // index mode: blocks whose envelope bound passed, per query
+  unsigned* tile_count;  // index mode: live tiles listed
+  unsigned* bmask;       // index mode: [ntiles*16] per-block live query-slot masks
+  unsigned* tile_list;   // index mode: live tiles
+  unsigned* tile_flag;   // index mode: [ntiles] tile already listed (zeroed per batch)
+  size_t flag_bytes;
   size_t zero_bytes;
   unsigned long long* best;
   uint64_t* cand;
@@ -1535,7 +1740,6 @@ struct Plan {
   bool tiled;     // TMA-tiled LB kernels (n % 16 == 0, w == 16)
   const uint32_t* perm;  // index mode (paris_knn_index): sorted position -> id
   const uint8_t* env;    // index mode: block envelopes
-  int group1;            // index mode: per-pair skip granularity (test/tuning hook)
   int idx_seeds;         // index mode: series around the query's leaf
 };
 
@@ -1559,7 +1763,7 @@ cudaError_t launch_lb(const Plan& p, const uint8_t* sax, int nb, const CardTable
   LbArgs la;
   la.sax = sax; la.n = p.n; la.w = p.w; la.seglen_f = (float)(p.len / p.w); la.tab = tab;
   la.g_q = ws.g_q; la.g_q16 = ws.g_q16; la.nb = nb; la.thr = ws.thr_seed; la.count = ws.count;
-  la.hist = ws.hist; la.cand = ws.cand; la.cap = cap; la.perm = nullptr; la.env = nullptr; la.group1 = 0;
+  la.hist = ws.hist; la.cand = ws.cand; la.cap = cap; la.perm = nullptr; la.env = nullptr;
   la.blocks = ws.blocks;
   return PARIS_LAUNCH("lb_pass", (k_lb<P, WT, AL>), grid, kLBThreads, 0, st, la);
 }
@@ -1606,10 +1810,46 @@ cudaError_t launch_lbt(const Plan& p, const uint8_t* sax, int nb, const CardTabl
   LbArgs la;
   la.sax = sax; la.n = p.n; la.w = p.w; la.seglen_f = (float)(p.len / p.w); la.tab = tab;
   la.g_q = ws.g_q; la.g_q16 = ws.g_q16; la.nb = nb; la.thr = ws.thr_seed; la.count = ws.count;
-  la.hist = ws.hist; la.cand = ws.cand; la.cap = cap; la.perm = p.perm; la.env = p.env; la.group1 = p.group1;
+  la.hist = ws.hist; la.cand = ws.cand; la.cap = cap; la.perm = p.perm; la.env = p.env;
   la.blocks = ws.blocks;
   return PARIS_LAUNCH(MODE ? "lb_pass" : "seed_lb", (k_lbt<P, MODE>), grid, kTThreads, kTSmem, st, la, nlim,
                       ws.seed_ids, p.S);
+}
+
+template <int P>
+cudaError_t launch_index_lb(const Plan& p, const uint8_t* sax, int nb, const CardTables* tab, const Ws& ws,
+                            cudaStream_t st, int64_t cap) {
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaError_t e = cudaFuncSetAttribute(k_lbi<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTSmem);
+    if (e != cudaSuccess) return e;
+    attr_dev = dev;
+  }
+  LbArgs la;
+  la.sax = sax; la.n = p.n; la.w = p.w; la.seglen_f = (float)(p.len / p.w); la.tab = tab;
+  la.g_q = ws.g_q; la.g_q16 = ws.g_q16; la.nb = nb; la.thr = ws.thr_seed; la.count = ws.count;
+  la.hist = ws.hist; la.cand = ws.cand; la.cap = cap; la.perm = p.perm; la.env = p.env;
+  la.blocks = ws.blocks;
+  const int64_t ntiles = (p.n + kTS - 1) / kTS;
+  const int64_t groups = (ntiles + 1) / 2;
+  const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms() * 8, (groups + 7) / 8));
+  cudaError_t e = PARIS_LAUNCH("lb_blocks", k_blkmask<P>, bgrid, 256, 0, st, la, ws.bmask, ws.tile_list,
+                               ws.tile_count, ws.blocks);
+  if (e != cudaSuccess) return e;
+  const int grid = (int)std::min<int64_t>(sms(), ntiles);
+  return PARIS_LAUNCH("lb_pass", k_lbi<P>, grid, kTThreads, kTSmem, st, la, ws.bmask, ws.tile_list, ws.tile_count);
+}
+
+cudaError_t dispatch_index_lb(int nb, const Plan& p, const uint8_t* sax, const CardTables* tab, const Ws& ws,
+                              cudaStream_t st, int64_t cap) {
+  switch (pairs_for(nb)) {
+    case 1: return launch_index_lb<1>(p, sax, nb, tab, ws, st, cap);
+    case 2: return launch_index_lb<2>(p, sax, nb, tab, ws, st, cap);
+    case 4: return launch_index_lb<4>(p, sax, nb, tab, ws, st, cap);
+    default: return launch_index_lb<8>(p, sax, nb, tab, ws, st, cap);
+  }
 }
 
 template <int MODE>
@@ -1651,13 +1891,17 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   const size_t o_q16 = take(sizeof(uint2) * (B / 2) * kMaxW);
   const size_t o_sid = take(sizeof(int) * B * p.S);
   const size_t o_skey = take(sizeof(uint64_t) * B * p.S);
-  const size_t zb = sizeof(unsigned) * (B + B + B * kNB + B * kNB + B + B);
+  const size_t zb = sizeof(unsigned) * (B + B + B * kNB + B * kNB + B + B + 1);
   const size_t o_zero = take(zb);
   const size_t o_best = take(sizeof(unsigned long long) * B * kPadU64);
   const size_t o_thr = take(sizeof(unsigned) * B * kPadU32);
   const size_t o_cand = take(sizeof(uint64_t) * B * (size_t)cap);
   const size_t o_sorted = take(sizeof(uint64_t) * B * (size_t)cap);
   const size_t o_lists = take(p.k > 1 ? sizeof(uint64_t) * B * (size_t)p.XB * p.k : 8);
+  const int64_t ntiles = (p.n + kTS - 1) / kTS;
+  const size_t o_bmask = take(p.perm ? sizeof(unsigned) * (size_t)ntiles * kTWarps : 8);
+  const size_t o_tlist = take(p.perm ? sizeof(unsigned) * (size_t)ntiles : 8);
+  const size_t o_tflag = take(p.perm ? sizeof(unsigned) * (size_t)ntiles : 8);
   void* base = nullptr;
   cudaError_t e = cudaMallocAsync(&base, off, st);
   if (e != cudaSuccess) {
@@ -1680,10 +1924,15 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   ws.cursor = ws.hist + B * kNB;
   ws.refined = ws.cursor + B * kNB;
   ws.blocks = ws.refined + B;
+  ws.tile_count = ws.blocks + B;
   ws.best = (unsigned long long*)(c + o_best);
   ws.cand = (uint64_t*)(c + o_cand);
   ws.sorted = (uint64_t*)(c + o_sorted);
   ws.lists = (uint64_t*)(c + o_lists);
+  ws.bmask = (unsigned*)(c + o_bmask);
+  ws.tile_list = (unsigned*)(c + o_tlist);
+  ws.tile_flag = (unsigned*)(c + o_tflag);
+  ws.flag_bytes = p.perm ? sizeof(unsigned) * (size_t)ntiles : 0;
   return PARIS_OK;
 }
 
@@ -1726,7 +1975,7 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
   }
   if (p.tiled) {
     const int grid = (int)std::min<int64_t>(sms(), (p.n + kTS - 1) / kTS);
-    if (p.perm) PARIS_CHECK_LAUNCH(dispatch_lbt<2>(nb, p, sax, tab, ws, st, cap, p.n, grid), "lb_pass launch");
+    if (p.perm) PARIS_CHECK_LAUNCH(dispatch_index_lb(nb, p, sax, tab, ws, st, cap), "lb_pass launch");
     else PARIS_CHECK_LAUNCH(dispatch_lbt<1>(nb, p, sax, tab, ws, st, cap, p.n, grid), "lb_pass launch");
   } else {
     PARIS_CHECK_LAUNCH(dispatch_p(P, true, p, sax, qbatch, nb, tab, ws, st, cap), "lb_pass launch");
@@ -1877,7 +2126,6 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   p.tiled = (n % 16 == 0) && (w == kTW) && (indexed || !(cfg && cfg->reserved[0] == 1));
   p.perm = perm;
   p.env = env;
-  p.group1 = (cfg && cfg->reserved[1] == 1) ? 1 : 0;
   p.idx_seeds = cfg ? cfg->reserved[2] : 0;
   plan_seed(p, (cfg && cfg->seed_div > 0) ? cfg->seed_div : 16);
   p.cap = std::min<int64_t>(n, std::max<int64_t>(65536, n / 32));

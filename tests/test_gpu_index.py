@@ -43,7 +43,12 @@ def test_index_build_matches_definition(P, n, card):
     order = np.lexsort((np.arange(n), keys))            # by (key, id)
     perm = idx.perm.cpu().numpy().astype(np.int64)
     np.testing.assert_array_equal(perm, order)
-    np.testing.assert_array_equal(idx.sax_sorted.cpu().numpy(), sax.cpu().numpy()[:, perm])
+    T = P.PARIS_INDEX_TILE
+    ntile = (n + T - 1) // T
+    tiled = idx.sax_sorted.cpu().numpy()
+    assert tiled.shape == (ntile, 16, T)
+    flat = tiled.transpose(1, 0, 2).reshape(16, ntile * T)[:, :n]   # tile-major -> [w][n]
+    np.testing.assert_array_equal(flat, sax.cpu().numpy()[:, perm])
     env = idx.env.cpu().numpy()
     ss = words[perm]
     for blk in range(env.shape[0]):
