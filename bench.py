@@ -243,7 +243,7 @@ def run_gpu(args):
     # ---- index (f1): iSAX-ordered SAX + block envelopes, built once (timed on its own)
     index = None
     index_ms = None
-    if args.path == "index":
+    if args.path == "index" or args.both:
         index = P.index_build(sax, W, CARD)
         torch.cuda.synchronize()
         e0.record(st)
@@ -251,141 +251,155 @@ def run_gpu(args):
         e1.record(st)
         torch.cuda.synchronize()
         index_ms = e0.elapsed_time(e1)
-
-    def knn(qsrc, **kw):
-        if index is not None:
-            return P.knn_index(raw, index, qsrc, k=k, **kw)
-        return P.knn_exact(raw, sax, qsrc, k=k, w=W, card=CARD, **kw)
-
-    # ---- query step = every query of the config through one ABI call per call_q queries
-    out_idx = torch.empty((nq, k), dtype=torch.int64, device=dev)
-    out_dist = torch.empty((nq, k), dtype=torch.float32, device=dev)
-
-    def step(qsrc, oi, od, cfg_=None):
-        cfg_ = cfg_ or kcfg
-        for c0 in range(0, nq, call_q):
-            c1 = min(nq, c0 + call_q)
-            knn(qsrc[c0:c1], out_idx=oi[c0:c1], out_dist=od[c0:c1], config=cfg_)
-
-    _, _, stats = knn(queries, out_idx=out_idx, out_dist=out_dist, config=kcfg, stats=True)
-    for _ in range(max(0, args.warmup - 1)):
-        step(queries, out_idx, out_dist)
-    torch.cuda.synchronize()
-
-    # ---- timed region (device events, max over ranks)
-    launches0 = P.launch_count()
-    if ws > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clocks:
-        e0.record(st)
-        for _ in range(args.steps):
-            step(queries, out_idx, out_dist)
-        e1.record(st)
-        torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
-    launches = P.launch_count() - launches0
-    step_ms = e0.elapsed_time(e1) / args.steps
-    # ---- the same K steps again with libparis' per-launch CUDA events (on the launching
-    # stream): per-kernel durations for the roofline and the time split (kept out of the
-    # headline timing because the event records add launch overhead on the small configs)
-    P.profile_reset()
-    P.profile_enable(True)
-    for _ in range(args.steps):
-        step(queries, out_idx, out_dist)
-    torch.cuda.synchronize()
-    P.profile_enable(False)
-    prof = P.profile_read()
-    step_ms_max = reduce_max_ms(step_ms, dev, ws)
-    value = weak_throughput(nq, ws, step_ms_max)
-
-    # ---- e2e through the same ABI call with HOST (pinned) buffers
-    hq = queries.cpu().pin_memory()
-    hidx = torch.empty((nq, k), dtype=torch.int64).pin_memory()
-    hdist = torch.empty((nq, k), dtype=torch.float32).pin_memory()
-    step(hq, hidx, hdist)
-    torch.cuda.synchronize()
-    e0.record(st)
-    for _ in range(args.steps):
-        step(hq, hidx, hdist)
-    e1.record(st)
-    torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1) / args.steps
-    e2e_value = weak_throughput(nq, ws, reduce_max_ms(e2e_ms, dev, ws))
-    assert torch.equal(hidx, out_idx.cpu()), "host-buffer path disagrees with device path"
-
-    # ---- roofline of the dominant kernel (algorithmic bytes / event-timed duration)
     peak, peak_src = measured_peaks()
-    cand = stats["candidates"].numpy().astype(np.float64)
-    refined = stats["refined"].numpy().astype(np.float64)
-    kern = {}
-    for name, (cnt, ms) in prof.items():
-        kern[name] = {"launches": cnt, "ms_per_step": ms / args.steps, "share": None}
-    tot = sum(v["ms_per_step"] for v in kern.values()) or 1.0
-    for v in kern.values():
-        v["share"] = v["ms_per_step"] / tot
     ncalls = (nq + call_q - 1) // call_q
     nbatches = sum((min(call_q, nq - c0) + batch - 1) // batch for c0 in range(0, nq, call_q))
     q_per_pass = nq / nbatches
-    alg = {
-        # SAX bytes per pass + 8 B per candidate written
-        "lb_pass": (nbatches * n * W + 8.0 * cand.sum()) / nbatches,
-        # raw bytes per refined series (K6)
-        "refine": 4.0 * length * refined.sum() / nbatches,
-    }
-    for name, v in kern.items():
-        if name in alg:
-            pl = v["ms_per_step"] * args.steps / prof[name][0]
-            v["launch_ms"] = pl
-            v["achieved_gbs"] = alg[name] / (pl / 1e3) / 1e9
-    dom = max(kern, key=lambda s: kern[s]["ms_per_step"]) if kern else None
-    roof = None
-    if dom:
-        per_launch_ms = kern[dom]["ms_per_step"] * args.steps / prof[dom][0]
-        if dom == "lb_pass" and index is not None:
-            # index path: the algorithmic work is the (block, query) pairs whose envelope bound
-            # passed (stats lb_blocks) x 128 series x w segments x 3 FMA-pipe half-ops
-            blocks = stats["lb_blocks"].numpy().astype(np.float64).sum()
-            ops = 3.0 * W * P.PARIS_INDEX_BLOCK * blocks / nbatches
-            ach = ops / (per_launch_ms / 1e3) / 1e12
-            pk = 148 * 64 * 2 * ALU_CLOCK_GHZ * 1e9 / 1e12
-            roof = {"kernel": dom, "bound": "alu", "achieved": ach, "peak": pk, "unit": "Tops/s (fp16x2 half-ops)",
-                    "frac": ach / pk, "traffic": ncu_traffic(dom, args.config),
-                    "algorithmic_ops_per_launch": ops, "launch_ms": per_launch_ms,
-                    "peak_source": f"derived: 148 SM x 64 FMA lanes/clk x 2 (f16x2) x {ALU_CLOCK_GHZ} GHz",
-                    "active_block_frac": blocks / (nq * (n / P.PARIS_INDEX_BLOCK)),
-                    "hbm_achieved_gbs": alg[dom] / (per_launch_ms / 1e3) / 1e9, "hbm_peak_gbs": peak,
-                    "queries_per_pass": q_per_pass}
-        elif dom == "lb_pass" and q_per_pass > 1.5:
-            # batched fp16x2 LB: bound by the FMA pipe, not HBM: 3 half-precision
-            # FMA-pipe ops per (series, segment, query); peak = 148 SMs x 64 lanes/clk x 2 halves
-            # x sm clock (B300_MICROARCH.md: FFMA/HFMA2 reciprocal throughput 2 per SMSP).
-            ops = 3.0 * n * W * q_per_pass
-            ach = ops / (per_launch_ms / 1e3) / 1e12
-            pk = 148 * 64 * 2 * ALU_CLOCK_GHZ * 1e9 / 1e12
-            roof = {"kernel": dom, "bound": "alu", "achieved": ach, "peak": pk, "unit": "Tops/s (fp16x2 half-ops)",
-                    "frac": ach / pk, "traffic": ncu_traffic(dom, args.config),
-                    "algorithmic_ops_per_launch": ops, "launch_ms": per_launch_ms,
-                    "peak_source": f"derived: 148 SM x 64 FMA lanes/clk x 2 (f16x2) x {ALU_CLOCK_GHZ} GHz",
-                    "hbm_achieved_gbs": alg[dom] / (per_launch_ms / 1e3) / 1e9, "hbm_peak_gbs": peak,
-                    "queries_per_pass": q_per_pass}
-        elif dom in alg:
-            ach = alg[dom] / (per_launch_ms / 1e3) / 1e9
-            roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                    "frac": ach / peak, "traffic": ncu_traffic(dom, args.config),
-                    "algorithmic_bytes_per_launch": alg[dom], "launch_ms": per_launch_ms, "peak_source": peak_src}
 
-    # ---- LB pass at one query per SAX read: the HBM-roofline configuration of K4 (SURVEY §7 hard part 1)
+    def measure_path(path: str, full: bool):
+        """Warm up, time K steps of `path` (device events, max over ranks), then the same K
+        steps with per-launch events for the kernel split and the roofline; with full=True
+        also the end-to-end variant through host buffers and the clock record."""
+        use_index = path == "index"
+
+        def knn(qsrc, **kw):
+            if use_index:
+                return P.knn_index(raw, index, qsrc, k=k, **kw)
+            return P.knn_exact(raw, sax, qsrc, k=k, w=W, card=CARD, **kw)
+
+        out_idx = torch.empty((nq, k), dtype=torch.int64, device=dev)
+        out_dist = torch.empty((nq, k), dtype=torch.float32, device=dev)
+
+        def step(qsrc, oi, od, cfg_=None):
+            cfg_ = cfg_ or kcfg
+            for c0 in range(0, nq, call_q):
+                c1 = min(nq, c0 + call_q)
+                knn(qsrc[c0:c1], out_idx=oi[c0:c1], out_dist=od[c0:c1], config=cfg_)
+
+        _, _, stats = knn(queries, out_idx=out_idx, out_dist=out_dist, config=kcfg, stats=True)
+        for _ in range(max(0, args.warmup - 1)):
+            step(queries, out_idx, out_dist)
+        torch.cuda.synchronize()
+        r = {"path": path, "stats": stats, "knn": knn, "out_idx": out_idx}
+        # timed region
+        launches0 = P.launch_count()
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        with ClockSampler(local) as clocks:
+            e0.record(st)
+            for _ in range(args.steps):
+                step(queries, out_idx, out_dist)
+            e1.record(st)
+            torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        r["launches"] = P.launch_count() - launches0
+        r["clocks"] = clocks.summary()
+        r["step_ms"] = reduce_max_ms(e0.elapsed_time(e1) / args.steps, dev, ws)
+        r["value"] = weak_throughput(nq, ws, r["step_ms"])
+        # the same K steps with libparis' per-launch CUDA events (launching stream)
+        P.profile_reset()
+        P.profile_enable(True)
+        for _ in range(args.steps):
+            step(queries, out_idx, out_dist)
+        torch.cuda.synchronize()
+        P.profile_enable(False)
+        prof = P.profile_read()
+        if full:
+            # e2e through the same ABI calls with HOST (pinned) buffers
+            hq = queries.cpu().pin_memory()
+            hidx = torch.empty((nq, k), dtype=torch.int64).pin_memory()
+            hdist = torch.empty((nq, k), dtype=torch.float32).pin_memory()
+            step(hq, hidx, hdist)
+            torch.cuda.synchronize()
+            e0.record(st)
+            for _ in range(args.steps):
+                step(hq, hidx, hdist)
+            e1.record(st)
+            torch.cuda.synchronize()
+            r["e2e_value"] = weak_throughput(nq, ws, reduce_max_ms(e0.elapsed_time(e1) / args.steps, dev, ws))
+            assert torch.equal(hidx, out_idx.cpu()), "host-buffer path disagrees with device path"
+        cand = stats["candidates"].numpy().astype(np.float64)
+        refined = stats["refined"].numpy().astype(np.float64)
+        kern = {}
+        for name, (cnt, ms) in prof.items():
+            kern[name] = {"launches": cnt, "ms_per_step": ms / args.steps, "share": None}
+        tot = sum(v["ms_per_step"] for v in kern.values()) or 1.0
+        for v in kern.values():
+            v["share"] = v["ms_per_step"] / tot
+        alg = {
+            # SAX bytes per pass + 8 B per candidate written (SURVEY §8(d) K4)
+            "lb_pass": (nbatches * n * W + 8.0 * cand.sum()) / nbatches,
+            # raw bytes per refined series (K6)
+            "refine": 4.0 * length * refined.sum() / nbatches,
+        }
+        for name, v in kern.items():
+            if name in alg:
+                pl = v["ms_per_step"] * args.steps / prof[name][0]
+                v["launch_ms"] = pl
+                v["achieved_gbs"] = alg[name] / (pl / 1e3) / 1e9
+        dom = max(kern, key=lambda s_: kern[s_]["ms_per_step"]) if kern else None
+        roof = None
+        if dom:
+            per_launch_ms = kern[dom]["ms_per_step"] * args.steps / prof[dom][0]
+            pk = 148 * 64 * 2 * ALU_CLOCK_GHZ * 1e9 / 1e12
+            alu_src = f"derived: 148 SM x 64 FMA lanes/clk x 2 (f16x2) x {ALU_CLOCK_GHZ} GHz"
+            if dom == "lb_pass" and use_index:
+                # index path: the algorithmic work is the (block, query) pairs whose envelope
+                # bound passed (stats lb_blocks) x 128 series x w segments x 3 FMA-pipe half-ops
+                blocks = stats["lb_blocks"].numpy().astype(np.float64).sum()
+                ops = 3.0 * W * P.PARIS_INDEX_BLOCK * blocks / nbatches
+                ach = ops / (per_launch_ms / 1e3) / 1e12
+                roof = {"kernel": dom, "bound": "alu", "achieved": ach, "peak": pk,
+                        "unit": "Tops/s (fp16x2 half-ops)", "frac": ach / pk,
+                        "traffic": ncu_traffic(dom + "_index", args.config),
+                        "algorithmic_ops_per_launch": ops, "launch_ms": per_launch_ms, "peak_source": alu_src,
+                        "active_block_frac": blocks / (nq * (n / P.PARIS_INDEX_BLOCK)),
+                        "hbm_achieved_gbs": alg[dom] / (per_launch_ms / 1e3) / 1e9, "hbm_peak_gbs": peak,
+                        "queries_per_pass": q_per_pass}
+            elif dom == "lb_pass" and q_per_pass > 1.5:
+                # batched fp16x2 LB: bound by the FMA pipe, not HBM (DESIGN.md §6): 3 half-precision
+                # FMA-pipe ops per (series, segment, query)
+                ops = 3.0 * n * W * q_per_pass
+                ach = ops / (per_launch_ms / 1e3) / 1e12
+                roof = {"kernel": dom, "bound": "alu", "achieved": ach, "peak": pk,
+                        "unit": "Tops/s (fp16x2 half-ops)", "frac": ach / pk,
+                        "traffic": ncu_traffic(dom, args.config),
+                        "algorithmic_ops_per_launch": ops, "launch_ms": per_launch_ms, "peak_source": alu_src,
+                        "hbm_achieved_gbs": alg[dom] / (per_launch_ms / 1e3) / 1e9, "hbm_peak_gbs": peak,
+                        "queries_per_pass": q_per_pass}
+            elif dom in alg:
+                ach = alg[dom] / (per_launch_ms / 1e3) / 1e9
+                roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                        "frac": ach / peak, "traffic": ncu_traffic(dom + ("_index" if use_index else ""), args.config),
+                        "algorithmic_bytes_per_launch": alg[dom], "launch_ms": per_launch_ms,
+                        "peak_source": peak_src}
+        r.update(kern=kern, roof=roof, cand=cand, refined=refined)
+        return r
+
+    primary = measure_path(args.path, True)
+    secondary = None
+    if args.both:
+        secondary = measure_path("flat" if args.path == "index" else "index", False)
+
+    def knn_flat(qsrc, **kw):
+        return P.knn_exact(raw, sax, qsrc, k=k, w=W, card=CARD, **kw)
+    stats, kern, roof = primary["stats"], primary["kern"], primary["roof"]
+    cand, refined = primary["cand"], primary["refined"]
+    value, step_ms_max, launches, clocks = primary["value"], primary["step_ms"], primary["launches"], primary["clocks"]
+    e2e_value = primary["e2e_value"]
+
+    # ---- flat LB pass at one query per SAX read: the HBM-roofline configuration of K4 (SURVEY §7 hard part 1)
     lb1 = None
     if not args.no_b1:
         nq1 = min(nq, 8)
         cfg1 = P.KnnConfig(batch=1)
-        knn(queries[:nq1], config=cfg1)
+        knn_flat(queries[:nq1], config=cfg1)
         torch.cuda.synchronize()
         P.profile_reset()
         P.profile_enable(True)
-        _, _, st1 = knn(queries[:nq1], config=cfg1, stats=True)
+        _, _, st1 = knn_flat(queries[:nq1], config=cfg1, stats=True)
         P.profile_enable(False)
         pr1 = P.profile_read()
         if "lb_pass" in pr1:
@@ -427,11 +441,15 @@ def run_gpu(args):
                        "l2": "inputs larger than L2 (no flush)"},
             "roofline": roof,
             "lb_batch1": lb1,
+            "other_path": None if secondary is None else {
+                "path": secondary["path"], "value": secondary["value"], "ms_per_step": secondary["step_ms"],
+                "roofline": secondary["roof"], "kernels": secondary["kern"],
+                "candidates_mean": float(secondary["cand"].mean()), "refined_mean": float(secondary["refined"].mean())},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": nq * length * 4,
                     "d2h_bytes_per_step": nq * k * 12},
             "gpu_launches": launches,
-            "clocks": clocks.summary(),
+            "clocks": clocks,
             "summarize": summarize,
             "kernels": kern,
             "pruning": {"candidates_mean": float(cand.mean()), "candidates_p50": float(np.median(cand)),
@@ -455,7 +473,8 @@ def main():
     ap.add_argument("--impl", default="paris", choices=["paris", "reference"])
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--index-seeds", type=int, default=0, help="index path: seed series around the leaf")
-    ap.add_argument("--path", default="flat", choices=["flat", "index"],
+    ap.add_argument("--both", type=int, default=1, help="also time the other query path (reported as a sub-object)")
+    ap.add_argument("--path", default="index", choices=["flat", "index"],
                     help="flat: paris_knn_exact over the SAX array (ParIS+ Alg9); index: paris_knn_index over "
                          "the iSAX-ordered array with block envelopes (SURVEY f1)")
     ap.add_argument("--n", type=int, default=0, help="override n (debug only)")
