@@ -212,7 +212,6 @@ def run_gpu(args):
         n = args.n
     if args.nq:
         nq = args.nq
-    batch = args.batch or 16
     call_q = cfg.get("call", nq)  # queries per paris_knn_exact call (C3: batches of 64)
     ds, qs = rank_seeds(args.config, rank)
 
@@ -226,7 +225,6 @@ def run_gpu(args):
     torch.cuda.synchronize()
     log(f"rank {rank}: generated n={n} len={length} nq={nq} in {time.time() - t0:.1f}s")
     st = torch.cuda.current_stream()
-    kcfg = P.KnnConfig(batch=batch, index_seeds=args.index_seeds)
 
     # ---- summarize (rows a1-a2): warmup + timed
     for _ in range(args.warmup):
@@ -252,15 +250,16 @@ def run_gpu(args):
         torch.cuda.synchronize()
         index_ms = e0.elapsed_time(e1)
     peak, peak_src = measured_peaks()
-    ncalls = (nq + call_q - 1) // call_q
-    nbatches = sum((min(call_q, nq - c0) + batch - 1) // batch for c0 in range(0, nq, call_q))
-    q_per_pass = nq / nbatches
 
     def measure_path(path: str, full: bool):
         """Warm up, time K steps of `path` (device events, max over ranks), then the same K
         steps with per-launch events for the kernel split and the roofline; with full=True
         also the end-to-end variant through host buffers and the clock record."""
         use_index = path == "index"
+        b_path = args.batch or (32 if use_index else 16)  # the library's default queries per pass
+        kcfg = P.KnnConfig(batch=b_path, index_seeds=args.index_seeds)
+        nbatches = sum((min(call_q, nq - c0) + b_path - 1) // b_path for c0 in range(0, nq, call_q))
+        q_per_pass = nq / nbatches
 
         def knn(qsrc, **kw):
             if use_index:
@@ -375,7 +374,7 @@ def run_gpu(args):
                         "frac": ach / peak, "traffic": ncu_traffic(dom + ("_index" if use_index else ""), args.config),
                         "algorithmic_bytes_per_launch": alg[dom], "launch_ms": per_launch_ms,
                         "peak_source": peak_src}
-        r.update(kern=kern, roof=roof, cand=cand, refined=refined)
+        r.update(kern=kern, roof=roof, cand=cand, refined=refined, batch=b_path)
         return r
 
     primary = measure_path(args.path, True)
@@ -437,7 +436,7 @@ def run_gpu(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded Philox random walks, z-normalized; no dataset on the box)",
             "config": {"workload": cfg["desc"], "n": n, "len": length, "w": W, "card": CARD, "nq": nq, "k": k,
-                       "batch": batch, "path": args.path, "index_build_ms": index_ms, "parallelism": f"weak x{ws} (independent collections + queries per GPU)",
+                       "batch": primary["batch"], "path": args.path, "index_build_ms": index_ms, "parallelism": f"weak x{ws} (independent collections + queries per GPU)",
                        "l2": "inputs larger than L2 (no flush)"},
             "roofline": roof,
             "lb_batch1": lb1,

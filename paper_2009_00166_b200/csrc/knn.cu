@@ -39,7 +39,8 @@ namespace {
 
 constexpr int kMaxW = 64;
 constexpr int kNB = 256;            // LB histogram bins per query
-constexpr int kMaxB = 16;           // queries per SAX pass
+constexpr int kMaxB = 32;           // queries per SAX pass (index path)
+constexpr int kMaxBFlat = 16;       // queries per SAX pass (flat path: P <= 8 pairs)
 constexpr int kLBThreads = 256;
 constexpr int kRefThreads = 256;
 constexpr int kRefWarps = kRefThreads / 32;
@@ -788,6 +789,7 @@ constexpr int kStages = 4;
 constexpr int kTW = 16;
 constexpr size_t kTileBytes = (size_t)kTW * kTS;
 constexpr size_t kTSmem = kStages * kTileBytes + kMaxCard * 32 * 4;
+constexpr size_t kLbiSmem = kTSmem + (size_t)kMaxB * kNB * 4;  // + the LB histograms
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -834,40 +836,6 @@ __device__ __forceinline__ void lbt_seg(uint32_t word, const uint32_t* __restric
   }
 }
 
-// Block MINDIST (the iSAX node bound) of this warp's 128-series block for every
-// query slot, from the block's per-segment [min, max] symbols: region
-// [L[min], U[max]] (outward fp32), round-down arithmetic -> bit b set iff the
-// block's LB^2 <= thr[b] (only then can one of its series be a candidate).
-__device__ __forceinline__ uint32_t block_mask(const uint8_t* __restrict__ env, int64_t blk, int nslots,
-                                               const float2* __restrict__ s_q, const float2* __restrict__ s_lu,
-                                               const LbConsts& c, float seglen) {
-  const int lane = threadIdx.x & 31;
-  const int b = lane >> 1, h = lane & 1;
-  float acc = 0.f;
-  if (b < nslots) {
-    const uint2 mn = __ldg(reinterpret_cast<const uint2*>(env + (size_t)blk * 32 + 8 * h));
-    const uint2 mx = __ldg(reinterpret_cast<const uint2*>(env + (size_t)blk * 32 + 16 + 8 * h));
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int seg = 8 * h + k;
-      const uint32_t cmin = ((k < 4 ? mn.x : mn.y) >> (8 * (k & 3))) & 0xFFu;
-      const uint32_t cmax = ((k < 4 ? mx.x : mx.y) >> (8 * (k & 3))) & 0xFFu;
-      const float2 q = s_q[b * kMaxW + seg];
-      const float above = __fsub_rd(q.x, s_lu[cmax].y);
-      const float below = __fsub_rd(s_lu[cmin].x, q.y);
-      const float delta = fmax3(above, below, 0.f);
-      acc = __fmaf_rd(delta, delta, acc);
-    }
-  }
-  acc = __fadd_rd(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
-  const bool act = (b < nslots) && h == 0 && __fmul_rd(acc, seglen) <= c.thr[b];
-  const uint32_t m = __ballot_sync(0xffffffffu, act);
-  uint32_t r = 0;
-#pragma unroll
-  for (int k = 0; k < 16; ++k) r |= ((m >> (2 * k)) & 1u) << k;
-  return r;
-}
-
 // Single-query form (B = 1): qd = half2(q_lo16, -q_hi16) against (-U16, L16):
 // one relu-FMA gives (relu(q-U), relu(L-q)), one FMA accumulates both halves
 // (at most one is non-zero); the LB sum is lo + hi at the end.
@@ -896,7 +864,7 @@ k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
   __shared__ uint2 s_q16[PP * kTW];
   __shared__ LbConsts s_c;
   __shared__ WarpBuf s_wb[MODE == 1 ? kTWarps : 1];
-  __shared__ unsigned s_hist[MODE == 1 ? kMaxB * kNB : 1];
+  __shared__ unsigned s_hist[MODE == 1 ? kMaxBFlat * kNB : 1];
   const int tid = threadIdx.x, lane = tid & 31;
   const int64_t ntiles = (nlim + kTS - 1) / kTS;
   const int nslots = P > 0 ? 2 * P : 1;
@@ -1167,12 +1135,12 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
   // at uint2 index 16c + (l % 16) -- a 64-bit load is served per half-warp, so the
   // 16 lanes of each half always hit distinct banks
   uint2* s_tab = reinterpret_cast<uint2*>(dsm + kStages * kTileBytes);
+  unsigned* s_hist = reinterpret_cast<unsigned*>(dsm + kTSmem);  // [kMaxB][kNB] after the ring + table
   __shared__ __align__(8) uint64_t s_full[kStages];
   __shared__ unsigned s_cnt[kStages];
   __shared__ uint32_t s_qs[2 * P][kTW];  // per slot and segment: half2(q_lo16, -q_hi16)
   __shared__ LbConsts s_c;
   __shared__ WarpBuf s_wb[kTWarps];
-  __shared__ unsigned s_hist[kMaxB * kNB];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nslots = 2 * P;
   const int64_t nlist = *tile_count;
@@ -1743,7 +1711,7 @@ struct Plan {
   int idx_seeds;         // index mode: series around the query's leaf
 };
 
-int pairs_for(int nb) { return nb <= 2 ? 1 : nb <= 4 ? 2 : nb <= 8 ? 4 : 8; }
+int pairs_for(int nb) { return nb <= 2 ? 1 : nb <= 4 ? 2 : nb <= 8 ? 4 : nb <= 16 ? 8 : 16; }
 
 template <int P, int WT, bool AL>
 cudaError_t launch_seed(const Plan& p, const uint8_t* sax, const float* qb, int nb,
@@ -1823,7 +1791,7 @@ cudaError_t launch_index_lb(const Plan& p, const uint8_t* sax, int nb, const Car
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(k_lbi<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTSmem);
+    cudaError_t e = cudaFuncSetAttribute(k_lbi<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLbiSmem);
     if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
@@ -1839,7 +1807,7 @@ cudaError_t launch_index_lb(const Plan& p, const uint8_t* sax, int nb, const Car
                                ws.tile_count, ws.blocks);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(sms(), ntiles);
-  return PARIS_LAUNCH("lb_pass", k_lbi<P>, grid, kTThreads, kTSmem, st, la, ws.bmask, ws.tile_list, ws.tile_count);
+  return PARIS_LAUNCH("lb_pass", k_lbi<P>, grid, kTThreads, kLbiSmem, st, la, ws.bmask, ws.tile_list, ws.tile_count);
 }
 
 cudaError_t dispatch_index_lb(int nb, const Plan& p, const uint8_t* sax, const CardTables* tab, const Ws& ws,
@@ -1848,7 +1816,8 @@ cudaError_t dispatch_index_lb(int nb, const Plan& p, const uint8_t* sax, const C
     case 1: return launch_index_lb<1>(p, sax, nb, tab, ws, st, cap);
     case 2: return launch_index_lb<2>(p, sax, nb, tab, ws, st, cap);
     case 4: return launch_index_lb<4>(p, sax, nb, tab, ws, st, cap);
-    default: return launch_index_lb<8>(p, sax, nb, tab, ws, st, cap);
+    case 8: return launch_index_lb<8>(p, sax, nb, tab, ws, st, cap);
+    default: return launch_index_lb<16>(p, sax, nb, tab, ws, st, cap);
   }
 }
 
@@ -1869,7 +1838,8 @@ cudaError_t launch_qprep(int nb, const Plan& p, const float* qb, const Ws& ws, c
     case 1: return PARIS_LAUNCH("qprep", k_qprep<1>, 1, 256, 0, st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
     case 2: return PARIS_LAUNCH("qprep", k_qprep<2>, 1, 256, 0, st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
     case 4: return PARIS_LAUNCH("qprep", k_qprep<4>, 1, 256, 0, st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
-    default: return PARIS_LAUNCH("qprep", k_qprep<8>, 1, 256, 0, st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
+    case 8: return PARIS_LAUNCH("qprep", k_qprep<8>, 1, 256, 0, st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
+    default: return PARIS_LAUNCH("qprep", k_qprep<16>, 1, 256, 0, st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
   }
 }
 
@@ -2122,7 +2092,10 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
 
   Plan p;
   p.n = n; p.len = len; p.w = w; p.card = card; p.k = k;
-  p.B = (cfg && cfg->batch > 0) ? std::min(cfg->batch, kMaxB) : kMaxB;
+  {
+    const int cap_b = indexed ? kMaxB : kMaxBFlat;  // index: 32 queries per pass, flat: 16
+    p.B = (cfg && cfg->batch > 0) ? std::min(cfg->batch, cap_b) : cap_b;
+  }
   p.tiled = (n % 16 == 0) && (w == kTW) && (indexed || !(cfg && cfg->reserved[0] == 1));
   p.perm = perm;
   p.env = env;

@@ -57,7 +57,7 @@ def test_index_build_matches_definition(P, n, card):
         np.testing.assert_array_equal(env[blk, 1], seg.max(0))
 
 
-@pytest.mark.parametrize("n,nq,k", [(2048, 3, 1), (40_000, 16, 1), (40_000, 5, 10), (100_000, 21, 1),
+@pytest.mark.parametrize("n,nq,k", [(2048, 3, 1), (40_000, 16, 1), (40_000, 5, 10), (100_000, 21, 1), (100_000, 32, 1), (60_000, 45, 10),
                                     (100_000, 9, 100), (6000 * 16, 1, 1)])
 def test_knn_index_parity(P, n, nq, k):
     import torch
