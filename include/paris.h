@@ -114,11 +114,11 @@ int paris_index_build(const uint8_t* sax, int64_t n, int32_t w, int32_t card, ui
 
 /* Tunables for paris_knn_exact_ex (0 = library default). */
 typedef struct paris_knn_config {
-  int32_t batch;        /* queries per SAX pass (1..16); default 16 */
+  int32_t batch;        /* queries per SAX pass: 1..16 (flat, default 16), 1..32 (index, default 32) */
   int32_t seed_div;     /* seed sample = n / seed_div series (default 16) */
   int32_t wave_a;       /* k = 1: candidates per query refined in the first (lowest-LB) wave; default 2048 */
   int32_t reserved[5];  /* tuning/test hooks: [0] = 1 forces the direct-load LB kernels;
-                           [1] unused; [2] index mode: seed series around the leaf (0 = 4096) */
+                           [1] unused; [2] index mode: seed series around the leaf (0 = 1024) */
 } paris_knn_config;
 
 /* Per-query counters (host memory, arrays of nq), filled by paris_knn_exact_ex. */
@@ -141,7 +141,7 @@ int paris_knn_exact_ex(const float* raw, const uint8_t* sax, int64_t n, const fl
  * paris_index_build (same results; raw stays in its original order):
  *   1. approximate search: the query's own word is located in the
  *      sorted array (the leaf it would be inserted into); the true distances of
- *      the 1024 series around it give tau_seed;
+ *      the 1024 series around it (configurable) give tau_seed;
  *   2. LBC pass over the sorted SAX array: each block's envelope MINDIST (the
  *      iSAX node bound) is computed first and only the queries the block can hold
  *      candidates for are evaluated on its series;

@@ -47,11 +47,11 @@ class _KProf(ctypes.Structure):
 
 @dataclass
 class KnnConfig:
-    batch: int = 0      # queries per SAX pass (1..16), 0 = default (16)
+    batch: int = 0      # queries per SAX pass: flat 1..16 (default 16), index 1..32 (default 32)
     seed_div: int = 0   # seed sample = n / seed_div (0 = 16)
     wave_a: int = 0     # k = 1: first refinement wave per query (0 = 2048)
     force_direct: bool = False  # test hook: use the direct-load LB kernels even where the TMA-tiled ones apply
-    index_seeds: int = 0        # index mode: seed series around the query's leaf (0 = 4096)
+    index_seeds: int = 0        # index mode: seed series around the query's leaf (0 = 1024)
 
 
 def library_path() -> str:

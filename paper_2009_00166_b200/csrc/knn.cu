@@ -1412,15 +1412,24 @@ k_refine1(RefineArgs a, int nb) {
   // every warp walks its interleaved share of EVERY query's list (balanced work:
   // a query with 5x the mean candidate count no longer leaves most SMs idle); the
   // query rows are read through L1 (all warps of a CTA share them)
-  __shared__ unsigned s_refined[kMaxB];
+  __shared__ unsigned s_refined[kMaxB], s_cnt[kMaxB];
+  __shared__ float s_scale[kMaxB];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nf = a.len >> 2;
-  if (threadIdx.x < kMaxB) s_refined[threadIdx.x] = 0;
+  if (threadIdx.x < kMaxB) {
+    s_refined[threadIdx.x] = 0;
+    // per-query list lengths and bin scales, read once per CTA (queries with no work
+    // in this wave then cost a shared-memory read, not a global round trip)
+    s_cnt[threadIdx.x] = threadIdx.x < nb
+        ? (unsigned)imin64(imin64((int64_t)a.count[threadIdx.x], a.cap), (int64_t)a.hi) : 0u;
+    s_scale[threadIdx.x] = threadIdx.x < nb ? bin_scale(__uint_as_float(a.thr_seed[threadIdx.x])) : 0.f;
+  }
   __syncthreads();
   const unsigned gw = blockIdx.x * kRefWarps + warp, GW = gridDim.x * kRefWarps;
   for (int b = 0; b < nb; ++b) {
-    const unsigned cnt = (unsigned)imin64(imin64((int64_t)a.count[b], a.cap), (int64_t)a.hi);
-    const float scale = bin_scale(__uint_as_float(a.thr_seed[b]));
+    const unsigned cnt = s_cnt[b];
+    if (a.lo + gw >= cnt) continue;
+    const float scale = s_scale[b];
     const uint64_t* list = a.sorted + (size_t)b * a.cap + a.lo;
     const float4* qv = reinterpret_cast<const float4*>(a.queries + (size_t)b * a.len);
     unsigned long long* bp = a.best + (size_t)b * kPadU64;
@@ -2028,7 +2037,7 @@ bool is_host_ptr(const void* p) {
   return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered;
 }
 
-constexpr int kIdxSeeds = 4096;  // index mode: series around the query's leaf (default)
+constexpr int kIdxSeeds = 1024;  // index mode: series around the query's leaf (default)
 
 void plan_seed(Plan& p, int seed_div) {
   if (p.perm) {
