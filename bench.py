@@ -455,7 +455,13 @@ def run_gpu(args):
                         "candidates_max": float(cand.max()), "refined_mean": float(refined.mean()),
                         "refined_max": float(refined.max()),
                         "pruning_ratio": float(1.0 - refined.mean() / n),
-                        "tau_seed_mean": float(stats["tau_seed"].mean())},
+                        "tau_seed_mean": float(stats["tau_seed"].mean()),
+                        "lb_blocks_frac_p50": float(np.median(stats["lb_blocks"].numpy())) / max(1.0, n / 128),
+                        "lb_blocks_frac_max": float(stats["lb_blocks"].numpy().max()) / max(1.0, n / 128),
+                        "lb_blocks_frac_mean": float(stats["lb_blocks"].numpy().mean()) / max(1.0, n / 128),
+                        "lb_blocks_top5_share": float(np.sort(stats["lb_blocks"].numpy())[-5:].sum()
+                                                      / max(1, stats["lb_blocks"].numpy().sum())),
+                        "refined_top5_share": float(np.sort(refined)[-5:].sum() / max(1.0, refined.sum()))},
         }
         print(json.dumps(line), flush=True)
     if ws > 1:

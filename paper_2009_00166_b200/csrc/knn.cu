@@ -487,7 +487,10 @@ k_approx_seed(const uint8_t* __restrict__ sax_sorted, const uint32_t* __restrict
   const int64_t cnt = min((int64_t)S, n);
   int64_t start = lo - cnt / 2;
   start = max((int64_t)0, min(start, n - cnt));
-  for (int t = lane; t < S; t += 32) seed_ids[b * S + t] = (t < cnt) ? (int)perm[start + t] : -1;
+  for (int t = lane; t < S; t += 32) {
+    PARIS_DCHECK(t >= cnt || (start + t >= 0 && start + t < n));
+    seed_ids[b * S + t] = (t < cnt) ? (int)perm[start + t] : -1;
+  }
 }
 
 // ---------------------------------------------------------------- K4 LBC pass
@@ -663,6 +666,7 @@ __device__ void wb_flush(WarpBuf& wb, int nslots, const LbConsts& c, const LbArg
   for (int e = lane; e < m; e += 32) {
     const int b = wb.slot[e];
     const uint64_t key = wb.key[e];
+    PARIS_DCHECK(b < nslots && key_id(key) < (uint64_t)a.n);
     const unsigned pos = atomicAdd(&wb.cur[b], 1u);
     // only stored candidates enter the histogram: on overflow (count > cap) the
     // bucket offsets must describe exactly the `cap` entries K5 orders
@@ -736,6 +740,7 @@ __device__ __forceinline__ void lb_emit_wb(const uint32_t (&acc)[4][P], int64_t 
       const float h = (b & 1) ? h_hi_f(v) : h_lo_f(v);
       const float lb = __fmul_rd(fmaxf(__fsub_rd(h, c.wabs), 0.f), c.lbconv);
       if (((h2_le_bits(v, T) >> (b & 1)) & 1u) && j < nvalid && lb <= c.thr[b + slot0]) {
+        PARIS_DCHECK(i0 + j < a.n && pos < kWB);
         wb.key[pos] = make_key(lb, perm ? __ldg(perm + i0 + j) : (uint32_t)(i0 + j));
         wb.slot[pos] = (uint8_t)(b + slot0);
         atomicAdd(&wb.cnt[b + slot0], 1u);
@@ -1054,6 +1059,7 @@ __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int s
   int pos = wb.n + incl - cntl;
   for (uint32_t r = pm; r; r &= r - 1) {
     const int bit = __ffs(r) - 1, j = bit >> 1, sl = (bit & 1) ? sb : sa;
+    PARIS_DCHECK(i0 + j < a.n && pos < kWB && sl >= 0);
     wb.key[pos] = make_key(lbv[j][bit & 1], __ldg(a.perm + i0 + j));
     wb.slot[pos] = (uint8_t)sl;
     atomicAdd(&wb.cnt[sl], 1u);
@@ -1185,6 +1191,7 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
     if (li >= nlist) break;
     const int st = (int)(it % kStages);
     const int64_t tile = tile_list[li];
+    PARIS_DCHECK(tile >= 0 && tile * kTS < a.n);
     // the tile's 16 block masks; a block's live slots are computed two at a time
     // (consecutive live slots form an item), items dealt round-robin to the warps
     uint32_t bm = 0;
@@ -1231,6 +1238,7 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
       }
       const int64_t i0 = tile * kTS + k * PARIS_INDEX_BLOCK + 4 * lane;
       const int nvalid = (int)std::max<int64_t>(0, imin64(4, a.n - i0));
+      PARIS_DCHECK(k < kTWarps && sa >= 0 && sa < nslots && sb < nslots);
       lbi_emit(acc, sa, sb, i0, nvalid, nslots, s_c, a, wb, s_hist);
     }
     __syncwarp();
@@ -1329,6 +1337,7 @@ struct RefineArgs {
   int k;
   float d2up;                // 1 + bound on the relative error of an fp32 d^2 (rounding up)
   unsigned lo, hi;           // k = 1: refine list positions [lo, min(hi, count)) (a wave)
+  int64_t n;                 // series in raw (debug bounds checks)
 };
 
 // One warp step: up to kU candidates (indices i0 + u*stride) against the live
@@ -1360,6 +1369,8 @@ __device__ __forceinline__ bool refine_step(const RefineArgs& a, const uint64_t*
   float acc[kU];
 #pragma unroll
   for (int u = 0; u < kU; ++u) acc[u] = 0.f;
+#pragma unroll
+  for (int u = 0; u < kU; ++u) PARIS_DCHECK(!live[u] || key_id(key[u]) < (uint64_t)a.n);
   for (int c0 = 0; c0 < nf; c0 += 32) {
     const int f = c0 + lane;
     float4 x[kU];
@@ -1457,6 +1468,8 @@ k_refine1(RefineArgs a, int nb) {
         }
       }
       float4 x[U][NC];
+#pragma unroll
+      for (int u = 0; u < U; ++u) PARIS_DCHECK(!live[u] || key_id(key[u]) < (uint64_t)a.n);
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -1970,7 +1983,7 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
   ra.raw = raw; ra.len = p.len; ra.queries = qbatch; ra.sorted = ws.sorted; ra.cap = cap;
   ra.count = ws.count; ra.thr_seed = ws.thr_seed; ra.thr = ws.thr; ra.best = ws.best;
   ra.refined = ws.refined; ra.lists = ws.lists; ra.k = p.k; ra.d2up = p.d2up;
-  ra.lo = 0; ra.hi = 0xFFFFFFFFu;
+  ra.lo = 0; ra.hi = 0xFFFFFFFFu; ra.n = p.n;
   dim3 g((unsigned)p.XB, (unsigned)nb);
   if (p.k == 1) {
     cudaError_t e1 = cudaSuccess;

@@ -89,6 +89,23 @@ struct LaunchScope {
 
 }  // namespace paris
 
+// Device-side bounds checks for debug builds (PARIS_DEBUG=1 at build time):
+// a violated check traps the kernel (cudaErrorLaunchFailure) instead of reading
+// or writing out of bounds.  Compiled out otherwise.
+#ifdef PARIS_DEBUG_CHECKS
+#define PARIS_DCHECK(cond)                                                             \
+  do {                                                                                 \
+    if (!(cond)) {                                                                     \
+      printf("PARIS_DCHECK failed: %s at %s:%d\n", #cond, __FILE__, __LINE__);         \
+      __trap();                                                                        \
+    }                                                                                  \
+  } while (0)
+#else
+#define PARIS_DCHECK(cond) \
+  do {                     \
+  } while (0)
+#endif
+
 // Launch a kernel with accounting; evaluates to the cudaError_t of the launch.
 #define PARIS_LAUNCH(name, kernel, grid, block, smem, stream, ...)            \
   ([&]() -> cudaError_t {                                                     \
