@@ -21,6 +21,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills"]
+if os.environ.get("PARIS_LB1_SPT"):  # tuning experiments only
+    FLAGS = FLAGS + [f"-DPARIS_LB1_SPT={int(os.environ['PARIS_LB1_SPT'])}"]
 if os.environ.get("PARIS_DEBUG"):  # device bounds checks (PARIS_DCHECK) -- debugging builds only
     FLAGS = FLAGS + ["-DPARIS_DEBUG_CHECKS"]
 SOURCES = ["runtime.cu", "summarize.cu", "knn.cu", "index.cu"]

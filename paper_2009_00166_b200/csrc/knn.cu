@@ -1259,6 +1259,93 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
     if (s_hist[i]) atomicAdd(&a.hist[i], s_hist[i]);
 }
 
+// ---------------------------------------------------------------- K4, one query per pass
+// B = 1 (flat path): the pass is one lookup + two FMAs per (series, segment), so
+// it is fed by plain 16-byte loads at high occupancy rather than the TMA ring
+// (whose 16 row copies per tile cap delivery near 2.7 TB/s): a thread owns 16
+// consecutive series (one uint4 per segment row, 256 B in flight), the region
+// table (-U16, L16) is replicated 32x in shared memory (conflict-free lookups),
+// and the single-query fp16x2 form accumulates (ABOVE, BELOW) per series.
+constexpr int kLb1Threads = 256;
+#ifndef PARIS_LB1_SPT
+#define PARIS_LB1_SPT 8
+#endif
+
+// SPT series per thread: 16 (one uint4 per row) or 8 (one uint2 per row, fewer
+// registers -> more resident warps).
+template <int SPT>
+__global__ void __launch_bounds__(kLb1Threads, SPT == 16 ? 2 : SPT == 8 ? 3 : 4)
+k_lb1(LbArgs a) {
+  __shared__ uint32_t s_tab[kMaxCard * 32];
+  __shared__ uint32_t s_qd[kTW];
+  __shared__ LbConsts s_c;
+  __shared__ WarpBuf s_wb[kLb1Threads / 32];
+  __shared__ unsigned s_hist[kNB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  WarpBuf& wb = s_wb[warp];
+  if (lane < kMaxB) wb.cnt[lane] = 0;
+  if (lane == 0) wb.n = 0;
+  for (int i = tid; i < kNB; i += kLb1Threads) s_hist[i] = 0;
+  for (int i = tid; i < kMaxCard * 32; i += kLb1Threads) s_tab[i] = a.tab->lu16p[i >> 5];
+  if (tid < kTW) {
+    const uint2 v = a.g_q16[tid];  // pair layout, slot 0 = low halves
+    s_qd[tid] = (v.x & 0xFFFFu) | (v.y << 16);
+  }
+  lb_consts_init(a, 1, &s_c);  // ends with __syncthreads
+  const uint32_t* tabl = s_tab + lane;
+  const int64_t n = a.n;
+  const int64_t ngroups = n / SPT;  // n % 16 == 0 (tiled-path condition)
+  for (int64_t g = (int64_t)blockIdx.x * kLb1Threads + tid; g - lane < ngroups;
+       g += (int64_t)gridDim.x * kLb1Threads) {
+    const int64_t i0 = (int64_t)SPT * g;
+    uint32_t acc[SPT];
+#pragma unroll
+    for (int j = 0; j < SPT; ++j) acc[j] = 0u;
+    if (g < ngroups) {
+      uint32_t wd[kTW][SPT / 4];
+#pragma unroll
+      for (int s = 0; s < kTW; ++s) {
+        if (SPT == 16) {
+          const uint4 v = __ldcs(reinterpret_cast<const uint4*>(a.sax + (size_t)s * n + i0));
+          wd[s][0] = v.x; wd[s][1 % (SPT / 4)] = v.y; wd[s][2 % (SPT / 4)] = v.z; wd[s][3 % (SPT / 4)] = v.w;
+        } else if (SPT == 8) {
+          const uint2 v = __ldcs(reinterpret_cast<const uint2*>(a.sax + (size_t)s * n + i0));
+          wd[s][0] = v.x; wd[s][1 % (SPT / 4)] = v.y;
+        } else {
+          wd[s][0] = __ldcs(reinterpret_cast<const uint32_t*>(a.sax + (size_t)s * n + i0));
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < kTW; ++s) {
+        const uint32_t qd = s_qd[s];
+#pragma unroll
+        for (int j = 0; j < SPT; ++j) {
+          const uint32_t t = tabl[__byte_perm(wd[s][j >> 2], 0, 0x4440 | (j & 3)) * 32];
+          const uint32_t d = h2_fma_relu(qd, kHalf2One, t);
+          acc[j] = h2_fma(d, d, acc[j]);
+        }
+      }
+    }
+    // LB16 = ABOVE + BELOW sums, rounded up into slot 0 (slot 1 = +inf never passes)
+#pragma unroll
+    for (int q4 = 0; q4 < SPT / 4; ++q4) {
+      uint32_t a4[4][1];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t v = acc[4 * q4 + j];
+        a4[j][0] = (uint32_t)__half_as_ushort(__float2half_ru(h_lo_f(v) + h_hi_f(v))) | (0x7C00u << 16);
+      }
+      const int64_t ib = i0 + 4 * q4;
+      const int nvalid = (g < ngroups) ? 4 : 0;
+      lb_emit_wb<1>(a4, ib, nvalid, 1, s_c, a, wb, s_hist);
+    }
+  }
+  wb_flush(wb, 1, s_c, a, s_hist);
+  __syncthreads();
+  for (int i = tid; i < kNB; i += kLb1Threads)
+    if (s_hist[i]) atomicAdd(&a.hist[i], s_hist[i]);
+}
+
 // Query prep alone (for the tiled seed, which has no prologue of its own).
 template <int P>
 __global__ void k_qprep(const float* __restrict__ queries, int nb, int len, int w, float2* __restrict__ g_q,
@@ -1843,6 +1930,22 @@ cudaError_t dispatch_index_lb(int nb, const Plan& p, const uint8_t* sax, const C
   }
 }
 
+cudaError_t launch_lb1(const Plan& p, const uint8_t* sax, const CardTables* tab, const Ws& ws, cudaStream_t st,
+                       int64_t cap) {
+  constexpr int SPT = PARIS_LB1_SPT;
+  static int occ = 0;
+  if (!occ) occ = occupancy(k_lb1<SPT>, kLb1Threads, 0);
+  LbArgs la;
+  la.sax = sax; la.n = p.n; la.w = p.w; la.seglen_f = (float)(p.len / p.w); la.tab = tab;
+  la.g_q = ws.g_q; la.g_q16 = ws.g_q16; la.nb = 1; la.thr = ws.thr_seed; la.count = ws.count;
+  la.hist = ws.hist; la.cand = ws.cand; la.cap = cap; la.perm = nullptr; la.env = nullptr;
+  la.blocks = ws.blocks;
+  const int64_t ngroups = p.n / SPT;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((ngroups + kLb1Threads - 1) / kLb1Threads,
+                                                              (int64_t)sms() * occ));
+  return PARIS_LAUNCH("lb_pass", k_lb1<SPT>, grid, kLb1Threads, 0, st, la);
+}
+
 template <int MODE>
 cudaError_t dispatch_lbt(int nb, const Plan& p, const uint8_t* sax, const CardTables* tab, const Ws& ws,
                          cudaStream_t st, int64_t cap, int64_t nlim, int grid) {
@@ -1968,6 +2071,7 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
   if (p.tiled) {
     const int grid = (int)std::min<int64_t>(sms(), (p.n + kTS - 1) / kTS);
     if (p.perm) PARIS_CHECK_LAUNCH(dispatch_index_lb(nb, p, sax, tab, ws, st, cap), "lb_pass launch");
+    else if (nb == 1) PARIS_CHECK_LAUNCH(launch_lb1(p, sax, tab, ws, st, cap), "lb_pass launch");
     else PARIS_CHECK_LAUNCH(dispatch_lbt<1>(nb, p, sax, tab, ws, st, cap, p.n, grid), "lb_pass launch");
   } else {
     PARIS_CHECK_LAUNCH(dispatch_p(P, true, p, sax, qbatch, nb, tab, ws, st, cap), "lb_pass launch");
