@@ -256,6 +256,7 @@ def run_gpu(args):
         steps with per-launch events for the kernel split and the roofline; with full=True
         also the end-to-end variant through host buffers and the clock record."""
         use_index = path == "index"
+        use_nb = path == "nb"
         b_path = args.batch or (32 if use_index else 16)  # the library's default queries per pass
         kcfg = P.KnnConfig(batch=b_path, index_seeds=args.index_seeds)
         nbatches = sum((min(call_q, nq - c0) + b_path - 1) // b_path for c0 in range(0, nq, call_q))
@@ -264,6 +265,8 @@ def run_gpu(args):
         def knn(qsrc, **kw):
             if use_index:
                 return P.knn_index(raw, index, qsrc, k=k, **kw)
+            if use_nb:
+                return P.knn_nb(raw, sax, qsrc, w=W, card=CARD, **kw)
             return P.knn_exact(raw, sax, qsrc, k=k, w=W, card=CARD, **kw)
 
         out_idx = torch.empty((nq, k), dtype=torch.int64, device=dev)
@@ -332,6 +335,8 @@ def run_gpu(args):
             "lb_pass": (nbatches * n * W + 8.0 * cand.sum()) / nbatches,
             # raw bytes per refined series (K6)
             "refine": 4.0 * length * refined.sum() / nbatches,
+            # nb-ParIS+ workers: the SAX array + the raw series they read
+            "nb_distcomp": (nbatches * n * W + 4.0 * length * refined.sum()) / nbatches,
         }
         for name, v in kern.items():
             if name in alg:
@@ -375,12 +380,14 @@ def run_gpu(args):
                         "algorithmic_bytes_per_launch": alg[dom], "launch_ms": per_launch_ms,
                         "peak_source": peak_src}
         r.update(kern=kern, roof=roof, cand=cand, refined=refined, batch=b_path)
+        if use_nb:
+            r["bsf_updates_mean"] = float(stats["bsf_updates"].numpy().astype(np.float64).mean())
         return r
 
     primary = measure_path(args.path, True)
     secondary = None
     if args.both:
-        secondary = measure_path("flat" if args.path == "index" else "index", False)
+        secondary = measure_path("flat" if args.path in ("index", "nb") else "index", False)
 
     def knn_flat(qsrc, **kw):
         return P.knn_exact(raw, sax, qsrc, k=k, w=W, card=CARD, **kw)
@@ -461,7 +468,8 @@ def run_gpu(args):
                         "lb_blocks_frac_mean": float(stats["lb_blocks"].numpy().mean()) / max(1.0, n / 128),
                         "lb_blocks_top5_share": float(np.sort(stats["lb_blocks"].numpy())[-5:].sum()
                                                       / max(1, stats["lb_blocks"].numpy().sum())),
-                        "refined_top5_share": float(np.sort(refined)[-5:].sum() / max(1.0, refined.sum()))},
+                        "refined_top5_share": float(np.sort(refined)[-5:].sum() / max(1.0, refined.sum())),
+                        "bsf_updates_mean": primary.get("bsf_updates_mean")},
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -479,7 +487,7 @@ def main():
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--index-seeds", type=int, default=0, help="index path: seed series around the leaf")
     ap.add_argument("--both", type=int, default=1, help="also time the other query path (reported as a sub-object)")
-    ap.add_argument("--path", default="index", choices=["flat", "index"],
+    ap.add_argument("--path", default="index", choices=["flat", "index", "nb"],
                     help="flat: paris_knn_exact over the SAX array (ParIS+ Alg9); index: paris_knn_index over "
                          "the iSAX-ordered array with block envelopes (SURVEY f1)")
     ap.add_argument("--n", type=int, default=0, help="override n (debug only)")

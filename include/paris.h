@@ -128,6 +128,7 @@ typedef struct paris_knn_stats {
   float* tau_seed;      /* seed BSF distance (rooted)                                 */
   int64_t* lb_blocks;   /* index mode: PARIS_INDEX_BLOCK-series blocks whose envelope
                            bound passed (their series' LBs were computed); 0 otherwise */
+  int64_t* bsf_updates; /* paris_knn_nb: updates of the workers' private BSF copies   */
 } paris_knn_stats;
 
 /* Same as paris_knn_exact with tunables and optional stats (either may be NULL). */
@@ -157,11 +158,27 @@ int paris_knn_index_ex(const float* raw, const uint8_t* sax_sorted, const uint32
                        float* out_dist, int32_t len, int32_t w, int32_t card, void* stream,
                        const paris_knn_config* config, paris_knn_stats* stats);
 
+/*
+ * paris_knn_nb -- exact 1-NN with nb-ParIS+ (Alg7-Alg8,
+ * P:1158-1246): the same seed as paris_knn_exact (approximate search analog),
+ * then SAX is split into contiguous parts, one per DistComp worker (a warp);
+ * each worker keeps its own copy of the BSF per query (no communication while
+ * scanning), computes the lower bound of every word of its part and refines a
+ * series at once when its bound is below that copy; the answer is the minimum
+ * over the copies.  The ablation of ParIS+'s shared candidate list: stats report
+ * raw series read (refined) and BSF-copy updates (bsf_updates) -- the quantities
+ * of the paper's fig:notpruned.  k = 1 (out rows [nq][1]);
+ * w == 16, n % 4 == 0.  Same pointer/stream conventions as paris_knn_exact.
+ */
+int paris_knn_nb(const float* raw, const uint8_t* sax, int64_t n, const float* queries, int32_t nq,
+                 int64_t* out_idx, float* out_dist, int32_t len, int32_t w, int32_t card, void* stream,
+                 const paris_knn_config* config, paris_knn_stats* stats);
+
 /* Thread-local text of the last failure (never NULL). */
 const char* paris_last_error(void);
 
 /* ABI version (major*100 + minor). */
-int32_t paris_version(void);  /* 101: paris_knn_stats.lb_blocks, index API */
+int32_t paris_version(void);  /* 102: paris_knn_nb, paris_knn_stats.bsf_updates */
 
 /* Test hook: the library's own fp64 breakpoints cut_1..cut_{card-1} (R2) into
  * out[0..card-2] (host memory).  PARIS_ECONFIG for a bad card. */

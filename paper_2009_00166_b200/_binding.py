@@ -37,7 +37,8 @@ class _Config(ctypes.Structure):
 
 class _Stats(ctypes.Structure):
     _fields_ = [("candidates", ctypes.c_void_p), ("refined", ctypes.c_void_p),
-                ("tau_seed", ctypes.c_void_p), ("lb_blocks", ctypes.c_void_p)]
+                ("tau_seed", ctypes.c_void_p), ("lb_blocks", ctypes.c_void_p),
+                ("bsf_updates", ctypes.c_void_p)]
 
 
 class _KProf(ctypes.Structure):
@@ -83,6 +84,9 @@ def load():
         lib.paris_knn_index_ex.restype = ctypes.c_int
         lib.paris_knn_index.argtypes = [P, P, P, P, i64, P, i32, i32, P, P, i32, i32, i32, P]
         lib.paris_knn_index.restype = ctypes.c_int
+        lib.paris_knn_nb.argtypes = [P, P, i64, P, i32, P, P, i32, i32, i32, P, ctypes.POINTER(_Config),
+                                     ctypes.POINTER(_Stats)]
+        lib.paris_knn_nb.restype = ctypes.c_int
         lib.paris_last_error.restype = ctypes.c_char_p
         lib.paris_version.restype = i32
         lib.paris_profile_enable.argtypes = [i32]
@@ -188,10 +192,19 @@ def knn_index(raw: torch.Tensor, index: Index, queries: torch.Tensor, k: int = 1
                      out_dist=out_dist, stream=stream, config=config, stats=stats, _index=index)
 
 
+def knn_nb(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, w: int = 16, card: int = 256,
+           out_idx: torch.Tensor | None = None, out_dist: torch.Tensor | None = None, stream=None,
+           config: KnnConfig | None = None, stats: bool = False):
+    """Exact 1-NN with nb-ParIS+ (paris_knn_nb): per-worker BSF copies, fused LB -> refine."""
+    return knn_exact(raw, sax, queries, k=1, w=w, card=card, out_idx=out_idx, out_dist=out_dist, stream=stream,
+                     config=config, stats=stats, _nb=True)
+
+
 def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: int = 1,
               w: int = 16, card: int = 256, out_idx: torch.Tensor | None = None,
               out_dist: torch.Tensor | None = None, stream=None,
-              config: KnnConfig | None = None, stats: bool = False, _index: Index | None = None):
+              config: KnnConfig | None = None, stats: bool = False, _index: Index | None = None,
+              _nb: bool = False):
     """Exact k-NN of every query (rows of `queries`, CUDA or host) over raw/sax (CUDA).
 
     Returns (idx int64 [nq][k], dist float32 [nq][k]) on the device of `queries`
@@ -227,9 +240,17 @@ def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: in
     arrays = None
     if stats:
         arrays = (torch.zeros(nq, dtype=torch.int64), torch.zeros(nq, dtype=torch.int64),
-                  torch.zeros(nq, dtype=torch.float32), torch.zeros(nq, dtype=torch.int64))
-        st = _Stats(arrays[0].data_ptr(), arrays[1].data_ptr(), arrays[2].data_ptr(), arrays[3].data_ptr())
-    if _index is None:
+                  torch.zeros(nq, dtype=torch.float32), torch.zeros(nq, dtype=torch.int64),
+                  torch.zeros(nq, dtype=torch.int64))
+        st = _Stats(arrays[0].data_ptr(), arrays[1].data_ptr(), arrays[2].data_ptr(), arrays[3].data_ptr(),
+                    arrays[4].data_ptr())
+    if _nb:
+        if k != 1:
+            raise ValueError("knn_nb answers 1-NN (nb-ParIS+, Alg7-8)")
+        rc = lib.paris_knn_nb(raw.data_ptr(), sax.data_ptr(), n, queries.data_ptr(), nq, out_idx.data_ptr(),
+                              out_dist.data_ptr(), length, w, card, _stream(stream),
+                              ctypes.byref(cfg) if cfg else None, ctypes.byref(st) if st else None)
+    elif _index is None:
         rc = lib.paris_knn_exact_ex(raw.data_ptr(), sax.data_ptr(), n, queries.data_ptr(), nq, k,
                                     out_idx.data_ptr(), out_dist.data_ptr(), length, w, card,
                                     _stream(stream), ctypes.byref(cfg) if cfg else None,
@@ -242,7 +263,7 @@ def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: in
     _check(rc)
     if stats:
         return out_idx, out_dist, {"candidates": arrays[0], "refined": arrays[1],
-                                   "tau_seed": arrays[2], "lb_blocks": arrays[3]}
+                                   "tau_seed": arrays[2], "lb_blocks": arrays[3], "bsf_updates": arrays[4]}
     return out_idx, out_dist
 
 

@@ -1346,6 +1346,163 @@ k_lb1(LbArgs a) {
     if (s_hist[i]) atomicAdd(&a.hist[i], s_hist[i]);
 }
 
+// ---------------------------------------------------------------- f2: nb-ParIS+
+// nb-ParIS+ ExactSearch (Alg7) with DistComp workers (Alg8,
+// P:1223-1246): SAX is split into contiguous parts, one per worker (a warp); a
+// worker keeps its OWN copy of the BSF per query (V_bsf, registers -- no
+// communication while scanning), computes the lower bound of every word of its
+// part (the same batched fp16 form as the LBC pass) and, whenever one is below
+// its BSF, reads the raw series at once, computes the true distance (early
+// abandoning) and lowers its copy.  The answer is min(V_bsf)
+// (P:1208): one 64-bit atomicMin per worker and query at the end.  k = 1.
+struct NbArgs {
+  const uint8_t* sax;
+  int64_t n;
+  int w;
+  float seglen_f;
+  const CardTables* tab;
+  const uint2* g_q16;
+  const float* queries;      // [nb][len]
+  const float* raw;
+  int len;
+  int nb;
+  unsigned long long* best;  // [nb] padded: seed key in, min(V_bsf) out
+  unsigned* refined;         // raw series read, per query
+  unsigned* updates;         // V_bsf updates, per query
+  float d2up;
+  int64_t part;              // series per worker (multiple of 4)
+};
+
+template <int P>
+__global__ void __launch_bounds__(kLBThreads)
+k_nb(NbArgs a) {
+  constexpr int NS = 2 * P;
+  __shared__ uint2 s_lu16[kMaxCard];
+  __shared__ uint2 s_q16[P * kMaxW];
+  __shared__ float2 s_lu[kMaxCard];
+  __shared__ float s_grow;
+  const int lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < kMaxCard; i += blockDim.x) {
+    s_lu16[i] = a.tab->lu16[i];
+    s_lu[i] = a.tab->lu[i];
+  }
+  for (int i = threadIdx.x; i < P * kMaxW; i += blockDim.x) s_q16[i] = a.g_q16[i];
+  if (threadIdx.x == 0) s_grow = (float)(pow(1.0 + 1.0 / 2048.0, (double)(a.w + 4)) * (1.0 + 1e-12));
+  __syncthreads();
+  const float lbconv = __fdiv_rd(a.seglen_f, s_grow);
+  const float wabs = (float)a.w * 5.9604644775390625e-08f;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t lo = gw * a.part, hi = imin64(a.n, lo + a.part);
+  // private BSF copies (V_bsf) seeded with the approximate search's BSF
+  uint64_t bkey[NS];
+  float thr[NS];
+  unsigned nref[NS], nupd[NS];
+#pragma unroll
+  for (int b = 0; b < NS; ++b) {
+    bkey[b] = (b < a.nb) ? a.best[(size_t)b * kPadU64] : kNoKey;
+    thr[b] = (b < a.nb && bkey[b] != kNoKey) ? __fmul_ru(key_val(bkey[b]), a.d2up) : (b < a.nb ? INFINITY : -1.f);
+    nref[b] = 0;
+    nupd[b] = 0;
+  }
+  auto t16 = [&](float t) -> uint32_t {  // fp16 filter threshold of a private BSF (see k_lb)
+    if (t < 0.f) return kHalfNeg1;
+    const float T = __fadd_ru(__fmul_ru(__fdiv_ru(t, a.seglen_f), s_grow), wabs);
+    return (T > 64000.f) ? 0x7C00u : (uint32_t)__half_as_ushort(__float2half_ru(T));
+  };
+  uint32_t T16[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) T16[p] = t16(thr[2 * p]) | (t16(thr[2 * p + 1]) << 16);
+
+  for (int64_t base = lo; base < hi; base += 128) {
+    const int64_t i0 = base + 4 * lane;
+    uint32_t acc[4][P];
+    const int nvalid = (int)std::max<int64_t>(0, imin64(4, hi - i0));
+    if (nvalid > 0) lb16_group<P, 16, true>(a.sax, a.n, a.w, i0, s_q16, s_lu16, acc);
+    else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int p = 0; p < P; ++p) acc[j][p] = 0x7C007C00u;
+    }
+    // (series j, slot b) pairs of this lane passing the fp16 test: bit 4b + j
+    uint64_t cm = 0;
+#pragma unroll
+    for (int p = 0; p < P; ++p)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t pb = (j < nvalid) ? h2_le_bits(acc[j][p], T16[p]) : 0u;
+        cm |= (uint64_t)(pb & 1u) << (8 * p + j);
+        cm |= (uint64_t)((pb >> 1) & 1u) << (8 * p + 4 + j);
+      }
+    // DistComp (Alg8 lines 4-8): the warp refines its candidates one at a time
+    while (true) {
+      const unsigned lanes = __ballot_sync(0xffffffffu, cm != 0);
+      if (!lanes) break;
+      const int L = __ffs(lanes) - 1;
+      const uint64_t cmL = __shfl_sync(0xffffffffu, cm, L);
+      const int bit = __ffsll((long long)cmL) - 1;
+      const int b = bit >> 2, j = bit & 3;
+      if (lane == L) cm &= ~(1ull << bit);
+      uint32_t v = 0;
+#pragma unroll
+      for (int p = 0; p < P; ++p)
+        if (p == (b >> 1)) v = acc[j][p];
+      v = __shfl_sync(0xffffffffu, v, L);
+      const float h = (b & 1) ? h_hi_f(v) : h_lo_f(v);
+      const float lb = __fmul_rd(fmaxf(__fsub_rd(h, wabs), 0.f), lbconv);
+      float tb = 0.f;
+#pragma unroll
+      for (int q = 0; q < NS; ++q)
+        if (q == b) tb = thr[q];
+      if (!(lb <= tb)) continue;  // minDist < BSF (line 4), against the worker's own copy
+      const int64_t id = base + 4 * L + j;
+      // realDist = Dist(rawData, TS) with early abandoning at the worker's BSF
+      const float4* row = reinterpret_cast<const float4*>(a.raw + (size_t)id * a.len);
+      const float4* qv = reinterpret_cast<const float4*>(a.queries + (size_t)b * a.len);
+      const int nf = a.len >> 2;
+      float accd = 0.f;
+      bool abandoned = false;
+      for (int c0 = 0; c0 < nf; c0 += 32) {
+        const int f = c0 + lane;
+        if (f < nf) {
+          const float4 x = ld_stream(row + f), y = __ldg(qv + f);
+          float d;
+          d = x.x - y.x; accd = fmaf(d, d, accd);
+          d = x.y - y.y; accd = fmaf(d, d, accd);
+          d = x.z - y.z; accd = fmaf(d, d, accd);
+          d = x.w - y.w; accd = fmaf(d, d, accd);
+        }
+        if (c0 + 32 < nf && warp_sum(accd) > tb) { abandoned = true; break; }
+      }
+#pragma unroll
+      for (int q = 0; q < NS; ++q)
+        if (q == b) ++nref[q];
+      if (abandoned) continue;
+      const uint64_t k2 = make_key(warp_sum(accd), (uint32_t)id);
+#pragma unroll
+      for (int q = 0; q < NS; ++q) {
+        if (q == b && k2 < bkey[q]) {  // line 7-8: realDist < BSF -> BSF = realDist
+          bkey[q] = k2;
+          thr[q] = __fmul_ru(key_val(k2), a.d2up);
+          ++nupd[q];
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < P; ++p) T16[p] = t16(thr[2 * p]) | (t16(thr[2 * p + 1]) << 16);
+    }
+  }
+  // return min(V_bsf) (Alg7 line 9)
+  if (lane == 0) {
+#pragma unroll
+    for (int b = 0; b < NS; ++b) {
+      if (b >= a.nb) break;
+      if (bkey[b] != kNoKey) atomicMin(a.best + (size_t)b * kPadU64, (unsigned long long)bkey[b]);
+      if (nref[b]) atomicAdd(&a.refined[b], nref[b]);
+      if (nupd[b]) atomicAdd(&a.updates[b], nupd[b]);
+    }
+  }
+}
+
 // Query prep alone (for the tiled seed, which has no prologue of its own).
 template <int P>
 __global__ void k_qprep(const float* __restrict__ queries, int nb, int len, int w, float2* __restrict__ g_q,
@@ -1791,6 +1948,7 @@ struct Ws {
   unsigned* refined;
   unsigned* blocks;      // index mode: blocks whose envelope bound passed, per query
   unsigned* tile_count;  // index mode: live tiles listed
+  unsigned* updates;     // nb mode: V_bsf updates per query
   unsigned* bmask;       // index mode: [ntiles*16] per-block live query-slot masks
   unsigned* tile_list;   // index mode: live tiles
   unsigned* tile_flag;   // index mode: [ntiles] tile already listed (zeroed per batch)
@@ -1818,6 +1976,7 @@ struct Plan {
   const uint32_t* perm;  // index mode (paris_knn_index): sorted position -> id
   const uint8_t* env;    // index mode: block envelopes
   int idx_seeds;         // index mode: series around the query's leaf
+  bool nb;               // f2: nb-ParIS+ (per-worker BSF copies, fused LB -> refine)
 };
 
 int pairs_for(int nb) { return nb <= 2 ? 1 : nb <= 4 ? 2 : nb <= 8 ? 4 : nb <= 16 ? 8 : 16; }
@@ -1930,6 +2089,30 @@ cudaError_t dispatch_index_lb(int nb, const Plan& p, const uint8_t* sax, const C
   }
 }
 
+template <int P, bool AL>
+cudaError_t launch_nb_t(const Plan& p, const float* raw, const uint8_t* sax, const float* qb, int nb,
+                        const CardTables* tab, const Ws& ws, cudaStream_t st) {
+  NbArgs na;
+  na.sax = sax; na.n = p.n; na.w = p.w; na.seglen_f = (float)(p.len / p.w); na.tab = tab; na.g_q16 = ws.g_q16;
+  na.queries = qb; na.raw = raw; na.len = p.len; na.nb = nb; na.best = ws.best; na.refined = ws.refined;
+  na.updates = ws.updates; na.d2up = p.d2up;
+  const int64_t workers = (int64_t)sms() * 8 * (kLBThreads / 32);
+  na.part = std::max<int64_t>(128, ((p.n + workers - 1) / workers + 127) / 128 * 128);
+  const int64_t nwarps = (p.n + na.part - 1) / na.part;
+  const int grid = (int)((nwarps * 32 + kLBThreads - 1) / kLBThreads);
+  return PARIS_LAUNCH("nb_distcomp", (k_nb<P>), grid, kLBThreads, 0, st, na);
+}
+
+cudaError_t launch_nb(const Plan& p, const float* raw, const uint8_t* sax, const float* qb, int nb,
+                      const CardTables* tab, const Ws& ws, cudaStream_t st) {
+  switch (pairs_for(nb)) {
+    case 1: return launch_nb_t<1, true>(p, raw, sax, qb, nb, tab, ws, st);
+    case 2: return launch_nb_t<2, true>(p, raw, sax, qb, nb, tab, ws, st);
+    case 4: return launch_nb_t<4, true>(p, raw, sax, qb, nb, tab, ws, st);
+    default: return launch_nb_t<8, true>(p, raw, sax, qb, nb, tab, ws, st);
+  }
+}
+
 cudaError_t launch_lb1(const Plan& p, const uint8_t* sax, const CardTables* tab, const Ws& ws, cudaStream_t st,
                        int64_t cap) {
   constexpr int SPT = PARIS_LB1_SPT;
@@ -1986,7 +2169,7 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   const size_t o_q16 = take(sizeof(uint2) * (B / 2) * kMaxW);
   const size_t o_sid = take(sizeof(int) * B * p.S);
   const size_t o_skey = take(sizeof(uint64_t) * B * p.S);
-  const size_t zb = sizeof(unsigned) * (B + B + B * kNB + B * kNB + B + B + 1);
+  const size_t zb = sizeof(unsigned) * (B + B + B * kNB + B * kNB + B + B + 1 + B);
   const size_t o_zero = take(zb);
   const size_t o_best = take(sizeof(unsigned long long) * B * kPadU64);
   const size_t o_thr = take(sizeof(unsigned) * B * kPadU32);
@@ -2020,6 +2203,7 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   ws.refined = ws.cursor + B * kNB;
   ws.blocks = ws.refined + B;
   ws.tile_count = ws.blocks + B;
+  ws.updates = ws.tile_count + 1;
   ws.best = (unsigned long long*)(c + o_best);
   ws.cand = (uint64_t*)(c + o_cand);
   ws.sorted = (uint64_t*)(c + o_sorted);
@@ -2067,6 +2251,15 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
     PARIS_CHECK_LAUNCH(PARIS_LAUNCH("seed_select", k_seed_select, nb, 1024, 0, st, ws.seed_keys, p.S, p.k,
                                     p.d2up, ws.thr, ws.thr_seed, ws.best, all_tau, q0),
                        "seed_select launch");
+  }
+  if (p.nb) {
+    // f2: nb-ParIS+ -- no candidate list: fused LB -> refine per worker, then min(V_bsf)
+    PARIS_CHECK_LAUNCH(launch_nb(p, raw, sax, qbatch, nb, tab, ws, st), "nb launch");
+    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("finalize", k_finalize1, 1, 32, 0, st, ws.best, nb, q0, d_idx, d_dist,
+                                    ws.count, ws.refined, all_count, all_refined, rescan ? 1 : 0,
+                                    ws.updates, all_blocks),
+                       "finalize launch");
+    return PARIS_OK;
   }
   if (p.tiled) {
     const int grid = (int)std::min<int64_t>(sms(), (p.n + kTS - 1) / kTS);
@@ -2185,7 +2378,11 @@ void plan_refine(Plan& p) {
 int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queries, int nq, int k,
              int64_t* out_idx, float* out_dist, int len, int w, int card, cudaStream_t st,
              const paris_knn_config* cfg, paris_knn_stats* stats, const uint32_t* perm = nullptr,
-             const uint8_t* env = nullptr) {
+             const uint8_t* env = nullptr, bool nb_mode = false) {
+  if (nb_mode && (k != 1 || w != kTW || n % 4 != 0)) {
+    set_error("paris_knn_nb: needs k == 1, w == 16, n %% 4 == 0 (k=%d, w=%d, n=%lld)", k, w, (long long)n);
+    return k != 1 ? PARIS_EINVAL : PARIS_ECONFIG;
+  }
   const bool indexed = perm || env;
   if (indexed && (!perm || !env)) {
     set_error("paris_knn_index: null perm/env");
@@ -2225,9 +2422,10 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   p.tiled = (n % 16 == 0) && (w == kTW) && (indexed || !(cfg && cfg->reserved[0] == 1));
   p.perm = perm;
   p.env = env;
+  p.nb = nb_mode;
   p.idx_seeds = cfg ? cfg->reserved[2] : 0;
   plan_seed(p, (cfg && cfg->seed_div > 0) ? cfg->seed_div : 16);
-  p.cap = std::min<int64_t>(n, std::max<int64_t>(65536, n / 32));
+  p.cap = nb_mode ? 1 : std::min<int64_t>(n, std::max<int64_t>(65536, n / 32));
   plan_refine(p);
   p.wave_a = (cfg && cfg->wave_a > 0) ? cfg->wave_a : 2048;
   // |fp32 d^2 - exact| <= e d^2 with e = (len/32 + 8) u (warp_ed2 / refine_step);
@@ -2317,7 +2515,8 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
         if (stats->candidates) stats->candidates[q] = h_count[q];
         if (stats->refined) stats->refined[q] = h_ref[q];
         if (stats->tau_seed) stats->tau_seed[q] = h_tau[q];
-        if (stats->lb_blocks) stats->lb_blocks[q] = h_blk[q];
+        if (stats->lb_blocks) stats->lb_blocks[q] = p.nb ? 0 : h_blk[q];
+        if (stats->bsf_updates) stats->bsf_updates[q] = p.nb ? h_blk[q] : 0;
       }
     }
   }
@@ -2343,6 +2542,13 @@ int paris_knn_exact_ex(const float* raw, const uint8_t* sax, int64_t n, const fl
                        paris_knn_stats* stats) {
   return paris::knn_impl(raw, sax, n, queries, nq, k, out_idx, out_dist, len, w, card,
                          (cudaStream_t)stream, config, stats);
+}
+
+int paris_knn_nb(const float* raw, const uint8_t* sax, int64_t n, const float* queries, int32_t nq,
+                 int64_t* out_idx, float* out_dist, int32_t len, int32_t w, int32_t card, void* stream,
+                 const paris_knn_config* config, paris_knn_stats* stats) {
+  return paris::knn_impl(raw, sax, n, queries, nq, 1, out_idx, out_dist, len, w, card, (cudaStream_t)stream,
+                         config, stats, nullptr, nullptr, /*nb_mode=*/true);
 }
 
 int paris_knn_index(const float* raw, const uint8_t* sax_sorted, const uint32_t* perm, const uint8_t* env,
