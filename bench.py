@@ -477,6 +477,86 @@ def run_gpu(args):
     return 0
 
 
+def run_gpu_sharded(args):
+    """--shard: ONE collection of the config's size split by id range across the ranks
+    (strong scaling); every query batch is searched per shard and merged exactly with one
+    all-gather of the per-rank rows + paris_merge_topk."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2009_00166_b200 as P
+    from paper_2009_00166_b200 import parallel as par
+    from datagen import gpu as dg
+    import datagen
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = CONFIGS[args.config]
+    n, length, nq, k = cfg["n"], cfg["len"], cfg["nq"], cfg["k"]
+    if args.n:
+        n = args.n
+    if args.nq:
+        nq = args.nq
+    call_q = cfg.get("call", nq)
+    ds, qs = datagen.config_seeds(args.config)
+    lo, hi = par.shard_range(n, rank, ws)
+    raw = dg.walks(hi - lo, length, ds, first_id=lo, device=dev)        # this rank's ids [lo, hi)
+    if cfg["queries"] == "fresh":
+        queries = dg.walks(nq, length, qs, device=dev)
+    else:
+        full_src = torch.empty(0)  # member queries need their source rows: generate them by id
+        src = datagen.member_ids(nq, n, qs)
+        base = torch.stack([dg.walks(1, length, ds, first_id=int(s_), device=dev)[0] for s_ in src])
+        queries, _ = dg.noisy_members(base, nq, float(cfg["queries"][5:]), qs)
+        del full_src
+    sax = P.summarize(raw, W, CARD)
+    index = P.index_build(sax, W, CARD)
+    local_fn = par.local_index_search(raw, index, config=P.KnnConfig(index_seeds=args.index_seeds))
+    torch.cuda.synchronize()
+
+    def step():
+        outs = []
+        for c0 in range(0, nq, call_q):
+            outs.append(par.knn_sharded(queries[c0:c0 + call_q], k, lo, local_fn))
+        return outs
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        e0.record(st)
+        for _ in range(args.steps):
+            step()
+        e1.record(st)
+        torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    ms = reduce_max_ms(e0.elapsed_time(e1) / args.steps, dev, ws)
+    value = nq / (ms / 1e3)
+    if rank == 0:
+        line = {"metric": "exact 1-NN queries/sec", "value": value, "unit": "queries/s", "n_gpus": ws,
+                "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (seeded Philox random walks, z-normalized; no dataset on the box)",
+                "config": {"workload": cfg["desc"], "n": n, "len": length, "w": W, "card": CARD, "nq": nq, "k": k,
+                           "path": "index, sharded by id range + all-gather + paris_merge_topk",
+                           "parallelism": f"shard x{ws}", "l2": "inputs larger than L2 (no flush)"},
+                "clocks": clocks.summary()}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -493,6 +573,9 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="override n (debug only)")
     ap.add_argument("--nq", type=int, default=0, help="override query count (debug only)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="one collection split across the ranks (strong scaling, exact merge) instead of one "
+                         "collection per rank (weak scaling)")
     ap.add_argument("--no-b1", action="store_true", help="skip the batch-1 LB roofline measurement")
     ap.add_argument("--ref-sample", type=int, default=2_000_000)
     ap.add_argument("--ref-queries", type=int, default=4)
@@ -500,6 +583,8 @@ def main():
     args.warmup = max(args.warmup, 3) if args.impl == "paris" else args.warmup
     if args.impl == "reference":
         return run_reference(args)
+    if args.shard:
+        return run_gpu_sharded(args)
     return run_gpu(args)
 
 

@@ -174,6 +174,17 @@ int paris_knn_nb(const float* raw, const uint8_t* sax, int64_t n, const float* q
                  int64_t* out_idx, float* out_dist, int32_t len, int32_t w, int32_t card, void* stream,
                  const paris_knn_config* config, paris_knn_stats* stats);
 
+/*
+ * paris_merge_topk -- exact merge of per-shard k-NN rows: a
+ * collection sharded by series-id range over R GPUs is searched per shard; the
+ * gathered rows dist/idx [R][nq][k] (each ascending by (distance, global id);
+ * id < 0 = empty) hold the global k best of every query, which are written to
+ * out_idx/out_dist [nq][k] ascending by (distance, id).  Device pointers,
+ * asynchronous on `stream`.  R >= 1, 1 <= k <= PARIS_MAX_K.
+ */
+int paris_merge_topk(const float* dist, const int64_t* idx, int32_t R, int32_t nq, int32_t k, int64_t* out_idx,
+                     float* out_dist, void* stream);
+
 /* Thread-local text of the last failure (never NULL). */
 const char* paris_last_error(void);
 

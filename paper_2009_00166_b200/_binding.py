@@ -87,6 +87,8 @@ def load():
         lib.paris_knn_nb.argtypes = [P, P, i64, P, i32, P, P, i32, i32, i32, P, ctypes.POINTER(_Config),
                                      ctypes.POINTER(_Stats)]
         lib.paris_knn_nb.restype = ctypes.c_int
+        lib.paris_merge_topk.argtypes = [P, P, i32, i32, i32, P, P, P]
+        lib.paris_merge_topk.restype = ctypes.c_int
         lib.paris_last_error.restype = ctypes.c_char_p
         lib.paris_version.restype = i32
         lib.paris_profile_enable.argtypes = [i32]
@@ -264,6 +266,21 @@ def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: in
     if stats:
         return out_idx, out_dist, {"candidates": arrays[0], "refined": arrays[1],
                                    "tau_seed": arrays[2], "lb_blocks": arrays[3], "bsf_updates": arrays[4]}
+    return out_idx, out_dist
+
+
+def merge_topk(dist: torch.Tensor, idx: torch.Tensor, stream=None):
+    """Merge gathered per-shard rows dist/idx [R][nq][k] into the global [nq][k] (CUDA)."""
+    lib = load()
+    _need_cuda(dist, "dist")
+    _need_cuda(idx, "idx")
+    if dist.dtype != torch.float32 or idx.dtype != torch.int64 or dist.shape != idx.shape or dist.dim() != 3:
+        raise ValueError("dist float32 / idx int64, both [R][nq][k]")
+    R, nq, k = dist.shape
+    out_idx = torch.empty((nq, k), dtype=torch.int64, device=dist.device)
+    out_dist = torch.empty((nq, k), dtype=torch.float32, device=dist.device)
+    _check(lib.paris_merge_topk(dist.data_ptr(), idx.data_ptr(), R, nq, k, out_idx.data_ptr(), out_dist.data_ptr(),
+                                _stream(stream)))
     return out_idx, out_dist
 
 

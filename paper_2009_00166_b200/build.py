@@ -25,7 +25,7 @@ if os.environ.get("PARIS_LB1_SPT"):  # tuning experiments only
     FLAGS = FLAGS + [f"-DPARIS_LB1_SPT={int(os.environ['PARIS_LB1_SPT'])}"]
 if os.environ.get("PARIS_DEBUG"):  # device bounds checks (PARIS_DCHECK) -- debugging builds only
     FLAGS = FLAGS + ["-DPARIS_DEBUG_CHECKS"]
-SOURCES = ["runtime.cu", "summarize.cu", "knn.cu", "index.cu"]
+SOURCES = ["runtime.cu", "summarize.cu", "knn.cu", "index.cu", "merge.cu"]
 HEADERS = ["runtime.cuh"]
 
 
