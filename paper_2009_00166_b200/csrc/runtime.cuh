@@ -34,10 +34,10 @@ constexpr int kNumCards = 8;  // 2, 4, ..., 256
 //              kLutMargin of bucket k (3e38 if none), #cuts <= left edge - margin}
 //              so that symbol = lut.y + (v >= cut) for every v whose computed
 //              bucket is k (the cut gap, >= 0.0097 at card 256, exceeds the
-//              window 1/kLutScale + 2*kLutMargin)
-constexpr int kLutN = 4096;
+//              window 1/kLutScale + 2*kLutMargin = 0.0059)
+constexpr int kLutN = 2048;
 constexpr float kLutLo = 4.0f;
-constexpr float kLutScale = 512.0f;
+constexpr float kLutScale = 256.0f;
 constexpr double kLutMargin = 1e-3;
 struct CardTables {
   float cuts_f[kMaxCard];

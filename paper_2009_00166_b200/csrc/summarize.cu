@@ -155,17 +155,17 @@ k_summarize_fast(const float* __restrict__ raw, int64_t n, int w, int card, int 
 }
 
 // TMA-tiled variant (len in {128, 256, 512}, n % 4 == 0): a persistent CTA per SM
-// streams 32 KB tiles of consecutive raw series (one contiguous range, one
+// streams 64 KB tiles of consecutive raw series (one contiguous range, one
 // cp.async.bulk each) into a kSumStages-deep shared-memory ring (mbarrier
 // completion), so HBM reads run ahead of the arithmetic.  Warp w owns SPW
 // consecutive series of a tile; lane l takes float4 #(l + 32j) of a series from
 // shared memory (conflict-free); segment sums by G-lane xor shuffles; the symbol
 // comes from the bucket table (one 8-byte shared load per segment, no search).
 // The owner lane of a segment packs the SPW symbols of its series into one store.
-constexpr int kSumThreads = 512;
+constexpr int kSumThreads = 1024;  // 32 warps: latency of the per-series shuffle chains is hidden by width
 constexpr int kSumWarps = kSumThreads / 32;
-constexpr int kSumStages = 4;
-constexpr int kSumTileBytes = 32768;
+constexpr int kSumStages = 3;
+constexpr int kSumTileBytes = 65536;
 constexpr size_t kSumSmem = (size_t)kSumStages * kSumTileBytes + kLutN * 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
