@@ -353,7 +353,7 @@ def run_gpu(args):
             alu_src = f"derived: 148 SM x 64 FMA lanes/clk x 2 (f16x2) x {ALU_CLOCK_GHZ} GHz"
             if dom == "lb_pass" and use_index:
                 # index path: the algorithmic work is the (block, query) pairs whose envelope
-                # bound passed (stats lb_blocks) x 128 series x w segments x 3 FMA-pipe half-ops
+                # bound passed (stats lb_blocks) x PARIS_INDEX_BLOCK series x w segments x 3 FMA-pipe half-ops
                 blocks = stats["lb_blocks"].numpy().astype(np.float64).sum()
                 ops = 3.0 * W * P.PARIS_INDEX_BLOCK * blocks / nbatches
                 ach = ops / (per_launch_ms / 1e3) / 1e12
@@ -465,9 +465,9 @@ def run_gpu(args):
                         "refined_max": float(refined.max()),
                         "pruning_ratio": float(1.0 - refined.mean() / n),
                         "tau_seed_mean": float(stats["tau_seed"].mean()),
-                        "lb_blocks_frac_p50": float(np.median(stats["lb_blocks"].numpy())) / max(1.0, n / 128),
-                        "lb_blocks_frac_max": float(stats["lb_blocks"].numpy().max()) / max(1.0, n / 128),
-                        "lb_blocks_frac_mean": float(stats["lb_blocks"].numpy().mean()) / max(1.0, n / 128),
+                        "lb_blocks_frac_p50": float(np.median(stats["lb_blocks"].numpy())) / max(1.0, n / P.PARIS_INDEX_BLOCK),
+                        "lb_blocks_frac_max": float(stats["lb_blocks"].numpy().max()) / max(1.0, n / P.PARIS_INDEX_BLOCK),
+                        "lb_blocks_frac_mean": float(stats["lb_blocks"].numpy().mean()) / max(1.0, n / P.PARIS_INDEX_BLOCK),
                         "lb_blocks_top5_share": float(np.sort(stats["lb_blocks"].numpy())[-5:].sum()
                                                       / max(1, stats["lb_blocks"].numpy().sum())),
                         "refined_top5_share": float(np.sort(refined)[-5:].sum() / max(1.0, refined.sum())),

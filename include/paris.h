@@ -40,7 +40,7 @@ extern "C" {
 #define PARIS_ENOMEM (-4)  /* scratch allocation failed */
 
 #define PARIS_MAX_K 1024
-#define PARIS_INDEX_BLOCK 128 /* series per envelope block of the index (paris_index_build) */
+#define PARIS_INDEX_BLOCK 64  /* series per envelope block of the index (paris_index_build) */
 #define PARIS_INDEX_TILE 2048 /* series per tile of the index's tile-major sorted SAX array   */
 
 /*
@@ -118,7 +118,9 @@ typedef struct paris_knn_config {
   int32_t seed_div;     /* seed sample = n / seed_div series (default 16) */
   int32_t wave_a;       /* k = 1: candidates per query refined in the first (lowest-LB) wave; default 2048 */
   int32_t reserved[5];  /* tuning/test hooks: [0] = 1 forces the direct-load LB kernels;
-                           [1] unused; [2] index mode: seed series around the leaf (0 = 1024) */
+                           [1] unused; [2] index mode: seed series around the leaf (0 = 1024);
+                           [3] = 1 seeds every batch from the rows already in out_idx/out_dist
+                           (device outputs; experiments with an ideal BSF) */
 } paris_knn_config;
 
 /* Per-query counters (host memory, arrays of nq), filled by paris_knn_exact_ex. */
@@ -189,7 +191,7 @@ int paris_merge_topk(const float* dist, const int64_t* idx, int32_t R, int32_t n
 const char* paris_last_error(void);
 
 /* ABI version (major*100 + minor). */
-int32_t paris_version(void);  /* 102: paris_knn_nb, paris_knn_stats.bsf_updates */
+int32_t paris_version(void);  /* 103: PARIS_INDEX_BLOCK 64 */
 
 /* Test hook: the library's own fp64 breakpoints cut_1..cut_{card-1} (R2) into
  * out[0..card-2] (host memory).  PARIS_ECONFIG for a bad card. */

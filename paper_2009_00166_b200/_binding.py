@@ -53,6 +53,7 @@ class KnnConfig:
     wave_a: int = 0     # k = 1: first refinement wave per query (0 = 2048)
     force_direct: bool = False  # test hook: use the direct-load LB kernels even where the TMA-tiled ones apply
     index_seeds: int = 0        # index mode: seed series around the query's leaf (0 = 1024)
+    seed_from_out: bool = False  # test hook: seed from the rows already in out_idx/out_dist (device)
 
 
 def library_path() -> str:
@@ -155,7 +156,7 @@ def summarize(raw: torch.Tensor, w: int = 16, card: int = 256, out: torch.Tensor
     return out
 
 
-PARIS_INDEX_BLOCK = 128
+PARIS_INDEX_BLOCK = 64
 PARIS_INDEX_TILE = 2048
 
 
@@ -164,7 +165,7 @@ class Index:
     """iSAX-ordered SAX array (paris_index_build): sorted SoA words, ids, block envelopes."""
     sax_sorted: torch.Tensor   # uint8 [ceil(n/2048)][w][2048] tile-major (include/paris.h)
     perm: torch.Tensor         # int32 [n] (uint32 ids)
-    env: torch.Tensor          # uint8 [ceil(n/128)][2][w]
+    env: torch.Tensor          # uint8 [ceil(n/64)][2][w]
     w: int
     card: int
 
@@ -238,6 +239,7 @@ def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: in
         cfg = _Config(config.batch, config.seed_div, config.wave_a)
         cfg.reserved[0] = 1 if config.force_direct else 0
         cfg.reserved[2] = int(config.index_seeds)
+        cfg.reserved[3] = 1 if config.seed_from_out else 0
     st = None
     arrays = None
     if stats:

@@ -790,6 +790,7 @@ k_lb(LbArgs a) {
 constexpr int kTS = 2048;
 constexpr int kTThreads = 512;
 constexpr int kTWarps = kTThreads / 32;
+constexpr int kBPT = 2048 / PARIS_INDEX_BLOCK;  // index blocks per tile (32: one per lane)
 constexpr int kStages = 4;
 constexpr int kTW = 16;
 constexpr size_t kTileBytes = (size_t)kTW * kTS;
@@ -1072,55 +1073,57 @@ __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int s
 
 // One lane per block: lane l of a warp bounds block 32*g + l against every query
 // slot (region [L[min_s], U[max_s]] per segment, outward fp32, round-down sums);
-// a warp covers two whole tiles, so it lists its live tiles itself.
+// the 32 blocks of a warp step are one whole tile, so the warp lists it itself.
 template <int P>
 __global__ void __launch_bounds__(256)
 k_blkmask(LbArgs a, unsigned* __restrict__ bmask, unsigned* __restrict__ tile_list,
           unsigned* __restrict__ tile_count, unsigned* __restrict__ blocks) {
+  // the envelope bound in the same packed fp16 pair form (and error budget, k_lb)
+  // as the series bound: per segment the region [L16[min], U16[max]], two query
+  // slots per instruction; a block is live for slot b iff its fp16 bound <= T16[b]
   constexpr int NS = 2 * P;
-  __shared__ float2 s_lu[kMaxCard];
-  __shared__ float2 s_qf[NS * kTW];
-  __shared__ float s_thr[NS];
+  __shared__ uint2 s_lu16[kMaxCard];
+  __shared__ uint2 s_q16[kTW * P];
+  __shared__ LbConsts s_c;
   __shared__ unsigned s_blk[kMaxB];
   const int tid = threadIdx.x, lane = tid & 31;
-  for (int i = tid; i < kMaxCard; i += blockDim.x) s_lu[i] = a.tab->lu[i];
-  for (int i = tid; i < NS * kTW; i += blockDim.x) s_qf[i] = a.g_q[(i / kTW) * kMaxW + (i % kTW)];
-  if (tid < NS) s_thr[tid] = (tid < a.nb) ? __uint_as_float(a.thr[tid]) : -1.f;
+  for (int i = tid; i < kMaxCard; i += blockDim.x) s_lu16[i] = a.tab->lu16[i];
+  for (int i = tid; i < kTW * P; i += blockDim.x) s_q16[i] = a.g_q16[i];
   if (tid < kMaxB) s_blk[tid] = 0;
-  __syncthreads();
+  lb_consts_init(a, NS, &s_c);  // ends with __syncthreads
   const int64_t nblocks = (a.n + PARIS_INDEX_BLOCK - 1) / PARIS_INDEX_BLOCK;
   const int64_t ntiles = (a.n + kTS - 1) / kTS;
-  const int64_t ngroups = (ntiles + 1) / 2;  // 32 blocks = 2 tiles per warp step
+  static_assert(kBPT == 32, "a warp step bounds the 32 blocks of one tile");
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + tid) >> 5, GW = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t g = gw; g < ngroups; g += GW) {
+  for (int64_t g = gw; g < ntiles; g += GW) {
     const int64_t blk = 32 * g + lane;
     uint32_t bm = 0;
     if (blk < nblocks) {
       const uint4 mn = __ldg(reinterpret_cast<const uint4*>(a.env + (size_t)blk * 32));
       const uint4 mx = __ldg(reinterpret_cast<const uint4*>(a.env + (size_t)blk * 32 + 16));
       const uint32_t mnw[4] = {mn.x, mn.y, mn.z, mn.w}, mxw[4] = {mx.x, mx.y, mx.z, mx.w};
-      float acc[NS];
+      uint32_t acc[P];
 #pragma unroll
-      for (int b = 0; b < NS; ++b) acc[b] = 0.f;
-#pragma unroll
+      for (int p = 0; p < P; ++p) acc[p] = 0u;
+#pragma unroll 4
       for (int seg = 0; seg < kTW; ++seg) {
-        const float Lo = s_lu[(mnw[seg >> 2] >> (8 * (seg & 3))) & 0xFFu].x;  // L of the min symbol (down)
-        const float Up = s_lu[(mxw[seg >> 2] >> (8 * (seg & 3))) & 0xFFu].y;  // U of the max symbol (up)
+        const uint32_t tx = s_lu16[(mxw[seg >> 2] >> (8 * (seg & 3))) & 0xFFu].x;  // -U16 of the max symbol
+        const uint32_t ty = s_lu16[(mnw[seg >> 2] >> (8 * (seg & 3))) & 0xFFu].y;  // L16 of the min symbol
 #pragma unroll
-        for (int b = 0; b < NS; ++b) {
-          const float2 q = s_qf[b * kTW + seg];
-          const float delta = fmax3(__fsub_rd(q.x, Up), __fsub_rd(Lo, q.y), 0.f);
-          acc[b] = __fmaf_rd(delta, delta, acc[b]);
+        for (int p = 0; p < P; ++p) {
+          const uint2 q = s_q16[seg * P + p];
+          const uint32_t a1 = h2_fma_relu(q.x, kHalf2One, tx);
+          const uint32_t b1 = h2_fma_relu(q.y, kHalf2One, ty);
+          const uint32_t d = h2_max(a1, b1);
+          acc[p] = h2_fma(d, d, acc[p]);
         }
       }
 #pragma unroll
-      for (int b = 0; b < NS; ++b) bm |= (__fmul_rd(acc[b], a.seglen_f) <= s_thr[b] ? 1u : 0u) << b;
+      for (int p = 0; p < P; ++p) bm |= h2_le_bits(acc[p], s_c.T16[p]) << (2 * p);
     }
-    const int64_t nbpad = ntiles * kTWarps;
-    if (blk < nbpad) bmask[blk] = bm;
+    bmask[blk] = bm;  // padded to whole tiles
     const unsigned live = __ballot_sync(0xffffffffu, bm != 0u);
-    if (lane == 0 && (live & 0xFFFFu)) tile_list[atomicAdd(tile_count, 1u)] = (unsigned)(2 * g);
-    if (lane == 16 && (live >> 16) && 2 * g + 1 < ntiles) tile_list[atomicAdd(tile_count, 1u)] = (unsigned)(2 * g + 1);
+    if (lane == 0 && live) tile_list[atomicAdd(tile_count, 1u)] = (unsigned)g;
 #pragma unroll
     for (int b = 0; b < NS; ++b) {
       const unsigned m = __ballot_sync(0xffffffffu, (bm >> b) & 1u);
@@ -1192,10 +1195,11 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
     const int st = (int)(it % kStages);
     const int64_t tile = tile_list[li];
     PARIS_DCHECK(tile >= 0 && tile * kTS < a.n);
-    // the tile's 16 block masks; a block's live slots are computed two at a time
-    // (consecutive live slots form an item), items dealt round-robin to the warps
-    uint32_t bm = 0;
-    if (lane < kTWarps) bm = __ldg(bmask + tile * kTWarps + lane);
+    // the tile's 32 block masks (lane = block); a block's live slots are computed two
+    // at a time (consecutive live slots form an item); a 64-series block is half a
+    // warp, so a warp takes two items per round (lanes 0-15 and 16-31); items are
+    // dealt round-robin, rotating, so no warp is systematically behind
+    const uint32_t bm = __ldg(bmask + tile * kBPT + lane);
     const int cnt = (__popc(bm) + 1) >> 1;
     int incl = cnt;
 #pragma unroll
@@ -1203,27 +1207,30 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
       const int v = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += v;
     }
-    const int total = __shfl_sync(0xffffffffu, incl, kTWarps - 1);
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
     mbar_wait(&s_full[st], (unsigned)((it / kStages) & 1));
     const uint32_t* rows = reinterpret_cast<const uint32_t*>(s_tiles + (size_t)st * kTileBytes);
-    // deal items round-robin starting where the previous tile stopped, so no warp
-    // is systematically one item behind (a lagging warp delays the stage refill)
     const int first = (warp - rot + 2 * kTWarps) % kTWarps;
-    rot = (rot + total) % kTWarps;
-    for (int t = first; t < total; t += kTWarps) {
-      // item t -> (block k, pair p)
-      const int k = __popc(__ballot_sync(0xffffffffu, lane < kTWarps && incl <= t));
+    rot = (rot + (total + 1) / 2) % kTWarps;
+    const int h = lane >> 4, hl = lane & 15;
+    for (int t0 = 2 * first; t0 < total; t0 += 2 * kTWarps) {
+      const int t = t0 + h;  // this half-warp's item
+      const unsigned m0 = __ballot_sync(0xffffffffu, incl <= t0);
+      const unsigned m1 = __ballot_sync(0xffffffffu, incl <= t0 + 1);
+      const bool active = t < total;
+      const int k = active ? __popc(h ? m1 : m0) : 0;
       const int excl = __shfl_sync(0xffffffffu, incl - cnt, k);
       const uint32_t bmk = __shfl_sync(0xffffffffu, bm, k);
       const int r = t - excl;
-      const int sa = __fns(bmk, 0, 2 * r + 1);
-      const int sbf = __fns(bmk, 0, 2 * r + 2);
+      const int saf = active ? __fns(bmk, 0, 2 * r + 1) : 0;
+      const int sa = (saf >= 0 && saf < 32) ? saf : 0;
+      const int sbf = active ? __fns(bmk, 0, 2 * r + 2) : -1;
       const int sb = (sbf >= 0 && sbf < 32) ? sbf : -1;
       const int sq = sb >= 0 ? sb : sa;  // odd count: duplicate lane, masked in emission
       uint32_t acc[4] = {0u, 0u, 0u, 0u};
 #pragma unroll 4
       for (int s = 0; s < kTW; ++s) {
-        const uint32_t word = rows[s * (kTS / 4) + k * 32 + lane];
+        const uint32_t word = rows[s * (kTS / 4) + k * (PARIS_INDEX_BLOCK / 4) + hl];
         const uint32_t qa = s_qs[sa][s], qb = s_qs[sq][s];
         const uint32_t qx = __byte_perm(qa, qb, 0x5410);  // (q_lo16[sa], q_lo16[sb])
         const uint32_t qy = __byte_perm(qa, qb, 0x7632);  // (-q_hi16[sa], -q_hi16[sb])
@@ -1236,9 +1243,9 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
           acc[j] = h2_fma(d, d, acc[j]);
         }
       }
-      const int64_t i0 = tile * kTS + k * PARIS_INDEX_BLOCK + 4 * lane;
-      const int nvalid = (int)std::max<int64_t>(0, imin64(4, a.n - i0));
-      PARIS_DCHECK(k < kTWarps && sa >= 0 && sa < nslots && sb < nslots);
+      const int64_t i0 = tile * kTS + k * PARIS_INDEX_BLOCK + 4 * hl;
+      const int nvalid = active ? (int)std::max<int64_t>(0, imin64(4, a.n - i0)) : 0;
+      PARIS_DCHECK(k < kBPT && sa >= 0 && sa < nslots && sb < nslots);
       lbi_emit(acc, sa, sb, i0, nvalid, nslots, s_c, a, wb, s_hist);
     }
     __syncwarp();
@@ -2069,8 +2076,7 @@ cudaError_t launch_index_lb(const Plan& p, const uint8_t* sax, int nb, const Car
   la.hist = ws.hist; la.cand = ws.cand; la.cap = cap; la.perm = p.perm; la.env = p.env;
   la.blocks = ws.blocks;
   const int64_t ntiles = (p.n + kTS - 1) / kTS;
-  const int64_t groups = (ntiles + 1) / 2;
-  const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms() * 8, (groups + 7) / 8));
+  const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms() * 8, (ntiles + 7) / 8));
   cudaError_t e = PARIS_LAUNCH("lb_blocks", k_blkmask<P>, bgrid, 256, 0, st, la, ws.bmask, ws.tile_list,
                                ws.tile_count, ws.blocks);
   if (e != cudaSuccess) return e;
@@ -2177,7 +2183,7 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   const size_t o_sorted = take(sizeof(uint64_t) * B * (size_t)cap);
   const size_t o_lists = take(p.k > 1 ? sizeof(uint64_t) * B * (size_t)p.XB * p.k : 8);
   const int64_t ntiles = (p.n + kTS - 1) / kTS;
-  const size_t o_bmask = take(p.perm ? sizeof(unsigned) * (size_t)ntiles * kTWarps : 8);
+  const size_t o_bmask = take(p.perm ? sizeof(unsigned) * (size_t)ntiles * kBPT : 8);
   const size_t o_tlist = take(p.perm ? sizeof(unsigned) * (size_t)ntiles : 8);
   const size_t o_tflag = take(p.perm ? sizeof(unsigned) * (size_t)ntiles : 8);
   void* base = nullptr;
@@ -2465,13 +2471,19 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
     return PARIS_EINVAL;
   }
 
+  e = cudaMemsetAsync(all_count, 0, cbytes, st);  // counters accumulate over a re-scan
+  if (e != cudaSuccess) { cudaFreeAsync(stage, st); return cuda_error(e, "memset counters"); }
+  // test hook (reserved[3] == 1): seed every batch from the rows already in out_idx/out_dist
+  // (device outputs) instead of the approximate search -- measures the LB pass under an
+  // ideal BSF; results stay exact for any seed
+  const bool seed_from_out = cfg && cfg->reserved[3] == 1 && !hi && !hd;
   Ws ws;
   int rc = alloc_ws(p, p.cap, ws, st);
   if (rc) { cudaFreeAsync(stage, st); return rc; }
   for (int q0 = 0; q0 < nq && rc == PARIS_OK; q0 += p.B) {
     const int nb = std::min(p.B, nq - q0);
     rc = run_batch(p, raw, sax, d_q + (size_t)q0 * len, nb, q0, p.cap, tab, ws, d_idx, d_dist,
-                   all_count, all_refined, all_tau, all_blocks, st);
+                   all_count, all_refined, all_tau, all_blocks, st, /*rescan=*/seed_from_out);
   }
   // overflow check: one synchronization per call
   std::vector<unsigned> h_count(nq), h_ref(nq), h_blk(nq);

@@ -52,7 +52,8 @@ def test_index_build_matches_definition(P, n, card):
     env = idx.env.cpu().numpy()
     ss = words[perm]
     for blk in range(env.shape[0]):
-        seg = ss[blk * 128:(blk + 1) * 128]
+        B = P.PARIS_INDEX_BLOCK
+        seg = ss[blk * B:(blk + 1) * B]
         np.testing.assert_array_equal(env[blk, 0], seg.min(0))
         np.testing.assert_array_equal(env[blk, 1], seg.max(0))
 
