@@ -141,14 +141,20 @@ def _need_cuda(t: torch.Tensor, name: str):
 
 def summarize(raw: torch.Tensor, w: int = 16, card: int = 256, out: torch.Tensor | None = None,
               stream=None) -> torch.Tensor:
-    """PAA + iSAX of every row of raw ([n][len] fp32, CUDA) -> uint8 [w][n] (segment-major)."""
+    """PAA + iSAX of every row of raw ([n][len] fp32) -> uint8 [w][n] (segment-major, CUDA).
+
+    raw may be a CUDA tensor or a host tensor (pinned or pageable): host rows are
+    streamed to the device in double-buffered chunks; `out` is always
+    device memory (the current CUDA device when not given).
+    """
     lib = load()
-    _need_cuda(raw, "raw")
+    if not raw.is_contiguous():
+        raise ValueError("raw must be contiguous")
     if raw.dtype != torch.float32 or raw.dim() != 2:
         raise ValueError("raw must be [n][len] float32")
     n, length = raw.shape
     if out is None:
-        out = torch.empty((w, n), dtype=torch.uint8, device=raw.device)
+        out = torch.empty((w, n), dtype=torch.uint8, device=raw.device if raw.is_cuda else "cuda")
     _need_cuda(out, "out")
     if out.dtype != torch.uint8 or out.numel() != n * w:
         raise ValueError("out must be uint8 with n*w elements")
@@ -208,13 +214,19 @@ def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: in
               out_dist: torch.Tensor | None = None, stream=None,
               config: KnnConfig | None = None, stats: bool = False, _index: Index | None = None,
               _nb: bool = False):
-    """Exact k-NN of every query (rows of `queries`, CUDA or host) over raw/sax (CUDA).
+    """Exact k-NN of every query (rows of `queries`, CUDA or host) over raw/sax.
+
+    sax (and the index) are CUDA tensors; raw is CUDA or pinned host memory (the
+    candidates' rows are then read through the host mapping).
 
     Returns (idx int64 [nq][k], dist float32 [nq][k]) on the device of `queries`
     (or the given out tensors); with stats=True also a dict of per-query counters.
     """
     lib = load()
-    _need_cuda(raw, "raw")
+    if not (raw.is_cuda or raw.is_pinned()):
+        raise ValueError("raw must be a CUDA tensor or a pinned host tensor (SURVEY f3)")
+    if not raw.is_contiguous():
+        raise ValueError("raw must be contiguous")
     _need_cuda(sax, "sax")
     if not queries.is_contiguous():
         queries = queries.contiguous()

@@ -2418,6 +2418,30 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
     set_error("paris_knn_exact: raw must be 16-byte aligned");
     return PARIS_EINVAL;
   }
+  // raw may live in page-locked host memory (the raw collection outside
+  // the device's memory, like the paper's raw data file on disk): the seed
+  // and the refinement then read only the candidates' rows, through the mapping
+  // (the paper's random reads of the raw file for the RDC pass).  The
+  // SAX array / index are always device-resident (TMA-streamed).
+  const float* d_raw = raw;
+  {
+    cudaPointerAttributes at;
+    cudaError_t ea = cudaPointerGetAttributes(&at, raw);
+    if (ea != cudaSuccess) { cudaGetLastError(); at.type = cudaMemoryTypeUnregistered; }
+    if (at.type == cudaMemoryTypeUnregistered || (at.type == cudaMemoryTypeHost && !at.devicePointer)) {
+      set_error("paris_knn_exact: raw must be device memory or page-locked host memory "
+                "(cudaHostAlloc / cudaHostRegister)");
+      return PARIS_EINVAL;
+    }
+    if (at.type == cudaMemoryTypeHost) d_raw = (const float*)at.devicePointer;
+    for (const void* dp : {(const void*)sax, (const void*)perm, (const void*)env}) {
+      if (dp && is_host_ptr(dp)) {
+        set_error("paris_knn_exact: sax / perm / env must be device memory");
+        return PARIS_EINVAL;
+      }
+    }
+  }
+  raw = d_raw;
 
   Plan p;
   p.n = n; p.len = len; p.w = w; p.card = card; p.k = k;

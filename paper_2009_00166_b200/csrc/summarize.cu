@@ -16,6 +16,9 @@
 // tile are staged in shared memory and leave as 16-byte row stores.
 #include "runtime.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace paris {
 namespace {
 
@@ -24,6 +27,7 @@ constexpr int kThreads = 256;    // 8 warps
 constexpr int kSeriesPerWarp = kTile / (kThreads / 32);  // 16
 constexpr int kUnroll = 4;       // series loaded per warp step (bytes in flight)
 constexpr int kMaxW = 64;
+constexpr size_t kHostChunkBytes = (size_t)256 << 20;  // host-raw staging: 2 x 256 MB device buffers
 
 // #{c : cuts[c] <= v} over a table padded with +inf to 256 entries; `top` is
 // the largest power of two <= card/2 (first step).
@@ -38,7 +42,7 @@ __device__ __forceinline__ int upper_bound_pow2(const T* cuts, T v, int top) {
 template <int NV>  // len = 128 * NV
 __global__ void __launch_bounds__(kThreads)
 k_summarize_fast(const float* __restrict__ raw, int64_t n, int w, int card, int G,
-                 uint8_t* __restrict__ sax, const CardTables* __restrict__ tab) {
+                 uint8_t* __restrict__ sax, int64_t ld, const CardTables* __restrict__ tab) {
   __shared__ float s_cf[kMaxCard];
   __shared__ double s_cd[kMaxCard];
   __shared__ __align__(16) uint8_t s_tile[kMaxW * kTile];
@@ -59,7 +63,7 @@ k_summarize_fast(const float* __restrict__ raw, int64_t n, int w, int card, int 
   for (int g = G; g > 1; g >>= 1) ++depth;
   // |fp32 sum - exact sum| <= depth * 2^-24 * sum|x| (pairwise summation bound, with slack)
   const float err_scale = (float)(depth + 1) * 5.9604645e-08f * inv_seglen * 1.001f;
-  const bool aligned = (n % 16) == 0;
+  const bool aligned = (ld % 16) == 0 && (reinterpret_cast<uintptr_t>(sax) & 15) == 0;
 
   for (int64_t base = (int64_t)blockIdx.x * kTile; base < n; base += (int64_t)gridDim.x * kTile) {
     const int cnt = (int)imin64(kTile, n - base);
@@ -137,17 +141,17 @@ k_summarize_fast(const float* __restrict__ raw, int64_t n, int w, int card, int 
       }
     }
     __syncthreads();
-    // write the tile: row s -> sax[s*n + base .. base+cnt)
+    // write the tile: row s -> sax[s*ld + base .. base+cnt)
     if (aligned && cnt == kTile) {
       for (int t = threadIdx.x; t < w * (kTile / 16); t += kThreads) {
         const int s = t / (kTile / 16), part = t % (kTile / 16);
         const uint4 val = *reinterpret_cast<const uint4*>(s_tile + s * kTile + part * 16);
-        __stcs(reinterpret_cast<uint4*>(sax + (size_t)s * n + base) + part, val);
+        __stcs(reinterpret_cast<uint4*>(sax + (size_t)s * ld + base) + part, val);
       }
     } else {
       for (int t = threadIdx.x; t < w * cnt; t += kThreads) {
         const int s = t / cnt, col = t % cnt;
-        sax[(size_t)s * n + base + col] = s_tile[s * kTile + col];
+        sax[(size_t)s * ld + base + col] = s_tile[s * kTile + col];
       }
     }
     __syncthreads();
@@ -196,7 +200,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 template <int NV>  // len = 128 * NV
 __global__ void __launch_bounds__(kSumThreads, 1)
 k_summarize_tma(const float* __restrict__ raw, int64_t n, int w, int card, int G,
-                uint8_t* __restrict__ sax, const CardTables* __restrict__ tab) {
+                uint8_t* __restrict__ sax, int64_t ld, const CardTables* __restrict__ tab) {
   constexpr int len = 128 * NV;
   constexpr int TS = kSumTileBytes / (4 * len);  // series per tile
   constexpr int SPW = TS / kSumWarps;             // series per warp per tile (1, 2 or 4)
@@ -317,7 +321,7 @@ k_summarize_tma(const float* __restrict__ raw, int64_t n, int w, int card, int G
     for (int j = 0; j < NV; ++j) {
       if ((lane % G) == (j % G) && cnt > 0) {
         const int seg = (lane + 32 * j) / G;
-        uint8_t* dst = sax + (size_t)seg * n + base;
+        uint8_t* dst = sax + (size_t)seg * ld + base;
         if (cnt == SPW) {
           if (SPW == 4) *reinterpret_cast<uint32_t*>(dst) = packed[j];
           else if (SPW == 2) *reinterpret_cast<uint16_t*>(dst) = (uint16_t)packed[j];
@@ -335,7 +339,7 @@ k_summarize_tma(const float* __restrict__ raw, int64_t n, int w, int card, int G
 // only when the fast path's shape conditions do not hold.
 __global__ void __launch_bounds__(kThreads)
 k_summarize_generic(const float* __restrict__ raw, int64_t n, int len, int w, int card,
-                    uint8_t* __restrict__ sax, const CardTables* __restrict__ tab) {
+                    uint8_t* __restrict__ sax, int64_t ld, const CardTables* __restrict__ tab) {
   __shared__ double s_cd[kMaxCard];
   for (int i = threadIdx.x; i < kMaxCard; i += blockDim.x) s_cd[i] = tab->cuts_d[i];
   __syncthreads();
@@ -346,7 +350,7 @@ k_summarize_generic(const float* __restrict__ raw, int64_t n, int len, int w, in
     for (int s = 0; s < w; ++s) {
       double acc = 0.0;
       for (int j = 0; j < seglen; ++j) acc += (double)x[s * seglen + j];
-      sax[(size_t)s * n + i] = (uint8_t)upper_bound_pow2(s_cd, acc / (double)seglen, card >> 1);
+      sax[(size_t)s * ld + i] = (uint8_t)upper_bound_pow2(s_cd, acc / (double)seglen, card >> 1);
     }
   }
 }
@@ -364,25 +368,15 @@ int sm_count() {
 
 }  // namespace
 
-int summarize_impl(const float* raw, int64_t n, int len, int w, int card, uint8_t* out_sax,
-                   cudaStream_t st) {
-  if (!raw || !out_sax) { set_error("paris_summarize: null pointer"); return PARIS_EINVAL; }
-  if (n < 1 || n >= (int64_t(1) << 31)) { set_error("paris_summarize: n=%lld out of range", (long long)n); return PARIS_EINVAL; }
-  if (len < 4 || len > 4096 || (len % 4) || w < 1 || w > kMaxW || (len % w)) {
-    set_error("paris_summarize: unsupported (len=%d, w=%d)", len, w);
-    return PARIS_ECONFIG;
-  }
-  const CardTables* tab = device_tables(card);
-  if (!tab) return PARIS_ECONFIG;
-  if ((reinterpret_cast<uintptr_t>(raw) & 15) != 0) {
-    set_error("paris_summarize: raw must be 16-byte aligned");
-    return PARIS_EINVAL;
-  }
+// Summarize n device-resident series into rows of stride ld (out_sax[s*ld + i]).
+static int summarize_device(const float* raw, int64_t n, int len, int w, int card, uint8_t* out_sax, int64_t ld,
+                            const CardTables* tab, cudaStream_t st) {
   const int seglen = len / w;
   const int G = seglen / 4;
   const bool fast = (len % 128 == 0) && (seglen % 4 == 0) && G >= 1 && G <= 32 && ((G & (G - 1)) == 0);
   const int sms = sm_count();
-  const bool tma = fast && (n % 4 == 0) && (len == 128 || len == 256 || len == 512);
+  const bool tma = fast && (ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(out_sax) & 3) == 0) &&
+                   (n % 4 == 0) && (len == 128 || len == 256 || len == 512);
   if (tma) {
     const int64_t tiles = (n + (kSumTileBytes / (4 * len)) - 1) / (kSumTileBytes / (4 * len));
     const int grid = (int)imin64(tiles, (int64_t)sms);
@@ -399,9 +393,9 @@ int summarize_impl(const float* raw, int64_t n, int len, int w, int card, uint8_
       attr_dev[ai] = dev;
     }
     switch (len) {
-      case 128: e = PARIS_LAUNCH("summarize", k_summarize_tma<1>, grid, kSumThreads, kSumSmem, st, raw, n, w, card, G, out_sax, tab); break;
-      case 256: e = PARIS_LAUNCH("summarize", k_summarize_tma<2>, grid, kSumThreads, kSumSmem, st, raw, n, w, card, G, out_sax, tab); break;
-      default: e = PARIS_LAUNCH("summarize", k_summarize_tma<4>, grid, kSumThreads, kSumSmem, st, raw, n, w, card, G, out_sax, tab); break;
+      case 128: e = PARIS_LAUNCH("summarize", k_summarize_tma<1>, grid, kSumThreads, kSumSmem, st, raw, n, w, card, G, out_sax, ld, tab); break;
+      case 256: e = PARIS_LAUNCH("summarize", k_summarize_tma<2>, grid, kSumThreads, kSumSmem, st, raw, n, w, card, G, out_sax, ld, tab); break;
+      default: e = PARIS_LAUNCH("summarize", k_summarize_tma<4>, grid, kSumThreads, kSumSmem, st, raw, n, w, card, G, out_sax, ld, tab); break;
     }
     PARIS_CHECK_LAUNCH(e, "summarize launch");
   } else if (fast) {
@@ -409,23 +403,97 @@ int summarize_impl(const float* raw, int64_t n, int len, int w, int card, uint8_
     const int grid = (int)imin64(tiles, (int64_t)sms * 8);
     cudaError_t e;
     switch (len / 128) {
-      case 1: e = PARIS_LAUNCH("summarize", k_summarize_fast<1>, grid, kThreads, 0, st, raw, n, w, card, G, out_sax, tab); break;
-      case 2: e = PARIS_LAUNCH("summarize", k_summarize_fast<2>, grid, kThreads, 0, st, raw, n, w, card, G, out_sax, tab); break;
-      case 4: e = PARIS_LAUNCH("summarize", k_summarize_fast<4>, grid, kThreads, 0, st, raw, n, w, card, G, out_sax, tab); break;
-      case 8: e = PARIS_LAUNCH("summarize", k_summarize_fast<8>, grid, kThreads, 0, st, raw, n, w, card, G, out_sax, tab); break;
+      case 1: e = PARIS_LAUNCH("summarize", k_summarize_fast<1>, grid, kThreads, 0, st, raw, n, w, card, G, out_sax, ld, tab); break;
+      case 2: e = PARIS_LAUNCH("summarize", k_summarize_fast<2>, grid, kThreads, 0, st, raw, n, w, card, G, out_sax, ld, tab); break;
+      case 4: e = PARIS_LAUNCH("summarize", k_summarize_fast<4>, grid, kThreads, 0, st, raw, n, w, card, G, out_sax, ld, tab); break;
+      case 8: e = PARIS_LAUNCH("summarize", k_summarize_fast<8>, grid, kThreads, 0, st, raw, n, w, card, G, out_sax, ld, tab); break;
       default: {
         const int gg = (int)imin64((n + kThreads - 1) / kThreads, (int64_t)sms * 8);
-        e = PARIS_LAUNCH("summarize_generic", k_summarize_generic, gg, kThreads, 0, st, raw, n, len, w, card, out_sax, tab);
+        e = PARIS_LAUNCH("summarize_generic", k_summarize_generic, gg, kThreads, 0, st, raw, n, len, w, card, out_sax, ld, tab);
       }
     }
     PARIS_CHECK_LAUNCH(e, "summarize launch");
   } else {
     const int gg = (int)imin64((n + kThreads - 1) / kThreads, (int64_t)sms * 8);
     PARIS_CHECK_LAUNCH(PARIS_LAUNCH("summarize_generic", k_summarize_generic, gg, kThreads, 0, st,
-                                    raw, n, len, w, card, out_sax, tab),
+                                    raw, n, len, w, card, out_sax, ld, tab),
                        "summarize launch");
   }
   return PARIS_OK;
+}
+
+
+
+// Raw series in HOST memory (the paper's raw data stays on disk, P:52-56,
+// 380-404): the Coordinator / IndexBulkLoading pipeline (Alg. Coordinator, P:477-483,
+// 552) -- the Coordinator fills one half of the double-buffered raw data buffer
+// while the workers summarize the other -- as stream-ordered
+// H2D copies into two device staging buffers on a copy stream, overlapped with
+// the summarize kernel on the caller's stream (truly asynchronous for pinned
+// memory; pageable memory still works, the copies are then staged by the driver).
+static int summarize_host(const float* raw, int64_t n, int len, int w, int card, uint8_t* out_sax,
+                          const CardTables* tab, cudaStream_t st) {
+  const size_t row = (size_t)len * 4;
+  size_t cbytes = kHostChunkBytes;
+  if (const char* ev = getenv("PARIS_HOST_CHUNK_BYTES")) {  // test hook: force many chunks
+    const long long v = atoll(ev);
+    if (v > 0) cbytes = (size_t)v;
+  }
+  int64_t chunk = std::max<int64_t>(16, ((int64_t)(cbytes / row)) / 16 * 16);
+  chunk = std::min<int64_t>(chunk, (n + 15) / 16 * 16);
+  float* buf[2] = {nullptr, nullptr};
+  cudaStream_t cs = nullptr;
+  cudaEvent_t copied[2] = {nullptr, nullptr}, consumed[2] = {nullptr, nullptr};
+  int rc = PARIS_OK;
+  cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    e = cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&consumed[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaMallocAsync((void**)&buf[i], (size_t)chunk * row, st);
+  }
+  if (e == cudaSuccess) e = cudaEventRecord(consumed[0], st);  // buffers allocated on st
+  if (e == cudaSuccess) e = cudaEventRecord(consumed[1], st);
+  for (int64_t c0 = 0, c = 0; c0 < n && e == cudaSuccess && rc == PARIS_OK; c0 += chunk, ++c) {
+    const int b = (int)(c & 1);
+    const int64_t m = std::min<int64_t>(chunk, n - c0);
+    e = cudaStreamWaitEvent(cs, consumed[b], 0);  // the summarize of chunk c-2 is done with buf[b]
+    if (e == cudaSuccess) e = cudaMemcpyAsync(buf[b], raw + (size_t)c0 * len, (size_t)m * row, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess) e = cudaEventRecord(copied[b], cs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, copied[b], 0);
+    if (e == cudaSuccess) rc = summarize_device(buf[b], m, len, w, card, out_sax + c0, n, tab, st);
+    if (e == cudaSuccess && rc == PARIS_OK) e = cudaEventRecord(consumed[b], st);
+  }
+  if (e != cudaSuccess && rc == PARIS_OK) rc = cuda_error(e, "paris_summarize (host raw)");
+  for (int i = 0; i < 2; ++i) {
+    if (buf[i]) cudaFreeAsync(buf[i], st);
+    if (copied[i]) cudaEventDestroy(copied[i]);
+    if (consumed[i]) cudaEventDestroy(consumed[i]);
+  }
+  if (cs) cudaStreamDestroy(cs);  // released once its queued copies complete
+  return rc;
+}
+
+int summarize_impl(const float* raw, int64_t n, int len, int w, int card, uint8_t* out_sax,
+                   cudaStream_t st) {
+  if (!raw || !out_sax) { set_error("paris_summarize: null pointer"); return PARIS_EINVAL; }
+  if (n < 1 || n >= (int64_t(1) << 31)) { set_error("paris_summarize: n=%lld out of range", (long long)n); return PARIS_EINVAL; }
+  if (len < 4 || len > 4096 || (len % 4) || w < 1 || w > kMaxW || (len % w)) {
+    set_error("paris_summarize: unsupported (len=%d, w=%d)", len, w);
+    return PARIS_ECONFIG;
+  }
+  const CardTables* tab = device_tables(card);
+  if (!tab) return PARIS_ECONFIG;
+  if ((reinterpret_cast<uintptr_t>(raw) & 15) != 0) {
+    set_error("paris_summarize: raw must be 16-byte aligned");
+    return PARIS_EINVAL;
+  }
+  retain_pool();
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, raw);
+  if (e != cudaSuccess) cudaGetLastError();
+  const bool host = (e != cudaSuccess) || at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered;
+  if (host) return summarize_host(raw, n, len, w, card, out_sax, tab, st);
+  return summarize_device(raw, n, len, w, card, out_sax, n, tab, st);
 }
 
 }  // namespace paris
