@@ -118,6 +118,17 @@ def weak_throughput(nq_per_rank: int, world_size: int, max_ms: float) -> float:
     return nq_per_rank * world_size / (max_ms / 1e3)
 
 
+def seed_series(n: int, use_index: bool, index_seeds: int, k: int) -> int:
+    """Series whose true distance the BSF seed computes per query (plan_seed in csrc/knn.cu):
+    index path -- the index_seeds (default 1024) series around the query's leaf; flat path --
+    the LB-best series of each of 16 warps x seed_grid CTAs over a prefix sample of n/16."""
+    if use_index:
+        return max(k, min(4096, index_seeds or 1024))
+    ns = min(n, max(n // 16, min(n, 65536)))
+    ns = min(n, (ns + 15) // 16 * 16)
+    return min(148, (ns + 2047) // 2048) * 16
+
+
 def refined_sum_of(stats) -> float:
     return float(stats["refined"].double().sum())
 
@@ -406,9 +417,12 @@ def run_gpu(args):
                         "algorithmic_ops_per_batch": ops, "ms_per_batch": per_launch_ms, "peak_source": alu_src,
                         "hbm_achieved_gbs": alg[dom] / (per_launch_ms / 1e3) / 1e9, "hbm_peak_gbs": peak,
                         "queries_per_pass": q_per_pass}
-            elif dom in alg and args.raw_host and dom in ("refine", "nb_distcomp"):
-                # f3: the candidates' raw rows cross PCIe (zero-copy reads of pinned host memory)
-                byts = 4.0 * length * refined_sum_of(stats) / nbatches
+            elif args.raw_host and dom in ("refine", "nb_distcomp", "seed_ed"):
+                # f3: the seeds' and candidates' raw rows cross PCIe (zero-copy reads of pinned host memory)
+                if dom == "seed_ed":
+                    byts = 4.0 * length * seed_series(n, use_index, args.index_seeds, k) * q_per_pass
+                else:
+                    byts = 4.0 * length * refined_sum_of(stats) / nbatches
                 ach = byts / (per_launch_ms / 1e3) / 1e9
                 roof = {"kernel": dom, "bound": "pcie", "achieved": ach, "peak": h2d_gbs, "unit": "GB/s",
                         "frac": ach / h2d_gbs, "traffic": None, "algorithmic_bytes_per_batch": byts,

@@ -52,8 +52,13 @@ extern "C" {
  *        a value on a cut goes to the upper region, R3).
  * The symbol is decided as if PAA were computed exactly: an fp32 PAA whose
  * rounding-error bound straddles a cut is recomputed in fp64.
- *   raw      device [n][len] fp32
+ *   raw      [n][len] fp32, device OR host memory (pinned or pageable; 16-byte aligned)
  *   out_sax  device [w][n] uint8 (caller-allocated, n*w bytes)
+ * Host raw (the paper's raw data is not in memory): rows are
+ * streamed in 256 MB chunks through two device staging buffers, the copy of chunk
+ * c+1 overlapping the summarize of chunk c (the Coordinator's double buffer,
+ * P:459-465, 477-483); pinned memory makes the copies asynchronous.  The host
+ * buffer must stay valid until `stream` completes.
  * Asynchronous: returns after enqueueing; results valid once `stream` completes.
  */
 int paris_summarize(const float* raw, int64_t n, int32_t len, int32_t w, int32_t card,
@@ -74,7 +79,10 @@ int paris_summarize(const float* raw, int64_t n, int32_t len, int32_t w, int32_t
  *      re-checked against the live BSF before its raw series is read; true squared
  *      ED with early abandoning; the BSF (k-th best) is shared through atomics.
  *   4. Result: ascending (distance, id); ties go to the lower id (R6).
- *   raw       device [n][len] fp32           sax  device [w][n] uint8 (paris_summarize)
+ *   raw       [n][len] fp32: device memory, or page-locked host memory (cudaHostAlloc /
+ *             cudaHostRegister) -- then only the seeds' and candidates' rows
+ *             cross PCIe; pageable host raw -> PARIS_EINVAL
+ *   sax       device [w][n] uint8 (paris_summarize); host sax -> PARIS_EINVAL
  *   queries   [nq][len] fp32                 -- device OR host memory
  *   out_idx   [nq][k] int64 series ids       -- device OR host memory
  *   out_dist  [nq][k] fp32 Euclidean (rooted) distance -- device OR host memory
@@ -118,7 +126,7 @@ typedef struct paris_knn_config {
   int32_t seed_div;     /* seed sample = n / seed_div series (default 16) */
   int32_t wave_a;       /* k = 1: candidates per query refined in the first (lowest-LB) wave; default 2048 */
   int32_t reserved[5];  /* tuning/test hooks: [0] = 1 forces the direct-load LB kernels;
-                           [1] unused; [2] index mode: seed series around the leaf (0 = 1024);
+                           [1] unused; [2] index mode: seed series around the leaf (0 = 1024, 64 when raw is host memory);
                            [3] = 1 seeds every batch from the rows already in out_idx/out_dist
                            (device outputs; experiments with an ideal BSF) */
 } paris_knn_config;
