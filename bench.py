@@ -300,7 +300,7 @@ def run_gpu(args):
         use_index = path == "index"
         use_nb = path == "nb"
         b_path = args.batch or (32 if use_index else 16)  # the library's default queries per pass
-        kcfg = P.KnnConfig(batch=b_path, index_seeds=args.index_seeds)
+        kcfg = P.KnnConfig(batch=b_path, index_seeds=args.index_seeds, sorted_refine=args.sorted_refine)
         nbatches = sum((min(call_q, nq - c0) + b_path - 1) // b_path for c0 in range(0, nq, call_q))
         q_per_pass = nq / nbatches
 
@@ -641,6 +641,8 @@ def main():
                     help="one collection split across the ranks (strong scaling, exact merge) instead of one "
                          "collection per rank (weak scaling)")
     ap.add_argument("--no-b1", action="store_true", help="skip the batch-1 LB roofline measurement")
+    ap.add_argument("--sorted-refine", action="store_true",
+                    help="k = 1: refine bucket-sorted lists (K5 scatter) instead of the unsorted waves (A/B)")
     ap.add_argument("--raw-host", action="store_true",
                     help="f3: keep the raw collection in pinned host memory (SAX/index in HBM)")
     ap.add_argument("--ref-sample", type=int, default=2_000_000)

@@ -126,7 +126,10 @@ typedef struct paris_knn_config {
   int32_t seed_div;     /* seed sample = n / seed_div series (default 16) */
   int32_t wave_a;       /* k = 1: candidates per query refined in the first (lowest-LB) wave; default 2048 */
   int32_t reserved[5];  /* tuning/test hooks: [0] = 1 forces the direct-load LB kernels;
-                           [1] unused; [2] index mode: seed series around the leaf (0 = 1024, 64 when raw is host memory);
+                           [1] = 1: the k = 1 refine walks bucket-sorted lists (K5 scatter)
+                           instead of taking its two LB waves from the unsorted lists;
+                           [2] index mode: seed series around the leaf (0 = 1024; 64 when
+                           raw is host memory);
                            [3] = 1 seeds every batch from the rows already in out_idx/out_dist
                            (device outputs; experiments with an ideal BSF) */
 } paris_knn_config;

@@ -52,6 +52,7 @@ class KnnConfig:
     seed_div: int = 0   # seed sample = n / seed_div (0 = 16)
     wave_a: int = 0     # k = 1: first refinement wave per query (0 = 2048)
     force_direct: bool = False  # test hook: use the direct-load LB kernels even where the TMA-tiled ones apply
+    sorted_refine: bool = False  # k = 1: refine the bucket-sorted lists (K5 scatter) instead of the unsorted waves
     index_seeds: int = 0        # index mode: seed series around the query's leaf (0 = 1024)
     seed_from_out: bool = False  # test hook: seed from the rows already in out_idx/out_dist (device)
 
@@ -250,6 +251,7 @@ def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: in
     if config is not None:
         cfg = _Config(config.batch, config.seed_div, config.wave_a)
         cfg.reserved[0] = 1 if config.force_direct else 0
+        cfg.reserved[1] = 1 if config.sorted_refine else 0
         cfg.reserved[2] = int(config.index_seeds)
         cfg.reserved[3] = 1 if config.seed_from_out else 0
     st = None

@@ -23,6 +23,8 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxe
          "-Xptxas", "-warn-spills"]
 if os.environ.get("PARIS_LB1_SPT"):  # tuning experiments only
     FLAGS = FLAGS + [f"-DPARIS_LB1_SPT={int(os.environ['PARIS_LB1_SPT'])}"]
+if os.environ.get("PARIS_LB_NOMAX"):  # tuning experiments only (bit-identical LB accumulation form)
+    FLAGS = FLAGS + [f"-DPARIS_LB_NOMAX={int(os.environ['PARIS_LB_NOMAX'])}"]
 if os.environ.get("PARIS_DEBUG"):  # device bounds checks (PARIS_DCHECK) -- debugging builds only
     FLAGS = FLAGS + ["-DPARIS_DEBUG_CHECKS"]
 SOURCES = ["runtime.cu", "summarize.cu", "knn.cu", "index.cu", "merge.cu"]

@@ -121,6 +121,23 @@ __device__ __forceinline__ uint32_t h2_fma(uint32_t a, uint32_t b, uint32_t c) {
   asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
   return d;
 }
+
+// acc += delta^2 for one (series, segment) of a query pair, delta = max(a, b) where
+// a = relu(q_lo - U) and b = relu(L - q_hi).  At most one of a, b is non-zero (U >= L
+// and q_lo <= q_hi hold for the rounded values), so a^2 + b^2 in two FMAs is the
+// same single rounding as max-then-FMA (fma(0, 0, acc) == acc exactly): bit-identical
+// results, with the ALU-pipe max traded for an FMA-pipe op (PARIS_LB_NOMAX=1).
+#ifndef PARIS_LB_NOMAX
+#define PARIS_LB_NOMAX 0
+#endif
+__device__ __forceinline__ uint32_t h2_acc_delta2(uint32_t acc, uint32_t a, uint32_t b) {
+#if PARIS_LB_NOMAX
+  return h2_fma(b, b, h2_fma(a, a, acc));
+#else
+  const uint32_t d = h2_max(a, b);
+  return h2_fma(d, d, acc);
+#endif
+}
 // bit 0: low half a <= b; bit 1: high half a <= b
 __device__ __forceinline__ uint32_t h2_le_bits(uint32_t a, uint32_t b) {
   const unsigned m = __hle2_mask(*reinterpret_cast<const __half2*>(&a), *reinterpret_cast<const __half2*>(&b));
@@ -160,8 +177,7 @@ __device__ __forceinline__ void lb16_seg(uint32_t word, const uint2* __restrict_
       const uint2 q = q16s[p];
       const uint32_t a = h2_fma_relu(q.x, kHalf2One, t.x);
       const uint32_t b = h2_fma_relu(q.y, kHalf2One, t.y);
-      const uint32_t d = h2_max(a, b);
-      acc[j][p] = h2_fma(d, d, acc[j][p]);
+      acc[j][p] = h2_acc_delta2(acc[j][p], a, b);
     }
   }
 }
@@ -795,7 +811,12 @@ constexpr int kStages = 4;
 constexpr int kTW = 16;
 constexpr size_t kTileBytes = (size_t)kTW * kTS;
 constexpr size_t kTSmem = kStages * kTileBytes + kMaxCard * 32 * 4;
-constexpr size_t kLbiSmem = kTSmem + (size_t)kMaxB * kNB * 4;  // + the LB histograms
+// k_lbi: 2-stage ring + the 32-copy pair-form table (64 KB) + the LB histograms
+constexpr int kIStages = 2;      // compute-bound on the live items: a tile's load (~0.8 us) < its work
+constexpr int kIThreads = 768;   // 24 warps: more warps to hide the lookup -> math latency chain
+constexpr int kIWarps = kIThreads / 32;
+constexpr size_t kITabEnd = kIStages * kTileBytes + (size_t)kMaxCard * 32 * 8;
+constexpr size_t kLbiSmem = kITabEnd + (size_t)kMaxB * kNB * 4;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -836,8 +857,7 @@ __device__ __forceinline__ void lbt_seg(uint32_t word, const uint32_t* __restric
       const uint2 q = q16s[p];
       const uint32_t a = h2_fma_relu(q.x, kHalf2One, tx);
       const uint32_t b = h2_fma_relu(q.y, kHalf2One, ty);
-      const uint32_t d = h2_max(a, b);
-      acc[j][p] = h2_fma(d, d, acc[j][p]);
+      acc[j][p] = h2_acc_delta2(acc[j][p], a, b);
     }
   }
 }
@@ -1114,8 +1134,7 @@ k_blkmask(LbArgs a, unsigned* __restrict__ bmask, unsigned* __restrict__ tile_li
           const uint2 q = s_q16[seg * P + p];
           const uint32_t a1 = h2_fma_relu(q.x, kHalf2One, tx);
           const uint32_t b1 = h2_fma_relu(q.y, kHalf2One, ty);
-          const uint32_t d = h2_max(a1, b1);
-          acc[p] = h2_fma(d, d, acc[p]);
+          acc[p] = h2_acc_delta2(acc[p], a1, b1);
         }
       }
 #pragma unroll
@@ -1135,28 +1154,29 @@ k_blkmask(LbArgs a, unsigned* __restrict__ bmask, unsigned* __restrict__ tile_li
 }
 
 template <int P>
-__global__ void __launch_bounds__(kTThreads, 1)
+__global__ void __launch_bounds__(kIThreads, 1)
 k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__ tile_list,
       const unsigned* __restrict__ tile_count) {
   extern __shared__ __align__(128) uint8_t dsm[];
   uint8_t* s_tiles = dsm;
-  // region table in pair form {(-U16,-U16), (L16,L16)}, 16 copies: entry c of lane l
-  // at uint2 index 16c + (l % 16) -- a 64-bit load is served per half-warp, so the
-  // 16 lanes of each half always hit distinct banks
-  uint2* s_tab = reinterpret_cast<uint2*>(dsm + kStages * kTileBytes);
-  unsigned* s_hist = reinterpret_cast<unsigned*>(dsm + kTSmem);  // [kMaxB][kNB] after the ring + table
-  __shared__ __align__(8) uint64_t s_full[kStages];
-  __shared__ unsigned s_cnt[kStages];
+  // region table in pair form {(-U16,-U16), (L16,L16)}, 32 copies: entry c of lane l
+  // at byte 256c + 8l, so ONE byte permute forms the address (symbol byte -> bits
+  // 8..15, lane*8 -> bits 0..7; no multiply); a 64-bit load is served per half-warp
+  // and the 16 lanes of each half hit distinct banks
+  uint2* s_tab = reinterpret_cast<uint2*>(dsm + kIStages * kTileBytes);
+  unsigned* s_hist = reinterpret_cast<unsigned*>(dsm + kITabEnd);  // [kMaxB][kNB] after the ring + table
+  __shared__ __align__(8) uint64_t s_full[kIStages];
+  __shared__ unsigned s_cnt[kIStages];
   __shared__ uint32_t s_qs[2 * P][kTW];  // per slot and segment: half2(q_lo16, -q_hi16)
   __shared__ LbConsts s_c;
-  __shared__ WarpBuf s_wb[kTWarps];
+  __shared__ WarpBuf s_wb[kIWarps];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nslots = 2 * P;
   const int64_t nlist = *tile_count;
   WarpBuf& wb = s_wb[warp];
   if (lane < kMaxB) wb.cnt[lane] = 0;
   if (lane == 0) wb.n = 0;
-  for (int i = tid; i < nslots * kNB; i += kTThreads) s_hist[i] = 0;
+  for (int i = tid; i < nslots * kNB; i += kIThreads) s_hist[i] = 0;
 
   static_assert(kTS == PARIS_INDEX_TILE, "index tiles are the LB kernel's tiles");
   auto issue = [&](int64_t li, int st) {
@@ -1166,7 +1186,7 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
              &s_full[st]);
   };
   if (tid == 0) {
-    for (int st = 0; st < kStages; ++st) {
+    for (int st = 0; st < kIStages; ++st) {
       mbar_init(&s_full[st], 1);
       s_cnt[st] = 0;
     }
@@ -1174,25 +1194,26 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
   }
   __syncthreads();
   if (tid == 0) {
-    for (int st = 0; st < kStages; ++st) {
+    for (int st = 0; st < kIStages; ++st) {
       const int64_t li = blockIdx.x + (int64_t)st * gridDim.x;
       if (li < nlist) issue(li, st);
     }
   }
-  for (int i = tid; i < kMaxCard * 16; i += kTThreads) s_tab[i] = a.tab->lu16[i >> 4];
-  for (int i = tid; i < 2 * P * kTW; i += kTThreads) {
+  for (int i = tid; i < kMaxCard * 32; i += kIThreads) s_tab[i] = a.tab->lu16[i >> 5];
+  for (int i = tid; i < 2 * P * kTW; i += kIThreads) {
     const int b = i / kTW, sg = i % kTW;
     const uint2 v = a.g_q16[sg * P + (b >> 1)];
     s_qs[b][sg] = half_of(v.x, b & 1) | (half_of(v.y, b & 1) << 16);
   }
   lb_consts_init(a, nslots, &s_c);  // ends with __syncthreads
-  const uint2* tabl = s_tab + (lane & 15);
+  const char* tabc = reinterpret_cast<const char*>(s_tab);
+  const uint32_t lane8 = (uint32_t)lane * 8u;  // < 256: byte 0 of the table offset
   int rot = 0;
 
   for (int64_t it = 0;; ++it) {
     const int64_t li = blockIdx.x + it * gridDim.x;
     if (li >= nlist) break;
-    const int st = (int)(it % kStages);
+    const int st = (int)(it % kIStages);
     const int64_t tile = tile_list[li];
     PARIS_DCHECK(tile >= 0 && tile * kTS < a.n);
     // the tile's 32 block masks (lane = block); a block's live slots are computed two
@@ -1208,12 +1229,12 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
       if (lane >= o) incl += v;
     }
     const int total = __shfl_sync(0xffffffffu, incl, 31);
-    mbar_wait(&s_full[st], (unsigned)((it / kStages) & 1));
+    mbar_wait(&s_full[st], (unsigned)((it / kIStages) & 1));
     const uint32_t* rows = reinterpret_cast<const uint32_t*>(s_tiles + (size_t)st * kTileBytes);
-    const int first = (warp - rot + 2 * kTWarps) % kTWarps;
-    rot = (rot + (total + 1) / 2) % kTWarps;
+    const int first = (warp - rot + 2 * kIWarps) % kIWarps;
+    rot = (rot + (total + 1) / 2) % kIWarps;
     const int h = lane >> 4, hl = lane & 15;
-    for (int t0 = 2 * first; t0 < total; t0 += 2 * kTWarps) {
+    for (int t0 = 2 * first; t0 < total; t0 += 2 * kIWarps) {
       const int t = t0 + h;  // this half-warp's item
       const unsigned m0 = __ballot_sync(0xffffffffu, incl <= t0);
       const unsigned m1 = __ballot_sync(0xffffffffu, incl <= t0 + 1);
@@ -1236,11 +1257,12 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
         const uint32_t qy = __byte_perm(qa, qb, 0x7632);  // (-q_hi16[sa], -q_hi16[sb])
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const uint2 tt = tabl[__byte_perm(word, 0, 0x4440 | j) * 16];
+          // offset = (symbol j << 8) | lane*8: bytes {lane8.b0, word.bj, 0, 0}
+          const uint32_t off = __byte_perm(word, lane8, 0x5504u | ((uint32_t)j << 4));
+          const uint2 tt = *reinterpret_cast<const uint2*>(tabc + off);
           const uint32_t a1 = h2_fma_relu(qx, kHalf2One, tt.x);
           const uint32_t b1 = h2_fma_relu(qy, kHalf2One, tt.y);
-          const uint32_t d = h2_max(a1, b1);
-          acc[j] = h2_fma(d, d, acc[j]);
+          acc[j] = h2_acc_delta2(acc[j], a1, b1);
         }
       }
       const int64_t i0 = tile * kTS + k * PARIS_INDEX_BLOCK + 4 * hl;
@@ -1250,9 +1272,9 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
     }
     __syncwarp();
     if (lane == 0) {
-      if (atomicAdd(&s_cnt[st], 1u) == kTWarps - 1) {
+      if (atomicAdd(&s_cnt[st], 1u) == kIWarps - 1) {
         s_cnt[st] = 0;
-        const int64_t next = li + (int64_t)kStages * gridDim.x;
+        const int64_t next = li + (int64_t)kIStages * gridDim.x;
         if (next < nlist) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           issue(next, st);
@@ -1262,7 +1284,7 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
   }
   wb_flush(wb, nslots, s_c, a, s_hist);
   __syncthreads();
-  for (int i = tid; i < nslots * kNB; i += kTThreads)
+  for (int i = tid; i < nslots * kNB; i += kIThreads)
     if (s_hist[i]) atomicAdd(&a.hist[i], s_hist[i]);
 }
 
@@ -1659,6 +1681,66 @@ __device__ __forceinline__ bool refine_step(const RefineArgs& a, const uint64_t*
   return stop;
 }
 
+// Refine up to U candidates of one query (k = 1): load the live rows whole
+// (lane l: float4 #(l + 32c)), accumulate the squared distance with early abandoning
+// after each 128-point chunk (north_star), lower the BSF (64-bit
+// atomicMin on (d^2, id)) and this warp's view of it (`cur`).
+template <int NC, int U>
+__device__ __forceinline__ void refine_group(const RefineArgs& a, const float4* __restrict__ qv,
+                                             const uint64_t (&key)[U], bool (&live)[U], float thr,
+                                             uint64_t& cur, unsigned long long* bp, unsigned& nref) {
+  const int lane = threadIdx.x & 31;
+  const int nf = a.len >> 2;
+  float4 x[U][NC];
+#pragma unroll
+  for (int u = 0; u < U; ++u) PARIS_DCHECK(!live[u] || key_id(key[u]) < (uint64_t)a.n);
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int f = lane + 32 * c;
+      x[u][c] = (live[u] && f < nf)
+                    ? ld_stream(reinterpret_cast<const float4*>(a.raw + (size_t)key_id(key[u]) * a.len) + f)
+                    : make_float4(0, 0, 0, 0);
+    }
+  float acc[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) acc[u] = 0.f;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const float4 q = (lane + 32 * c < nf) ? __ldg(qv + lane + 32 * c) : make_float4(0, 0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float d;
+      d = x[u][c].x - q.x; acc[u] = fmaf(d, d, acc[u]);
+      d = x[u][c].y - q.y; acc[u] = fmaf(d, d, acc[u]);
+      d = x[u][c].z - q.z; acc[u] = fmaf(d, d, acc[u]);
+      d = x[u][c].w - q.w; acc[u] = fmaf(d, d, acc[u]);
+    }
+    if (c + 1 < NC && 32 * (c + 1) < nf) {
+      // early abandoning after each 128-point chunk (the rest is not accumulated)
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (live[u] && warp_sum(acc[u]) > thr) { live[u] = false; ++nref; }
+      bool any = false;
+#pragma unroll
+      for (int u = 0; u < U; ++u) any |= live[u];
+      if (!any) break;
+    }
+  }
+  uint64_t mk = kNoKey;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    if (!live[u]) continue;
+    ++nref;
+    mk = min(mk, make_key(warp_sum(acc[u]), key_id(key[u])));
+  }
+  if (mk < cur) {
+    if (lane == 0) atomicMin(bp, (unsigned long long)mk);
+    cur = mk;
+  }
+}
+
 // k = 1 (P:1357-1378 with BSF = the best (d^2, id) key): a warp takes U
 // candidates at a time from its interleaved share of the query's LB-ordered list;
 // the live BSF is read (relaxed) in parallel with the keys; surviving rows are
@@ -1677,7 +1759,6 @@ k_refine1(RefineArgs a, int nb) {
   __shared__ unsigned s_refined[kMaxB], s_cnt[kMaxB];
   __shared__ float s_scale[kMaxB];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nf = a.len >> 2;
   if (threadIdx.x < kMaxB) {
     s_refined[threadIdx.x] = 0;
     // per-query list lengths and bin scales, read once per CTA (queries with no work
@@ -1718,55 +1799,92 @@ k_refine1(RefineArgs a, int nb) {
           stop = (a.lo + i0 + u * GW >= cnt) || (bin >= 1 && (float)(bin - 1) > thr * scale);
         }
       }
-      float4 x[U][NC];
-#pragma unroll
-      for (int u = 0; u < U; ++u) PARIS_DCHECK(!live[u] || key_id(key[u]) < (uint64_t)a.n);
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          const int f = lane + 32 * c;
-          x[u][c] = (live[u] && f < nf)
-                        ? ld_stream(reinterpret_cast<const float4*>(a.raw + (size_t)key_id(key[u]) * a.len) + f)
-                        : make_float4(0, 0, 0, 0);
-        }
-      float acc[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) acc[u] = 0.f;
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        const float4 q = (lane + 32 * c < nf) ? __ldg(qv + lane + 32 * c) : make_float4(0, 0, 0, 0);
+      refine_group<NC, U>(a, qv, key, live, thr, cur, bp, nref);
+      if (stop) break;
+    }
+    if (lane == 0 && nref) atomicAdd(&s_refined[b], nref);
+  }
+  __syncthreads();
+  if (threadIdx.x < nb && s_refined[threadIdx.x]) atomicAdd(&a.refined[threadIdx.x], s_refined[threadIdx.x]);
+}
+
+// k = 1 without the bucket sort (K5 skipped): the two LB-ordered waves are taken
+// straight from the LB pass's unsorted candidate lists.  Wave A refines the
+// candidates whose LB bin is <= cut[b] (the first bin at which the query's LB
+// histogram reaches wave_a candidates: the lowest-LB ~wave_a, which find the NN
+// early), wave B the rest.  A warp reads 32 keys at a time (one per lane,
+// coalesced), keeps those inside its wave with LB <= the live BSF, and
+// refines them U at a time, warp-cooperatively (refine_group).  Every key is read
+// once per wave (8 bytes against 4*len bytes per refined row), and the pruning
+// test is the same as the sorted walk's, so the refined set differs only by the
+// order within a wave.
+__global__ void __launch_bounds__(kNB) k_wave_cut(const unsigned* __restrict__ hist, unsigned wave_a,
+                                                  unsigned* __restrict__ cut) {
+  __shared__ unsigned s[kNB];
+  const int b = blockIdx.x, t = threadIdx.x;
+  s[t] = hist[b * kNB + t];
+  __syncthreads();
+  for (int o = 1; o < kNB; o <<= 1) {
+    const unsigned v = (t >= o) ? s[t - o] : 0u;
+    __syncthreads();
+    s[t] += v;
+    __syncthreads();
+  }
+  const bool reach = s[t] >= wave_a, prev = t > 0 && s[t - 1] >= wave_a;
+  if (reach && !prev) cut[b * kNB] = (unsigned)t;
+  if (t == kNB - 1 && !reach) cut[b * kNB] = (unsigned)(kNB - 1);
+}
+
+template <int NC, int U>
+__global__ void __launch_bounds__(kRefThreads, NC <= 2 ? 8 : 2)
+k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
+  __shared__ unsigned s_refined[kMaxB], s_cnt[kMaxB], s_cut[kMaxB];
+  __shared__ float s_scale[kMaxB];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x < kMaxB) {
+    const bool on = threadIdx.x < nb;
+    s_refined[threadIdx.x] = 0;
+    s_cnt[threadIdx.x] = on ? (unsigned)imin64((int64_t)a.count[threadIdx.x], a.cap) : 0u;
+    s_cut[threadIdx.x] = on ? cut[threadIdx.x * kNB] : 0u;
+    s_scale[threadIdx.x] = on ? bin_scale(__uint_as_float(a.thr_seed[threadIdx.x])) : 0.f;
+  }
+  __syncthreads();
+  const unsigned gw = blockIdx.x * kRefWarps + warp, GW = gridDim.x * kRefWarps;
+  for (int b = 0; b < nb; ++b) {
+    const unsigned cnt = s_cnt[b];
+    const unsigned nchunk = (cnt + 31) / 32;
+    const unsigned first = (gw + (unsigned)b * 613u) % GW;  // rotate: spread small lists over all warps
+    if (first >= nchunk) continue;
+    const float scale = s_scale[b];
+    const int cutb = (int)s_cut[b];
+    const uint64_t* list = a.sorted + (size_t)b * a.cap;
+    const float4* qv = reinterpret_cast<const float4*>(a.queries + (size_t)b * a.len);
+    unsigned long long* bp = a.best + (size_t)b * kPadU64;
+    unsigned nref = 0;
+    uint64_t cur = kNoKey;
+    for (unsigned ch = first; ch < nchunk; ch += GW) {
+      const unsigned i = ch * 32 + lane;
+      const uint64_t k0 = i < cnt ? __ldg(list + i) : kNoKey;
+      cur = min(cur, ld_relaxed_u64(bp));
+      float thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
+      const float lb0 = key_val(k0);
+      const int bin = lb_bin(lb0, scale);
+      const bool mine = i < cnt && (wave == 0 ? bin <= cutb : bin > cutb);
+      unsigned m = __ballot_sync(0xffffffffu, mine && lb0 <= thr);
+      while (m) {
+        uint64_t key[U];
+        bool live[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          float d;
-          d = x[u][c].x - q.x; acc[u] = fmaf(d, d, acc[u]);
-          d = x[u][c].y - q.y; acc[u] = fmaf(d, d, acc[u]);
-          d = x[u][c].z - q.z; acc[u] = fmaf(d, d, acc[u]);
-          d = x[u][c].w - q.w; acc[u] = fmaf(d, d, acc[u]);
+          const int src = m ? __ffs(m) - 1 : 0;
+          const bool has = m != 0u;
+          m &= m - 1;
+          key[u] = __shfl_sync(0xffffffffu, k0, src);
+          live[u] = has && key_val(key[u]) <= thr;
         }
-        if (c + 1 < NC && 32 * (c + 1) < nf) {
-          // early abandoning after each 128-point chunk (the rest is not accumulated)
-#pragma unroll
-          for (int u = 0; u < U; ++u)
-            if (live[u] && warp_sum(acc[u]) > thr) { live[u] = false; ++nref; }
-          bool any = false;
-#pragma unroll
-          for (int u = 0; u < U; ++u) any |= live[u];
-          if (!any) break;
-        }
+        refine_group<NC, U>(a, qv, key, live, thr, cur, bp, nref);
+        thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
       }
-      uint64_t mk = kNoKey;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (!live[u]) continue;
-        ++nref;
-        mk = min(mk, make_key(warp_sum(acc[u]), key_id(key[u])));
-      }
-      if (mk < cur) {
-        if (lane == 0) atomicMin(bp, (unsigned long long)mk);
-        cur = mk;
-      }
-      if (stop) break;
     }
     if (lane == 0 && nref) atomicAdd(&s_refined[b], nref);
   }
@@ -1984,6 +2102,7 @@ struct Plan {
   const uint8_t* env;    // index mode: block envelopes
   int idx_seeds;         // index mode: series around the query's leaf
   bool nb;               // f2: nb-ParIS+ (per-worker BSF copies, fused LB -> refine)
+  bool sorted_refine = false;  // k = 1: walk bucket-sorted lists (K5) instead of the unsorted waves
 };
 
 int pairs_for(int nb) { return nb <= 2 ? 1 : nb <= 4 ? 2 : nb <= 8 ? 4 : nb <= 16 ? 8 : 16; }
@@ -2081,7 +2200,7 @@ cudaError_t launch_index_lb(const Plan& p, const uint8_t* sax, int nb, const Car
                                ws.tile_count, ws.blocks);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(sms(), ntiles);
-  return PARIS_LAUNCH("lb_pass", k_lbi<P>, grid, kTThreads, kLbiSmem, st, la, ws.bmask, ws.tile_list, ws.tile_count);
+  return PARIS_LAUNCH("lb_pass", k_lbi<P>, grid, kIThreads, kLbiSmem, st, la, ws.bmask, ws.tile_list, ws.tile_count);
 }
 
 cudaError_t dispatch_index_lb(int nb, const Plan& p, const uint8_t* sax, const CardTables* tab, const Ws& ws,
@@ -2164,6 +2283,12 @@ cudaError_t launch_refine1(const RefineArgs& ra, int nb, int64_t max_work, cudaS
   const int64_t need = (max_work + (int64_t)kRefWarps * U - 1) / ((int64_t)kRefWarps * U);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(full, need));
   return PARIS_LAUNCH("refine", (k_refine1<NC, U>), grid, kRefThreads, 0, st, ra, nb);
+}
+
+template <int NC, int U>
+cudaError_t launch_refine1u(const RefineArgs& ra, int nb, int wave, const unsigned* cut, cudaStream_t st) {
+  const int grid = sms() * (NC <= 2 ? 8 : 2);
+  return PARIS_LAUNCH("refine", (k_refine1u<NC, U>), grid, kRefThreads, 0, st, ra, nb, wave, cut);
 }
 
 // Allocate the batch scratch for `cap` candidates per query.
@@ -2275,15 +2400,22 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
   } else {
     PARIS_CHECK_LAUNCH(dispatch_p(P, true, p, sax, qbatch, nb, tab, ws, st, cap), "lb_pass launch");
   }
-  {
+  // k = 1: the refine takes its two LB waves straight from the unsorted lists (K5
+  // skipped; config reserved[1] = 1 restores the bucket-sorted walk); k > 1 walks
+  // the bucket-sorted lists
+  const bool unsorted = p.k == 1 && !p.sorted_refine;
+  if (!unsorted) {
     const int xs = std::max(1, std::min(sms() * 4 / nb, 1024));
     dim3 g((unsigned)xs, (unsigned)nb);
     PARIS_CHECK_LAUNCH(PARIS_LAUNCH("scatter", k_scatter, g, 256, 0, st, ws.cand, ws.count, ws.hist, ws.thr_seed,
                                     ws.cursor, ws.sorted, cap),
                        "scatter launch");
+  } else {
+    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("wave_cut", k_wave_cut, nb, kNB, 0, st, ws.hist, (unsigned)p.wave_a, ws.cursor),
+                       "wave_cut launch");
   }
   RefineArgs ra;
-  ra.raw = raw; ra.len = p.len; ra.queries = qbatch; ra.sorted = ws.sorted; ra.cap = cap;
+  ra.raw = raw; ra.len = p.len; ra.queries = qbatch; ra.sorted = unsorted ? ws.cand : ws.sorted; ra.cap = cap;
   ra.count = ws.count; ra.thr_seed = ws.thr_seed; ra.thr = ws.thr; ra.best = ws.best;
   ra.refined = ws.refined; ra.lists = ws.lists; ra.k = p.k; ra.d2up = p.d2up;
   ra.lo = 0; ra.hi = 0xFFFFFFFFu; ra.n = p.n;
@@ -2293,7 +2425,16 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
     const int NC = p.len <= 128 ? 1 : p.len <= 256 ? 2 : p.len <= 512 ? 4 : p.len <= 1024 ? 8 : 32;
     // wave A: the lowest-LB wave_a candidates of every query (finds the NN early, so
     // wave B -- the rest, in LB order -- prunes against a tight BSF)
-    for (int wv = 0; wv < 2 && e1 == cudaSuccess; ++wv) {
+    for (int wv = 0; wv < 2 && e1 == cudaSuccess && unsorted; ++wv) {
+      switch (NC) {
+        case 1: e1 = launch_refine1u<1, 2>(ra, nb, wv, ws.cursor, st); break;
+        case 2: e1 = launch_refine1u<2, 1>(ra, nb, wv, ws.cursor, st); break;
+        case 4: e1 = launch_refine1u<4, 1>(ra, nb, wv, ws.cursor, st); break;
+        case 8: e1 = launch_refine1u<8, 1>(ra, nb, wv, ws.cursor, st); break;
+        default: e1 = launch_refine1u<32, 1>(ra, nb, wv, ws.cursor, st); break;
+      }
+    }
+    for (int wv = 0; wv < 2 && e1 == cudaSuccess && !unsorted; ++wv) {
       RefineArgs rb = ra;
       rb.lo = wv == 0 ? 0u : (unsigned)p.wave_a;
       rb.hi = wv == 0 ? (unsigned)p.wave_a : 0xFFFFFFFFu;
@@ -2460,6 +2601,7 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   p.nb = nb_mode;
   // index seeds: 1024 series around the leaf by default; 64 when raw is in host memory,
   // where every seed is a PCIe read (measured: C5 62.7 K q/s with 64 vs 29 K with 1024)
+  p.sorted_refine = cfg && cfg->reserved[1] == 1;
   p.idx_seeds = (cfg && cfg->reserved[2] > 0) ? cfg->reserved[2] : (raw_host ? kIdxSeedsHost : 0);
   plan_seed(p, (cfg && cfg->seed_div > 0) ? cfg->seed_div : 16);
   p.cap = nb_mode ? 1 : std::min<int64_t>(n, std::max<int64_t>(65536, n / 32));

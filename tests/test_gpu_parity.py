@@ -220,3 +220,26 @@ def test_knn_tiled_path_parity(P, torch_dev, n, nq):
         check_knn(x, q, gi, gd, ri, rd2)
         gi2, gd2 = _knn_case(P, torch_dev, x, q, k, config=p.KnnConfig(force_direct=True))
         check_knn(x, q, gi2, gd2, ri, rd2)
+
+
+@pytest.mark.parametrize("wave_a", [1, 7, 2048, 1_000_000])
+@pytest.mark.parametrize("sorted_refine", [False, True])
+def test_knn_refine_waves(P, torch_dev, wave_a, sorted_refine):
+    """k = 1 refinement: the two LB waves taken from the unsorted candidate lists (default)
+    and from the bucket-sorted lists (K5), for wave cuts from one candidate to all of them,
+    on the flat and the index path, against the oracle (noisy members: many near ties)."""
+    import paper_2009_00166_b200 as p
+    torch, dev = torch_dev
+    n = 30_000
+    x = datagen.random_walks(n, 256, 4242)
+    q = datagen.random_walks(20, 256, 4243)
+    q[:10] = datagen.noisy_members(x, np.arange(10) * 2999, 0.2, 4244)
+    ri, rd2 = oracle.knn_bruteforce(x, q, 1)
+    cfg = p.KnnConfig(wave_a=wave_a, sorted_refine=sorted_refine)
+    gi, gd = _knn_case(P, torch_dev, x, q, 1, config=cfg)
+    check_knn(x, q, gi, gd, ri, rd2)
+    xd = torch.from_numpy(x).to(dev)
+    sax = P.summarize(xd, 16, 256)
+    idx = P.index_build(sax, 16, 256)
+    hi, hd = P.knn_index(xd, idx, torch.from_numpy(q).to(dev), k=1, config=cfg)
+    check_knn(x, q, hi.cpu().numpy(), hd.cpu().numpy(), ri, rd2)
