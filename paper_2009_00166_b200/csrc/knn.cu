@@ -1167,6 +1167,10 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
   unsigned* s_hist = reinterpret_cast<unsigned*>(dsm + kITabEnd);  // [kMaxB][kNB] after the ring + table
   __shared__ __align__(8) uint64_t s_full[kIStages];
   __shared__ unsigned s_cnt[kIStages];
+  // per stage: the tile's id and its 32 block masks, delivered with the tile (the
+  // warps never wait on a global load at a tile boundary)
+  __shared__ __align__(16) uint32_t s_bm[kIStages][kBPT];
+  __shared__ int64_t s_tile[kIStages];
   __shared__ uint32_t s_qs[2 * P][kTW];  // per slot and segment: half2(q_lo16, -q_hi16)
   __shared__ LbConsts s_c;
   __shared__ WarpBuf s_wb[kIWarps];
@@ -1180,10 +1184,15 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
 
   static_assert(kTS == PARIS_INDEX_TILE, "index tiles are the LB kernel's tiles");
   auto issue = [&](int64_t li, int st) {
-    // tile-major sorted SAX: the tile's 16 rows are one contiguous 32 KB range
-    mbar_expect_tx(&s_full[st], (unsigned)kTileBytes);
-    bulk_g2s(s_tiles + (size_t)st * kTileBytes, a.sax + (size_t)tile_list[li] * kTileBytes, (unsigned)kTileBytes,
+    // tile-major sorted SAX: the tile's 16 rows are one contiguous 32 KB range; its
+    // block masks (128 B) ride on the same barrier; the id is published before the
+    // arrive (release), so waiters that see the phase flip see it too
+    const int64_t tile = tile_list[li];
+    s_tile[st] = tile;
+    mbar_expect_tx(&s_full[st], (unsigned)(kTileBytes + kBPT * 4));
+    bulk_g2s(s_tiles + (size_t)st * kTileBytes, a.sax + (size_t)tile * kTileBytes, (unsigned)kTileBytes,
              &s_full[st]);
+    bulk_g2s(&s_bm[st][0], bmask + (size_t)tile * kBPT, (unsigned)(kBPT * 4), &s_full[st]);
   };
   if (tid == 0) {
     for (int st = 0; st < kIStages; ++st) {
@@ -1214,13 +1223,14 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
     const int64_t li = blockIdx.x + it * gridDim.x;
     if (li >= nlist) break;
     const int st = (int)(it % kIStages);
-    const int64_t tile = tile_list[li];
+    mbar_wait(&s_full[st], (unsigned)((it / kIStages) & 1));
+    const int64_t tile = s_tile[st];
     PARIS_DCHECK(tile >= 0 && tile * kTS < a.n);
     // the tile's 32 block masks (lane = block); a block's live slots are computed two
     // at a time (consecutive live slots form an item); a 64-series block is half a
     // warp, so a warp takes two items per round (lanes 0-15 and 16-31); items are
     // dealt round-robin, rotating, so no warp is systematically behind
-    const uint32_t bm = __ldg(bmask + tile * kBPT + lane);
+    const uint32_t bm = s_bm[st][lane];
     const int cnt = (__popc(bm) + 1) >> 1;
     int incl = cnt;
 #pragma unroll
@@ -1229,7 +1239,6 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
       if (lane >= o) incl += v;
     }
     const int total = __shfl_sync(0xffffffffu, incl, 31);
-    mbar_wait(&s_full[st], (unsigned)((it / kIStages) & 1));
     const uint32_t* rows = reinterpret_cast<const uint32_t*>(s_tiles + (size_t)st * kTileBytes);
     const int first = (warp - rot + 2 * kIWarps) % kIWarps;
     rot = (rot + (total + 1) / 2) % kIWarps;
