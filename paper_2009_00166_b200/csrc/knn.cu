@@ -815,6 +815,7 @@ constexpr size_t kTSmem = kStages * kTileBytes + kMaxCard * 32 * 4;
 constexpr int kIStages = 2;      // compute-bound on the live items: a tile's load (~0.8 us) < its work
 constexpr int kIThreads = 768;   // 24 warps: more warps to hide the lookup -> math latency chain
 constexpr int kIWarps = kIThreads / 32;
+constexpr int kITileIds = 1024;  // tile ids staged per CTA (148 CTAs: 310 M series; beyond, global loads)
 constexpr size_t kITabEnd = kIStages * kTileBytes + (size_t)kMaxCard * 32 * 8;
 constexpr size_t kLbiSmem = kITabEnd + (size_t)kMaxB * kNB * 4;
 
@@ -1171,6 +1172,9 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
   // warps never wait on a global load at a tile boundary)
   __shared__ __align__(16) uint32_t s_bm[kIStages][kBPT];
   __shared__ int64_t s_tile[kIStages];
+  // this CTA's share of the tile list (entries blockIdx.x + i * gridDim.x), staged once:
+  // a refill then starts its TMA without a dependent global load
+  __shared__ unsigned s_tl[kITileIds];
   __shared__ uint32_t s_qs[2 * P][kTW];  // per slot and segment: half2(q_lo16, -q_hi16)
   __shared__ LbConsts s_c;
   __shared__ WarpBuf s_wb[kIWarps];
@@ -1187,7 +1191,8 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
     // tile-major sorted SAX: the tile's 16 rows are one contiguous 32 KB range; its
     // block masks (128 B) ride on the same barrier; the id is published before the
     // arrive (release), so waiters that see the phase flip see it too
-    const int64_t tile = tile_list[li];
+    const int64_t i = (li - blockIdx.x) / gridDim.x;
+    const int64_t tile = i < kITileIds ? s_tl[i] : tile_list[li];
     s_tile[st] = tile;
     mbar_expect_tx(&s_full[st], (unsigned)(kTileBytes + kBPT * 4));
     bulk_g2s(s_tiles + (size_t)st * kTileBytes, a.sax + (size_t)tile * kTileBytes, (unsigned)kTileBytes,
@@ -1200,6 +1205,11 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
       s_cnt[st] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int64_t i = tid; i < kITileIds; i += kIThreads) {
+    const int64_t li = blockIdx.x + i * gridDim.x;
+    if (li >= nlist) break;
+    s_tl[i] = tile_list[li];
   }
   __syncthreads();
   if (tid == 0) {
