@@ -540,8 +540,9 @@ struct LbArgs {
   uint64_t* cand;
   int64_t cap;
   const uint32_t* perm;  // index mode: sorted position -> series id (else nullptr)
-  const uint8_t* env;    // index mode: [n/128 blocks][2][16] min/max symbols (else nullptr)
-  unsigned* blocks;      // index mode: per query, blocks whose envelope bound passed
+  const uint8_t* env;    // index mode: [ceil(n/64) blocks][2][16] min/max symbols (else nullptr)
+  const uint8_t* env_sub = nullptr;  // index mode: [n/16 sub-blocks][2][16] min/max symbols
+  unsigned* blocks;      // index mode: per query, sub-blocks whose envelope bound passed
 };
 
 struct LbConsts {
@@ -815,6 +816,9 @@ constexpr size_t kTSmem = kStages * kTileBytes + kMaxCard * 32 * 4;
 constexpr int kIStages = 2;      // compute-bound on the live items: a tile's load (~0.8 us) < its work
 constexpr int kIThreads = 768;   // 24 warps: more warps to hide the lookup -> math latency chain
 constexpr int kIWarps = kIThreads / 32;
+constexpr int kSPT = 2048 / PARIS_INDEX_SUB;    // index sub-blocks per tile (128)
+constexpr int kSubPB = PARIS_INDEX_BLOCK / PARIS_INDEX_SUB;  // sub-blocks per block (4)
+constexpr int kUPR = 32 / (PARIS_INDEX_SUB / 4);  // units per warp round (8: 4 lanes x 4 series each)
 constexpr int kITileIds = 1024;  // tile ids staged per CTA (148 CTAs: 310 M series; beyond, global loads)
 constexpr size_t kITabEnd = kIStages * kTileBytes + (size_t)kMaxCard * 32 * 8;
 constexpr size_t kLbiSmem = kITabEnd + (size_t)kMaxB * kNB * 4;
@@ -1024,15 +1028,13 @@ k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
 }
 
 // ---------------------------------------------------------------- index mode LB (f1)
-// Pass 1 (k_blkmask): the envelope MINDIST of every 128-series block for every
-// query slot (the iSAX node bound): bit b of bmask[blk] = block may hold a
-// candidate of slot b.  A CTA covers the 16 blocks of one SAX tile and appends
-// the tile to a work list when any of its blocks is live.
-// Pass 2 (k_lbi): the TMA ring streams only listed tiles; the live (block, query
-// pair) items of a tile are dealt round-robin to its 16 warps (every warp derives
-// the same item list from the 16 block masks, no CTA barrier), so warps stay
-// balanced however the live blocks are spread.
-// Candidate emission of one index item: 4 series x 2 query slots (sa = low half,
+// Three levels, each a valid lower bound on its members' MINDIST (the iSAX node
+// bound of the sorted array's blocks):
+//   k_blkmask  64-series blocks x every query slot -> (block, slot pair) items;
+//   k_submask  the items' 16-series sub-blocks -> per sub-block live-slot masks,
+//              and the list of tiles holding a live sub-block;
+//   k_lbi      the series of live sub-blocks, for their live slots only.
+// Candidate emission of one index unit: 4 series x 2 query slots// Candidate emission of one index item: 4 series x 2 query slots (sa = low half,
 // sb = high half, sb < 0: none).  Same tests and warp buffer as lb_emit_wb.
 __device__ __forceinline__ uint32_t half_of(uint32_t v, int h) { return (v >> (16 * h)) & 0xFFFFu; }
 
@@ -1092,26 +1094,22 @@ __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int s
   __syncwarp();
 }
 
-// One lane per block: lane l of a warp bounds block 32*g + l against every query
-// slot (region [L[min_s], U[max_s]] per segment, outward fp32, round-down sums);
-// the 32 blocks of a warp step are one whole tile, so the warp lists it itself.
+// Level 1 (k_blkmask), one lane per 64-series block: lane l of a warp bounds block
+// 32*g + l against every query slot (region [L[min_s], U[max_s]] per segment, in
+// the packed fp16 pair form and error budget of the series bound); every (block,
+// slot pair) with a live slot becomes an item for level 2, and the block's four
+// sub-block masks are cleared.
 template <int P>
 __global__ void __launch_bounds__(256)
-k_blkmask(LbArgs a, unsigned* __restrict__ bmask, unsigned* __restrict__ tile_list,
-          unsigned* __restrict__ tile_count, unsigned* __restrict__ blocks) {
-  // the envelope bound in the same packed fp16 pair form (and error budget, k_lb)
-  // as the series bound: per segment the region [L16[min], U16[max]], two query
-  // slots per instruction; a block is live for slot b iff its fp16 bound <= T16[b]
-  constexpr int NS = 2 * P;
+k_blkmask(LbArgs a, unsigned* __restrict__ items, unsigned* __restrict__ item_count,
+          unsigned* __restrict__ submask) {
   __shared__ uint2 s_lu16[kMaxCard];
   __shared__ uint2 s_q16[kTW * P];
   __shared__ LbConsts s_c;
-  __shared__ unsigned s_blk[kMaxB];
   const int tid = threadIdx.x, lane = tid & 31;
   for (int i = tid; i < kMaxCard; i += blockDim.x) s_lu16[i] = a.tab->lu16[i];
   for (int i = tid; i < kTW * P; i += blockDim.x) s_q16[i] = a.g_q16[i];
-  if (tid < kMaxB) s_blk[tid] = 0;
-  lb_consts_init(a, NS, &s_c);  // ends with __syncthreads
+  lb_consts_init(a, 2 * P, &s_c);  // ends with __syncthreads
   const int64_t nblocks = (a.n + PARIS_INDEX_BLOCK - 1) / PARIS_INDEX_BLOCK;
   const int64_t ntiles = (a.n + kTS - 1) / kTS;
   static_assert(kBPT == 32, "a warp step bounds the 32 blocks of one tile");
@@ -1141,22 +1139,88 @@ k_blkmask(LbArgs a, unsigned* __restrict__ bmask, unsigned* __restrict__ tile_li
 #pragma unroll
       for (int p = 0; p < P; ++p) bm |= h2_le_bits(acc[p], s_c.T16[p]) << (2 * p);
     }
-    bmask[blk] = bm;  // padded to whole tiles
-    const unsigned live = __ballot_sync(0xffffffffu, bm != 0u);
-    if (lane == 0 && live) tile_list[atomicAdd(tile_count, 1u)] = (unsigned)g;
+    // the block's 4 sub-block masks start empty (padded to whole tiles)
+    reinterpret_cast<uint4*>(submask)[blk] = make_uint4(0u, 0u, 0u, 0u);
+    // items: (block << 6) | (pair << 2) | the pair's live slots
+    uint32_t pm = 0;
 #pragma unroll
-    for (int b = 0; b < NS; ++b) {
-      const unsigned m = __ballot_sync(0xffffffffu, (bm >> b) & 1u);
-      if (lane == 0 && m) atomicAdd(&s_blk[b], (unsigned)__popc(m));
+    for (int p = 0; p < P; ++p) pm |= ((bm >> (2 * p)) & 3u) ? (1u << p) : 0u;
+    const int cnt = __popc(pm);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    unsigned base = 0;
+    if (lane == 31 && incl) base = atomicAdd(item_count, (unsigned)incl);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    unsigned pos = base + (unsigned)(incl - cnt);
+    for (uint32_t r = pm; r; r &= r - 1) {
+      const int p = __ffs(r) - 1;
+      items[pos++] = ((uint32_t)blk << 6) | ((uint32_t)p << 2) | ((bm >> (2 * p)) & 3u);
     }
   }
-  __syncthreads();
-  if (tid < NS && s_blk[tid]) atomicAdd(&blocks[tid], s_blk[tid]);
 }
 
+// Level 2 (k_submask), one thread per (item, sub-block): the envelope bound of a
+// 16-series sub-block for the item's live slots; a live (sub-block, slot) sets its
+// bit in submask[sub-block] and the sub-block's tile joins the tile list (once).
+// A sub-block's symbol ranges lie inside its block's, so its bound is the tighter
+// of the two (the k_lbi work drops to the series of live sub-blocks).
+template <int P>
+__global__ void __launch_bounds__(256)
+k_submask(LbArgs a, const unsigned* __restrict__ items, const unsigned* __restrict__ item_count,
+          unsigned* __restrict__ submask, unsigned* __restrict__ tile_list, unsigned* __restrict__ tile_count,
+          unsigned* __restrict__ tile_flag) {
+  __shared__ uint2 s_lu16[kMaxCard];
+  __shared__ uint2 s_q16[kTW * P];
+  __shared__ LbConsts s_c;
+  __shared__ unsigned s_sub[kMaxB];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < kMaxCard; i += blockDim.x) s_lu16[i] = a.tab->lu16[i];
+  for (int i = tid; i < kTW * P; i += blockDim.x) s_q16[i] = a.g_q16[i];
+  if (tid < kMaxB) s_sub[tid] = 0;
+  lb_consts_init(a, 2 * P, &s_c);  // ends with __syncthreads
+  const int64_t ntest = (int64_t)*item_count * kSubPB;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + tid; t < ntest; t += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t it = items[t / kSubPB];
+    const int64_t sb = (int64_t)(it >> 6) * kSubPB + (t % kSubPB);
+    const int p = (it >> 2) & 15;
+    const uint32_t live2 = it & 3u;
+    if (sb * PARIS_INDEX_SUB >= a.n) continue;
+    const uint4 mn = __ldg(reinterpret_cast<const uint4*>(a.env_sub + (size_t)sb * 32));
+    const uint4 mx = __ldg(reinterpret_cast<const uint4*>(a.env_sub + (size_t)sb * 32 + 16));
+    const uint32_t mnw[4] = {mn.x, mn.y, mn.z, mn.w}, mxw[4] = {mx.x, mx.y, mx.z, mx.w};
+    uint32_t acc = 0u;
+#pragma unroll
+    for (int seg = 0; seg < kTW; ++seg) {
+      const uint32_t tx = s_lu16[(mxw[seg >> 2] >> (8 * (seg & 3))) & 0xFFu].x;
+      const uint32_t ty = s_lu16[(mnw[seg >> 2] >> (8 * (seg & 3))) & 0xFFu].y;
+      const uint2 q = s_q16[seg * P + p];
+      acc = h2_acc_delta2(acc, h2_fma_relu(q.x, kHalf2One, tx), h2_fma_relu(q.y, kHalf2One, ty));
+    }
+    const uint32_t bits = h2_le_bits(acc, s_c.T16[p]) & live2;
+    if (!bits) continue;
+    atomicOr(&submask[sb], bits << (2 * p));
+    if (bits & 1u) atomicAdd(&s_sub[2 * p], 1u);
+    if (bits & 2u) atomicAdd(&s_sub[2 * p + 1], 1u);
+    const int64_t tile = sb / kSPT;
+    if (ld_relaxed_u32(tile_flag + tile) == 0u && atomicExch(&tile_flag[tile], 1u) == 0u)
+      tile_list[atomicAdd(tile_count, 1u)] = (unsigned)tile;
+  }
+  __syncthreads();
+  if (tid < 2 * P && s_sub[tid]) atomicAdd(&a.blocks[tid], s_sub[tid]);
+}
+
+// Level 3 (k_lbi): the TMA ring streams the listed tiles (32 KB of SAX + the 128
+// sub-block masks, on one barrier); the live (sub-block, slot pair) units of a tile
+// -- consecutive live slots of a sub-block, two at a time -- are dealt round-robin
+// to the warps, 8 units per warp round (4 lanes x 4 series per unit).  Every warp
+// derives the same unit list from the masks (no CTA barrier).
 template <int P>
 __global__ void __launch_bounds__(kIThreads, 1)
-k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__ tile_list,
+k_lbi(LbArgs a, const unsigned* __restrict__ submask, const unsigned* __restrict__ tile_list,
       const unsigned* __restrict__ tile_count) {
   extern __shared__ __align__(128) uint8_t dsm[];
   uint8_t* s_tiles = dsm;
@@ -1168,14 +1232,14 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
   unsigned* s_hist = reinterpret_cast<unsigned*>(dsm + kITabEnd);  // [kMaxB][kNB] after the ring + table
   __shared__ __align__(8) uint64_t s_full[kIStages];
   __shared__ unsigned s_cnt[kIStages];
-  // per stage: the tile's id and its 32 block masks, delivered with the tile (the
-  // warps never wait on a global load at a tile boundary)
-  __shared__ __align__(16) uint32_t s_bm[kIStages][kBPT];
+  // per stage: the tile's id and its sub-block masks, delivered with the tile
+  __shared__ __align__(16) uint32_t s_sm[kIStages][kSPT];
   __shared__ int64_t s_tile[kIStages];
   // this CTA's share of the tile list (entries blockIdx.x + i * gridDim.x), staged once:
   // a refill then starts its TMA without a dependent global load
   __shared__ unsigned s_tl[kITileIds];
-  __shared__ uint32_t s_qs[2 * P][kTW];  // per slot and segment: half2(q_lo16, -q_hi16)
+  __shared__ uint16_t s_uinc[kIWarps][kSPT];  // per warp: inclusive unit counts over the tile's sub-blocks
+  __shared__ uint32_t s_qs[2 * P][kTW + 1];   // per slot and segment: half2(q_lo16, -q_hi16); +1: banks
   __shared__ LbConsts s_c;
   __shared__ WarpBuf s_wb[kIWarps];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1186,18 +1250,18 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
   if (lane == 0) wb.n = 0;
   for (int i = tid; i < nslots * kNB; i += kIThreads) s_hist[i] = 0;
 
-  static_assert(kTS == PARIS_INDEX_TILE, "index tiles are the LB kernel's tiles");
+  static_assert(kTS == PARIS_INDEX_TILE && kSPT == 128, "index tiles are the LB kernel's tiles");
   auto issue = [&](int64_t li, int st) {
     // tile-major sorted SAX: the tile's 16 rows are one contiguous 32 KB range; its
-    // block masks (128 B) ride on the same barrier; the id is published before the
-    // arrive (release), so waiters that see the phase flip see it too
+    // sub-block masks (512 B) ride on the same barrier; the id is published before
+    // the arrive (release), so waiters that see the phase flip see it too
     const int64_t i = (li - blockIdx.x) / gridDim.x;
     const int64_t tile = i < kITileIds ? s_tl[i] : tile_list[li];
     s_tile[st] = tile;
-    mbar_expect_tx(&s_full[st], (unsigned)(kTileBytes + kBPT * 4));
+    mbar_expect_tx(&s_full[st], (unsigned)(kTileBytes + kSPT * 4));
     bulk_g2s(s_tiles + (size_t)st * kTileBytes, a.sax + (size_t)tile * kTileBytes, (unsigned)kTileBytes,
              &s_full[st]);
-    bulk_g2s(&s_bm[st][0], bmask + (size_t)tile * kBPT, (unsigned)(kBPT * 4), &s_full[st]);
+    bulk_g2s(&s_sm[st][0], submask + (size_t)tile * kSPT, (unsigned)(kSPT * 4), &s_full[st]);
   };
   if (tid == 0) {
     for (int st = 0; st < kIStages; ++st) {
@@ -1227,6 +1291,8 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
   lb_consts_init(a, nslots, &s_c);  // ends with __syncthreads
   const char* tabc = reinterpret_cast<const char*>(s_tab);
   const uint32_t lane8 = (uint32_t)lane * 8u;  // < 256: byte 0 of the table offset
+  const int grp = lane >> 2, gl = lane & 3;    // unit slot of this lane in a round, lane within the unit
+  uint16_t* uinc = s_uinc[warp];
   int rot = 0;
 
   for (int64_t it = 0;; ++it) {
@@ -1236,41 +1302,51 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
     mbar_wait(&s_full[st], (unsigned)((it / kIStages) & 1));
     const int64_t tile = s_tile[st];
     PARIS_DCHECK(tile >= 0 && tile * kTS < a.n);
-    // the tile's 32 block masks (lane = block); a block's live slots are computed two
-    // at a time (consecutive live slots form an item); a 64-series block is half a
-    // warp, so a warp takes two items per round (lanes 0-15 and 16-31); items are
-    // dealt round-robin, rotating, so no warp is systematically behind
-    const uint32_t bm = s_bm[st][lane];
-    const int cnt = (__popc(bm) + 1) >> 1;
-    int incl = cnt;
+    // unit counts: lane l owns sub-blocks 4l..4l+3
+    const uint4 smv = *reinterpret_cast<const uint4*>(&s_sm[st][4 * lane]);
+    const int c0 = (__popc(smv.x) + 1) >> 1, c1 = (__popc(smv.y) + 1) >> 1;
+    const int c2 = (__popc(smv.z) + 1) >> 1, c3 = (__popc(smv.w) + 1) >> 1;
+    const int own = c0 + c1 + c2 + c3;
+    int incl = own;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int v = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += v;
     }
     const int total = __shfl_sync(0xffffffffu, incl, 31);
+    {
+      const int e = incl - own;
+      uinc[4 * lane] = (uint16_t)(e + c0);
+      uinc[4 * lane + 1] = (uint16_t)(e + c0 + c1);
+      uinc[4 * lane + 2] = (uint16_t)(e + c0 + c1 + c2);
+      uinc[4 * lane + 3] = (uint16_t)incl;
+    }
+    __syncwarp();
     const uint32_t* rows = reinterpret_cast<const uint32_t*>(s_tiles + (size_t)st * kTileBytes);
     const int first = (warp - rot + 2 * kIWarps) % kIWarps;
-    rot = (rot + (total + 1) / 2) % kIWarps;
-    const int h = lane >> 4, hl = lane & 15;
-    for (int t0 = 2 * first; t0 < total; t0 += 2 * kIWarps) {
-      const int t = t0 + h;  // this half-warp's item
-      const unsigned m0 = __ballot_sync(0xffffffffu, incl <= t0);
-      const unsigned m1 = __ballot_sync(0xffffffffu, incl <= t0 + 1);
+    rot = (rot + (total + kUPR - 1) / kUPR) % kIWarps;
+    for (int t0 = kUPR * first; t0 < total; t0 += kUPR * kIWarps) {
+      const int t = t0 + grp;  // this lane group's unit
       const bool active = t < total;
-      const int k = active ? __popc(h ? m1 : m0) : 0;
-      const int excl = __shfl_sync(0xffffffffu, incl - cnt, k);
-      const uint32_t bmk = __shfl_sync(0xffffffffu, bm, k);
+      // sub-block of unit t: the number of sub-blocks whose inclusive count is <= t
+      int k = 0;
+#pragma unroll
+      for (int stp = kSPT / 2; stp > 0; stp >>= 1)
+        if ((int)uinc[k + stp - 1] <= t) k += stp;
+      k = active ? k : 0;
+      const int excl = k ? (int)uinc[k - 1] : 0;
+      const uint32_t smk = s_sm[st][k];
       const int r = t - excl;
-      const int saf = active ? __fns(bmk, 0, 2 * r + 1) : 0;
+      const int saf = active ? __fns(smk, 0, 2 * r + 1) : 0;
       const int sa = (saf >= 0 && saf < 32) ? saf : 0;
-      const int sbf = active ? __fns(bmk, 0, 2 * r + 2) : -1;
+      const int sbf = active ? __fns(smk, 0, 2 * r + 2) : -1;
       const int sb = (sbf >= 0 && sbf < 32) ? sbf : -1;
       const int sq = sb >= 0 ? sb : sa;  // odd count: duplicate lane, masked in emission
       uint32_t acc[4] = {0u, 0u, 0u, 0u};
+      const uint32_t* rw = rows + k * (PARIS_INDEX_SUB / 4) + gl;
 #pragma unroll 4
       for (int s = 0; s < kTW; ++s) {
-        const uint32_t word = rows[s * (kTS / 4) + k * (PARIS_INDEX_BLOCK / 4) + hl];
+        const uint32_t word = rw[s * (kTS / 4)];
         const uint32_t qa = s_qs[sa][s], qb = s_qs[sq][s];
         const uint32_t qx = __byte_perm(qa, qb, 0x5410);  // (q_lo16[sa], q_lo16[sb])
         const uint32_t qy = __byte_perm(qa, qb, 0x7632);  // (-q_hi16[sa], -q_hi16[sb])
@@ -1284,9 +1360,9 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
           acc[j] = h2_acc_delta2(acc[j], a1, b1);
         }
       }
-      const int64_t i0 = tile * kTS + k * PARIS_INDEX_BLOCK + 4 * hl;
+      const int64_t i0 = tile * kTS + k * PARIS_INDEX_SUB + 4 * gl;
       const int nvalid = active ? (int)std::max<int64_t>(0, imin64(4, a.n - i0)) : 0;
-      PARIS_DCHECK(k < kBPT && sa >= 0 && sa < nslots && sb < nslots);
+      PARIS_DCHECK(k < kSPT && sa >= 0 && sa < nslots && sb < nslots);
       lbi_emit(acc, sa, sb, i0, nvalid, nslots, s_c, a, wb, s_hist);
     }
     __syncwarp();
@@ -1837,6 +1913,17 @@ k_refine1(RefineArgs a, int nb) {
 // once per wave (8 bytes against 4*len bytes per refined row), and the pruning
 // test is the same as the sorted walk's, so the refined set differs only by the
 // order within a wave.
+// 6 CTAs (48 warps) per SM for len <= 256: 42 registers per thread, room for U rows
+// in flight per warp without spilling (U = 2 at len 256: 96 KB of rows in flight per SM)
+#ifndef PARIS_REFU_CTAS
+#define PARIS_REFU_CTAS 6
+#endif
+constexpr int kRefUCtas = PARIS_REFU_CTAS;
+#ifndef PARIS_REFU_U
+#define PARIS_REFU_U 2
+#endif
+constexpr int kRefUU = PARIS_REFU_U;  // rows in flight per warp at len <= 256
+
 __global__ void __launch_bounds__(kNB) k_wave_cut(const unsigned* __restrict__ hist, unsigned wave_a,
                                                   unsigned* __restrict__ cut) {
   __shared__ unsigned s[kNB];
@@ -1855,7 +1942,7 @@ __global__ void __launch_bounds__(kNB) k_wave_cut(const unsigned* __restrict__ h
 }
 
 template <int NC, int U>
-__global__ void __launch_bounds__(kRefThreads, NC <= 2 ? 8 : 2)
+__global__ void __launch_bounds__(kRefThreads, NC <= 2 ? kRefUCtas : 2)
 k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
   __shared__ unsigned s_refined[kMaxB], s_cnt[kMaxB], s_cut[kMaxB];
   __shared__ float s_scale[kMaxB];
@@ -2093,7 +2180,9 @@ struct Ws {
   unsigned* blocks;      // index mode: blocks whose envelope bound passed, per query
   unsigned* tile_count;  // index mode: live tiles listed
   unsigned* updates;     // nb mode: V_bsf updates per query
-  unsigned* bmask;       // index mode: [ntiles*16] per-block live query-slot masks
+  unsigned* submask;     // index mode: [ntiles*128] per-sub-block live query-slot masks
+  unsigned* items;       // index mode: live (block, slot pair) items of level 1
+  unsigned* item_count;
   unsigned* tile_list;   // index mode: live tiles
   unsigned* tile_flag;   // index mode: [ntiles] tile already listed (zeroed per batch)
   size_t flag_bytes;
@@ -2213,13 +2302,20 @@ cudaError_t launch_index_lb(const Plan& p, const uint8_t* sax, int nb, const Car
   la.g_q = ws.g_q; la.g_q16 = ws.g_q16; la.nb = nb; la.thr = ws.thr_seed; la.count = ws.count;
   la.hist = ws.hist; la.cand = ws.cand; la.cap = cap; la.perm = p.perm; la.env = p.env;
   la.blocks = ws.blocks;
+  la.env_sub = p.env + (size_t)((p.n + PARIS_INDEX_BLOCK - 1) / PARIS_INDEX_BLOCK) * 2 * kTW;
   const int64_t ntiles = (p.n + kTS - 1) / kTS;
   const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms() * 8, (ntiles + 7) / 8));
-  cudaError_t e = PARIS_LAUNCH("lb_blocks", k_blkmask<P>, bgrid, 256, 0, st, la, ws.bmask, ws.tile_list,
-                               ws.tile_count, ws.blocks);
+  cudaError_t e = PARIS_LAUNCH("lb_blocks", k_blkmask<P>, bgrid, 256, 0, st, la, ws.items, ws.item_count,
+                               ws.submask);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(ws.tile_flag, 0, ws.flag_bytes, st);
+  if (e != cudaSuccess) return e;
+  e = PARIS_LAUNCH("lb_subblocks", k_submask<P>, sms() * 8, 256, 0, st, la, ws.items, ws.item_count, ws.submask,
+                   ws.tile_list, ws.tile_count, ws.tile_flag);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(sms(), ntiles);
-  return PARIS_LAUNCH("lb_pass", k_lbi<P>, grid, kIThreads, kLbiSmem, st, la, ws.bmask, ws.tile_list, ws.tile_count);
+  return PARIS_LAUNCH("lb_pass", k_lbi<P>, grid, kIThreads, kLbiSmem, st, la, ws.submask, ws.tile_list,
+                      ws.tile_count);
 }
 
 cudaError_t dispatch_index_lb(int nb, const Plan& p, const uint8_t* sax, const CardTables* tab, const Ws& ws,
@@ -2306,7 +2402,7 @@ cudaError_t launch_refine1(const RefineArgs& ra, int nb, int64_t max_work, cudaS
 
 template <int NC, int U>
 cudaError_t launch_refine1u(const RefineArgs& ra, int nb, int wave, const unsigned* cut, cudaStream_t st) {
-  const int grid = sms() * (NC <= 2 ? 8 : 2);
+  const int grid = sms() * (NC <= 2 ? kRefUCtas : 2);
   return PARIS_LAUNCH("refine", (k_refine1u<NC, U>), grid, kRefThreads, 0, st, ra, nb, wave, cut);
 }
 
@@ -2319,7 +2415,7 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   const size_t o_q16 = take(sizeof(uint2) * (B / 2) * kMaxW);
   const size_t o_sid = take(sizeof(int) * B * p.S);
   const size_t o_skey = take(sizeof(uint64_t) * B * p.S);
-  const size_t zb = sizeof(unsigned) * (B + B + B * kNB + B * kNB + B + B + 1 + B);
+  const size_t zb = sizeof(unsigned) * (B + B + B * kNB + B * kNB + B + B + 1 + B + 1);
   const size_t o_zero = take(zb);
   const size_t o_best = take(sizeof(unsigned long long) * B * kPadU64);
   const size_t o_thr = take(sizeof(unsigned) * B * kPadU32);
@@ -2327,7 +2423,8 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   const size_t o_sorted = take(sizeof(uint64_t) * B * (size_t)cap);
   const size_t o_lists = take(p.k > 1 ? sizeof(uint64_t) * B * (size_t)p.XB * p.k : 8);
   const int64_t ntiles = (p.n + kTS - 1) / kTS;
-  const size_t o_bmask = take(p.perm ? sizeof(unsigned) * (size_t)ntiles * kBPT : 8);
+  const size_t o_smask = take(p.perm ? sizeof(unsigned) * (size_t)ntiles * kSPT : 8);
+  const size_t o_items = take(p.perm ? sizeof(unsigned) * (size_t)ntiles * kBPT * (B / 2) : 8);
   const size_t o_tlist = take(p.perm ? sizeof(unsigned) * (size_t)ntiles : 8);
   const size_t o_tflag = take(p.perm ? sizeof(unsigned) * (size_t)ntiles : 8);
   void* base = nullptr;
@@ -2354,11 +2451,13 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   ws.blocks = ws.refined + B;
   ws.tile_count = ws.blocks + B;
   ws.updates = ws.tile_count + 1;
+  ws.item_count = ws.updates + B;
   ws.best = (unsigned long long*)(c + o_best);
   ws.cand = (uint64_t*)(c + o_cand);
   ws.sorted = (uint64_t*)(c + o_sorted);
   ws.lists = (uint64_t*)(c + o_lists);
-  ws.bmask = (unsigned*)(c + o_bmask);
+  ws.submask = (unsigned*)(c + o_smask);
+  ws.items = (unsigned*)(c + o_items);
   ws.tile_list = (unsigned*)(c + o_tlist);
   ws.tile_flag = (unsigned*)(c + o_tflag);
   ws.flag_bytes = p.perm ? sizeof(unsigned) * (size_t)ntiles : 0;
@@ -2446,8 +2545,8 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
     // wave B -- the rest, in LB order -- prunes against a tight BSF)
     for (int wv = 0; wv < 2 && e1 == cudaSuccess && unsorted; ++wv) {
       switch (NC) {
-        case 1: e1 = launch_refine1u<1, 2>(ra, nb, wv, ws.cursor, st); break;
-        case 2: e1 = launch_refine1u<2, 1>(ra, nb, wv, ws.cursor, st); break;
+        case 1: e1 = launch_refine1u<1, kRefUU * 2>(ra, nb, wv, ws.cursor, st); break;
+        case 2: e1 = launch_refine1u<2, kRefUU>(ra, nb, wv, ws.cursor, st); break;
         case 4: e1 = launch_refine1u<4, 1>(ra, nb, wv, ws.cursor, st); break;
         case 8: e1 = launch_refine1u<8, 1>(ra, nb, wv, ws.cursor, st); break;
         default: e1 = launch_refine1u<32, 1>(ra, nb, wv, ws.cursor, st); break;
