@@ -121,6 +121,11 @@ __device__ __forceinline__ uint32_t h2_fma(uint32_t a, uint32_t b, uint32_t c) {
   asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
   return d;
 }
+__device__ __forceinline__ uint32_t h2_add(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("add.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
 
 // acc += delta^2 for one (series, segment) of a query pair, delta = max(a, b) where
 // a = relu(q_lo - U) and b = relu(L - q_hi).  At most one of a, b is non-zero (U >= L
@@ -819,7 +824,9 @@ constexpr int kIWarps = kIThreads / 32;
 constexpr int kSPT = 2048 / PARIS_INDEX_SUB;    // index sub-blocks per tile (128)
 constexpr int kSubPB = PARIS_INDEX_BLOCK / PARIS_INDEX_SUB;  // sub-blocks per block (4)
 constexpr int kUPR = 32 / (PARIS_INDEX_SUB / 4);  // units per warp round (8: 4 lanes x 4 series each)
-constexpr int kITileIds = 1024;  // tile ids staged per CTA (148 CTAs: 310 M series; beyond, global loads)
+constexpr int kBmThreads = 256;   // k_blkmask: 8 warps, a tile per warp step
+constexpr int kITileIds = 1024;
+constexpr int kIPf = 4;          // L2 prefetch distance (CTA iterations past the refilled tile)  // tile ids staged per CTA (148 CTAs: 310 M series; beyond, global loads)
 constexpr size_t kITabEnd = kIStages * kTileBytes + (size_t)kMaxCard * 32 * 8;
 constexpr size_t kLbiSmem = kITabEnd + (size_t)kMaxB * kNB * 4;
 
@@ -837,6 +844,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+// Pull a range toward L2 ahead of its TMA copy (no shared memory, no completion).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
@@ -1094,26 +1105,38 @@ __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int s
   __syncwarp();
 }
 
-// Level 1 (k_blkmask), one lane per 64-series block: lane l of a warp bounds block
-// 32*g + l against every query slot (region [L[min_s], U[max_s]] per segment, in
-// the packed fp16 pair form and error budget of the series bound); every (block,
-// slot pair) with a live slot becomes an item for level 2, and the block's four
-// sub-block masks are cleared.
+// Levels 1 and 2 (k_blkmask), a warp per tile.  Level 1, one lane per 64-series
+// block: lane l bounds block 32g + l against every query slot (region [L[min_s],
+// U[max_s]] per segment, in the packed fp16 pair form and error budget of the
+// series bound).  Level 2: every (block, slot pair) with a live slot is an item;
+// the warp takes 4 items per round, 8 lanes per item = 4 sub-blocks x 2 halves of
+// the segments (the two partial sums meet in one fp16 add, depth 9 <= w + 2 of the
+// budget), from the tile's sub-block envelopes staged in shared memory.  A live
+// (sub-block, slot) sets its bit in the sub-block's mask; the tile's 128 masks are
+// written once, and the tile is listed when any is non-zero.
 template <int P>
-__global__ void __launch_bounds__(256)
-k_blkmask(LbArgs a, unsigned* __restrict__ items, unsigned* __restrict__ item_count,
-          unsigned* __restrict__ submask) {
+__global__ void __launch_bounds__(kBmThreads)
+k_blkmask(LbArgs a, unsigned* __restrict__ submask, unsigned* __restrict__ tile_list,
+          unsigned* __restrict__ tile_count) {
+  constexpr int NW = kBmThreads / 32;
   __shared__ uint2 s_lu16[kMaxCard];
   __shared__ uint2 s_q16[kTW * P];
   __shared__ LbConsts s_c;
-  const int tid = threadIdx.x, lane = tid & 31;
+  __shared__ unsigned s_sub[kMaxB];
+  __shared__ __align__(16) uint8_t s_env[NW][kSPT][2 * kTW];  // per warp: the tile's sub-block envelopes
+  __shared__ __align__(16) unsigned s_msk[NW][kSPT];          // per warp: the tile's sub-block masks
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < kMaxCard; i += blockDim.x) s_lu16[i] = a.tab->lu16[i];
   for (int i = tid; i < kTW * P; i += blockDim.x) s_q16[i] = a.g_q16[i];
+  if (tid < kMaxB) s_sub[tid] = 0;
   lb_consts_init(a, 2 * P, &s_c);  // ends with __syncthreads
   const int64_t nblocks = (a.n + PARIS_INDEX_BLOCK - 1) / PARIS_INDEX_BLOCK;
+  const int64_t nsub = a.n / PARIS_INDEX_SUB;  // n % 16 == 0
   const int64_t ntiles = (a.n + kTS - 1) / kTS;
-  static_assert(kBPT == 32, "a warp step bounds the 32 blocks of one tile");
+  static_assert(kBPT == 32 && kSubPB == 4, "a warp step bounds the 32 blocks (128 sub-blocks) of one tile");
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + tid) >> 5, GW = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  uint8_t (*env)[2 * kTW] = s_env[warp];
+  unsigned* msk = s_msk[warp];
   for (int64_t g = gw; g < ntiles; g += GW) {
     const int64_t blk = 32 * g + lane;
     uint32_t bm = 0;
@@ -1139,9 +1162,20 @@ k_blkmask(LbArgs a, unsigned* __restrict__ items, unsigned* __restrict__ item_co
 #pragma unroll
       for (int p = 0; p < P; ++p) bm |= h2_le_bits(acc[p], s_c.T16[p]) << (2 * p);
     }
-    // the block's 4 sub-block masks start empty (padded to whole tiles)
-    reinterpret_cast<uint4*>(submask)[blk] = make_uint4(0u, 0u, 0u, 0u);
-    // items: (block << 6) | (pair << 2) | the pair's live slots
+    // stage the block's 4 sub-block envelopes (128 B) and clear their masks
+#pragma unroll
+    for (int j = 0; j < kSubPB; ++j) {
+      const int64_t sb = blk * kSubPB + j;
+      uint4 lo = make_uint4(0u, 0u, 0u, 0u), hi = lo;
+      if (bm && sb < nsub) {
+        lo = __ldg(reinterpret_cast<const uint4*>(a.env_sub + (size_t)sb * 32));
+        hi = __ldg(reinterpret_cast<const uint4*>(a.env_sub + (size_t)sb * 32 + 16));
+      }
+      *reinterpret_cast<uint4*>(env[kSubPB * lane + j]) = lo;
+      *reinterpret_cast<uint4*>(env[kSubPB * lane + j] + kTW) = hi;
+      msk[kSubPB * lane + j] = 0u;
+    }
+    // items: (block, pair) with a live slot; pm = the block's live pairs
     uint32_t pm = 0;
 #pragma unroll
     for (int p = 0; p < P; ++p) pm |= ((bm >> (2 * p)) & 3u) ? (1u << p) : 0u;
@@ -1152,62 +1186,45 @@ k_blkmask(LbArgs a, unsigned* __restrict__ items, unsigned* __restrict__ item_co
       const int v = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += v;
     }
-    unsigned base = 0;
-    if (lane == 31 && incl) base = atomicAdd(item_count, (unsigned)incl);
-    base = __shfl_sync(0xffffffffu, base, 31);
-    unsigned pos = base + (unsigned)(incl - cnt);
-    for (uint32_t r = pm; r; r &= r - 1) {
-      const int p = __ffs(r) - 1;
-      items[pos++] = ((uint32_t)blk << 6) | ((uint32_t)p << 2) | ((bm >> (2 * p)) & 3u);
-    }
-  }
-}
-
-// Level 2 (k_submask), one thread per (item, sub-block): the envelope bound of a
-// 16-series sub-block for the item's live slots; a live (sub-block, slot) sets its
-// bit in submask[sub-block] and the sub-block's tile joins the tile list (once).
-// A sub-block's symbol ranges lie inside its block's, so its bound is the tighter
-// of the two (the k_lbi work drops to the series of live sub-blocks).
-template <int P>
-__global__ void __launch_bounds__(256)
-k_submask(LbArgs a, const unsigned* __restrict__ items, const unsigned* __restrict__ item_count,
-          unsigned* __restrict__ submask, unsigned* __restrict__ tile_list, unsigned* __restrict__ tile_count,
-          unsigned* __restrict__ tile_flag) {
-  __shared__ uint2 s_lu16[kMaxCard];
-  __shared__ uint2 s_q16[kTW * P];
-  __shared__ LbConsts s_c;
-  __shared__ unsigned s_sub[kMaxB];
-  const int tid = threadIdx.x;
-  for (int i = tid; i < kMaxCard; i += blockDim.x) s_lu16[i] = a.tab->lu16[i];
-  for (int i = tid; i < kTW * P; i += blockDim.x) s_q16[i] = a.g_q16[i];
-  if (tid < kMaxB) s_sub[tid] = 0;
-  lb_consts_init(a, 2 * P, &s_c);  // ends with __syncthreads
-  const int64_t ntest = (int64_t)*item_count * kSubPB;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + tid; t < ntest; t += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t it = items[t / kSubPB];
-    const int64_t sb = (int64_t)(it >> 6) * kSubPB + (t % kSubPB);
-    const int p = (it >> 2) & 15;
-    const uint32_t live2 = it & 3u;
-    if (sb * PARIS_INDEX_SUB >= a.n) continue;
-    const uint4 mn = __ldg(reinterpret_cast<const uint4*>(a.env_sub + (size_t)sb * 32));
-    const uint4 mx = __ldg(reinterpret_cast<const uint4*>(a.env_sub + (size_t)sb * 32 + 16));
-    const uint32_t mnw[4] = {mn.x, mn.y, mn.z, mn.w}, mxw[4] = {mx.x, mx.y, mx.z, mx.w};
-    uint32_t acc = 0u;
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    __syncwarp();
+    const int gi = lane >> 3, g4 = (lane >> 1) & 3, h = lane & 1;
+    for (int t0 = 0; t0 < total; t0 += 4) {
+      const int t = t0 + gi;
+      const unsigned m0 = __ballot_sync(0xffffffffu, incl <= t0), m1 = __ballot_sync(0xffffffffu, incl <= t0 + 1);
+      const unsigned m2 = __ballot_sync(0xffffffffu, incl <= t0 + 2), m3 = __ballot_sync(0xffffffffu, incl <= t0 + 3);
+      const bool active = t < total;
+      const int b = __popc(gi == 0 ? m0 : gi == 1 ? m1 : gi == 2 ? m2 : m3) & 31;
+      const int excl = __shfl_sync(0xffffffffu, incl - cnt, b);
+      const uint32_t pmb = __shfl_sync(0xffffffffu, pm, b), bmb = __shfl_sync(0xffffffffu, bm, b);
+      const int pf = active ? __fns(pmb, 0, t - excl + 1) : 0;
+      const int p = (pf >= 0 && pf < P) ? pf : 0;
+      const uint32_t live2 = active ? (bmb >> (2 * p)) & 3u : 0u;
+      const int sbl = kSubPB * b + g4;
+      const uint2 mnv = *reinterpret_cast<const uint2*>(env[sbl] + 8 * h);
+      const uint2 mxv = *reinterpret_cast<const uint2*>(env[sbl] + kTW + 8 * h);
+      uint32_t acc = 0u;
 #pragma unroll
-    for (int seg = 0; seg < kTW; ++seg) {
-      const uint32_t tx = s_lu16[(mxw[seg >> 2] >> (8 * (seg & 3))) & 0xFFu].x;
-      const uint32_t ty = s_lu16[(mnw[seg >> 2] >> (8 * (seg & 3))) & 0xFFu].y;
-      const uint2 q = s_q16[seg * P + p];
-      acc = h2_acc_delta2(acc, h2_fma_relu(q.x, kHalf2One, tx), h2_fma_relu(q.y, kHalf2One, ty));
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t mnj = ((j < 4 ? mnv.x : mnv.y) >> (8 * (j & 3))) & 0xFFu;
+        const uint32_t mxj = ((j < 4 ? mxv.x : mxv.y) >> (8 * (j & 3))) & 0xFFu;
+        const uint2 q = s_q16[(8 * h + j) * P + p];
+        acc = h2_acc_delta2(acc, h2_fma_relu(q.x, kHalf2One, s_lu16[mxj].x), h2_fma_relu(q.y, kHalf2One, s_lu16[mnj].y));
+      }
+      acc = h2_add(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
+      const uint32_t bits = h2_le_bits(acc, s_c.T16[p]) & live2;
+      if (h == 0 && bits) {
+        atomicOr(&msk[sbl], bits << (2 * p));
+        if (bits & 1u) atomicAdd(&s_sub[2 * p], 1u);
+        if (bits & 2u) atomicAdd(&s_sub[2 * p + 1], 1u);
+      }
     }
-    const uint32_t bits = h2_le_bits(acc, s_c.T16[p]) & live2;
-    if (!bits) continue;
-    atomicOr(&submask[sb], bits << (2 * p));
-    if (bits & 1u) atomicAdd(&s_sub[2 * p], 1u);
-    if (bits & 2u) atomicAdd(&s_sub[2 * p + 1], 1u);
-    const int64_t tile = sb / kSPT;
-    if (ld_relaxed_u32(tile_flag + tile) == 0u && atomicExch(&tile_flag[tile], 1u) == 0u)
-      tile_list[atomicAdd(tile_count, 1u)] = (unsigned)tile;
+    __syncwarp();
+    const uint4 mv = reinterpret_cast<const uint4*>(msk)[lane];
+    reinterpret_cast<uint4*>(submask)[(size_t)g * (kSPT / 4) + lane] = mv;  // padded to whole tiles
+    if (__ballot_sync(0xffffffffu, (mv.x | mv.y | mv.z | mv.w) != 0u) && lane == 0)
+      tile_list[atomicAdd(tile_count, 1u)] = (unsigned)g;
+    __syncwarp();
   }
   __syncthreads();
   if (tid < 2 * P && s_sub[tid]) atomicAdd(&a.blocks[tid], s_sub[tid]);
@@ -1262,6 +1279,13 @@ k_lbi(LbArgs a, const unsigned* __restrict__ submask, const unsigned* __restrict
     bulk_g2s(s_tiles + (size_t)st * kTileBytes, a.sax + (size_t)tile * kTileBytes, (unsigned)kTileBytes,
              &s_full[st]);
     bulk_g2s(&s_sm[st][0], submask + (size_t)tile * kSPT, (unsigned)(kSPT * 4), &s_full[st]);
+    // the ring holds 2 tiles; the tile kIPf refills later is pulled into L2 now, so
+    // its copy is served at L2 latency
+    const int64_t pf = li + (int64_t)kIPf * gridDim.x, ip = i + kIPf;
+    if (pf < nlist) {
+      const int64_t tp = ip < kITileIds ? s_tl[ip] : tile_list[pf];
+      bulk_prefetch_l2(a.sax + (size_t)tp * kTileBytes, (unsigned)kTileBytes);
+    }
   };
   if (tid == 0) {
     for (int st = 0; st < kIStages; ++st) {
@@ -1280,6 +1304,10 @@ k_lbi(LbArgs a, const unsigned* __restrict__ submask, const unsigned* __restrict
     for (int st = 0; st < kIStages; ++st) {
       const int64_t li = blockIdx.x + (int64_t)st * gridDim.x;
       if (li < nlist) issue(li, st);
+    }
+    for (int i = kIStages; i < kIPf; ++i) {  // the tiles between the ring and the first prefetch
+      const int64_t li = blockIdx.x + (int64_t)i * gridDim.x;
+      if (li < nlist) bulk_prefetch_l2(a.sax + (size_t)s_tl[i] * kTileBytes, (unsigned)kTileBytes);
     }
   }
   for (int i = tid; i < kMaxCard * 32; i += kIThreads) s_tab[i] = a.tab->lu16[i >> 5];
@@ -2181,11 +2209,7 @@ struct Ws {
   unsigned* tile_count;  // index mode: live tiles listed
   unsigned* updates;     // nb mode: V_bsf updates per query
   unsigned* submask;     // index mode: [ntiles*128] per-sub-block live query-slot masks
-  unsigned* items;       // index mode: live (block, slot pair) items of level 1
-  unsigned* item_count;
   unsigned* tile_list;   // index mode: live tiles
-  unsigned* tile_flag;   // index mode: [ntiles] tile already listed (zeroed per batch)
-  size_t flag_bytes;
   size_t zero_bytes;
   unsigned long long* best;
   uint64_t* cand;
@@ -2305,13 +2329,8 @@ cudaError_t launch_index_lb(const Plan& p, const uint8_t* sax, int nb, const Car
   la.env_sub = p.env + (size_t)((p.n + PARIS_INDEX_BLOCK - 1) / PARIS_INDEX_BLOCK) * 2 * kTW;
   const int64_t ntiles = (p.n + kTS - 1) / kTS;
   const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms() * 8, (ntiles + 7) / 8));
-  cudaError_t e = PARIS_LAUNCH("lb_blocks", k_blkmask<P>, bgrid, 256, 0, st, la, ws.items, ws.item_count,
-                               ws.submask);
-  if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(ws.tile_flag, 0, ws.flag_bytes, st);
-  if (e != cudaSuccess) return e;
-  e = PARIS_LAUNCH("lb_subblocks", k_submask<P>, sms() * 8, 256, 0, st, la, ws.items, ws.item_count, ws.submask,
-                   ws.tile_list, ws.tile_count, ws.tile_flag);
+  cudaError_t e = PARIS_LAUNCH("lb_blocks", k_blkmask<P>, bgrid, kBmThreads, 0, st, la, ws.submask, ws.tile_list,
+                               ws.tile_count);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(sms(), ntiles);
   return PARIS_LAUNCH("lb_pass", k_lbi<P>, grid, kIThreads, kLbiSmem, st, la, ws.submask, ws.tile_list,
@@ -2415,7 +2434,7 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   const size_t o_q16 = take(sizeof(uint2) * (B / 2) * kMaxW);
   const size_t o_sid = take(sizeof(int) * B * p.S);
   const size_t o_skey = take(sizeof(uint64_t) * B * p.S);
-  const size_t zb = sizeof(unsigned) * (B + B + B * kNB + B * kNB + B + B + 1 + B + 1);
+  const size_t zb = sizeof(unsigned) * (B + B + B * kNB + B * kNB + B + B + 1 + B);
   const size_t o_zero = take(zb);
   const size_t o_best = take(sizeof(unsigned long long) * B * kPadU64);
   const size_t o_thr = take(sizeof(unsigned) * B * kPadU32);
@@ -2424,9 +2443,7 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   const size_t o_lists = take(p.k > 1 ? sizeof(uint64_t) * B * (size_t)p.XB * p.k : 8);
   const int64_t ntiles = (p.n + kTS - 1) / kTS;
   const size_t o_smask = take(p.perm ? sizeof(unsigned) * (size_t)ntiles * kSPT : 8);
-  const size_t o_items = take(p.perm ? sizeof(unsigned) * (size_t)ntiles * kBPT * (B / 2) : 8);
   const size_t o_tlist = take(p.perm ? sizeof(unsigned) * (size_t)ntiles : 8);
-  const size_t o_tflag = take(p.perm ? sizeof(unsigned) * (size_t)ntiles : 8);
   void* base = nullptr;
   cudaError_t e = cudaMallocAsync(&base, off, st);
   if (e != cudaSuccess) {
@@ -2451,16 +2468,12 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   ws.blocks = ws.refined + B;
   ws.tile_count = ws.blocks + B;
   ws.updates = ws.tile_count + 1;
-  ws.item_count = ws.updates + B;
   ws.best = (unsigned long long*)(c + o_best);
   ws.cand = (uint64_t*)(c + o_cand);
   ws.sorted = (uint64_t*)(c + o_sorted);
   ws.lists = (uint64_t*)(c + o_lists);
   ws.submask = (unsigned*)(c + o_smask);
-  ws.items = (unsigned*)(c + o_items);
   ws.tile_list = (unsigned*)(c + o_tlist);
-  ws.tile_flag = (unsigned*)(c + o_tflag);
-  ws.flag_bytes = p.perm ? sizeof(unsigned) * (size_t)ntiles : 0;
   return PARIS_OK;
 }
 
