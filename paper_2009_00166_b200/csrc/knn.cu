@@ -818,7 +818,7 @@ constexpr int kTW = 16;
 constexpr size_t kTileBytes = (size_t)kTW * kTS;
 constexpr size_t kTSmem = kStages * kTileBytes + kMaxCard * 32 * 4;
 // k_lbi: 2-stage ring + the 32-copy pair-form table (64 KB) + the LB histograms
-constexpr int kIStages = 2;      // compute-bound on the live items: a tile's load (~0.8 us) < its work
+constexpr int kIStages = 2;      // + an L2 prefetch kIPf tiles ahead (the ring alone starved at 2 stages)
 constexpr int kIThreads = 768;   // 24 warps: more warps to hide the lookup -> math latency chain
 constexpr int kIWarps = kIThreads / 32;
 constexpr int kSPT = 2048 / PARIS_INDEX_SUB;    // index sub-blocks per tile (128)
@@ -1041,9 +1041,9 @@ k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
 // ---------------------------------------------------------------- index mode LB (f1)
 // Three levels, each a valid lower bound on its members' MINDIST (the iSAX node
 // bound of the sorted array's blocks):
-//   k_blkmask  64-series blocks x every query slot -> (block, slot pair) items;
-//   k_submask  the items' 16-series sub-blocks -> per sub-block live-slot masks,
-//              and the list of tiles holding a live sub-block;
+//   k_blkmask  64-series blocks x every query slot -> (block, slot pair) items,
+//              then the items' 16-series sub-blocks -> per sub-block live-slot
+//              masks, and the list of tiles holding a live sub-block;
 //   k_lbi      the series of live sub-blocks, for their live slots only.
 // Candidate emission of one index unit: 4 series x 2 query slots// Candidate emission of one index item: 4 series x 2 query slots (sa = low half,
 // sb = high half, sb < 0: none).  Same tests and warp buffer as lb_emit_wb.
