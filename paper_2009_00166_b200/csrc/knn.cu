@@ -825,6 +825,7 @@ constexpr int kSPT = 2048 / PARIS_INDEX_SUB;    // index sub-blocks per tile (12
 constexpr int kSubPB = PARIS_INDEX_BLOCK / PARIS_INDEX_SUB;  // sub-blocks per block (4)
 constexpr int kUPR = 32 / (PARIS_INDEX_SUB / 4);  // units per warp round (8: 4 lanes x 4 series each)
 constexpr int kBmThreads = 256;   // k_blkmask: 8 warps, a tile per warp step
+constexpr size_t kBmSmem = (size_t)kMaxCard * 32 * 4;  // k_blkmask: the 32-copy region table
 constexpr int kITileIds = 1024;
 constexpr int kIPf = 4;          // L2 prefetch distance (CTA iterations past the refilled tile)  // tile ids staged per CTA (148 CTAs: 310 M series; beyond, global loads)
 constexpr size_t kITabEnd = kIStages * kTileBytes + (size_t)kMaxCard * 32 * 8;
@@ -1119,14 +1120,18 @@ __global__ void __launch_bounds__(kBmThreads)
 k_blkmask(LbArgs a, unsigned* __restrict__ submask, unsigned* __restrict__ tile_list,
           unsigned* __restrict__ tile_count) {
   constexpr int NW = kBmThreads / 32;
-  __shared__ uint2 s_lu16[kMaxCard];
+  // single-form table half2(-U16, L16), 32 copies (entry c of lane l at word 32c + l):
+  // lanes look up unrelated symbols, so one copy per lane keeps every lookup a
+  // single conflict-free wavefront
+  extern __shared__ uint32_t s_tab[];  // [kMaxCard * 32] (dynamic: kBmSmem)
   __shared__ uint2 s_q16[kTW * P];
   __shared__ LbConsts s_c;
   __shared__ unsigned s_sub[kMaxB];
   __shared__ __align__(16) uint8_t s_env[NW][kSPT][2 * kTW];  // per warp: the tile's sub-block envelopes
   __shared__ __align__(16) unsigned s_msk[NW][kSPT];          // per warp: the tile's sub-block masks
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < kMaxCard; i += blockDim.x) s_lu16[i] = a.tab->lu16[i];
+  for (int i = tid; i < kMaxCard * 32; i += blockDim.x) s_tab[i] = a.tab->lu16p[i >> 5];
+  const uint32_t* tabl = s_tab + lane;
   for (int i = tid; i < kTW * P; i += blockDim.x) s_q16[i] = a.g_q16[i];
   if (tid < kMaxB) s_sub[tid] = 0;
   lb_consts_init(a, 2 * P, &s_c);  // ends with __syncthreads
@@ -1149,8 +1154,8 @@ k_blkmask(LbArgs a, unsigned* __restrict__ submask, unsigned* __restrict__ tile_
       for (int p = 0; p < P; ++p) acc[p] = 0u;
 #pragma unroll 4
       for (int seg = 0; seg < kTW; ++seg) {
-        const uint32_t tx = s_lu16[(mxw[seg >> 2] >> (8 * (seg & 3))) & 0xFFu].x;  // -U16 of the max symbol
-        const uint32_t ty = s_lu16[(mnw[seg >> 2] >> (8 * (seg & 3))) & 0xFFu].y;  // L16 of the min symbol
+        const uint32_t tx = __byte_perm(tabl[32 * ((mxw[seg >> 2] >> (8 * (seg & 3))) & 0xFFu)], 0, 0x1010);  // -U16 of the max
+        const uint32_t ty = __byte_perm(tabl[32 * ((mnw[seg >> 2] >> (8 * (seg & 3))) & 0xFFu)], 0, 0x3232);  // L16 of the min
 #pragma unroll
         for (int p = 0; p < P; ++p) {
           const uint2 q = s_q16[seg * P + p];
@@ -1209,7 +1214,8 @@ k_blkmask(LbArgs a, unsigned* __restrict__ submask, unsigned* __restrict__ tile_
         const uint32_t mnj = ((j < 4 ? mnv.x : mnv.y) >> (8 * (j & 3))) & 0xFFu;
         const uint32_t mxj = ((j < 4 ? mxv.x : mxv.y) >> (8 * (j & 3))) & 0xFFu;
         const uint2 q = s_q16[(8 * h + j) * P + p];
-        acc = h2_acc_delta2(acc, h2_fma_relu(q.x, kHalf2One, s_lu16[mxj].x), h2_fma_relu(q.y, kHalf2One, s_lu16[mnj].y));
+        const uint32_t tx = __byte_perm(tabl[32 * mxj], 0, 0x1010), ty = __byte_perm(tabl[32 * mnj], 0, 0x3232);
+        acc = h2_acc_delta2(acc, h2_fma_relu(q.x, kHalf2One, tx), h2_fma_relu(q.y, kHalf2One, ty));
       }
       acc = h2_add(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
       const uint32_t bits = h2_le_bits(acc, s_c.T16[p]) & live2;
@@ -1365,9 +1371,9 @@ k_lbi(LbArgs a, const unsigned* __restrict__ submask, const unsigned* __restrict
       const int excl = k ? (int)uinc[k - 1] : 0;
       const uint32_t smk = s_sm[st][k];
       const int r = t - excl;
-      const int saf = active ? __fns(smk, 0, 2 * r + 1) : 0;
+      const int saf = active ? (int)__fns(smk, 0, 2 * r + 1) : 0;
       const int sa = (saf >= 0 && saf < 32) ? saf : 0;
-      const int sbf = active ? __fns(smk, 0, 2 * r + 2) : -1;
+      const int sbf = active ? (int)__fns(smk, 0, 2 * r + 2) : -1;
       const int sb = (sbf >= 0 && sbf < 32) ? sbf : -1;
       const int sq = sb >= 0 ? sb : sa;  // odd count: duplicate lane, masked in emission
       uint32_t acc[4] = {0u, 0u, 0u, 0u};
@@ -2319,6 +2325,8 @@ cudaError_t launch_index_lb(const Plan& p, const uint8_t* sax, int nb, const Car
   if (attr_dev != dev) {
     cudaError_t e = cudaFuncSetAttribute(k_lbi<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLbiSmem);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_blkmask<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBmSmem);
+    if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
   LbArgs la;
@@ -2329,7 +2337,7 @@ cudaError_t launch_index_lb(const Plan& p, const uint8_t* sax, int nb, const Car
   la.env_sub = p.env + (size_t)((p.n + PARIS_INDEX_BLOCK - 1) / PARIS_INDEX_BLOCK) * 2 * kTW;
   const int64_t ntiles = (p.n + kTS - 1) / kTS;
   const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms() * 8, (ntiles + 7) / 8));
-  cudaError_t e = PARIS_LAUNCH("lb_blocks", k_blkmask<P>, bgrid, kBmThreads, 0, st, la, ws.submask, ws.tile_list,
+  cudaError_t e = PARIS_LAUNCH("lb_blocks", k_blkmask<P>, bgrid, kBmThreads, kBmSmem, st, la, ws.submask, ws.tile_list,
                                ws.tile_count);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(sms(), ntiles);
