@@ -1347,7 +1347,11 @@ k_lbi(LbArgs a, const unsigned* __restrict__ submask, const unsigned* __restrict
       const int v = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += v;
     }
+#if PARIS_EXP_NOUNITS  // timing experiment only: stream + enumerate, no unit work (results invalid)
+    const int total = 0 * __shfl_sync(0xffffffffu, incl, 31);
+#else
     const int total = __shfl_sync(0xffffffffu, incl, 31);
+#endif
     {
       const int e = incl - own;
       uinc[4 * lane] = (uint16_t)(e + c0);
