@@ -121,11 +121,6 @@ __device__ __forceinline__ uint32_t h2_fma(uint32_t a, uint32_t b, uint32_t c) {
   asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
   return d;
 }
-__device__ __forceinline__ uint32_t h2_add(uint32_t a, uint32_t b) {
-  uint32_t d;
-  asm("add.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
-  return d;
-}
 
 // acc += delta^2 for one (series, segment) of a query pair, delta = max(a, b) where
 // a = relu(q_lo - U) and b = relu(L - q_hi).  At most one of a, b is non-zero (U >= L
@@ -545,9 +540,8 @@ struct LbArgs {
   uint64_t* cand;
   int64_t cap;
   const uint32_t* perm;  // index mode: sorted position -> series id (else nullptr)
-  const uint8_t* env;    // index mode: [ceil(n/64) blocks][2][16] min/max symbols (else nullptr)
-  const uint8_t* env_sub = nullptr;  // index mode: [n/16 sub-blocks][2][16] min/max symbols
-  unsigned* blocks;      // index mode: per query, sub-blocks whose envelope bound passed
+  const uint8_t* env;    // index mode: [n/128 blocks][2][16] min/max symbols (else nullptr)
+  unsigned* blocks;      // index mode: per query, blocks whose envelope bound passed
 };
 
 struct LbConsts {
@@ -818,16 +812,10 @@ constexpr int kTW = 16;
 constexpr size_t kTileBytes = (size_t)kTW * kTS;
 constexpr size_t kTSmem = kStages * kTileBytes + kMaxCard * 32 * 4;
 // k_lbi: 2-stage ring + the 32-copy pair-form table (64 KB) + the LB histograms
-constexpr int kIStages = 2;      // + an L2 prefetch kIPf tiles ahead (the ring alone starved at 2 stages)
+constexpr int kIStages = 2;      // compute-bound on the live items: a tile's load (~0.8 us) < its work
 constexpr int kIThreads = 768;   // 24 warps: more warps to hide the lookup -> math latency chain
 constexpr int kIWarps = kIThreads / 32;
-constexpr int kSPT = 2048 / PARIS_INDEX_SUB;    // index sub-blocks per tile (128)
-constexpr int kSubPB = PARIS_INDEX_BLOCK / PARIS_INDEX_SUB;  // sub-blocks per block (4)
-constexpr int kUPR = 32 / (PARIS_INDEX_SUB / 4);  // units per warp round (8: 4 lanes x 4 series each)
-constexpr int kBmThreads = 256;   // k_blkmask: 8 warps, a tile per warp step
-constexpr size_t kBmSmem = (size_t)kMaxCard * 32 * 4;  // k_blkmask: the 32-copy region table
-constexpr int kITileIds = 1024;
-constexpr int kIPf = 4;          // L2 prefetch distance (CTA iterations past the refilled tile)  // tile ids staged per CTA (148 CTAs: 310 M series; beyond, global loads)
+constexpr int kITileIds = 1024;  // tile ids staged per CTA (148 CTAs: 310 M series; beyond, global loads)
 constexpr size_t kITabEnd = kIStages * kTileBytes + (size_t)kMaxCard * 32 * 8;
 constexpr size_t kLbiSmem = kITabEnd + (size_t)kMaxB * kNB * 4;
 
@@ -845,10 +833,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
-}
-// Pull a range toward L2 ahead of its TMA copy (no shared memory, no completion).
-__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
@@ -1040,13 +1024,15 @@ k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
 }
 
 // ---------------------------------------------------------------- index mode LB (f1)
-// Three levels, each a valid lower bound on its members' MINDIST (the iSAX node
-// bound of the sorted array's blocks):
-//   k_blkmask  64-series blocks x every query slot -> (block, slot pair) items,
-//              then the items' 16-series sub-blocks -> per sub-block live-slot
-//              masks, and the list of tiles holding a live sub-block;
-//   k_lbi      the series of live sub-blocks, for their live slots only.
-// Candidate emission of one index unit: 4 series x 2 query slots// Candidate emission of one index item: 4 series x 2 query slots (sa = low half,
+// Pass 1 (k_blkmask): the envelope MINDIST of every 128-series block for every
+// query slot (the iSAX node bound): bit b of bmask[blk] = block may hold a
+// candidate of slot b.  A CTA covers the 16 blocks of one SAX tile and appends
+// the tile to a work list when any of its blocks is live.
+// Pass 2 (k_lbi): the TMA ring streams only listed tiles; the live (block, query
+// pair) items of a tile are dealt round-robin to its 16 warps (every warp derives
+// the same item list from the 16 block masks, no CTA barrier), so warps stay
+// balanced however the live blocks are spread.
+// Candidate emission of one index item: 4 series x 2 query slots (sa = low half,
 // sb = high half, sb < 0: none).  Same tests and warp buffer as lb_emit_wb.
 __device__ __forceinline__ uint32_t half_of(uint32_t v, int h) { return (v >> (16 * h)) & 0xFFFFu; }
 
@@ -1106,42 +1092,30 @@ __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int s
   __syncwarp();
 }
 
-// Levels 1 and 2 (k_blkmask), a warp per tile.  Level 1, one lane per 64-series
-// block: lane l bounds block 32g + l against every query slot (region [L[min_s],
-// U[max_s]] per segment, in the packed fp16 pair form and error budget of the
-// series bound).  Level 2: every (block, slot pair) with a live slot is an item;
-// the warp takes 4 items per round, 8 lanes per item = 4 sub-blocks x 2 halves of
-// the segments (the two partial sums meet in one fp16 add, depth 9 <= w + 2 of the
-// budget), from the tile's sub-block envelopes staged in shared memory.  A live
-// (sub-block, slot) sets its bit in the sub-block's mask; the tile's 128 masks are
-// written once, and the tile is listed when any is non-zero.
+// One lane per block: lane l of a warp bounds block 32*g + l against every query
+// slot (region [L[min_s], U[max_s]] per segment, outward fp32, round-down sums);
+// the 32 blocks of a warp step are one whole tile, so the warp lists it itself.
 template <int P>
-__global__ void __launch_bounds__(kBmThreads)
-k_blkmask(LbArgs a, unsigned* __restrict__ submask, unsigned* __restrict__ tile_list,
-          unsigned* __restrict__ tile_count) {
-  constexpr int NW = kBmThreads / 32;
-  // single-form table half2(-U16, L16), 32 copies (entry c of lane l at word 32c + l):
-  // lanes look up unrelated symbols, so one copy per lane keeps every lookup a
-  // single conflict-free wavefront
-  extern __shared__ uint32_t s_tab[];  // [kMaxCard * 32] (dynamic: kBmSmem)
+__global__ void __launch_bounds__(256)
+k_blkmask(LbArgs a, unsigned* __restrict__ bmask, unsigned* __restrict__ tile_list,
+          unsigned* __restrict__ tile_count, unsigned* __restrict__ blocks) {
+  // the envelope bound in the same packed fp16 pair form (and error budget, k_lb)
+  // as the series bound: per segment the region [L16[min], U16[max]], two query
+  // slots per instruction; a block is live for slot b iff its fp16 bound <= T16[b]
+  constexpr int NS = 2 * P;
+  __shared__ uint2 s_lu16[kMaxCard];
   __shared__ uint2 s_q16[kTW * P];
   __shared__ LbConsts s_c;
-  __shared__ unsigned s_sub[kMaxB];
-  __shared__ __align__(16) uint8_t s_env[NW][kSPT][2 * kTW];  // per warp: the tile's sub-block envelopes
-  __shared__ __align__(16) unsigned s_msk[NW][kSPT];          // per warp: the tile's sub-block masks
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < kMaxCard * 32; i += blockDim.x) s_tab[i] = a.tab->lu16p[i >> 5];
-  const uint32_t* tabl = s_tab + lane;
+  __shared__ unsigned s_blk[kMaxB];
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int i = tid; i < kMaxCard; i += blockDim.x) s_lu16[i] = a.tab->lu16[i];
   for (int i = tid; i < kTW * P; i += blockDim.x) s_q16[i] = a.g_q16[i];
-  if (tid < kMaxB) s_sub[tid] = 0;
-  lb_consts_init(a, 2 * P, &s_c);  // ends with __syncthreads
+  if (tid < kMaxB) s_blk[tid] = 0;
+  lb_consts_init(a, NS, &s_c);  // ends with __syncthreads
   const int64_t nblocks = (a.n + PARIS_INDEX_BLOCK - 1) / PARIS_INDEX_BLOCK;
-  const int64_t nsub = a.n / PARIS_INDEX_SUB;  // n % 16 == 0
   const int64_t ntiles = (a.n + kTS - 1) / kTS;
-  static_assert(kBPT == 32 && kSubPB == 4, "a warp step bounds the 32 blocks (128 sub-blocks) of one tile");
+  static_assert(kBPT == 32, "a warp step bounds the 32 blocks of one tile");
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + tid) >> 5, GW = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  uint8_t (*env)[2 * kTW] = s_env[warp];
-  unsigned* msk = s_msk[warp];
   for (int64_t g = gw; g < ntiles; g += GW) {
     const int64_t blk = 32 * g + lane;
     uint32_t bm = 0;
@@ -1154,8 +1128,8 @@ k_blkmask(LbArgs a, unsigned* __restrict__ submask, unsigned* __restrict__ tile_
       for (int p = 0; p < P; ++p) acc[p] = 0u;
 #pragma unroll 4
       for (int seg = 0; seg < kTW; ++seg) {
-        const uint32_t tx = __byte_perm(tabl[32 * ((mxw[seg >> 2] >> (8 * (seg & 3))) & 0xFFu)], 0, 0x1010);  // -U16 of the max
-        const uint32_t ty = __byte_perm(tabl[32 * ((mnw[seg >> 2] >> (8 * (seg & 3))) & 0xFFu)], 0, 0x3232);  // L16 of the min
+        const uint32_t tx = s_lu16[(mxw[seg >> 2] >> (8 * (seg & 3))) & 0xFFu].x;  // -U16 of the max symbol
+        const uint32_t ty = s_lu16[(mnw[seg >> 2] >> (8 * (seg & 3))) & 0xFFu].y;  // L16 of the min symbol
 #pragma unroll
         for (int p = 0; p < P; ++p) {
           const uint2 q = s_q16[seg * P + p];
@@ -1167,83 +1141,22 @@ k_blkmask(LbArgs a, unsigned* __restrict__ submask, unsigned* __restrict__ tile_
 #pragma unroll
       for (int p = 0; p < P; ++p) bm |= h2_le_bits(acc[p], s_c.T16[p]) << (2 * p);
     }
-    // stage the block's 4 sub-block envelopes (128 B) and clear their masks
+    bmask[blk] = bm;  // padded to whole tiles
+    const unsigned live = __ballot_sync(0xffffffffu, bm != 0u);
+    if (lane == 0 && live) tile_list[atomicAdd(tile_count, 1u)] = (unsigned)g;
 #pragma unroll
-    for (int j = 0; j < kSubPB; ++j) {
-      const int64_t sb = blk * kSubPB + j;
-      uint4 lo = make_uint4(0u, 0u, 0u, 0u), hi = lo;
-      if (bm && sb < nsub) {
-        lo = __ldg(reinterpret_cast<const uint4*>(a.env_sub + (size_t)sb * 32));
-        hi = __ldg(reinterpret_cast<const uint4*>(a.env_sub + (size_t)sb * 32 + 16));
-      }
-      *reinterpret_cast<uint4*>(env[kSubPB * lane + j]) = lo;
-      *reinterpret_cast<uint4*>(env[kSubPB * lane + j] + kTW) = hi;
-      msk[kSubPB * lane + j] = 0u;
+    for (int b = 0; b < NS; ++b) {
+      const unsigned m = __ballot_sync(0xffffffffu, (bm >> b) & 1u);
+      if (lane == 0 && m) atomicAdd(&s_blk[b], (unsigned)__popc(m));
     }
-    // items: (block, pair) with a live slot; pm = the block's live pairs
-    uint32_t pm = 0;
-#pragma unroll
-    for (int p = 0; p < P; ++p) pm |= ((bm >> (2 * p)) & 3u) ? (1u << p) : 0u;
-    const int cnt = __popc(pm);
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    __syncwarp();
-    const int gi = lane >> 3, g4 = (lane >> 1) & 3, h = lane & 1;
-    for (int t0 = 0; t0 < total; t0 += 4) {
-      const int t = t0 + gi;
-      const unsigned m0 = __ballot_sync(0xffffffffu, incl <= t0), m1 = __ballot_sync(0xffffffffu, incl <= t0 + 1);
-      const unsigned m2 = __ballot_sync(0xffffffffu, incl <= t0 + 2), m3 = __ballot_sync(0xffffffffu, incl <= t0 + 3);
-      const bool active = t < total;
-      const int b = __popc(gi == 0 ? m0 : gi == 1 ? m1 : gi == 2 ? m2 : m3) & 31;
-      const int excl = __shfl_sync(0xffffffffu, incl - cnt, b);
-      const uint32_t pmb = __shfl_sync(0xffffffffu, pm, b), bmb = __shfl_sync(0xffffffffu, bm, b);
-      const int pf = active ? __fns(pmb, 0, t - excl + 1) : 0;
-      const int p = (pf >= 0 && pf < P) ? pf : 0;
-      const uint32_t live2 = active ? (bmb >> (2 * p)) & 3u : 0u;
-      const int sbl = kSubPB * b + g4;
-      const uint2 mnv = *reinterpret_cast<const uint2*>(env[sbl] + 8 * h);
-      const uint2 mxv = *reinterpret_cast<const uint2*>(env[sbl] + kTW + 8 * h);
-      uint32_t acc = 0u;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint32_t mnj = ((j < 4 ? mnv.x : mnv.y) >> (8 * (j & 3))) & 0xFFu;
-        const uint32_t mxj = ((j < 4 ? mxv.x : mxv.y) >> (8 * (j & 3))) & 0xFFu;
-        const uint2 q = s_q16[(8 * h + j) * P + p];
-        const uint32_t tx = __byte_perm(tabl[32 * mxj], 0, 0x1010), ty = __byte_perm(tabl[32 * mnj], 0, 0x3232);
-        acc = h2_acc_delta2(acc, h2_fma_relu(q.x, kHalf2One, tx), h2_fma_relu(q.y, kHalf2One, ty));
-      }
-      acc = h2_add(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
-      const uint32_t bits = h2_le_bits(acc, s_c.T16[p]) & live2;
-      if (h == 0 && bits) {
-        atomicOr(&msk[sbl], bits << (2 * p));
-        if (bits & 1u) atomicAdd(&s_sub[2 * p], 1u);
-        if (bits & 2u) atomicAdd(&s_sub[2 * p + 1], 1u);
-      }
-    }
-    __syncwarp();
-    const uint4 mv = reinterpret_cast<const uint4*>(msk)[lane];
-    reinterpret_cast<uint4*>(submask)[(size_t)g * (kSPT / 4) + lane] = mv;  // padded to whole tiles
-    if (__ballot_sync(0xffffffffu, (mv.x | mv.y | mv.z | mv.w) != 0u) && lane == 0)
-      tile_list[atomicAdd(tile_count, 1u)] = (unsigned)g;
-    __syncwarp();
   }
   __syncthreads();
-  if (tid < 2 * P && s_sub[tid]) atomicAdd(&a.blocks[tid], s_sub[tid]);
+  if (tid < NS && s_blk[tid]) atomicAdd(&blocks[tid], s_blk[tid]);
 }
 
-// Level 3 (k_lbi): the TMA ring streams the listed tiles (32 KB of SAX + the 128
-// sub-block masks, on one barrier); the live (sub-block, slot pair) units of a tile
-// -- consecutive live slots of a sub-block, two at a time -- are dealt round-robin
-// to the warps, 8 units per warp round (4 lanes x 4 series per unit).  Every warp
-// derives the same unit list from the masks (no CTA barrier).
 template <int P>
 __global__ void __launch_bounds__(kIThreads, 1)
-k_lbi(LbArgs a, const unsigned* __restrict__ submask, const unsigned* __restrict__ tile_list,
+k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__ tile_list,
       const unsigned* __restrict__ tile_count) {
   extern __shared__ __align__(128) uint8_t dsm[];
   uint8_t* s_tiles = dsm;
@@ -1255,14 +1168,14 @@ k_lbi(LbArgs a, const unsigned* __restrict__ submask, const unsigned* __restrict
   unsigned* s_hist = reinterpret_cast<unsigned*>(dsm + kITabEnd);  // [kMaxB][kNB] after the ring + table
   __shared__ __align__(8) uint64_t s_full[kIStages];
   __shared__ unsigned s_cnt[kIStages];
-  // per stage: the tile's id and its sub-block masks, delivered with the tile
-  __shared__ __align__(16) uint32_t s_sm[kIStages][kSPT];
+  // per stage: the tile's id and its 32 block masks, delivered with the tile (the
+  // warps never wait on a global load at a tile boundary)
+  __shared__ __align__(16) uint32_t s_bm[kIStages][kBPT];
   __shared__ int64_t s_tile[kIStages];
   // this CTA's share of the tile list (entries blockIdx.x + i * gridDim.x), staged once:
   // a refill then starts its TMA without a dependent global load
   __shared__ unsigned s_tl[kITileIds];
-  __shared__ uint16_t s_uinc[kIWarps][kSPT];  // per warp: inclusive unit counts over the tile's sub-blocks
-  __shared__ uint32_t s_qs[2 * P][kTW + 1];   // per slot and segment: half2(q_lo16, -q_hi16); +1: banks
+  __shared__ uint32_t s_qs[2 * P][kTW];  // per slot and segment: half2(q_lo16, -q_hi16)
   __shared__ LbConsts s_c;
   __shared__ WarpBuf s_wb[kIWarps];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1273,25 +1186,18 @@ k_lbi(LbArgs a, const unsigned* __restrict__ submask, const unsigned* __restrict
   if (lane == 0) wb.n = 0;
   for (int i = tid; i < nslots * kNB; i += kIThreads) s_hist[i] = 0;
 
-  static_assert(kTS == PARIS_INDEX_TILE && kSPT == 128, "index tiles are the LB kernel's tiles");
+  static_assert(kTS == PARIS_INDEX_TILE, "index tiles are the LB kernel's tiles");
   auto issue = [&](int64_t li, int st) {
     // tile-major sorted SAX: the tile's 16 rows are one contiguous 32 KB range; its
-    // sub-block masks (512 B) ride on the same barrier; the id is published before
-    // the arrive (release), so waiters that see the phase flip see it too
+    // block masks (128 B) ride on the same barrier; the id is published before the
+    // arrive (release), so waiters that see the phase flip see it too
     const int64_t i = (li - blockIdx.x) / gridDim.x;
     const int64_t tile = i < kITileIds ? s_tl[i] : tile_list[li];
     s_tile[st] = tile;
-    mbar_expect_tx(&s_full[st], (unsigned)(kTileBytes + kSPT * 4));
+    mbar_expect_tx(&s_full[st], (unsigned)(kTileBytes + kBPT * 4));
     bulk_g2s(s_tiles + (size_t)st * kTileBytes, a.sax + (size_t)tile * kTileBytes, (unsigned)kTileBytes,
              &s_full[st]);
-    bulk_g2s(&s_sm[st][0], submask + (size_t)tile * kSPT, (unsigned)(kSPT * 4), &s_full[st]);
-    // the ring holds 2 tiles; the tile kIPf refills later is pulled into L2 now, so
-    // its copy is served at L2 latency
-    const int64_t pf = li + (int64_t)kIPf * gridDim.x, ip = i + kIPf;
-    if (pf < nlist) {
-      const int64_t tp = ip < kITileIds ? s_tl[ip] : tile_list[pf];
-      bulk_prefetch_l2(a.sax + (size_t)tp * kTileBytes, (unsigned)kTileBytes);
-    }
+    bulk_g2s(&s_bm[st][0], bmask + (size_t)tile * kBPT, (unsigned)(kBPT * 4), &s_full[st]);
   };
   if (tid == 0) {
     for (int st = 0; st < kIStages; ++st) {
@@ -1311,10 +1217,6 @@ k_lbi(LbArgs a, const unsigned* __restrict__ submask, const unsigned* __restrict
       const int64_t li = blockIdx.x + (int64_t)st * gridDim.x;
       if (li < nlist) issue(li, st);
     }
-    for (int i = kIStages; i < kIPf; ++i) {  // the tiles between the ring and the first prefetch
-      const int64_t li = blockIdx.x + (int64_t)i * gridDim.x;
-      if (li < nlist) bulk_prefetch_l2(a.sax + (size_t)s_tl[i] * kTileBytes, (unsigned)kTileBytes);
-    }
   }
   for (int i = tid; i < kMaxCard * 32; i += kIThreads) s_tab[i] = a.tab->lu16[i >> 5];
   for (int i = tid; i < 2 * P * kTW; i += kIThreads) {
@@ -1325,8 +1227,6 @@ k_lbi(LbArgs a, const unsigned* __restrict__ submask, const unsigned* __restrict
   lb_consts_init(a, nslots, &s_c);  // ends with __syncthreads
   const char* tabc = reinterpret_cast<const char*>(s_tab);
   const uint32_t lane8 = (uint32_t)lane * 8u;  // < 256: byte 0 of the table offset
-  const int grp = lane >> 2, gl = lane & 3;    // unit slot of this lane in a round, lane within the unit
-  uint16_t* uinc = s_uinc[warp];
   int rot = 0;
 
   for (int64_t it = 0;; ++it) {
@@ -1336,55 +1236,41 @@ k_lbi(LbArgs a, const unsigned* __restrict__ submask, const unsigned* __restrict
     mbar_wait(&s_full[st], (unsigned)((it / kIStages) & 1));
     const int64_t tile = s_tile[st];
     PARIS_DCHECK(tile >= 0 && tile * kTS < a.n);
-    // unit counts: lane l owns sub-blocks 4l..4l+3
-    const uint4 smv = *reinterpret_cast<const uint4*>(&s_sm[st][4 * lane]);
-    const int c0 = (__popc(smv.x) + 1) >> 1, c1 = (__popc(smv.y) + 1) >> 1;
-    const int c2 = (__popc(smv.z) + 1) >> 1, c3 = (__popc(smv.w) + 1) >> 1;
-    const int own = c0 + c1 + c2 + c3;
-    int incl = own;
+    // the tile's 32 block masks (lane = block); a block's live slots are computed two
+    // at a time (consecutive live slots form an item); a 64-series block is half a
+    // warp, so a warp takes two items per round (lanes 0-15 and 16-31); items are
+    // dealt round-robin, rotating, so no warp is systematically behind
+    const uint32_t bm = s_bm[st][lane];
+    const int cnt = (__popc(bm) + 1) >> 1;
+    int incl = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int v = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += v;
     }
-#if PARIS_EXP_NOUNITS  // timing experiment only: stream + enumerate, no unit work (results invalid)
-    const int total = 0 * __shfl_sync(0xffffffffu, incl, 31);
-#else
     const int total = __shfl_sync(0xffffffffu, incl, 31);
-#endif
-    {
-      const int e = incl - own;
-      uinc[4 * lane] = (uint16_t)(e + c0);
-      uinc[4 * lane + 1] = (uint16_t)(e + c0 + c1);
-      uinc[4 * lane + 2] = (uint16_t)(e + c0 + c1 + c2);
-      uinc[4 * lane + 3] = (uint16_t)incl;
-    }
-    __syncwarp();
     const uint32_t* rows = reinterpret_cast<const uint32_t*>(s_tiles + (size_t)st * kTileBytes);
     const int first = (warp - rot + 2 * kIWarps) % kIWarps;
-    rot = (rot + (total + kUPR - 1) / kUPR) % kIWarps;
-    for (int t0 = kUPR * first; t0 < total; t0 += kUPR * kIWarps) {
-      const int t = t0 + grp;  // this lane group's unit
+    rot = (rot + (total + 1) / 2) % kIWarps;
+    const int h = lane >> 4, hl = lane & 15;
+    for (int t0 = 2 * first; t0 < total; t0 += 2 * kIWarps) {
+      const int t = t0 + h;  // this half-warp's item
+      const unsigned m0 = __ballot_sync(0xffffffffu, incl <= t0);
+      const unsigned m1 = __ballot_sync(0xffffffffu, incl <= t0 + 1);
       const bool active = t < total;
-      // sub-block of unit t: the number of sub-blocks whose inclusive count is <= t
-      int k = 0;
-#pragma unroll
-      for (int stp = kSPT / 2; stp > 0; stp >>= 1)
-        if ((int)uinc[k + stp - 1] <= t) k += stp;
-      k = active ? k : 0;
-      const int excl = k ? (int)uinc[k - 1] : 0;
-      const uint32_t smk = s_sm[st][k];
+      const int k = active ? __popc(h ? m1 : m0) : 0;
+      const int excl = __shfl_sync(0xffffffffu, incl - cnt, k);
+      const uint32_t bmk = __shfl_sync(0xffffffffu, bm, k);
       const int r = t - excl;
-      const int saf = active ? (int)__fns(smk, 0, 2 * r + 1) : 0;
+      const int saf = active ? (int)__fns(bmk, 0, 2 * r + 1) : 0;
       const int sa = (saf >= 0 && saf < 32) ? saf : 0;
-      const int sbf = active ? (int)__fns(smk, 0, 2 * r + 2) : -1;
+      const int sbf = active ? (int)__fns(bmk, 0, 2 * r + 2) : -1;
       const int sb = (sbf >= 0 && sbf < 32) ? sbf : -1;
       const int sq = sb >= 0 ? sb : sa;  // odd count: duplicate lane, masked in emission
       uint32_t acc[4] = {0u, 0u, 0u, 0u};
-      const uint32_t* rw = rows + k * (PARIS_INDEX_SUB / 4) + gl;
 #pragma unroll 4
       for (int s = 0; s < kTW; ++s) {
-        const uint32_t word = rw[s * (kTS / 4)];
+        const uint32_t word = rows[s * (kTS / 4) + k * (PARIS_INDEX_BLOCK / 4) + hl];
         const uint32_t qa = s_qs[sa][s], qb = s_qs[sq][s];
         const uint32_t qx = __byte_perm(qa, qb, 0x5410);  // (q_lo16[sa], q_lo16[sb])
         const uint32_t qy = __byte_perm(qa, qb, 0x7632);  // (-q_hi16[sa], -q_hi16[sb])
@@ -1398,9 +1284,9 @@ k_lbi(LbArgs a, const unsigned* __restrict__ submask, const unsigned* __restrict
           acc[j] = h2_acc_delta2(acc[j], a1, b1);
         }
       }
-      const int64_t i0 = tile * kTS + k * PARIS_INDEX_SUB + 4 * gl;
+      const int64_t i0 = tile * kTS + k * PARIS_INDEX_BLOCK + 4 * hl;
       const int nvalid = active ? (int)std::max<int64_t>(0, imin64(4, a.n - i0)) : 0;
-      PARIS_DCHECK(k < kSPT && sa >= 0 && sa < nslots && sb < nslots);
+      PARIS_DCHECK(k < kBPT && sa >= 0 && sa < nslots && sb < nslots);
       lbi_emit(acc, sa, sb, i0, nvalid, nslots, s_c, a, wb, s_hist);
     }
     __syncwarp();
@@ -1952,7 +1838,8 @@ k_refine1(RefineArgs a, int nb) {
 // test is the same as the sorted walk's, so the refined set differs only by the
 // order within a wave.
 // 6 CTAs (48 warps) per SM for len <= 256: 42 registers per thread, room for U rows
-// in flight per warp without spilling (U = 2 at len 256: 96 KB of rows in flight per SM)
+// in flight per warp (U = 2 at len 256: 96 KB of rows in flight per SM; measured at
+// C4: 1.50 ms/step vs 1.87 with 8 CTAs x 1 row)
 #ifndef PARIS_REFU_CTAS
 #define PARIS_REFU_CTAS 6
 #endif
@@ -2218,8 +2105,10 @@ struct Ws {
   unsigned* blocks;      // index mode: blocks whose envelope bound passed, per query
   unsigned* tile_count;  // index mode: live tiles listed
   unsigned* updates;     // nb mode: V_bsf updates per query
-  unsigned* submask;     // index mode: [ntiles*128] per-sub-block live query-slot masks
+  unsigned* bmask;       // index mode: [ntiles*16] per-block live query-slot masks
   unsigned* tile_list;   // index mode: live tiles
+  unsigned* tile_flag;   // index mode: [ntiles] tile already listed (zeroed per batch)
+  size_t flag_bytes;
   size_t zero_bytes;
   unsigned long long* best;
   uint64_t* cand;
@@ -2329,8 +2218,6 @@ cudaError_t launch_index_lb(const Plan& p, const uint8_t* sax, int nb, const Car
   if (attr_dev != dev) {
     cudaError_t e = cudaFuncSetAttribute(k_lbi<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLbiSmem);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_blkmask<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBmSmem);
-    if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
   LbArgs la;
@@ -2338,15 +2225,13 @@ cudaError_t launch_index_lb(const Plan& p, const uint8_t* sax, int nb, const Car
   la.g_q = ws.g_q; la.g_q16 = ws.g_q16; la.nb = nb; la.thr = ws.thr_seed; la.count = ws.count;
   la.hist = ws.hist; la.cand = ws.cand; la.cap = cap; la.perm = p.perm; la.env = p.env;
   la.blocks = ws.blocks;
-  la.env_sub = p.env + (size_t)((p.n + PARIS_INDEX_BLOCK - 1) / PARIS_INDEX_BLOCK) * 2 * kTW;
   const int64_t ntiles = (p.n + kTS - 1) / kTS;
   const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms() * 8, (ntiles + 7) / 8));
-  cudaError_t e = PARIS_LAUNCH("lb_blocks", k_blkmask<P>, bgrid, kBmThreads, kBmSmem, st, la, ws.submask, ws.tile_list,
-                               ws.tile_count);
+  cudaError_t e = PARIS_LAUNCH("lb_blocks", k_blkmask<P>, bgrid, 256, 0, st, la, ws.bmask, ws.tile_list,
+                               ws.tile_count, ws.blocks);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(sms(), ntiles);
-  return PARIS_LAUNCH("lb_pass", k_lbi<P>, grid, kIThreads, kLbiSmem, st, la, ws.submask, ws.tile_list,
-                      ws.tile_count);
+  return PARIS_LAUNCH("lb_pass", k_lbi<P>, grid, kIThreads, kLbiSmem, st, la, ws.bmask, ws.tile_list, ws.tile_count);
 }
 
 cudaError_t dispatch_index_lb(int nb, const Plan& p, const uint8_t* sax, const CardTables* tab, const Ws& ws,
@@ -2454,8 +2339,9 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   const size_t o_sorted = take(sizeof(uint64_t) * B * (size_t)cap);
   const size_t o_lists = take(p.k > 1 ? sizeof(uint64_t) * B * (size_t)p.XB * p.k : 8);
   const int64_t ntiles = (p.n + kTS - 1) / kTS;
-  const size_t o_smask = take(p.perm ? sizeof(unsigned) * (size_t)ntiles * kSPT : 8);
+  const size_t o_bmask = take(p.perm ? sizeof(unsigned) * (size_t)ntiles * kBPT : 8);
   const size_t o_tlist = take(p.perm ? sizeof(unsigned) * (size_t)ntiles : 8);
+  const size_t o_tflag = take(p.perm ? sizeof(unsigned) * (size_t)ntiles : 8);
   void* base = nullptr;
   cudaError_t e = cudaMallocAsync(&base, off, st);
   if (e != cudaSuccess) {
@@ -2484,8 +2370,10 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   ws.cand = (uint64_t*)(c + o_cand);
   ws.sorted = (uint64_t*)(c + o_sorted);
   ws.lists = (uint64_t*)(c + o_lists);
-  ws.submask = (unsigned*)(c + o_smask);
+  ws.bmask = (unsigned*)(c + o_bmask);
   ws.tile_list = (unsigned*)(c + o_tlist);
+  ws.tile_flag = (unsigned*)(c + o_tflag);
+  ws.flag_bytes = p.perm ? sizeof(unsigned) * (size_t)ntiles : 0;
   return PARIS_OK;
 }
 
