@@ -2425,7 +2425,16 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
   }
   if (p.tiled) {
     const int grid = (int)std::min<int64_t>(sms(), (p.n + kTS - 1) / kTS);
-    if (p.perm) PARIS_CHECK_LAUNCH(dispatch_index_lb(nb, p, sax, tab, ws, st, cap), "lb_pass launch");
+    if (p.perm) {
+      PARIS_CHECK_LAUNCH(dispatch_index_lb(nb, p, sax, tab, ws, st, cap), "lb_pass launch");
+      if (getenv("PARIS_DEBUG_TILES")) {  // debugging aid: live tiles streamed by this batch
+        unsigned tc = 0;
+        cudaMemcpyAsync(&tc, ws.tile_count, 4, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        fprintf(stderr, "[paris] batch q0=%d nb=%d: %u of %lld tiles live\n", q0, nb, tc,
+                (long long)((p.n + kTS - 1) / kTS));
+      }
+    }
     else if (nb == 1) PARIS_CHECK_LAUNCH(launch_lb1(p, sax, tab, ws, st, cap), "lb_pass launch");
     else PARIS_CHECK_LAUNCH(dispatch_lbt<1>(nb, p, sax, tab, ws, st, cap, p.n, grid), "lb_pass launch");
   } else {
