@@ -299,7 +299,7 @@ def run_gpu(args):
         also the end-to-end variant through host buffers and the clock record."""
         use_index = path == "index"
         use_nb = path == "nb"
-        b_path = args.batch or (32 if use_index else 16)  # the library's default queries per pass
+        b_path = args.batch or (64 if use_index else 16)  # the library's default queries per pass
         kcfg = P.KnnConfig(batch=b_path, index_seeds=args.index_seeds, sorted_refine=args.sorted_refine)
         nbatches = sum((min(call_q, nq - c0) + b_path - 1) // b_path for c0 in range(0, nq, call_q))
         q_per_pass = nq / nbatches

@@ -122,7 +122,7 @@ int paris_index_build(const uint8_t* sax, int64_t n, int32_t w, int32_t card, ui
 
 /* Tunables for paris_knn_exact_ex (0 = library default). */
 typedef struct paris_knn_config {
-  int32_t batch;        /* queries per SAX pass: 1..16 (flat, default 16), 1..32 (index, default 32) */
+  int32_t batch;        /* queries per SAX pass: 1..16 (flat, default 16), 1..64 (index, default 64) */
   int32_t seed_div;     /* seed sample = n / seed_div series (default 16) */
   int32_t wave_a;       /* k = 1: candidates per query refined in the first (lowest-LB) wave; default 2048 */
   int32_t reserved[5];  /* tuning/test hooks: [0] = 1 forces the direct-load LB kernels;

@@ -48,7 +48,7 @@ class _KProf(ctypes.Structure):
 
 @dataclass
 class KnnConfig:
-    batch: int = 0      # queries per SAX pass: flat 1..16 (default 16), index 1..32 (default 32)
+    batch: int = 0      # queries per SAX pass: flat 1..16 (default 16), index 1..64 (default 64)
     seed_div: int = 0   # seed sample = n / seed_div (0 = 16)
     wave_a: int = 0     # k = 1: first refinement wave per query (0 = 2048)
     force_direct: bool = False  # test hook: use the direct-load LB kernels even where the TMA-tiled ones apply

@@ -39,7 +39,7 @@ namespace {
 
 constexpr int kMaxW = 64;
 constexpr int kNB = 256;            // LB histogram bins per query
-constexpr int kMaxB = 32;           // queries per SAX pass (index path)
+constexpr int kMaxB = 64;           // queries per SAX pass (index path)
 constexpr int kMaxBFlat = 16;       // queries per SAX pass (flat path: P <= 8 pairs)
 constexpr int kLBThreads = 256;
 constexpr int kRefThreads = 256;
@@ -667,16 +667,31 @@ struct WarpBuf {
   int n;
 };
 
-// s_hist: the CTA's shared-memory LB histogram [kMaxB][kNB] (flushed at kernel end)
+// Shared-memory LB histogram of 64 slots in 16-bit halves (32 KB instead of 64):
+// word i/2 holds bins i (low half) and i+1 (high half).  The increment that takes a
+// half to 0x8000 moves 0x8000 to the global histogram, so a half never carries
+// into its neighbour (at most a CTA's threads increment it in between).
+__device__ __forceinline__ void hist16_add(unsigned* s_h16, int idx, unsigned* g_hist) {
+  const unsigned sh = (unsigned)(idx & 1) * 16u;
+  const unsigned old = atomicAdd(&s_h16[idx >> 1], 1u << sh);
+  if (((old >> sh) & 0xFFFFu) == 0x7FFFu) {
+    atomicSub(&s_h16[idx >> 1], 0x8000u << sh);
+    atomicAdd(&g_hist[idx], 0x8000u);
+  }
+}
+
+// s_hist: the CTA's shared-memory LB histogram [kMaxB][kNB] (flushed at kernel end);
+// HIST16: the packed 16-bit form (hist16_add)
+template <bool HIST16 = false>
 __device__ void wb_flush(WarpBuf& wb, int nslots, const LbConsts& c, const LbArgs& a, unsigned* s_hist) {
   const int lane = threadIdx.x & 31;
   __syncwarp();
   const int m = wb.n;
   if (m == 0) return;
-  if (lane < nslots) {
-    const unsigned k = wb.cnt[lane];
-    wb.cur[lane] = k ? atomicAdd(&a.count[lane], k) : 0u;
-    wb.cnt[lane] = 0;
+  for (int b = lane; b < nslots; b += 32) {
+    const unsigned k = wb.cnt[b];
+    wb.cur[b] = k ? atomicAdd(&a.count[b], k) : 0u;
+    wb.cnt[b] = 0;
   }
   __syncwarp();
   for (int e = lane; e < m; e += 32) {
@@ -688,7 +703,9 @@ __device__ void wb_flush(WarpBuf& wb, int nslots, const LbConsts& c, const LbArg
     // bucket offsets must describe exactly the `cap` entries K5 orders
     if ((int64_t)pos < a.cap) {
       a.cand[(size_t)b * a.cap + pos] = key;
-      atomicAdd(&s_hist[b * kNB + lb_bin(key_val(key), c.scale[b])], 1u);
+      const int idx = b * kNB + lb_bin(key_val(key), c.scale[b]);
+      if (HIST16) hist16_add(s_hist, idx, a.hist);
+      else atomicAdd(&s_hist[idx], 1u);
     }
   }
   __syncwarp();
@@ -815,9 +832,9 @@ constexpr size_t kTSmem = kStages * kTileBytes + kMaxCard * 32 * 4;
 constexpr int kIStages = 2;      // compute-bound on the live items: a tile's load (~0.8 us) < its work
 constexpr int kIThreads = 768;   // 24 warps: more warps to hide the lookup -> math latency chain
 constexpr int kIWarps = kIThreads / 32;
-constexpr int kITileIds = 1024;  // tile ids staged per CTA (148 CTAs: 310 M series; beyond, global loads)
+constexpr int kITileIds = 512;   // tile ids staged per CTA (148 CTAs: 155 M series; beyond, global loads)
 constexpr size_t kITabEnd = kIStages * kTileBytes + (size_t)kMaxCard * 32 * 8;
-constexpr size_t kLbiSmem = kITabEnd + (size_t)kMaxB * kNB * 4;
+constexpr size_t kLbiSmem = kITabEnd + (size_t)kMaxB * kNB * 2;  // + the 16-bit LB histograms
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -897,7 +914,7 @@ k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
   const int nslots = P > 0 ? 2 * P : 1;
   WarpBuf& wb = s_wb[MODE == 1 ? (tid >> 5) : 0];
   if (MODE == 1) {
-    if (lane < kMaxB) wb.cnt[lane] = 0;
+    for (int b = lane; b < kMaxB; b += 32) wb.cnt[b] = 0;
     if (lane == 0) wb.n = 0;
     for (int i = tid; i < nslots * kNB; i += kTThreads) s_hist[i] = 0;
   }
@@ -1035,6 +1052,13 @@ k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
 // Candidate emission of one index item: 4 series x 2 query slots (sa = low half,
 // sb = high half, sb < 0: none).  Same tests and warp buffer as lb_emit_wb.
 __device__ __forceinline__ uint32_t half_of(uint32_t v, int h) { return (v >> (16 * h)) & 0xFFFFu; }
+// Position of the n-th (1-based) set bit of a 64-bit mask, -1 if it has fewer.
+__device__ __forceinline__ int fns64(uint64_t m, int n) {
+  const uint32_t lo = (uint32_t)m, hi = (uint32_t)(m >> 32);
+  const int cl = __popc(lo);
+  const int r = n <= cl ? (int)__fns(lo, 0, n) : (n - cl <= __popc(hi) ? 32 + (int)__fns(hi, 0, n - cl) : -1);
+  return (r >= 0 && r < 64) ? r : -1;
+}
 
 __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int sb, int64_t i0, int nvalid,
                                          int nslots, const LbConsts& c, const LbArgs& a, WarpBuf& wb,
@@ -1066,7 +1090,7 @@ __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int s
     if (lane >= o) incl += v;
   }
   const int total = __shfl_sync(0xffffffffu, incl, 31);
-  if (wb.n + total > kWB) wb_flush(wb, nslots, c, a, s_hist);
+  if (wb.n + total > kWB) wb_flush<true>(wb, nslots, c, a, s_hist);
   if (total > kWB) {  // degenerate (e.g. tau = inf): straight to global memory
     for (uint32_t r = pm; r; r &= r - 1) {
       const int bit = __ffs(r) - 1, j = bit >> 1, sl = (bit & 1) ? sb : sa;
@@ -1097,7 +1121,7 @@ __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int s
 // the 32 blocks of a warp step are one whole tile, so the warp lists it itself.
 template <int P>
 __global__ void __launch_bounds__(256)
-k_blkmask(LbArgs a, unsigned* __restrict__ bmask, unsigned* __restrict__ tile_list,
+k_blkmask(LbArgs a, unsigned long long* __restrict__ bmask, unsigned* __restrict__ tile_list,
           unsigned* __restrict__ tile_count, unsigned* __restrict__ blocks) {
   // the envelope bound in the same packed fp16 pair form (and error budget, k_lb)
   // as the series bound: per segment the region [L16[min], U16[max]], two query
@@ -1118,7 +1142,7 @@ k_blkmask(LbArgs a, unsigned* __restrict__ bmask, unsigned* __restrict__ tile_li
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + tid) >> 5, GW = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t g = gw; g < ntiles; g += GW) {
     const int64_t blk = 32 * g + lane;
-    uint32_t bm = 0;
+    uint64_t bm = 0;
     if (blk < nblocks) {
       const uint4 mn = __ldg(reinterpret_cast<const uint4*>(a.env + (size_t)blk * 32));
       const uint4 mx = __ldg(reinterpret_cast<const uint4*>(a.env + (size_t)blk * 32 + 16));
@@ -1139,10 +1163,10 @@ k_blkmask(LbArgs a, unsigned* __restrict__ bmask, unsigned* __restrict__ tile_li
         }
       }
 #pragma unroll
-      for (int p = 0; p < P; ++p) bm |= h2_le_bits(acc[p], s_c.T16[p]) << (2 * p);
+      for (int p = 0; p < P; ++p) bm |= (uint64_t)h2_le_bits(acc[p], s_c.T16[p]) << (2 * p);
     }
     bmask[blk] = bm;  // padded to whole tiles
-    const unsigned live = __ballot_sync(0xffffffffu, bm != 0u);
+    const unsigned live = __ballot_sync(0xffffffffu, bm != 0ull);
     if (lane == 0 && live) tile_list[atomicAdd(tile_count, 1u)] = (unsigned)g;
 #pragma unroll
     for (int b = 0; b < NS; ++b) {
@@ -1156,7 +1180,7 @@ k_blkmask(LbArgs a, unsigned* __restrict__ bmask, unsigned* __restrict__ tile_li
 
 template <int P>
 __global__ void __launch_bounds__(kIThreads, 1)
-k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__ tile_list,
+k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __restrict__ tile_list,
       const unsigned* __restrict__ tile_count) {
   extern __shared__ __align__(128) uint8_t dsm[];
   uint8_t* s_tiles = dsm;
@@ -1165,12 +1189,12 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
   // 8..15, lane*8 -> bits 0..7; no multiply); a 64-bit load is served per half-warp
   // and the 16 lanes of each half hit distinct banks
   uint2* s_tab = reinterpret_cast<uint2*>(dsm + kIStages * kTileBytes);
-  unsigned* s_hist = reinterpret_cast<unsigned*>(dsm + kITabEnd);  // [kMaxB][kNB] after the ring + table
+  unsigned* s_hist = reinterpret_cast<unsigned*>(dsm + kITabEnd);  // [kMaxB][kNB] 16-bit (hist16_add)
   __shared__ __align__(8) uint64_t s_full[kIStages];
   __shared__ unsigned s_cnt[kIStages];
   // per stage: the tile's id and its 32 block masks, delivered with the tile (the
   // warps never wait on a global load at a tile boundary)
-  __shared__ __align__(16) uint32_t s_bm[kIStages][kBPT];
+  __shared__ __align__(16) unsigned long long s_bm[kIStages][kBPT];
   __shared__ int64_t s_tile[kIStages];
   // this CTA's share of the tile list (entries blockIdx.x + i * gridDim.x), staged once:
   // a refill then starts its TMA without a dependent global load
@@ -1182,9 +1206,9 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
   const int nslots = 2 * P;
   const int64_t nlist = *tile_count;
   WarpBuf& wb = s_wb[warp];
-  if (lane < kMaxB) wb.cnt[lane] = 0;
+  for (int b = lane; b < kMaxB; b += 32) wb.cnt[b] = 0;
   if (lane == 0) wb.n = 0;
-  for (int i = tid; i < nslots * kNB; i += kIThreads) s_hist[i] = 0;
+  for (int i = tid; i < nslots * kNB / 2; i += kIThreads) s_hist[i] = 0;
 
   static_assert(kTS == PARIS_INDEX_TILE, "index tiles are the LB kernel's tiles");
   auto issue = [&](int64_t li, int st) {
@@ -1194,10 +1218,10 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
     const int64_t i = (li - blockIdx.x) / gridDim.x;
     const int64_t tile = i < kITileIds ? s_tl[i] : tile_list[li];
     s_tile[st] = tile;
-    mbar_expect_tx(&s_full[st], (unsigned)(kTileBytes + kBPT * 4));
+    mbar_expect_tx(&s_full[st], (unsigned)(kTileBytes + kBPT * 8));
     bulk_g2s(s_tiles + (size_t)st * kTileBytes, a.sax + (size_t)tile * kTileBytes, (unsigned)kTileBytes,
              &s_full[st]);
-    bulk_g2s(&s_bm[st][0], bmask + (size_t)tile * kBPT, (unsigned)(kBPT * 4), &s_full[st]);
+    bulk_g2s(&s_bm[st][0], bmask + (size_t)tile * kBPT, (unsigned)(kBPT * 8), &s_full[st]);
   };
   if (tid == 0) {
     for (int st = 0; st < kIStages; ++st) {
@@ -1240,8 +1264,8 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
     // at a time (consecutive live slots form an item); a 64-series block is half a
     // warp, so a warp takes two items per round (lanes 0-15 and 16-31); items are
     // dealt round-robin, rotating, so no warp is systematically behind
-    const uint32_t bm = s_bm[st][lane];
-    const int cnt = (__popc(bm) + 1) >> 1;
+    const uint64_t bm = s_bm[st][lane];
+    const int cnt = (__popcll(bm) + 1) >> 1;
     int incl = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -1260,12 +1284,11 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
       const bool active = t < total;
       const int k = active ? __popc(h ? m1 : m0) : 0;
       const int excl = __shfl_sync(0xffffffffu, incl - cnt, k);
-      const uint32_t bmk = __shfl_sync(0xffffffffu, bm, k);
+      const uint64_t bmk = __shfl_sync(0xffffffffu, (unsigned long long)bm, k);
       const int r = t - excl;
-      const int saf = active ? (int)__fns(bmk, 0, 2 * r + 1) : 0;
-      const int sa = (saf >= 0 && saf < 32) ? saf : 0;
-      const int sbf = active ? (int)__fns(bmk, 0, 2 * r + 2) : -1;
-      const int sb = (sbf >= 0 && sbf < 32) ? sbf : -1;
+      const int saf = active ? fns64(bmk, 2 * r + 1) : 0;
+      const int sa = saf >= 0 ? saf : 0;
+      const int sb = active ? fns64(bmk, 2 * r + 2) : -1;
       const int sq = sb >= 0 ? sb : sa;  // odd count: duplicate lane, masked in emission
       uint32_t acc[4] = {0u, 0u, 0u, 0u};
 #pragma unroll 4
@@ -1301,10 +1324,12 @@ k_lbi(LbArgs a, const unsigned* __restrict__ bmask, const unsigned* __restrict__
       }
     }
   }
-  wb_flush(wb, nslots, s_c, a, s_hist);
+  wb_flush<true>(wb, nslots, s_c, a, s_hist);
   __syncthreads();
-  for (int i = tid; i < nslots * kNB; i += kIThreads)
-    if (s_hist[i]) atomicAdd(&a.hist[i], s_hist[i]);
+  for (int i = tid; i < nslots * kNB; i += kIThreads) {
+    const unsigned v = (s_hist[i >> 1] >> (16 * (i & 1))) & 0xFFFFu;
+    if (v) atomicAdd(&a.hist[i], v);
+  }
 }
 
 // ---------------------------------------------------------------- K4, one query per pass
@@ -1331,7 +1356,7 @@ k_lb1(LbArgs a) {
   __shared__ unsigned s_hist[kNB];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   WarpBuf& wb = s_wb[warp];
-  if (lane < kMaxB) wb.cnt[lane] = 0;
+  for (int b = lane; b < kMaxB; b += 32) wb.cnt[b] = 0;
   if (lane == 0) wb.n = 0;
   for (int i = tid; i < kNB; i += kLb1Threads) s_hist[i] = 0;
   for (int i = tid; i < kMaxCard * 32; i += kLb1Threads) s_tab[i] = a.tab->lu16p[i >> 5];
@@ -1555,9 +1580,8 @@ k_nb(NbArgs a) {
 template <int P>
 __global__ void k_qprep(const float* __restrict__ queries, int nb, int len, int w, float2* __restrict__ g_q,
                         uint2* __restrict__ g_q16) {
-  __shared__ float2 s_q[2 * P * kMaxW];
-  __shared__ uint2 s_q16[P * kMaxW];
-  query_prep<P>(queries, nb, len, w, s_q, s_q16, g_q, g_q16);
+  extern __shared__ float2 s_qdyn[];  // [2P * kMaxW] intervals, then [P * kMaxW] fp16 pairs (qprep_smem)
+  query_prep<P>(queries, nb, len, w, s_qdyn, reinterpret_cast<uint2*>(s_qdyn + 2 * P * kMaxW), g_q, g_q16);
 }
 
 // ---------------------------------------------------------------- K5 bucket order
@@ -2105,7 +2129,7 @@ struct Ws {
   unsigned* blocks;      // index mode: blocks whose envelope bound passed, per query
   unsigned* tile_count;  // index mode: live tiles listed
   unsigned* updates;     // nb mode: V_bsf updates per query
-  unsigned* bmask;       // index mode: [ntiles*16] per-block live query-slot masks
+  unsigned long long* bmask;  // index mode: [ntiles*32] per-block live query-slot masks
   unsigned* tile_list;   // index mode: live tiles
   unsigned* tile_flag;   // index mode: [ntiles] tile already listed (zeroed per batch)
   size_t flag_bytes;
@@ -2136,7 +2160,7 @@ struct Plan {
   bool sorted_refine = false;  // k = 1: walk bucket-sorted lists (K5) instead of the unsorted waves
 };
 
-int pairs_for(int nb) { return nb <= 2 ? 1 : nb <= 4 ? 2 : nb <= 8 ? 4 : nb <= 16 ? 8 : 16; }
+int pairs_for(int nb) { return nb <= 2 ? 1 : nb <= 4 ? 2 : nb <= 8 ? 4 : nb <= 16 ? 8 : nb <= 32 ? 16 : 32; }
 
 template <int P, int WT, bool AL>
 cudaError_t launch_seed(const Plan& p, const uint8_t* sax, const float* qb, int nb,
@@ -2241,7 +2265,8 @@ cudaError_t dispatch_index_lb(int nb, const Plan& p, const uint8_t* sax, const C
     case 2: return launch_index_lb<2>(p, sax, nb, tab, ws, st, cap);
     case 4: return launch_index_lb<4>(p, sax, nb, tab, ws, st, cap);
     case 8: return launch_index_lb<8>(p, sax, nb, tab, ws, st, cap);
-    default: return launch_index_lb<16>(p, sax, nb, tab, ws, st, cap);
+    case 16: return launch_index_lb<16>(p, sax, nb, tab, ws, st, cap);
+    default: return launch_index_lb<32>(p, sax, nb, tab, ws, st, cap);
   }
 }
 
@@ -2297,13 +2322,16 @@ cudaError_t dispatch_lbt(int nb, const Plan& p, const uint8_t* sax, const CardTa
   }
 }
 
+constexpr size_t qprep_smem(int P) { return (size_t)3 * P * kMaxW * 8; }  // <= 48 KB at P = 32
+
 cudaError_t launch_qprep(int nb, const Plan& p, const float* qb, const Ws& ws, cudaStream_t st) {
   switch (pairs_for(nb)) {
-    case 1: return PARIS_LAUNCH("qprep", k_qprep<1>, 1, 256, 0, st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
-    case 2: return PARIS_LAUNCH("qprep", k_qprep<2>, 1, 256, 0, st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
-    case 4: return PARIS_LAUNCH("qprep", k_qprep<4>, 1, 256, 0, st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
-    case 8: return PARIS_LAUNCH("qprep", k_qprep<8>, 1, 256, 0, st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
-    default: return PARIS_LAUNCH("qprep", k_qprep<16>, 1, 256, 0, st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
+    case 1: return PARIS_LAUNCH("qprep", k_qprep<1>, 1, 256, qprep_smem(1), st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
+    case 2: return PARIS_LAUNCH("qprep", k_qprep<2>, 1, 256, qprep_smem(2), st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
+    case 4: return PARIS_LAUNCH("qprep", k_qprep<4>, 1, 256, qprep_smem(4), st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
+    case 8: return PARIS_LAUNCH("qprep", k_qprep<8>, 1, 256, qprep_smem(8), st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
+    case 16: return PARIS_LAUNCH("qprep", k_qprep<16>, 1, 256, qprep_smem(16), st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
+    default: return PARIS_LAUNCH("qprep", k_qprep<32>, 1, 256, qprep_smem(32), st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
   }
 }
 
@@ -2339,7 +2367,7 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   const size_t o_sorted = take(sizeof(uint64_t) * B * (size_t)cap);
   const size_t o_lists = take(p.k > 1 ? sizeof(uint64_t) * B * (size_t)p.XB * p.k : 8);
   const int64_t ntiles = (p.n + kTS - 1) / kTS;
-  const size_t o_bmask = take(p.perm ? sizeof(unsigned) * (size_t)ntiles * kBPT : 8);
+  const size_t o_bmask = take(p.perm ? sizeof(unsigned long long) * (size_t)ntiles * kBPT : 8);
   const size_t o_tlist = take(p.perm ? sizeof(unsigned) * (size_t)ntiles : 8);
   const size_t o_tflag = take(p.perm ? sizeof(unsigned) * (size_t)ntiles : 8);
   void* base = nullptr;
@@ -2370,7 +2398,7 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   ws.cand = (uint64_t*)(c + o_cand);
   ws.sorted = (uint64_t*)(c + o_sorted);
   ws.lists = (uint64_t*)(c + o_lists);
-  ws.bmask = (unsigned*)(c + o_bmask);
+  ws.bmask = (unsigned long long*)(c + o_bmask);
   ws.tile_list = (unsigned*)(c + o_tlist);
   ws.tile_flag = (unsigned*)(c + o_tflag);
   ws.flag_bytes = p.perm ? sizeof(unsigned) * (size_t)ntiles : 0;
@@ -2389,7 +2417,7 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
     // query PAA (the direct LB kernels compute it in their seed prologue) + BSF from the first pass
     if (p.tiled) PARIS_CHECK_LAUNCH(launch_qprep(nb, p, qbatch, ws, st), "qprep launch");
     else PARIS_CHECK_LAUNCH(dispatch_p(P, false, p, sax, qbatch, nb, tab, ws, st, cap), "seed_lb launch");
-    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("seed_select", k_seed_prev, 1, 32, 0, st, d_idx, d_dist, nb, q0, p.k, p.d2up,
+    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("seed_select", k_seed_prev, 1, kMaxB, 0, st, d_idx, d_dist, nb, q0, p.k, p.d2up,
                                     ws.thr, ws.thr_seed, ws.best),
                        "seed_prev launch");
   } else {
@@ -2417,7 +2445,7 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
   if (p.nb) {
     // f2: nb-ParIS+ -- no candidate list: fused LB -> refine per worker, then min(V_bsf)
     PARIS_CHECK_LAUNCH(launch_nb(p, raw, sax, qbatch, nb, tab, ws, st), "nb launch");
-    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("finalize", k_finalize1, 1, 32, 0, st, ws.best, nb, q0, d_idx, d_dist,
+    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("finalize", k_finalize1, 1, kMaxB, 0, st, ws.best, nb, q0, d_idx, d_dist,
                                     ws.count, ws.refined, all_count, all_refined, rescan ? 1 : 0,
                                     ws.updates, all_blocks),
                        "finalize launch");
@@ -2488,7 +2516,7 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
       }
     }
     PARIS_CHECK_LAUNCH(e1, "refine launch");
-    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("finalize", k_finalize1, 1, 32, 0, st, ws.best, nb, q0, d_idx, d_dist,
+    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("finalize", k_finalize1, 1, kMaxB, 0, st, ws.best, nb, q0, d_idx, d_dist,
                                     ws.count, ws.refined, all_count, all_refined, rescan ? 1 : 0,
                                     ws.blocks, all_blocks),
                        "finalize launch");
