@@ -658,7 +658,7 @@ __device__ __forceinline__ void lb_emit(const uint32_t (&acc)[4][P], int64_t i0,
 // its candidates (key + query slot) with shared-memory atomics only; when the
 // buffer would overflow (and at the end) the warp flushes it: one global
 // atomicAdd per query slot reserves the slots of all its entries at once.
-constexpr int kWB = 64;
+constexpr int kWB = 128;
 struct WarpBuf {
   uint64_t key[kWB];
   uint8_t slot[kWB];
@@ -829,7 +829,7 @@ constexpr int kTW = 16;
 constexpr size_t kTileBytes = (size_t)kTW * kTS;
 constexpr size_t kTSmem = kStages * kTileBytes + kMaxCard * 32 * 4;
 // k_lbi: 2-stage ring + the 32-copy pair-form table (64 KB) + the LB histograms
-constexpr int kIStages = 3;      // compute-bound on the live items: a tile's load (~0.8 us) < its work
+constexpr int kIStages = 2;      // compute-bound on the live items: a tile's load (~0.8 us) < its work
 constexpr int kIThreads = 768;   // 24 warps: more warps to hide the lookup -> math latency chain
 constexpr int kIWarps = kIThreads / 32;
 constexpr int kITileIds = 512;   // tile ids staged per CTA (148 CTAs: 155 M series; beyond, global loads)
