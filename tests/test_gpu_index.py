@@ -59,7 +59,8 @@ def test_index_build_matches_definition(P, n, card):
 
 
 @pytest.mark.parametrize("n,nq,k", [(2048, 3, 1), (40_000, 16, 1), (40_000, 5, 10), (100_000, 21, 1), (100_000, 32, 1), (60_000, 45, 10),
-                                    (100_000, 9, 100), (6000 * 16, 1, 1)])
+                                    (100_000, 9, 100), (6000 * 16, 1, 1), (50_000, 64, 1), (50_000, 65, 3),
+                                    (40_000, 100, 1), (30_000, 128, 2)])
 def test_knn_index_parity(P, n, nq, k):
     import torch
     x = datagen.random_walks(n, 256, 500 + n)
