@@ -1178,6 +1178,55 @@ k_blkmask(LbArgs a, unsigned long long* __restrict__ bmask, unsigned* __restrict
   if (tid < NS && s_blk[tid]) atomicAdd(&blocks[tid], s_blk[tid]);
 }
 
+// One index item on a half-warp: 64 series (4 per lane, one 32-bit word per
+// segment row) x NP fp16x2 slot pairs; sl[] = the pairs' slots (-1 = none: computed
+// on a valid slot, masked in emission).  Each table lookup serves all NP pairs.
+template <int NP>
+__device__ __forceinline__ void lbi_item(const uint32_t* __restrict__ rows, const char* __restrict__ tabc,
+                                         uint32_t lane8, const uint32_t (*__restrict__ s_qs)[kTW], int k, int hl,
+                                         const int (&sl)[2 * NP], int64_t tile, int nslots, const LbConsts& c,
+                                         const LbArgs& a, WarpBuf& wb, unsigned* s_hist) {
+  int sq[2 * NP];
+#pragma unroll
+  for (int i = 0; i < 2 * NP; ++i) sq[i] = sl[i] >= 0 ? sl[i] : (sl[0] >= 0 ? sl[0] : 0);
+  uint32_t acc[NP][4];
+#pragma unroll
+  for (int p = 0; p < NP; ++p)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[p][j] = 0u;
+#pragma unroll 4
+  for (int s = 0; s < kTW; ++s) {
+    const uint32_t word = rows[s * (kTS / 4) + k * (PARIS_INDEX_BLOCK / 4) + hl];
+    uint32_t qx[NP], qy[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const uint32_t qa = s_qs[sq[2 * p]][s], qb = s_qs[sq[2 * p + 1]][s];
+      qx[p] = __byte_perm(qa, qb, 0x5410);  // (q_lo16[a], q_lo16[b])
+      qy[p] = __byte_perm(qa, qb, 0x7632);  // (-q_hi16[a], -q_hi16[b])
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      // offset = (symbol j << 8) | lane*8: bytes {lane8.b0, word.bj, 0, 0}
+      const uint32_t off = __byte_perm(word, lane8, 0x5504u | ((uint32_t)j << 4));
+      const uint2 tt = *reinterpret_cast<const uint2*>(tabc + off);
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        const uint32_t a1 = h2_fma_relu(qx[p], kHalf2One, tt.x);
+        const uint32_t b1 = h2_fma_relu(qy[p], kHalf2One, tt.y);
+        acc[p][j] = h2_acc_delta2(acc[p][j], a1, b1);
+      }
+    }
+  }
+  const int64_t i0 = tile * kTS + k * PARIS_INDEX_BLOCK + 4 * hl;
+  const int nv = (int)std::max<int64_t>(0, imin64(4, a.n - i0));
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const bool on = sl[2 * p] >= 0;
+    PARIS_DCHECK(k < kBPT && sl[2 * p] < nslots && sl[2 * p + 1] < nslots);
+    lbi_emit(acc[p], on ? sl[2 * p] : 0, on ? sl[2 * p + 1] : -1, i0, on ? nv : 0, nslots, c, a, wb, s_hist);
+  }
+}
+
 template <int P>
 __global__ void __launch_bounds__(kIThreads, 1)
 k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __restrict__ tile_list,
@@ -1260,57 +1309,59 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
     mbar_wait(&s_full[st], (unsigned)((it / kIStages) & 1));
     const int64_t tile = s_tile[st];
     PARIS_DCHECK(tile >= 0 && tile * kTS < a.n);
-    // the tile's 32 block masks (lane = block); a block's live slots are computed two
-    // at a time (consecutive live slots form an item); a 64-series block is half a
-    // warp, so a warp takes two items per round (lanes 0-15 and 16-31); items are
-    // dealt round-robin, rotating, so no warp is systematically behind
+    // the tile's 32 block masks (lane = block).  A block's live slots are taken four
+    // at a time (quad items: two fp16x2 pairs share every table lookup), the last
+    // 1-2 in a pair item (a remainder of 3 is a quad with one dummy slot).  A
+    // 64-series block is half a warp, so a warp takes two items per round (lanes
+    // 0-15 and 16-31); quads first, then pairs (each phase one code path), dealt
+    // round-robin, rotating, so no warp is systematically behind.
     const uint64_t bm = s_bm[st][lane];
-    const int cnt = (__popcll(bm) + 1) >> 1;
-    int incl = cnt;
+    const int pc = __popcll(bm), rem = pc & 3;
+    const int cq = (pc >> 2) + (rem == 3 ? 1 : 0), cp = (rem == 1 || rem == 2) ? 1 : 0;
+    int incl = cq | (cp << 16);
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int v = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += v;
     }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+    const int inq = incl & 0xFFFF, inp = incl >> 16, totq = tot & 0xFFFF, totp = tot >> 16;
     const uint32_t* rows = reinterpret_cast<const uint32_t*>(s_tiles + (size_t)st * kTileBytes);
-    const int first = (warp - rot + 2 * kIWarps) % kIWarps;
-    rot = (rot + (total + 1) / 2) % kIWarps;
     const int h = lane >> 4, hl = lane & 15;
-    for (int t0 = 2 * first; t0 < total; t0 += 2 * kIWarps) {
-      const int t = t0 + h;  // this half-warp's item
-      const unsigned m0 = __ballot_sync(0xffffffffu, incl <= t0);
-      const unsigned m1 = __ballot_sync(0xffffffffu, incl <= t0 + 1);
-      const bool active = t < total;
-      const int k = active ? __popc(h ? m1 : m0) : 0;
-      const int excl = __shfl_sync(0xffffffffu, incl - cnt, k);
-      const uint64_t bmk = __shfl_sync(0xffffffffu, (unsigned long long)bm, k);
-      const int r = t - excl;
-      const int saf = active ? fns64(bmk, 2 * r + 1) : 0;
-      const int sa = saf >= 0 ? saf : 0;
-      const int sb = active ? fns64(bmk, 2 * r + 2) : -1;
-      const int sq = sb >= 0 ? sb : sa;  // odd count: duplicate lane, masked in emission
-      uint32_t acc[4] = {0u, 0u, 0u, 0u};
-#pragma unroll 4
-      for (int s = 0; s < kTW; ++s) {
-        const uint32_t word = rows[s * (kTS / 4) + k * (PARIS_INDEX_BLOCK / 4) + hl];
-        const uint32_t qa = s_qs[sa][s], qb = s_qs[sq][s];
-        const uint32_t qx = __byte_perm(qa, qb, 0x5410);  // (q_lo16[sa], q_lo16[sb])
-        const uint32_t qy = __byte_perm(qa, qb, 0x7632);  // (-q_hi16[sa], -q_hi16[sb])
+    {
+      const int first = (warp - rot + 2 * kIWarps) % kIWarps;
+      rot = (rot + (totq + 1) / 2) % kIWarps;
+      for (int t0 = 2 * first; t0 < totq; t0 += 2 * kIWarps) {
+        const int t = t0 + h;  // this half-warp's item
+        const unsigned m0 = __ballot_sync(0xffffffffu, inq <= t0);
+        const unsigned m1 = __ballot_sync(0xffffffffu, inq <= t0 + 1);
+        const bool active = t < totq;
+        const int k = active ? __popc(h ? m1 : m0) : 0;
+        const int excl = __shfl_sync(0xffffffffu, inq - cq, k);
+        const uint64_t bmk = __shfl_sync(0xffffffffu, (unsigned long long)bm, k);
+        const int r = t - excl;
+        int sl[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          // offset = (symbol j << 8) | lane*8: bytes {lane8.b0, word.bj, 0, 0}
-          const uint32_t off = __byte_perm(word, lane8, 0x5504u | ((uint32_t)j << 4));
-          const uint2 tt = *reinterpret_cast<const uint2*>(tabc + off);
-          const uint32_t a1 = h2_fma_relu(qx, kHalf2One, tt.x);
-          const uint32_t b1 = h2_fma_relu(qy, kHalf2One, tt.y);
-          acc[j] = h2_acc_delta2(acc[j], a1, b1);
-        }
+        for (int i = 0; i < 4; ++i) sl[i] = active ? fns64(bmk, 4 * r + 1 + i) : -1;
+        lbi_item<2>(rows, tabc, lane8, s_qs, k, hl, sl, tile, nslots, s_c, a, wb, s_hist);
       }
-      const int64_t i0 = tile * kTS + k * PARIS_INDEX_BLOCK + 4 * hl;
-      const int nvalid = active ? (int)std::max<int64_t>(0, imin64(4, a.n - i0)) : 0;
-      PARIS_DCHECK(k < kBPT && sa >= 0 && sa < nslots && sb < nslots);
-      lbi_emit(acc, sa, sb, i0, nvalid, nslots, s_c, a, wb, s_hist);
+    }
+    {
+      const int first = (warp - rot + 2 * kIWarps) % kIWarps;
+      rot = (rot + (totp + 1) / 2) % kIWarps;
+      for (int t0 = 2 * first; t0 < totp; t0 += 2 * kIWarps) {
+        const int t = t0 + h;
+        const unsigned m0 = __ballot_sync(0xffffffffu, inp <= t0);
+        const unsigned m1 = __ballot_sync(0xffffffffu, inp <= t0 + 1);
+        const bool active = t < totp;
+        const int k = active ? __popc(h ? m1 : m0) : 0;
+        const uint64_t bmk = __shfl_sync(0xffffffffu, (unsigned long long)bm, k);
+        const int base = 4 * (__popcll(bmk) >> 2);  // the slots after the block's whole quads
+        int sl[2];
+        sl[0] = active ? fns64(bmk, base + 1) : -1;
+        sl[1] = active ? fns64(bmk, base + 2) : -1;
+        lbi_item<1>(rows, tabc, lane8, s_qs, k, hl, sl, tile, nslots, s_c, a, wb, s_hist);
+      }
     }
     __syncwarp();
     if (lane == 0) {
