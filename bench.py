@@ -395,15 +395,15 @@ def run_gpu(args):
             alu_src = f"derived: 148 SM x 64 FMA lanes/clk x 2 (f16x2) x {ALU_CLOCK_GHZ} GHz"
             if dom == "lb_pass" and use_index:
                 # index path: the algorithmic work is the (block, query) pairs whose envelope
-                # bound passed (stats lb_blocks: sub-blocks) x PARIS_INDEX_SUB series x w segments x 3 FMA-pipe half-ops
+                # bound passed (stats lb_blocks) x PARIS_INDEX_BLOCK series x w segments x 3 FMA-pipe half-ops
                 blocks = stats["lb_blocks"].numpy().astype(np.float64).sum()
-                ops = 3.0 * W * P.PARIS_INDEX_SUB * blocks / nbatches
+                ops = 3.0 * W * P.PARIS_INDEX_BLOCK * blocks / nbatches
                 ach = ops / (per_launch_ms / 1e3) / 1e12
                 roof = {"kernel": dom, "bound": "alu", "achieved": ach, "peak": pk,
                         "unit": "Tops/s (fp16x2 half-ops)", "frac": ach / pk,
                         "traffic": ncu_traffic(dom + "_index", args.config),
                         "algorithmic_ops_per_batch": ops, "ms_per_batch": per_launch_ms, "peak_source": alu_src,
-                        "active_subblock_frac": blocks / (nq * (n / P.PARIS_INDEX_SUB)),
+                        "active_block_frac": blocks / (nq * (n / P.PARIS_INDEX_BLOCK)),
                         "hbm_achieved_gbs": alg[dom] / (per_launch_ms / 1e3) / 1e9, "hbm_peak_gbs": peak,
                         "queries_per_pass": q_per_pass}
             elif dom == "lb_pass" and q_per_pass > 1.5:
@@ -527,9 +527,9 @@ def run_gpu(args):
                         "refined_max": float(refined.max()),
                         "pruning_ratio": float(1.0 - refined.mean() / n),
                         "tau_seed_mean": float(stats["tau_seed"].mean()),
-                        "lb_blocks_frac_p50": float(np.median(stats["lb_blocks"].numpy())) / max(1.0, n / P.PARIS_INDEX_SUB),
-                        "lb_blocks_frac_max": float(stats["lb_blocks"].numpy().max()) / max(1.0, n / P.PARIS_INDEX_SUB),
-                        "lb_blocks_frac_mean": float(stats["lb_blocks"].numpy().mean()) / max(1.0, n / P.PARIS_INDEX_SUB),
+                        "lb_blocks_frac_p50": float(np.median(stats["lb_blocks"].numpy())) / max(1.0, n / P.PARIS_INDEX_BLOCK),
+                        "lb_blocks_frac_max": float(stats["lb_blocks"].numpy().max()) / max(1.0, n / P.PARIS_INDEX_BLOCK),
+                        "lb_blocks_frac_mean": float(stats["lb_blocks"].numpy().mean()) / max(1.0, n / P.PARIS_INDEX_BLOCK),
                         "lb_blocks_top5_share": float(np.sort(stats["lb_blocks"].numpy())[-5:].sum()
                                                       / max(1, stats["lb_blocks"].numpy().sum())),
                         "refined_top5_share": float(np.sort(refined)[-5:].sum() / max(1.0, refined.sum())),

@@ -42,7 +42,6 @@ extern "C" {
 #define PARIS_MAX_K 1024
 #define PARIS_INDEX_BLOCK 64  /* series per envelope block of the index (paris_index_build) */
 #define PARIS_INDEX_TILE 2048 /* series per tile of the index's tile-major sorted SAX array   */
-#define PARIS_INDEX_SUB 16    /* series per envelope sub-block of the index (paris_index_build) */
 
 /*
  * paris_summarize -- ConvertToSAX over a whole collection (IndexBulkLoading,
@@ -112,11 +111,9 @@ int paris_knn_exact(const float* raw, const uint8_t* sax, int64_t n, const float
  *                  SoA; the last tile padded): the symbol of segment s of sorted series j
  *                  is out_sax_sorted[(j/T)*w*T + s*T + j%T] = sax[s*n + perm[j]], T = PARIS_INDEX_TILE
  *   out_perm       device [n] uint32: series id at sorted position j
- *   out_env        device [ceil(n/PARIS_INDEX_BLOCK) + n/PARIS_INDEX_SUB][2][w] uint8: per
- *                  block of PARIS_INDEX_BLOCK consecutive sorted series, the min
- *                  ([blk][0][s]) and max ([blk][1][s]) symbol of segment s (the node
- *                  envelope); then the same for every sub-block of PARIS_INDEX_SUB
- *                  series (entry ceil(n/PARIS_INDEX_BLOCK) + sub)
+ *   out_env        device [ceil(n/PARIS_INDEX_BLOCK)][2][w] uint8: per block of
+ *                  PARIS_INDEX_BLOCK consecutive sorted series, the min ([blk][0][s])
+ *                  and max ([blk][1][s]) symbol of segment s (the node envelope)
  * Requires w == 16, n % 16 == 0 (PARIS_ECONFIG otherwise).  Asynchronous on
  * `stream`; scratch (~36 bytes per series) is stream-ordered.
  */
@@ -142,7 +139,7 @@ typedef struct paris_knn_stats {
   int64_t* candidates;  /* series whose LB passed tau_seed (Alg10 list length)       */
   int64_t* refined;     /* raw series read and distance computed (Alg11 line al9:rcal) */
   float* tau_seed;      /* seed BSF distance (rooted)                                 */
-  int64_t* lb_blocks;   /* index mode: PARIS_INDEX_SUB-series sub-blocks whose envelope
+  int64_t* lb_blocks;   /* index mode: PARIS_INDEX_BLOCK-series blocks whose envelope
                            bound passed (their series' LBs were computed); 0 otherwise */
   int64_t* bsf_updates; /* paris_knn_nb: updates of the workers' private BSF copies   */
 } paris_knn_stats;
@@ -160,9 +157,8 @@ int paris_knn_exact_ex(const float* raw, const uint8_t* sax, int64_t n, const fl
  *      sorted array (the leaf it would be inserted into); the true distances of
  *      the 1024 series around it (configurable) give tau_seed;
  *   2. LBC pass over the sorted SAX array: each block's envelope MINDIST (the
- *      iSAX node bound) is computed first, then that of its sub-blocks for the
- *      queries the block can hold candidates for; only the queries a sub-block can
- *      hold candidates for are evaluated on its series;
+ *      iSAX node bound) is computed first and only the queries the block can hold
+ *      candidates for are evaluated on its series;
  *   3-4. as paris_knn_exact (candidate ids are the original series ids).
  * Requires w == 16 and n % 16 == 0.
  */
@@ -206,7 +202,7 @@ int paris_merge_topk(const float* dist, const int64_t* idx, int32_t R, int32_t n
 const char* paris_last_error(void);
 
 /* ABI version (major*100 + minor). */
-int32_t paris_version(void);  /* 104: sub-block envelopes (PARIS_INDEX_SUB) */
+int32_t paris_version(void);  /* 103: PARIS_INDEX_BLOCK 64 */
 
 /* Test hook: the library's own fp64 breakpoints cut_1..cut_{card-1} (R2) into
  * out[0..card-2] (host memory).  PARIS_ECONFIG for a bad card. */

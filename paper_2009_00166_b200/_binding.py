@@ -164,7 +164,6 @@ def summarize(raw: torch.Tensor, w: int = 16, card: int = 256, out: torch.Tensor
 
 
 PARIS_INDEX_BLOCK = 64
-PARIS_INDEX_SUB = 16
 PARIS_INDEX_TILE = 2048
 
 
@@ -173,7 +172,7 @@ class Index:
     """iSAX-ordered SAX array (paris_index_build): sorted SoA words, ids, block envelopes."""
     sax_sorted: torch.Tensor   # uint8 [ceil(n/2048)][w][2048] tile-major (include/paris.h)
     perm: torch.Tensor         # int32 [n] (uint32 ids)
-    env: torch.Tensor          # uint8 [ceil(n/64) + n/16][2][w]: block, then sub-block envelopes
+    env: torch.Tensor          # uint8 [ceil(n/64)][2][w]
     w: int
     card: int
 
@@ -185,7 +184,7 @@ def index_build(sax: torch.Tensor, w: int = 16, card: int = 256, stream=None) ->
     if sax.dtype != torch.uint8 or sax.dim() != 2 or sax.shape[0] != w:
         raise ValueError("sax must be uint8 [w][n]")
     n = sax.shape[1]
-    nblk = (n + PARIS_INDEX_BLOCK - 1) // PARIS_INDEX_BLOCK + n // PARIS_INDEX_SUB  # blocks, then sub-blocks
+    nblk = (n + PARIS_INDEX_BLOCK - 1) // PARIS_INDEX_BLOCK
     ntile = (n + PARIS_INDEX_TILE - 1) // PARIS_INDEX_TILE
     out = torch.zeros((ntile, w, PARIS_INDEX_TILE), dtype=torch.uint8, device=sax.device)
     perm = torch.empty(n, dtype=torch.int32, device=sax.device)

@@ -64,11 +64,10 @@ k_idx_aos(const uint8_t* __restrict__ sax, int64_t n, int shift, uint4* __restri
 }
 
 // sorted position j <- series perm[j]: SoA rows of the sorted array + envelopes
-// of every PARIS_INDEX_BLOCK-series block ([blk][0][s] = min symbol, [blk][1][s] =
-// max) and of every PARIS_INDEX_SUB-series sub-block (env_sub, same layout).
+// of every kIdxBlock-series block ([blk][0][s] = min symbol, [blk][1][s] = max).
 __global__ void __launch_bounds__(kIdxTile)
 k_idx_gather(const uint4* __restrict__ aos, const uint32_t* __restrict__ perm, int64_t n,
-             uint8_t* __restrict__ sax_sorted, uint8_t* __restrict__ env, uint8_t* __restrict__ env_sub) {
+             uint8_t* __restrict__ sax_sorted, uint8_t* __restrict__ env) {
   static_assert(kIdxTile % PARIS_INDEX_BLOCK == 0, "tile holds whole blocks");
   __shared__ __align__(16) uint8_t tile[kIdxW][kIdxTile];
   for (int64_t base = (int64_t)blockIdx.x * kIdxTile; base < n; base += (int64_t)gridDim.x * kIdxTile) {
@@ -105,24 +104,6 @@ k_idx_gather(const uint4* __restrict__ aos, const uint32_t* __restrict__ perm, i
         const int64_t blk = (base + j0) / PARIS_INDEX_BLOCK;
         env[(size_t)blk * 2 * kIdxW + s] = (uint8_t)mn;
         env[(size_t)blk * 2 * kIdxW + kIdxW + s] = (uint8_t)mx;
-      }
-    }
-    // sub-block envelopes (after the block entries): one thread per (sub-block, segment)
-    constexpr int kSubs = kIdxTile / PARIS_INDEX_SUB;
-    static_assert(kSubs * kIdxW == kIdxTile, "one thread per (sub-block, segment)");
-    {
-      const int sbl = threadIdx.x / kIdxW, s = threadIdx.x % kIdxW;
-      const int j0 = sbl * PARIS_INDEX_SUB;
-      if (j0 < cnt) {  // n % 16 == 0: whole sub-blocks
-        unsigned mn = 255, mx = 0;
-        for (int jj = j0; jj < j0 + PARIS_INDEX_SUB; ++jj) {
-          const unsigned c = tile[s][jj];
-          mn = min(mn, c);
-          mx = max(mx, c);
-        }
-        const int64_t sb = (base + j0) / PARIS_INDEX_SUB;
-        env_sub[(size_t)sb * 2 * kIdxW + s] = (uint8_t)mn;
-        env_sub[(size_t)sb * 2 * kIdxW + kIdxW + s] = (uint8_t)mx;
       }
     }
     __syncthreads();
@@ -187,8 +168,7 @@ int index_build_impl(const uint8_t* sax, int64_t n, int w, int card, uint8_t* ou
     e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, ids_in, out_perm, (int)n, 0, 64, st);
   }
   if (e == cudaSuccess)
-    e = PARIS_LAUNCH("index_gather", k_idx_gather, grid, kIdxTile, 0, st, aos, out_perm, n, out_sax_sorted, out_env,
-                     out_env + (size_t)((n + PARIS_INDEX_BLOCK - 1) / PARIS_INDEX_BLOCK) * 2 * kIdxW);
+    e = PARIS_LAUNCH("index_gather", k_idx_gather, grid, kIdxTile, 0, st, aos, out_perm, n, out_sax_sorted, out_env);
   if (e != cudaSuccess) rc = cuda_error(e, "paris_index_build");
   cudaFreeAsync(scratch, st);
   return rc;

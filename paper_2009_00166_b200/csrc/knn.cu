@@ -121,11 +121,6 @@ __device__ __forceinline__ uint32_t h2_fma(uint32_t a, uint32_t b, uint32_t c) {
   asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
   return d;
 }
-__device__ __forceinline__ uint32_t h2_add(uint32_t a, uint32_t b) {
-  uint32_t d;
-  asm("add.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
-  return d;
-}
 
 // acc += delta^2 for one (series, segment) of a query pair, delta = max(a, b) where
 // a = relu(q_lo - U) and b = relu(L - q_hi).  At most one of a, b is non-zero (U >= L
@@ -545,9 +540,8 @@ struct LbArgs {
   uint64_t* cand;
   int64_t cap;
   const uint32_t* perm;  // index mode: sorted position -> series id (else nullptr)
-  const uint8_t* env;    // index mode: [ceil(n/64) blocks][2][16] min/max symbols (else nullptr)
-  const uint8_t* env_sub = nullptr;  // index mode: [n/16 sub-blocks][2][16] min/max symbols
-  unsigned* blocks;      // index mode: per query, sub-blocks whose envelope bound passed
+  const uint8_t* env;    // index mode: [n/128 blocks][2][16] min/max symbols (else nullptr)
+  unsigned* blocks;      // index mode: per query, blocks whose envelope bound passed
 };
 
 struct LbConsts {
@@ -840,14 +834,7 @@ constexpr int kIThreads = 768;   // 24 warps: more warps to hide the lookup -> m
 constexpr int kIWarps = kIThreads / 32;
 constexpr int kITileIds = 512;   // tile ids staged per CTA (148 CTAs: 155 M series; beyond, global loads)
 constexpr size_t kITabEnd = kIStages * kTileBytes + (size_t)kMaxCard * 32 * 8;
-constexpr int kSPT = 2048 / PARIS_INDEX_SUB;    // index sub-blocks per tile (128)
-constexpr int kSubPB = PARIS_INDEX_BLOCK / PARIS_INDEX_SUB;  // sub-blocks per block (4)
-constexpr int kUPR = 32 / (PARIS_INDEX_SUB / 4);  // units per warp round (8: 4 lanes x 4 series each)
-constexpr size_t kIHistEnd = kITabEnd + (size_t)kMaxB * kNB * 2;            // + the 16-bit LB histograms
-constexpr size_t kIUincEnd = kIHistEnd + (size_t)kIWarps * kSPT * 2;         // + per-warp unit counts
-constexpr size_t kLbiSmem = kIUincEnd + (size_t)kMaxB * (kTW + 1) * 4;      // + the query slots' fp16 pairs
-constexpr int kSmThreads = 256;  // k_submask: 8 warps, a tile per warp step
-constexpr size_t kSmSmem = (size_t)kMaxCard * 32 * 4;  // k_submask: the 32-copy single-form region table
+constexpr size_t kLbiSmem = kITabEnd + (size_t)kMaxB * kNB * 2;  // + the 16-bit LB histograms
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -1129,20 +1116,26 @@ __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int s
   __syncwarp();
 }
 
-// Level 1 (k_blkmask), one lane per 64-series block: lane l of a warp bounds
-// block 32g + l against every query slot (region [L16[min_s], U16[max_s]] per
-// segment, in the packed fp16 pair form and error budget of the series bound);
-// bit b of bmask[blk] = the block may hold a candidate of slot b.
+// One lane per block: lane l of a warp bounds block 32*g + l against every query
+// slot (region [L[min_s], U[max_s]] per segment, outward fp32, round-down sums);
+// the 32 blocks of a warp step are one whole tile, so the warp lists it itself.
 template <int P>
 __global__ void __launch_bounds__(256)
-k_blkmask(LbArgs a, unsigned long long* __restrict__ bmask) {
+k_blkmask(LbArgs a, unsigned long long* __restrict__ bmask, unsigned* __restrict__ tile_list,
+          unsigned* __restrict__ tile_count, unsigned* __restrict__ blocks) {
+  // the envelope bound in the same packed fp16 pair form (and error budget, k_lb)
+  // as the series bound: per segment the region [L16[min], U16[max]], two query
+  // slots per instruction; a block is live for slot b iff its fp16 bound <= T16[b]
+  constexpr int NS = 2 * P;
   __shared__ uint2 s_lu16[kMaxCard];
   __shared__ uint2 s_q16[kTW * P];
   __shared__ LbConsts s_c;
+  __shared__ unsigned s_blk[kMaxB];
   const int tid = threadIdx.x, lane = tid & 31;
   for (int i = tid; i < kMaxCard; i += blockDim.x) s_lu16[i] = a.tab->lu16[i];
   for (int i = tid; i < kTW * P; i += blockDim.x) s_q16[i] = a.g_q16[i];
-  lb_consts_init(a, 2 * P, &s_c);  // ends with __syncthreads
+  if (tid < kMaxB) s_blk[tid] = 0;
+  lb_consts_init(a, NS, &s_c);  // ends with __syncthreads
   const int64_t nblocks = (a.n + PARIS_INDEX_BLOCK - 1) / PARIS_INDEX_BLOCK;
   const int64_t ntiles = (a.n + kTS - 1) / kTS;
   static_assert(kBPT == 32, "a warp step bounds the 32 blocks of one tile");
@@ -1173,126 +1166,21 @@ k_blkmask(LbArgs a, unsigned long long* __restrict__ bmask) {
       for (int p = 0; p < P; ++p) bm |= (uint64_t)h2_le_bits(acc[p], s_c.T16[p]) << (2 * p);
     }
     bmask[blk] = bm;  // padded to whole tiles
-  }
-}
-
-// Level 2 (k_submask), a warp per tile: every (block, slot pair p) with a live
-// slot is an item; the warp takes 4 items per round, 8 lanes per item = the
-// block's 4 sub-blocks x 2 halves of the segments (the partial sums meet in one
-// fp16 add: at most 9 roundings per term, inside the w + 4 of the budget), from
-// the tile's sub-block envelopes staged in shared memory.  A live (sub-block,
-// slot) sets its bit in the sub-block's 64-bit mask; the tile's 128 masks are
-// written once, and the tile is listed when any is non-zero.  A sub-block's
-// symbol ranges lie inside its block's, so this bound is the tighter of the two.
-template <int P>
-__global__ void __launch_bounds__(kSmThreads)
-k_submask(LbArgs a, const unsigned long long* __restrict__ bmask, unsigned long long* __restrict__ submask,
-          unsigned* __restrict__ tile_list, unsigned* __restrict__ tile_count) {
-  constexpr int NW = kSmThreads / 32;
-  extern __shared__ uint32_t s_tab[];  // [kMaxCard * 32] half2(-U16, L16), 32 copies (lane-private)
-  __shared__ uint2 s_q16[kTW * P];
-  __shared__ LbConsts s_c;
-  __shared__ unsigned s_sub[kMaxB];
-  __shared__ __align__(16) uint8_t s_env[NW][kSPT][2 * kTW];   // per warp: the tile's sub-block envelopes
-  __shared__ __align__(16) unsigned long long s_msk[NW][kSPT];  // per warp: the tile's sub-block masks
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < kMaxCard * 32; i += blockDim.x) s_tab[i] = a.tab->lu16p[i >> 5];
-  for (int i = tid; i < kTW * P; i += blockDim.x) s_q16[i] = a.g_q16[i];
-  for (int i = tid; i < kMaxB; i += blockDim.x) s_sub[i] = 0;
-  lb_consts_init(a, 2 * P, &s_c);  // ends with __syncthreads
-  const uint32_t* tabl = s_tab + lane;
-  const int64_t nsub = a.n / PARIS_INDEX_SUB;  // n % 16 == 0
-  const int64_t ntiles = (a.n + kTS - 1) / kTS;
-  static_assert(kSubPB == 4, "4 sub-blocks per block");
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + tid) >> 5, GW = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  uint8_t (*env)[2 * kTW] = s_env[warp];
-  unsigned long long* msk = s_msk[warp];
-  const int gi = lane >> 3, g4 = (lane >> 1) & 3, hh = lane & 1;
-  for (int64_t g = gw; g < ntiles; g += GW) {
-    const int64_t blk = 32 * g + lane;
-    const uint64_t bm = bmask[blk];
-    // the block's live pairs (static pairs p = slots 2p, 2p+1)
-    uint32_t pm = 0;
+    const unsigned live = __ballot_sync(0xffffffffu, bm != 0ull);
+    if (lane == 0 && live) tile_list[atomicAdd(tile_count, 1u)] = (unsigned)g;
 #pragma unroll
-    for (int p = 0; p < P; ++p) pm |= ((bm >> (2 * p)) & 3ull) ? (1u << p) : 0u;
-    // stage the block's 4 sub-block envelopes (128 B) and clear their masks
-#pragma unroll
-    for (int j = 0; j < kSubPB; ++j) {
-      const int64_t sb = blk * kSubPB + j;
-      uint4 lo = make_uint4(0u, 0u, 0u, 0u), hi = lo;
-      if (pm && sb < nsub) {
-        lo = __ldg(reinterpret_cast<const uint4*>(a.env_sub + (size_t)sb * 32));
-        hi = __ldg(reinterpret_cast<const uint4*>(a.env_sub + (size_t)sb * 32 + 16));
-      }
-      *reinterpret_cast<uint4*>(env[kSubPB * lane + j]) = lo;
-      *reinterpret_cast<uint4*>(env[kSubPB * lane + j] + kTW) = hi;
-      msk[kSubPB * lane + j] = 0ull;
+    for (int b = 0; b < NS; ++b) {
+      const unsigned m = __ballot_sync(0xffffffffu, (bm >> b) & 1u);
+      if (lane == 0 && m) atomicAdd(&s_blk[b], (unsigned)__popc(m));
     }
-    const int cnt = __popc(pm);
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    __syncwarp();
-    for (int t0 = 0; t0 < total; t0 += 4) {
-      const int t = t0 + gi;
-      const unsigned m0 = __ballot_sync(0xffffffffu, incl <= t0), m1 = __ballot_sync(0xffffffffu, incl <= t0 + 1);
-      const unsigned m2 = __ballot_sync(0xffffffffu, incl <= t0 + 2), m3 = __ballot_sync(0xffffffffu, incl <= t0 + 3);
-      const bool active = t < total;
-      const int k = __popc(gi == 0 ? m0 : gi == 1 ? m1 : gi == 2 ? m2 : m3) & 31;
-      const int excl = __shfl_sync(0xffffffffu, incl - cnt, k);
-      const uint32_t pmk = __shfl_sync(0xffffffffu, pm, k);
-      const uint64_t bmk = __shfl_sync(0xffffffffu, (unsigned long long)bm, k);
-      const int pf = active ? (int)__fns(pmk, 0, t - excl + 1) : 0;
-      const int p = (pf >= 0 && pf < P) ? pf : 0;
-      const uint32_t live2 = active ? (uint32_t)(bmk >> (2 * p)) & 3u : 0u;
-      const int sbl = kSubPB * k + g4;
-      const uint2 mnv = *reinterpret_cast<const uint2*>(env[sbl] + 8 * hh);
-      const uint2 mxv = *reinterpret_cast<const uint2*>(env[sbl] + kTW + 8 * hh);
-      uint32_t acc = 0u;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint32_t mnj = ((j < 4 ? mnv.x : mnv.y) >> (8 * (j & 3))) & 0xFFu;
-        const uint32_t mxj = ((j < 4 ? mxv.x : mxv.y) >> (8 * (j & 3))) & 0xFFu;
-        const uint2 q = s_q16[(8 * hh + j) * P + p];
-        const uint32_t tx = __byte_perm(tabl[32 * mxj], 0, 0x1010), ty = __byte_perm(tabl[32 * mnj], 0, 0x3232);
-        acc = h2_acc_delta2(acc, h2_fma_relu(q.x, kHalf2One, tx), h2_fma_relu(q.y, kHalf2One, ty));
-      }
-      acc = h2_add(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
-      const uint32_t bits = h2_le_bits(acc, s_c.T16[p]) & live2;
-      if (hh == 0 && bits) {
-        atomicOr(&msk[sbl], (unsigned long long)bits << (2 * p));
-        if (bits & 1u) atomicAdd(&s_sub[2 * p], 1u);
-        if (bits & 2u) atomicAdd(&s_sub[2 * p + 1], 1u);
-      }
-    }
-    __syncwarp();
-    bool any = false;
-#pragma unroll
-    for (int j = 0; j < kSubPB; ++j) {
-      const unsigned long long v = msk[kSubPB * lane + j];
-      submask[(size_t)g * kSPT + kSubPB * lane + j] = v;  // padded to whole tiles
-      any |= v != 0ull;
-    }
-    if (__ballot_sync(0xffffffffu, any) && lane == 0) tile_list[atomicAdd(tile_count, 1u)] = (unsigned)g;
-    __syncwarp();
   }
   __syncthreads();
-  for (int i = tid; i < 2 * P; i += blockDim.x)
-    if (s_sub[i]) atomicAdd(&a.blocks[i], s_sub[i]);
+  if (tid < NS && s_blk[tid]) atomicAdd(&blocks[tid], s_blk[tid]);
 }
 
-// Level 3 (k_lbi): the TMA ring streams the listed tiles (32 KB of SAX + the 128
-// sub-block masks, on one barrier); the live (sub-block, slot pair) units of a
-// tile -- consecutive live slots of a sub-block, two at a time -- are dealt
-// round-robin to the warps, 8 units per warp round (4 lanes x 4 series per unit).
-// Every warp derives the same unit list from the masks (no CTA barrier).
 template <int P>
 __global__ void __launch_bounds__(kIThreads, 1)
-k_lbi(LbArgs a, const unsigned long long* __restrict__ submask, const unsigned* __restrict__ tile_list,
+k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __restrict__ tile_list,
       const unsigned* __restrict__ tile_count) {
   extern __shared__ __align__(128) uint8_t dsm[];
   uint8_t* s_tiles = dsm;
@@ -1302,16 +1190,16 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ submask, const unsigned* 
   // and the 16 lanes of each half hit distinct banks
   uint2* s_tab = reinterpret_cast<uint2*>(dsm + kIStages * kTileBytes);
   unsigned* s_hist = reinterpret_cast<unsigned*>(dsm + kITabEnd);  // [kMaxB][kNB] 16-bit (hist16_add)
-  uint16_t (*s_uinc)[kSPT] = reinterpret_cast<uint16_t (*)[kSPT]>(dsm + kIHistEnd);  // per warp: unit counts
-  uint32_t (*s_qs)[kTW + 1] = reinterpret_cast<uint32_t (*)[kTW + 1]>(dsm + kIUincEnd);  // +1: banks
   __shared__ __align__(8) uint64_t s_full[kIStages];
   __shared__ unsigned s_cnt[kIStages];
-  // per stage: the tile's id and its sub-block masks, delivered with the tile
-  __shared__ __align__(16) unsigned long long s_sm[kIStages][kSPT];
+  // per stage: the tile's id and its 32 block masks, delivered with the tile (the
+  // warps never wait on a global load at a tile boundary)
+  __shared__ __align__(16) unsigned long long s_bm[kIStages][kBPT];
   __shared__ int64_t s_tile[kIStages];
   // this CTA's share of the tile list (entries blockIdx.x + i * gridDim.x), staged once:
   // a refill then starts its TMA without a dependent global load
   __shared__ unsigned s_tl[kITileIds];
+  __shared__ uint32_t s_qs[2 * P][kTW];  // per slot and segment: half2(q_lo16, -q_hi16)
   __shared__ LbConsts s_c;
   __shared__ WarpBuf s_wb[kIWarps];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1322,18 +1210,18 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ submask, const unsigned* 
   if (lane == 0) wb.n = 0;
   for (int i = tid; i < nslots * kNB / 2; i += kIThreads) s_hist[i] = 0;
 
-  static_assert(kTS == PARIS_INDEX_TILE && kSPT == 128, "index tiles are the LB kernel's tiles");
+  static_assert(kTS == PARIS_INDEX_TILE, "index tiles are the LB kernel's tiles");
   auto issue = [&](int64_t li, int st) {
     // tile-major sorted SAX: the tile's 16 rows are one contiguous 32 KB range; its
-    // sub-block masks (1 KB) ride on the same barrier; the id is published before
-    // the arrive (release), so waiters that see the phase flip see it too
+    // block masks (128 B) ride on the same barrier; the id is published before the
+    // arrive (release), so waiters that see the phase flip see it too
     const int64_t i = (li - blockIdx.x) / gridDim.x;
     const int64_t tile = i < kITileIds ? s_tl[i] : tile_list[li];
     s_tile[st] = tile;
-    mbar_expect_tx(&s_full[st], (unsigned)(kTileBytes + kSPT * 8));
+    mbar_expect_tx(&s_full[st], (unsigned)(kTileBytes + kBPT * 8));
     bulk_g2s(s_tiles + (size_t)st * kTileBytes, a.sax + (size_t)tile * kTileBytes, (unsigned)kTileBytes,
              &s_full[st]);
-    bulk_g2s(&s_sm[st][0], submask + (size_t)tile * kSPT, (unsigned)(kSPT * 8), &s_full[st]);
+    bulk_g2s(&s_bm[st][0], bmask + (size_t)tile * kBPT, (unsigned)(kBPT * 8), &s_full[st]);
   };
   if (tid == 0) {
     for (int st = 0; st < kIStages; ++st) {
@@ -1363,8 +1251,6 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ submask, const unsigned* 
   lb_consts_init(a, nslots, &s_c);  // ends with __syncthreads
   const char* tabc = reinterpret_cast<const char*>(s_tab);
   const uint32_t lane8 = (uint32_t)lane * 8u;  // < 256: byte 0 of the table offset
-  const int grp = lane >> 2, gl = lane & 3;    // unit slot of this lane in a round, lane within the unit
-  uint16_t* uinc = s_uinc[warp];
   int rot = 0;
 
   for (int64_t it = 0;; ++it) {
@@ -1374,50 +1260,40 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ submask, const unsigned* 
     mbar_wait(&s_full[st], (unsigned)((it / kIStages) & 1));
     const int64_t tile = s_tile[st];
     PARIS_DCHECK(tile >= 0 && tile * kTS < a.n);
-    // unit counts: lane l owns sub-blocks 4l..4l+3
-    int c4[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) c4[j] = (__popcll(s_sm[st][4 * lane + j]) + 1) >> 1;
-    const int own = c4[0] + c4[1] + c4[2] + c4[3];
-    int incl = own;
+    // the tile's 32 block masks (lane = block); a block's live slots are computed two
+    // at a time (consecutive live slots form an item); a 64-series block is half a
+    // warp, so a warp takes two items per round (lanes 0-15 and 16-31); items are
+    // dealt round-robin, rotating, so no warp is systematically behind
+    const uint64_t bm = s_bm[st][lane];
+    const int cnt = (__popcll(bm) + 1) >> 1;
+    int incl = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int v = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += v;
     }
     const int total = __shfl_sync(0xffffffffu, incl, 31);
-    {
-      const int e = incl - own;
-      uinc[4 * lane] = (uint16_t)(e + c4[0]);
-      uinc[4 * lane + 1] = (uint16_t)(e + c4[0] + c4[1]);
-      uinc[4 * lane + 2] = (uint16_t)(e + c4[0] + c4[1] + c4[2]);
-      uinc[4 * lane + 3] = (uint16_t)incl;
-    }
-    __syncwarp();
     const uint32_t* rows = reinterpret_cast<const uint32_t*>(s_tiles + (size_t)st * kTileBytes);
     const int first = (warp - rot + 2 * kIWarps) % kIWarps;
-    rot = (rot + (total + kUPR - 1) / kUPR) % kIWarps;
-    for (int t0 = kUPR * first; t0 < total; t0 += kUPR * kIWarps) {
-      const int t = t0 + grp;  // this lane group's unit
+    rot = (rot + (total + 1) / 2) % kIWarps;
+    const int h = lane >> 4, hl = lane & 15;
+    for (int t0 = 2 * first; t0 < total; t0 += 2 * kIWarps) {
+      const int t = t0 + h;  // this half-warp's item
+      const unsigned m0 = __ballot_sync(0xffffffffu, incl <= t0);
+      const unsigned m1 = __ballot_sync(0xffffffffu, incl <= t0 + 1);
       const bool active = t < total;
-      // sub-block of unit t: the number of sub-blocks whose inclusive count is <= t
-      int k = 0;
-#pragma unroll
-      for (int stp = kSPT / 2; stp > 0; stp >>= 1)
-        if ((int)uinc[k + stp - 1] <= t) k += stp;
-      k = active ? k : 0;
-      const int excl = k ? (int)uinc[k - 1] : 0;
-      const uint64_t smk = s_sm[st][k];
+      const int k = active ? __popc(h ? m1 : m0) : 0;
+      const int excl = __shfl_sync(0xffffffffu, incl - cnt, k);
+      const uint64_t bmk = __shfl_sync(0xffffffffu, (unsigned long long)bm, k);
       const int r = t - excl;
-      const int saf = active ? fns64(smk, 2 * r + 1) : 0;
+      const int saf = active ? fns64(bmk, 2 * r + 1) : 0;
       const int sa = saf >= 0 ? saf : 0;
-      const int sb = active ? fns64(smk, 2 * r + 2) : -1;
+      const int sb = active ? fns64(bmk, 2 * r + 2) : -1;
       const int sq = sb >= 0 ? sb : sa;  // odd count: duplicate lane, masked in emission
       uint32_t acc[4] = {0u, 0u, 0u, 0u};
-      const uint32_t* rw = rows + k * (PARIS_INDEX_SUB / 4) + gl;
 #pragma unroll 4
       for (int s = 0; s < kTW; ++s) {
-        const uint32_t word = rw[s * (kTS / 4)];
+        const uint32_t word = rows[s * (kTS / 4) + k * (PARIS_INDEX_BLOCK / 4) + hl];
         const uint32_t qa = s_qs[sa][s], qb = s_qs[sq][s];
         const uint32_t qx = __byte_perm(qa, qb, 0x5410);  // (q_lo16[sa], q_lo16[sb])
         const uint32_t qy = __byte_perm(qa, qb, 0x7632);  // (-q_hi16[sa], -q_hi16[sb])
@@ -1431,9 +1307,9 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ submask, const unsigned* 
           acc[j] = h2_acc_delta2(acc[j], a1, b1);
         }
       }
-      const int64_t i0 = tile * kTS + k * PARIS_INDEX_SUB + 4 * gl;
+      const int64_t i0 = tile * kTS + k * PARIS_INDEX_BLOCK + 4 * hl;
       const int nvalid = active ? (int)std::max<int64_t>(0, imin64(4, a.n - i0)) : 0;
-      PARIS_DCHECK(k < kSPT && sa >= 0 && sa < nslots && sb < nslots);
+      PARIS_DCHECK(k < kBPT && sa >= 0 && sa < nslots && sb < nslots);
       lbi_emit(acc, sa, sb, i0, nvalid, nslots, s_c, a, wb, s_hist);
     }
     __syncwarp();
@@ -2253,8 +2129,7 @@ struct Ws {
   unsigned* blocks;      // index mode: blocks whose envelope bound passed, per query
   unsigned* tile_count;  // index mode: live tiles listed
   unsigned* updates;     // nb mode: V_bsf updates per query
-  unsigned long long* bmask;    // index mode: [ntiles*32] per-block live query-slot masks
-  unsigned long long* submask;  // index mode: [ntiles*128] per-sub-block live query-slot masks
+  unsigned long long* bmask;  // index mode: [ntiles*32] per-block live query-slot masks
   unsigned* tile_list;   // index mode: live tiles
   unsigned* tile_flag;   // index mode: [ntiles] tile already listed (zeroed per batch)
   size_t flag_bytes;
@@ -2367,8 +2242,6 @@ cudaError_t launch_index_lb(const Plan& p, const uint8_t* sax, int nb, const Car
   if (attr_dev != dev) {
     cudaError_t e = cudaFuncSetAttribute(k_lbi<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLbiSmem);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_submask<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmSmem);
-    if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
   LbArgs la;
@@ -2376,18 +2249,13 @@ cudaError_t launch_index_lb(const Plan& p, const uint8_t* sax, int nb, const Car
   la.g_q = ws.g_q; la.g_q16 = ws.g_q16; la.nb = nb; la.thr = ws.thr_seed; la.count = ws.count;
   la.hist = ws.hist; la.cand = ws.cand; la.cap = cap; la.perm = p.perm; la.env = p.env;
   la.blocks = ws.blocks;
-  la.env_sub = p.env + (size_t)((p.n + PARIS_INDEX_BLOCK - 1) / PARIS_INDEX_BLOCK) * 2 * kTW;
   const int64_t ntiles = (p.n + kTS - 1) / kTS;
   const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms() * 8, (ntiles + 7) / 8));
-  cudaError_t e = PARIS_LAUNCH("lb_blocks", k_blkmask<P>, bgrid, 256, 0, st, la, ws.bmask);
-  if (e != cudaSuccess) return e;
-  const int sgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms() * 2, (ntiles + 7) / 8));
-  e = PARIS_LAUNCH("lb_subblocks", k_submask<P>, sgrid, kSmThreads, kSmSmem, st, la, ws.bmask, ws.submask,
-                   ws.tile_list, ws.tile_count);
+  cudaError_t e = PARIS_LAUNCH("lb_blocks", k_blkmask<P>, bgrid, 256, 0, st, la, ws.bmask, ws.tile_list,
+                               ws.tile_count, ws.blocks);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(sms(), ntiles);
-  return PARIS_LAUNCH("lb_pass", k_lbi<P>, grid, kIThreads, kLbiSmem, st, la, ws.submask, ws.tile_list,
-                      ws.tile_count);
+  return PARIS_LAUNCH("lb_pass", k_lbi<P>, grid, kIThreads, kLbiSmem, st, la, ws.bmask, ws.tile_list, ws.tile_count);
 }
 
 cudaError_t dispatch_index_lb(int nb, const Plan& p, const uint8_t* sax, const CardTables* tab, const Ws& ws,
@@ -2500,7 +2368,6 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   const size_t o_lists = take(p.k > 1 ? sizeof(uint64_t) * B * (size_t)p.XB * p.k : 8);
   const int64_t ntiles = (p.n + kTS - 1) / kTS;
   const size_t o_bmask = take(p.perm ? sizeof(unsigned long long) * (size_t)ntiles * kBPT : 8);
-  const size_t o_smask = take(p.perm ? sizeof(unsigned long long) * (size_t)ntiles * kSPT : 8);
   const size_t o_tlist = take(p.perm ? sizeof(unsigned) * (size_t)ntiles : 8);
   const size_t o_tflag = take(p.perm ? sizeof(unsigned) * (size_t)ntiles : 8);
   void* base = nullptr;
@@ -2532,7 +2399,6 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   ws.sorted = (uint64_t*)(c + o_sorted);
   ws.lists = (uint64_t*)(c + o_lists);
   ws.bmask = (unsigned long long*)(c + o_bmask);
-  ws.submask = (unsigned long long*)(c + o_smask);
   ws.tile_list = (unsigned*)(c + o_tlist);
   ws.tile_flag = (unsigned*)(c + o_tflag);
   ws.flag_bytes = p.perm ? sizeof(unsigned) * (size_t)ntiles : 0;
