@@ -334,6 +334,142 @@ k_summarize_tma(const float* __restrict__ raw, int64_t n, int w, int card, int G
   }
 }
 
+// Segment-per-lane variant of the TMA-tiled kernel (w = 16, len = 64 F): the
+// same 64 KB tile ring, but a half-warp owns a series and lane l its segment l --
+// the segment's 4F points are summed in registers (no shuffles; the same
+// pairwise tree, depth 2 + log2 F, as the xor-shuffle form, so the same rounding
+// bound), and each lane quantizes one segment (no lane repeats another's lookup).
+// Lane l reads float4 #((c + l / (8/F)) mod F) of its segment at step c: the 8
+// lanes of each shared-memory phase then cover all 32 banks (segments are 16F
+// bytes apart).
+template <int F>
+__global__ void __launch_bounds__(kSumThreads, 1)
+k_summarize_seg(const float* __restrict__ raw, int64_t n, int card, uint8_t* __restrict__ sax, int64_t ld,
+                const CardTables* __restrict__ tab) {
+  constexpr int w = 16, len = 64 * F, seglen = 4 * F;
+  constexpr int TS = kSumTileBytes / (4 * len);  // series per tile
+  constexpr int SPW = TS / kSumWarps;             // series per warp per tile (2 halves x SPW/2)
+  static_assert(SPW % 2 == 0 && SPW >= 2 && SPW <= 4, "tile shape");
+  constexpr int SPH = SPW / 2;                    // series per half-warp
+  extern __shared__ __align__(128) uint8_t dsm[];
+  float* s_tiles = reinterpret_cast<float*>(dsm);
+  uint2* s_lut = reinterpret_cast<uint2*>(dsm + (size_t)kSumStages * kSumTileBytes);
+  __shared__ double s_cd[kMaxCard];
+  __shared__ __align__(8) uint64_t s_full[kSumStages];
+  __shared__ unsigned s_cnt[kSumStages];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int hf = lane >> 4, hl = lane & 15;
+  const int64_t ntiles = (n + TS - 1) / TS;
+
+  auto issue = [&](int64_t tile, int st) {
+    const int64_t base = tile * TS;
+    const unsigned bytes = (unsigned)(imin64(TS, n - base) * len * 4);
+    mbar_expect_tx(&s_full[st], bytes);
+    bulk_g2s(s_tiles + (size_t)st * (kSumTileBytes / 4), raw + (size_t)base * len, bytes, &s_full[st]);
+  };
+  if (tid == 0) {
+    for (int st = 0; st < kSumStages; ++st) {
+      mbar_init(&s_full[st], 1);
+      s_cnt[st] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int st = 0; st < kSumStages; ++st) {
+      const int64_t tile = blockIdx.x + (int64_t)st * gridDim.x;
+      if (tile < ntiles) issue(tile, st);
+    }
+  }
+  for (int i = tid; i < kLutN; i += kSumThreads) s_lut[i] = tab->lut[i];
+  for (int i = tid; i < kMaxCard; i += kSumThreads) s_cd[i] = tab->cuts_d[i];
+  __syncthreads();
+
+  constexpr float inv_seglen = 1.0f / (float)seglen;
+  const int top = card >> 1;
+  constexpr int depth = 2 + (F == 1 ? 0 : F == 2 ? 1 : F == 4 ? 2 : 3);
+  const float err_scale = (float)(depth + 1) * 5.9604645e-08f * inv_seglen * 1.001f;
+  constexpr int rdiv = 8 / F;  // lanes per rotation step
+
+  for (int64_t it = 0;; ++it) {
+    const int64_t tile = blockIdx.x + it * gridDim.x;
+    if (tile >= ntiles) break;
+    const int st = (int)(it % kSumStages);
+    mbar_wait(&s_full[st], (unsigned)((it / kSumStages) & 1));
+    const int64_t base = tile * TS + warp * SPW;  // series base of this warp
+    const int cnt = (int)std::max<int64_t>(0, imin64(SPW, n - base));
+    const float4* tl = reinterpret_cast<const float4*>(s_tiles + (size_t)st * (kSumTileBytes / 4));
+    float4 v[SPH][F];
+#pragma unroll
+    for (int u = 0; u < SPH; ++u) {
+      const int sl = warp * SPW + 2 * u + hf;  // series within the tile: halves interleave
+      const float4* sp = tl + (size_t)sl * (len / 4) + hl * F;
+#pragma unroll
+      for (int c = 0; c < F; ++c)  // register c holds float4 #r (the sum tree is order-free in its bound)
+        v[u][c] = (2 * u + hf < cnt) ? sp[(c + hl / rdiv) & (F - 1)] : make_float4(0, 0, 0, 0);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (atomicAdd(&s_cnt[st], 1u) == kSumWarps - 1) {
+        s_cnt[st] = 0;
+        const int64_t next = tile + (int64_t)kSumStages * gridDim.x;
+        if (next < ntiles) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(next, st);
+        }
+      }
+    }
+    uint32_t packed = 0;  // symbols of this lane's segment for the warp's SPW series (byte 2u + hf)
+#pragma unroll
+    for (int u = 0; u < SPH; ++u) {
+      float part[F], apart[F];
+#pragma unroll
+      for (int c = 0; c < F; ++c) {
+        const float4 x = v[u][c];
+        part[c] = (x.x + x.y) + (x.z + x.w);
+        apart[c] = (fabsf(x.x) + fabsf(x.y)) + (fabsf(x.z) + fabsf(x.w));
+      }
+#pragma unroll
+      for (int o = 1; o < F; o <<= 1)
+#pragma unroll
+        for (int c = 0; c < F; c += 2 * o) {
+          part[c] += part[c + o];
+          apart[c] += apart[c + o];
+        }
+      const float paa = part[0] * inv_seglen;
+      int k = __float2int_rd((paa + kLutLo) * kLutScale);
+      k = min(max(k, 0), kLutN - 1);
+      const uint2 e = s_lut[k];
+      const float cut = __uint_as_float(e.x);
+      int sym = (int)e.y + (paa >= cut ? 1 : 0);
+      const bool amb = fabsf(paa - cut) <= apart[0] * err_scale + fabsf(cut) * 1.2e-7f + 1e-30f;
+      if (__any_sync(0xffffffffu, amb) && amb) {
+        // exact path: the fp64 segment sum and the fp64 cuts
+        double d = 0.0;
+#pragma unroll
+        for (int c = 0; c < F; ++c) {
+          const float4 x = v[u][c];
+          d += ((double)x.x + (double)x.y) + ((double)x.z + (double)x.w);
+        }
+        sym = upper_bound_pow2(s_cd, d / (double)seglen, top);
+      }
+      packed |= (uint32_t)sym << (8 * (2 * u + hf));
+    }
+    // lane hl of the first half stores segment hl's SPW symbols (both halves' bytes)
+    packed |= __shfl_down_sync(0xffffffffu, packed, 16);
+    if (hf == 0 && cnt > 0) {
+      uint8_t* dst = sax + (size_t)hl * ld + base;
+      if (cnt == SPW) {
+        if (SPW == 4) *reinterpret_cast<uint32_t*>(dst) = packed;
+        else *reinterpret_cast<uint16_t*>(dst) = (uint16_t)packed;
+      } else {
+        for (int u = 0; u < cnt; ++u) dst[u] = (uint8_t)(packed >> (8 * u));
+      }
+    }
+    (void)w;
+  }
+}
+
 // Generic fallback (any len % w == 0): one thread per series, fp64 segment sums
 // (sequential), fp64 binary search.  Correct for every supported shape; used
 // only when the fast path's shape conditions do not hold.
@@ -392,10 +528,24 @@ static int summarize_device(const float* raw, int64_t n, int len, int w, int car
       PARIS_CHECK_LAUNCH(e, "summarize smem attribute");
       attr_dev[ai] = dev;
     }
-    switch (len) {
-      case 128: e = PARIS_LAUNCH("summarize", k_summarize_tma<1>, grid, kSumThreads, kSumSmem, st, raw, n, w, card, G, out_sax, ld, tab); break;
-      case 256: e = PARIS_LAUNCH("summarize", k_summarize_tma<2>, grid, kSumThreads, kSumSmem, st, raw, n, w, card, G, out_sax, ld, tab); break;
-      default: e = PARIS_LAUNCH("summarize", k_summarize_tma<4>, grid, kSumThreads, kSumSmem, st, raw, n, w, card, G, out_sax, ld, tab); break;
+    if (w == 16 && len <= 256 && !getenv("PARIS_SUMMARIZE_SHFL")) {  // segment per lane (env: A/B of the shuffle form)
+      static int seg_dev[3] = {-1, -1, -1};
+      if (seg_dev[ai] != dev) {
+        e = (len == 128) ? cudaFuncSetAttribute(k_summarize_seg<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSumSmem)
+                         : cudaFuncSetAttribute(k_summarize_seg<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSumSmem);
+        PARIS_CHECK_LAUNCH(e, "summarize smem attribute");
+        seg_dev[ai] = dev;
+      }
+      switch (len) {
+        case 128: e = PARIS_LAUNCH("summarize", k_summarize_seg<2>, grid, kSumThreads, kSumSmem, st, raw, n, card, out_sax, ld, tab); break;
+        default: e = PARIS_LAUNCH("summarize", k_summarize_seg<4>, grid, kSumThreads, kSumSmem, st, raw, n, card, out_sax, ld, tab); break;
+      }
+    } else {
+      switch (len) {
+        case 128: e = PARIS_LAUNCH("summarize", k_summarize_tma<1>, grid, kSumThreads, kSumSmem, st, raw, n, w, card, G, out_sax, ld, tab); break;
+        case 256: e = PARIS_LAUNCH("summarize", k_summarize_tma<2>, grid, kSumThreads, kSumSmem, st, raw, n, w, card, G, out_sax, ld, tab); break;
+        default: e = PARIS_LAUNCH("summarize", k_summarize_tma<4>, grid, kSumThreads, kSumSmem, st, raw, n, w, card, G, out_sax, ld, tab); break;
+      }
     }
     PARIS_CHECK_LAUNCH(e, "summarize launch");
   } else if (fast) {
