@@ -13,6 +13,9 @@ $CMD > gpurun_out/ev/ncu_plain.json 2> gpurun_out/ev/ncu_plain.log && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/ev/launches_c4.csv $CMD > gpurun_out/ev/ncu_launch.log 2>&1
 echo "rc=$?" >> gpurun_out/ev/ncu_launch.log
 ncu --set full --clock-control none --import-source on -k regex:k_lbi -s 1 -c 1 -o gpurun_out/ev/full_c4_k_lbi -f $CMD > gpurun_out/ev/ncu_full_lbi.log 2>&1; echo "rc=$?" >> gpurun_out/ev/ncu_full_lbi.log
-ncu --set full --clock-control none --import-source on -k regex:k_refine1 -s 2 -c 1 -o gpurun_out/ev/full_c4_k_refine1 -f $CMD > gpurun_out/ev/ncu_full_ref.log 2>&1; echo "rc=$?" >> gpurun_out/ev/ncu_full_ref.log
-ncu --set full --clock-control none --import-source on -k regex:k_summarize_tma -s 1 -c 1 -o gpurun_out/ev/full_c4_k_summarize -f $CMD > gpurun_out/ev/ncu_full_sum.log 2>&1; echo "rc=$?" >> gpurun_out/ev/ncu_full_sum.log
+ncu --set full --clock-control none --import-source on -k regex:k_refine1u -s 3 -c 1 -o gpurun_out/ev/full_c4_k_refine1 -f $CMD > gpurun_out/ev/ncu_full_ref.log 2>&1; echo "rc=$?" >> gpurun_out/ev/ncu_full_ref.log
+ncu --set full --clock-control none --import-source on -k regex:k_summarize_seg -s 1 -c 1 -o gpurun_out/ev/full_c4_k_summarize -f $CMD > gpurun_out/ev/ncu_full_sum.log 2>&1; echo "rc=$?" >> gpurun_out/ev/ncu_full_sum.log
+ncu --set full --clock-control none --import-source on -k regex:k_blkmask -s 1 -c 1 -o gpurun_out/ev/full_c4_k_blkmask -f $CMD > gpurun_out/ev/ncu_full_blk.log 2>&1; echo "rc=$?" >> gpurun_out/ev/ncu_full_blk.log
+CMDF="python bench.py --steps 2 --warmup 3 --no-cpu --no-b1 --both 0 --path flat"
+ncu --set full --clock-control none --import-source on -k regex:k_lbt -s 1 -c 1 -o gpurun_out/ev/full_c4_k_lbt -f $CMDF > gpurun_out/ev/ncu_full_lbt.log 2>&1; echo "rc=$?" >> gpurun_out/ev/ncu_full_lbt.log
 exit 0
