@@ -1142,36 +1142,76 @@ k_blkmask(LbArgs a, unsigned long long* __restrict__ bmask, unsigned* __restrict
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + tid) >> 5, GW = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t g = gw; g < ntiles; g += GW) {
     const int64_t blk = 32 * g + lane;
-    uint64_t bm = 0;
-    if (blk < nblocks) {
-      const uint4 mn = __ldg(reinterpret_cast<const uint4*>(a.env + (size_t)blk * 32));
-      const uint4 mx = __ldg(reinterpret_cast<const uint4*>(a.env + (size_t)blk * 32 + 16));
-      const uint32_t mnw[4] = {mn.x, mn.y, mn.z, mn.w}, mxw[4] = {mx.x, mx.y, mx.z, mx.w};
-      uint32_t acc[P];
+    const bool valid = blk < nblocks;
+    uint4 mn = make_uint4(~0u, ~0u, ~0u, ~0u), mx = make_uint4(0u, 0u, 0u, 0u);  // neutral for padding
+    if (valid) {
+      mn = __ldg(reinterpret_cast<const uint4*>(a.env + (size_t)blk * 32));
+      mx = __ldg(reinterpret_cast<const uint4*>(a.env + (size_t)blk * 32 + 16));
+    }
+    // the tile's envelope (byte-wise min / max over its 32 blocks) bounds every block
+    // of the tile: lane p bounds slot pair p on it, and only the pairs it leaves live
+    // are evaluated per block (at C4 about a third of the pairs)
+    uint4 tn = mn, tx4 = mx;
 #pragma unroll
-      for (int p = 0; p < P; ++p) acc[p] = 0u;
-#pragma unroll 4
-      for (int seg = 0; seg < kTW; ++seg) {
+    for (int o = 16; o > 0; o >>= 1) {
+      tn.x = __vminu4(tn.x, __shfl_xor_sync(0xffffffffu, tn.x, o));
+      tn.y = __vminu4(tn.y, __shfl_xor_sync(0xffffffffu, tn.y, o));
+      tn.z = __vminu4(tn.z, __shfl_xor_sync(0xffffffffu, tn.z, o));
+      tn.w = __vminu4(tn.w, __shfl_xor_sync(0xffffffffu, tn.w, o));
+      tx4.x = __vmaxu4(tx4.x, __shfl_xor_sync(0xffffffffu, tx4.x, o));
+      tx4.y = __vmaxu4(tx4.y, __shfl_xor_sync(0xffffffffu, tx4.y, o));
+      tx4.z = __vmaxu4(tx4.z, __shfl_xor_sync(0xffffffffu, tx4.z, o));
+      tx4.w = __vmaxu4(tx4.w, __shfl_xor_sync(0xffffffffu, tx4.w, o));
+    }
+    unsigned tp;
+    {
+      const uint32_t tnw[4] = {tn.x, tn.y, tn.z, tn.w}, txw[4] = {tx4.x, tx4.y, tx4.z, tx4.w};
+      const int pl = lane < P ? lane : 0;
+      uint32_t tacc = 0u;
+#pragma unroll
+      for (int seg = 0; seg < kTW; ++seg) {  // fully unrolled: register-indexed words
+        const uint32_t tx = s_lu16[(txw[seg >> 2] >> (8 * (seg & 3))) & 0xFFu].x;
+        const uint32_t ty = s_lu16[(tnw[seg >> 2] >> (8 * (seg & 3))) & 0xFFu].y;
+        const uint2 q = s_q16[seg * P + pl];
+        tacc = h2_acc_delta2(tacc, h2_fma_relu(q.x, kHalf2One, tx), h2_fma_relu(q.y, kHalf2One, ty));
+      }
+      tp = __ballot_sync(0xffffffffu, lane < P && h2_le_bits(tacc, s_c.T16[pl]) != 0u);
+    }
+    uint64_t bm = 0;
+    const uint32_t mnw[4] = {mn.x, mn.y, mn.z, mn.w}, mxw[4] = {mx.x, mx.y, mx.z, mx.w};
+    for (unsigned rem = tp; rem;) {  // the live pairs, 4 at a time (tp is warp-uniform)
+      int pp[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        pp[i] = rem ? __ffs(rem) - 1 : -1;
+        rem &= rem - 1;
+      }
+      uint32_t acc[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int seg = 0; seg < kTW; ++seg) {  // fully unrolled: register-indexed words
         const uint32_t tx = s_lu16[(mxw[seg >> 2] >> (8 * (seg & 3))) & 0xFFu].x;  // -U16 of the max symbol
         const uint32_t ty = s_lu16[(mnw[seg >> 2] >> (8 * (seg & 3))) & 0xFFu].y;  // L16 of the min symbol
 #pragma unroll
-        for (int p = 0; p < P; ++p) {
-          const uint2 q = s_q16[seg * P + p];
+        for (int i = 0; i < 4; ++i) {
+          const uint2 q = s_q16[seg * P + (pp[i] >= 0 ? pp[i] : 0)];
           const uint32_t a1 = h2_fma_relu(q.x, kHalf2One, tx);
           const uint32_t b1 = h2_fma_relu(q.y, kHalf2One, ty);
-          acc[p] = h2_acc_delta2(acc[p], a1, b1);
+          acc[i] = h2_acc_delta2(acc[i], a1, b1);
         }
       }
 #pragma unroll
-      for (int p = 0; p < P; ++p) bm |= (uint64_t)h2_le_bits(acc[p], s_c.T16[p]) << (2 * p);
+      for (int i = 0; i < 4; ++i)
+        if (pp[i] >= 0 && valid) bm |= (uint64_t)h2_le_bits(acc[i], s_c.T16[pp[i]]) << (2 * pp[i]);
     }
     bmask[blk] = bm;  // padded to whole tiles
     const unsigned live = __ballot_sync(0xffffffffu, bm != 0ull);
     if (lane == 0 && live) tile_list[atomicAdd(tile_count, 1u)] = (unsigned)g;
-#pragma unroll
-    for (int b = 0; b < NS; ++b) {
-      const unsigned m = __ballot_sync(0xffffffffu, (bm >> b) & 1u);
-      if (lane == 0 && m) atomicAdd(&s_blk[b], (unsigned)__popc(m));
+    for (unsigned r = live ? tp : 0u; r; r &= r - 1) {  // per-slot block counts (stats), live pairs only
+      const int p = __ffs(r) - 1;
+      const unsigned m0 = __ballot_sync(0xffffffffu, (bm >> (2 * p)) & 1ull);
+      const unsigned m1 = __ballot_sync(0xffffffffu, (bm >> (2 * p + 1)) & 1ull);
+      if (lane == 0 && m0) atomicAdd(&s_blk[2 * p], (unsigned)__popc(m0));
+      if (lane == 0 && m1) atomicAdd(&s_blk[2 * p + 1], (unsigned)__popc(m1));
     }
   }
   __syncthreads();
