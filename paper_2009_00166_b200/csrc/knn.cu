@@ -833,8 +833,12 @@ constexpr int kIStages = 2;      // compute-bound on the live items: a tile's lo
 constexpr int kIThreads = 768;   // 24 warps: more warps to hide the lookup -> math latency chain
 constexpr int kIWarps = kIThreads / 32;
 constexpr int kITileIds = 512;   // tile ids staged per CTA (148 CTAs: 155 M series; beyond, global loads)
-constexpr size_t kITabEnd = kIStages * kTileBytes + (size_t)kMaxCard * 32 * 8;
-constexpr size_t kLbiSmem = kITabEnd + (size_t)kMaxB * kNB * 2;  // + the 16-bit LB histograms
+// k_lbi dynamic shared memory: [ring][pad][table: 64 KB at a 64 KB-aligned shared
+// address][16-bit LB histograms]; the pad depends on where the dynamic region
+// starts (after the static arrays), so the launch requests what the static size
+// leaves and the kernel checks the layout fits (kLbiSmem below, set at launch).
+constexpr size_t kITabBytes = (size_t)kMaxCard * 32 * 8;
+constexpr size_t kIHistBytes = (size_t)kMaxB * kNB * 2;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -847,9 +851,16 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
                : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+  asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+// 8-byte shared-memory load at a 32-bit shared address (base + offset folds into
+// one LDS [R + UR] when the base is uniform).
+__device__ __forceinline__ uint2 lds_u2(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
@@ -1224,12 +1235,23 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
       const unsigned* __restrict__ tile_count) {
   extern __shared__ __align__(128) uint8_t dsm[];
   uint8_t* s_tiles = dsm;
+  // the table at the first 64 KB-aligned shared address past the ring, so one byte
+  // permute builds a lookup's full address: {lane*8, symbol, table address bits 16-31}
+  const uint32_t dsm_s = smem_u32(dsm);
+  const uint32_t ring_end = dsm_s + (uint32_t)(kIStages * kTileBytes);
+  const uint32_t tab_s = (ring_end + 0xFFFFu) & ~0xFFFFu;
+  const uint32_t tab_off = tab_s - dsm_s;
+  {
+    uint32_t dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    if ((size_t)tab_off + kITabBytes + kIHistBytes > dyn) __trap();  // launch config inconsistent with the layout
+  }
   // region table in pair form {(-U16,-U16), (L16,L16)}, 32 copies: entry c of lane l
   // at byte 256c + 8l, so ONE byte permute forms the address (symbol byte -> bits
   // 8..15, lane*8 -> bits 0..7; no multiply); a 64-bit load is served per half-warp
   // and the 16 lanes of each half hit distinct banks
-  uint2* s_tab = reinterpret_cast<uint2*>(dsm + kIStages * kTileBytes);
-  unsigned* s_hist = reinterpret_cast<unsigned*>(dsm + kITabEnd);  // [kMaxB][kNB] 16-bit (hist16_add)
+  uint2* s_tab = reinterpret_cast<uint2*>(dsm + tab_off);
+  unsigned* s_hist = reinterpret_cast<unsigned*>(dsm + tab_off + kITabBytes);  // [kMaxB][kNB] 16-bit (hist16_add)
   __shared__ __align__(8) uint64_t s_full[kIStages];
   __shared__ unsigned s_cnt[kIStages];
   // per stage: the tile's id and its 32 block masks, delivered with the tile (the
@@ -1289,8 +1311,7 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
     s_qs[b][sg] = half_of(v.x, b & 1) | (half_of(v.y, b & 1) << 16);
   }
   lb_consts_init(a, nslots, &s_c);  // ends with __syncthreads
-  const char* tabc = reinterpret_cast<const char*>(s_tab);
-  const uint32_t lane8 = (uint32_t)lane * 8u;  // < 256: byte 0 of the table offset
+  const uint32_t lanebase = tab_s | ((uint32_t)lane * 8u);  // bytes {lane*8, 0, table bits 16-31}
   int rot = 0;
 
   for (int64_t it = 0;; ++it) {
@@ -1339,9 +1360,8 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
         const uint32_t qy = __byte_perm(qa, qb, 0x7632);  // (-q_hi16[sa], -q_hi16[sb])
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          // offset = (symbol j << 8) | lane*8: bytes {lane8.b0, word.bj, 0, 0}
-          const uint32_t off = __byte_perm(word, lane8, 0x5504u | ((uint32_t)j << 4));
-          const uint2 tt = *reinterpret_cast<const uint2*>(tabc + off);
+          // address = {lanebase.b0, word.bj, lanebase.b2, lanebase.b3}
+          const uint2 tt = lds_u2(__byte_perm(word, lanebase, 0x7604u | ((uint32_t)j << 4)));
           const uint32_t a1 = h2_fma_relu(qx, kHalf2One, tt.x);
           const uint32_t b1 = h2_fma_relu(qy, kHalf2One, tt.y);
           acc[j] = h2_acc_delta2(acc[j], a1, b1);
@@ -2274,13 +2294,25 @@ cudaError_t launch_lbt(const Plan& p, const uint8_t* sax, int nb, const CardTabl
 }
 
 template <int P>
+size_t& lbi_smem() {  // dynamic shared memory of k_lbi<P> (set once per device)
+  static size_t v = 0;
+  return v;
+}
+
+template <int P>
 cudaError_t launch_index_lb(const Plan& p, const uint8_t* sax, int nb, const CardTables* tab, const Ws& ws,
                             cudaStream_t st, int64_t cap) {
   static int attr_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(k_lbi<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLbiSmem);
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, k_lbi<P>);
+    if (e != cudaSuccess) return e;
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    lbi_smem<P>() = (size_t)optin - fa.sharedSizeBytes;
+    e = cudaFuncSetAttribute(k_lbi<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lbi_smem<P>());
     if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
@@ -2295,7 +2327,8 @@ cudaError_t launch_index_lb(const Plan& p, const uint8_t* sax, int nb, const Car
                                ws.tile_count, ws.blocks);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(sms(), ntiles);
-  return PARIS_LAUNCH("lb_pass", k_lbi<P>, grid, kIThreads, kLbiSmem, st, la, ws.bmask, ws.tile_list, ws.tile_count);
+  return PARIS_LAUNCH("lb_pass", k_lbi<P>, grid, kIThreads, lbi_smem<P>(), st, la, ws.bmask, ws.tile_list,
+                      ws.tile_count);
 }
 
 cudaError_t dispatch_index_lb(int nb, const Plan& p, const uint8_t* sax, const CardTables* tab, const Ws& ws,
