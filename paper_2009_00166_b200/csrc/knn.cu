@@ -1066,13 +1066,6 @@ k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
 // Candidate emission of one index item: 4 series x 2 query slots (sa = low half,
 // sb = high half, sb < 0: none).  Same tests and warp buffer as lb_emit_wb.
 __device__ __forceinline__ uint32_t half_of(uint32_t v, int h) { return (v >> (16 * h)) & 0xFFFFu; }
-// Position of the n-th (1-based) set bit of a 64-bit mask, -1 if it has fewer.
-__device__ __forceinline__ int fns64(uint64_t m, int n) {
-  const uint32_t lo = (uint32_t)m, hi = (uint32_t)(m >> 32);
-  const int cl = __popc(lo);
-  const int r = n <= cl ? (int)__fns(lo, 0, n) : (n - cl <= __popc(hi) ? 32 + (int)__fns(hi, 0, n - cl) : -1);
-  return (r >= 0 && r < 64) ? r : -1;
-}
 
 __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int sb, int64_t i0, int nvalid,
                                          int nslots, const LbConsts& c, const LbArgs& a, WarpBuf& wb,
@@ -1082,16 +1075,23 @@ __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int s
                       ((sb >= 0 ? half_of(c.T16[sb >> 1], sb & 1) : (uint32_t)kHalfNeg1) << 16);
   uint32_t pm = 0;  // bit 2j+h: series j passes for slot h
   float lbv[4][2];
-  if (nvalid > 0) {
+  // the packed fp16 test first (almost every item fails it everywhere); the fp32
+  // bounds only where some lane of the warp passed it
+  uint32_t pf = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) pf |= h2_le_bits(acc[j], Tp) << (2 * j);
+  if (nvalid < 4) pf &= (1u << (2 * nvalid)) - 1u;
+  if (sb < 0) pf &= 0x55u;
+  if (!__any_sync(0xffffffffu, pf != 0u)) return;
+  if (pf) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const uint32_t pb = h2_le_bits(acc[j], Tp);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int sl = h ? sb : sa;
         const float hv = h ? h_hi_f(acc[j]) : h_lo_f(acc[j]);
         lbv[j][h] = __fmul_rd(fmaxf(__fsub_rd(hv, c.wabs), 0.f), c.lbconv);
-        if (((pb >> h) & 1u) && sl >= 0 && j < nvalid && lbv[j][h] <= c.thr[sl]) pm |= 1u << (2 * j + h);
+        if (((pf >> (2 * j + h)) & 1u) && lbv[j][h] <= c.thr[sl]) pm |= 1u << (2 * j + h);
       }
     }
   }
@@ -1349,10 +1349,15 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
       const int k = active ? __popc(h ? m1 : m0) : 0;
       const int excl = __shfl_sync(0xffffffffu, incl - cnt, k);
       const uint64_t bmk = __shfl_sync(0xffffffffu, (unsigned long long)bm, k);
-      const int r = t - excl;
-      const int saf = active ? fns64(bmk, 2 * r + 1) : 0;
-      const int sa = saf >= 0 ? saf : 0;
-      const int sb = active ? fns64(bmk, 2 * r + 2) : -1;
+      // slots 2r+1 and 2r+2 (1-based) of the block's live set: clear the first 2r bits
+      uint64_t m = active ? bmk : 0ull;
+      for (int i = t - excl; i > 0; --i) {
+        m &= m - 1;
+        m &= m - 1;
+      }
+      const int sa = m ? __ffsll((long long)m) - 1 : 0;
+      m &= m - 1;
+      const int sb = (active && m) ? __ffsll((long long)m) - 1 : -1;
       const int sq = sb >= 0 ? sb : sa;  // odd count: duplicate lane, masked in emission
       uint32_t acc[4] = {0u, 0u, 0u, 0u};
 #pragma unroll 4
