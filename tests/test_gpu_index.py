@@ -133,3 +133,20 @@ def test_knn_index_overflow_rescan(P):
                                  config=P.KnnConfig(index_seeds=1), stats=True)
         ri, rd2 = oracle.knn_bruteforce(x, q, k)
         check_knn(x, q, gi.cpu().numpy(), gd.cpu().numpy(), ri, rd2)
+
+
+@pytest.mark.parametrize("card,length,k", [(64, 256, 1), (16, 256, 3), (256, 128, 1), (8, 128, 5)])
+def test_knn_index_cardinalities_and_lengths(P, card, length, k):
+    """The index path at every supported shape the LB tables take: cardinalities below 256
+    (symbols scaled to 8 bits in the key; region tables of the smaller card) and len 128."""
+    import torch
+    n, nq = 30_000, 70
+    x = datagen.random_walks(n, length, 600 + card + length)
+    q = datagen.random_walks(nq, length, 601 + card)
+    q[:5] = x[[0, 7, 29_999, 15_000, 123]]
+    xd = torch.from_numpy(x).cuda()
+    sax = P.summarize(xd, 16, card)
+    idx = P.index_build(sax, 16, card)
+    gi, gd = P.knn_index(xd, idx, torch.from_numpy(q).cuda(), k=k)
+    ri, rd2 = oracle.knn_bruteforce(x, q, k)
+    check_knn(x, q, gi.cpu().numpy(), gd.cpu().numpy(), ri, rd2)
