@@ -1105,9 +1105,12 @@ __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int s
   }
   const int total = __shfl_sync(0xffffffffu, incl, 31);
   if (wb.n + total > kWB) wb_flush<true>(wb, nslots, c, a, s_hist);
+  // (static bit loops: lbv stays in registers)
   if (total > kWB) {  // degenerate (e.g. tau = inf): straight to global memory
-    for (uint32_t r = pm; r; r &= r - 1) {
-      const int bit = __ffs(r) - 1, j = bit >> 1, sl = (bit & 1) ? sb : sa;
+#pragma unroll
+    for (int bit = 0; bit < 8; ++bit) {
+      if (!((pm >> bit) & 1u)) continue;
+      const int j = bit >> 1, sl = (bit & 1) ? sb : sa;
       const unsigned pos = atomicAdd(&a.count[sl], 1u);
       if ((int64_t)pos < a.cap) {
         a.cand[(size_t)sl * a.cap + pos] = make_key(lbv[j][bit & 1], __ldg(a.perm + i0 + j));
@@ -1117,8 +1120,10 @@ __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int s
     return;
   }
   int pos = wb.n + incl - cntl;
-  for (uint32_t r = pm; r; r &= r - 1) {
-    const int bit = __ffs(r) - 1, j = bit >> 1, sl = (bit & 1) ? sb : sa;
+#pragma unroll
+  for (int bit = 0; bit < 8; ++bit) {
+    if (!((pm >> bit) & 1u)) continue;
+    const int j = bit >> 1, sl = (bit & 1) ? sb : sa;
     PARIS_DCHECK(i0 + j < a.n && pos < kWB && sl >= 0);
     wb.key[pos] = make_key(lbv[j][bit & 1], __ldg(a.perm + i0 + j));
     wb.slot[pos] = (uint8_t)sl;
