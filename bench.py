@@ -240,6 +240,15 @@ def run_gpu(args):
     torch.cuda.synchronize()
     log(f"rank {rank}: generated n={n} len={length} nq={nq} in {time.time() - t0:.1f}s")
     h2d_gbs = None
+    # the bf16 copy of raw for the index path's refinement pre-filter (paris_raw_bf16), built once
+    raw16, raw16_ms = None, None
+    if not args.no_raw16 and (args.path == "index" or args.both):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        raw16 = P.raw_bf16(raw)
+        e1.record()
+        torch.cuda.synchronize()
+        raw16_ms = e0.elapsed_time(e1)
     if args.raw_host:
         # f3: the raw collection lives in pinned host memory (not in HBM); summarize streams
         # it through the double-buffered H2D pipeline, the refinement reads candidates' rows
@@ -306,7 +315,7 @@ def run_gpu(args):
 
         def knn(qsrc, **kw):
             if use_index:
-                return P.knn_index(raw, index, qsrc, k=k, **kw)
+                return P.knn_index(raw, index, qsrc, k=k, raw16=raw16, **kw)
             if use_nb:
                 return P.knn_nb(raw, sax, qsrc, w=W, card=CARD, **kw)
             return P.knn_exact(raw, sax, qsrc, k=k, w=W, card=CARD, **kw)
@@ -506,7 +515,8 @@ def run_gpu(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded Philox random walks, z-normalized; no dataset on the box)",
             "config": {"workload": cfg["desc"], "n": n, "len": length, "w": W, "card": CARD, "nq": nq, "k": k,
-                       "batch": primary["batch"], "path": args.path, "index_build_ms": index_ms, "parallelism": f"weak x{ws} (independent collections + queries per GPU)",
+                       "batch": primary["batch"], "path": args.path, "index_build_ms": index_ms,
+                       "raw_bf16": None if raw16 is None else {"build_ms": raw16_ms, "bytes": raw16.numel() * 2}, "parallelism": f"weak x{ws} (independent collections + queries per GPU)",
                        "l2": "inputs larger than L2 (no flush)",
                        "raw": "pinned host memory (f3)" if args.raw_host else "HBM"},
             "roofline": roof,
@@ -643,6 +653,8 @@ def main():
     ap.add_argument("--no-b1", action="store_true", help="skip the batch-1 LB roofline measurement")
     ap.add_argument("--sorted-refine", action="store_true",
                     help="k = 1: refine bucket-sorted lists (K5 scatter) instead of the unsorted waves (A/B)")
+    ap.add_argument("--no-raw16", action="store_true",
+                    help="index path without the bf16 refinement pre-filter (paris_knn_index_ex)")
     ap.add_argument("--raw-host", action="store_true",
                     help="f3: keep the raw collection in pinned host memory (SAX/index in HBM)")
     ap.add_argument("--ref-sample", type=int, default=2_000_000)

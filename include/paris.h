@@ -172,6 +172,29 @@ int paris_knn_index_ex(const float* raw, const uint8_t* sax_sorted, const uint32
                        const paris_knn_config* config, paris_knn_stats* stats);
 
 /*
+ * paris_raw_bf16 -- a bf16 copy of the raw collection for the refinement pre-filter
+ * of paris_knn_index_x (a B200 addition, not in the paper):
+ *   raw  device [n][len] fp32, out device [n][len] bf16 bits (round to nearest even),
+ *   caller-allocated (2*n*len bytes); both 16-byte aligned, len % 8 == 0.
+ * Asynchronous on `stream`.
+ */
+int paris_raw_bf16(const float* raw, int64_t n, int32_t len, uint16_t* out, void* stream);
+
+/*
+ * paris_knn_index_x -- paris_knn_index_ex with the bf16 pre-filter: for k = 1 the
+ * refinement first bounds each candidate's true distance from below with its bf16
+ * row (half the bytes): ED(q, x) >= ED(q, x~) - rho ||x~||, rho = 2^-8 (1 + 2^-7),
+ * with fp32 error margins and directed roundings; a candidate whose bound exceeds
+ * the live BSF is dropped without reading its fp32 row (same exact results).
+ *   raw_bf16  device [n][len] bf16 (paris_raw_bf16 of `raw`), 16-byte aligned,
+ *             len % 8 == 0; NULL = paris_knn_index_ex.  k > 1 ignores it.
+ */
+int paris_knn_index_x(const float* raw, const uint16_t* raw_bf16, const uint8_t* sax_sorted, const uint32_t* perm,
+                      const uint8_t* env, int64_t n, const float* queries, int32_t nq, int32_t k, int64_t* out_idx,
+                      float* out_dist, int32_t len, int32_t w, int32_t card, void* stream,
+                      const paris_knn_config* config, paris_knn_stats* stats);
+
+/*
  * paris_knn_nb -- exact 1-NN with nb-ParIS+ (Alg7-Alg8,
  * P:1158-1246): the same seed as paris_knn_exact (approximate search analog),
  * then SAX is split into contiguous parts, one per DistComp worker (a warp);
@@ -202,7 +225,7 @@ int paris_merge_topk(const float* dist, const int64_t* idx, int32_t R, int32_t n
 const char* paris_last_error(void);
 
 /* ABI version (major*100 + minor). */
-int32_t paris_version(void);  /* 103: PARIS_INDEX_BLOCK 64 */
+int32_t paris_version(void);  /* 104: paris_raw_bf16, paris_knn_index_x */
 
 /* Test hook: the library's own fp64 breakpoints cut_1..cut_{card-1} (R2) into
  * out[0..card-2] (host memory).  PARIS_ECONFIG for a bad card. */

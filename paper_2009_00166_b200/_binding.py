@@ -84,6 +84,11 @@ def load():
         lib.paris_knn_index_ex.argtypes = [P, P, P, P, i64, P, i32, i32, P, P, i32, i32, i32, P,
                                            ctypes.POINTER(_Config), ctypes.POINTER(_Stats)]
         lib.paris_knn_index_ex.restype = ctypes.c_int
+        lib.paris_knn_index_x.argtypes = [P, P, P, P, P, i64, P, i32, i32, P, P, i32, i32, i32, P,
+                                          ctypes.POINTER(_Config), ctypes.POINTER(_Stats)]
+        lib.paris_knn_index_x.restype = ctypes.c_int
+        lib.paris_raw_bf16.argtypes = [P, i64, i32, P, P]
+        lib.paris_raw_bf16.restype = ctypes.c_int
         lib.paris_knn_index.argtypes = [P, P, P, P, i64, P, i32, i32, P, P, i32, i32, i32, P]
         lib.paris_knn_index.restype = ctypes.c_int
         lib.paris_knn_nb.argtypes = [P, P, i64, P, i32, P, P, i32, i32, i32, P, ctypes.POINTER(_Config),
@@ -194,12 +199,24 @@ def index_build(sax: torch.Tensor, w: int = 16, card: int = 256, stream=None) ->
     return Index(out, perm, env, w, card)
 
 
+def raw_bf16(raw: torch.Tensor, stream=None) -> torch.Tensor:
+    """bf16 copy of raw ([n][len] fp32, CUDA) for the refinement pre-filter (paris_raw_bf16)."""
+    lib = load()
+    _need_cuda(raw, "raw")
+    if raw.dtype != torch.float32 or raw.dim() != 2:
+        raise ValueError("raw must be [n][len] float32")
+    out = torch.empty(raw.shape, dtype=torch.int16, device=raw.device)  # bf16 bits
+    _check(lib.paris_raw_bf16(raw.data_ptr(), raw.shape[0], raw.shape[1], out.data_ptr(), _stream(stream)))
+    return out
+
+
 def knn_index(raw: torch.Tensor, index: Index, queries: torch.Tensor, k: int = 1,
               out_idx: torch.Tensor | None = None, out_dist: torch.Tensor | None = None, stream=None,
-              config: KnnConfig | None = None, stats: bool = False):
-    """Exact k-NN over an Index (paris_knn_index); same results as knn_exact."""
+              config: KnnConfig | None = None, stats: bool = False, raw16: torch.Tensor | None = None):
+    """Exact k-NN over an Index (paris_knn_index); same results as knn_exact.  raw16: the
+    bf16 copy of raw (raw_bf16) -> the refinement pre-filter (paris_knn_index_x)."""
     return knn_exact(raw, index.sax_sorted, queries, k=k, w=index.w, card=index.card, out_idx=out_idx,
-                     out_dist=out_dist, stream=stream, config=config, stats=stats, _index=index)
+                     out_dist=out_dist, stream=stream, config=config, stats=stats, _index=index, _raw16=raw16)
 
 
 def knn_nb(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, w: int = 16, card: int = 256,
@@ -214,7 +231,7 @@ def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: in
               w: int = 16, card: int = 256, out_idx: torch.Tensor | None = None,
               out_dist: torch.Tensor | None = None, stream=None,
               config: KnnConfig | None = None, stats: bool = False, _index: Index | None = None,
-              _nb: bool = False):
+              _nb: bool = False, _raw16: torch.Tensor | None = None):
     """Exact k-NN of every query (rows of `queries`, CUDA or host) over raw/sax.
 
     sax (and the index) are CUDA tensors; raw is CUDA or pinned host memory (the
@@ -273,6 +290,14 @@ def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: in
                                     out_idx.data_ptr(), out_dist.data_ptr(), length, w, card,
                                     _stream(stream), ctypes.byref(cfg) if cfg else None,
                                     ctypes.byref(st) if st else None)
+    elif _raw16 is not None:
+        _need_cuda(_raw16, "raw16")
+        if _raw16.shape != raw.shape or _raw16.element_size() != 2:
+            raise ValueError("raw16 must be the [n][len] 16-bit copy of raw (raw_bf16)")
+        rc = lib.paris_knn_index_x(raw.data_ptr(), _raw16.data_ptr(), sax.data_ptr(), _index.perm.data_ptr(),
+                                   _index.env.data_ptr(), n, queries.data_ptr(), nq, k, out_idx.data_ptr(),
+                                   out_dist.data_ptr(), length, w, card, _stream(stream),
+                                   ctypes.byref(cfg) if cfg else None, ctypes.byref(st) if st else None)
     else:
         rc = lib.paris_knn_index_ex(raw.data_ptr(), sax.data_ptr(), _index.perm.data_ptr(), _index.env.data_ptr(),
                                     n, queries.data_ptr(), nq, k, out_idx.data_ptr(), out_dist.data_ptr(),

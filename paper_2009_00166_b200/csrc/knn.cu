@@ -1727,6 +1727,7 @@ struct RefineArgs {
   float d2up;                // 1 + bound on the relative error of an fp32 d^2 (rounding up)
   unsigned lo, hi;           // k = 1: refine list positions [lo, min(hi, count)) (a wave)
   int64_t n;                 // series in raw (debug bounds checks)
+  const uint16_t* raw16 = nullptr;  // optional bf16 copy of raw [n][len] (paris_raw_bf16): pre-filter
 };
 
 // One warp step: up to kU candidates (indices i0 + u*stride) against the live
@@ -1797,6 +1798,64 @@ __device__ __forceinline__ bool refine_step(const RefineArgs& a, const uint64_t*
   return stop;
 }
 
+// bf16 pre-filter (optional, a.raw16): a row's bf16 copy x~ (half the bytes)
+// gives a rigorous lower bound on the true distance before the fp32 row is read:
+// round-to-nearest bf16 keeps |x_i - x~_i| <= rho |x~_i|, rho = 2^-8 (1 + 2^-7), so
+// ED(x, x~) <= rho ||x~|| and ED(q, x) >= ED(q, x~) - rho ||x~||.  Both sums are
+// fp32 (relative error <= e = (len/32 + 8) 2^-24, the d^2 bound of refine_group),
+// taken with directed roundings: L = sqrt(s (1 - 2e)) - rho sqrt(n2 (1 + 2e)).  A
+// candidate with L^2 > thr (the live BSF threshold) cannot beat the BSF and is
+// dropped without its fp32 row; the rest are refined exactly as before.
+template <int NC, int U>
+__device__ __forceinline__ void bf16_prefilter(const RefineArgs& a, const float4* __restrict__ qv,
+                                               const uint64_t (&key)[U], bool (&live)[U], float thr) {
+  constexpr int NH = (NC + 1) / 2;  // uint4 (8 bf16) per lane
+  const int lane = threadIdx.x & 31;
+  const int nh = a.len >> 3;
+  uint4 h[U][NH];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int c = 0; c < NH; ++c) {
+      const int f = lane + 32 * c;
+      h[u][c] = (live[u] && f < nh)
+                    ? __ldg(reinterpret_cast<const uint4*>(a.raw16 + (size_t)key_id(key[u]) * a.len) + f)
+                    : make_uint4(0u, 0u, 0u, 0u);
+    }
+  float s2[U], n2[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) s2[u] = n2[u] = 0.f;
+#pragma unroll
+  for (int c = 0; c < NH; ++c) {
+    const int f = lane + 32 * c;
+    const float4 q0 = f < nh ? __ldg(qv + 2 * f) : make_float4(0, 0, 0, 0);
+    const float4 q1 = f < nh ? __ldg(qv + 2 * f + 1) : make_float4(0, 0, 0, 0);
+    const float qq[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t w4[4] = {h[u][c].x, h[u][c].y, h[u][c].z, h[u][c].w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float x = __uint_as_float((e & 1) ? (w4[e >> 1] & 0xFFFF0000u) : (w4[e >> 1] << 16));
+        const float d = x - qq[e];
+        s2[u] = fmaf(d, d, s2[u]);
+        n2[u] = fmaf(x, x, n2[u]);
+      }
+    }
+  }
+  const float e2 = 2.f * (float)((a.len >> 5) + 8) * 5.9604644775390625e-08f;
+  constexpr float rho = 0.00392150878906250f;  // 2^-8 (1 + 2^-7), rounded up
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    if (!__any_sync(0xffffffffu, live[u])) continue;
+    const float s = warp_sum(s2[u]), nn = warp_sum(n2[u]);
+    // (1e-30: the absolute error of bf16 subnormals, below any relative bound)
+    const float lo = __fsub_rd(__fsub_rd(__fsqrt_rd(__fmul_rd(s, 1.f - e2)),
+                                         __fmul_ru(rho, __fsqrt_ru(__fmul_ru(nn, 1.f + e2)))), 1e-30f);
+    if (live[u] && lo > 0.f && __fmul_rd(lo, lo) > thr) live[u] = false;
+  }
+}
+
 // Refine up to U candidates of one query (k = 1): load the live rows whole
 // (lane l: float4 #(l + 32c)), accumulate the squared distance with early abandoning
 // after each 128-point chunk (north_star), lower the BSF (64-bit
@@ -1807,9 +1866,16 @@ __device__ __forceinline__ void refine_group(const RefineArgs& a, const float4* 
                                              uint64_t& cur, unsigned long long* bp, unsigned& nref) {
   const int lane = threadIdx.x & 31;
   const int nf = a.len >> 2;
-  float4 x[U][NC];
 #pragma unroll
   for (int u = 0; u < U; ++u) PARIS_DCHECK(!live[u] || key_id(key[u]) < (uint64_t)a.n);
+  if (a.raw16) {
+    bf16_prefilter<NC, U>(a, qv, key, live, thr);
+    bool any = false;
+#pragma unroll
+    for (int u = 0; u < U; ++u) any |= live[u];
+    if (!any) return;
+  }
+  float4 x[U][NC];
 #pragma unroll
   for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -2231,6 +2297,7 @@ struct Plan {
   int idx_seeds;         // index mode: series around the query's leaf
   bool nb;               // f2: nb-ParIS+ (per-worker BSF copies, fused LB -> refine)
   bool sorted_refine = false;  // k = 1: walk bucket-sorted lists (K5) instead of the unsorted waves
+  const uint16_t* raw16 = nullptr;  // optional bf16 copy of raw: refine pre-filter (k = 1)
 };
 
 int pairs_for(int nb) { return nb <= 2 ? 1 : nb <= 4 ? 2 : nb <= 8 ? 4 : nb <= 16 ? 8 : nb <= 32 ? 16 : 32; }
@@ -2573,6 +2640,7 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
   ra.count = ws.count; ra.thr_seed = ws.thr_seed; ra.thr = ws.thr; ra.best = ws.best;
   ra.refined = ws.refined; ra.lists = ws.lists; ra.k = p.k; ra.d2up = p.d2up;
   ra.lo = 0; ra.hi = 0xFFFFFFFFu; ra.n = p.n;
+  ra.raw16 = p.k == 1 ? p.raw16 : nullptr;
   dim3 g((unsigned)p.XB, (unsigned)nb);
   if (p.k == 1) {
     cudaError_t e1 = cudaSuccess;
@@ -2680,7 +2748,7 @@ void plan_refine(Plan& p) {
 int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queries, int nq, int k,
              int64_t* out_idx, float* out_dist, int len, int w, int card, cudaStream_t st,
              const paris_knn_config* cfg, paris_knn_stats* stats, const uint32_t* perm = nullptr,
-             const uint8_t* env = nullptr, bool nb_mode = false) {
+             const uint8_t* env = nullptr, bool nb_mode = false, const uint16_t* raw16 = nullptr) {
   if (nb_mode && (k != 1 || w != kTW || n % 4 != 0)) {
     set_error("paris_knn_nb: needs k == 1, w == 16, n %% 4 == 0 (k=%d, w=%d, n=%lld)", k, w, (long long)n);
     return k != 1 ? PARIS_EINVAL : PARIS_ECONFIG;
@@ -2756,6 +2824,13 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   // index seeds: 1024 series around the leaf by default; 64 when raw is in host memory,
   // where every seed is a PCIe read (measured: C5 62.7 K q/s with 64 vs 29 K with 1024)
   p.sorted_refine = cfg && cfg->reserved[1] == 1;
+  if (raw16) {
+    if ((len % 8) || is_host_ptr(raw16) || (reinterpret_cast<uintptr_t>(raw16) & 15)) {
+      set_error("paris_knn_index_x: raw_bf16 must be 16-byte aligned device memory and len %% 8 == 0");
+      return PARIS_EINVAL;
+    }
+    p.raw16 = raw16;
+  }
   p.idx_seeds = (cfg && cfg->reserved[2] > 0) ? cfg->reserved[2] : (raw_host ? kIdxSeedsHost : 0);
   plan_seed(p, (cfg && cfg->seed_div > 0) ? cfg->seed_div : 16);
   p.cap = nb_mode ? 1 : std::min<int64_t>(n, std::max<int64_t>(65536, n / 32));
@@ -2903,6 +2978,14 @@ int paris_knn_index_ex(const float* raw, const uint8_t* sax_sorted, const uint32
                        const paris_knn_config* config, paris_knn_stats* stats) {
   return paris::knn_impl(raw, sax_sorted, n, queries, nq, k, out_idx, out_dist, len, w, card,
                          (cudaStream_t)stream, config, stats, perm, env);
+}
+
+int paris_knn_index_x(const float* raw, const uint16_t* raw_bf16, const uint8_t* sax_sorted, const uint32_t* perm,
+                      const uint8_t* env, int64_t n, const float* queries, int32_t nq, int32_t k, int64_t* out_idx,
+                      float* out_dist, int32_t len, int32_t w, int32_t card, void* stream,
+                      const paris_knn_config* config, paris_knn_stats* stats) {
+  return paris::knn_impl(raw, sax_sorted, n, queries, nq, k, out_idx, out_dist, len, w, card,
+                         (cudaStream_t)stream, config, stats, perm, env, false, raw_bf16);
 }
 
 }  // extern "C"

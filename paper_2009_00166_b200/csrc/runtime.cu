@@ -279,7 +279,7 @@ extern "C" {
 
 const char* paris_last_error(void) { return paris::g_err.c_str(); }
 
-int32_t paris_version(void) { return 103; }
+int32_t paris_version(void) { return 104; }
 
 void paris_profile_enable(int32_t on) { paris::g_profile_on.store(on ? 1 : 0); }
 

@@ -16,6 +16,8 @@
 // tile are staged in shared memory and leave as 16-byte row stores.
 #include "runtime.cuh"
 
+#include <cuda_bf16.h>
+
 #include <algorithm>
 #include <cstdlib>
 
@@ -27,6 +29,12 @@ constexpr int kThreads = 256;    // 8 warps
 constexpr int kSeriesPerWarp = kTile / (kThreads / 32);  // 16
 constexpr int kUnroll = 4;       // series loaded per warp step (bytes in flight)
 constexpr int kMaxW = 64;
+__device__ __forceinline__ float4 ld_stream_f4(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+}
 constexpr size_t kHostChunkBytes = (size_t)256 << 20;  // host-raw staging: 2 x 256 MB device buffers
 
 // #{c : cuts[c] <= v} over a table padded with +inf to 256 entries; `top` is
@@ -650,6 +658,39 @@ int summarize_impl(const float* raw, int64_t n, int len, int w, int card, uint8_
 }
 
 }  // namespace paris
+
+namespace paris {
+namespace {
+// fp32 -> bf16 (round to nearest even), 8 values per thread-iteration
+__global__ void __launch_bounds__(256) k_raw_bf16(const float4* __restrict__ raw, int64_t n8,
+                                                  uint4* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 a = ld_stream_f4(raw + 2 * i), b = ld_stream_f4(raw + 2 * i + 1);
+    uint4 o;
+    o.x = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(a.x)) | ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(a.y)) << 16);
+    o.y = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(a.z)) | ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(a.w)) << 16);
+    o.z = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(b.x)) | ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(b.y)) << 16);
+    o.w = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(b.z)) | ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(b.w)) << 16);
+    out[i] = o;
+  }
+}
+}  // namespace
+}  // namespace paris
+
+extern "C" int paris_raw_bf16(const float* raw, int64_t n, int32_t len, uint16_t* out, void* stream) {
+  if (!raw || !out || n < 1 || len < 8 || (len % 8) || (reinterpret_cast<uintptr_t>(raw) & 15) ||
+      (reinterpret_cast<uintptr_t>(out) & 15)) {
+    paris::set_error("paris_raw_bf16: bad arguments (n=%lld len=%d; 16-byte aligned device pointers, len %% 8 == 0)",
+                     (long long)n, len);
+    return PARIS_EINVAL;
+  }
+  const int64_t n8 = n * (int64_t)len / 8;
+  const int grid = (int)std::min<int64_t>((n8 + 255) / 256, (int64_t)paris::sm_count() * 16);
+  PARIS_CHECK_LAUNCH(PARIS_LAUNCH("raw_bf16", paris::k_raw_bf16, grid, 256, 0, (cudaStream_t)stream,
+                                  reinterpret_cast<const float4*>(raw), n8, reinterpret_cast<uint4*>(out)),
+                     "raw_bf16 launch");
+  return PARIS_OK;
+}
 
 extern "C" int paris_summarize(const float* raw, int64_t n, int32_t len, int32_t w, int32_t card,
                                uint8_t* out_sax, void* stream) {

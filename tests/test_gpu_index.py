@@ -150,3 +150,41 @@ def test_knn_index_cardinalities_and_lengths(P, card, length, k):
     gi, gd = P.knn_index(xd, idx, torch.from_numpy(q).cuda(), k=k)
     ri, rd2 = oracle.knn_bruteforce(x, q, k)
     check_knn(x, q, gi.cpu().numpy(), gd.cpu().numpy(), ri, rd2)
+
+
+@pytest.mark.parametrize("scale,shift", [(1.0, 0.0), (1e6, 3e6), (1e-4, 0.0)])
+@pytest.mark.parametrize("k", [1, 4])
+def test_knn_index_bf16_prefilter(P, scale, shift, k):
+    """paris_knn_index_x: the bf16 pre-filter only drops candidates whose rigorous lower bound
+    exceeds the BSF -> results identical to paris_knn_index_ex and to the oracle, on z-normalized
+    data, on data far from unit scale (the bound is relative to ||x~||), with near-member queries
+    (distances of the order of the bf16 rounding), exact duplicates (ties) and k > 1 (ignored)."""
+    import torch
+    n, nq, length = 40_000, 40, 256
+    x = datagen.random_walks(n, length, 700 + k) * np.float32(scale) + np.float32(shift)
+    q = datagen.random_walks(nq, length, 701 + k) * np.float32(scale) + np.float32(shift)
+    rng = np.random.default_rng(5)
+    q[:6] = x[[3, 3000, 39_999, 20_000, 77, 5]] + (1e-3 * scale * rng.standard_normal((6, length))).astype(np.float32)
+    x[9] = x[3]                                          # duplicate of a near-member's source (tie)
+    xd = torch.from_numpy(x).cuda()
+    sax = P.summarize(xd, 16, 256)
+    idx = P.index_build(sax, 16, 256)
+    r16 = P.raw_bf16(xd)
+    qd = torch.from_numpy(q).cuda()
+    gi, gd, st = P.knn_index(xd, idx, qd, k=k, raw16=r16, stats=True)
+    hi, hd = P.knn_index(xd, idx, qd, k=k)
+    assert torch.equal(gi, hi) and torch.equal(gd, hd)
+    ri, rd2 = oracle.knn_bruteforce(x, q, k)
+    check_knn(x, q, gi.cpu().numpy(), gd.cpu().numpy(), ri, rd2)
+    if k == 1 and scale == 1.0:
+        assert gi[0, 0].item() == 3                      # tie with id 9: the lower id
+        _, _, st0 = P.knn_index(xd, idx, qd, k=k, stats=True)
+        assert st["refined"].sum() < st0["refined"].sum()  # fp32 rows actually skipped
+
+
+def test_raw_bf16_definition(P):
+    import torch
+    x = torch.randn(1000, 64, device="cuda") * 100
+    r = P.raw_bf16(x)
+    ref = x.to(torch.bfloat16).view(torch.int16)
+    assert torch.equal(r, ref)
