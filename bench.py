@@ -384,8 +384,9 @@ def run_gpu(args):
         alg = {
             # SAX bytes per pass + 8 B per candidate written
             "lb_pass": (nbatches * n * W + 8.0 * cand.sum()) / nbatches,
-            # raw bytes per refined series (K6)
-            "refine": 4.0 * length * refined.sum() / nbatches,
+            # raw bytes per refined series (K6): fp32 rows + the bf16 rows of the pre-filter
+            "refine": (4.0 * length * refined.sum()
+                       + 2.0 * length * stats["raw16_rows"].numpy().astype(np.float64).sum()) / nbatches,
             # nb-ParIS+ workers: the SAX array + the raw series they read
             "nb_distcomp": (nbatches * n * W + 4.0 * length * refined.sum()) / nbatches,
         }
@@ -543,7 +544,8 @@ def run_gpu(args):
                         "lb_blocks_top5_share": float(np.sort(stats["lb_blocks"].numpy())[-5:].sum()
                                                       / max(1, stats["lb_blocks"].numpy().sum())),
                         "refined_top5_share": float(np.sort(refined)[-5:].sum() / max(1.0, refined.sum())),
-                        "bsf_updates_mean": primary.get("bsf_updates_mean")},
+                        "bsf_updates_mean": primary.get("bsf_updates_mean"),
+                        "raw16_rows_mean": float(stats["raw16_rows"].numpy().astype(np.float64).mean())},
         }
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -142,6 +142,8 @@ typedef struct paris_knn_stats {
   int64_t* lb_blocks;   /* index mode: PARIS_INDEX_BLOCK-series blocks whose envelope
                            bound passed (their series' LBs were computed); 0 otherwise */
   int64_t* bsf_updates; /* paris_knn_nb: updates of the workers' private BSF copies   */
+  int64_t* raw16_rows;  /* paris_knn_index_x: bf16 rows read by the refinement pre-filter
+                           (refined = the fp32 rows read after it)                     */
 } paris_knn_stats;
 
 /* Same as paris_knn_exact with tunables and optional stats (either may be NULL). */

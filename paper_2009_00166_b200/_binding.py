@@ -38,7 +38,7 @@ class _Config(ctypes.Structure):
 class _Stats(ctypes.Structure):
     _fields_ = [("candidates", ctypes.c_void_p), ("refined", ctypes.c_void_p),
                 ("tau_seed", ctypes.c_void_p), ("lb_blocks", ctypes.c_void_p),
-                ("bsf_updates", ctypes.c_void_p)]
+                ("bsf_updates", ctypes.c_void_p), ("raw16_rows", ctypes.c_void_p)]
 
 
 class _KProf(ctypes.Structure):
@@ -276,9 +276,9 @@ def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: in
     if stats:
         arrays = (torch.zeros(nq, dtype=torch.int64), torch.zeros(nq, dtype=torch.int64),
                   torch.zeros(nq, dtype=torch.float32), torch.zeros(nq, dtype=torch.int64),
-                  torch.zeros(nq, dtype=torch.int64))
+                  torch.zeros(nq, dtype=torch.int64), torch.zeros(nq, dtype=torch.int64))
         st = _Stats(arrays[0].data_ptr(), arrays[1].data_ptr(), arrays[2].data_ptr(), arrays[3].data_ptr(),
-                    arrays[4].data_ptr())
+                    arrays[4].data_ptr(), arrays[5].data_ptr())
     if _nb:
         if k != 1:
             raise ValueError("knn_nb answers 1-NN (nb-ParIS+, Alg7-8)")
@@ -306,7 +306,8 @@ def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: in
     _check(rc)
     if stats:
         return out_idx, out_dist, {"candidates": arrays[0], "refined": arrays[1],
-                                   "tau_seed": arrays[2], "lb_blocks": arrays[3], "bsf_updates": arrays[4]}
+                                   "tau_seed": arrays[2], "lb_blocks": arrays[3], "bsf_updates": arrays[4],
+                                   "raw16_rows": arrays[5]}
     return out_idx, out_dist
 
 

@@ -1728,6 +1728,7 @@ struct RefineArgs {
   unsigned lo, hi;           // k = 1: refine list positions [lo, min(hi, count)) (a wave)
   int64_t n;                 // series in raw (debug bounds checks)
   const uint16_t* raw16 = nullptr;  // optional bf16 copy of raw [n][len] (paris_raw_bf16): pre-filter
+  unsigned* refined16 = nullptr;    // per query: bf16 rows read by the pre-filter
 };
 
 // One warp step: up to kU candidates (indices i0 + u*stride) against the live
@@ -1863,12 +1864,15 @@ __device__ __forceinline__ void bf16_prefilter(const RefineArgs& a, const float4
 template <int NC, int U>
 __device__ __forceinline__ void refine_group(const RefineArgs& a, const float4* __restrict__ qv,
                                              const uint64_t (&key)[U], bool (&live)[U], float thr,
-                                             uint64_t& cur, unsigned long long* bp, unsigned& nref) {
+                                             uint64_t& cur, unsigned long long* bp, unsigned& nref,
+                                             unsigned& nref16) {
   const int lane = threadIdx.x & 31;
   const int nf = a.len >> 2;
 #pragma unroll
   for (int u = 0; u < U; ++u) PARIS_DCHECK(!live[u] || key_id(key[u]) < (uint64_t)a.n);
   if (a.raw16) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) nref16 += live[u] ? 1u : 0u;
     bf16_prefilter<NC, U>(a, qv, key, live, thr);
     bool any = false;
 #pragma unroll
@@ -1938,11 +1942,12 @@ k_refine1(RefineArgs a, int nb) {
   // every warp walks its interleaved share of EVERY query's list (balanced work:
   // a query with 5x the mean candidate count no longer leaves most SMs idle); the
   // query rows are read through L1 (all warps of a CTA share them)
-  __shared__ unsigned s_refined[kMaxB], s_cnt[kMaxB];
+  __shared__ unsigned s_refined[kMaxB], s_cnt[kMaxB], s_r16[kMaxB];
   __shared__ float s_scale[kMaxB];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x < kMaxB) {
     s_refined[threadIdx.x] = 0;
+    s_r16[threadIdx.x] = 0;
     // per-query list lengths and bin scales, read once per CTA (queries with no work
     // in this wave then cost a shared-memory read, not a global round trip)
     s_cnt[threadIdx.x] = threadIdx.x < nb
@@ -1958,7 +1963,7 @@ k_refine1(RefineArgs a, int nb) {
     const uint64_t* list = a.sorted + (size_t)b * a.cap + a.lo;
     const float4* qv = reinterpret_cast<const float4*>(a.queries + (size_t)b * a.len);
     unsigned long long* bp = a.best + (size_t)b * kPadU64;
-    unsigned nref = 0;
+    unsigned nref = 0, nref16 = 0;
     uint64_t cur = kNoKey;  // this warp's view of the BSF: refreshed every 4 steps, lowered by its own finds
     unsigned step = 0;
     for (unsigned i0 = gw; a.lo + i0 < cnt; i0 += U * GW, ++step) {
@@ -1981,13 +1986,15 @@ k_refine1(RefineArgs a, int nb) {
           stop = (a.lo + i0 + u * GW >= cnt) || (bin >= 1 && (float)(bin - 1) > thr * scale);
         }
       }
-      refine_group<NC, U>(a, qv, key, live, thr, cur, bp, nref);
+      refine_group<NC, U>(a, qv, key, live, thr, cur, bp, nref, nref16);
       if (stop) break;
     }
     if (lane == 0 && nref) atomicAdd(&s_refined[b], nref);
+    if (lane == 0 && nref16) atomicAdd(&s_r16[b], nref16);
   }
   __syncthreads();
   if (threadIdx.x < nb && s_refined[threadIdx.x]) atomicAdd(&a.refined[threadIdx.x], s_refined[threadIdx.x]);
+  if (threadIdx.x < nb && s_r16[threadIdx.x]) atomicAdd(&a.refined16[threadIdx.x], s_r16[threadIdx.x]);
 }
 
 // k = 1 without the bucket sort (K5 skipped): the two LB-ordered waves are taken
@@ -2032,12 +2039,13 @@ __global__ void __launch_bounds__(kNB) k_wave_cut(const unsigned* __restrict__ h
 template <int NC, int U>
 __global__ void __launch_bounds__(kRefThreads, NC <= 2 ? kRefUCtas : 2)
 k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
-  __shared__ unsigned s_refined[kMaxB], s_cnt[kMaxB], s_cut[kMaxB];
+  __shared__ unsigned s_refined[kMaxB], s_cnt[kMaxB], s_cut[kMaxB], s_r16[kMaxB];
   __shared__ float s_scale[kMaxB];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x < kMaxB) {
     const bool on = threadIdx.x < nb;
     s_refined[threadIdx.x] = 0;
+    s_r16[threadIdx.x] = 0;
     s_cnt[threadIdx.x] = on ? (unsigned)imin64((int64_t)a.count[threadIdx.x], a.cap) : 0u;
     s_cut[threadIdx.x] = on ? cut[threadIdx.x * kNB] : 0u;
     s_scale[threadIdx.x] = on ? bin_scale(__uint_as_float(a.thr_seed[threadIdx.x])) : 0.f;
@@ -2054,7 +2062,7 @@ k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     const uint64_t* list = a.sorted + (size_t)b * a.cap;
     const float4* qv = reinterpret_cast<const float4*>(a.queries + (size_t)b * a.len);
     unsigned long long* bp = a.best + (size_t)b * kPadU64;
-    unsigned nref = 0;
+    unsigned nref = 0, nref16 = 0;
     uint64_t cur = kNoKey;
     for (unsigned ch = first; ch < nchunk; ch += GW) {
       const unsigned i = ch * 32 + lane;
@@ -2076,14 +2084,16 @@ k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
           key[u] = __shfl_sync(0xffffffffu, k0, src);
           live[u] = has && key_val(key[u]) <= thr;
         }
-        refine_group<NC, U>(a, qv, key, live, thr, cur, bp, nref);
+        refine_group<NC, U>(a, qv, key, live, thr, cur, bp, nref, nref16);
         thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
       }
     }
     if (lane == 0 && nref) atomicAdd(&s_refined[b], nref);
+    if (lane == 0 && nref16) atomicAdd(&s_r16[b], nref16);
   }
   __syncthreads();
   if (threadIdx.x < nb && s_refined[threadIdx.x]) atomicAdd(&a.refined[threadIdx.x], s_refined[threadIdx.x]);
+  if (threadIdx.x < nb && s_r16[threadIdx.x]) atomicAdd(&a.refined16[threadIdx.x], s_r16[threadIdx.x]);
 }
 
 // k > 1: rounds of (every warp: one refine_step) -> merge the round's admitted
@@ -2188,7 +2198,8 @@ __global__ void k_finalize1(const unsigned long long* __restrict__ best, int nb,
                             int64_t* __restrict__ out_idx, float* __restrict__ out_dist,
                             const unsigned* __restrict__ count, const unsigned* __restrict__ refined,
                             unsigned* __restrict__ all_count, unsigned* __restrict__ all_refined, int accum,
-                            const unsigned* __restrict__ blocks, unsigned* __restrict__ all_blocks) {
+                            const unsigned* __restrict__ blocks, unsigned* __restrict__ all_blocks,
+                            const unsigned* __restrict__ extra, unsigned* __restrict__ all_extra) {
   const int b = threadIdx.x;
   if (b >= nb) return;
   const uint64_t key = best[b * kPadU64];
@@ -2197,6 +2208,7 @@ __global__ void k_finalize1(const unsigned long long* __restrict__ best, int nb,
   all_count[q0 + b] = (accum ? all_count[q0 + b] : 0u) + count[b];
   all_refined[q0 + b] = (accum ? all_refined[q0 + b] : 0u) + refined[b];
   all_blocks[q0 + b] = (accum ? all_blocks[q0 + b] : 0u) + blocks[b];
+  all_extra[q0 + b] = (accum ? all_extra[q0 + b] : 0u) + extra[b];
 }
 
 // Merge the per-CTA top-k lists: repeatedly sort [current top-k | next chunk]
@@ -2206,7 +2218,8 @@ k_finalize(const uint64_t* __restrict__ lists, int nslots, int k, int q0,
            int64_t* __restrict__ out_idx, float* __restrict__ out_dist,
            const unsigned* __restrict__ count, const unsigned* __restrict__ refined,
            unsigned* __restrict__ all_count, unsigned* __restrict__ all_refined, int accum,
-           const unsigned* __restrict__ blocks, unsigned* __restrict__ all_blocks) {
+           const unsigned* __restrict__ blocks, unsigned* __restrict__ all_blocks,
+           const unsigned* __restrict__ extra, unsigned* __restrict__ all_extra) {
   __shared__ uint64_t buf[kSortP];
   const int b = blockIdx.x;
   const int64_t total = (int64_t)nslots * k;
@@ -2230,6 +2243,7 @@ k_finalize(const uint64_t* __restrict__ lists, int nslots, int k, int q0,
     all_count[q0 + b] = (accum ? all_count[q0 + b] : 0u) + count[b];
     all_refined[q0 + b] = (accum ? all_refined[q0 + b] : 0u) + refined[b];
     all_blocks[q0 + b] = (accum ? all_blocks[q0 + b] : 0u) + blocks[b];
+    all_extra[q0 + b] = (accum ? all_extra[q0 + b] : 0u) + extra[b];
   }
 }
 
@@ -2562,7 +2576,7 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
 int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* qbatch, int nb, int q0,
               int64_t cap, const CardTables* tab, const Ws& ws, int64_t* d_idx, float* d_dist,
               unsigned* all_count, unsigned* all_refined, float* all_tau, unsigned* all_blocks,
-              cudaStream_t st, bool rescan = false) {
+              unsigned* all_extra, cudaStream_t st, bool rescan = false) {
   const int P = pairs_for(nb);
   cudaError_t e = cudaMemsetAsync(ws.zero_block, 0, ws.zero_bytes, st);
   if (e != cudaSuccess) return cuda_error(e, "memset scratch");
@@ -2600,7 +2614,7 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
     PARIS_CHECK_LAUNCH(launch_nb(p, raw, sax, qbatch, nb, tab, ws, st), "nb launch");
     PARIS_CHECK_LAUNCH(PARIS_LAUNCH("finalize", k_finalize1, 1, kMaxB, 0, st, ws.best, nb, q0, d_idx, d_dist,
                                     ws.count, ws.refined, all_count, all_refined, rescan ? 1 : 0,
-                                    ws.updates, all_blocks),
+                                    ws.blocks, all_blocks, ws.updates, all_extra),
                        "finalize launch");
     return PARIS_OK;
   }
@@ -2641,6 +2655,7 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
   ra.refined = ws.refined; ra.lists = ws.lists; ra.k = p.k; ra.d2up = p.d2up;
   ra.lo = 0; ra.hi = 0xFFFFFFFFu; ra.n = p.n;
   ra.raw16 = p.k == 1 ? p.raw16 : nullptr;
+  ra.refined16 = ws.updates;
   dim3 g((unsigned)p.XB, (unsigned)nb);
   if (p.k == 1) {
     cudaError_t e1 = cudaSuccess;
@@ -2672,7 +2687,7 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
     PARIS_CHECK_LAUNCH(e1, "refine launch");
     PARIS_CHECK_LAUNCH(PARIS_LAUNCH("finalize", k_finalize1, 1, kMaxB, 0, st, ws.best, nb, q0, d_idx, d_dist,
                                     ws.count, ws.refined, all_count, all_refined, rescan ? 1 : 0,
-                                    ws.blocks, all_blocks),
+                                    ws.blocks, all_blocks, ws.updates, all_extra),
                        "finalize launch");
   } else {
     const size_t rsmem = (size_t)p.len * 4 + (size_t)p.k * 16;
@@ -2703,7 +2718,7 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
     }
     PARIS_CHECK_LAUNCH(PARIS_LAUNCH("finalize", k_finalize, nb, 1024, 0, st, ws.lists, p.XB, p.k, q0,
                                     d_idx, d_dist, ws.count, ws.refined, all_count, all_refined, rescan ? 1 : 0,
-                                    ws.blocks, all_blocks),
+                                    ws.blocks, all_blocks, ws.updates, all_extra),
                        "finalize launch");
   }
   return PARIS_OK;
@@ -2846,7 +2861,7 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   cudaError_t e;
   char* stage = nullptr;
   const size_t qbytes = (size_t)nq * len * 4, ibytes = (size_t)nq * k * 8, dbytes = (size_t)nq * k * 4;
-  const size_t cbytes = (size_t)nq * 4 * 4;
+  const size_t cbytes = (size_t)nq * 4 * 5;
   e = cudaMallocAsync((void**)&stage, qbytes + ibytes + dbytes + cbytes + 1024, st);
   if (e != cudaSuccess) { cudaGetLastError(); set_error("paris_knn_exact: staging alloc failed"); return PARIS_ENOMEM; }
   const float* d_q = queries;
@@ -2860,6 +2875,7 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   unsigned* all_refined = all_count + nq;
   float* all_tau = (float*)(all_refined + nq);
   unsigned* all_blocks = (unsigned*)(all_tau + nq);
+  unsigned* all_extra = all_blocks + nq;  // nb: BSF-copy updates; index + bf16: pre-filter rows
   if (hq) {
     e = cudaMemcpyAsync(sq, queries, qbytes, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) { cudaFreeAsync(stage, st); return cuda_error(e, "H2D queries"); }
@@ -2885,10 +2901,10 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   for (int q0 = 0; q0 < nq && rc == PARIS_OK; q0 += p.B) {
     const int nb = std::min(p.B, nq - q0);
     rc = run_batch(p, raw, sax, d_q + (size_t)q0 * len, nb, q0, p.cap, tab, ws, d_idx, d_dist,
-                   all_count, all_refined, all_tau, all_blocks, st, /*rescan=*/seed_from_out);
+                   all_count, all_refined, all_tau, all_blocks, all_extra, st, /*rescan=*/seed_from_out);
   }
   // overflow check: one synchronization per call
-  std::vector<unsigned> h_count(nq), h_ref(nq), h_blk(nq);
+  std::vector<unsigned> h_count(nq), h_ref(nq), h_blk(nq), h_ext(nq);
   std::vector<float> h_tau(nq);
   if (rc == PARIS_OK) {
     e = cudaMemcpyAsync(h_count.data(), all_count, (size_t)nq * 4, cudaMemcpyDeviceToHost, st);
@@ -2908,7 +2924,7 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
       rc = alloc_ws(p1, p1.cap, ws1, st);
       if (rc) break;
       rc = run_batch(p1, raw, sax, d_q + (size_t)q * len, 1, q, p1.cap, tab, ws1, d_idx, d_dist,
-                     all_count, all_refined, all_tau, all_blocks, st, /*rescan=*/true);
+                     all_count, all_refined, all_tau, all_blocks, all_extra, st, /*rescan=*/true);
       cudaFreeAsync(ws1.base, st);
     }
   }
@@ -2921,6 +2937,7 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
       if (e == cudaSuccess) e = cudaMemcpyAsync(h_ref.data(), all_refined, (size_t)nq * 4, cudaMemcpyDeviceToHost, st);
       if (e == cudaSuccess) e = cudaMemcpyAsync(h_tau.data(), all_tau, (size_t)nq * 4, cudaMemcpyDeviceToHost, st);
       if (e == cudaSuccess) e = cudaMemcpyAsync(h_blk.data(), all_blocks, (size_t)nq * 4, cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(h_ext.data(), all_extra, (size_t)nq * 4, cudaMemcpyDeviceToHost, st);
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) rc = cuda_error(e, "paris_knn_exact D2H");
@@ -2930,7 +2947,8 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
         if (stats->refined) stats->refined[q] = h_ref[q];
         if (stats->tau_seed) stats->tau_seed[q] = h_tau[q];
         if (stats->lb_blocks) stats->lb_blocks[q] = p.nb ? 0 : h_blk[q];
-        if (stats->bsf_updates) stats->bsf_updates[q] = p.nb ? h_blk[q] : 0;
+        if (stats->bsf_updates) stats->bsf_updates[q] = p.nb ? h_ext[q] : 0;
+        if (stats->raw16_rows) stats->raw16_rows[q] = p.nb ? 0 : h_ext[q];
       }
     }
   }
