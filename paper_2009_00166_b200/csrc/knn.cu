@@ -1864,21 +1864,11 @@ __device__ __forceinline__ void bf16_prefilter(const RefineArgs& a, const float4
 template <int NC, int U>
 __device__ __forceinline__ void refine_group(const RefineArgs& a, const float4* __restrict__ qv,
                                              const uint64_t (&key)[U], bool (&live)[U], float thr,
-                                             uint64_t& cur, unsigned long long* bp, unsigned& nref,
-                                             unsigned& nref16) {
+                                             uint64_t& cur, unsigned long long* bp, unsigned& nref) {
   const int lane = threadIdx.x & 31;
   const int nf = a.len >> 2;
 #pragma unroll
   for (int u = 0; u < U; ++u) PARIS_DCHECK(!live[u] || key_id(key[u]) < (uint64_t)a.n);
-  if (a.raw16) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) nref16 += live[u] ? 1u : 0u;
-    bf16_prefilter<NC, U>(a, qv, key, live, thr);
-    bool any = false;
-#pragma unroll
-    for (int u = 0; u < U; ++u) any |= live[u];
-    if (!any) return;
-  }
   float4 x[U][NC];
 #pragma unroll
   for (int u = 0; u < U; ++u)
@@ -1986,7 +1976,7 @@ k_refine1(RefineArgs a, int nb) {
           stop = (a.lo + i0 + u * GW >= cnt) || (bin >= 1 && (float)(bin - 1) > thr * scale);
         }
       }
-      refine_group<NC, U>(a, qv, key, live, thr, cur, bp, nref, nref16);
+      refine_group<NC, U>(a, qv, key, live, thr, cur, bp, nref);
       if (stop) break;
     }
     if (lane == 0 && nref) atomicAdd(&s_refined[b], nref);
@@ -2039,6 +2029,7 @@ __global__ void __launch_bounds__(kNB) k_wave_cut(const unsigned* __restrict__ h
 template <int NC, int U>
 __global__ void __launch_bounds__(kRefThreads, NC <= 2 ? kRefUCtas : 2)
 k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
+  constexpr int kPF = 2 * U;  // bf16 pre-filter rows per warp step (the bytes U fp32 rows would take)
   __shared__ unsigned s_refined[kMaxB], s_cnt[kMaxB], s_cut[kMaxB], s_r16[kMaxB];
   __shared__ float s_scale[kMaxB];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -2073,6 +2064,38 @@ k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
       const int bin = lb_bin(lb0, scale);
       const bool mine = i < cnt && (wave == 0 ? bin <= cutb : bin > cutb);
       unsigned m = __ballot_sync(0xffffffffu, mine && lb0 <= thr);
+      if (a.raw16) {
+        // bf16 pre-filter over kPF candidates at a time (their 2*len-byte rows in flight
+        // together), then the survivors' fp32 rows U at a time
+        while (m) {
+          uint64_t kp[kPF];
+          bool lp[kPF];
+#pragma unroll
+          for (int u = 0; u < kPF; ++u) {
+            const int src = m ? __ffs(m) - 1 : 0;
+            const bool has = m != 0u;
+            m &= m - 1;
+            kp[u] = __shfl_sync(0xffffffffu, k0, src);
+            lp[u] = has && key_val(kp[u]) <= thr;
+            nref16 += lp[u] ? 1u : 0u;
+          }
+          bf16_prefilter<NC, kPF>(a, qv, kp, lp, thr);
+#pragma unroll
+          for (int g = 0; g < kPF; g += U) {
+            uint64_t key[U];
+            bool live[U], any = false;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              key[u] = kp[g + u];
+              live[u] = lp[g + u] && key_val(key[u]) <= thr;
+              any |= live[u];
+            }
+            if (!any) continue;
+            refine_group<NC, U>(a, qv, key, live, thr, cur, bp, nref);
+            thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
+          }
+        }
+      }
       while (m) {
         uint64_t key[U];
         bool live[U];
@@ -2084,7 +2107,7 @@ k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
           key[u] = __shfl_sync(0xffffffffu, k0, src);
           live[u] = has && key_val(key[u]) <= thr;
         }
-        refine_group<NC, U>(a, qv, key, live, thr, cur, bp, nref, nref16);
+        refine_group<NC, U>(a, qv, key, live, thr, cur, bp, nref);
         thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
       }
     }
