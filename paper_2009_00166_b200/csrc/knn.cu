@@ -371,6 +371,53 @@ k_seed_ed(const float* __restrict__ raw, int len, const float* __restrict__ quer
   }
 }
 
+// K3b with raw in host memory and its bf16 copy in HBM (f3 + paris_knn_index_x):
+// the seeds' distances come from the bf16 rows as rigorous UPPER bounds,
+// ED(q, x) <= ED(q, x~) + rho ||x~|| (bf16_prefilter's rho and fp32 margins, rounded
+// up), so the seed needs no PCIe read.  tau_seed only has to bound the k-th NN
+// distance from above; the seed series themselves are candidates (LB <= ED <= the
+// bound) and get their exact distances in the refinement (k = 1 only).
+__global__ void __launch_bounds__(kRefThreads)
+k_seed_ed16(const uint16_t* __restrict__ raw16, int len, const float* __restrict__ queries,
+            const int* __restrict__ seed_ids, int S, uint64_t* __restrict__ seed_keys) {
+  extern __shared__ float4 s_qv[];
+  const int b = blockIdx.y;
+  const float4* qsrc = reinterpret_cast<const float4*>(queries + (size_t)b * len);
+  for (int i = threadIdx.x; i < len / 4; i += blockDim.x) s_qv[i] = qsrc[i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  const int nh = len >> 3;
+  const float e2 = 2.f * (float)((len >> 5) + 8) * 5.9604644775390625e-08f;
+  constexpr float rho = 0.00392150878906250f;
+  for (int j = blockIdx.x * nw + warp; j < S; j += gridDim.x * nw) {
+    const int id = seed_ids[b * S + j];
+    uint64_t key = kNoKey;
+    if (id >= 0) {
+      const uint4* row = reinterpret_cast<const uint4*>(raw16 + (size_t)id * len);
+      float s2 = 0.f, n2 = 0.f;
+      for (int f = lane; f < nh; f += 32) {
+        const uint4 h = __ldg(row + f);
+        const float4 q0 = s_qv[2 * f], q1 = s_qv[2 * f + 1];
+        const uint32_t w4[4] = {h.x, h.y, h.z, h.w};
+        const float qq[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float x = __uint_as_float((e & 1) ? (w4[e >> 1] & 0xFFFF0000u) : (w4[e >> 1] << 16));
+          const float d = x - qq[e];
+          s2 = fmaf(d, d, s2);
+          n2 = fmaf(x, x, n2);
+        }
+      }
+      const float s = warp_sum(s2), nn = warp_sum(n2);
+      const float hi = __fadd_ru(__fadd_ru(__fsqrt_ru(__fmul_ru(s, 1.f + e2)),
+                                           __fmul_ru(rho, __fsqrt_ru(__fmul_ru(nn, 1.f + e2)))), 1e-30f);
+      key = make_key(__fmul_ru(hi, hi), (uint32_t)id);
+    }
+    if (lane == 0) seed_keys[b * S + j] = key;
+  }
+}
+
 // ---------------------------------------------------------------- bitonic sort (smem)
 __device__ void bitonic_sort(uint64_t* buf, int P) {
   for (int size = 2; size <= P; size <<= 1) {
@@ -2335,6 +2382,7 @@ struct Plan {
   bool nb;               // f2: nb-ParIS+ (per-worker BSF copies, fused LB -> refine)
   bool sorted_refine = false;  // k = 1: walk bucket-sorted lists (K5) instead of the unsorted waves
   const uint16_t* raw16 = nullptr;  // optional bf16 copy of raw: refine pre-filter (k = 1)
+  bool raw_host = false;            // raw in pinned host memory (f3)
 };
 
 int pairs_for(int nb) { return nb <= 2 ? 1 : nb <= 4 ? 2 : nb <= 8 ? 4 : nb <= 16 ? 8 : nb <= 32 ? 16 : 32; }
@@ -2624,9 +2672,14 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
     }
     {
       dim3 g((unsigned)((p.S + 7) / 8), (unsigned)nb);
-      PARIS_CHECK_LAUNCH(PARIS_LAUNCH("seed_ed", k_seed_ed, g, kRefThreads, (size_t)p.len * 4, st, raw, p.len,
-                                      qbatch, ws.seed_ids, p.S, ws.seed_keys),
-                         "seed_ed launch");
+      if (p.raw16 && p.raw_host && p.k == 1)
+        PARIS_CHECK_LAUNCH(PARIS_LAUNCH("seed_ed", k_seed_ed16, g, kRefThreads, (size_t)p.len * 4, st, p.raw16,
+                                        p.len, qbatch, ws.seed_ids, p.S, ws.seed_keys),
+                           "seed_ed launch");
+      else
+        PARIS_CHECK_LAUNCH(PARIS_LAUNCH("seed_ed", k_seed_ed, g, kRefThreads, (size_t)p.len * 4, st, raw, p.len,
+                                        qbatch, ws.seed_ids, p.S, ws.seed_keys),
+                           "seed_ed launch");
     }
     PARIS_CHECK_LAUNCH(PARIS_LAUNCH("seed_select", k_seed_select, nb, 1024, 0, st, ws.seed_keys, p.S, p.k,
                                     p.d2up, ws.thr, ws.thr_seed, ws.best, all_tau, q0),
@@ -2869,7 +2922,10 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
     }
     p.raw16 = raw16;
   }
-  p.idx_seeds = (cfg && cfg->reserved[2] > 0) ? cfg->reserved[2] : (raw_host ? kIdxSeedsHost : 0);
+  p.raw_host = raw_host;
+  // (host raw with the bf16 copy in HBM: the seeds read bf16 rows, so the full 1024)
+  p.idx_seeds = (cfg && cfg->reserved[2] > 0) ? cfg->reserved[2]
+                                               : ((raw_host && !(raw16 && k == 1)) ? kIdxSeedsHost : 0);
   plan_seed(p, (cfg && cfg->seed_div > 0) ? cfg->seed_div : 16);
   p.cap = nb_mode ? 1 : std::min<int64_t>(n, std::max<int64_t>(65536, n / 32));
   plan_refine(p);

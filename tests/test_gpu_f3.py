@@ -122,3 +122,28 @@ def test_knn_pageable_raw_rejected(P):
     rc = lib.paris_knn_exact(xd.data_ptr(), sax_h.data_ptr(), 64, xd.data_ptr(), 2, 1, oi.data_ptr(),
                              od.data_ptr(), 256, 16, 256, ctypes.c_void_p(0))
     assert rc == -1
+
+
+@pytest.mark.parametrize("k", [1, 3])
+def test_knn_index_pinned_raw_bf16(P, k):
+    """Raw in pinned host memory with its bf16 copy in HBM (paris_knn_index_x): the seed's
+    distances are bf16 upper bounds and the pre-filter keeps almost every fp32 row off PCIe;
+    results identical to the device-raw run and the oracle (k > 1 ignores the copy)."""
+    import torch
+    n, length, nq = 40_000, 256, 30
+    x = datagen.random_walks(n, length, 91 + k)
+    q = datagen.random_walks(nq, length, 92 + k)
+    q[:3] = x[[4, 30_000, 39_999]]
+    xd = torch.from_numpy(x).cuda()
+    xh = torch.from_numpy(x).pin_memory()
+    sax = P.summarize(xd, 16, 256)
+    idx = P.index_build(sax, 16, 256)
+    r16 = P.raw_bf16(xd)
+    qd = torch.from_numpy(q).cuda()
+    hi, hd, st = P.knn_index(xh, idx, qd, k=k, raw16=r16, stats=True)
+    di, dd = P.knn_index(xd, idx, qd, k=k)
+    assert torch.equal(hi, di) and torch.equal(hd, dd)
+    ri, rd2 = oracle.knn_bruteforce(x, q, k)
+    check_knn(x, q, hi.cpu().numpy(), hd.cpu().numpy(), ri, rd2)
+    if k == 1:
+        assert st["refined"].float().mean().item() < 50   # fp32 rows read per query
