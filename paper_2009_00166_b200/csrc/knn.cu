@@ -93,6 +93,12 @@ __device__ __forceinline__ uint64_t ld_relaxed_u64(const unsigned long long* p) 
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
   return v;
 }
+__device__ __forceinline__ uint4 ld_stream_u4(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
 __device__ __forceinline__ float4 ld_stream(const float4* p) {
   float4 v;
   asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
@@ -1847,15 +1853,23 @@ __device__ __forceinline__ bool refine_step(const RefineArgs& a, const uint64_t*
 }
 
 // bf16 pre-filter (optional, a.raw16): a row's bf16 copy x~ (half the bytes)
-// gives a rigorous lower bound on the true distance before the fp32 row is read:
-// round-to-nearest bf16 keeps |x_i - x~_i| <= rho |x~_i|, rho = 2^-8 (1 + 2^-7), so
-// ED(x, x~) <= rho ||x~|| and ED(q, x) >= ED(q, x~) - rho ||x~||.  Both sums are
-// fp32 (relative error <= e = (len/32 + 8) 2^-24, the d^2 bound of refine_group),
-// taken with directed roundings: L = sqrt(s (1 - 2e)) - rho sqrt(n2 (1 + 2e)).  A
-// candidate with L^2 > thr (the live BSF threshold) cannot beat the BSF and is
-// dropped without its fp32 row; the rest are refined exactly as before.
+// gives a rigorous lower bound on the true distance before the fp32 row is read.
+// Round-to-nearest bf16 keeps |x_i - x~_i| <= rho |x~_i|, rho = 2^-8 (1 + 2^-7), so
+// ED(x, x~) <= rho ||x~|| <= rho (||q|| + D) with D = ED(q, x~), and
+// ED(q, x) >= D - rho (||q|| + D) = (1 - rho) D - rho ||q||.  D^2 is an fp32 sum
+// (relative error <= e = (len/32 + 8) 2^-24, the d^2 bound of refine_group), taken
+// as D >= sqrt(D^2 (1 - 2e)) with directed roundings; qn_hi >= ||q||.  A candidate
+// whose bound squared exceeds thr (the live BSF threshold) cannot beat the BSF and
+// is dropped without its fp32 row; the rest are refined exactly as before.
+__device__ __forceinline__ float bf16_lb(float d2, float qn_hi, float e2) {
+  constexpr float rho = 0.00392150878906250f;       // 2^-8 (1 + 2^-7), rounded up
+  constexpr float one_m_rho = 0.99607849121093750f; // 1 - rho, rounded down
+  return __fsub_rd(__fsub_rd(__fmul_rd(one_m_rho, __fsqrt_rd(__fmul_rd(d2, 1.f - e2))), __fmul_ru(rho, qn_hi)),
+                   1e-30f);  // (1e-30: the absolute error of bf16 subnormals)
+}
+
 template <int NC, int U>
-__device__ __forceinline__ void bf16_prefilter(const RefineArgs& a, const float4* __restrict__ qv,
+__device__ __forceinline__ void bf16_prefilter(const RefineArgs& a, const float4* __restrict__ qv, float qn_hi,
                                                const uint64_t (&key)[U], bool (&live)[U], float thr) {
   constexpr int NH = (NC + 1) / 2;  // uint4 (8 bf16) per lane
   const int lane = threadIdx.x & 31;
@@ -1866,13 +1880,12 @@ __device__ __forceinline__ void bf16_prefilter(const RefineArgs& a, const float4
 #pragma unroll
     for (int c = 0; c < NH; ++c) {
       const int f = lane + 32 * c;
-      h[u][c] = (live[u] && f < nh)
-                    ? __ldg(reinterpret_cast<const uint4*>(a.raw16 + (size_t)key_id(key[u]) * a.len) + f)
-                    : make_uint4(0u, 0u, 0u, 0u);
+      h[u][c] = (live[u] && f < nh) ? ld_stream_u4(reinterpret_cast<const uint4*>(a.raw16 + (size_t)key_id(key[u]) * a.len) + f)
+                                    : make_uint4(0u, 0u, 0u, 0u);
     }
-  float s2[U], n2[U];
+  float s2[U];
 #pragma unroll
-  for (int u = 0; u < U; ++u) s2[u] = n2[u] = 0.f;
+  for (int u = 0; u < U; ++u) s2[u] = 0.f;
 #pragma unroll
   for (int c = 0; c < NH; ++c) {
     const int f = lane + 32 * c;
@@ -1884,23 +1897,36 @@ __device__ __forceinline__ void bf16_prefilter(const RefineArgs& a, const float4
       const uint32_t w4[4] = {h[u][c].x, h[u][c].y, h[u][c].z, h[u][c].w};
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const float x = __uint_as_float((e & 1) ? (w4[e >> 1] & 0xFFFF0000u) : (w4[e >> 1] << 16));
-        const float d = x - qq[e];
+        const float d = __uint_as_float((e & 1) ? (w4[e >> 1] & 0xFFFF0000u) : (w4[e >> 1] << 16)) - qq[e];
         s2[u] = fmaf(d, d, s2[u]);
-        n2[u] = fmaf(x, x, n2[u]);
       }
     }
   }
   const float e2 = 2.f * (float)((a.len >> 5) + 8) * 5.9604644775390625e-08f;
-  constexpr float rho = 0.00392150878906250f;  // 2^-8 (1 + 2^-7), rounded up
+  if constexpr (U == 4) {
+    // four sums in one reduction: halves exchange two values (xor 16), then one
+    // (xor 8), then each 8-lane group finishes its own value; one ballot spreads
+    // the four decisions (lane 8u holds value u's sum)
+    const bool hi16 = lane & 16, hi8 = lane & 8;
+    float w0 = hi16 ? s2[2] : s2[0], w1 = hi16 ? s2[3] : s2[1];
+    w0 += __shfl_xor_sync(0xffffffffu, hi16 ? s2[0] : s2[2], 16);
+    w1 += __shfl_xor_sync(0xffffffffu, hi16 ? s2[1] : s2[3], 16);
+    float z = hi8 ? w1 : w0;
+    z += __shfl_xor_sync(0xffffffffu, hi8 ? w0 : w1, 8);
+    z += __shfl_xor_sync(0xffffffffu, z, 4);
+    z += __shfl_xor_sync(0xffffffffu, z, 2);
+    z += __shfl_xor_sync(0xffffffffu, z, 1);
+    const float lb = bf16_lb(z, qn_hi, e2);
+    const unsigned drop = __ballot_sync(0xffffffffu, lb > 0.f && __fmul_rd(lb, lb) > thr);
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    if (!__any_sync(0xffffffffu, live[u])) continue;
-    const float s = warp_sum(s2[u]), nn = warp_sum(n2[u]);
-    // (1e-30: the absolute error of bf16 subnormals, below any relative bound)
-    const float lo = __fsub_rd(__fsub_rd(__fsqrt_rd(__fmul_rd(s, 1.f - e2)),
-                                         __fmul_ru(rho, __fsqrt_ru(__fmul_ru(nn, 1.f + e2)))), 1e-30f);
-    if (live[u] && lo > 0.f && __fmul_rd(lo, lo) > thr) live[u] = false;
+    for (int u = 0; u < 4; ++u)
+      if ((drop >> (8 * u)) & 1u) live[u] = false;
+  } else {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float lb = bf16_lb(warp_sum(s2[u]), qn_hi, e2);
+      if (lb > 0.f && __fmul_rd(lb, lb) > thr) live[u] = false;
+    }
   }
 }
 
@@ -2055,6 +2081,10 @@ constexpr int kRefUCtas = PARIS_REFU_CTAS;
 #define PARIS_REFU_U 2
 #endif
 constexpr int kRefUU = PARIS_REFU_U;  // rows in flight per warp at len <= 256
+#ifndef PARIS_REFU16_CTAS
+#define PARIS_REFU16_CTAS 4
+#endif
+constexpr int kRefU16Ctas = PARIS_REFU16_CTAS;  // with the bf16 pre-filter (more registers per warp)
 
 __global__ void __launch_bounds__(kNB) k_wave_cut(const unsigned* __restrict__ hist, unsigned wave_a,
                                                   unsigned* __restrict__ cut) {
@@ -2073,8 +2103,8 @@ __global__ void __launch_bounds__(kNB) k_wave_cut(const unsigned* __restrict__ h
   if (t == kNB - 1 && !reach) cut[b * kNB] = (unsigned)(kNB - 1);
 }
 
-template <int NC, int U>
-__global__ void __launch_bounds__(kRefThreads, NC <= 2 ? kRefUCtas : 2)
+template <int NC, int U, bool R16>
+__global__ void __launch_bounds__(kRefThreads, NC <= 2 ? (R16 ? kRefU16Ctas : kRefUCtas) : 2)
 k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
   constexpr int kPF = 2 * U;  // bf16 pre-filter rows per warp step (the bytes U fp32 rows would take)
   __shared__ unsigned s_refined[kMaxB], s_cnt[kMaxB], s_cut[kMaxB], s_r16[kMaxB];
@@ -2102,6 +2132,16 @@ k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     unsigned long long* bp = a.best + (size_t)b * kPadU64;
     unsigned nref = 0, nref16 = 0;
     uint64_t cur = kNoKey;
+    float qn_hi = 0.f;  // >= ||q|| (pre-filter only)
+    if (R16) {
+      float qs = 0.f;
+      for (int f = lane; f < (a.len >> 2); f += 32) {
+        const float4 v = __ldg(qv + f);
+        qs = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, qs))));
+      }
+      const float e2 = 2.f * (float)((a.len >> 5) + 8) * 5.9604644775390625e-08f;
+      qn_hi = __fsqrt_ru(__fmul_ru(warp_sum(qs), 1.f + e2));
+    }
     for (unsigned ch = first; ch < nchunk; ch += GW) {
       const unsigned i = ch * 32 + lane;
       const uint64_t k0 = i < cnt ? __ldg(list + i) : kNoKey;
@@ -2111,7 +2151,7 @@ k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
       const int bin = lb_bin(lb0, scale);
       const bool mine = i < cnt && (wave == 0 ? bin <= cutb : bin > cutb);
       unsigned m = __ballot_sync(0xffffffffu, mine && lb0 <= thr);
-      if (a.raw16) {
+      if (R16) {
         // bf16 pre-filter over kPF candidates at a time (their 2*len-byte rows in flight
         // together), then the survivors' fp32 rows U at a time
         while (m) {
@@ -2126,7 +2166,7 @@ k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
             lp[u] = has && key_val(kp[u]) <= thr;
             nref16 += lp[u] ? 1u : 0u;
           }
-          bf16_prefilter<NC, kPF>(a, qv, kp, lp, thr);
+          bf16_prefilter<NC, kPF>(a, qv, qn_hi, kp, lp, thr);
 #pragma unroll
           for (int g = 0; g < kPF; g += U) {
             uint64_t key[U];
@@ -2584,8 +2624,12 @@ cudaError_t launch_refine1(const RefineArgs& ra, int nb, int64_t max_work, cudaS
 
 template <int NC, int U>
 cudaError_t launch_refine1u(const RefineArgs& ra, int nb, int wave, const unsigned* cut, cudaStream_t st) {
+  if (ra.raw16) {
+    const int grid = sms() * (NC <= 2 ? kRefU16Ctas : 2);
+    return PARIS_LAUNCH("refine", (k_refine1u<NC, U, true>), grid, kRefThreads, 0, st, ra, nb, wave, cut);
+  }
   const int grid = sms() * (NC <= 2 ? kRefUCtas : 2);
-  return PARIS_LAUNCH("refine", (k_refine1u<NC, U>), grid, kRefThreads, 0, st, ra, nb, wave, cut);
+  return PARIS_LAUNCH("refine", (k_refine1u<NC, U, false>), grid, kRefThreads, 0, st, ra, nb, wave, cut);
 }
 
 // Allocate the batch scratch for `cap` candidates per query.
