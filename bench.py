@@ -242,7 +242,7 @@ def run_gpu(args):
     h2d_gbs = None
     # the bf16 copy of raw for the index path's refinement pre-filter (paris_raw_bf16), built once
     raw16, raw16_ms = None, None
-    if (args.raw16 or args.raw_host) and not args.no_raw16 and (args.path == "index" or args.both):
+    if not args.no_raw16 and (args.path == "index" or args.both):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         raw16 = P.raw_bf16(raw)
@@ -655,10 +655,9 @@ def main():
     ap.add_argument("--no-b1", action="store_true", help="skip the batch-1 LB roofline measurement")
     ap.add_argument("--sorted-refine", action="store_true",
                     help="k = 1: refine bucket-sorted lists (K5 scatter) instead of the unsorted waves (A/B)")
-    ap.add_argument("--raw16", action="store_true",
-                    help="index path with the bf16 refinement pre-filter (paris_knn_index_x); on by default "
-                         "with --raw-host, where it keeps the fp32 rows off PCIe")
-    ap.add_argument("--no-raw16", action="store_true", help="never use the bf16 pre-filter")
+    ap.add_argument("--raw16", action="store_true", help="(default) index path with the bf16 refinement "
+                    "pre-filter (paris_raw_bf16 + paris_knn_index_x)")
+    ap.add_argument("--no-raw16", action="store_true", help="index path without the bf16 pre-filter")
     ap.add_argument("--raw-host", action="store_true",
                     help="f3: keep the raw collection in pinned host memory (SAX/index in HBM)")
     ap.add_argument("--ref-sample", type=int, default=2_000_000)
