@@ -1903,24 +1903,27 @@ __device__ __forceinline__ void bf16_prefilter(const RefineArgs& a, const float4
     }
   }
   const float e2 = 2.f * (float)((a.len >> 5) + 8) * 5.9604644775390625e-08f;
-  if constexpr (U == 4) {
-    // four sums in one reduction: halves exchange two values (xor 16), then one
-    // (xor 8), then each 8-lane group finishes its own value; one ballot spreads
-    // the four decisions (lane 8u holds value u's sum)
+  if constexpr (U % 4 == 0) {
+    // four sums per reduction: halves exchange two values (xor 16), then one (xor 8),
+    // then each 8-lane group finishes its own value; one ballot spreads the four
+    // decisions (lane 8u holds value u's sum)
     const bool hi16 = lane & 16, hi8 = lane & 8;
-    float w0 = hi16 ? s2[2] : s2[0], w1 = hi16 ? s2[3] : s2[1];
-    w0 += __shfl_xor_sync(0xffffffffu, hi16 ? s2[0] : s2[2], 16);
-    w1 += __shfl_xor_sync(0xffffffffu, hi16 ? s2[1] : s2[3], 16);
-    float z = hi8 ? w1 : w0;
-    z += __shfl_xor_sync(0xffffffffu, hi8 ? w0 : w1, 8);
-    z += __shfl_xor_sync(0xffffffffu, z, 4);
-    z += __shfl_xor_sync(0xffffffffu, z, 2);
-    z += __shfl_xor_sync(0xffffffffu, z, 1);
-    const float lb = bf16_lb(z, qn_hi, e2);
-    const unsigned drop = __ballot_sync(0xffffffffu, lb > 0.f && __fmul_rd(lb, lb) > thr);
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if ((drop >> (8 * u)) & 1u) live[u] = false;
+    for (int g = 0; g < U; g += 4) {
+      float w0 = hi16 ? s2[g + 2] : s2[g], w1 = hi16 ? s2[g + 3] : s2[g + 1];
+      w0 += __shfl_xor_sync(0xffffffffu, hi16 ? s2[g] : s2[g + 2], 16);
+      w1 += __shfl_xor_sync(0xffffffffu, hi16 ? s2[g + 1] : s2[g + 3], 16);
+      float z = hi8 ? w1 : w0;
+      z += __shfl_xor_sync(0xffffffffu, hi8 ? w0 : w1, 8);
+      z += __shfl_xor_sync(0xffffffffu, z, 4);
+      z += __shfl_xor_sync(0xffffffffu, z, 2);
+      z += __shfl_xor_sync(0xffffffffu, z, 1);
+      const float lb = bf16_lb(z, qn_hi, e2);
+      const unsigned drop = __ballot_sync(0xffffffffu, lb > 0.f && __fmul_rd(lb, lb) > thr);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if ((drop >> (8 * u)) & 1u) live[g + u] = false;
+    }
   } else {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -2085,6 +2088,10 @@ constexpr int kRefUU = PARIS_REFU_U;  // rows in flight per warp at len <= 256
 #define PARIS_REFU16_CTAS 4
 #endif
 constexpr int kRefU16Ctas = PARIS_REFU16_CTAS;  // with the bf16 pre-filter (more registers per warp)
+#ifndef PARIS_REFU16_MUL
+#define PARIS_REFU16_MUL 2
+#endif
+constexpr int kPFMul = PARIS_REFU16_MUL;  // bf16 rows per warp step = kPFMul x U
 
 __global__ void __launch_bounds__(kNB) k_wave_cut(const unsigned* __restrict__ hist, unsigned wave_a,
                                                   unsigned* __restrict__ cut) {
@@ -2106,7 +2113,7 @@ __global__ void __launch_bounds__(kNB) k_wave_cut(const unsigned* __restrict__ h
 template <int NC, int U, bool R16>
 __global__ void __launch_bounds__(kRefThreads, NC <= 2 ? (R16 ? kRefU16Ctas : kRefUCtas) : 2)
 k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
-  constexpr int kPF = 2 * U;  // bf16 pre-filter rows per warp step (the bytes U fp32 rows would take)
+  constexpr int kPF = kPFMul * U;  // bf16 pre-filter rows per warp step
   __shared__ unsigned s_refined[kMaxB], s_cnt[kMaxB], s_cut[kMaxB], s_r16[kMaxB];
   __shared__ float s_scale[kMaxB];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
