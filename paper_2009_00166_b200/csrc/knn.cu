@@ -55,11 +55,6 @@ constexpr int kPadU64 = 16;
 constexpr uint32_t kHalf2One = 0x3C003C00u;
 constexpr uint32_t kHalfNeg1 = 0xBC00u;
 
-__device__ __forceinline__ float fmax3(float a, float b, float c) {
-  float r;
-  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
-  return r;
-}
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -219,25 +214,6 @@ __device__ __forceinline__ void lb16_group(const uint8_t* __restrict__ sax, int6
 #pragma unroll
         for (int p = 0; p < P; ++p) acc[j][p] = 0x7C007C00u;
   }
-}
-
-// Rigorous fp32 LB^2 sum (without the len/w factor) of series i (byte j of the
-// words at i0) for one query interval q[s] = {q_lo, q_hi}: outward-rounded
-// region bounds, every operation rounded toward -inf, so the result is <= the
-// exact sum of delta^2 of the exact query PAA.
-template <bool AL>
-__device__ float lb32_series(const uint8_t* __restrict__ sax, int64_t n, int w, int64_t i0, int j,
-                             const float2* __restrict__ q, const float2* __restrict__ s_lu) {
-  float acc = 0.f;
-  for (int s = 0; s < w; ++s) {
-    const uint32_t word = load_word<AL>(sax, n, s, i0);
-    const float2 lu = s_lu[(word >> (8 * j)) & 0xFFu];
-    const float above = __fsub_rd(q[s].x, lu.y);  // q_lo - U_up <= q - U
-    const float below = __fsub_rd(lu.x, q[s].y);  // L_dn - q_hi <= L - q
-    const float delta = fmax3(above, below, 0.f);
-    acc = __fmaf_rd(delta, delta, acc);
-  }
-  return acc;
 }
 
 // Query PAA in fp64 (segment means) for the B = 2P slots of a batch:
@@ -882,7 +858,7 @@ constexpr int kTW = 16;
 constexpr size_t kTileBytes = (size_t)kTW * kTS;
 constexpr size_t kTSmem = kStages * kTileBytes + kMaxCard * 32 * 4;
 // k_lbi: 2-stage ring + the 32-copy pair-form table (64 KB) + the LB histograms
-constexpr int kIStages = 2;      // compute-bound on the live items: a tile's load (~0.8 us) < its work
+constexpr int kIStages = 2;      // 2 x 32 KB; the table and histograms take the rest of shared memory
 constexpr int kIThreads = 768;   // 24 warps: more warps to hide the lookup -> math latency chain
 constexpr int kIWarps = kIThreads / 32;
 constexpr int kITileIds = 512;   // tile ids staged per CTA (148 CTAs: 155 M series; beyond, global loads)
