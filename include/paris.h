@@ -189,7 +189,8 @@ int paris_raw_bf16(const float* raw, int64_t n, int32_t len, uint16_t* out, void
  * with fp32 error margins and directed roundings; a candidate whose bound exceeds
  * the live BSF is dropped without reading its fp32 row (same exact results).
  *   raw_bf16  device [n][len] bf16 (paris_raw_bf16 of `raw`), 16-byte aligned,
- *             len % 8 == 0; NULL = paris_knn_index_ex.  k > 1 ignores it.
+ *             len % 8 == 0; NULL = paris_knn_index_ex.  k > 1 ignores it, and so
+ *             does raw in device memory with len < 256 (no gain on short rows).
  */
 int paris_knn_index_x(const float* raw, const uint16_t* raw_bf16, const uint8_t* sax_sorted, const uint32_t* perm,
                       const uint8_t* env, int64_t n, const float* queries, int32_t nq, int32_t k, int64_t* out_idx,

@@ -2757,7 +2757,9 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
   ra.count = ws.count; ra.thr_seed = ws.thr_seed; ra.thr = ws.thr; ra.best = ws.best;
   ra.refined = ws.refined; ra.lists = ws.lists; ra.k = p.k; ra.d2up = p.d2up;
   ra.lo = 0; ra.hi = 0xFFFFFFFFu; ra.n = p.n;
-  ra.raw16 = p.k == 1 ? p.raw16 : nullptr;
+  // the pre-filter pays when its rows save real bytes: rows of len >= 256 in HBM
+  // (C3's 512-byte rows refine faster without it), any len when raw is on the host
+  ra.raw16 = (p.k == 1 && (p.raw_host || p.len >= 256)) ? p.raw16 : nullptr;
   ra.refined16 = ws.updates;
   dim3 g((unsigned)p.XB, (unsigned)nb);
   if (p.k == 1) {
