@@ -31,10 +31,10 @@ sys.path.insert(0, ROOT)
 
 CONFIGS = {
     1: dict(n=100_000, len=256, nq=100, k=1, queries="fresh", desc="C1: 1e5 x 256 fp32 RW, 100 fresh RW queries, exact 1-NN"),
-    2: dict(n=1_000_000, len=256, nq=1000, k=1, queries="noise0.05", desc="C2: 1e6 x 256 fp32 RW, 1000 member+N(0,0.05^2) queries, exact 1-NN"),
+    2: dict(n=1_000_000, len=256, nq=1000, k=1, queries="noise0.05", desc="C2: 1e6 x 256 fp32 RW, 1000 member+N(0,0.05^2) queries, exact 1-NN (line); 'sweep': k = 10"),
     3: dict(n=10_000_000, len=128, nq=1000, k=1, queries="fresh", call=64, desc="C3: 1e7 x 128 fp32 RW, 1000 fresh RW queries in calls of 64, exact 1-NN"),
     4: dict(n=100_000_000, len=256, nq=100, k=1, queries="fresh", desc="C4: 1e8 x 256 fp32 RW (102.4 GB raw + 1.6 GB SAX in HBM), 100 fresh RW queries, exact 1-NN"),
-    5: dict(n=20_000_000, len=256, nq=200, k=1, queries="noise0.05", desc="C5: 2e7 x 256 fp32 RW, 200 member+N(0,0.05^2) queries, exact 1-NN"),
+    5: dict(n=20_000_000, len=256, nq=200, k=1, queries="noise0.05", desc="C5: 2e7 x 256 fp32 RW, 200 member+N(0,0.05^2) queries, exact 1-NN (line); 'sweep': 5 sets x 200 queries, sigma in {0.01..0.2}, k = 1 and 100"),
 }
 W, CARD = 16, 256
 ALU_CLOCK_GHZ = 1.965  # B200 clocks.max.sm (B200_PROFILING.md)
@@ -301,6 +301,19 @@ def run_gpu(args):
         torch.cuda.synchronize()
         index_ms = e0.elapsed_time(e1)
     peak, peak_src = measured_peaks()
+    # read-only streaming peak: the library's 16-byte read probe over >= 8 GB
+    read_peak = None
+    if not args.raw_host:
+        probe = raw if raw.numel() * 4 >= (8 << 30) else torch.empty(8 << 30, dtype=torch.uint8, device=dev)
+        P.debug_read_probe(probe)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            P.debug_read_probe(probe)
+        e1.record()
+        torch.cuda.synchronize()
+        read_peak = 3.0 * probe.numel() * probe.element_size() / (e0.elapsed_time(e1) / 1e3) / 1e9
+        del probe
 
     def measure_path(path: str, full: bool):
         """Warm up, time K steps of `path` (device events, max over ranks), then the same K
@@ -454,6 +467,36 @@ def run_gpu(args):
     if args.both:
         secondary = measure_path("flat" if args.path in ("index", "nb") else "index", False)
 
+    def timed_index(qsrc, kk):
+        """q/s and pruning of the index path on a query set (events, max over ranks)."""
+        kc = P.KnnConfig(batch=args.batch or 64, index_seeds=args.index_seeds)
+        _, _, stq = P.knn_index(raw, index, qsrc, k=kk, config=kc, stats=True, raw16=raw16)
+        torch.cuda.synchronize()
+        e0.record(st)
+        for _ in range(args.steps):
+            for c0 in range(0, qsrc.shape[0], call_q):
+                P.knn_index(raw, index, qsrc[c0:c0 + call_q], k=kk, config=kc, raw16=raw16)
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = reduce_max_ms(e0.elapsed_time(e1) / args.steps, dev, ws)
+        ref = stq["refined"].numpy().astype(np.float64)
+        return {"k": kk, "queries": int(qsrc.shape[0]), "value": weak_throughput(int(qsrc.shape[0]), ws, ms),
+                "unit": "queries/s", "ms_per_step": ms,
+                "candidates_mean": float(stq["candidates"].numpy().astype(np.float64).mean()),
+                "refined_mean": float(ref.mean()), "pruning_ratio": float(1.0 - ref.mean() / n),
+                "raw16_rows_mean": float(stq["raw16_rows"].numpy().astype(np.float64).mean())}
+
+    sweep = None
+    if index is not None and not args.no_sweep and not args.raw_host:
+        if args.config == 2:  # BASELINE config 2: exact 1-NN and k = 10
+            sweep = [dict(timed_index(queries, 10), sigma=0.05)]
+        elif args.config == 5:  # config 5: 5 sets x 200 member + N(0, sigma^2) queries, k = 1 and 100
+            sweep = []
+            for si, sig in enumerate((0.01, 0.02, 0.05, 0.1, 0.2)):
+                qset, _ = dg.noisy_members(raw, nq, sig, qs + 101 * (si + 1))
+                for kk in (1, 100):
+                    sweep.append(dict(timed_index(qset, kk), sigma=sig))
+
     def knn_flat(qsrc, **kw):
         return P.knn_exact(raw, sax, qsrc, k=k, w=W, card=CARD, **kw)
     stats, kern, roof = primary["stats"], primary["kern"], primary["roof"]
@@ -520,13 +563,17 @@ def run_gpu(args):
                        "raw_bf16": None if raw16 is None else {"build_ms": raw16_ms, "bytes": raw16.numel() * 2}, "parallelism": f"weak x{ws} (independent collections + queries per GPU)",
                        "l2": "inputs larger than L2 (no flush)",
                        "raw": "pinned host memory (f3)" if args.raw_host else "HBM"},
-            "roofline": roof,
+            "roofline": dict(roof, read_peak_gbs=read_peak,
+                             frac_of_read_peak=(roof["achieved"] / read_peak
+                                                if read_peak and roof and roof.get("unit") == "GB/s" else None))
+                        if roof else roof,
             "lb_batch1": lb1,
             "other_path": None if secondary is None else {
                 "path": secondary["path"], "value": secondary["value"], "ms_per_step": secondary["step_ms"],
                 "roofline": secondary["roof"], "kernels": secondary["kern"],
                 "candidates_mean": float(secondary["cand"].mean()), "refined_mean": float(secondary["refined"].mean())},
             "cpu_baseline": cpu,
+            "sweep": sweep,
             "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": nq * length * 4,
                     "d2h_bytes_per_step": nq * k * 12},
             "gpu_launches": launches,
@@ -658,6 +705,7 @@ def main():
     ap.add_argument("--raw16", action="store_true", help="(default) index path with the bf16 refinement "
                     "pre-filter (paris_raw_bf16 + paris_knn_index_x)")
     ap.add_argument("--no-raw16", action="store_true", help="index path without the bf16 pre-filter")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the C2 k=10 / C5 sigma x k sweeps")
     ap.add_argument("--raw-host", action="store_true",
                     help="f3: keep the raw collection in pinned host memory (SAX/index in HBM)")
     ap.add_argument("--ref-sample", type=int, default=2_000_000)

@@ -234,6 +234,11 @@ int32_t paris_version(void);  /* 104: paris_raw_bf16, paris_knn_index_x */
  * out[0..card-2] (host memory).  PARIS_ECONFIG for a bad card. */
 int paris_debug_cuts(int32_t card, double* out);
 
+/* Measurement hook: stream `bytes` of device memory at p with read-only 16-byte
+ * loads (no writes) -- the read-only HBM peak beside MEASURED_PEAKS.json's copy
+ * peak (bench.py times it).  Asynchronous on `stream`. */
+int paris_debug_read_probe(const void* p, int64_t bytes, void* stream);
+
 /* Test hook: IEEE binary16 bits of v rounded toward -inf (dir < 0) or +inf
  * (dir > 0) -- the directed rounding behind the batched fp16 lower bound. */
 uint16_t paris_debug_half_dir(double v, int32_t dir);

@@ -104,6 +104,8 @@ def load():
         lib.paris_launch_count.restype = i64
         lib.paris_debug_cuts.argtypes = [i32, P]
         lib.paris_debug_cuts.restype = ctypes.c_int
+        lib.paris_debug_read_probe.argtypes = [P, i64, P]
+        lib.paris_debug_read_probe.restype = ctypes.c_int
         lib.paris_debug_half_dir.argtypes = [ctypes.c_double, i32]
         lib.paris_debug_half_dir.restype = ctypes.c_uint16
         _lib = lib
@@ -345,6 +347,12 @@ def profile_read() -> dict:
 
 def launch_count() -> int:
     return int(load().paris_launch_count())
+
+
+def debug_read_probe(t: torch.Tensor, stream=None):
+    """Stream the bytes of a CUDA tensor with read-only loads (the read-only HBM peak probe)."""
+    _need_cuda(t, "t")
+    _check(load().paris_debug_read_probe(t.data_ptr(), t.numel() * t.element_size() // 16 * 16, _stream(stream)))
 
 
 def debug_half_dir(v: float, direction: int) -> int:

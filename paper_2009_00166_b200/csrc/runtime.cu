@@ -275,7 +275,38 @@ const CardTables* device_tables(int card) {
 }  // namespace paris
 
 // ------------------------------------------------------------------ C ABI (misc)
+namespace paris {
+namespace {
+// Read-only streaming probe (the read peak beside the copy peak):
+// grid-stride 16-byte non-allocating loads folded into one word per thread.
+__global__ void __launch_bounds__(512) k_read_probe(const uint4* __restrict__ p, int64_t n16, unsigned* out) {
+  uint32_t x = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p + i));
+    x ^= v.x ^ v.y ^ v.z ^ v.w;
+  }
+  if (x == 0x9E3779B9u) out[0] = x;  // keeps the loads live; practically never taken
+}
+}  // namespace
+}  // namespace paris
+
 extern "C" {
+
+int paris_debug_read_probe(const void* p, int64_t bytes, void* stream) {
+  if (!p || bytes < 16 || (reinterpret_cast<uintptr_t>(p) & 15)) return PARIS_EINVAL;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static unsigned* sink = nullptr;
+  if (!sink && cudaMalloc(&sink, 4) != cudaSuccess) return PARIS_ENOMEM;
+  PARIS_CHECK_LAUNCH(PARIS_LAUNCH("read_probe", paris::k_read_probe, sms * 4, 512, 0, (cudaStream_t)stream,
+                                  reinterpret_cast<const uint4*>(p), bytes / 16, sink),
+                     "read probe launch");
+  return 0;
+}
+
 
 const char* paris_last_error(void) { return paris::g_err.c_str(); }
 
