@@ -2843,7 +2843,10 @@ void plan_seed(Plan& p, int seed_div) {
   if (p.perm) {
     p.ns = 0;
     p.seed_grid = 0;
-    p.S = std::max(p.k, std::min(kMaxSeed, p.idx_seeds > 0 ? p.idx_seeds : kIdxSeeds));
+    // default: 1024 series around the leaf; for k > 1, 32 per requested neighbour (the
+    // k-th best of the seeds must bound the k-th NN distance tightly), up to kMaxSeed
+    const int dflt = std::max(kIdxSeeds, std::min(kMaxSeed, 32 * p.k));
+    p.S = std::max(p.k, std::min(kMaxSeed, p.idx_seeds > 0 ? p.idx_seeds : dflt));
     return;
   }
   p.ns = std::min<int64_t>(p.n, std::max<int64_t>(p.n / seed_div, std::min<int64_t>(p.n, 65536)));
