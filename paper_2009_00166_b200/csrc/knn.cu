@@ -709,9 +709,12 @@ __device__ __forceinline__ void hist16_add(unsigned* s_h16, int idx, unsigned* g
   }
 }
 
-// s_hist: the CTA's shared-memory LB histogram [kMaxB][kNB] (flushed at kernel end);
-// HIST16: the packed 16-bit form (hist16_add)
-template <bool HIST16 = false>
+// s_hist: the CTA's shared-memory LB histogram (flushed at kernel end).  HMODE 0:
+// [kMaxB][kNB] 32-bit; 1: the packed 16-bit form (hist16_add); 2: coarse, kNBC
+// 32-bit bins per slot (bin >> 3) -- enough for the k = 1 wave cut, which only needs
+// a quantile (flushed to fine bin 8c + 7 of each coarse group c).
+constexpr int kNBC = kNB / 8;
+template <int HMODE = 0>
 __device__ void wb_flush(WarpBuf& wb, int nslots, const LbConsts& c, const LbArgs& a, unsigned* s_hist) {
   const int lane = threadIdx.x & 31;
   __syncwarp();
@@ -732,9 +735,10 @@ __device__ void wb_flush(WarpBuf& wb, int nslots, const LbConsts& c, const LbArg
     // bucket offsets must describe exactly the `cap` entries K5 orders
     if ((int64_t)pos < a.cap) {
       a.cand[(size_t)b * a.cap + pos] = key;
-      const int idx = b * kNB + lb_bin(key_val(key), c.scale[b]);
-      if (HIST16) hist16_add(s_hist, idx, a.hist);
-      else atomicAdd(&s_hist[idx], 1u);
+      const int bin = lb_bin(key_val(key), c.scale[b]);
+      if (HMODE == 1) hist16_add(s_hist, b * kNB + bin, a.hist);
+      else if (HMODE == 2) atomicAdd(&s_hist[b * kNBC + (bin >> 3)], 1u);
+      else atomicAdd(&s_hist[b * kNB + bin], 1u);
     }
   }
   __syncwarp();
@@ -868,6 +872,7 @@ constexpr int kITileIds = 512;   // tile ids staged per CTA (148 CTAs: 155 M ser
 // leaves and the kernel checks the layout fits (kLbiSmem below, set at launch).
 constexpr size_t kITabBytes = (size_t)kMaxCard * 32 * 8;
 constexpr size_t kIHistBytes = (size_t)kMaxB * kNB * 2;
+constexpr size_t kIHistCBytes = (size_t)kMaxB * (kNB / 8) * 4;  // coarse (k = 1) histograms
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -1096,6 +1101,7 @@ k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
 // sb = high half, sb < 0: none).  Same tests and warp buffer as lb_emit_wb.
 __device__ __forceinline__ uint32_t half_of(uint32_t v, int h) { return (v >> (16 * h)) & 0xFFFFu; }
 
+template <int HMODE>
 __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int sb, int64_t i0, int nvalid,
                                          int nslots, const LbConsts& c, const LbArgs& a, WarpBuf& wb,
                                          unsigned* s_hist) {
@@ -1133,7 +1139,7 @@ __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int s
     if (lane >= o) incl += v;
   }
   const int total = __shfl_sync(0xffffffffu, incl, 31);
-  if (wb.n + total > kWB) wb_flush<true>(wb, nslots, c, a, s_hist);
+  if (wb.n + total > kWB) wb_flush<HMODE>(wb, nslots, c, a, s_hist);
   // (static bit loops: lbv stays in registers)
   if (total > kWB) {  // degenerate (e.g. tau = inf): straight to global memory
 #pragma unroll
@@ -1143,7 +1149,8 @@ __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int s
       const unsigned pos = atomicAdd(&a.count[sl], 1u);
       if ((int64_t)pos < a.cap) {
         a.cand[(size_t)sl * a.cap + pos] = make_key(lbv[j][bit & 1], __ldg(a.perm + i0 + j));
-        atomicAdd(&a.hist[sl * kNB + lb_bin(lbv[j][bit & 1], c.scale[sl])], 1u);
+        const int fb = lb_bin(lbv[j][bit & 1], c.scale[sl]);
+        atomicAdd(&a.hist[sl * kNB + (HMODE == 2 ? (fb | 7) : fb)], 1u);
       }
     }
     return;
@@ -1266,35 +1273,42 @@ k_blkmask(LbArgs a, unsigned long long* __restrict__ bmask, unsigned* __restrict
   if (tid < NS && s_blk[tid]) atomicAdd(&blocks[tid], s_blk[tid]);
 }
 
-template <int P>
+// HC (k = 1 with the unsorted refine waves): coarse LB histograms (8 KB) below the
+// table, so a third 32 KB ring stage fits; else the 16-bit 256-bin histograms
+// (k > 1 and the sorted walk order candidates by them exactly) and two stages.
+template <int P, bool HC>
 __global__ void __launch_bounds__(kIThreads, 1)
 k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __restrict__ tile_list,
       const unsigned* __restrict__ tile_count) {
+  constexpr int NST = HC ? 3 : 2;  // ring stages
   extern __shared__ __align__(128) uint8_t dsm[];
-  uint8_t* s_tiles = dsm;
-  // the table at the first 64 KB-aligned shared address past the ring, so one byte
-  // permute builds a lookup's full address: {lane*8, symbol, table address bits 16-31}
+  // the table sits at a 64 KB-aligned shared address, so one byte permute builds a
+  // lookup's full address: {lane*8, symbol, table address bits 16-31}.
+  //   HC:  [coarse hist][pad][table][ring x 3]     else: [ring x 2][pad][table][hist16]
   const uint32_t dsm_s = smem_u32(dsm);
-  const uint32_t ring_end = dsm_s + (uint32_t)(kIStages * kTileBytes);
-  const uint32_t tab_s = (ring_end + 0xFFFFu) & ~0xFFFFu;
+  const uint32_t tab_s = HC ? ((dsm_s + (uint32_t)kIHistCBytes + 0xFFFFu) & ~0xFFFFu)
+                            : ((dsm_s + (uint32_t)(NST * kTileBytes) + 0xFFFFu) & ~0xFFFFu);
   const uint32_t tab_off = tab_s - dsm_s;
+  uint8_t* s_tiles = HC ? dsm + tab_off + kITabBytes : dsm;
   {
     uint32_t dyn;
     asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
-    if ((size_t)tab_off + kITabBytes + kIHistBytes > dyn) __trap();  // launch config inconsistent with the layout
+    const size_t need = (size_t)tab_off + kITabBytes + (HC ? (size_t)NST * kTileBytes : kIHistBytes);
+    if (need > dyn) __trap();  // launch config inconsistent with the layout
   }
   // region table in pair form {(-U16,-U16), (L16,L16)}, 32 copies: entry c of lane l
   // at byte 256c + 8l, so ONE byte permute forms the address (symbol byte -> bits
   // 8..15, lane*8 -> bits 0..7; no multiply); a 64-bit load is served per half-warp
   // and the 16 lanes of each half hit distinct banks
   uint2* s_tab = reinterpret_cast<uint2*>(dsm + tab_off);
-  unsigned* s_hist = reinterpret_cast<unsigned*>(dsm + tab_off + kITabBytes);  // [kMaxB][kNB] 16-bit (hist16_add)
-  __shared__ __align__(8) uint64_t s_full[kIStages];
-  __shared__ unsigned s_cnt[kIStages];
+  unsigned* s_hist = HC ? reinterpret_cast<unsigned*>(dsm)                        // [kMaxB][kNBC] coarse
+                        : reinterpret_cast<unsigned*>(dsm + tab_off + kITabBytes);  // [kMaxB][kNB] 16-bit
+  __shared__ __align__(8) uint64_t s_full[NST];
+  __shared__ unsigned s_cnt[NST];
   // per stage: the tile's id and its 32 block masks, delivered with the tile (the
   // warps never wait on a global load at a tile boundary)
-  __shared__ __align__(16) unsigned long long s_bm[kIStages][kBPT];
-  __shared__ int64_t s_tile[kIStages];
+  __shared__ __align__(16) unsigned long long s_bm[NST][kBPT];
+  __shared__ int64_t s_tile[NST];
   // this CTA's share of the tile list (entries blockIdx.x + i * gridDim.x), staged once:
   // a refill then starts its TMA without a dependent global load
   __shared__ unsigned s_tl[kITileIds];
@@ -1307,7 +1321,7 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
   WarpBuf& wb = s_wb[warp];
   for (int b = lane; b < kMaxB; b += 32) wb.cnt[b] = 0;
   if (lane == 0) wb.n = 0;
-  for (int i = tid; i < nslots * kNB / 2; i += kIThreads) s_hist[i] = 0;
+  for (int i = tid; i < (HC ? nslots * kNBC : nslots * kNB / 2); i += kIThreads) s_hist[i] = 0;
 
   static_assert(kTS == PARIS_INDEX_TILE, "index tiles are the LB kernel's tiles");
   auto issue = [&](int64_t li, int st) {
@@ -1323,7 +1337,7 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
     bulk_g2s(&s_bm[st][0], bmask + (size_t)tile * kBPT, (unsigned)(kBPT * 8), &s_full[st]);
   };
   if (tid == 0) {
-    for (int st = 0; st < kIStages; ++st) {
+    for (int st = 0; st < NST; ++st) {
       mbar_init(&s_full[st], 1);
       s_cnt[st] = 0;
     }
@@ -1336,7 +1350,7 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
   }
   __syncthreads();
   if (tid == 0) {
-    for (int st = 0; st < kIStages; ++st) {
+    for (int st = 0; st < NST; ++st) {
       const int64_t li = blockIdx.x + (int64_t)st * gridDim.x;
       if (li < nlist) issue(li, st);
     }
@@ -1354,8 +1368,8 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
   for (int64_t it = 0;; ++it) {
     const int64_t li = blockIdx.x + it * gridDim.x;
     if (li >= nlist) break;
-    const int st = (int)(it % kIStages);
-    mbar_wait(&s_full[st], (unsigned)((it / kIStages) & 1));
+    const int st = (int)(it % NST);
+    mbar_wait(&s_full[st], (unsigned)((it / NST) & 1));
     const int64_t tile = s_tile[st];
     PARIS_DCHECK(tile >= 0 && tile * kTS < a.n);
     // the tile's 32 block masks (lane = block); a block's live slots are computed two
@@ -1412,13 +1426,13 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
       const int64_t i0 = tile * kTS + k * PARIS_INDEX_BLOCK + 4 * hl;
       const int nvalid = active ? (int)std::max<int64_t>(0, imin64(4, a.n - i0)) : 0;
       PARIS_DCHECK(k < kBPT && sa >= 0 && sa < nslots && sb < nslots);
-      lbi_emit(acc, sa, sb, i0, nvalid, nslots, s_c, a, wb, s_hist);
+      lbi_emit<HC ? 2 : 1>(acc, sa, sb, i0, nvalid, nslots, s_c, a, wb, s_hist);
     }
     __syncwarp();
     if (lane == 0) {
       if (atomicAdd(&s_cnt[st], 1u) == kIWarps - 1) {
         s_cnt[st] = 0;
-        const int64_t next = li + (int64_t)kIStages * gridDim.x;
+        const int64_t next = li + (int64_t)NST * gridDim.x;
         if (next < nlist) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           issue(next, st);
@@ -1426,11 +1440,16 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
       }
     }
   }
-  wb_flush<true>(wb, nslots, s_c, a, s_hist);
+  wb_flush<HC ? 2 : 1>(wb, nslots, s_c, a, s_hist);
   __syncthreads();
-  for (int i = tid; i < nslots * kNB; i += kIThreads) {
-    const unsigned v = (s_hist[i >> 1] >> (16 * (i & 1))) & 0xFFFFu;
-    if (v) atomicAdd(&a.hist[i], v);
+  if (HC) {
+    for (int i = tid; i < nslots * kNBC; i += kIThreads)
+      if (s_hist[i]) atomicAdd(&a.hist[(i / kNBC) * kNB + (i % kNBC) * 8 + 7], s_hist[i]);
+  } else {
+    for (int i = tid; i < nslots * kNB; i += kIThreads) {
+      const unsigned v = (s_hist[i >> 1] >> (16 * (i & 1))) & 0xFFFFu;
+      if (v) atomicAdd(&a.hist[i], v);
+    }
   }
 }
 
@@ -2481,8 +2500,8 @@ cudaError_t launch_lbt(const Plan& p, const uint8_t* sax, int nb, const CardTabl
                       ws.seed_ids, p.S);
 }
 
-template <int P>
-size_t& lbi_smem() {  // dynamic shared memory of k_lbi<P> (set once per device)
+template <int P, bool HC>
+size_t& lbi_smem() {  // dynamic shared memory of k_lbi<P, HC> (set once per device)
   static size_t v = 0;
   return v;
 }
@@ -2494,13 +2513,18 @@ cudaError_t launch_index_lb(const Plan& p, const uint8_t* sax, int nb, const Car
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    cudaFuncAttributes fa;
-    cudaError_t e = cudaFuncGetAttributes(&fa, k_lbi<P>);
-    if (e != cudaSuccess) return e;
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    lbi_smem<P>() = (size_t)optin - fa.sharedSizeBytes;
-    e = cudaFuncSetAttribute(k_lbi<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lbi_smem<P>());
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, k_lbi<P, false>);
+    if (e != cudaSuccess) return e;
+    lbi_smem<P, false>() = (size_t)optin - fa.sharedSizeBytes;
+    e = cudaFuncSetAttribute(k_lbi<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lbi_smem<P, false>());
+    if (e != cudaSuccess) return e;
+    e = cudaFuncGetAttributes(&fa, k_lbi<P, true>);
+    if (e != cudaSuccess) return e;
+    lbi_smem<P, true>() = (size_t)optin - fa.sharedSizeBytes;
+    e = cudaFuncSetAttribute(k_lbi<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lbi_smem<P, true>());
     if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
@@ -2515,8 +2539,11 @@ cudaError_t launch_index_lb(const Plan& p, const uint8_t* sax, int nb, const Car
                                ws.tile_count, ws.blocks);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(sms(), ntiles);
-  return PARIS_LAUNCH("lb_pass", k_lbi<P>, grid, kIThreads, lbi_smem<P>(), st, la, ws.bmask, ws.tile_list,
-                      ws.tile_count);
+  if (p.k == 1 && !p.sorted_refine)  // coarse histograms suffice for the wave cut: 3 ring stages
+    return PARIS_LAUNCH("lb_pass", (k_lbi<P, true>), grid, kIThreads, (lbi_smem<P, true>()), st, la, ws.bmask,
+                        ws.tile_list, ws.tile_count);
+  return PARIS_LAUNCH("lb_pass", (k_lbi<P, false>), grid, kIThreads, (lbi_smem<P, false>()), st, la, ws.bmask,
+                      ws.tile_list, ws.tile_count);
 }
 
 cudaError_t dispatch_index_lb(int nb, const Plan& p, const uint8_t* sax, const CardTables* tab, const Ws& ws,
