@@ -2144,9 +2144,15 @@ k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
       const float e2 = 2.f * (float)((a.len >> 5) + 8) * 5.9604644775390625e-08f;
       qn_hi = __fsqrt_ru(__fmul_ru(warp_sum(qs), 1.f + e2));
     }
+    // the next chunk's keys are loaded while this chunk is processed
+    uint64_t knext = (first * 32 + lane < cnt) ? __ldg(list + first * 32 + lane) : kNoKey;
     for (unsigned ch = first; ch < nchunk; ch += GW) {
       const unsigned i = ch * 32 + lane;
-      const uint64_t k0 = i < cnt ? __ldg(list + i) : kNoKey;
+      const uint64_t k0 = knext;
+      {
+        const unsigned in = (ch + GW) * 32 + lane;
+        knext = (ch + GW < nchunk && in < cnt) ? __ldg(list + in) : kNoKey;
+      }
       cur = min(cur, ld_relaxed_u64(bp));
       float thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
       const float lb0 = key_val(k0);
