@@ -1777,6 +1777,7 @@ struct RefineArgs {
   int64_t n;                 // series in raw (debug bounds checks)
   const uint16_t* raw16 = nullptr;  // optional bf16 copy of raw [n][len] (paris_raw_bf16): pre-filter
   unsigned* refined16 = nullptr;    // per query: bf16 rows read by the pre-filter
+  unsigned* ghist = nullptr;        // k > 1: per query, histogram of refined exact d^2 (kNB bins of tau_seed^2)
 };
 
 // One warp step: up to kU candidates (indices i0 + u*stride) against the live
@@ -2247,6 +2248,7 @@ k_refine_topk(RefineArgs a) {
   const uint64_t* list = a.sorted + (size_t)b * a.cap;
   const unsigned gw = blockIdx.x * kRefWarps + warp, GW = gridDim.x * kRefWarps;
   unsigned nref = 0;
+  unsigned round_no = 0;
   bool done = false;
   for (unsigned i0 = gw;; i0 += kU * GW) {
     if (!done && i0 < cnt) {
@@ -2260,6 +2262,10 @@ k_refine_topk(RefineArgs a) {
         if (d2[u] < INFINITY) {
           const uint64_t k2 = make_key(d2[u], key_id(key[u]));
           if (k2 < kk && lane == 0) s_pend[atomicAdd(&s_np, 1)] = k2;
+          // the query-wide histogram of exact distances (all CTAs): its k-th count
+          // bounds the global k-th distance, which one CTA's own top-k cannot
+          const float f = d2[u] * scale;
+          if (lane == 0 && f < (float)(kNB - 2)) atomicAdd(&a.ghist[b * kNB + (int)f], 1u);
         }
       }
     } else {
@@ -2299,6 +2305,41 @@ k_refine_topk(RefineArgs a) {
           const float up = __fmul_ru(key_val(kk), a.d2up);
           s_thr_local = up;
           atomicMin(&a.thr[b * kPadU32], __float_as_uint(up));
+        }
+      }
+    }
+    // every 4th round: the query-wide threshold from the histogram -- at least k refined
+    // series have fp32 d^2 < (t + 2) / scale (one bin of slack for the rounding of
+    // d^2 * scale), so the global k-th exact d^2 <= that edge x d2up
+    if (warp == 0 && (++round_no & 3) == 0 && scale > 0.f) {
+      const uint4 h0 = __ldcg(reinterpret_cast<const uint4*>(a.ghist + b * kNB + 8 * lane));  // L2: the atomics' copy
+      const uint4 h1 = __ldcg(reinterpret_cast<const uint4*>(a.ghist + b * kNB + 8 * lane + 4));
+      const unsigned hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+      unsigned own = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) own += hv[i];
+      unsigned incl = own;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const unsigned reach = __ballot_sync(0xffffffffu, incl >= (unsigned)k);
+      if (reach) {
+        const int L = __ffs(reach) - 1;
+        if (lane == L) {
+          unsigned c = incl - own;
+          int t = 8 * L;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            c += hv[i];
+            if (c >= (unsigned)k) { t = 8 * L + i; break; }
+          }
+          const float up = __fmul_ru(__fdiv_ru((float)(t + 2), scale), a.d2up);
+          if (up < s_thr_local) {
+            s_thr_local = up;
+            atomicMin(&a.thr[b * kPadU32], __float_as_uint(up));
+          }
         }
       }
     }
@@ -2400,6 +2441,7 @@ struct Ws {
   unsigned* blocks;      // index mode: blocks whose envelope bound passed, per query
   unsigned* tile_count;  // index mode: live tiles listed
   unsigned* updates;     // nb mode: V_bsf updates per query
+  unsigned* ghist;       // k > 1: refined-distance histograms [B][kNB]
   unsigned long long* bmask;  // index mode: [ntiles*32] per-block live query-slot masks
   unsigned* tile_list;   // index mode: live tiles
   unsigned* tile_flag;   // index mode: [ntiles] tile already listed (zeroed per batch)
@@ -2657,7 +2699,7 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   const size_t o_q16 = take(sizeof(uint2) * (B / 2) * kMaxW);
   const size_t o_sid = take(sizeof(int) * B * p.S);
   const size_t o_skey = take(sizeof(uint64_t) * B * p.S);
-  const size_t zb = sizeof(unsigned) * (B + B + B * kNB + B * kNB + B + B + 1 + B);
+  const size_t zb = sizeof(unsigned) * (B + B + B * kNB + B * kNB + B + B + 1 + B + (p.k > 1 ? B * kNB + 4 : 0));
   const size_t o_zero = take(zb);
   const size_t o_best = take(sizeof(unsigned long long) * B * kPadU64);
   const size_t o_thr = take(sizeof(unsigned) * B * kPadU32);
@@ -2692,6 +2734,7 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   ws.blocks = ws.refined + B;
   ws.tile_count = ws.blocks + B;
   ws.updates = ws.tile_count + 1;
+  ws.ghist = p.k > 1 ? (unsigned*)(((uintptr_t)(ws.updates + B) + 15) & ~(uintptr_t)15) : nullptr;
   ws.best = (unsigned long long*)(c + o_best);
   ws.cand = (uint64_t*)(c + o_cand);
   ws.sorted = (uint64_t*)(c + o_sorted);
@@ -2794,6 +2837,7 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
   // (C3's 512-byte rows refine faster without it), any len when raw is on the host
   ra.raw16 = (p.k == 1 && (p.raw_host || p.len >= 256)) ? p.raw16 : nullptr;
   ra.refined16 = ws.updates;
+  ra.ghist = ws.ghist;
   dim3 g((unsigned)p.XB, (unsigned)nb);
   if (p.k == 1) {
     cudaError_t e1 = cudaSuccess;
