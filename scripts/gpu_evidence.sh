@@ -18,4 +18,11 @@ ncu --set full --clock-control none --import-source on -k regex:k_summarize_seg 
 ncu --set full --clock-control none --import-source on -k regex:k_blkmask -s 1 -c 1 -o gpurun_out/ev/full_c4_k_blkmask -f $CMD > gpurun_out/ev/ncu_full_blk.log 2>&1; echo "rc=$?" >> gpurun_out/ev/ncu_full_blk.log
 CMDF="python bench.py --steps 2 --warmup 3 --no-cpu --no-b1 --both 0 --path flat"
 ncu --set full --clock-control none --import-source on -k regex:k_lbt -s 1 -c 1 -o gpurun_out/ev/full_c4_k_lbt -f $CMDF > gpurun_out/ev/ncu_full_lbt.log 2>&1; echo "rc=$?" >> gpurun_out/ev/ncu_full_lbt.log
+# summaries on the box; keep only the k_lbi report (gpurun copies back <= 64 MiB)
+for k in k_lbi k_refine1 k_summarize k_blkmask k_lbt; do
+  python scripts/ncu_summary.py gpurun_out/ev/full_c4_$k.ncu-rep > gpurun_out/ev/full_c4_${k}_summary.txt 2>&1
+done
+python scripts/ncu_hot.py gpurun_out/ev/full_c4_k_lbi.ncu-rep k_lbi 30 > gpurun_out/ev/full_c4_k_lbi_hot_sass.txt 2>&1
+python scripts/launch_shares.py gpurun_out/ev/launches_c4.csv > gpurun_out/ev/launches_c4_shares.txt 2>&1
+rm -f gpurun_out/ev/full_c4_k_refine1.ncu-rep gpurun_out/ev/full_c4_k_summarize.ncu-rep gpurun_out/ev/full_c4_k_blkmask.ncu-rep gpurun_out/ev/full_c4_k_lbt.ncu-rep
 exit 0
