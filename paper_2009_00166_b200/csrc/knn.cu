@@ -2215,6 +2215,289 @@ k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
   if (threadIdx.x < nb && s_r16[threadIdx.x]) atomicAdd(&a.refined16[threadIdx.x], s_r16[threadIdx.x]);
 }
 
+// ---------------------------------------------------------------- K6, k > 1 (append, then select)
+// The query-wide threshold from the refined-distance histogram: at least k distinct
+// refined series have fp32 d^2 < (t + 2) / scale for the first bin t where the count
+// reaches k (one bin of slack for the rounding of d^2 * scale), so that edge x d2up
+// bounds the global k-th exact d^2.  One warp; lowers a.thr[b] (atomicMin on bits).
+__device__ __forceinline__ float hist_threshold(const RefineArgs& a, int b, float scale) {
+  const int lane = threadIdx.x & 31;
+  const uint4 h0 = __ldcg(reinterpret_cast<const uint4*>(a.ghist + b * kNB + 8 * lane));  // L2: the atomics' copy
+  const uint4 h1 = __ldcg(reinterpret_cast<const uint4*>(a.ghist + b * kNB + 8 * lane + 4));
+  const unsigned hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+  unsigned own = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) own += hv[i];
+  unsigned incl = own;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const unsigned reach = __ballot_sync(0xffffffffu, incl >= (unsigned)a.k);
+  float up = INFINITY;
+  if (reach) {
+    const int L = __ffs(reach) - 1;
+    if (lane == L) {
+      unsigned c = incl - own;
+      int t = 8 * L + 7;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        c += hv[i];
+        if (c >= (unsigned)a.k) { t = 8 * L + i; break; }
+      }
+      up = __fmul_ru(__fdiv_ru((float)(t + 2), scale), a.d2up);
+      atomicMin(&a.thr[b * kPadU32], __float_as_uint(up));
+    }
+    up = __shfl_sync(0xffffffffu, up, L);
+  }
+  return up;
+}
+
+// Refine up to U candidates for k > 1: exact d^2 with early abandoning at thr; each
+// completed distance is appended to the query's result list and counted in its
+// histogram.  Returns the number of completed rows (for the threshold cadence).
+template <int NC, int U>
+__device__ __forceinline__ int refine_group_k(const RefineArgs& a, const float4* __restrict__ qv, int b, float scale,
+                                              const uint64_t (&key)[U], bool (&live)[U], float thr,
+                                              uint64_t* __restrict__ res, unsigned* __restrict__ res_cnt,
+                                              unsigned& nref) {
+  const int lane = threadIdx.x & 31;
+  const int nf = a.len >> 2;
+  float4 x[U][NC];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int f = lane + 32 * c;
+      x[u][c] = (live[u] && f < nf)
+                    ? ld_stream(reinterpret_cast<const float4*>(a.raw + (size_t)key_id(key[u]) * a.len) + f)
+                    : make_float4(0, 0, 0, 0);
+    }
+  float acc[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) acc[u] = 0.f;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const float4 q = (lane + 32 * c < nf) ? __ldg(qv + lane + 32 * c) : make_float4(0, 0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float d;
+      d = x[u][c].x - q.x; acc[u] = fmaf(d, d, acc[u]);
+      d = x[u][c].y - q.y; acc[u] = fmaf(d, d, acc[u]);
+      d = x[u][c].z - q.z; acc[u] = fmaf(d, d, acc[u]);
+      d = x[u][c].w - q.w; acc[u] = fmaf(d, d, acc[u]);
+    }
+    if (c + 1 < NC && 32 * (c + 1) < nf) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (live[u] && warp_sum(acc[u]) > thr) { live[u] = false; ++nref; }
+      bool any = false;
+#pragma unroll
+      for (int u = 0; u < U; ++u) any |= live[u];
+      if (!any) return 0;
+    }
+  }
+  int done = 0;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    if (!live[u]) continue;
+    ++nref;
+    const float d2 = warp_sum(acc[u]);
+    if (d2 > thr) continue;
+    ++done;
+    if (lane == 0) {
+      res[(size_t)b * a.cap + atomicAdd(&res_cnt[b], 1u)] = make_key(d2, key_id(key[u]));
+      const float f = d2 * scale;
+      if (f < (float)(kNB - 2)) atomicAdd(&a.ghist[b * kNB + (int)f], 1u);
+    }
+  }
+  return done;
+}
+
+// k > 1 refinement without rounds: every warp walks its rotated share of every query's
+// unsorted candidate list (as k_refine1u, in the same two LB waves), skips candidates
+// above the query's live threshold, refines the rest U at a time, appends completed
+// (d^2, id) keys to the query's result list, and lowers the threshold from the
+// query-wide histogram after every 16 rows it completed.  k_select_topk then picks
+// the exact top-k of the results.
+template <int NC, int U>
+__global__ void __launch_bounds__(kRefThreads, NC <= 2 ? kRefUCtas : 2)
+k_refine_kx(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut, uint64_t* __restrict__ res,
+            unsigned* __restrict__ res_cnt) {
+  __shared__ unsigned s_refined[kMaxB], s_cnt[kMaxB], s_cut[kMaxB];
+  __shared__ float s_scale[kMaxB];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x < kMaxB) {
+    const bool on = threadIdx.x < nb;
+    s_refined[threadIdx.x] = 0;
+    s_cnt[threadIdx.x] = on ? (unsigned)imin64((int64_t)a.count[threadIdx.x], a.cap) : 0u;
+    s_cut[threadIdx.x] = on ? cut[threadIdx.x * kNB] : 0u;
+    s_scale[threadIdx.x] = on ? bin_scale(__uint_as_float(a.thr_seed[threadIdx.x])) : 0.f;
+  }
+  __syncthreads();
+  const unsigned gw = blockIdx.x * kRefWarps + warp, GW = gridDim.x * kRefWarps;
+  for (int b = 0; b < nb; ++b) {
+    const unsigned cnt = s_cnt[b];
+    const unsigned nchunk = (cnt + 31) / 32;
+    const unsigned first = (gw + (unsigned)b * 613u) % GW;
+    if (first >= nchunk) continue;
+    const float scale = s_scale[b];
+    const int cutb = (int)s_cut[b];
+    const uint64_t* list = a.sorted + (size_t)b * a.cap;
+    const float4* qv = reinterpret_cast<const float4*>(a.queries + (size_t)b * a.len);
+    unsigned nref = 0;
+    int since = 0;
+    uint64_t knext = (first * 32 + lane < cnt) ? __ldg(list + first * 32 + lane) : kNoKey;
+    for (unsigned ch = first; ch < nchunk; ch += GW) {
+      const unsigned i = ch * 32 + lane;
+      const uint64_t k0 = knext;
+      {
+        const unsigned in = (ch + GW) * 32 + lane;
+        knext = (ch + GW < nchunk && in < cnt) ? __ldg(list + in) : kNoKey;
+      }
+      float thr = __uint_as_float(ld_relaxed_u32(&a.thr[b * kPadU32]));
+      const float lb0 = key_val(k0);
+      const int bin = lb_bin(lb0, scale);
+      const bool mine = i < cnt && (wave == 0 ? bin <= cutb : bin > cutb);
+      unsigned m = __ballot_sync(0xffffffffu, mine && lb0 <= thr);
+      while (m) {
+        uint64_t key[U];
+        bool live[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int src = m ? __ffs(m) - 1 : 0;
+          const bool has = m != 0u;
+          m &= m - 1;
+          key[u] = __shfl_sync(0xffffffffu, k0, src);
+          live[u] = has && key_val(key[u]) <= thr;
+        }
+        since += refine_group_k<NC, U>(a, qv, b, scale, key, live, thr, res, res_cnt, nref);
+        if (since >= 16 && scale > 0.f) {
+          since = 0;
+          thr = fminf(thr, hist_threshold(a, b, scale));
+        }
+      }
+    }
+    if (lane == 0 && nref) atomicAdd(&s_refined[b], nref);
+  }
+  __syncthreads();
+  if (threadIdx.x < nb && s_refined[threadIdx.x]) atomicAdd(&a.refined[threadIdx.x], s_refined[threadIdx.x]);
+}
+
+// Exact top-k of a query's result list: every true top-k member is there (its exact
+// d^2 <= the final threshold, so it was neither pruned nor abandoned nor dropped).
+// Narrow a d^2 window [0, hi) with 256-bin shared histograms until it holds at most
+// kSortP keys but at least k (or everything), gather the window, bitonic-sort it,
+// write the first k ascending (d^2, id).  A window that cannot be narrowed below
+// kSortP keys (massive exact ties) falls back to merging fixed index ranges.
+__global__ void __launch_bounds__(1024)
+k_select_topk(const uint64_t* __restrict__ res, const unsigned* __restrict__ res_cnt, int64_t cap,
+              const unsigned* __restrict__ thr, int k, int q0, int64_t* __restrict__ out_idx,
+              float* __restrict__ out_dist, const unsigned* __restrict__ count, const unsigned* __restrict__ refined,
+              unsigned* __restrict__ all_count, unsigned* __restrict__ all_refined, int accum,
+              const unsigned* __restrict__ blocks, unsigned* __restrict__ all_blocks,
+              const unsigned* __restrict__ extra, unsigned* __restrict__ all_extra) {
+  __shared__ uint64_t buf[kSortP];
+  __shared__ unsigned s_h[kNB];
+  __shared__ unsigned s_n;
+  __shared__ float s_hi;
+  const int b = blockIdx.x;
+  const unsigned L = (unsigned)imin64((int64_t)res_cnt[b], cap);
+  const uint64_t* src = res + (size_t)b * cap;
+  float hi = __uint_as_float(thr[b * kPadU32]);  // every key is <= hi (appended only if d^2 <= thr)
+  bool narrowed = false;  // window = keys with d^2 < hi once narrowed, else every key
+  if (threadIdx.x == 0) s_hi = INFINITY;
+  // narrowing: the first bin where the running count reaches k; keep [0, edge(t + 1))
+  for (int it = 0; it < 4 && L > (unsigned)(kSortP - 1) && hi < INFINITY && hi > 0.f; ++it) {
+    for (int i = threadIdx.x; i < kNB; i += blockDim.x) s_h[i] = 0;
+    __syncthreads();
+    const float sc = (float)kNB / hi;
+    for (unsigned i = threadIdx.x; i < L; i += blockDim.x) {
+      const float v = key_val(src[i]);
+      if (v < hi) atomicAdd(&s_h[min((int)(v * sc), kNB - 1)], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      unsigned own = 0;
+      for (int j = 0; j < 8; ++j) own += s_h[8 * lane + j];
+      unsigned incl = own;
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const unsigned reach = __ballot_sync(0xffffffffu, incl >= (unsigned)k);
+      if (lane == 0) s_hi = hi;
+      if (reach) {
+        const int Lr = __ffs(reach) - 1;
+        if (lane == Lr) {
+          unsigned c = incl - own;
+          int t = 8 * Lr + 7;
+          for (int j = 0; j < 8; ++j) {
+            c += s_h[8 * Lr + j];
+            if (c >= (unsigned)k) { t = 8 * Lr + j; break; }
+          }
+          // keys of bins <= t + 1 (one bin of slack for the rounding of v * sc)
+          if (t + 2 < kNB) s_hi = __fdiv_ru((float)(t + 2), sc);
+        }
+      }
+    }
+    __syncthreads();
+    const float nh = s_hi;
+    __syncthreads();
+    if (!(nh < hi)) break;
+    hi = nh;
+    narrowed = true;
+    // count the keys left in the window
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    unsigned mine = 0;
+    for (unsigned i = threadIdx.x; i < L; i += blockDim.x) mine += key_val(src[i]) < hi ? 1u : 0u;
+    atomicAdd(&s_n, mine);
+    __syncthreads();
+    if (s_n <= (unsigned)kSortP) break;
+  }
+  // gather the window and sort it (or merge index ranges when it is still too large)
+  for (int i = threadIdx.x; i < kSortP; i += blockDim.x) buf[i] = kNoKey;
+  if (threadIdx.x == 0) s_n = 0;
+  __syncthreads();
+  bool over = false;
+  for (unsigned i = threadIdx.x; i < L; i += blockDim.x) {
+    const uint64_t key = src[i];
+    if (!narrowed || key_val(key) < hi) {
+      const unsigned pos = atomicAdd(&s_n, 1u);
+      if (pos < (unsigned)kSortP) buf[pos] = key;
+      else over = true;
+    }
+  }
+  if (__syncthreads_or(over)) {
+    // fallback: running top-k over fixed index windows of kSortP - k entries
+    for (int i = threadIdx.x; i < kSortP; i += blockDim.x) buf[i] = kNoKey;
+    __syncthreads();
+    const unsigned W = (unsigned)(kSortP - k);
+    for (unsigned off = 0; off < L; off += W) {
+      for (unsigned i = threadIdx.x; i < W; i += blockDim.x) buf[k + i] = (off + i < L) ? src[off + i] : kNoKey;
+      __syncthreads();
+      bitonic_sort(buf, kSortP);
+    }
+  } else {
+    bitonic_sort(buf, kSortP);
+  }
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    const uint64_t key = buf[i];
+    const size_t o = (size_t)(q0 + b) * k + i;
+    if (key == kNoKey) { out_idx[o] = -1; out_dist[o] = INFINITY; }
+    else { out_idx[o] = (int64_t)key_id(key); out_dist[o] = sqrtf(key_val(key)); }
+  }
+  if (threadIdx.x == 0) {
+    all_count[q0 + b] = (accum ? all_count[q0 + b] : 0u) + count[b];
+    all_refined[q0 + b] = (accum ? all_refined[q0 + b] : 0u) + refined[b];
+    all_blocks[q0 + b] = (accum ? all_blocks[q0 + b] : 0u) + blocks[b];
+    all_extra[q0 + b] = (accum ? all_extra[q0 + b] : 0u) + extra[b];
+  }
+}
+
 // k > 1: rounds of (every warp: one refine_step) -> merge the round's admitted
 // keys into the CTA's sorted top-k -> publish the k-th (rounded up) to the
 // query's global threshold.  Each true top-k member lands in the top-k of the
@@ -2587,7 +2870,7 @@ cudaError_t launch_index_lb(const Plan& p, const uint8_t* sax, int nb, const Car
                                ws.tile_count, ws.blocks);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(sms(), ntiles);
-  if (p.k == 1 && !p.sorted_refine)  // coarse histograms suffice for the wave cut: 3 ring stages
+  if (!p.sorted_refine)  // coarse histograms suffice for the wave cut (no bucket sort): 3 ring stages
     return PARIS_LAUNCH("lb_pass", (k_lbi<P, true>), grid, kIThreads, (lbi_smem<P, true>()), st, la, ws.bmask,
                         ws.tile_list, ws.tile_count);
   return PARIS_LAUNCH("lb_pass", (k_lbi<P, false>), grid, kIThreads, (lbi_smem<P, false>()), st, la, ws.bmask,
@@ -2817,7 +3100,7 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
   // k = 1: the refine takes its two LB waves straight from the unsorted lists (K5
   // skipped; config reserved[1] = 1 restores the bucket-sorted walk); k > 1 walks
   // the bucket-sorted lists
-  const bool unsorted = p.k == 1 && !p.sorted_refine;
+  const bool unsorted = !p.sorted_refine;  // k = 1: two waves + BSF; k > 1: append + select
   if (!unsorted) {
     const int xs = std::max(1, std::min(sms() * 4 / nb, 1024));
     dim3 g((unsigned)xs, (unsigned)nb);
@@ -2825,7 +3108,8 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
                                     ws.cursor, ws.sorted, cap),
                        "scatter launch");
   } else {
-    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("wave_cut", k_wave_cut, nb, kNB, 0, st, ws.hist, (unsigned)p.wave_a, ws.cursor),
+    const unsigned wa = (unsigned)std::max(p.wave_a, 16 * p.k);
+    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("wave_cut", k_wave_cut, nb, kNB, 0, st, ws.hist, wa, ws.cursor),
                        "wave_cut launch");
   }
   RefineArgs ra;
@@ -2869,6 +3153,28 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
     PARIS_CHECK_LAUNCH(e1, "refine launch");
     PARIS_CHECK_LAUNCH(PARIS_LAUNCH("finalize", k_finalize1, 1, kMaxB, 0, st, ws.best, nb, q0, d_idx, d_dist,
                                     ws.count, ws.refined, all_count, all_refined, rescan ? 1 : 0,
+                                    ws.blocks, all_blocks, ws.updates, all_extra),
+                       "finalize launch");
+  } else if (unsorted) {
+    // k > 1: the same two waves (the first holding >= 16k candidates), results appended
+    // to ws.sorted (free: no bucket sort on this path), then the exact top-k per query
+    static_assert(kMaxB < kNB, "result counters sit between the wave-cut entries of ws.cursor");
+    unsigned* res_cnt = ws.cursor + 1;  // (k_wave_cut writes cursor[b * kNB] only)
+    cudaError_t e1 = cudaSuccess;
+    const int NC = p.len <= 128 ? 1 : p.len <= 256 ? 2 : p.len <= 512 ? 4 : p.len <= 1024 ? 8 : 32;
+    for (int wv = 0; wv < 2 && e1 == cudaSuccess; ++wv) {
+      const int grid = sms() * (NC <= 2 ? kRefUCtas : 2);
+      switch (NC) {
+        case 1: e1 = PARIS_LAUNCH("refine", (k_refine_kx<1, kRefUU * 2>), grid, kRefThreads, 0, st, ra, nb, wv, ws.cursor, ws.sorted, res_cnt); break;
+        case 2: e1 = PARIS_LAUNCH("refine", (k_refine_kx<2, kRefUU>), grid, kRefThreads, 0, st, ra, nb, wv, ws.cursor, ws.sorted, res_cnt); break;
+        case 4: e1 = PARIS_LAUNCH("refine", (k_refine_kx<4, 1>), grid, kRefThreads, 0, st, ra, nb, wv, ws.cursor, ws.sorted, res_cnt); break;
+        case 8: e1 = PARIS_LAUNCH("refine", (k_refine_kx<8, 1>), grid, kRefThreads, 0, st, ra, nb, wv, ws.cursor, ws.sorted, res_cnt); break;
+        default: e1 = PARIS_LAUNCH("refine", (k_refine_kx<32, 1>), grid, kRefThreads, 0, st, ra, nb, wv, ws.cursor, ws.sorted, res_cnt); break;
+      }
+    }
+    PARIS_CHECK_LAUNCH(e1, "refine launch");
+    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("finalize", k_select_topk, nb, 1024, 0, st, ws.sorted, res_cnt, cap, ws.thr, p.k,
+                                    q0, d_idx, d_dist, ws.count, ws.refined, all_count, all_refined, rescan ? 1 : 0,
                                     ws.blocks, all_blocks, ws.updates, all_extra),
                        "finalize launch");
   } else {
