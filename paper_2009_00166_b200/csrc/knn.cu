@@ -2348,6 +2348,8 @@ k_refine_kx(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut, ui
     const float4* qv = reinterpret_cast<const float4*>(a.queries + (size_t)b * a.len);
     unsigned nref = 0;
     int since = 0;
+    // wave B starts from the threshold wave A's results imply
+    if (wave == 1 && scale > 0.f) hist_threshold(a, b, scale);
     uint64_t knext = (first * 32 + lane < cnt) ? __ldg(list + first * 32 + lane) : kNoKey;
     for (unsigned ch = first; ch < nchunk; ch += GW) {
       const unsigned i = ch * 32 + lane;
@@ -2373,7 +2375,7 @@ k_refine_kx(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut, ui
           live[u] = has && key_val(key[u]) <= thr;
         }
         since += refine_group_k<NC, U>(a, qv, b, scale, key, live, thr, res, res_cnt, nref);
-        if (since >= 16 && scale > 0.f) {
+        if (since >= 8 && scale > 0.f) {
           since = 0;
           thr = fminf(thr, hist_threshold(a, b, scale));
         }
