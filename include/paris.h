@@ -88,7 +88,8 @@ int paris_summarize(const float* raw, int64_t n, int32_t len, int32_t w, int32_t
  *   out_dist  [nq][k] fp32 Euclidean (rooted) distance -- device OR host memory
  * queries/out_idx/out_dist may be host pointers (pageable or pinned): the library
  * then stages them through device memory on `stream`.
- * Scratch (candidate lists, up to 16 * 2 * 8 * max(65536, n/32) bytes) is
+ * Scratch (candidate lists, up to B * 2 * 8 * max(65536, n/32) bytes -- n/16 for k > 1 --
+ * with B = 16 queries per pass on the flat path, 64 on the index path) is
  * allocated stream-ordered from the device's default memory pool; the library
  * raises that pool's release threshold so repeated calls reuse the mapping.
  * Synchronizes `stream` once per call (to check per-query candidate-buffer

@@ -3344,7 +3344,10 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   p.idx_seeds = (cfg && cfg->reserved[2] > 0) ? cfg->reserved[2]
                                                : ((raw_host && !(raw16 && k == 1)) ? kIdxSeedsHost : 0);
   plan_seed(p, (cfg && cfg->seed_div > 0) ? cfg->seed_div : 16);
-  p.cap = nb_mode ? 1 : std::min<int64_t>(n, std::max<int64_t>(65536, n / 32));
+  // candidate buffer per query: n/32 for k = 1; k > 1 keeps far more candidates on hard
+  // queries (C5 sigma = 0.2, k = 100: ~670 K of 2e7), so n/16 -- an overflow costs a
+  // per-query re-scan
+  p.cap = nb_mode ? 1 : std::min<int64_t>(n, std::max<int64_t>(65536, k > 1 ? n / 16 : n / 32));
   plan_refine(p);
   p.wave_a = (cfg && cfg->wave_a > 0) ? cfg->wave_a : 2048;
   // |fp32 d^2 - exact| <= e d^2 with e = (len/32 + 8) u (warp_ed2 / refine_step);
