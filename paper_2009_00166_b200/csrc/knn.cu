@@ -865,6 +865,10 @@ constexpr size_t kTSmem = kStages * kTileBytes + kMaxCard * 32 * 4;
 constexpr int kIStages = 2;      // 2 x 32 KB; the table and histograms take the rest of shared memory
 constexpr int kIThreads = 768;   // 24 warps: more warps to hide the lookup -> math latency chain
 constexpr int kIWarps = kIThreads / 32;
+#ifndef PARIS_LBI_UNROLL
+#define PARIS_LBI_UNROLL 4
+#endif
+constexpr int kLbiUnroll = PARIS_LBI_UNROLL;  // segment-loop unroll of the index LB items
 constexpr int kITileIds = 512;   // tile ids staged per CTA (148 CTAs: 155 M series; beyond, global loads)
 // k_lbi dynamic shared memory: [ring][pad][table: 64 KB at a 64 KB-aligned shared
 // address][16-bit LB histograms]; the pad depends on where the dynamic region
@@ -1408,7 +1412,7 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
       const int sb = (active && m) ? __ffsll((long long)m) - 1 : -1;
       const int sq = sb >= 0 ? sb : sa;  // odd count: duplicate lane, masked in emission
       uint32_t acc[4] = {0u, 0u, 0u, 0u};
-#pragma unroll 4
+#pragma unroll kLbiUnroll
       for (int s = 0; s < kTW; ++s) {
         const uint32_t word = rows[s * (kTS / 4) + k * (PARIS_INDEX_BLOCK / 4) + hl];
         const uint32_t qa = s_qs[sa][s], qb = s_qs[sq][s];
