@@ -866,7 +866,7 @@ constexpr int kIStages = 2;      // 2 x 32 KB; the table and histograms take the
 constexpr int kIThreads = 768;   // 24 warps: more warps to hide the lookup -> math latency chain
 constexpr int kIWarps = kIThreads / 32;
 #ifndef PARIS_LBI_UNROLL
-#define PARIS_LBI_UNROLL 4
+#define PARIS_LBI_UNROLL 16
 #endif
 constexpr int kLbiUnroll = PARIS_LBI_UNROLL;  // segment-loop unroll of the index LB items
 constexpr int kITileIds = 512;   // tile ids staged per CTA (148 CTAs: 155 M series; beyond, global loads)
