@@ -2092,6 +2092,10 @@ constexpr int kRefU16Ctas = PARIS_REFU16_CTAS;  // with the bf16 pre-filter (mor
 #define PARIS_REFU16_MUL 2
 #endif
 constexpr int kPFMul = PARIS_REFU16_MUL;  // bf16 rows per warp step = kPFMul x U
+#ifndef PARIS_RAW16_MINLEN
+#define PARIS_RAW16_MINLEN 256
+#endif
+constexpr int kRaw16MinLen = PARIS_RAW16_MINLEN;  // shortest rows (in HBM) the pre-filter is used for
 
 __global__ void __launch_bounds__(kNB) k_wave_cut(const unsigned* __restrict__ hist, unsigned wave_a,
                                                   unsigned* __restrict__ cut) {
@@ -3125,7 +3129,7 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
   ra.lo = 0; ra.hi = 0xFFFFFFFFu; ra.n = p.n;
   // the pre-filter pays when its rows save real bytes: rows of len >= 256 in HBM
   // (C3's 512-byte rows refine faster without it), any len when raw is on the host
-  ra.raw16 = (p.k == 1 && (p.raw_host || p.len >= 256)) ? p.raw16 : nullptr;
+  ra.raw16 = (p.k == 1 && (p.raw_host || p.len >= kRaw16MinLen)) ? p.raw16 : nullptr;
   ra.refined16 = ws.updates;
   ra.ghist = ws.ghist;
   dim3 g((unsigned)p.XB, (unsigned)nb);
