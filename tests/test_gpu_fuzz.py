@@ -1,6 +1,7 @@
 """Randomized parity sweep of the CUDA path (through the C ABI) against the oracle:
-seeded random shapes, cardinalities, k, batch sizes and paths (flat, index, index with
-the bf16 pre-filter, nb), plus the k > 1 selection's tie fallback (thousands of exact
+seeded random shapes, cardinalities, k, batch sizes and paths (flat, flat with the
+bucket-sorted refine, index, index with the bf16 pre-filter, index with raw in pinned
+host memory, nb), plus the k > 1 selection's tie fallback (thousands of exact
 duplicates, so the distance window cannot be narrowed below the sort buffer)."""
 import numpy as np
 import pytest
@@ -28,12 +29,12 @@ def _case(seed):
     k = int(rng.choice([1, 1, 2, 7, 33]))
     k = min(k, n)
     card = int(rng.choice([16, 64, 256]))
-    path = str(rng.choice(["flat", "index", "index16", "nb"]))
+    path = str(rng.choice(["flat", "index", "index16", "nb", "host", "sorted"]))
     batch = int(rng.choice([0, 1, 5, 16, 33]))
     return dict(seed=seed, length=length, n=n, nq=nq, k=k, card=card, path=path, batch=batch)
 
 
-@pytest.mark.parametrize("seed", list(range(24)))
+@pytest.mark.parametrize("seed", list(range(60)))
 def test_random_parity(P, seed):
     import torch
     c = _case(1000 + seed)
@@ -46,9 +47,13 @@ def test_random_parity(P, seed):
     xd = torch.from_numpy(x).cuda()
     qd = torch.from_numpy(q).cuda()
     sax = P.summarize(xd, 16, c["card"])
-    cfg = P.KnnConfig(batch=c["batch"])
-    if c["path"] == "flat":
+    cfg = P.KnnConfig(batch=c["batch"], sorted_refine=c["path"] == "sorted")
+    if c["path"] in ("flat", "sorted"):
         gi, gd = P.knn_exact(xd, sax, qd, k=c["k"], card=c["card"], config=cfg)
+    elif c["path"] == "host":  # raw in pinned host memory, index path with the bf16 copy in HBM
+        idx = P.index_build(sax, 16, c["card"])
+        gi, gd = P.knn_index(torch.from_numpy(x).pin_memory(), idx, qd, k=c["k"], config=cfg,
+                             raw16=P.raw_bf16(xd))
     elif c["path"] == "nb":
         gi, gd = P.knn_nb(xd, sax, qd, card=c["card"], config=cfg)
     else:
