@@ -863,7 +863,10 @@ constexpr size_t kTileBytes = (size_t)kTW * kTS;
 constexpr size_t kTSmem = kStages * kTileBytes + kMaxCard * 32 * 4;
 // k_lbi: 2-stage ring + the 32-copy pair-form table (64 KB) + the LB histograms
 constexpr int kIStages = 2;      // 2 x 32 KB; the table and histograms take the rest of shared memory
-constexpr int kIThreads = 768;   // 24 warps: more warps to hide the lookup -> math latency chain
+#ifndef PARIS_LBI_THREADS
+#define PARIS_LBI_THREADS 768
+#endif
+constexpr int kIThreads = PARIS_LBI_THREADS;  // 24 warps: more warps to hide the lookup -> math latency chain
 constexpr int kIWarps = kIThreads / 32;
 #ifndef PARIS_LBI_UNROLL
 #define PARIS_LBI_UNROLL 16
