@@ -1871,21 +1871,28 @@ __device__ __forceinline__ float bf16_lb(float d2, float qn_hi, float e2) {
                    1e-30f);  // (1e-30: the absolute error of bf16 subnormals)
 }
 
+// The candidates are given as lanes of the chunk's key register k0 (src[u]) and a
+// live mask lm (bit u): their keys are re-read with a shuffle where needed, so the
+// warp keeps U row buffers but not U 64-bit keys in registers.  Clears the bits of
+// the candidates it drops.
 template <int NC, int U>
 __device__ __forceinline__ void bf16_prefilter(const RefineArgs& a, const float4* __restrict__ qv, float qn_hi,
-                                               const uint64_t (&key)[U], bool (&live)[U], float thr) {
+                                               uint64_t k0, const int (&src)[U], unsigned& lm, float thr) {
   constexpr int NH = (NC + 1) / 2;  // uint4 (8 bf16) per lane
   const int lane = threadIdx.x & 31;
   const int nh = a.len >> 3;
   uint4 h[U][NH];
 #pragma unroll
-  for (int u = 0; u < U; ++u)
+  for (int u = 0; u < U; ++u) {
+    const uint32_t id = (uint32_t)__shfl_sync(0xffffffffu, k0, src[u]);
+    const bool on = (lm >> u) & 1u;
 #pragma unroll
     for (int c = 0; c < NH; ++c) {
       const int f = lane + 32 * c;
-      h[u][c] = (live[u] && f < nh) ? ld_stream_u4(reinterpret_cast<const uint4*>(a.raw16 + (size_t)key_id(key[u]) * a.len) + f)
-                                    : make_uint4(0u, 0u, 0u, 0u);
+      h[u][c] = (on && f < nh) ? ld_stream_u4(reinterpret_cast<const uint4*>(a.raw16 + (size_t)id * a.len) + f)
+                               : make_uint4(0u, 0u, 0u, 0u);
     }
+  }
   float s2[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) s2[u] = 0.f;
@@ -1925,13 +1932,13 @@ __device__ __forceinline__ void bf16_prefilter(const RefineArgs& a, const float4
       const unsigned drop = __ballot_sync(0xffffffffu, lb > 0.f && __fmul_rd(lb, lb) > thr);
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        if ((drop >> (8 * u)) & 1u) live[g + u] = false;
+        if ((drop >> (8 * u)) & 1u) lm &= ~(1u << (g + u));
     }
   } else {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const float lb = bf16_lb(warp_sum(s2[u]), qn_hi, e2);
-      if (lb > 0.f && __fmul_rd(lb, lb) > thr) live[u] = false;
+      if (lb > 0.f && __fmul_rd(lb, lb) > thr) lm &= ~(1u << u);
     }
   }
 }
@@ -2175,26 +2182,27 @@ k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
         // bf16 pre-filter over kPF candidates at a time (their 2*len-byte rows in flight
         // together), then the survivors' fp32 rows U at a time
         while (m) {
-          uint64_t kp[kPF];
-          bool lp[kPF];
+          int src[kPF];
+          unsigned lm = 0;
 #pragma unroll
           for (int u = 0; u < kPF; ++u) {
-            const int src = m ? __ffs(m) - 1 : 0;
+            src[u] = m ? __ffs(m) - 1 : 0;
             const bool has = m != 0u;
             m &= m - 1;
-            kp[u] = __shfl_sync(0xffffffffu, k0, src);
-            lp[u] = has && key_val(kp[u]) <= thr;
-            nref16 += lp[u] ? 1u : 0u;
+            const float lbu = key_val(__shfl_sync(0xffffffffu, k0, src[u]));
+            if (has && lbu <= thr) lm |= 1u << u;
           }
-          bf16_prefilter<NC, kPF>(a, qv, qn_hi, kp, lp, thr);
+          nref16 += __popc(lm);
+          bf16_prefilter<NC, kPF>(a, qv, qn_hi, k0, src, lm, thr);
 #pragma unroll
           for (int g = 0; g < kPF; g += U) {
+            if (!((lm >> g) & ((1u << U) - 1u))) continue;
             uint64_t key[U];
             bool live[U], any = false;
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-              key[u] = kp[g + u];
-              live[u] = lp[g + u] && key_val(key[u]) <= thr;
+              key[u] = __shfl_sync(0xffffffffu, k0, src[g + u]);
+              live[u] = ((lm >> (g + u)) & 1u) && key_val(key[u]) <= thr;
               any |= live[u];
             }
             if (!any) continue;
