@@ -871,7 +871,10 @@ constexpr int kIWarps = kIThreads / 32;
 #ifndef PARIS_LBI_UNROLL
 #define PARIS_LBI_UNROLL 16
 #endif
-constexpr int kLbiUnroll = PARIS_LBI_UNROLL;  // segment-loop unroll of the index LB items
+constexpr int kLbiUnroll = PARIS_LBI_UNROLL;
+#ifndef PARIS_LBI_DYN
+#define PARIS_LBI_DYN 0  // 1: warps claim a tile's items dynamically instead of the rotated round-robin
+#endif  // segment-loop unroll of the index LB items
 constexpr int kITileIds = 512;   // tile ids staged per CTA (148 CTAs: 155 M series; beyond, global loads)
 // k_lbi dynamic shared memory: [ring][pad][table: 64 KB at a 64 KB-aligned shared
 // address][16-bit LB histograms]; the pad depends on where the dynamic region
@@ -1312,6 +1315,7 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
                         : reinterpret_cast<unsigned*>(dsm + tab_off + kITabBytes);  // [kMaxB][kNB] 16-bit
   __shared__ __align__(8) uint64_t s_full[NST];
   __shared__ unsigned s_cnt[NST];
+  __shared__ unsigned s_next[NST];  // PARIS_LBI_DYN: the stage's next unclaimed item pair
   // per stage: the tile's id and its 32 block masks, delivered with the tile (the
   // warps never wait on a global load at a tile boundary)
   __shared__ __align__(16) unsigned long long s_bm[NST][kBPT];
@@ -1347,6 +1351,7 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
     for (int st = 0; st < NST; ++st) {
       mbar_init(&s_full[st], 1);
       s_cnt[st] = 0;
+      s_next[st] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1396,7 +1401,17 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
     const int first = (warp - rot + 2 * kIWarps) % kIWarps;
     rot = (rot + (total + 1) / 2) % kIWarps;
     const int h = lane >> 4, hl = lane & 15;
+#if PARIS_LBI_DYN
+    // dynamic: a warp claims the stage's next item pair until none is left
+    for (int t0;;) {
+      unsigned c = 0;
+      if (lane == 0) c = atomicAdd(&s_next[st], 2u);
+      t0 = (int)__shfl_sync(0xffffffffu, c, 0);
+      if (t0 >= total) break;
+      (void)first;
+#else
     for (int t0 = 2 * first; t0 < total; t0 += 2 * kIWarps) {
+#endif
       const int t = t0 + h;  // this half-warp's item
       const unsigned m0 = __ballot_sync(0xffffffffu, incl <= t0);
       const unsigned m1 = __ballot_sync(0xffffffffu, incl <= t0 + 1);
@@ -1439,6 +1454,7 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
     if (lane == 0) {
       if (atomicAdd(&s_cnt[st], 1u) == kIWarps - 1) {
         s_cnt[st] = 0;
+        s_next[st] = 0;
         const int64_t next = li + (int64_t)NST * gridDim.x;
         if (next < nlist) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
