@@ -873,7 +873,7 @@ constexpr int kIWarps = kIThreads / 32;
 #endif
 constexpr int kLbiUnroll = PARIS_LBI_UNROLL;
 #ifndef PARIS_LBI_DYN
-#define PARIS_LBI_DYN 0  // 1: warps claim a tile's items dynamically instead of the rotated round-robin
+#define PARIS_LBI_DYN 1  // 0: the rotated round-robin dealing instead of dynamic claiming
 #endif  // segment-loop unroll of the index LB items
 constexpr int kITileIds = 512;   // tile ids staged per CTA (148 CTAs: 155 M series; beyond, global loads)
 // k_lbi dynamic shared memory: [ring][pad][table: 64 KB at a 64 KB-aligned shared
