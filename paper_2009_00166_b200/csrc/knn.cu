@@ -1801,7 +1801,6 @@ struct RefineArgs {
   const uint16_t* raw16 = nullptr;  // optional bf16 copy of raw [n][len] (paris_raw_bf16): pre-filter
   unsigned* refined16 = nullptr;    // per query: bf16 rows read by the pre-filter
   unsigned* ghist = nullptr;        // k > 1: per query, histogram of refined exact d^2 (kNB bins of tau_seed^2)
-  unsigned* claim = nullptr;        // k = 1: per (wave, query) next unclaimed chunk (zeroed per batch)
 };
 
 // One warp step: up to kU candidates (indices i0 + u*stride) against the live
@@ -2123,9 +2122,6 @@ constexpr int kPFMul = PARIS_REFU16_MUL;  // bf16 rows per warp step = kPFMul x 
 #define PARIS_RAW16_MINLEN 256
 #endif
 constexpr int kRaw16MinLen = PARIS_RAW16_MINLEN;  // shortest rows (in HBM) the pre-filter is used for
-#ifndef PARIS_REF_DYN
-#define PARIS_REF_DYN 1  // k = 1 refine: chunks claimed dynamically (0: static interleave)
-#endif
 
 __global__ void __launch_bounds__(kNB) k_wave_cut(const unsigned* __restrict__ hist, unsigned wave_a,
                                                   unsigned* __restrict__ cut) {
@@ -2164,16 +2160,7 @@ k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
   for (int b = 0; b < nb; ++b) {
     const unsigned cnt = s_cnt[b];
     const unsigned nchunk = (cnt + 31) / 32;
-#if PARIS_REF_DYN
-    // chunks are claimed from a per-(wave, query) counter: warps that drew light
-    // chunks take more (the static interleave left the heavy ones' warps behind)
-    unsigned* ctr = a.claim + (wave * kMaxB + b);
-    unsigned first = 0;
-    if (lane == 0) first = atomicAdd(ctr, 1u);
-    first = __shfl_sync(0xffffffffu, first, 0);
-#else
     const unsigned first = (gw + (unsigned)b * 613u) % GW;  // rotate: spread small lists over all warps
-#endif
     if (first >= nchunk) continue;
     const float scale = s_scale[b];
     const int cutb = (int)s_cut[b];
@@ -2194,20 +2181,12 @@ k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     }
     // the next chunk's keys are loaded while this chunk is processed
     uint64_t knext = (first * 32 + lane < cnt) ? __ldg(list + first * 32 + lane) : kNoKey;
-#if PARIS_REF_DYN
-    for (unsigned ch = first, nx; ch < nchunk; ch = nx) {
-      nx = 0;
-      if (lane == 0) nx = atomicAdd(ctr, 1u);
-      nx = __shfl_sync(0xffffffffu, nx, 0);
-#else
-    for (unsigned ch = first, nx; ch < nchunk; ch = nx) {
-      nx = ch + GW;
-#endif
+    for (unsigned ch = first; ch < nchunk; ch += GW) {
       const unsigned i = ch * 32 + lane;
       const uint64_t k0 = knext;
       {
-        const unsigned in = nx * 32 + lane;
-        knext = (nx < nchunk && in < cnt) ? __ldg(list + in) : kNoKey;
+        const unsigned in = (ch + GW) * 32 + lane;
+        knext = (ch + GW < nchunk && in < cnt) ? __ldg(list + in) : kNoKey;
       }
       cur = min(cur, ld_relaxed_u64(bp));
       float thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
@@ -2783,7 +2762,6 @@ struct Ws {
   unsigned* tile_count;  // index mode: live tiles listed
   unsigned* updates;     // nb mode: V_bsf updates per query
   unsigned* ghist;       // k > 1: refined-distance histograms [B][kNB]
-  unsigned* claim;       // k = 1 refine: per (wave, query) chunk counters [2][kMaxB]
   unsigned long long* bmask;  // index mode: [ntiles*32] per-block live query-slot masks
   unsigned* tile_list;   // index mode: live tiles
   unsigned* tile_flag;   // index mode: [ntiles] tile already listed (zeroed per batch)
@@ -3041,8 +3019,7 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   const size_t o_q16 = take(sizeof(uint2) * (B / 2) * kMaxW);
   const size_t o_sid = take(sizeof(int) * B * p.S);
   const size_t o_skey = take(sizeof(uint64_t) * B * p.S);
-  const size_t zb = sizeof(unsigned) * (B + B + B * kNB + B * kNB + B + B + 1 + B + (p.k > 1 ? B * kNB + 4 : 0) +
-                                        2 * kMaxB);
+  const size_t zb = sizeof(unsigned) * (B + B + B * kNB + B * kNB + B + B + 1 + B + (p.k > 1 ? B * kNB + 4 : 0));
   const size_t o_zero = take(zb);
   const size_t o_best = take(sizeof(unsigned long long) * B * kPadU64);
   const size_t o_thr = take(sizeof(unsigned) * B * kPadU32);
@@ -3078,7 +3055,6 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   ws.tile_count = ws.blocks + B;
   ws.updates = ws.tile_count + 1;
   ws.ghist = p.k > 1 ? (unsigned*)(((uintptr_t)(ws.updates + B) + 15) & ~(uintptr_t)15) : nullptr;
-  ws.claim = (p.k > 1 ? ws.ghist + B * kNB : ws.updates + B);  // [2][kMaxB]
   ws.best = (unsigned long long*)(c + o_best);
   ws.cand = (uint64_t*)(c + o_cand);
   ws.sorted = (uint64_t*)(c + o_sorted);
@@ -3183,7 +3159,6 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
   ra.raw16 = (p.k == 1 && (p.raw_host || p.len >= kRaw16MinLen)) ? p.raw16 : nullptr;
   ra.refined16 = ws.updates;
   ra.ghist = ws.ghist;
-  ra.claim = ws.claim;
   dim3 g((unsigned)p.XB, (unsigned)nb);
   if (p.k == 1) {
     cudaError_t e1 = cudaSuccess;
