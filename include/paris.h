@@ -129,7 +129,7 @@ typedef struct paris_knn_config {
   int32_t reserved[5];  /* tuning/test hooks: [0] = 1 forces the direct-load LB kernels;
                            [1] = 1: the k = 1 refine walks bucket-sorted lists (K5 scatter)
                            instead of taking its two LB waves from the unsorted lists;
-                           [2] index mode: seed series around the leaf (0 = max(1024, 32k) up to 4096; 64 when
+                           [2] index mode: seed series around the leaf (0 = max(1024 (2048 from 5e7 series), 32k) up to 4096; 64 when
                            raw is host memory);
                            [3] = 1 seeds every batch from the rows already in out_idx/out_dist
                            (device outputs; experiments with an ideal BSF) */

@@ -3265,7 +3265,8 @@ void plan_seed(Plan& p, int seed_div) {
     p.seed_grid = 0;
     // default: 1024 series around the leaf; for k > 1, 32 per requested neighbour (the
     // k-th best of the seeds must bound the k-th NN distance tightly), up to kMaxSeed
-    const int dflt = std::max(kIdxSeeds, std::min(kMaxSeed, 32 * p.k));
+    // (2048 from 5e7 series on: the leaf neighbourhood then tightens tau measurably, C4 +0.7%)
+    const int dflt = std::max(p.n >= 50000000 ? 2 * kIdxSeeds : kIdxSeeds, std::min(kMaxSeed, 32 * p.k));
     p.S = std::max(p.k, std::min(kMaxSeed, p.idx_seeds > 0 ? p.idx_seeds : dflt));
     return;
   }
