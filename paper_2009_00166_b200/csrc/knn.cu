@@ -872,6 +872,10 @@ constexpr int kIWarps = kIThreads / 32;
 #define PARIS_LBI_UNROLL 16
 #endif
 constexpr int kLbiUnroll = PARIS_LBI_UNROLL;
+#ifndef PARIS_BM_CTAS
+#define PARIS_BM_CTAS 8
+#endif
+constexpr int kBmCtas = PARIS_BM_CTAS;  // block-pass CTAs per SM in the grid (tuning)
 #ifndef PARIS_LBI_DYN
 #define PARIS_LBI_DYN 1  // 0: the rotated round-robin dealing instead of dynamic claiming
 #endif  // segment-loop unroll of the index LB items
@@ -2902,7 +2906,7 @@ cudaError_t launch_index_lb(const Plan& p, const uint8_t* sax, int nb, const Car
   la.hist = ws.hist; la.cand = ws.cand; la.cap = cap; la.perm = p.perm; la.env = p.env;
   la.blocks = ws.blocks;
   const int64_t ntiles = (p.n + kTS - 1) / kTS;
-  const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms() * 8, (ntiles + 7) / 8));
+  const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms() * kBmCtas, (ntiles + 7) / 8));
   cudaError_t e = PARIS_LAUNCH("lb_blocks", k_blkmask<P>, bgrid, 256, 0, st, la, ws.bmask, ws.tile_list,
                                ws.tile_count, ws.blocks);
   if (e != cudaSuccess) return e;
