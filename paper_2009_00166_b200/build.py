@@ -49,10 +49,21 @@ def _run(cmd):
     return r.stdout + r.stderr
 
 
+STAMP = LIB + ".flags"
+
+
+def _stamp_ok(path: str, flags) -> bool:
+    """The library at `path` was built with exactly these flags (tuning -D values included)."""
+    try:
+        return open(path + ".flags").read() == " ".join(flags)
+    except OSError:
+        return False
+
+
 def build_paris(force: bool = False, verbose: bool = False) -> str:
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     deps = srcs + [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "paris.h")]
-    if not force and not _newer(LIB, deps + [__file__]):
+    if not force and not _newer(LIB, deps + [__file__]) and _stamp_ok(LIB, FLAGS):
         return LIB
     objdir = os.path.join(PKG, "build")
     os.makedirs(objdir, exist_ok=True)
@@ -71,15 +82,19 @@ def build_paris(force: bool = False, verbose: bool = False) -> str:
     tmp = LIB + f".tmp{os.getpid()}"
     _run([NVCC, *ARCH, "-shared", "-o", tmp, *[o for o, _ in results], "-lcudart"])
     os.replace(tmp, LIB)
+    with open(STAMP, "w") as f:  # a later default build() rebuilds over a tuned (-D...) variant
+        f.write(" ".join(FLAGS))
     return LIB
 
 
 def build_datagen(force: bool = False) -> str:
-    if not force and not _newer(DATAGEN_LIB, [DATAGEN_SRC, __file__]):
+    if not force and not _newer(DATAGEN_LIB, [DATAGEN_SRC, __file__]) and _stamp_ok(DATAGEN_LIB, FLAGS):
         return DATAGEN_LIB
     tmp = DATAGEN_LIB + f".tmp{os.getpid()}"
     _run([NVCC, *ARCH, *FLAGS, "-shared", "-o", tmp, DATAGEN_SRC, "-lcudart"])
     os.replace(tmp, DATAGEN_LIB)
+    with open(DATAGEN_LIB + ".flags", "w") as f:
+        f.write(" ".join(FLAGS))
     return DATAGEN_LIB
 
 
