@@ -88,13 +88,19 @@ int paris_summarize(const float* raw, int64_t n, int32_t len, int32_t w, int32_t
  *   out_dist  [nq][k] fp32 Euclidean (rooted) distance -- device OR host memory
  * queries/out_idx/out_dist may be host pointers (pageable or pinned): the library
  * then stages them through device memory on `stream`.
- * Scratch (candidate lists, up to B * 2 * 8 * max(65536, n/32) bytes -- n/16 for k > 1 --
- * with B = 16 queries per pass on the flat path, 64 on the index path) is
- * allocated stream-ordered from the device's default memory pool; the library
- * raises that pool's release threshold so repeated calls reuse the mapping.
- * Synchronizes `stream` once per call (to check per-query candidate-buffer
- * overflow; an overflowed query is re-scanned with an exact-size buffer), so on
- * return the outputs are final.  nq == 0 is a no-op.
+ * Asynchronous: the call enqueues its work on `stream` and returns without waiting;
+ * outputs are final once `stream` completes (host outputs: pinned ones are copied back
+ * stream-ordered; pageable ones block the call until the copy is done, as
+ * cudaMemcpyAsync does).  The host never reads device state: a query whose candidate
+ * list outgrew its buffer (more than max(65536, n/32) candidates, n/16 for k > 1) is
+ * completed on the device by a fused LB -> refine scan seeded with its first-pass
+ * result (gated kernels that exit at once when no query overflowed).
+ * Scratch (candidate lists, up to B * 8 * max(65536, n/32) bytes, with B = 16 queries
+ * per pass on the flat path, 64 on the index path) comes from a workspace cached per
+ * device (grown on demand, reused across calls, each reuse ordered after the previous
+ * call's work by an event): no allocation and no synchronization in the steady state.
+ * paris_release_workspace() frees it.  With `stats` (paris_knn_exact_ex) the call
+ * synchronizes to read the counters.  nq == 0 is a no-op.
  */
 int paris_knn_exact(const float* raw, const uint8_t* sax, int64_t n, const float* queries,
                     int32_t nq, int32_t k, int64_t* out_idx, float* out_dist, int32_t len,
@@ -225,11 +231,15 @@ int paris_knn_nb(const float* raw, const uint8_t* sax, int64_t n, const float* q
 int paris_merge_topk(const float* dist, const int64_t* idx, int32_t R, int32_t nq, int32_t k, int64_t* out_idx,
                      float* out_dist, void* stream);
 
+/* Free the cached device workspace of the k-NN calls (all devices; synchronizes the
+ * device).  The next call allocates it again. */
+void paris_release_workspace(void);
+
 /* Thread-local text of the last failure (never NULL). */
 const char* paris_last_error(void);
 
 /* ABI version (major*100 + minor). */
-int32_t paris_version(void);  /* 104: paris_raw_bf16, paris_knn_index_x */
+int32_t paris_version(void);  /* 105: asynchronous k-NN calls, device-side overflow, paris_release_workspace */
 
 /* Test hook: the library's own fp64 breakpoints cut_1..cut_{card-1} (R2) into
  * out[0..card-2] (host memory).  PARIS_ECONFIG for a bad card. */

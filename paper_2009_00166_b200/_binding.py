@@ -96,6 +96,7 @@ def load():
         lib.paris_knn_nb.restype = ctypes.c_int
         lib.paris_merge_topk.argtypes = [P, P, i32, i32, i32, P, P, P]
         lib.paris_merge_topk.restype = ctypes.c_int
+        lib.paris_release_workspace.restype = None
         lib.paris_last_error.restype = ctypes.c_char_p
         lib.paris_version.restype = i32
         lib.paris_profile_enable.argtypes = [i32]
@@ -214,11 +215,13 @@ def raw_bf16(raw: torch.Tensor, stream=None) -> torch.Tensor:
 
 def knn_index(raw: torch.Tensor, index: Index, queries: torch.Tensor, k: int = 1,
               out_idx: torch.Tensor | None = None, out_dist: torch.Tensor | None = None, stream=None,
-              config: KnnConfig | None = None, stats: bool = False, raw16: torch.Tensor | None = None):
+              config: KnnConfig | None = None, stats: bool = False, raw16: torch.Tensor | None = None,
+              sync: bool | None = None):
     """Exact k-NN over an Index (paris_knn_index); same results as knn_exact.  raw16: the
     bf16 copy of raw (raw_bf16) -> the refinement pre-filter (paris_knn_index_x)."""
     return knn_exact(raw, index.sax_sorted, queries, k=k, w=index.w, card=index.card, out_idx=out_idx,
-                     out_dist=out_dist, stream=stream, config=config, stats=stats, _index=index, _raw16=raw16)
+                     out_dist=out_dist, stream=stream, config=config, stats=stats, _index=index, _raw16=raw16,
+                     sync=sync)
 
 
 def knn_nb(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, w: int = 16, card: int = 256,
@@ -233,7 +236,7 @@ def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: in
               w: int = 16, card: int = 256, out_idx: torch.Tensor | None = None,
               out_dist: torch.Tensor | None = None, stream=None,
               config: KnnConfig | None = None, stats: bool = False, _index: Index | None = None,
-              _nb: bool = False, _raw16: torch.Tensor | None = None):
+              _nb: bool = False, _raw16: torch.Tensor | None = None, sync: bool | None = None):
     """Exact k-NN of every query (rows of `queries`, CUDA or host) over raw/sax.
 
     sax (and the index) are CUDA tensors; raw is CUDA or pinned host memory (the
@@ -241,6 +244,8 @@ def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: in
 
     Returns (idx int64 [nq][k], dist float32 [nq][k]) on the device of `queries`
     (or the given out tensors); with stats=True also a dict of per-query counters.
+    The library call is asynchronous on the stream; with host outputs the binding waits
+    for the stream before returning unless sync=False (then the caller synchronizes).
     """
     lib = load()
     if not (raw.is_cuda or raw.is_pinned()):
@@ -306,11 +311,25 @@ def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: in
                                     length, w, card, _stream(stream), ctypes.byref(cfg) if cfg else None,
                                     ctypes.byref(st) if st else None)
     _check(rc)
+    if sync is None:
+        sync = not (out_idx.is_cuda and out_dist.is_cuda)
+    if sync:
+        if stream is None:
+            torch.cuda.current_stream().synchronize()
+        elif isinstance(stream, torch.cuda.Stream):
+            stream.synchronize()
+        else:
+            torch.cuda.ExternalStream(int(stream)).synchronize()
     if stats:
         return out_idx, out_dist, {"candidates": arrays[0], "refined": arrays[1],
                                    "tau_seed": arrays[2], "lb_blocks": arrays[3], "bsf_updates": arrays[4],
                                    "raw16_rows": arrays[5]}
     return out_idx, out_dist
+
+
+def release_workspace():
+    """Free the library's cached k-NN workspace (paris_release_workspace; synchronizes)."""
+    load().paris_release_workspace()
 
 
 def merge_topk(dist: torch.Tensor, idx: torch.Tensor, stream=None):

@@ -110,16 +110,7 @@ k_idx_gather(const uint4* __restrict__ aos, const uint32_t* __restrict__ perm, i
   }
 }
 
-int sm_count_idx() {
-  static int cached = 0;
-  if (!cached) {
-    int dev = 0, v = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    cached = v > 0 ? v : 148;
-  }
-  return cached;
-}
+int sm_count_idx() { return device_sms(); }
 
 }  // namespace
 

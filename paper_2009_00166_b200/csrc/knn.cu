@@ -472,10 +472,9 @@ k_seed_select(const uint64_t* __restrict__ seed_keys, int S, int k, float d2up,
   }
 }
 
-// Re-scan seed (candidate-buffer overflow): the first pass already refined the
-// `cap` candidates it kept, so its result row is a real (and much tighter) BSF:
-// tau^2 = (k-th returned distance)^2 rounded up (the fp32 sqrt/square round trip
-// is covered by a further 2^-20), the k = 1 BSF key restarts from that row.
+// Seed from a previous result row (test hook config reserved[3]: the LB pass under an
+// ideal BSF): tau^2 = (k-th returned distance)^2 rounded up (the fp32 sqrt/square round
+// trip is covered by a further 2^-20), the k = 1 BSF key restarts from that row.
 __global__ void k_seed_prev(const int64_t* __restrict__ prev_idx, const float* __restrict__ prev_dist, int nb,
                             int q0, int k, float d2up, unsigned* __restrict__ thr, unsigned* __restrict__ thr_seed,
                             unsigned long long* __restrict__ best) {
@@ -861,32 +860,11 @@ constexpr int kStages = 4;
 constexpr int kTW = 16;
 constexpr size_t kTileBytes = (size_t)kTW * kTS;
 constexpr size_t kTSmem = kStages * kTileBytes + kMaxCard * 32 * 4;
-// k_lbi: 2-stage ring + the 32-copy pair-form table (64 KB) + the LB histograms
-constexpr int kIStages = 2;      // 2 x 32 KB; the table and histograms take the rest of shared memory
-#ifndef PARIS_LBI_THREADS
-#define PARIS_LBI_THREADS 768
-#endif
-constexpr int kIThreads = PARIS_LBI_THREADS;  // 24 warps: more warps to hide the lookup -> math latency chain
-constexpr int kIWarps = kIThreads / 32;
-#ifndef PARIS_LBI_UNROLL
-#define PARIS_LBI_UNROLL 16
-#endif
-constexpr int kLbiUnroll = PARIS_LBI_UNROLL;
 #ifndef PARIS_BM_CTAS
 #define PARIS_BM_CTAS 8
 #endif
 constexpr int kBmCtas = PARIS_BM_CTAS;  // block-pass CTAs per SM in the grid (tuning)
-#ifndef PARIS_LBI_DYN
-#define PARIS_LBI_DYN 1  // 0: the rotated round-robin dealing instead of dynamic claiming
-#endif  // segment-loop unroll of the index LB items
-constexpr int kITileIds = 512;   // tile ids staged per CTA (148 CTAs: 155 M series; beyond, global loads)
-// k_lbi dynamic shared memory: [ring][pad][table: 64 KB at a 64 KB-aligned shared
-// address][16-bit LB histograms]; the pad depends on where the dynamic region
-// starts (after the static arrays), so the launch requests what the static size
-// leaves and the kernel checks the layout fits (kLbiSmem below, set at launch).
-constexpr size_t kITabBytes = (size_t)kMaxCard * 32 * 8;
-constexpr size_t kIHistBytes = (size_t)kMaxB * kNB * 2;
-constexpr size_t kIHistCBytes = (size_t)kMaxB * (kNB / 8) * 4;  // coarse (k = 1) histograms
+constexpr size_t kIHistBytes = (size_t)kMaxB * kNB * 2;  // k_lbi !HC: 16-bit LB histograms
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -1103,35 +1081,152 @@ k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
 }
 
 // ---------------------------------------------------------------- index mode LB (f1)
-// Pass 1 (k_blkmask): the envelope MINDIST of every 128-series block for every
+// Pass 1 (k_blkmask): the envelope MINDIST of every 64-series block for every
 // query slot (the iSAX node bound): bit b of bmask[blk] = block may hold a
-// candidate of slot b.  A CTA covers the 16 blocks of one SAX tile and appends
+// candidate of slot b.  A warp covers the 32 blocks of one SAX tile and appends
 // the tile to a work list when any of its blocks is live.
-// Pass 2 (k_lbi): the TMA ring streams only listed tiles; the live (block, query
-// pair) items of a tile are dealt round-robin to its 16 warps (every warp derives
-// the same item list from the 16 block masks, no CTA barrier), so warps stay
-// balanced however the live blocks are spread.
-// Candidate emission of one index item: 4 series x 2 query slots (sa = low half,
-// sb = high half, sb < 0: none).  Same tests and warp buffer as lb_emit_wb.
+// Pass 2 (k_lbi): a producer warp streams the listed tiles through a ring of
+// NST stages (full/empty mbarrier pairs); the live (block, query pair) items of a
+// tile are claimed dynamically by the consumer warps, a half-warp per item.
 __device__ __forceinline__ uint32_t half_of(uint32_t v, int h) { return (v >> (16 * h)) & 0xFFFFu; }
 
-template <int HMODE>
+// Shared-memory plan of k_lbi (dynamic shared memory only; S0 = its shared address,
+// T = the 64 KB boundary above it):
+//   [S0, S0 + 32K)         ring stage 0
+//   [S0 + 32K, T)          misc (LbiMisc): barriers, per-stage tile id / claim counter /
+//                          block masks, LbConsts, per-warp candidate slots and counters
+//   [T, T + 64K)           region table, 16 copies: entry c of copy j at T + 256c + 8j
+//                          (copy = lane % 16: an 8-byte load is served per half-warp, whose
+//                          16 lanes then hit distinct banks).  Bytes [128, 256) of each
+//                          256-byte row are "holes" (128 B each, 256 of them):
+//                            holes   0..31   per-slot query words s_qs (two slots per hole)
+//                            holes  32..127  per-warp candidate keys (kWBI per warp)
+//                            holes 128..191  coarse LB histograms (HC), a slot per hole
+//   [T + 64K, ...)         ring stages 1 .. NST-1, then the 16-bit histograms (!HC)
+// One byte permute of a SAX word with {lane%16 * 8, -, T bits 16..31} is a lookup's
+// whole shared address (the symbol lands in bits 8..15).
+constexpr int kIWarps = 24;                   // consumer warps
+constexpr int kIThreads = (kIWarps + 1) * 32; // + the producer warp
+constexpr int kWBI = 64;                      // staged candidates per consumer warp
+constexpr uint32_t kIStageBytes = (uint32_t)kTileBytes;
+struct LbiWarp {
+  uint8_t slot[kWBI];
+  unsigned cnt[kMaxB];  // entries per slot; during a flush the slot's global cursor
+  unsigned n;
+  unsigned pad[3];
+};
+struct LbiMisc {
+  uint64_t full[4], empty[4];
+  int64_t tile[4];
+  unsigned next[4];
+  unsigned pad[4];
+  unsigned long long bm[4][kBPT];
+  LbConsts c;
+  LbiWarp w[kIWarps];
+};
+constexpr size_t kIMiscBytes = (sizeof(LbiMisc) + 127) & ~(size_t)127;
+static_assert(kTileBytes + kIMiscBytes + 4096 <= 65536, "stage 0 + misc must fit below the table");
+
+__device__ __forceinline__ uint32_t hole_addr(uint32_t T, int h) { return T + 256u * (uint32_t)h + 128u; }
+__device__ __forceinline__ uint32_t lbi_key_addr(uint32_t T, int warp, int e) {
+  return hole_addr(T, 32 + 4 * warp + (e >> 4)) + 8u * (uint32_t)(e & 15);
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint64_t lds_u64(uint32_t addr) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts_u64(uint32_t addr, uint64_t v) {
+  asm volatile("st.shared.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u2(uint32_t addr, uint2 v) {
+  asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(addr), "r"(v.x), "r"(v.y) : "memory");
+}
+__device__ __forceinline__ void atoms_add(uint32_t addr, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// LB histogram of a stored candidate: HC -> coarse bins (bin >> 3) in the holes; else
+// the packed 16-bit form at hist16 (hist16_add).
+template <bool HC>
+__device__ __forceinline__ void lbi_hist(uint32_t T, unsigned* hist16, int b, int bin, unsigned* g_hist) {
+  if (HC) atoms_add(hole_addr(T, 128 + b) + 4u * (uint32_t)(bin >> 3), 1u);
+  else hist16_add(hist16, b * kNB + bin, g_hist);
+}
+
+// Flush a warp's staged candidates: one global atomicAdd per query slot reserves the
+// slots of all its entries; sorted positions become series ids through perm here
+// (a warp's loads in parallel, off the per-item path).
+template <bool HC>
+__device__ void lbi_flush(LbiWarp& wb, uint32_t T, int warp, int nslots, const LbConsts& c, const LbArgs& a,
+                          unsigned* hist16) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  const int m = (int)wb.n;
+  if (m == 0) return;
+  for (int b = lane; b < nslots; b += 32) {
+    const unsigned k = wb.cnt[b];
+    wb.cnt[b] = k ? atomicAdd(&a.count[b], k) : 0u;
+  }
+  __syncwarp();
+  static_assert(kWBI == 64, "two entries per lane");
+  uint64_t key[2];
+  uint32_t id[2];
+  int sl[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int e = lane + 32 * r;
+    key[r] = e < m ? lds_u64(lbi_key_addr(T, warp, e)) : kNoKey;
+    sl[r] = e < m ? wb.slot[e] : 0;
+    id[r] = e < m ? __ldg(a.perm + key_id(key[r])) : 0u;
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    if (lane + 32 * r >= m) continue;
+    const int b = sl[r];
+    const unsigned pos = atomicAdd(&wb.cnt[b], 1u);
+    // only stored candidates enter the histogram (on overflow the wave cut must describe
+    // the `cap` stored entries)
+    if ((int64_t)pos < a.cap) {
+      a.cand[(size_t)b * a.cap + pos] = make_key(key_val(key[r]), id[r]);
+      lbi_hist<HC>(T, hist16, b, lb_bin(key_val(key[r]), c.scale[b]), a.hist);
+    }
+  }
+  __syncwarp();
+  for (int b = lane; b < nslots; b += 32) wb.cnt[b] = 0;
+  if (lane == 0) wb.n = 0;
+  __syncwarp();
+}
+
+// Candidate emission of one item per half-warp: 4 series x 2 query slots (sa = low half,
+// sb = high half, sb < 0: none).  The packed fp16 test first (almost every item fails it
+// everywhere), the rigorous fp32 bound (k_lb's error budget) only where a lane passed.
+template <bool HC>
 __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int sb, int64_t i0, int nvalid,
-                                         int nslots, const LbConsts& c, const LbArgs& a, WarpBuf& wb,
-                                         unsigned* s_hist) {
+                                         int nslots, const LbConsts& c, const LbArgs& a, LbiWarp& wb,
+                                         uint32_t T, int warp, unsigned* hist16) {
   const int lane = threadIdx.x & 31;
   const uint32_t Tp = half_of(c.T16[sa >> 1], sa & 1) |
                       ((sb >= 0 ? half_of(c.T16[sb >> 1], sb & 1) : (uint32_t)kHalfNeg1) << 16);
-  uint32_t pm = 0;  // bit 2j+h: series j passes for slot h
-  float lbv[4][2];
-  // the packed fp16 test first (almost every item fails it everywhere); the fp32
-  // bounds only where some lane of the warp passed it
   uint32_t pf = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) pf |= h2_le_bits(acc[j], Tp) << (2 * j);
   if (nvalid < 4) pf &= (1u << (2 * nvalid)) - 1u;
   if (sb < 0) pf &= 0x55u;
   if (!__any_sync(0xffffffffu, pf != 0u)) return;
+  uint32_t pm = 0;  // bit 2j+h: series j passes for slot h
+  float lbv[4][2];
   if (pf) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -1153,9 +1248,8 @@ __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int s
     if (lane >= o) incl += v;
   }
   const int total = __shfl_sync(0xffffffffu, incl, 31);
-  if (wb.n + total > kWB) wb_flush<HMODE>(wb, nslots, c, a, s_hist);
-  // (static bit loops: lbv stays in registers)
-  if (total > kWB) {  // degenerate (e.g. tau = inf): straight to global memory
+  if ((int)wb.n + total > kWBI) lbi_flush<HC>(wb, T, warp, nslots, c, a, hist16);
+  if (total > kWBI) {  // degenerate (e.g. tau = inf): straight to global memory
 #pragma unroll
     for (int bit = 0; bit < 8; ++bit) {
       if (!((pm >> bit) & 1u)) continue;
@@ -1164,18 +1258,18 @@ __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int s
       if ((int64_t)pos < a.cap) {
         a.cand[(size_t)sl * a.cap + pos] = make_key(lbv[j][bit & 1], __ldg(a.perm + i0 + j));
         const int fb = lb_bin(lbv[j][bit & 1], c.scale[sl]);
-        atomicAdd(&a.hist[sl * kNB + (HMODE == 2 ? (fb | 7) : fb)], 1u);
+        atomicAdd(&a.hist[sl * kNB + (HC ? (fb | 7) : fb)], 1u);
       }
     }
     return;
   }
-  int pos = wb.n + incl - cntl;
+  int pos = (int)wb.n + incl - cntl;
 #pragma unroll
   for (int bit = 0; bit < 8; ++bit) {
     if (!((pm >> bit) & 1u)) continue;
     const int j = bit >> 1, sl = (bit & 1) ? sb : sa;
-    PARIS_DCHECK(i0 + j < a.n && pos < kWB && sl >= 0);
-    wb.key[pos] = make_key(lbv[j][bit & 1], __ldg(a.perm + i0 + j));
+    PARIS_DCHECK(i0 + j < a.n && pos < kWBI && sl >= 0);
+    sts_u64(lbi_key_addr(T, warp, pos), make_key(lbv[j][bit & 1], (uint32_t)(i0 + j)));  // sorted position
     wb.slot[pos] = (uint8_t)sl;
     atomicAdd(&wb.cnt[sl], 1u);
     ++pos;
@@ -1287,194 +1381,163 @@ k_blkmask(LbArgs a, unsigned long long* __restrict__ bmask, unsigned* __restrict
   if (tid < NS && s_blk[tid]) atomicAdd(&blocks[tid], s_blk[tid]);
 }
 
-// HC (k = 1 with the unsorted refine waves): coarse LB histograms (8 KB) below the
-// table, so a third 32 KB ring stage fits; else the 16-bit 256-bin histograms
-// (k > 1 and the sorted walk order candidates by them exactly) and two stages.
+// HC: coarse LB histograms (the k = 1 / k > 1 refine waves only need a quantile of
+// them) in the table's holes and a 4-stage ring; !HC (the opt-in bucket-sorted walk,
+// whose scatter needs exact bins): 16-bit 256-bin histograms and 3 stages.
 template <int P, bool HC>
 __global__ void __launch_bounds__(kIThreads, 1)
 k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __restrict__ tile_list,
       const unsigned* __restrict__ tile_count) {
-  constexpr int NST = HC ? 3 : 2;  // ring stages
+  constexpr int NST = HC ? 4 : 3;
   extern __shared__ __align__(128) uint8_t dsm[];
-  // the table sits at a 64 KB-aligned shared address, so one byte permute builds a
-  // lookup's full address: {lane*8, symbol, table address bits 16-31}.
-  //   HC:  [coarse hist][pad][table][ring x 3]     else: [ring x 2][pad][table][hist16]
-  const uint32_t dsm_s = smem_u32(dsm);
-  const uint32_t tab_s = HC ? ((dsm_s + (uint32_t)kIHistCBytes + 0xFFFFu) & ~0xFFFFu)
-                            : ((dsm_s + (uint32_t)(NST * kTileBytes) + 0xFFFFu) & ~0xFFFFu);
-  const uint32_t tab_off = tab_s - dsm_s;
-  uint8_t* s_tiles = HC ? dsm + tab_off + kITabBytes : dsm;
+  const uint32_t S0 = smem_u32(dsm);
+  const uint32_t T = (S0 + (uint32_t)(kTileBytes + kIMiscBytes) + 0xFFFFu) & ~0xFFFFu;  // the table
+  uint8_t* const gbase = dsm - S0;  // generic pointer of shared address x: gbase + x
+  LbiMisc& M = *reinterpret_cast<LbiMisc*>(dsm + kTileBytes);
+  unsigned* hist16 = reinterpret_cast<unsigned*>(gbase + T + 65536u + (uint32_t)(NST - 1) * kIStageBytes);
+  auto stage_addr = [&](int st) -> uint32_t {
+    return st == 0 ? S0 : T + 65536u + (uint32_t)(st - 1) * kIStageBytes;
+  };
   {
     uint32_t dyn;
     asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
-    const size_t need = (size_t)tab_off + kITabBytes + (HC ? (size_t)NST * kTileBytes : kIHistBytes);
-    if (need > dyn) __trap();  // launch config inconsistent with the layout
+    const uint32_t need = T + 65536u + (uint32_t)(NST - 1) * kIStageBytes + (HC ? 0u : (uint32_t)kIHistBytes);
+    if (need > S0 + dyn) __trap();  // launch config inconsistent with the layout
   }
-  // region table in pair form {(-U16,-U16), (L16,L16)}, 32 copies: entry c of lane l
-  // at byte 256c + 8l, so ONE byte permute forms the address (symbol byte -> bits
-  // 8..15, lane*8 -> bits 0..7; no multiply); a 64-bit load is served per half-warp
-  // and the 16 lanes of each half hit distinct banks
-  uint2* s_tab = reinterpret_cast<uint2*>(dsm + tab_off);
-  unsigned* s_hist = HC ? reinterpret_cast<unsigned*>(dsm)                        // [kMaxB][kNBC] coarse
-                        : reinterpret_cast<unsigned*>(dsm + tab_off + kITabBytes);  // [kMaxB][kNB] 16-bit
-  __shared__ __align__(8) uint64_t s_full[NST];
-  __shared__ unsigned s_cnt[NST];
-  __shared__ unsigned s_next[NST];  // PARIS_LBI_DYN: the stage's next unclaimed item pair
-  // per stage: the tile's id and its 32 block masks, delivered with the tile (the
-  // warps never wait on a global load at a tile boundary)
-  __shared__ __align__(16) unsigned long long s_bm[NST][kBPT];
-  __shared__ int64_t s_tile[NST];
-  // this CTA's share of the tile list (entries blockIdx.x + i * gridDim.x), staged once:
-  // a refill then starts its TMA without a dependent global load
-  __shared__ unsigned s_tl[kITileIds];
-  __shared__ uint32_t s_qs[2 * P][kTW];  // per slot and segment: half2(q_lo16, -q_hi16)
-  __shared__ LbConsts s_c;
-  __shared__ WarpBuf s_wb[kIWarps];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nslots = 2 * P;
   const int64_t nlist = *tile_count;
-  WarpBuf& wb = s_wb[warp];
-  for (int b = lane; b < kMaxB; b += 32) wb.cnt[b] = 0;
-  if (lane == 0) wb.n = 0;
-  for (int i = tid; i < (HC ? nslots * kNBC : nslots * kNB / 2); i += kIThreads) s_hist[i] = 0;
 
-  static_assert(kTS == PARIS_INDEX_TILE, "index tiles are the LB kernel's tiles");
-  auto issue = [&](int64_t li, int st) {
-    // tile-major sorted SAX: the tile's 16 rows are one contiguous 32 KB range; its
-    // block masks (128 B) ride on the same barrier; the id is published before the
-    // arrive (release), so waiters that see the phase flip see it too
-    const int64_t i = (li - blockIdx.x) / gridDim.x;
-    const int64_t tile = i < kITileIds ? s_tl[i] : tile_list[li];
-    s_tile[st] = tile;
-    mbar_expect_tx(&s_full[st], (unsigned)(kTileBytes + kBPT * 8));
-    bulk_g2s(s_tiles + (size_t)st * kTileBytes, a.sax + (size_t)tile * kTileBytes, (unsigned)kTileBytes,
-             &s_full[st]);
-    bulk_g2s(&s_bm[st][0], bmask + (size_t)tile * kBPT, (unsigned)(kBPT * 8), &s_full[st]);
-  };
+  // ---- setup: barriers, table (16 copies), query words, histograms, warp buffers
   if (tid == 0) {
     for (int st = 0; st < NST; ++st) {
-      mbar_init(&s_full[st], 1);
-      s_cnt[st] = 0;
-      s_next[st] = 0;
+      mbar_init(&M.full[st], 1);
+      mbar_init(&M.empty[st], kIWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int64_t i = tid; i < kITileIds; i += kIThreads) {
-    const int64_t li = blockIdx.x + i * gridDim.x;
-    if (li >= nlist) break;
-    s_tl[i] = tile_list[li];
-  }
-  __syncthreads();
-  if (tid == 0) {
-    for (int st = 0; st < NST; ++st) {
-      const int64_t li = blockIdx.x + (int64_t)st * gridDim.x;
-      if (li < nlist) issue(li, st);
-    }
-  }
-  for (int i = tid; i < kMaxCard * 32; i += kIThreads) s_tab[i] = a.tab->lu16[i >> 5];
-  for (int i = tid; i < 2 * P * kTW; i += kIThreads) {
+  for (int i = tid; i < kMaxCard * 16; i += kIThreads) sts_u2(T + 256u * (uint32_t)(i >> 4) + 8u * (uint32_t)(i & 15), a.tab->lu16[i >> 4]);
+  for (int i = tid; i < nslots * kTW; i += kIThreads) {  // slot b, segment s: half2(q_lo16, -q_hi16)
     const int b = i / kTW, sg = i % kTW;
     const uint2 v = a.g_q16[sg * P + (b >> 1)];
-    s_qs[b][sg] = half_of(v.x, b & 1) | (half_of(v.y, b & 1) << 16);
+    sts_u32(hole_addr(T, b >> 1) + 64u * (uint32_t)(b & 1) + 4u * (uint32_t)sg,
+            half_of(v.x, b & 1) | (half_of(v.y, b & 1) << 16));
   }
-  lb_consts_init(a, nslots, &s_c);  // ends with __syncthreads
-  const uint32_t lanebase = tab_s | ((uint32_t)lane * 8u);  // bytes {lane*8, 0, table bits 16-31}
-  int rot = 0;
+  if (HC) {
+    for (int i = tid; i < nslots * kNBC; i += kIThreads) sts_u32(hole_addr(T, 128 + i / kNBC) + 4u * (uint32_t)(i % kNBC), 0u);
+  } else {
+    for (int i = tid; i < nslots * kNB / 2; i += kIThreads) hist16[i] = 0;
+  }
+  if (warp < kIWarps) {
+    for (int b = lane; b < kMaxB; b += 32) M.w[warp].cnt[b] = 0;
+    if (lane == 0) M.w[warp].n = 0;
+  }
+  lb_consts_init(a, nslots, &M.c);  // ends with __syncthreads
 
-  for (int64_t it = 0;; ++it) {
-    const int64_t li = blockIdx.x + it * gridDim.x;
-    if (li >= nlist) break;
-    const int st = (int)(it % NST);
-    mbar_wait(&s_full[st], (unsigned)((it / NST) & 1));
-    const int64_t tile = s_tile[st];
-    PARIS_DCHECK(tile >= 0 && tile * kTS < a.n);
-    // the tile's 32 block masks (lane = block); a block's live slots are computed two
-    // at a time (consecutive live slots form an item); a 64-series block is half a
-    // warp, so a warp takes two items per round (lanes 0-15 and 16-31); items are
-    // dealt round-robin, rotating, so no warp is systematically behind
-    const uint64_t bm = s_bm[st][lane];
-    const int cnt = (__popcll(bm) + 1) >> 1;
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    const uint32_t* rows = reinterpret_cast<const uint32_t*>(s_tiles + (size_t)st * kTileBytes);
-    const int first = (warp - rot + 2 * kIWarps) % kIWarps;
-    rot = (rot + (total + 1) / 2) % kIWarps;
-    const int h = lane >> 4, hl = lane & 15;
-#if PARIS_LBI_DYN
-    // dynamic: a warp claims the stage's next item pair until none is left
-    for (int t0;;) {
-      unsigned c = 0;
-      if (lane == 0) c = atomicAdd(&s_next[st], 2u);
-      t0 = (int)__shfl_sync(0xffffffffu, c, 0);
-      if (t0 >= total) break;
-      (void)first;
-#else
-    for (int t0 = 2 * first; t0 < total; t0 += 2 * kIWarps) {
-#endif
-      const int t = t0 + h;  // this half-warp's item
-      const unsigned m0 = __ballot_sync(0xffffffffu, incl <= t0);
-      const unsigned m1 = __ballot_sync(0xffffffffu, incl <= t0 + 1);
-      const bool active = t < total;
-      const int k = active ? __popc(h ? m1 : m0) : 0;
-      const int excl = __shfl_sync(0xffffffffu, incl - cnt, k);
-      const uint64_t bmk = __shfl_sync(0xffffffffu, (unsigned long long)bm, k);
-      // slots 2r+1 and 2r+2 (1-based) of the block's live set: clear the first 2r bits
-      uint64_t m = active ? bmk : 0ull;
-      for (int i = t - excl; i > 0; --i) {
-        m &= m - 1;
-        m &= m - 1;
-      }
-      const int sa = m ? __ffsll((long long)m) - 1 : 0;
-      m &= m - 1;
-      const int sb = (active && m) ? __ffsll((long long)m) - 1 : -1;
-      const int sq = sb >= 0 ? sb : sa;  // odd count: duplicate lane, masked in emission
-      uint32_t acc[4] = {0u, 0u, 0u, 0u};
-#pragma unroll kLbiUnroll
-      for (int s = 0; s < kTW; ++s) {
-        const uint32_t word = rows[s * (kTS / 4) + k * (PARIS_INDEX_BLOCK / 4) + hl];
-        const uint32_t qa = s_qs[sa][s], qb = s_qs[sq][s];
-        const uint32_t qx = __byte_perm(qa, qb, 0x5410);  // (q_lo16[sa], q_lo16[sb])
-        const uint32_t qy = __byte_perm(qa, qb, 0x7632);  // (-q_hi16[sa], -q_hi16[sb])
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          // address = {lanebase.b0, word.bj, lanebase.b2, lanebase.b3}
-          const uint2 tt = lds_u2(__byte_perm(word, lanebase, 0x7604u | ((uint32_t)j << 4)));
-          const uint32_t a1 = h2_fma_relu(qx, kHalf2One, tt.x);
-          const uint32_t b1 = h2_fma_relu(qy, kHalf2One, tt.y);
-          acc[j] = h2_acc_delta2(acc[j], a1, b1);
-        }
-      }
-      const int64_t i0 = tile * kTS + k * PARIS_INDEX_BLOCK + 4 * hl;
-      const int nvalid = active ? (int)std::max<int64_t>(0, imin64(4, a.n - i0)) : 0;
-      PARIS_DCHECK(k < kBPT && sa >= 0 && sa < nslots && sb < nslots);
-      lbi_emit<HC ? 2 : 1>(acc, sa, sb, i0, nvalid, nslots, s_c, a, wb, s_hist);
-    }
-    __syncwarp();
+  if (warp == kIWarps) {
+    // ---- producer: refill stage st as soon as every consumer warp released it
     if (lane == 0) {
-      if (atomicAdd(&s_cnt[st], 1u) == kIWarps - 1) {
-        s_cnt[st] = 0;
-        s_next[st] = 0;
-        const int64_t next = li + (int64_t)NST * gridDim.x;
-        if (next < nlist) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          issue(next, st);
-        }
+      int64_t li = blockIdx.x;
+      unsigned tnext = li < nlist ? __ldg(tile_list + li) : 0u;
+      for (int64_t it = 0; li < nlist; ++it, li += gridDim.x) {
+        const int st = (int)(it % NST);
+        const unsigned tile = tnext;
+        if (li + gridDim.x < nlist) tnext = __ldg(tile_list + li + gridDim.x);  // the next id, early
+        if (it >= NST) mbar_wait(&M.empty[st], (unsigned)(((it / NST) - 1) & 1));
+        M.tile[st] = tile;
+        M.next[st] = 0;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&M.full[st], (unsigned)(kTileBytes + kBPT * 8));
+        bulk_g2s(gbase + stage_addr(st), a.sax + (size_t)tile * kTileBytes, (unsigned)kTileBytes, &M.full[st]);
+        bulk_g2s(&M.bm[st][0], bmask + (size_t)tile * kBPT, (unsigned)(kBPT * 8), &M.full[st]);
       }
     }
+  } else {
+    // ---- consumers
+    LbiWarp& wb = M.w[warp];
+    const LbConsts& c = M.c;
+    const uint32_t lanebase = T | ((uint32_t)(lane & 15) * 8u);  // bytes {lane%16 * 8, 0, T bits 16-31}
+    const int h = lane >> 4, hl = lane & 15;
+    for (int64_t it = 0;; ++it) {
+      const int64_t li = blockIdx.x + it * gridDim.x;
+      if (li >= nlist) break;
+      const int st = (int)(it % NST);
+      mbar_wait(&M.full[st], (unsigned)((it / NST) & 1));
+      const int64_t tile = M.tile[st];
+      PARIS_DCHECK(tile >= 0 && tile * kTS < a.n);
+      // the tile's 32 block masks (lane = block); a block's live slots are evaluated two
+      // at a time (an item); a 64-series block is half a warp, so a warp claims two items
+      const uint64_t bm = M.bm[st][lane];
+      const int cnt = (__popcll(bm) + 1) >> 1;
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      const uint32_t rows = stage_addr(st);
+      for (;;) {
+        unsigned cl = 0;
+        if (lane == 0) cl = atomicAdd(&M.next[st], 2u);
+        const int t0 = (int)__shfl_sync(0xffffffffu, cl, 0);
+        if (t0 >= total) break;
+        const int t = t0 + h;  // this half-warp's item
+        const unsigned m0 = __ballot_sync(0xffffffffu, incl <= t0);
+        const unsigned m1 = __ballot_sync(0xffffffffu, incl <= t0 + 1);
+        const bool active = t < total;
+        const int k = active ? __popc(h ? m1 : m0) : 0;
+        const int excl = __shfl_sync(0xffffffffu, incl - cnt, k);
+        const uint64_t bmk = __shfl_sync(0xffffffffu, (unsigned long long)bm, k);
+        // slots 2r+1 and 2r+2 (1-based) of the block's live set: clear the first 2r bits
+        uint64_t m = active ? bmk : 0ull;
+        for (int i = t - excl; i > 0; --i) {
+          m &= m - 1;
+          m &= m - 1;
+        }
+        const int sa = m ? __ffsll((long long)m) - 1 : 0;
+        m &= m - 1;
+        const int sb = (active && m) ? __ffsll((long long)m) - 1 : -1;
+        const int sq = sb >= 0 ? sb : sa;  // odd count: duplicate lane, masked in emission
+        // (generic pointers derived from dsm: LDS with immediate segment offsets)
+        const uint32_t* qa_p = reinterpret_cast<const uint32_t*>(gbase + hole_addr(T, sa >> 1) + 64u * (uint32_t)(sa & 1));
+        const uint32_t* qb_p = reinterpret_cast<const uint32_t*>(gbase + hole_addr(T, sq >> 1) + 64u * (uint32_t)(sq & 1));
+        const uint32_t* wp = reinterpret_cast<const uint32_t*>(gbase + rows) + k * (PARIS_INDEX_BLOCK / 4) + hl;
+        uint32_t acc[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int s = 0; s < kTW; ++s) {
+          const uint32_t word = wp[s * (kTS / 4)];
+          const uint32_t qa = qa_p[s], qb = qb_p[s];
+          const uint32_t qx = __byte_perm(qa, qb, 0x5410);  // (q_lo16[sa], q_lo16[sb])
+          const uint32_t qy = __byte_perm(qa, qb, 0x7632);  // (-q_hi16[sa], -q_hi16[sb])
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            // address = {lanebase.b0, word.bj, lanebase.b2, lanebase.b3}
+            const uint2 tt = lds_u2(__byte_perm(word, lanebase, 0x7604u | ((uint32_t)j << 4)));
+            const uint32_t a1 = h2_fma_relu(qx, kHalf2One, tt.x);
+            const uint32_t b1 = h2_fma_relu(qy, kHalf2One, tt.y);
+            acc[j] = h2_acc_delta2(acc[j], a1, b1);
+          }
+        }
+        const int64_t i0 = tile * kTS + k * PARIS_INDEX_BLOCK + 4 * hl;
+        const int nvalid = active ? (int)std::max<int64_t>(0, imin64(4, a.n - i0)) : 0;
+        PARIS_DCHECK(k < kBPT && sa >= 0 && sa < nslots && sb < nslots);
+        lbi_emit<HC>(acc, sa, sb, i0, nvalid, nslots, c, a, wb, T, warp, hist16);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&M.empty[st]);  // this warp is done reading stage st
+    }
+    lbi_flush<HC>(wb, T, warp, nslots, c, a, hist16);
   }
-  wb_flush<HC ? 2 : 1>(wb, nslots, s_c, a, s_hist);
   __syncthreads();
   if (HC) {
-    for (int i = tid; i < nslots * kNBC; i += kIThreads)
-      if (s_hist[i]) atomicAdd(&a.hist[(i / kNBC) * kNB + (i % kNBC) * 8 + 7], s_hist[i]);
+    for (int i = tid; i < nslots * kNBC; i += kIThreads) {
+      const uint32_t v = lds_u32(hole_addr(T, 128 + i / kNBC) + 4u * (uint32_t)(i % kNBC));
+      if (v) atomicAdd(&a.hist[(i / kNBC) * kNB + (i % kNBC) * 8 + 7], v);
+    }
   } else {
     for (int i = tid; i < nslots * kNB; i += kIThreads) {
-      const unsigned v = (s_hist[i >> 1] >> (16 * (i & 1))) & 0xFFFFu;
+      const unsigned v = (hist16[i >> 1] >> (16 * (i & 1))) & 0xFFFFu;
       if (v) atomicAdd(&a.hist[i], v);
     }
   }
@@ -2730,17 +2793,205 @@ k_finalize(const uint64_t* __restrict__ lists, int nslots, int k, int q0,
   }
 }
 
-// ---------------------------------------------------------------- host side
-int g_sms = 0;
-int sms() {
-  if (!g_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_sms <= 0) g_sms = 148;
+// ---------------------------------------------------------------- candidate-buffer overflow
+// A query whose LB pass kept more than `cap` candidates (count[b] > cap) had only the
+// stored ones refined.  Its result so far is a real BSF (k = 1: the best key; k > 1:
+// the live threshold thr[b], a rigorous bound of the k-th exact distance), so an exact
+// answer needs every series whose bound is below it -- this kernel scans them all
+// without a candidate buffer: a rigorous fp32 MINDIST (outward fp32 regions, round-down
+// arithmetic) per series, the survivors refined at once (fused LB -> refine, the
+// DistComp loop of Alg8, with the BSF shared as in ParIS+).  k = 1 lowers
+// the shared BSF key; k > 1 keeps a warp-private top-k (shared memory) whose k-th also
+// lowers thr[b]; the warps' lists are merged by k_finalize_ovf.  Gated on the device:
+// every CTA leaves at once when no query of the batch overflowed, so the host never
+// waits for the counts.
+struct FbArgs {
+  const uint8_t* sax;      // flat [w][n], or the index's tile-major sorted array (perm != nullptr)
+  const uint32_t* perm;
+  int64_t n;
+  int w, len;
+  float seglen_f;
+  const CardTables* tab;
+  const float2* g_q;       // [slot][kMaxW] query PAA intervals (round down, round up)
+  const float* queries;    // batch [nb][len]
+  const float* raw;
+  int nb;
+  const unsigned* count;
+  int64_t cap;
+  int k;
+  float d2up;
+  unsigned long long* best;  // k = 1
+  unsigned* thr;             // k > 1: per query (kPadU32 stride), float bits
+  uint64_t* lists;           // k > 1: [nb][L][k]
+  int L;                     // warps of the grid (lists per query)
+  unsigned* refined;         // per query: rows refined here
+};
+constexpr int kFbThreads = 128;
+
+template <bool K1>
+__global__ void __launch_bounds__(kFbThreads)
+k_fallback(FbArgs a) {
+  extern __shared__ uint64_t s_top[];  // k > 1: [warps][k] ascending keys
+  __shared__ float2 s_lu[kMaxCard];
+  __shared__ float2 s_q[kMaxW];
+  __shared__ int s_any;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    int any = 0;
+    for (int b = 0; b < a.nb; ++b) any |= (int64_t)a.count[b] > a.cap;
+    s_any = any;
   }
-  return g_sms;
+  __syncthreads();
+  if (!s_any) return;  // the common case: one shared load, then exit
+  for (int i = tid; i < kMaxCard; i += blockDim.x) s_lu[i] = a.tab->lu[i];
+  const int nw = blockDim.x >> 5;
+  const int gw = blockIdx.x * nw + warp;
+  const int64_t per = ((a.n + (int64_t)a.L - 1) / a.L + 31) / 32 * 32;
+  const int64_t lo = imin64(a.n, (int64_t)gw * per), hi = imin64(a.n, lo + per);
+  const int nf = a.len >> 2;
+  uint64_t* top = s_top + (size_t)warp * (K1 ? 1 : a.k);
+  for (int b = 0; b < a.nb; ++b) {
+    if ((int64_t)a.count[b] <= a.cap) continue;
+    __syncthreads();
+    for (int i = tid; i < kMaxW; i += blockDim.x) s_q[i] = a.g_q[b * kMaxW + i];
+    __syncthreads();
+    const float4* qv = reinterpret_cast<const float4*>(a.queries + (size_t)b * a.len);
+    unsigned long long* bp = a.best + (size_t)b * kPadU64;
+    uint64_t cur = K1 ? ld_relaxed_u64(bp) : kNoKey;
+    int filled = 0;  // k > 1: entries in this warp's list
+    if (!K1)
+      for (int i = lane; i < a.k; i += 32) top[i] = kNoKey;
+    __syncwarp();
+    unsigned nref = 0;
+    for (int64_t base = lo; base < hi; base += 32) {
+      const int64_t i = base + lane;
+      float thr;
+      if (K1) {
+        cur = min(cur, ld_relaxed_u64(bp));
+        thr = cur == kNoKey ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
+      } else {
+        thr = __uint_as_float(ld_relaxed_u32(&a.thr[b * kPadU32]));
+        if (filled == a.k) thr = fminf(thr, __fmul_ru(key_val(top[a.k - 1]), a.d2up));
+      }
+      float lb = INFINITY;
+      uint32_t id = 0;
+      if (i < hi) {
+        lb = 0.f;
+        for (int s = 0; s < a.w; ++s) {
+          const uint8_t sym = a.perm ? a.sax[(size_t)(i / kTS) * kTW * kTS + (size_t)s * kTS + i % kTS]
+                                     : a.sax[(size_t)s * a.n + i];
+          const float2 r = s_lu[sym];   // {L rounded down, U rounded up}
+          const float2 q = s_q[s];      // {q rounded down, q rounded up}
+          const float d = fmaxf(fmaxf(__fsub_rd(q.x, r.y), __fsub_rd(r.x, q.y)), 0.f);
+          lb = __fadd_rd(lb, __fmul_rd(d, d));
+        }
+        lb = __fmul_rd(lb, a.seglen_f);
+        id = a.perm ? __ldg(a.perm + i) : (uint32_t)i;
+      }
+      unsigned m = __ballot_sync(0xffffffffu, lb <= thr);
+      while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const uint32_t cid = __shfl_sync(0xffffffffu, id, src);
+        if (__shfl_sync(0xffffffffu, lb, src) > thr) continue;
+        const float4* row = reinterpret_cast<const float4*>(a.raw + (size_t)cid * a.len);
+        float acc = 0.f;
+        bool abandoned = false;
+        for (int c0 = 0; c0 < nf; c0 += 32) {
+          const int f = c0 + lane;
+          if (f < nf) {
+            const float4 x = ld_stream(row + f), y = __ldg(qv + f);
+            float d;
+            d = x.x - y.x; acc = fmaf(d, d, acc);
+            d = x.y - y.y; acc = fmaf(d, d, acc);
+            d = x.z - y.z; acc = fmaf(d, d, acc);
+            d = x.w - y.w; acc = fmaf(d, d, acc);
+          }
+          if (c0 + 32 < nf && warp_sum(acc) > thr) { abandoned = true; break; }  // early abandoning
+        }
+        ++nref;
+        if (abandoned) continue;
+        const float d2 = warp_sum(acc);
+        const uint64_t key = make_key(d2, cid);
+        if (K1) {
+          if (key < cur) {
+            if (lane == 0) atomicMin(bp, (unsigned long long)key);
+            cur = key;
+            thr = __fmul_ru(d2, a.d2up);
+          }
+        } else if (filled < a.k || key < top[a.k - 1]) {
+          // sorted insert into the warp's list: rank = #entries < key
+          int r = 0;
+          for (int j = lane; j < filled; j += 32) r += top[j] < key;
+          r = __reduce_add_sync(0xffffffffu, r);
+          const int last = min(filled, a.k - 1);  // entries [r, last) move up by one
+          for (int hi2 = last; hi2 > r; hi2 -= 32) {
+            const int j = hi2 - 1 - lane;
+            const uint64_t v = (j >= r) ? top[j] : 0ull;
+            __syncwarp();
+            if (j >= r) top[j + 1] = v;
+            __syncwarp();
+          }
+          if (lane == 0) top[r] = key;
+          __syncwarp();
+          filled = min(filled + 1, a.k);
+          if (filled == a.k) {
+            const float t = __fmul_ru(key_val(top[a.k - 1]), a.d2up);
+            if (lane == 0) atomicMin(&a.thr[b * kPadU32], __float_as_uint(t));
+            thr = fminf(thr, t);
+          }
+        }
+      }
+    }
+    if (!K1) {
+      uint64_t* out = a.lists + ((size_t)b * a.L + gw) * a.k;
+      for (int j = lane; j < a.k; j += 32) out[j] = top[j];
+    }
+    if (lane == 0 && nref) atomicAdd(&a.refined[b], nref);
+  }
 }
+
+// Merge sorted lists (nlists x k keys per query) into the query's top-k; ascending
+// (d^2, id) -> (id, sqrt d^2).  One CTA of 1024 threads per query.
+__device__ void merge_lists_topk(const uint64_t* __restrict__ src, int64_t total, int k, uint64_t* buf) {
+  for (int i = threadIdx.x; i < kSortP; i += blockDim.x) buf[i] = kNoKey;
+  __syncthreads();
+  const int chunk = kSortP - k;
+  for (int64_t off = 0; off < total; off += chunk) {
+    for (int i = threadIdx.x; i < chunk; i += blockDim.x) buf[k + i] = (off + i < total) ? src[off + i] : kNoKey;
+    __syncthreads();
+    bitonic_sort(buf, kSortP);
+  }
+}
+
+// k_fallback's outputs for the overflowed queries of a batch (others untouched).
+__global__ void __launch_bounds__(1024)
+k_finalize_ovf(const unsigned long long* __restrict__ best, const uint64_t* __restrict__ lists, int L, int k, int q0,
+               const unsigned* __restrict__ count, int64_t cap, int64_t* __restrict__ out_idx,
+               float* __restrict__ out_dist, const unsigned* __restrict__ fb_refined, unsigned* __restrict__ all_refined) {
+  __shared__ uint64_t buf[kSortP];
+  const int b = blockIdx.x;
+  if ((int64_t)count[b] <= cap) return;
+  if (k == 1) {
+    if (threadIdx.x == 0) {
+      const uint64_t key = best[b * kPadU64];
+      out_idx[q0 + b] = key == kNoKey ? -1 : (int64_t)key_id(key);
+      out_dist[q0 + b] = key == kNoKey ? INFINITY : sqrtf(key_val(key));
+    }
+  } else {
+    merge_lists_topk(lists + (size_t)b * L * k, (int64_t)L * k, k, buf);
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+      const uint64_t key = buf[i];
+      const size_t o = (size_t)(q0 + b) * k + i;
+      if (key == kNoKey) { out_idx[o] = -1; out_dist[o] = INFINITY; }
+      else { out_idx[o] = (int64_t)key_id(key); out_dist[o] = sqrtf(key_val(key)); }
+    }
+  }
+  if (threadIdx.x == 0) all_refined[q0 + b] += fb_refined[b];
+}
+
+// ---------------------------------------------------------------- host side
+int sms() { return device_sms(); }
 
 template <typename K>
 int occupancy(K kernel, int threads, size_t smem) {
@@ -2768,8 +3019,8 @@ struct Ws {
   unsigned* ghist;       // k > 1: refined-distance histograms [B][kNB]
   unsigned long long* bmask;  // index mode: [ntiles*32] per-block live query-slot masks
   unsigned* tile_list;   // index mode: live tiles
-  unsigned* tile_flag;   // index mode: [ntiles] tile already listed (zeroed per batch)
-  size_t flag_bytes;
+  unsigned* fb_refined;  // overflow fallback: rows refined per query
+  uint64_t* fb_lists;    // overflow fallback, k > 1: [B][fbL][k] warp lists
   size_t zero_bytes;
   unsigned long long* best;
   uint64_t* cand;
@@ -2797,6 +3048,7 @@ struct Plan {
   bool sorted_refine = false;  // k = 1: walk bucket-sorted lists (K5) instead of the unsorted waves
   const uint16_t* raw16 = nullptr;  // optional bf16 copy of raw: refine pre-filter (k = 1)
   bool raw_host = false;            // raw in pinned host memory (f3)
+  int fbL = 0;                      // overflow fallback: warps of its grid (= lists per query for k > 1)
 };
 
 int pairs_for(int nb) { return nb <= 2 ? 1 : nb <= 4 ? 2 : nb <= 8 ? 4 : nb <= 16 ? 8 : nb <= 32 ? 16 : 32; }
@@ -2811,8 +3063,8 @@ cudaError_t launch_seed(const Plan& p, const uint8_t* sax, const float* qb, int 
 template <int P, int WT, bool AL>
 cudaError_t launch_lb(const Plan& p, const uint8_t* sax, int nb, const CardTables* tab, const Ws& ws,
                       cudaStream_t st, int64_t cap) {
-  static int occ = 0;
-  if (!occ) occ = occupancy(k_lb<P, WT, AL>, kLBThreads, 0);
+  const int occ = cached_per_device((const void*)k_lb<P, WT, AL>,
+                                    [](int) { return occupancy(k_lb<P, WT, AL>, kLBThreads, 0); });
   const int64_t ngroups = (p.n + 3) / 4;
   const int64_t need = (ngroups + kLBThreads - 1) / kLBThreads;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)sms() * occ));
@@ -2855,14 +3107,10 @@ cudaError_t dispatch_p(int P, bool lb, const Plan& p, const uint8_t* sax, const 
 template <int P, int MODE>
 cudaError_t launch_lbt(const Plan& p, const uint8_t* sax, int nb, const CardTables* tab, const Ws& ws,
                        cudaStream_t st, int64_t cap, int64_t nlim, int grid) {
-  static int attr_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(k_lbt<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTSmem);
-    if (e != cudaSuccess) return e;
-    attr_dev = dev;
-  }
+  cudaError_t ea = once_per_device((const void*)k_lbt<P, MODE>, [](int) {
+    return cudaFuncSetAttribute(k_lbt<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTSmem);
+  });
+  if (ea != cudaSuccess) return ea;
   LbArgs la;
   la.sax = sax; la.n = p.n; la.w = p.w; la.seglen_f = (float)(p.len / p.w); la.tab = tab;
   la.g_q = ws.g_q; la.g_q16 = ws.g_q16; la.nb = nb; la.thr = ws.thr_seed; la.count = ws.count;
@@ -2872,34 +3120,26 @@ cudaError_t launch_lbt(const Plan& p, const uint8_t* sax, int nb, const CardTabl
                       ws.seed_ids, p.S);
 }
 
+// dynamic shared memory of k_lbi<P, HC>: everything the device allows a CTA beyond the
+// kernel's static shared memory (the kernel checks its layout fits)
 template <int P, bool HC>
-size_t& lbi_smem() {  // dynamic shared memory of k_lbi<P, HC> (set once per device)
-  static size_t v = 0;
-  return v;
+int lbi_smem() {
+  return cached_per_device((const void*)k_lbi<P, HC>, [](int dev) {
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, k_lbi<P, HC>) != cudaSuccess) return 0;
+    const int v = optin - (int)fa.sharedSizeBytes;
+    if (cudaFuncSetAttribute(k_lbi<P, HC>, cudaFuncAttributeMaxDynamicSharedMemorySize, v) != cudaSuccess) return 0;
+    return v;
+  });
 }
 
 template <int P>
 cudaError_t launch_index_lb(const Plan& p, const uint8_t* sax, int nb, const CardTables* tab, const Ws& ws,
                             cudaStream_t st, int64_t cap) {
-  static int attr_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (attr_dev != dev) {
-    int optin = 0;
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncAttributes fa;
-    cudaError_t e = cudaFuncGetAttributes(&fa, k_lbi<P, false>);
-    if (e != cudaSuccess) return e;
-    lbi_smem<P, false>() = (size_t)optin - fa.sharedSizeBytes;
-    e = cudaFuncSetAttribute(k_lbi<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lbi_smem<P, false>());
-    if (e != cudaSuccess) return e;
-    e = cudaFuncGetAttributes(&fa, k_lbi<P, true>);
-    if (e != cudaSuccess) return e;
-    lbi_smem<P, true>() = (size_t)optin - fa.sharedSizeBytes;
-    e = cudaFuncSetAttribute(k_lbi<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lbi_smem<P, true>());
-    if (e != cudaSuccess) return e;
-    attr_dev = dev;
-  }
+  const int smem = p.sorted_refine ? lbi_smem<P, false>() : lbi_smem<P, true>();
+  if (smem <= 0) return cudaErrorInvalidConfiguration;
   LbArgs la;
   la.sax = sax; la.n = p.n; la.w = p.w; la.seglen_f = (float)(p.len / p.w); la.tab = tab;
   la.g_q = ws.g_q; la.g_q16 = ws.g_q16; la.nb = nb; la.thr = ws.thr_seed; la.count = ws.count;
@@ -2911,11 +3151,11 @@ cudaError_t launch_index_lb(const Plan& p, const uint8_t* sax, int nb, const Car
                                ws.tile_count, ws.blocks);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(sms(), ntiles);
-  if (!p.sorted_refine)  // coarse histograms suffice for the wave cut (no bucket sort): 3 ring stages
-    return PARIS_LAUNCH("lb_pass", (k_lbi<P, true>), grid, kIThreads, (lbi_smem<P, true>()), st, la, ws.bmask,
-                        ws.tile_list, ws.tile_count);
-  return PARIS_LAUNCH("lb_pass", (k_lbi<P, false>), grid, kIThreads, (lbi_smem<P, false>()), st, la, ws.bmask,
-                      ws.tile_list, ws.tile_count);
+  if (!p.sorted_refine)  // coarse histograms suffice for the wave cut (no bucket sort): 4 ring stages
+    return PARIS_LAUNCH("lb_pass", (k_lbi<P, true>), grid, kIThreads, smem, st, la, ws.bmask, ws.tile_list,
+                        ws.tile_count);
+  return PARIS_LAUNCH("lb_pass", (k_lbi<P, false>), grid, kIThreads, smem, st, la, ws.bmask, ws.tile_list,
+                      ws.tile_count);
 }
 
 cudaError_t dispatch_index_lb(int nb, const Plan& p, const uint8_t* sax, const CardTables* tab, const Ws& ws,
@@ -2957,8 +3197,7 @@ cudaError_t launch_nb(const Plan& p, const float* raw, const uint8_t* sax, const
 cudaError_t launch_lb1(const Plan& p, const uint8_t* sax, const CardTables* tab, const Ws& ws, cudaStream_t st,
                        int64_t cap) {
   constexpr int SPT = PARIS_LB1_SPT;
-  static int occ = 0;
-  if (!occ) occ = occupancy(k_lb1<SPT>, kLb1Threads, 0);
+  const int occ = cached_per_device((const void*)k_lb1<SPT>, [](int) { return occupancy(k_lb1<SPT>, kLb1Threads, 0); });
   LbArgs la;
   la.sax = sax; la.n = p.n; la.w = p.w; la.seglen_f = (float)(p.len / p.w); la.tab = tab;
   la.g_q = ws.g_q; la.g_q16 = ws.g_q16; la.nb = 1; la.thr = ws.thr_seed; la.count = ws.count;
@@ -3014,8 +3253,9 @@ cudaError_t launch_refine1u(const RefineArgs& ra, int nb, int wave, const unsign
   return PARIS_LAUNCH("refine", (k_refine1u<NC, U, false>), grid, kRefThreads, 0, st, ra, nb, wave, cut);
 }
 
-// Allocate the batch scratch for `cap` candidates per query.
-int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
+// Layout of the batch scratch for `cap` candidates per query: returns its size; with
+// base != nullptr also carves `ws` out of it.
+size_t ws_layout(const Plan& p, int64_t cap, Ws* ws, char* base) {
   const int B = 2 * pairs_for(p.B);
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off = (off + bytes + 255) & ~(size_t)255; return o; };
@@ -3023,50 +3263,72 @@ int alloc_ws(const Plan& p, int64_t cap, Ws& ws, cudaStream_t st) {
   const size_t o_q16 = take(sizeof(uint2) * (B / 2) * kMaxW);
   const size_t o_sid = take(sizeof(int) * B * p.S);
   const size_t o_skey = take(sizeof(uint64_t) * B * p.S);
-  const size_t zb = sizeof(unsigned) * (B + B + B * kNB + B * kNB + B + B + 1 + B + (p.k > 1 ? B * kNB + 4 : 0));
+  // zeroed per batch: thr_seed | count | hist | cursor | refined | blocks | tile_count | updates
+  //                   | fb_refined | (k > 1) ghist
+  const size_t zb = sizeof(unsigned) * (B + B + B * kNB + B * kNB + B + B + 1 + B + B + (p.k > 1 ? B * kNB + 4 : 0));
   const size_t o_zero = take(zb);
   const size_t o_best = take(sizeof(unsigned long long) * B * kPadU64);
   const size_t o_thr = take(sizeof(unsigned) * B * kPadU32);
   const size_t o_cand = take(sizeof(uint64_t) * B * (size_t)cap);
-  const size_t o_sorted = take(sizeof(uint64_t) * B * (size_t)cap);
-  const size_t o_lists = take(p.k > 1 ? sizeof(uint64_t) * B * (size_t)p.XB * p.k : 8);
+  // the bucket-sorted lists (sorted walk) or the k > 1 result lists; k = 1 on the unsorted
+  // waves needs neither
+  const bool need_sorted = p.sorted_refine || p.k > 1;
+  const size_t o_sorted = take(need_sorted ? sizeof(uint64_t) * B * (size_t)cap : 8);
+  const size_t o_lists = take(p.k > 1 && p.sorted_refine ? sizeof(uint64_t) * B * (size_t)p.XB * p.k : 8);
+  const size_t o_fbl = take(p.k > 1 ? sizeof(uint64_t) * B * (size_t)p.fbL * p.k : 8);
   const int64_t ntiles = (p.n + kTS - 1) / kTS;
   const size_t o_bmask = take(p.perm ? sizeof(unsigned long long) * (size_t)ntiles * kBPT : 8);
   const size_t o_tlist = take(p.perm ? sizeof(unsigned) * (size_t)ntiles : 8);
-  const size_t o_tflag = take(p.perm ? sizeof(unsigned) * (size_t)ntiles : 8);
-  void* base = nullptr;
-  cudaError_t e = cudaMallocAsync(&base, off, st);
-  if (e != cudaSuccess) {
-    set_error("paris_knn_exact: scratch allocation of %zu bytes failed (%s)", off, cudaGetErrorString(e));
-    cudaGetLastError();
-    return PARIS_ENOMEM;
-  }
-  char* c = (char*)base;
-  ws.base = base;
-  ws.g_q = (float2*)(c + o_q);
-  ws.g_q16 = (uint2*)(c + o_q16);
-  ws.seed_ids = (int*)(c + o_sid);
-  ws.seed_keys = (uint64_t*)(c + o_skey);
-  ws.zero_block = (unsigned*)(c + o_zero);
-  ws.zero_bytes = zb;
-  ws.thr = (unsigned*)(c + o_thr);
-  ws.thr_seed = ws.zero_block;
-  ws.count = ws.thr_seed + B;
-  ws.hist = ws.count + B;
-  ws.cursor = ws.hist + B * kNB;
-  ws.refined = ws.cursor + B * kNB;
-  ws.blocks = ws.refined + B;
-  ws.tile_count = ws.blocks + B;
-  ws.updates = ws.tile_count + 1;
-  ws.ghist = p.k > 1 ? (unsigned*)(((uintptr_t)(ws.updates + B) + 15) & ~(uintptr_t)15) : nullptr;
-  ws.best = (unsigned long long*)(c + o_best);
-  ws.cand = (uint64_t*)(c + o_cand);
-  ws.sorted = (uint64_t*)(c + o_sorted);
-  ws.lists = (uint64_t*)(c + o_lists);
-  ws.bmask = (unsigned long long*)(c + o_bmask);
-  ws.tile_list = (unsigned*)(c + o_tlist);
-  ws.tile_flag = (unsigned*)(c + o_tflag);
-  ws.flag_bytes = p.perm ? sizeof(unsigned) * (size_t)ntiles : 0;
+  if (!base) return off;
+  char* c = base;
+  ws->base = base;
+  ws->g_q = (float2*)(c + o_q);
+  ws->g_q16 = (uint2*)(c + o_q16);
+  ws->seed_ids = (int*)(c + o_sid);
+  ws->seed_keys = (uint64_t*)(c + o_skey);
+  ws->zero_block = (unsigned*)(c + o_zero);
+  ws->zero_bytes = zb;
+  ws->thr = (unsigned*)(c + o_thr);
+  ws->thr_seed = ws->zero_block;
+  ws->count = ws->thr_seed + B;
+  ws->hist = ws->count + B;
+  ws->cursor = ws->hist + B * kNB;
+  ws->refined = ws->cursor + B * kNB;
+  ws->blocks = ws->refined + B;
+  ws->tile_count = ws->blocks + B;
+  ws->updates = ws->tile_count + 1;
+  ws->fb_refined = ws->updates + B;
+  ws->ghist = p.k > 1 ? (unsigned*)(((uintptr_t)(ws->fb_refined + B) + 15) & ~(uintptr_t)15) : nullptr;
+  ws->best = (unsigned long long*)(c + o_best);
+  ws->cand = (uint64_t*)(c + o_cand);
+  ws->sorted = (uint64_t*)(c + o_sorted);
+  ws->lists = (uint64_t*)(c + o_lists);
+  ws->fb_lists = (uint64_t*)(c + o_fbl);
+  ws->bmask = (unsigned long long*)(c + o_bmask);
+  ws->tile_list = (unsigned*)(c + o_tlist);
+  return off;
+}
+
+// The overflow fallback of a batch (k_fallback + k_finalize_ovf): two launches that
+// leave at once unless a query of the batch kept more than `cap` candidates.
+int launch_fallback(const Plan& p, const float* raw, const uint8_t* sax, const float* qbatch, int nb, int q0,
+                    int64_t cap, const CardTables* tab, const Ws& ws, int64_t* d_idx, float* d_dist,
+                    unsigned* all_refined, cudaStream_t st) {
+  FbArgs fa;
+  fa.sax = sax; fa.perm = p.perm; fa.n = p.n; fa.w = p.w; fa.len = p.len; fa.seglen_f = (float)(p.len / p.w);
+  fa.tab = tab; fa.g_q = ws.g_q; fa.queries = qbatch; fa.raw = raw; fa.nb = nb; fa.count = ws.count; fa.cap = cap;
+  fa.k = p.k; fa.d2up = p.d2up; fa.best = ws.best; fa.thr = ws.thr; fa.lists = ws.fb_lists; fa.L = p.fbL;
+  fa.refined = ws.fb_refined;
+  const int grid = p.fbL / (kFbThreads / 32);
+  if (p.k == 1)
+    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("fallback", k_fallback<true>, grid, kFbThreads, 0, st, fa), "fallback launch");
+  else
+    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("fallback", k_fallback<false>, grid, kFbThreads,
+                                    (size_t)(kFbThreads / 32) * p.k * 8, st, fa),
+                       "fallback launch");
+  PARIS_CHECK_LAUNCH(PARIS_LAUNCH("fallback", k_finalize_ovf, nb, 1024, 0, st, ws.best, ws.fb_lists, p.fbL, p.k, q0,
+                                  ws.count, cap, d_idx, d_dist, ws.fb_refined, all_refined),
+                     "fallback finalize launch");
   return PARIS_OK;
 }
 
@@ -3250,7 +3512,7 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
                                     ws.blocks, all_blocks, ws.updates, all_extra),
                        "finalize launch");
   }
-  return PARIS_OK;
+  return launch_fallback(p, raw, sax, qbatch, nb, q0, cap, tab, ws, d_idx, d_dist, all_refined, st);
 }
 
 bool is_host_ptr(const void* p) {
@@ -3394,93 +3656,93 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   // d2up >= (1+e)/(1-e) with margin, u = 2^-24
   p.d2up = (float)(1.0 + 2.5 * (len / 32 + 8) * 5.9604644775390625e-08);
 
+  // overflow fallback grid: 4 CTAs per SM (k = 1); for k > 1 its warp lists
+  // ([B][fbL][k] keys) are kept to <= 32 MB
+  {
+    const int Bq = 2 * pairs_for(p.B);
+    int L = sms() * 4 * (kFbThreads / 32);
+    if (k > 1) L = (int)std::max<int64_t>(kFbThreads / 32, std::min<int64_t>(L, (32ll << 20) / ((int64_t)Bq * k * 8)));
+    p.fbL = L / (kFbThreads / 32) * (kFbThreads / 32);
+  }
+  if (k > 1) {
+    const cudaError_t ea = once_per_device((const void*)k_fallback<false>, [](int) {
+      return cudaFuncSetAttribute(k_fallback<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (kFbThreads / 32) * PARIS_MAX_K * 8);
+    });
+    if (ea != cudaSuccess) return cuda_error(ea, "fallback smem attribute");
+  }
+
   retain_pool();
-  // host <-> device staging of queries / outputs
+  // host <-> device staging of queries / outputs, carved from the cached workspace after
+  // the batch scratch (no allocation in the steady state)
   const bool hq = is_host_ptr(queries), hi = is_host_ptr(out_idx), hd = is_host_ptr(out_dist);
   cudaError_t e;
-  char* stage = nullptr;
   const size_t qbytes = (size_t)nq * len * 4, ibytes = (size_t)nq * k * 8, dbytes = (size_t)nq * k * 4;
   const size_t cbytes = (size_t)nq * 4 * 5;
-  e = cudaMallocAsync((void**)&stage, qbytes + ibytes + dbytes + cbytes + 1024, st);
-  if (e != cudaSuccess) { cudaGetLastError(); set_error("paris_knn_exact: staging alloc failed"); return PARIS_ENOMEM; }
-  const float* d_q = queries;
-  int64_t* d_idx = out_idx;
-  float* d_dist = out_dist;
-  char* cur = stage;
-  float* sq = (float*)cur; cur += (qbytes + 255) & ~255ull;
-  int64_t* sidx = (int64_t*)cur; cur += (ibytes + 255) & ~255ull;
-  float* sdist = (float*)cur; cur += (dbytes + 255) & ~255ull;
+  auto up = [](size_t v) { return (v + 255) & ~(size_t)255; };
+  const size_t wsb = up(ws_layout(p, p.cap, nullptr, nullptr));
+  const size_t total = wsb + up(qbytes) + up(ibytes) + up(dbytes) + up(cbytes);
+  void* wsh = nullptr;
+  char* base = (char*)ws_acquire(total, st, &wsh, nullptr);
+  if (!base) return PARIS_ENOMEM;
+  Ws ws;
+  ws_layout(p, p.cap, &ws, base);
+  char* cur = base + wsb;
+  float* sq = (float*)cur; cur += up(qbytes);
+  int64_t* sidx = (int64_t*)cur; cur += up(ibytes);
+  float* sdist = (float*)cur; cur += up(dbytes);
   unsigned* all_count = (unsigned*)cur;
   unsigned* all_refined = all_count + nq;
   float* all_tau = (float*)(all_refined + nq);
   unsigned* all_blocks = (unsigned*)(all_tau + nq);
   unsigned* all_extra = all_blocks + nq;  // nb: BSF-copy updates; index + bf16: pre-filter rows
+  const float* d_q = queries;
+  int64_t* d_idx = hi ? sidx : out_idx;
+  float* d_dist = hd ? sdist : out_dist;
+  int rc = PARIS_OK;
   if (hq) {
     e = cudaMemcpyAsync(sq, queries, qbytes, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) { cudaFreeAsync(stage, st); return cuda_error(e, "H2D queries"); }
+    if (e != cudaSuccess) rc = cuda_error(e, "H2D queries");
     d_q = sq;
   }
-  if (hi) d_idx = sidx;
-  if (hd) d_dist = sdist;
-  if ((reinterpret_cast<uintptr_t>(d_q) & 15) != 0) {
-    cudaFreeAsync(stage, st);
+  if (rc == PARIS_OK && (reinterpret_cast<uintptr_t>(d_q) & 15) != 0) {
     set_error("paris_knn_exact: queries must be 16-byte aligned");
-    return PARIS_EINVAL;
+    rc = PARIS_EINVAL;
   }
-
-  e = cudaMemsetAsync(all_count, 0, cbytes, st);  // counters accumulate over a re-scan
-  if (e != cudaSuccess) { cudaFreeAsync(stage, st); return cuda_error(e, "memset counters"); }
+  if (rc == PARIS_OK) {
+    e = cudaMemsetAsync(all_count, 0, cbytes, st);
+    if (e != cudaSuccess) rc = cuda_error(e, "memset counters");
+  }
   // test hook (reserved[3] == 1): seed every batch from the rows already in out_idx/out_dist
   // (device outputs) instead of the approximate search -- measures the LB pass under an
   // ideal BSF; results stay exact for any seed
   const bool seed_from_out = cfg && cfg->reserved[3] == 1 && !hi && !hd;
-  Ws ws;
-  int rc = alloc_ws(p, p.cap, ws, st);
-  if (rc) { cudaFreeAsync(stage, st); return rc; }
   for (int q0 = 0; q0 < nq && rc == PARIS_OK; q0 += p.B) {
     const int nb = std::min(p.B, nq - q0);
     rc = run_batch(p, raw, sax, d_q + (size_t)q0 * len, nb, q0, p.cap, tab, ws, d_idx, d_dist,
                    all_count, all_refined, all_tau, all_blocks, all_extra, st, /*rescan=*/seed_from_out);
   }
-  // overflow check: one synchronization per call
-  std::vector<unsigned> h_count(nq), h_ref(nq), h_blk(nq), h_ext(nq);
-  std::vector<float> h_tau(nq);
-  if (rc == PARIS_OK) {
+  // no synchronization: a query whose candidate buffer overflowed was completed on the
+  // device (k_fallback); host outputs are copied back stream-ordered
+  if (rc == PARIS_OK && hi) {
+    e = cudaMemcpyAsync(out_idx, sidx, ibytes, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) rc = cuda_error(e, "D2H out_idx");
+  }
+  if (rc == PARIS_OK && hd) {
+    e = cudaMemcpyAsync(out_dist, sdist, dbytes, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) rc = cuda_error(e, "D2H out_dist");
+  }
+  if (rc == PARIS_OK && stats) {  // measurement path: read the counters (synchronizes)
+    std::vector<unsigned> h_count(nq), h_ref(nq), h_blk(nq), h_ext(nq);
+    std::vector<float> h_tau(nq);
     e = cudaMemcpyAsync(h_count.data(), all_count, (size_t)nq * 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h_ref.data(), all_refined, (size_t)nq * 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h_tau.data(), all_tau, (size_t)nq * 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h_blk.data(), all_blocks, (size_t)nq * 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h_ext.data(), all_extra, (size_t)nq * 4, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) rc = cuda_error(e, "paris_knn_exact execution");
-  }
-  if (rc == PARIS_OK) {
-    for (int q = 0; q < nq && rc == PARIS_OK; ++q) {
-      if ((int64_t)h_count[q] <= p.cap) continue;
-      // re-scan this query alone, seeded with its first-pass result (refined over the
-      // `cap` candidates kept) -- its candidates are a subset of the first pass's
-      Plan p1 = p;
-      p1.B = 1;
-      plan_refine(p1);
-      p1.cap = std::min<int64_t>(n, (int64_t)h_count[q]);
-      Ws ws1;
-      rc = alloc_ws(p1, p1.cap, ws1, st);
-      if (rc) break;
-      rc = run_batch(p1, raw, sax, d_q + (size_t)q * len, 1, q, p1.cap, tab, ws1, d_idx, d_dist,
-                     all_count, all_refined, all_tau, all_blocks, all_extra, st, /*rescan=*/true);
-      cudaFreeAsync(ws1.base, st);
-    }
-  }
-  if (rc == PARIS_OK && (hi || hd || stats)) {
-    e = cudaSuccess;
-    if (hi) e = cudaMemcpyAsync(out_idx, sidx, ibytes, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess && hd) e = cudaMemcpyAsync(out_dist, sdist, dbytes, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess && stats) {
-      e = cudaMemcpyAsync(h_count.data(), all_count, (size_t)nq * 4, cudaMemcpyDeviceToHost, st);
-      if (e == cudaSuccess) e = cudaMemcpyAsync(h_ref.data(), all_refined, (size_t)nq * 4, cudaMemcpyDeviceToHost, st);
-      if (e == cudaSuccess) e = cudaMemcpyAsync(h_tau.data(), all_tau, (size_t)nq * 4, cudaMemcpyDeviceToHost, st);
-      if (e == cudaSuccess) e = cudaMemcpyAsync(h_blk.data(), all_blocks, (size_t)nq * 4, cudaMemcpyDeviceToHost, st);
-      if (e == cudaSuccess) e = cudaMemcpyAsync(h_ext.data(), all_extra, (size_t)nq * 4, cudaMemcpyDeviceToHost, st);
-    }
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) rc = cuda_error(e, "paris_knn_exact D2H");
-    if (rc == PARIS_OK && stats) {
+    if (e != cudaSuccess) rc = cuda_error(e, "paris_knn_exact stats D2H");
+    if (rc == PARIS_OK) {
       for (int q = 0; q < nq; ++q) {
         if (stats->candidates) stats->candidates[q] = h_count[q];
         if (stats->refined) stats->refined[q] = h_ref[q];
@@ -3491,8 +3753,7 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
       }
     }
   }
-  cudaFreeAsync(ws.base, st);
-  cudaFreeAsync(stage, st);
+  ws_release(wsh, st);
   return rc;
 }
 

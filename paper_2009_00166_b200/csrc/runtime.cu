@@ -9,7 +9,10 @@
 #include <string.h>
 
 #include <atomic>
+#include <map>
 #include <mutex>
+#include <set>
+#include <utility>
 #include <vector>
 
 namespace paris {
@@ -190,17 +193,145 @@ uint16_t half_bits_dir(double v, int dir) {
   return (uint16_t)(sign | bits);
 }
 
+static int retain_pool_key;
 void retain_pool() {
-  static int done[64] = {0};
+  once_per_device(&retain_pool_key, [](int dev) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    return cudaSuccess;
+  });
+}
+
+// ------------------------------------------------------------------ per-device caches
+static std::mutex g_once_mu;
+static std::set<std::pair<const void*, int>> g_once_done;
+static std::map<std::pair<const void*, int>, int> g_cached_int;
+
+cudaError_t once_per_device(const void* key, const std::function<cudaError_t(int)>& f) {
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t thr = ~0ull;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(g_once_mu);
+  if (g_once_done.count({key, dev})) return cudaSuccess;
+  e = f(dev);
+  if (e == cudaSuccess) g_once_done.insert({key, dev});
+  return e;
+}
+
+int cached_per_device(const void* key, const std::function<int(int)>& f) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_once_mu);
+  auto it = g_cached_int.find({key, dev});
+  if (it != g_cached_int.end()) return it->second;
+  const int v = f(dev);
+  g_cached_int[{key, dev}] = v;
+  return v;
+}
+
+static int sms_key;
+int device_sms() {
+  return cached_per_device(&sms_key, [](int dev) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  });
+}
+
+// ------------------------------------------------------------------ workspace cache
+struct WsEntry {
+  int dev = 0;
+  void* base = nullptr;
+  size_t bytes = 0;
+  cudaEvent_t done = nullptr;  // recorded when the last user released it
+  bool busy = false;
+  uint64_t gen = 0;
+};
+static std::mutex g_ws_mu;
+static std::vector<WsEntry*> g_ws;
+static std::atomic<uint64_t> g_ws_gen{1};
+
+void* ws_acquire(size_t bytes, cudaStream_t st, void** handle, uint64_t* gen) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  WsEntry* e = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    for (WsEntry* w : g_ws) {
+      if (w->dev != dev || w->busy) continue;
+      // prefer the smallest entry that is large enough, else the largest one (grown below)
+      if (!e) e = w;
+      else if (w->bytes >= bytes) { if (e->bytes < bytes || w->bytes < e->bytes) e = w; }
+      else if (e->bytes < bytes && w->bytes > e->bytes) e = w;
+    }
+    if (!e) {
+      e = new WsEntry;
+      e->dev = dev;
+      g_ws.push_back(e);
+    }
+    e->busy = true;
   }
+  cudaError_t err = cudaSuccess;
+  if (!e->done) err = cudaEventCreateWithFlags(&e->done, cudaEventDisableTiming);
+  else err = cudaStreamWaitEvent(st, e->done, 0);  // after the previous user's work
+  if (err == cudaSuccess && e->bytes < bytes) {
+    if (e->base) cudaFreeAsync(e->base, st);
+    e->base = nullptr;
+    e->bytes = 0;
+    size_t want = bytes + bytes / 8;  // headroom: fewer regrowths across calls
+    err = cudaMallocAsync(&e->base, want, st);
+    if (err != cudaSuccess) {
+      cudaGetLastError();
+      want = bytes;
+      err = cudaMallocAsync(&e->base, want, st);
+    }
+    if (err == cudaSuccess) {
+      e->bytes = want;
+      e->gen = g_ws_gen.fetch_add(1);
+    } else {
+      e->base = nullptr;
+    }
+  }
+  if (err != cudaSuccess) {
+    cudaGetLastError();
+    set_error("workspace allocation of %zu bytes failed (%s)", bytes, cudaGetErrorString(err));
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    e->busy = false;
+    return nullptr;
+  }
+  *handle = e;
+  if (gen) *gen = e->gen;
+  return e->base;
+}
+
+void ws_release(void* handle, cudaStream_t st) {
+  WsEntry* e = static_cast<WsEntry*>(handle);
+  if (!e) return;
+  cudaEventRecord(e->done, st);
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  e->busy = false;
+}
+
+void ws_free_all() {
+  cudaDeviceSynchronize();
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  std::vector<WsEntry*> keep;
+  for (WsEntry* w : g_ws) {
+    if (w->busy) { keep.push_back(w); continue; }
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(w->dev);
+    if (w->base) cudaFree(w->base);
+    if (w->done) cudaEventDestroy(w->done);
+    cudaSetDevice(cur);
+    delete w;
+  }
+  g_ws = keep;
   cudaGetLastError();
-  done[dev] = 1;
 }
 
 static std::mutex g_tab_mu;
@@ -296,11 +427,16 @@ extern "C" {
 
 int paris_debug_read_probe(const void* p, int64_t bytes, void* stream) {
   if (!p || bytes < 16 || (reinterpret_cast<uintptr_t>(p) & 15)) return PARIS_EINVAL;
-  int dev = 0, sms = 148;
+  const int sms = paris::device_sms();
+  static int sink_key;
+  static unsigned* sinks[64] = {nullptr};  // per device, allocated once
+  const cudaError_t ea = paris::once_per_device(&sink_key, [](int dev) {
+    return dev < 64 ? cudaMalloc(&sinks[dev], 4) : cudaErrorInvalidDevice;
+  });
+  if (ea != cudaSuccess) return paris::cuda_error(ea, "read probe sink");
+  int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  static unsigned* sink = nullptr;
-  if (!sink && cudaMalloc(&sink, 4) != cudaSuccess) return PARIS_ENOMEM;
+  unsigned* sink = sinks[dev];
   PARIS_CHECK_LAUNCH(PARIS_LAUNCH("read_probe", paris::k_read_probe, sms * 4, 512, 0, (cudaStream_t)stream,
                                   reinterpret_cast<const uint4*>(p), bytes / 16, sink),
                      "read probe launch");
@@ -310,7 +446,9 @@ int paris_debug_read_probe(const void* p, int64_t bytes, void* stream) {
 
 const char* paris_last_error(void) { return paris::g_err.c_str(); }
 
-int32_t paris_version(void) { return 104; }
+int32_t paris_version(void) { return 105; }
+
+void paris_release_workspace(void) { paris::ws_free_all(); }
 
 void paris_profile_enable(int32_t on) { paris::g_profile_on.store(on ? 1 : 0); }
 

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <functional>
 #include <string>
 
 #include "../../include/paris.h"
@@ -73,6 +74,28 @@ uint16_t half_bits_dir(double v, int dir);
 // Keep freed stream-ordered scratch mapped in the current device's default
 // memory pool (release threshold = max) so repeated calls do not remap it.
 void retain_pool();
+
+// SM count of the current device (cached per device; thread-safe).
+int device_sms();
+
+// Per-(key, device) one-time setup -- e.g. cudaFuncSetAttribute of a kernel -- run under
+// a lock, so a concurrent first caller waits until it is done; cached only on success.
+cudaError_t once_per_device(const void* key, const std::function<cudaError_t(int dev)>& f);
+
+// Per-(key, device) integer (an occupancy or a shared-memory size), computed once
+// under a lock by f (thread-safe).
+int cached_per_device(const void* key, const std::function<int(int dev)>& f);
+
+// Cached device scratch (the boundary's workspace): `bytes` of device memory usable by
+// work on stream st.  A grow-only entry per device is reused across calls; every reuse
+// is ordered after the previous user's work on the device (an event recorded at
+// release), so a call never allocates or synchronizes in the steady state.  Distinct
+// host threads get distinct entries.  *gen changes whenever the entry's memory is
+// reallocated.  nullptr (+ error set) on failure.
+void* ws_acquire(size_t bytes, cudaStream_t st, void** handle, uint64_t* gen);
+void ws_release(void* handle, cudaStream_t st);
+// Free every idle cached entry (synchronizes the device).
+void ws_free_all();
 
 // ---- errors
 void set_error(const char* fmt, ...);

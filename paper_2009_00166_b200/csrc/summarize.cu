@@ -502,16 +502,7 @@ k_summarize_generic(const float* __restrict__ raw, int64_t n, int len, int w, in
   }
 }
 
-int sm_count() {
-  static int cached = 0;
-  if (!cached) {
-    int dev = 0, v = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    cached = v > 0 ? v : 148;
-  }
-  return cached;
-}
+int sm_count() { return device_sms(); }
 
 }  // namespace
 
@@ -528,25 +519,17 @@ static int summarize_device(const float* raw, int64_t n, int len, int w, int car
     const int64_t tiles = (n + (kSumTileBytes / (4 * len)) - 1) / (kSumTileBytes / (4 * len));
     const int grid = (int)imin64(tiles, (int64_t)sms);
     cudaError_t e;
-    static int attr_dev[3] = {-1, -1, -1};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const int ai = len == 128 ? 0 : len == 256 ? 1 : 2;
-    if (attr_dev[ai] != dev) {
-      e = (len == 128) ? cudaFuncSetAttribute(k_summarize_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSumSmem)
-        : (len == 256) ? cudaFuncSetAttribute(k_summarize_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSumSmem)
-                       : cudaFuncSetAttribute(k_summarize_tma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSumSmem);
-      PARIS_CHECK_LAUNCH(e, "summarize smem attribute");
-      attr_dev[ai] = dev;
-    }
+    static int attr_key;
+    e = once_per_device(&attr_key, [](int) {  // every variant's shared-memory limit, once per device
+      cudaError_t r = cudaFuncSetAttribute(k_summarize_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSumSmem);
+      if (r == cudaSuccess) r = cudaFuncSetAttribute(k_summarize_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSumSmem);
+      if (r == cudaSuccess) r = cudaFuncSetAttribute(k_summarize_tma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSumSmem);
+      if (r == cudaSuccess) r = cudaFuncSetAttribute(k_summarize_seg<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSumSmem);
+      if (r == cudaSuccess) r = cudaFuncSetAttribute(k_summarize_seg<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSumSmem);
+      return r;
+    });
+    PARIS_CHECK_LAUNCH(e, "summarize smem attribute");
     if (w == 16 && len <= 256 && !getenv("PARIS_SUMMARIZE_SHFL")) {  // segment per lane (env: A/B of the shuffle form)
-      static int seg_dev[3] = {-1, -1, -1};
-      if (seg_dev[ai] != dev) {
-        e = (len == 128) ? cudaFuncSetAttribute(k_summarize_seg<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSumSmem)
-                         : cudaFuncSetAttribute(k_summarize_seg<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSumSmem);
-        PARIS_CHECK_LAUNCH(e, "summarize smem attribute");
-        seg_dev[ai] = dev;
-      }
       switch (len) {
         case 128: e = PARIS_LAUNCH("summarize", k_summarize_seg<2>, grid, kSumThreads, kSumSmem, st, raw, n, card, out_sax, ld, tab); break;
         default: e = PARIS_LAUNCH("summarize", k_summarize_seg<4>, grid, kSumThreads, kSumSmem, st, raw, n, card, out_sax, ld, tab); break;

@@ -73,7 +73,7 @@ def test_c4_bench_call_parity(P):
     gi, gd, st = P.knn_index(raw, idx, q, k=1, raw16=raw16, stats=True)    # one call: 64 + 36
     assert st["raw16_rows"].sum() > 0, "the bf16 pre-filter did not run"
     del raw16, idx
-    gi_f, gd_f = P.knn_exact(raw, sax, q[:8], k=1)
+    gi_f, gd_f = P.knn_exact(raw, sax, q[:32], k=1)     # flat path: two 16-query passes
     del sax
     torch.cuda.empty_cache()
     x = raw.cpu().numpy()

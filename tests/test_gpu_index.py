@@ -188,3 +188,31 @@ def test_raw_bf16_definition(P):
     r = P.raw_bf16(x)
     ref = x.to(torch.bfloat16).view(torch.int16)
     assert torch.equal(r, ref)
+
+
+@pytest.mark.parametrize("k", [1, 7, 1000])
+def test_knn_overflow_fallback_mixed(P, k):
+    """Device-side overflow handling: in one call, some queries flood their candidate
+    buffers (all-zero queries with a one-series seed: nearly every LB is tiny) while the
+    others do not; the flooded ones are completed by the gated fused scan (k_fallback),
+    the rest must be untouched by it.  Both paths, two passes of the index path, and
+    k > 1 rows whose first pass kept fewer than k results.  Checked against brute force."""
+    import torch
+    n, length, nq = 70_000 - 16 * 3, 128, 70
+    x = datagen.random_walks(n, length, 4242)
+    q = datagen.random_walks(nq, length, 4243)
+    flood = [0, 5, 63, 64, 69]
+    q[flood] = 0.0
+    q[10] = x[77]
+    xd = torch.from_numpy(x).cuda()
+    qd = torch.from_numpy(q).cuda()
+    sax = P.summarize(xd, 16, 256)
+    idx = P.index_build(sax, 16, 256)
+    cfg = P.KnnConfig(index_seeds=1, seed_div=n)
+    gi, gd, st = P.knn_index(xd, idx, qd, k=k, config=cfg, stats=True)
+    fi, fd = P.knn_exact(xd, sax, qd, k=k, config=cfg)
+    ri, rd2 = oracle.knn_bruteforce(x, q, k)
+    check_knn(x, q, gi.cpu().numpy(), gd.cpu().numpy(), ri, rd2)
+    check_knn(x, q, fi.cpu().numpy(), fd.cpu().numpy(), ri, rd2)
+    cap = max(65536, n // (16 if k > 1 else 32))
+    assert (st["candidates"].numpy()[flood] > cap).all(), "the flooded queries did not overflow"
