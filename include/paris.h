@@ -138,7 +138,17 @@ typedef struct paris_knn_config {
                            [2] index mode: seed series around the leaf (0 = max(1024 (2048 from 5e7 series), 32k) up to 4096; 64 when
                            raw is host memory);
                            [3] = 1 seeds every batch from the rows already in out_idx/out_dist
-                           (device outputs; experiments with an ideal BSF) */
+                           (device outputs; experiments with an ideal BSF);
+                           [4] > 0: candidate-buffer capacity per query (test hook: forces the
+                           overflow fallback; default max(65536, n/32 | n/16 for k > 1) grown
+                           to a 2 GB budget per candidate array) */
+  const float* tau_in;  /* optional DEVICE [nq]: per query, an upper bound of its k-th NN
+                           distance from outside the call (+inf = none) -- e.g. the minimum
+                           over the shards of a sharded collection of their approximate
+                           answers' k-th distances (paris_knn_approx); the
+                           search then prunes against min(its own seed, tau_in) and rows
+                           with no series within the bound come back as id -1 / +inf.
+                           NULL = none. */
 } paris_knn_config;
 
 /* Per-query counters (host memory, arrays of nq), filled by paris_knn_exact_ex. */
@@ -179,6 +189,24 @@ int paris_knn_index_ex(const float* raw, const uint8_t* sax_sorted, const uint32
                        int64_t n, const float* queries, int32_t nq, int32_t k, int64_t* out_idx,
                        float* out_dist, int32_t len, int32_t w, int32_t card, void* stream,
                        const paris_knn_config* config, paris_knn_stats* stats);
+
+/*
+ * paris_knn_approx / paris_knn_index_approx -- approximate k-NN (ParIS+ approximate
+ * search): only step 1 of paris_knn_exact / paris_knn_index -- for every
+ * query the k best of the seed series (flat: the LB-best series of a prefix sample;
+ * index: the series around the leaf the query's word would be inserted into), with
+ * their true fp32 distances, ascending (distance, id); -1 / +inf pads a row when fewer
+ * than k seeds exist.  The k-th distance bounds the exact k-th NN distance from above,
+ * which is what a sharded search exchanges (paris_knn_config.tau_in).  Same arguments,
+ * conventions and asynchrony as the exact calls (config: batch / seed_div /
+ * reserved[2] apply).
+ */
+int paris_knn_approx(const float* raw, const uint8_t* sax, int64_t n, const float* queries, int32_t nq, int32_t k,
+                     int64_t* out_idx, float* out_dist, int32_t len, int32_t w, int32_t card, void* stream,
+                     const paris_knn_config* config);
+int paris_knn_index_approx(const float* raw, const uint8_t* sax_sorted, const uint32_t* perm, const uint8_t* env,
+                           int64_t n, const float* queries, int32_t nq, int32_t k, int64_t* out_idx, float* out_dist,
+                           int32_t len, int32_t w, int32_t card, void* stream, const paris_knn_config* config);
 
 /*
  * paris_raw_bf16 -- a bf16 copy of the raw collection for the refinement pre-filter
@@ -239,7 +267,8 @@ void paris_release_workspace(void);
 const char* paris_last_error(void);
 
 /* ABI version (major*100 + minor). */
-int32_t paris_version(void);  /* 105: asynchronous k-NN calls, device-side overflow, paris_release_workspace */
+int32_t paris_version(void);  /* 106: asynchronous k-NN calls, device-side overflow, paris_release_workspace,
+                                 paris_knn_approx / paris_knn_index_approx, paris_knn_config.tau_in */
 
 /* Test hook: the library's own fp64 breakpoints cut_1..cut_{card-1} (R2) into
  * out[0..card-2] (host memory).  PARIS_ECONFIG for a bad card. */
@@ -249,6 +278,11 @@ int paris_debug_cuts(int32_t card, double* out);
  * loads (no writes) -- the read-only HBM peak beside MEASURED_PEAKS.json's copy
  * peak (bench.py times it).  Asynchronous on `stream`. */
 int paris_debug_read_probe(const void* p, int64_t bytes, void* stream);
+
+/* Measurement hook: the fp16x2 FMA-pipe peak -- device_sms * blocks_per_sm CTAs of 512
+ * threads, each thread `iters` x 8 independent fma.rn.f16x2 (2 fp16 FMAs each); bench.py
+ * times it for the batched LB's "alu" roofline denominator.  Asynchronous on `stream`. */
+int paris_debug_hfma2_probe(int32_t iters, int32_t blocks_per_sm, void* stream);
 
 /* Test hook: IEEE binary16 bits of v rounded toward -inf (dir < 0) or +inf
  * (dir > 0) -- the directed rounding behind the batched fp16 lower bound. */

@@ -32,7 +32,7 @@ class ParisError(RuntimeError):
 
 class _Config(ctypes.Structure):
     _fields_ = [("batch", ctypes.c_int32), ("seed_div", ctypes.c_int32),
-                ("wave_a", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
+                ("wave_a", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5), ("tau_in", ctypes.c_void_p)]
 
 
 class _Stats(ctypes.Structure):
@@ -55,6 +55,8 @@ class KnnConfig:
     sorted_refine: bool = False  # k = 1: refine the bucket-sorted lists (K5 scatter) instead of the unsorted waves
     index_seeds: int = 0        # index mode: seed series around the query's leaf (0 = 1024)
     seed_from_out: bool = False  # test hook: seed from the rows already in out_idx/out_dist (device)
+    tau_in: "torch.Tensor | None" = None  # [nq] float32 CUDA: external bound of each query's k-th NN distance
+    cap: int = 0                # test hook: candidate-buffer capacity per query (forces the overflow fallback)
 
 
 def library_path() -> str:
@@ -91,6 +93,11 @@ def load():
         lib.paris_raw_bf16.restype = ctypes.c_int
         lib.paris_knn_index.argtypes = [P, P, P, P, i64, P, i32, i32, P, P, i32, i32, i32, P]
         lib.paris_knn_index.restype = ctypes.c_int
+        lib.paris_knn_approx.argtypes = [P, P, i64, P, i32, i32, P, P, i32, i32, i32, P, ctypes.POINTER(_Config)]
+        lib.paris_knn_approx.restype = ctypes.c_int
+        lib.paris_knn_index_approx.argtypes = [P, P, P, P, i64, P, i32, i32, P, P, i32, i32, i32, P,
+                                               ctypes.POINTER(_Config)]
+        lib.paris_knn_index_approx.restype = ctypes.c_int
         lib.paris_knn_nb.argtypes = [P, P, i64, P, i32, P, P, i32, i32, i32, P, ctypes.POINTER(_Config),
                                      ctypes.POINTER(_Stats)]
         lib.paris_knn_nb.restype = ctypes.c_int
@@ -107,6 +114,8 @@ def load():
         lib.paris_debug_cuts.restype = ctypes.c_int
         lib.paris_debug_read_probe.argtypes = [P, i64, P]
         lib.paris_debug_read_probe.restype = ctypes.c_int
+        lib.paris_debug_hfma2_probe.argtypes = [i32, i32, P]
+        lib.paris_debug_hfma2_probe.restype = ctypes.c_int
         lib.paris_debug_half_dir.argtypes = [ctypes.c_double, i32]
         lib.paris_debug_half_dir.restype = ctypes.c_uint16
         _lib = lib
@@ -232,6 +241,52 @@ def knn_nb(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, w: int =
                      config=config, stats=stats, _nb=True)
 
 
+def _make_config(config, nq: int):
+    if config is None:
+        return None
+    cfg = _Config(config.batch, config.seed_div, config.wave_a)
+    cfg.reserved[0] = 1 if config.force_direct else 0
+    cfg.reserved[1] = 1 if config.sorted_refine else 0
+    cfg.reserved[2] = int(config.index_seeds)
+    cfg.reserved[3] = 1 if config.seed_from_out else 0
+    cfg.reserved[4] = int(config.cap)
+    if config.tau_in is not None:
+        t = config.tau_in
+        if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous() and t.numel() == nq):
+            raise ValueError("tau_in must be a contiguous float32 CUDA tensor of nq entries")
+        cfg.tau_in = t.data_ptr()
+    return cfg
+
+
+def knn_approx(raw: torch.Tensor, sax, queries: torch.Tensor, k: int = 1, w: int = 16, card: int = 256,
+               index: Index | None = None, config: KnnConfig | None = None, stream=None):
+    """Approximate k-NN (paris_knn_approx / paris_knn_index_approx): the k best
+    seed series per query with their true distances; `sax` is the flat SAX array, or pass
+    `index` (then sax may be None).  Returns (idx int64 [nq][k], dist float32 [nq][k]) on
+    the device of `queries` (CUDA)."""
+    lib = load()
+    if queries.dim() == 1:
+        queries = queries.unsqueeze(0)
+    queries = queries.contiguous()
+    n, length = raw.shape
+    nq = queries.shape[0]
+    out_idx = torch.empty((nq, k), dtype=torch.int64, device=queries.device)
+    out_dist = torch.empty((nq, k), dtype=torch.float32, device=queries.device)
+    cfg = _make_config(config, nq)
+    if index is not None:
+        rc = lib.paris_knn_index_approx(raw.data_ptr(), index.sax_sorted.data_ptr(), index.perm.data_ptr(),
+                                        index.env.data_ptr(), n, queries.data_ptr(), nq, k, out_idx.data_ptr(),
+                                        out_dist.data_ptr(), length, index.w, index.card, _stream(stream),
+                                        ctypes.byref(cfg) if cfg else None)
+    else:
+        _need_cuda(sax, "sax")
+        rc = lib.paris_knn_approx(raw.data_ptr(), sax.data_ptr(), n, queries.data_ptr(), nq, k, out_idx.data_ptr(),
+                                  out_dist.data_ptr(), length, w, card, _stream(stream),
+                                  ctypes.byref(cfg) if cfg else None)
+    _check(rc)
+    return out_idx, out_dist
+
+
 def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: int = 1,
               w: int = 16, card: int = 256, out_idx: torch.Tensor | None = None,
               out_dist: torch.Tensor | None = None, stream=None,
@@ -271,13 +326,7 @@ def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: in
         out_idx = torch.empty((nq, k), dtype=torch.int64, device=dev, pin_memory=pin)
     if out_dist is None:
         out_dist = torch.empty((nq, k), dtype=torch.float32, device=dev, pin_memory=pin)
-    cfg = None
-    if config is not None:
-        cfg = _Config(config.batch, config.seed_div, config.wave_a)
-        cfg.reserved[0] = 1 if config.force_direct else 0
-        cfg.reserved[1] = 1 if config.sorted_refine else 0
-        cfg.reserved[2] = int(config.index_seeds)
-        cfg.reserved[3] = 1 if config.seed_from_out else 0
+    cfg = _make_config(config, nq)
     st = None
     arrays = None
     if stats:
@@ -372,6 +421,14 @@ def debug_read_probe(t: torch.Tensor, stream=None):
     """Stream the bytes of a CUDA tensor with read-only loads (the read-only HBM peak probe)."""
     _need_cuda(t, "t")
     _check(load().paris_debug_read_probe(t.data_ptr(), t.numel() * t.element_size() // 16 * 16, _stream(stream)))
+
+
+def debug_hfma2_probe(iters: int, blocks_per_sm: int = 4, stream=None) -> float:
+    """Launch the fp16x2 FMA probe; returns the fp16 FMAs it performs (time it with events)."""
+    _check(load().paris_debug_hfma2_probe(int(iters), int(blocks_per_sm), _stream(stream)))
+    import torch as _t
+    sms = _t.cuda.get_device_properties(_t.cuda.current_device()).multi_processor_count
+    return float(sms) * blocks_per_sm * 512 * iters * 8 * 2
 
 
 def debug_half_dir(v: float, direction: int) -> int:

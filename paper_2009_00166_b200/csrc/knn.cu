@@ -489,6 +489,42 @@ __global__ void k_seed_prev(const int64_t* __restrict__ prev_idx, const float* _
   if (k == 1) best[b * kPadU64] = ok ? make_key(__fmul_ru(__fmul_ru(d, d), 1.00000096f), (uint32_t)id) : kNoKey;
 }
 
+// An external bound (paris_knn_config.tau_in, rooted distances): per query the pruning
+// threshold becomes min(own seed, tau_in^2 rounded up); for k = 1 the BSF key starts no
+// higher than (tau_in^2, sentinel id 0xFFFFFFFF) -- a bound, not a series: a row whose
+// BSF is still the sentinel at the end has no series within the bound (-1 / +inf).
+constexpr uint32_t kSentinelId = 0xFFFFFFFFu;
+__global__ void k_tau_in(const float* __restrict__ tau_in, int nb, int q0, int k, float d2up,
+                         unsigned* __restrict__ thr, unsigned* __restrict__ thr_seed,
+                         unsigned long long* __restrict__ best) {
+  const int b = threadIdx.x;
+  if (b >= nb) return;
+  const float d = tau_in[q0 + b];
+  if (!(d < INFINITY)) return;
+  const float d2 = __fmul_ru(__fmul_ru(fmaxf(d, 0.f), fmaxf(d, 0.f)), 1.00000096f);
+  const float t = __fmul_ru(d2, d2up);
+  thr[b * kPadU32] = min(thr[b * kPadU32], __float_as_uint(t));  // non-negative floats: bits order
+  thr_seed[b] = min(thr_seed[b], __float_as_uint(t));
+  if (k == 1) best[b * kPadU64] = min((uint64_t)best[b * kPadU64], make_key(d2, kSentinelId));
+}
+
+// Approximate k-NN (paris_knn_approx): the k best seed keys of each query, ascending.
+__global__ void __launch_bounds__(1024)
+k_seed_topk(const uint64_t* __restrict__ seed_keys, int S, int k, int q0, int64_t* __restrict__ out_idx,
+            float* __restrict__ out_dist) {
+  __shared__ uint64_t buf[kSortP];
+  const int b = blockIdx.x;
+  for (int i = threadIdx.x; i < kSortP; i += blockDim.x) buf[i] = (i < S) ? seed_keys[b * S + i] : kNoKey;
+  __syncthreads();
+  bitonic_sort(buf, kSortP);
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    const uint64_t key = buf[i];
+    const size_t o = (size_t)(q0 + b) * k + i;
+    if (key == kNoKey) { out_idx[o] = -1; out_dist[o] = INFINITY; }
+    else { out_idx[o] = (int64_t)key_id(key); out_dist[o] = sqrtf(key_val(key)); }
+  }
+}
+
 // Index mode seed = approximate search: the leaf the query's own
 // iSAX word would be inserted into.  One warp per query: the word (symbols of the
 // query PAA midpoints; any word is sound, this one is the closest leaf), its key,
@@ -2749,7 +2785,7 @@ __global__ void k_finalize1(const unsigned long long* __restrict__ best, int nb,
   const int b = threadIdx.x;
   if (b >= nb) return;
   const uint64_t key = best[b * kPadU64];
-  if (key == kNoKey) { out_idx[q0 + b] = -1; out_dist[q0 + b] = INFINITY; }
+  if (key == kNoKey || key_id(key) == kSentinelId) { out_idx[q0 + b] = -1; out_dist[q0 + b] = INFINITY; }
   else { out_idx[q0 + b] = (int64_t)key_id(key); out_dist[q0 + b] = sqrtf(key_val(key)); }
   all_count[q0 + b] = (accum ? all_count[q0 + b] : 0u) + count[b];
   all_refined[q0 + b] = (accum ? all_refined[q0 + b] : 0u) + refined[b];
@@ -2828,7 +2864,46 @@ struct FbArgs {
 };
 constexpr int kFbThreads = 128;
 
-template <bool K1>
+// Up to 4 rows refined together (4 rows in flight per lane step), early abandoning at
+// thr after each 128-point chunk; d2[u] = +inf when abandoned or not live.
+__device__ __forceinline__ void fb_refine4(const float* __restrict__ raw, int len, const float4* __restrict__ qv,
+                                           const uint32_t (&id)[4], bool (&live)[4], float thr, float (&d2)[4]) {
+  const int lane = threadIdx.x & 31;
+  const int nf = len >> 2;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int c0 = 0; c0 < nf; c0 += 32) {
+    const int f = c0 + lane;
+    float4 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      x[u] = (live[u] && f < nf) ? ld_stream(reinterpret_cast<const float4*>(raw + (size_t)id[u] * len) + f)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 q = f < nf ? __ldg(qv + f) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      float d;
+      d = x[u].x - q.x; acc[u] = fmaf(d, d, acc[u]);
+      d = x[u].y - q.y; acc[u] = fmaf(d, d, acc[u]);
+      d = x[u].z - q.z; acc[u] = fmaf(d, d, acc[u]);
+      d = x[u].w - q.w; acc[u] = fmaf(d, d, acc[u]);
+    }
+    if (c0 + 32 < nf) {
+      bool any = false;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (live[u] && warp_sum(acc[u]) > thr) live[u] = false;  // early abandoning
+        any |= live[u];
+      }
+      if (!any) break;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) d2[u] = live[u] ? warp_sum(acc[u]) : INFINITY;
+}
+
+// FAST (w == 16, n % 4 == 0): a lane bounds 4 consecutive series per step from one 32-bit
+// word per segment row (16 independent loads in flight); else one series per lane.
+template <bool K1, bool FAST>
 __global__ void __launch_bounds__(kFbThreads)
 k_fallback(FbArgs a) {
   extern __shared__ uint64_t s_top[];  // k > 1: [warps][k] ascending keys
@@ -2844,11 +2919,11 @@ k_fallback(FbArgs a) {
   __syncthreads();
   if (!s_any) return;  // the common case: one shared load, then exit
   for (int i = tid; i < kMaxCard; i += blockDim.x) s_lu[i] = a.tab->lu[i];
+  constexpr int SPL = FAST ? 4 : 1;  // series per lane per step
   const int nw = blockDim.x >> 5;
   const int gw = blockIdx.x * nw + warp;
-  const int64_t per = ((a.n + (int64_t)a.L - 1) / a.L + 31) / 32 * 32;
+  const int64_t per = ((a.n + (int64_t)a.L - 1) / a.L + 32 * SPL - 1) / (32 * SPL) * (32 * SPL);
   const int64_t lo = imin64(a.n, (int64_t)gw * per), hi = imin64(a.n, lo + per);
-  const int nf = a.len >> 2;
   uint64_t* top = s_top + (size_t)warp * (K1 ? 1 : a.k);
   for (int b = 0; b < a.nb; ++b) {
     if ((int64_t)a.count[b] <= a.cap) continue;
@@ -2863,82 +2938,105 @@ k_fallback(FbArgs a) {
       for (int i = lane; i < a.k; i += 32) top[i] = kNoKey;
     __syncwarp();
     unsigned nref = 0;
-    for (int64_t base = lo; base < hi; base += 32) {
-      const int64_t i = base + lane;
-      float thr;
+    auto cur_thr = [&]() -> float {
       if (K1) {
         cur = min(cur, ld_relaxed_u64(bp));
-        thr = cur == kNoKey ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
-      } else {
-        thr = __uint_as_float(ld_relaxed_u32(&a.thr[b * kPadU32]));
-        if (filled == a.k) thr = fminf(thr, __fmul_ru(key_val(top[a.k - 1]), a.d2up));
+        return cur == kNoKey ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
       }
-      float lb = INFINITY;
-      uint32_t id = 0;
-      if (i < hi) {
-        lb = 0.f;
-        for (int s = 0; s < a.w; ++s) {
-          const uint8_t sym = a.perm ? a.sax[(size_t)(i / kTS) * kTW * kTS + (size_t)s * kTS + i % kTS]
-                                     : a.sax[(size_t)s * a.n + i];
-          const float2 r = s_lu[sym];   // {L rounded down, U rounded up}
-          const float2 q = s_q[s];      // {q rounded down, q rounded up}
-          const float d = fmaxf(fmaxf(__fsub_rd(q.x, r.y), __fsub_rd(r.x, q.y)), 0.f);
-          lb = __fadd_rd(lb, __fmul_rd(d, d));
+      float t = __uint_as_float(ld_relaxed_u32(&a.thr[b * kPadU32]));
+      if (filled == a.k) t = fminf(t, __fmul_ru(key_val(top[a.k - 1]), a.d2up));
+      return t;
+    };
+    for (int64_t base = lo; base < hi; base += 32 * SPL) {
+      const int64_t i0 = base + (int64_t)SPL * lane;
+      float lb[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+      uint32_t id[4] = {0u, 0u, 0u, 0u};
+      if (FAST) {
+        if (i0 < hi) {  // hi % 4 == 0 (n % 4 == 0, per % 4 == 0)
+          uint32_t wd[kTW];
+#pragma unroll
+          for (int s2 = 0; s2 < kTW; ++s2)
+            wd[s2] = a.perm ? __ldg(reinterpret_cast<const uint32_t*>(
+                                  a.sax + (size_t)(i0 / kTS) * kTW * kTS + (size_t)s2 * kTS + i0 % kTS))
+                            : __ldg(reinterpret_cast<const uint32_t*>(a.sax + (size_t)s2 * a.n + i0));
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            float acc = 0.f;
+#pragma unroll
+            for (int s2 = 0; s2 < kTW; ++s2) {
+              const float2 r = s_lu[(wd[s2] >> (8 * j)) & 0xFFu];  // {L rounded down, U rounded up}
+              const float2 q = s_q[s2];                            // {q rounded down, q rounded up}
+              const float d = fmaxf(fmaxf(__fsub_rd(q.x, r.y), __fsub_rd(r.x, q.y)), 0.f);
+              acc = __fadd_rd(acc, __fmul_rd(d, d));
+            }
+            lb[j] = __fmul_rd(acc, a.seglen_f);
+            id[j] = a.perm ? __ldg(a.perm + i0 + j) : (uint32_t)(i0 + j);
+          }
         }
-        lb = __fmul_rd(lb, a.seglen_f);
-        id = a.perm ? __ldg(a.perm + i) : (uint32_t)i;
-      }
-      unsigned m = __ballot_sync(0xffffffffu, lb <= thr);
-      while (m) {
-        const int src = __ffs(m) - 1;
-        m &= m - 1;
-        const uint32_t cid = __shfl_sync(0xffffffffu, id, src);
-        if (__shfl_sync(0xffffffffu, lb, src) > thr) continue;
-        const float4* row = reinterpret_cast<const float4*>(a.raw + (size_t)cid * a.len);
+      } else if (i0 < hi) {
         float acc = 0.f;
-        bool abandoned = false;
-        for (int c0 = 0; c0 < nf; c0 += 32) {
-          const int f = c0 + lane;
-          if (f < nf) {
-            const float4 x = ld_stream(row + f), y = __ldg(qv + f);
-            float d;
-            d = x.x - y.x; acc = fmaf(d, d, acc);
-            d = x.y - y.y; acc = fmaf(d, d, acc);
-            d = x.z - y.z; acc = fmaf(d, d, acc);
-            d = x.w - y.w; acc = fmaf(d, d, acc);
-          }
-          if (c0 + 32 < nf && warp_sum(acc) > thr) { abandoned = true; break; }  // early abandoning
+        for (int s2 = 0; s2 < a.w; ++s2) {
+          const uint8_t sym = a.perm ? a.sax[(size_t)(i0 / kTS) * kTW * kTS + (size_t)s2 * kTS + i0 % kTS]
+                                     : a.sax[(size_t)s2 * a.n + i0];
+          const float2 r = s_lu[sym];
+          const float2 q = s_q[s2];
+          const float d = fmaxf(fmaxf(__fsub_rd(q.x, r.y), __fsub_rd(r.x, q.y)), 0.f);
+          acc = __fadd_rd(acc, __fmul_rd(d, d));
         }
-        ++nref;
-        if (abandoned) continue;
-        const float d2 = warp_sum(acc);
-        const uint64_t key = make_key(d2, cid);
-        if (K1) {
-          if (key < cur) {
-            if (lane == 0) atomicMin(bp, (unsigned long long)key);
-            cur = key;
-            thr = __fmul_ru(d2, a.d2up);
+        lb[0] = __fmul_rd(acc, a.seglen_f);
+        id[0] = a.perm ? __ldg(a.perm + i0) : (uint32_t)i0;
+      }
+      float thr = cur_thr();
+#pragma unroll
+      for (int j = 0; j < SPL; ++j) {
+        unsigned m = __ballot_sync(0xffffffffu, lb[j] <= thr);
+        while (m) {
+          uint32_t cid[4];
+          bool live[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int src = m ? __ffs(m) - 1 : 0;
+            live[u] = m != 0u;
+            m &= m - 1;
+            cid[u] = __shfl_sync(0xffffffffu, id[j], src);
+            live[u] = live[u] && __shfl_sync(0xffffffffu, lb[j], src) <= thr;
           }
-        } else if (filled < a.k || key < top[a.k - 1]) {
-          // sorted insert into the warp's list: rank = #entries < key
-          int r = 0;
-          for (int j = lane; j < filled; j += 32) r += top[j] < key;
-          r = __reduce_add_sync(0xffffffffu, r);
-          const int last = min(filled, a.k - 1);  // entries [r, last) move up by one
-          for (int hi2 = last; hi2 > r; hi2 -= 32) {
-            const int j = hi2 - 1 - lane;
-            const uint64_t v = (j >= r) ? top[j] : 0ull;
-            __syncwarp();
-            if (j >= r) top[j + 1] = v;
-            __syncwarp();
-          }
-          if (lane == 0) top[r] = key;
-          __syncwarp();
-          filled = min(filled + 1, a.k);
-          if (filled == a.k) {
-            const float t = __fmul_ru(key_val(top[a.k - 1]), a.d2up);
-            if (lane == 0) atomicMin(&a.thr[b * kPadU32], __float_as_uint(t));
-            thr = fminf(thr, t);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) nref += live[u] ? 1u : 0u;  // raw rows read
+          float d2[4];
+          fb_refine4(a.raw, a.len, qv, cid, live, thr, d2);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (d2[u] == INFINITY) continue;
+            const uint64_t key = make_key(d2[u], cid[u]);
+            if (K1) {
+              if (key < cur) {
+                if (lane == 0) atomicMin(bp, (unsigned long long)key);
+                cur = key;
+                thr = fminf(thr, __fmul_ru(d2[u], a.d2up));
+              }
+            } else if (filled < a.k || key < top[a.k - 1]) {
+              // sorted insert into the warp's list: rank = #entries < key
+              int r = 0;
+              for (int jj = lane; jj < filled; jj += 32) r += top[jj] < key;
+              r = __reduce_add_sync(0xffffffffu, r);
+              const int last = min(filled, a.k - 1);  // entries [r, last) move up by one
+              for (int hi2 = last; hi2 > r; hi2 -= 32) {
+                const int jj = hi2 - 1 - lane;
+                const uint64_t v = (jj >= r) ? top[jj] : 0ull;
+                __syncwarp();
+                if (jj >= r) top[jj + 1] = v;
+                __syncwarp();
+              }
+              if (lane == 0) top[r] = key;
+              __syncwarp();
+              filled = min(filled + 1, a.k);
+              if (filled == a.k) {
+                const float t = __fmul_ru(key_val(top[a.k - 1]), a.d2up);
+                if (lane == 0) atomicMin(&a.thr[b * kPadU32], __float_as_uint(t));
+                thr = fminf(thr, t);
+              }
+            }
           }
         }
       }
@@ -2975,8 +3073,9 @@ k_finalize_ovf(const unsigned long long* __restrict__ best, const uint64_t* __re
   if (k == 1) {
     if (threadIdx.x == 0) {
       const uint64_t key = best[b * kPadU64];
-      out_idx[q0 + b] = key == kNoKey ? -1 : (int64_t)key_id(key);
-      out_dist[q0 + b] = key == kNoKey ? INFINITY : sqrtf(key_val(key));
+      const bool none = key == kNoKey || key_id(key) == kSentinelId;
+      out_idx[q0 + b] = none ? -1 : (int64_t)key_id(key);
+      out_dist[q0 + b] = none ? INFINITY : sqrtf(key_val(key));
     }
   } else {
     merge_lists_topk(lists + (size_t)b * L * k, (int64_t)L * k, k, buf);
@@ -3049,6 +3148,8 @@ struct Plan {
   const uint16_t* raw16 = nullptr;  // optional bf16 copy of raw: refine pre-filter (k = 1)
   bool raw_host = false;            // raw in pinned host memory (f3)
   int fbL = 0;                      // overflow fallback: warps of its grid (= lists per query for k > 1)
+  const float* tau_in = nullptr;    // external per-query bound of the k-th NN distance (device)
+  bool approx = false;              // paris_knn_approx: the seeds' top-k only
 };
 
 int pairs_for(int nb) { return nb <= 2 ? 1 : nb <= 4 ? 2 : nb <= 8 ? 4 : nb <= 16 ? 8 : nb <= 32 ? 16 : 32; }
@@ -3320,12 +3421,14 @@ int launch_fallback(const Plan& p, const float* raw, const uint8_t* sax, const f
   fa.k = p.k; fa.d2up = p.d2up; fa.best = ws.best; fa.thr = ws.thr; fa.lists = ws.fb_lists; fa.L = p.fbL;
   fa.refined = ws.fb_refined;
   const int grid = p.fbL / (kFbThreads / 32);
-  if (p.k == 1)
-    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("fallback", k_fallback<true>, grid, kFbThreads, 0, st, fa), "fallback launch");
-  else
-    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("fallback", k_fallback<false>, grid, kFbThreads,
-                                    (size_t)(kFbThreads / 32) * p.k * 8, st, fa),
-                       "fallback launch");
+  const bool fast = p.w == kTW && p.n % 4 == 0;
+  const size_t tsm = (size_t)(kFbThreads / 32) * p.k * 8;
+  cudaError_t e;
+  if (p.k == 1) e = fast ? PARIS_LAUNCH("fallback", (k_fallback<true, true>), grid, kFbThreads, 0, st, fa)
+                         : PARIS_LAUNCH("fallback", (k_fallback<true, false>), grid, kFbThreads, 0, st, fa);
+  else e = fast ? PARIS_LAUNCH("fallback", (k_fallback<false, true>), grid, kFbThreads, tsm, st, fa)
+                : PARIS_LAUNCH("fallback", (k_fallback<false, false>), grid, kFbThreads, tsm, st, fa);
+  PARIS_CHECK_LAUNCH(e, "fallback launch");
   PARIS_CHECK_LAUNCH(PARIS_LAUNCH("fallback", k_finalize_ovf, nb, 1024, 0, st, ws.best, ws.fb_lists, p.fbL, p.k, q0,
                                   ws.count, cap, d_idx, d_dist, ws.fb_refined, all_refined),
                      "fallback finalize launch");
@@ -3361,7 +3464,7 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
     }
     {
       dim3 g((unsigned)((p.S + 7) / 8), (unsigned)nb);
-      if (p.raw16 && p.raw_host && p.k == 1)
+      if (p.raw16 && p.raw_host && p.k == 1 && !p.approx)
         PARIS_CHECK_LAUNCH(PARIS_LAUNCH("seed_ed", k_seed_ed16, g, kRefThreads, (size_t)p.len * 4, st, p.raw16,
                                         p.len, qbatch, ws.seed_ids, p.S, ws.seed_keys),
                            "seed_ed launch");
@@ -3370,10 +3473,20 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
                                         qbatch, ws.seed_ids, p.S, ws.seed_keys),
                            "seed_ed launch");
     }
+    if (p.approx) {  // approximate search only: the seeds' top-k is the answer
+      PARIS_CHECK_LAUNCH(PARIS_LAUNCH("seed_select", k_seed_topk, nb, 1024, 0, st, ws.seed_keys, p.S, p.k, q0,
+                                      d_idx, d_dist),
+                         "seed_topk launch");
+      return PARIS_OK;
+    }
     PARIS_CHECK_LAUNCH(PARIS_LAUNCH("seed_select", k_seed_select, nb, 1024, 0, st, ws.seed_keys, p.S, p.k,
                                     p.d2up, ws.thr, ws.thr_seed, ws.best, all_tau, q0),
                        "seed_select launch");
   }
+  if (p.tau_in)
+    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("seed_select", k_tau_in, 1, kMaxB, 0, st, p.tau_in, nb, q0, p.k, p.d2up, ws.thr,
+                                    ws.thr_seed, ws.best),
+                       "tau_in launch");
   if (p.nb) {
     // f2: nb-ParIS+ -- no candidate list: fused LB -> refine per worker, then min(V_bsf)
     PARIS_CHECK_LAUNCH(launch_nb(p, raw, sax, qbatch, nb, tab, ws, st), "nb launch");
@@ -3558,7 +3671,8 @@ void plan_refine(Plan& p) {
 int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queries, int nq, int k,
              int64_t* out_idx, float* out_dist, int len, int w, int card, cudaStream_t st,
              const paris_knn_config* cfg, paris_knn_stats* stats, const uint32_t* perm = nullptr,
-             const uint8_t* env = nullptr, bool nb_mode = false, const uint16_t* raw16 = nullptr) {
+             const uint8_t* env = nullptr, bool nb_mode = false, const uint16_t* raw16 = nullptr,
+             bool approx = false) {
   if (nb_mode && (k != 1 || w != kTW || n % 4 != 0)) {
     set_error("paris_knn_nb: needs k == 1, w == 16, n %% 4 == 0 (k=%d, w=%d, n=%lld)", k, w, (long long)n);
     return k != 1 ? PARIS_EINVAL : PARIS_ECONFIG;
@@ -3642,6 +3756,14 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
     p.raw16 = raw16;
   }
   p.raw_host = raw_host;
+  p.approx = approx;
+  if (cfg && cfg->tau_in && !approx && !nb_mode) {
+    if (is_host_ptr(cfg->tau_in)) {
+      set_error("paris_knn: config.tau_in must be device memory");
+      return PARIS_EINVAL;
+    }
+    p.tau_in = cfg->tau_in;
+  }
   // (host raw with the bf16 copy in HBM: the seeds read bf16 rows, so the full 1024)
   p.idx_seeds = (cfg && cfg->reserved[2] > 0) ? cfg->reserved[2]
                                                : ((raw_host && !(raw16 && k == 1)) ? kIdxSeedsHost : 0);
@@ -3649,7 +3771,16 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   // candidate buffer per query: n/32 for k = 1; k > 1 keeps far more candidates on hard
   // queries (C5 sigma = 0.2, k = 100: ~670 K of 2e7), so n/16 -- an overflow costs a
   // per-query re-scan
-  p.cap = nb_mode ? 1 : std::min<int64_t>(n, std::max<int64_t>(65536, k > 1 ? n / 16 : n / 32));
+  // candidate buffer per query: at least max(65536, n/32) (n/16 for k > 1), grown to a
+  // 2 GB budget per candidate array when that is larger (hard queries -- C3: up to 24% of
+  // n -- then stay on the regular path instead of the overflow fallback)
+  {
+    const int Bq = 2 * pairs_for(p.B);
+    const int64_t floor_cap = std::max<int64_t>(65536, k > 1 ? n / 16 : n / 32);
+    const int64_t budget = (int64_t)(2ll << 30) / (8ll * Bq);
+    p.cap = (nb_mode || approx) ? 1 : std::min<int64_t>(n, std::max(floor_cap, budget));
+    if (cfg && cfg->reserved[4] > 0 && !nb_mode && !approx) p.cap = std::min<int64_t>(n, cfg->reserved[4]);  // test hook
+  }
   plan_refine(p);
   p.wave_a = (cfg && cfg->wave_a > 0) ? cfg->wave_a : 2048;
   // |fp32 d^2 - exact| <= e d^2 with e = (len/32 + 8) u (warp_ed2 / refine_step);
@@ -3665,9 +3796,13 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
     p.fbL = L / (kFbThreads / 32) * (kFbThreads / 32);
   }
   if (k > 1) {
-    const cudaError_t ea = once_per_device((const void*)k_fallback<false>, [](int) {
-      return cudaFuncSetAttribute(k_fallback<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (kFbThreads / 32) * PARIS_MAX_K * 8);
+    const cudaError_t ea = once_per_device((const void*)k_fallback<false, true>, [](int) {
+      cudaError_t r = cudaFuncSetAttribute(k_fallback<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (kFbThreads / 32) * PARIS_MAX_K * 8);
+      if (r == cudaSuccess)
+        r = cudaFuncSetAttribute(k_fallback<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (kFbThreads / 32) * PARIS_MAX_K * 8);
+      return r;
     });
     if (ea != cudaSuccess) return cuda_error(ea, "fallback smem attribute");
   }
@@ -3796,6 +3931,20 @@ int paris_knn_index_ex(const float* raw, const uint8_t* sax_sorted, const uint32
                        const paris_knn_config* config, paris_knn_stats* stats) {
   return paris::knn_impl(raw, sax_sorted, n, queries, nq, k, out_idx, out_dist, len, w, card,
                          (cudaStream_t)stream, config, stats, perm, env);
+}
+
+int paris_knn_approx(const float* raw, const uint8_t* sax, int64_t n, const float* queries, int32_t nq, int32_t k,
+                     int64_t* out_idx, float* out_dist, int32_t len, int32_t w, int32_t card, void* stream,
+                     const paris_knn_config* config) {
+  return paris::knn_impl(raw, sax, n, queries, nq, k, out_idx, out_dist, len, w, card, (cudaStream_t)stream, config,
+                         nullptr, nullptr, nullptr, false, nullptr, /*approx=*/true);
+}
+
+int paris_knn_index_approx(const float* raw, const uint8_t* sax_sorted, const uint32_t* perm, const uint8_t* env,
+                           int64_t n, const float* queries, int32_t nq, int32_t k, int64_t* out_idx, float* out_dist,
+                           int32_t len, int32_t w, int32_t card, void* stream, const paris_knn_config* config) {
+  return paris::knn_impl(raw, sax_sorted, n, queries, nq, k, out_idx, out_dist, len, w, card, (cudaStream_t)stream,
+                         config, nullptr, perm, env, false, nullptr, /*approx=*/true);
 }
 
 int paris_knn_index_x(const float* raw, const uint16_t* raw_bf16, const uint8_t* sax_sorted, const uint32_t* perm,

@@ -420,10 +420,42 @@ __global__ void __launch_bounds__(512) k_read_probe(const uint4* __restrict__ p,
   }
   if (x == 0x9E3779B9u) out[0] = x;  // keeps the loads live; practically never taken
 }
+
+// fp16x2 FMA-pipe probe (the measured peak behind the batched LB's "alu" roofline):
+// every thread runs 8 independent chains of fma.rn.f16x2; one instruction = 2 fp16 FMAs.
+__global__ void __launch_bounds__(512) k_hfma2_probe(int iters, unsigned* out) {
+  uint32_t a[8], b = 0x3C003C00u ^ (threadIdx.x & 1u), c = 0x00010001u;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = 0x3C003C00u + j + threadIdx.x;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) asm volatile("fma.rn.f16x2 %0, %0, %1, %2;" : "+r"(a[j]) : "r"(b), "r"(c));
+  }
+  uint32_t x = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) x ^= a[j];
+  if (x == 0x9E3779B9u) out[0] = x;  // keeps the chains live; practically never taken
+}
 }  // namespace
 }  // namespace paris
 
 extern "C" {
+
+int paris_debug_hfma2_probe(int32_t iters, int32_t blocks_per_sm, void* stream) {
+  if (iters < 1 || blocks_per_sm < 1) return PARIS_EINVAL;
+  static int sink_key;
+  static unsigned* sinks[64] = {nullptr};
+  const cudaError_t ea = paris::once_per_device(&sink_key, [](int dev) {
+    return dev < 64 ? cudaMalloc(&sinks[dev], 4) : cudaErrorInvalidDevice;
+  });
+  if (ea != cudaSuccess) return paris::cuda_error(ea, "hfma2 probe sink");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  PARIS_CHECK_LAUNCH(PARIS_LAUNCH("hfma2_probe", paris::k_hfma2_probe, paris::device_sms() * blocks_per_sm, 512, 0,
+                                  (cudaStream_t)stream, iters, sinks[dev]),
+                     "hfma2 probe launch");
+  return 0;
+}
 
 int paris_debug_read_probe(const void* p, int64_t bytes, void* stream) {
   if (!p || bytes < 16 || (reinterpret_cast<uintptr_t>(p) & 15)) return PARIS_EINVAL;
@@ -446,7 +478,7 @@ int paris_debug_read_probe(const void* p, int64_t bytes, void* stream) {
 
 const char* paris_last_error(void) { return paris::g_err.c_str(); }
 
-int32_t paris_version(void) { return 105; }
+int32_t paris_version(void) { return 106; }
 
 void paris_release_workspace(void) { paris::ws_free_all(); }
 

@@ -130,7 +130,7 @@ def test_knn_index_overflow_rescan(P):
     idx = P.index_build(sax, 16, 256)
     for k in (1, 1000):
         gi, gd, st = P.knn_index(xd, idx, torch.from_numpy(q).cuda(), k=k,
-                                 config=P.KnnConfig(index_seeds=1), stats=True)
+                                 config=P.KnnConfig(index_seeds=1, cap=65536), stats=True)
         ri, rd2 = oracle.knn_bruteforce(x, q, k)
         check_knn(x, q, gi.cpu().numpy(), gd.cpu().numpy(), ri, rd2)
 
@@ -208,11 +208,11 @@ def test_knn_overflow_fallback_mixed(P, k):
     qd = torch.from_numpy(q).cuda()
     sax = P.summarize(xd, 16, 256)
     idx = P.index_build(sax, 16, 256)
-    cfg = P.KnnConfig(index_seeds=1, seed_div=n)
+    cfg = P.KnnConfig(index_seeds=1, seed_div=n, cap=65536)
     gi, gd, st = P.knn_index(xd, idx, qd, k=k, config=cfg, stats=True)
     fi, fd = P.knn_exact(xd, sax, qd, k=k, config=cfg)
     ri, rd2 = oracle.knn_bruteforce(x, q, k)
     check_knn(x, q, gi.cpu().numpy(), gd.cpu().numpy(), ri, rd2)
     check_knn(x, q, fi.cpu().numpy(), fd.cpu().numpy(), ri, rd2)
-    cap = max(65536, n // (16 if k > 1 else 32))
+    cap = 65536
     assert (st["candidates"].numpy()[flood] > cap).all(), "the flooded queries did not overflow"

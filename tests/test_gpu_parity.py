@@ -187,7 +187,7 @@ def test_knn_overflow_rescan(P, torch_dev):
     n = 70_000  # default capacity is max(65536, n/32) = 65536 < n
     x = datagen.random_walks(n, 128, 8)
     q = -datagen.random_walks(2, 128, 9) * 0.0  # all-zero queries: LB of most series is small
-    gi, gd = _knn_case(P, torch_dev, x, q, 1000, config=p.KnnConfig(seed_div=n))
+    gi, gd = _knn_case(P, torch_dev, x, q, 1000, config=p.KnnConfig(seed_div=n, cap=65536))
     ri, rd2 = oracle.knn_bruteforce(x, q, 1000)
     check_knn(x, q, gi, gd, ri, rd2)
 
@@ -243,3 +243,18 @@ def test_knn_refine_waves(P, torch_dev, wave_a, sorted_refine):
     idx = P.index_build(sax, 16, 256)
     hi, hd = P.knn_index(xd, idx, torch.from_numpy(q).to(dev), k=1, config=cfg)
     check_knn(x, q, hi.cpu().numpy(), hd.cpu().numpy(), ri, rd2)
+
+
+@pytest.mark.parametrize("n,w,length,k", [(5003, 8, 64, 1), (5003, 16, 128, 5), (4096, 12, 96, 1), (4096, 16, 256, 1000)])
+def test_knn_overflow_fallback_shapes(P, torch_dev, n, w, length, k):
+    """The overflow fallback on every layout it has: the generic per-series loop (w != 16 or
+    n % 4 != 0) and the 4-series-per-lane form, k = 1 (shared BSF key) and k > 1 (warp lists
+    merged): a tiny forced capacity makes most queries overflow."""
+    import paper_2009_00166_b200 as p
+    x = datagen.random_walks(n, length, 7000 + n + w)
+    q = datagen.random_walks(6, length, 7001 + w)
+    q[1] = 0.0
+    q[4] = x[n - 1]
+    gi, gd = _knn_case(P, torch_dev, x, q, k, w=w, config=p.KnnConfig(cap=16, seed_div=n))
+    ri, rd2 = oracle.knn_bruteforce(x, q, k)
+    check_knn(x, q, gi, gd, ri, rd2)
