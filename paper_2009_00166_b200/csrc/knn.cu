@@ -1131,16 +1131,19 @@ __device__ __forceinline__ uint32_t half_of(uint32_t v, int h) { return (v >> (1
 //   [S0, S0 + 32K)         ring stage 0
 //   [S0 + 32K, T)          misc (LbiMisc): barriers, per-stage tile id / claim counter /
 //                          block masks, LbConsts, per-warp candidate slots and counters
-//   [T, T + 64K)           region table, 16 copies: entry c of copy j at T + 256c + 8j
-//                          (copy = lane % 16: an 8-byte load is served per half-warp, whose
-//                          16 lanes then hit distinct banks).  Bytes [128, 256) of each
-//                          256-byte row are "holes" (128 B each, 256 of them):
-//                            holes   0..31   per-slot query words s_qs (two slots per hole)
-//                            holes  32..127  per-warp candidate keys (kWBI per warp)
-//                            holes 128..191  coarse LB histograms (HC), a slot per hole
+//   [T, T + 64K)           region table half2(-U16, L16) (the single-query form), 32 copies:
+//                          entry c of lane l's copy at T + 256c + 4l (a lookup by 32 lanes
+//                          hits 32 distinct banks).  Bytes [128, 256) of each 256-byte row
+//                          are "holes" (128 B each, 256 of them):
+//                            holes   0..63   per-slot query words half2(q_lo16, -q_hi16),
+//                                            two copies (bytes 0..63 for half-warp 0, 64..127
+//                                            for half-warp 1: 16-byte broadcast loads of two
+//                                            different slots never share a bank)
+//                            holes  64..159  per-warp candidate keys (kWBI per warp)
+//                            holes 160..223  coarse LB histograms (HC), a slot per hole
 //   [T + 64K, ...)         ring stages 1 .. NST-1, then the 16-bit histograms (!HC)
-// One byte permute of a SAX word with {lane%16 * 8, -, T bits 16..31} is a lookup's
-// whole shared address (the symbol lands in bits 8..15).
+// One byte permute of a SAX word with {lane * 4, -, T bits 16..31} is a lookup's whole
+// shared address (the symbol lands in bits 8..15).
 constexpr int kIWarps = 24;                   // consumer warps
 constexpr int kIThreads = (kIWarps + 1) * 32; // + the producer warp
 constexpr int kWBI = 64;                      // staged candidates per consumer warp
@@ -1165,7 +1168,7 @@ static_assert(kTileBytes + kIMiscBytes + 4096 <= 65536, "stage 0 + misc must fit
 
 __device__ __forceinline__ uint32_t hole_addr(uint32_t T, int h) { return T + 256u * (uint32_t)h + 128u; }
 __device__ __forceinline__ uint32_t lbi_key_addr(uint32_t T, int warp, int e) {
-  return hole_addr(T, 32 + 4 * warp + (e >> 4)) + 8u * (uint32_t)(e & 15);
+  return hole_addr(T, 64 + 4 * warp + (e >> 4)) + 8u * (uint32_t)(e & 15);
 }
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
   uint32_t v;
@@ -1197,7 +1200,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // the packed 16-bit form at hist16 (hist16_add).
 template <bool HC>
 __device__ __forceinline__ void lbi_hist(uint32_t T, unsigned* hist16, int b, int bin, unsigned* g_hist) {
-  if (HC) atoms_add(hole_addr(T, 128 + b) + 4u * (uint32_t)(bin >> 3), 1u);
+  if (HC) atoms_add(hole_addr(T, 160 + b) + 4u * (uint32_t)(bin >> 3), 1u);
   else hist16_add(hist16, b * kNB + bin, g_hist);
 }
 
@@ -1300,15 +1303,29 @@ __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int s
     return;
   }
   int pos = (int)wb.n + incl - cntl;
-#pragma unroll
-  for (int bit = 0; bit < 8; ++bit) {
-    if (!((pm >> bit) & 1u)) continue;
+  for (uint32_t r = pm; r; r &= r - 1) {
+    const int bit = __ffs(r) - 1;
     const int j = bit >> 1, sl = (bit & 1) ? sb : sa;
     PARIS_DCHECK(i0 + j < a.n && pos < kWBI && sl >= 0);
-    sts_u64(lbi_key_addr(T, warp, pos), make_key(lbv[j][bit & 1], (uint32_t)(i0 + j)));  // sorted position
+    float lv = 0.f;  // lbv[j][bit & 1] without dynamic register indexing
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q == bit) lv = lbv[q >> 1][q & 1];
+    sts_u64(lbi_key_addr(T, warp, pos), make_key(lv, (uint32_t)(i0 + j)));  // sorted position
     wb.slot[pos] = (uint8_t)sl;
-    atomicAdd(&wb.cnt[sl], 1u);
     ++pos;
+  }
+  // per-slot counts: summed over each half-warp (its item has slots sa, sb), one shared
+  // atomic per (half, slot) instead of one per candidate
+  int na = __popc(pm & 0x55u), nbb = __popc(pm & 0xAAu);
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) {
+    na += __shfl_xor_sync(0xffffffffu, na, o);
+    nbb += __shfl_xor_sync(0xffffffffu, nbb, o);
+  }
+  if ((lane & 15) == 0) {
+    if (na) atomicAdd(&wb.cnt[sa], (unsigned)na);
+    if (nbb) atomicAdd(&wb.cnt[sb], (unsigned)nbb);
   }
   __syncwarp();
   if (lane == 31) wb.n += total;
@@ -1444,7 +1461,7 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
   const int nslots = 2 * P;
   const int64_t nlist = *tile_count;
 
-  // ---- setup: barriers, table (16 copies), query words, histograms, warp buffers
+  // ---- setup: barriers, table (32 copies), query words, histograms, warp buffers
   if (tid == 0) {
     for (int st = 0; st < NST; ++st) {
       mbar_init(&M.full[st], 1);
@@ -1452,15 +1469,17 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int i = tid; i < kMaxCard * 16; i += kIThreads) sts_u2(T + 256u * (uint32_t)(i >> 4) + 8u * (uint32_t)(i & 15), a.tab->lu16[i >> 4]);
+  for (int i = tid; i < kMaxCard * 32; i += kIThreads)
+    sts_u32(T + 256u * (uint32_t)(i >> 5) + 4u * (uint32_t)(i & 31), a.tab->lu16p[i >> 5]);
   for (int i = tid; i < nslots * kTW; i += kIThreads) {  // slot b, segment s: half2(q_lo16, -q_hi16)
     const int b = i / kTW, sg = i % kTW;
     const uint2 v = a.g_q16[sg * P + (b >> 1)];
-    sts_u32(hole_addr(T, b >> 1) + 64u * (uint32_t)(b & 1) + 4u * (uint32_t)sg,
-            half_of(v.x, b & 1) | (half_of(v.y, b & 1) << 16));
+    const uint32_t qw = half_of(v.x, b & 1) | (half_of(v.y, b & 1) << 16);
+    sts_u32(hole_addr(T, b) + 4u * (uint32_t)sg, qw);
+    sts_u32(hole_addr(T, b) + 64u + 4u * (uint32_t)sg, qw);
   }
   if (HC) {
-    for (int i = tid; i < nslots * kNBC; i += kIThreads) sts_u32(hole_addr(T, 128 + i / kNBC) + 4u * (uint32_t)(i % kNBC), 0u);
+    for (int i = tid; i < nslots * kNBC; i += kIThreads) sts_u32(hole_addr(T, 160 + i / kNBC) + 4u * (uint32_t)(i % kNBC), 0u);
   } else {
     for (int i = tid; i < nslots * kNB / 2; i += kIThreads) hist16[i] = 0;
   }
@@ -1492,7 +1511,7 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
     // ---- consumers
     LbiWarp& wb = M.w[warp];
     const LbConsts& c = M.c;
-    const uint32_t lanebase = T | ((uint32_t)(lane & 15) * 8u);  // bytes {lane%16 * 8, 0, T bits 16-31}
+    const uint32_t lanebase = T | ((uint32_t)lane * 4u);  // bytes {lane * 4, 0, T bits 16-31}
     const int h = lane >> 4, hl = lane & 15;
     for (int64_t it = 0;; ++it) {
       const int64_t li = blockIdx.x + it * gridDim.x;
@@ -1535,25 +1554,42 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
         m &= m - 1;
         const int sb = (active && m) ? __ffsll((long long)m) - 1 : -1;
         const int sq = sb >= 0 ? sb : sa;  // odd count: duplicate lane, masked in emission
-        // (generic pointers derived from dsm: LDS with immediate segment offsets)
-        const uint32_t* qa_p = reinterpret_cast<const uint32_t*>(gbase + hole_addr(T, sa >> 1) + 64u * (uint32_t)(sa & 1));
-        const uint32_t* qb_p = reinterpret_cast<const uint32_t*>(gbase + hole_addr(T, sq >> 1) + 64u * (uint32_t)(sq & 1));
+        // single-query form per slot (as k_lb1): one lookup t = (-U16, L16) serves both
+        // slots; d = relu(q2 + t) = (relu(q_lo - U), relu(L - q_hi)) and acc += d^2 keep the
+        // ABOVE and BELOW sums in the two halves (at most one is non-zero per segment).
+        // Query words: 16-byte broadcast loads from this half-warp's copy (generic pointers
+        // derived from dsm: LDS with immediate segment offsets).
+        const uint4* qa4 = reinterpret_cast<const uint4*>(gbase + hole_addr(T, sa) + 64u * (uint32_t)h);
+        const uint4* qb4 = reinterpret_cast<const uint4*>(gbase + hole_addr(T, sq) + 64u * (uint32_t)h);
         const uint32_t* wp = reinterpret_cast<const uint32_t*>(gbase + rows) + k * (PARIS_INDEX_BLOCK / 4) + hl;
-        uint32_t acc[4] = {0u, 0u, 0u, 0u};
+        uint32_t acca[4] = {0u, 0u, 0u, 0u}, accb[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-        for (int s = 0; s < kTW; ++s) {
-          const uint32_t word = wp[s * (kTS / 4)];
-          const uint32_t qa = qa_p[s], qb = qb_p[s];
-          const uint32_t qx = __byte_perm(qa, qb, 0x5410);  // (q_lo16[sa], q_lo16[sb])
-          const uint32_t qy = __byte_perm(qa, qb, 0x7632);  // (-q_hi16[sa], -q_hi16[sb])
+        for (int s4 = 0; s4 < kTW / 4; ++s4) {
+          const uint4 qa = qa4[s4], qb = qb4[s4];
+          const uint32_t qaw[4] = {qa.x, qa.y, qa.z, qa.w}, qbw[4] = {qb.x, qb.y, qb.z, qb.w};
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            // address = {lanebase.b0, word.bj, lanebase.b2, lanebase.b3}
-            const uint2 tt = lds_u2(__byte_perm(word, lanebase, 0x7604u | ((uint32_t)j << 4)));
-            const uint32_t a1 = h2_fma_relu(qx, kHalf2One, tt.x);
-            const uint32_t b1 = h2_fma_relu(qy, kHalf2One, tt.y);
-            acc[j] = h2_acc_delta2(acc[j], a1, b1);
+          for (int s1 = 0; s1 < 4; ++s1) {
+            const int s = 4 * s4 + s1;
+            const uint32_t word = wp[s * (kTS / 4)];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              // address = {lanebase.b0, word.bj, lanebase.b2, lanebase.b3}
+              const uint32_t t = lds_u32(__byte_perm(word, lanebase, 0x7604u | ((uint32_t)j << 4)));
+              const uint32_t da = h2_fma_relu(qaw[s1], kHalf2One, t);
+              const uint32_t db = h2_fma_relu(qbw[s1], kHalf2One, t);
+              acca[j] = h2_fma(da, da, acca[j]);
+              accb[j] = h2_fma(db, db, accb[j]);
+            }
           }
+        }
+        // LB16 per (series, slot) = ABOVE + BELOW sums (fp32 add, rounded up to fp16 -- the
+        // single-query form inside k_lb's error budget), packed (slot sa low, sb high)
+        uint32_t acc[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t la = __half_as_ushort(__float2half_ru(h_lo_f(acca[j]) + h_hi_f(acca[j])));
+          const uint32_t lb = __half_as_ushort(__float2half_ru(h_lo_f(accb[j]) + h_hi_f(accb[j])));
+          acc[j] = la | (lb << 16);
         }
         const int64_t i0 = tile * kTS + k * PARIS_INDEX_BLOCK + 4 * hl;
         const int nvalid = active ? (int)std::max<int64_t>(0, imin64(4, a.n - i0)) : 0;
@@ -1568,7 +1604,7 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
   __syncthreads();
   if (HC) {
     for (int i = tid; i < nslots * kNBC; i += kIThreads) {
-      const uint32_t v = lds_u32(hole_addr(T, 128 + i / kNBC) + 4u * (uint32_t)(i % kNBC));
+      const uint32_t v = lds_u32(hole_addr(T, 160 + i / kNBC) + 4u * (uint32_t)(i % kNBC));
       if (v) atomicAdd(&a.hist[(i / kNBC) * kNB + (i % kNBC) * 8 + 7], v);
     }
   } else {

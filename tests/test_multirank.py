@@ -74,7 +74,7 @@ def _ref_merge(dst, idx):
     return torch.from_numpy(out_i), torch.from_numpy(out_d)
 
 
-def _shard_worker(rank, world, port, q, n, k):
+def _shard_worker(rank, world, port, q, n, k, use_tau=False):
     import datagen
     import oracle
     from paper_2009_00166_b200 import parallel as par
@@ -85,19 +85,38 @@ def _shard_worker(rank, world, port, q, n, k):
         lo, hi = par.shard_range(n, rank, world)
         shard = datagen.random_walks(hi - lo, 128, 77, first_id=lo)     # this rank's ids [lo, hi)
         queries = datagen.random_walks(5, 128, 78)
+        seen = {}
 
-        def local(qs, kk):                                             # test-side stand-in for the GPU search
-            ri, rd2 = oracle.knn_bruteforce(shard, qs.numpy(), kk)
-            return torch.from_numpy(ri), torch.from_numpy(np.sqrt(rd2).astype(np.float32))
+        def local(qs, kk, tau_in=None):                                # test-side stand-in for the GPU search:
+            ri, rd2 = oracle.knn_bruteforce(shard, qs.numpy(), kk)     # the library's tau_in semantics --
+            d = np.sqrt(rd2).astype(np.float32)                        # rows beyond the bound come back -1
+            if tau_in is not None:
+                seen["tau"] = tau_in.numpy().copy()
+                out = d > tau_in.numpy()[:, None]
+                ri = np.where(out, -1, ri)
+                d = np.where(out, np.float32(np.inf), d)
+            return torch.from_numpy(ri), torch.from_numpy(d)
 
-        gi, gd = par.knn_sharded(torch.from_numpy(queries), k, lo, local, merge=_ref_merge)
-        q.put((rank, gi.numpy(), gd.numpy()))
+        def approx(qs, kk):                                             # a shard's approximate answer: the k-th
+            seeds = shard[: 40 + 30 * rank]                             # best of a few of its series (a real bound)
+            _, rd2 = oracle.knn_bruteforce(seeds, qs.numpy(), kk)
+            tau = torch.from_numpy(np.sqrt(rd2[:, kk - 1]).astype(np.float32))
+            seen["own"] = tau.numpy().copy()
+            return tau
+
+        gi, gd = par.knn_sharded(torch.from_numpy(queries), k, lo, local, merge=_ref_merge,
+                                 approx=approx if use_tau else None)
+        q.put((rank, gi.numpy(), gd.numpy(), seen))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("k", [1, 7])
-def test_two_rank_sharded_knn_is_exact(k):
+@pytest.mark.parametrize("k,use_tau", [(1, False), (7, False), (1, True), (7, True)])
+def test_two_rank_sharded_knn_is_exact(k, use_tau):
+    """Sharded exact k-NN over gloo (world size 2): with use_tau, the tau_seed exchange --
+    every shard's approximate k-th distance, all-reduced with min, bounds every shard's
+    search (rows beyond it come back empty) -- must leave the merged answer exact, and both
+    ranks must have searched with the same bound, the minimum of their own."""
     import datagen
     import oracle
     from paper_2009_00166_b200 import parallel as par
@@ -105,7 +124,7 @@ def test_two_rank_sharded_knn_is_exact(k):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_shard_worker, args=(r, 2, port, q, n, k)) for r in range(2)]
+    procs = [ctx.Process(target=_shard_worker, args=(r, 2, port, q, n, k, use_tau)) for r in range(2)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=180) for _ in range(2)], key=lambda t: t[0])
@@ -116,9 +135,14 @@ def test_two_rank_sharded_knn_is_exact(k):
                            for lo, hi in (par.shard_range(n, r, 2) for r in range(2))])
     assert np.array_equal(full, datagen.random_walks(n, 128, 77))   # shards tile the collection
     ri, rd2 = oracle.knn_bruteforce(full, datagen.random_walks(5, 128, 78), k)
-    for _, gi, gd in res:                                           # same answer on every rank
+    for _, gi, gd, _ in res:                                        # same answer on every rank
         np.testing.assert_array_equal(gi, ri)
         np.testing.assert_allclose(gd, np.sqrt(rd2), rtol=1e-6)
+    if use_tau:
+        own = np.minimum(res[0][3]["own"], res[1][3]["own"])
+        for _, _, _, seen in res:
+            np.testing.assert_array_equal(seen["tau"], own)         # all-reduce(min) of the shards' bounds
+        assert not np.array_equal(res[0][3]["own"], res[1][3]["own"])
 
 
 def test_shard_ranges_partition():
