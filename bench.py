@@ -3,23 +3,28 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
 
-One step = one paris_knn_exact call answering the config's whole query batch (rows
-a3-a8 of SURVEY §8: query PAA, BSF seed, LB pass, candidate order, refinement,
-finalize) over a device-resident collection + SAX array.  Summarization (rows a1-a2)
-is timed in the same run as its own line item ("summarize").  Inputs are larger than
-L2 (config 4: SAX 1.6 GB, raw 102.4 GB vs 126 MB L2), so no flush is needed.
+One step = the config's whole query batch answered exactly (rows a3-a8 of SURVEY §8: query
+PAA, BSF seed, LB pass, candidate order, refinement, finalize) over a device-resident
+collection + SAX array / index, through the library's public calls.  Summarization (rows
+a1-a2) is timed in the same run as its own line item ("summarize").  Inputs are larger
+than L2 (config 4: SAX 1.6 GB, raw 102.4 GB vs 126 MB L2), so no flush is needed.
 
-Multi-GPU (torchrun): weak scaling -- every rank holds its own collection of the
-config's size and answers its own queries (queries are independent problems); no
-data-path collective; the only NCCL calls are the timing barrier/max.
---impl reference: the CPU oracle (oracle/, single thread) timed on a bounded sample of
-the same workload, scaled to queries/s over the full collection.
+Multi-GPU (torchrun): by default ONE collection of the config's size is
+sharded by series-id range over the ranks (strong scaling): every query batch is searched
+on every shard after an all-reduce(min) of the shards' approximate-answer bounds (the
+tau_seed exchange), and the per-shard rows are all-gathered and merged exactly
+(paris_merge_topk).  --weak instead gives every rank its own collection of the config's
+size (independent problems, no data-path collective).
+--impl reference: the CPU oracle (oracle/, single thread) timed on a bounded sample of the
+same workload, scaled to queries/s over the full collection.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -96,7 +101,7 @@ class ClockSampler:
 
 
 def rank_seeds(config: int, rank: int):
-    """(dataset seed, query seed) of a rank: weak scaling -- every rank owns a distinct
+    """(dataset seed, query seed) of a rank in --weak mode: every rank owns a distinct
     collection and query set of the config's size (queries are independent problems)."""
     import datagen
     ds, qs = datagen.config_seeds(config)
@@ -114,23 +119,25 @@ def reduce_max_ms(ms: float, device, world_size: int) -> float:
 
 
 def weak_throughput(nq_per_rank: int, world_size: int, max_ms: float) -> float:
-    """Whole-job queries/s: every rank answered nq_per_rank queries within max_ms."""
+    """Whole-job queries/s in --weak mode: every rank answered nq_per_rank queries within max_ms."""
     return nq_per_rank * world_size / (max_ms / 1e3)
 
 
-def seed_series(n: int, use_index: bool, index_seeds: int, k: int) -> int:
-    """Series whose true distance the BSF seed computes per query (plan_seed in csrc/knn.cu):
-    index path -- the index_seeds (default 1024) series around the query's leaf; flat path --
-    the LB-best series of each of 16 warps x seed_grid CTAs over a prefix sample of n/16."""
-    if use_index:
-        return max(k, min(4096, index_seeds or 1024))
-    ns = min(n, max(n // 16, min(n, 65536)))
-    ns = min(n, (ns + 15) // 16 * 16)
-    return min(148, (ns + 2047) // 2048) * 16
+def spread(ms_list):
+    """Mean / spread of per-step device times (mean of runs, spread stated)."""
+    if not ms_list:
+        return None
+    m = statistics.mean(ms_list)
+    sd = statistics.pstdev(ms_list) if len(ms_list) > 1 else 0.0
+    return {"steps": len(ms_list), "mean_ms": m, "std_ms": sd, "min_ms": min(ms_list), "max_ms": max(ms_list),
+            "rel_spread": (max(ms_list) - min(ms_list)) / m if m > 0 else None}
 
 
-def refined_sum_of(stats) -> float:
-    return float(stats["refined"].double().sum())
+def lib_sha16() -> str | None:
+    p = os.path.join(ROOT, "paper_2009_00166_b200", "libparis.so")
+    if not os.path.exists(p):
+        return None
+    return hashlib.sha256(open(p, "rb").read()).hexdigest()[:16]
 
 
 def measured_peaks():
@@ -142,28 +149,63 @@ def measured_peaks():
 
 
 def ncu_traffic(kernel: str, config: int):
+    """DRAM bytes per launch of `kernel` from an ncu --set full capture of THIS build
+    (profiles/ncu_traffic.json records the libparis.so hash it was captured on); None when
+    the capture is of another build."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     d = json.load(open(p))
+    if d.get("lib_sha16") != lib_sha16():
+        return None
     return d.get(f"C{config}", {}).get(kernel)
 
 
+def host_info():
+    model = platform.processor() or None
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if line.lower().startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
 # --------------------------------------------------------------------------- CPU oracle arm
-def oracle_sample(raw_dev, queries_dev, k, n_sample, nq_sample):
-    """Time the oracle's LB-pruned exact search (its own SAX) on the first n_sample series
-    for nq_sample queries; returns (seconds per query on the sample, threads)."""
-    import numpy as np
+def oracle_sample(raw_dev, queries_dev, k, n_sample, nq_sample, pin_core: bool = True):
+    """Time the oracle's LB-pruned exact search (its own SAX, its own code) on the first
+    n_sample series for nq_sample queries, on host core 0 (taskset -c 0 semantics: this
+    thread's affinity pinned for the call); returns seconds per query on the sample."""
     import oracle
     x = raw_dev[:n_sample].cpu().numpy()
     q = queries_dev[:nq_sample].cpu().numpy()
     sax = oracle.summarize(x, W, CARD)
-    t0 = time.perf_counter()
-    oracle.knn_pruned(x, sax, q, k, W, CARD)
-    dt = time.perf_counter() - t0
-    del x, sax
-    _ = np
+    old = None
+    if pin_core and hasattr(os, "sched_setaffinity"):
+        old = os.sched_getaffinity(0)
+        os.sched_setaffinity(0, {min(old)})
+    try:
+        t0 = time.perf_counter()
+        oracle.knn_pruned(x, sax, q, k, W, CARD)
+        dt = time.perf_counter() - t0
+    finally:
+        if old is not None:
+            os.sched_setaffinity(0, old)
     return dt / nq_sample
+
+
+def oracle_scaling(raw, queries, k, n, samples, nq_sample):
+    """The oracle at several sample sizes: seconds per query at each n_s and
+    the full-collection estimate extrapolated from the largest sample (pruned cost grows
+    at most linearly in n)."""
+    pts = []
+    for ns in samples:
+        ns = min(n, ns)
+        pts.append({"n": ns, "sec_per_query": oracle_sample(raw, queries, k, ns, nq_sample)})
+    last = pts[-1]
+    est = last["sec_per_query"] * n / last["n"]
+    return pts, est
 
 
 def run_reference(args):
@@ -172,18 +214,17 @@ def run_reference(args):
         return 0
     import torch
     from datagen import gpu as dg
+    import datagen
     cfg = CONFIGS[args.config]
     n, length, nq, k = cfg["n"], cfg["len"], cfg["nq"], cfg["k"]
     dev = torch.device("cuda:0") if torch.cuda.is_available() else None
     n_sample = min(n, args.ref_sample)
     log(f"reference arm: oracle on {n_sample} of {n} series")
+    ds, qs = datagen.config_seeds(args.config)
     if dev is not None:
-        ds, qs = __import__("datagen").config_seeds(args.config)
         raw = dg.walks(n_sample, length, ds, device=dev)
         queries = dg.walks(max(2, args.ref_queries), length, qs, device=dev)
     else:
-        import datagen
-        ds, qs = datagen.config_seeds(args.config)
         raw = torch.from_numpy(datagen.random_walks(n_sample, length, ds))
         queries = torch.from_numpy(datagen.random_walks(max(2, args.ref_queries), length, qs))
     per_q = []
@@ -193,14 +234,15 @@ def run_reference(args):
             per_q.append(t * (n / n_sample))  # scaled to the full collection (linear in n)
     sec_per_query = statistics.mean(per_q)
     value = 1.0 / sec_per_query
-    sample = (f"oracle_knn_pruned (single thread, fp64) over the first {n_sample} series of {cfg['desc']}, "
-              f"{args.ref_queries} queries per step, time scaled x{n / n_sample:.0f} to n={n}")
+    sample = (f"oracle_knn_pruned (single thread pinned to one core, fp64) over the first {n_sample} series of "
+              f"{cfg['desc']}, {args.ref_queries} queries per step, time scaled x{n / n_sample:.0f} to n={n}")
     line = {"impl": "reference", "metric": "exact 1-NN queries/sec", "value": value, "unit": "queries/s",
             "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": sec_per_query * nq * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": sec_per_query * nq * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["desc"], "n": n, "len": length, "w": W, "card": CARD, "nq": nq, "k": k},
-            "cpu_baseline": {"value": value, "unit": "queries/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": dict({"value": value, "unit": "queries/s", "cores": 1, "kind": "oracle", "sample": sample},
+                                 **host_info()),
             "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -213,36 +255,48 @@ def run_gpu(args):
     import torch.distributed as dist
 
     import paper_2009_00166_b200 as P
+    from paper_2009_00166_b200 import parallel as par
     from datagen import gpu as dg
     import datagen
 
     ws, rank, local = dist_env()
-    if ws > 1:
-        dist.init_process_group("nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
     cfg = CONFIGS[args.config]
     n, length, nq, k = cfg["n"], cfg["len"], cfg["nq"], cfg["k"]
     if args.n:
         n = args.n
     if args.nq:
         nq = args.nq
-    call_q = cfg.get("call", nq)  # queries per paris_knn_exact call (C3: batches of 64)
-    ds, qs = rank_seeds(args.config, rank)
+    call_q = cfg.get("call", nq)  # queries per library call (C3: batches of 64)
+    sharded = not args.weak
+    if sharded:
+        ds, qs = datagen.config_seeds(args.config)
+        lo, hi = par.shard_range(n, rank, ws)
+    else:
+        ds, qs = rank_seeds(args.config, rank)
+        lo, hi = 0, n
+    n_local = hi - lo
 
     t0 = time.time()
-    raw = dg.walks(n, length, ds, device=dev)
-    if cfg["queries"] == "fresh":
+    raw = dg.walks(n_local, length, ds, first_id=lo, device=dev)          # this rank's ids [lo, hi)
+    sigma = None if cfg["queries"] == "fresh" else float(cfg["queries"][5:])
+    if sigma is None:
         queries = dg.walks(nq, length, qs, device=dev)
+    elif sharded and ws > 1:
+        queries, _ = dg.member_queries(n, length, ds, nq, sigma, qs, device=dev)   # same on every rank
     else:
-        queries, _ = dg.noisy_members(raw, nq, float(cfg["queries"][5:]), qs)
-    sax = torch.empty((W, n), dtype=torch.uint8, device=dev)
+        queries, _ = dg.noisy_members(raw, nq, sigma, qs)
+    sax = torch.empty((W, n_local), dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
-    log(f"rank {rank}: generated n={n} len={length} nq={nq} in {time.time() - t0:.1f}s")
+    log(f"rank {rank}: generated ids [{lo}, {hi}) of n={n} len={length} nq={nq} in {time.time() - t0:.1f}s")
     h2d_gbs = None
+    use_index = args.path == "index"
     # the bf16 copy of raw for the index path's refinement pre-filter (paris_raw_bf16), built once
     raw16, raw16_ms = None, None
-    if not args.no_raw16 and (args.path == "index" or args.both):
+    if not args.no_raw16 and (use_index or args.both):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         raw16 = P.raw_bf16(raw)
@@ -252,18 +306,17 @@ def run_gpu(args):
     if args.raw_host:
         # f3: the raw collection lives in pinned host memory (not in HBM); summarize streams
         # it through the double-buffered H2D pipeline, the refinement reads candidates' rows
-        # through the host mapping.  Only SAX (+ index) stays in HBM.
+        # through the host mapping.  Only SAX (+ index, + the bf16 copy) stays in HBM.
         t1 = time.time()
-        raw_h = torch.empty((n, length), dtype=torch.float32, pin_memory=True)
+        raw_h = torch.empty((n_local, length), dtype=torch.float32, pin_memory=True)
         step_rows = 1 << 20
-        for r0 in range(0, n, step_rows):
+        for r0 in range(0, n_local, step_rows):
             raw_h[r0:r0 + step_rows].copy_(raw[r0:r0 + step_rows])
         torch.cuda.synchronize()
         del raw
         torch.cuda.empty_cache()
         raw = raw_h
-        # the PCIe roofline: a plain pinned -> device copy of 1 GB (cudaMemcpyAsync)
-        tmp = torch.empty(1 << 28, dtype=torch.float32, device=dev)
+        tmp = torch.empty(1 << 28, dtype=torch.float32, device=dev)        # the PCIe roofline
         src = raw.view(-1)[:1 << 28]
         tmp.copy_(src, non_blocking=True)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -277,7 +330,7 @@ def run_gpu(args):
         log(f"rank {rank}: raw moved to pinned host memory in {time.time() - t1:.1f}s; H2D copy {h2d_gbs:.1f} GB/s")
     st = torch.cuda.current_stream()
 
-    # ---- summarize (rows a1-a2): warmup + timed
+    # ---- summarize (rows a1-a2): warmup + timed (each rank its shard; whole job = n / max)
     for _ in range(args.warmup):
         P.summarize(raw, W, CARD, out=sax)
     torch.cuda.synchronize()
@@ -287,12 +340,13 @@ def run_gpu(args):
         P.summarize(raw, W, CARD, out=sax)
     e1.record(st)
     torch.cuda.synchronize()
-    sum_ms = e0.elapsed_time(e1) / args.steps
+    sum_ms_local = e0.elapsed_time(e1) / args.steps
+    sum_ms = reduce_max_ms(sum_ms_local, dev, ws)
 
     # ---- index (f1): iSAX-ordered SAX + block envelopes, built once (timed on its own)
     index = None
     index_ms = None
-    if args.path == "index" or args.both:
+    if use_index or args.both:
         index = P.index_build(sax, W, CARD)
         torch.cuda.synchronize()
         e0.record(st)
@@ -301,7 +355,7 @@ def run_gpu(args):
         torch.cuda.synchronize()
         index_ms = e0.elapsed_time(e1)
     peak, peak_src = measured_peaks()
-    # read-only streaming peak: the library's 16-byte read probe over >= 8 GB
+    # read-only streaming peak and the fp16x2 FMA-pipe peak, measured here
     read_peak = None
     if not args.raw_host:
         probe = raw if raw.numel() * 4 >= (8 << 30) else torch.empty(8 << 30, dtype=torch.uint8, device=dev)
@@ -314,20 +368,37 @@ def run_gpu(args):
         torch.cuda.synchronize()
         read_peak = 3.0 * probe.numel() * probe.element_size() / (e0.elapsed_time(e1) / 1e3) / 1e9
         del probe
+    fma_peak = 0.0
+    P.debug_hfma2_probe(100, 4)
+    for _ in range(3):
+        e0.record()
+        ops = P.debug_hfma2_probe(20000, 4)
+        e1.record()
+        torch.cuda.synchronize()
+        fma_peak = max(fma_peak, ops / (e0.elapsed_time(e1) / 1e3) / 1e12)
+
+    def local_fn(path, kcfg):
+        if path == "index":
+            return par.local_index_search(raw, index, config=kcfg, raw16=raw16)
+        if path == "nb":
+            return lambda qq, kk, tau_in=None: P.knn_nb(raw, sax, qq, w=W, card=CARD, config=kcfg)
+        return par.local_flat_search(raw, sax, W, CARD, config=kcfg)
 
     def measure_path(path: str, full: bool):
-        """Warm up, time K steps of `path` (device events, max over ranks), then the same K
-        steps with per-launch events for the kernel split and the roofline; with full=True
-        also the end-to-end variant through host buffers and the clock record."""
-        use_index = path == "index"
+        """Warm up, time K steps of `path` (device events per step, max over ranks), then the
+        same K steps with per-launch events for the kernel split and the roofline; with
+        full=True also the end-to-end variant through host buffers and the clock record."""
+        use_idx = path == "index"
         use_nb = path == "nb"
-        b_path = args.batch or (64 if use_index else 16)  # the library's default queries per pass
+        b_path = args.batch or (64 if use_idx else 16)  # the library's default queries per pass
         kcfg = P.KnnConfig(batch=b_path, index_seeds=args.index_seeds, sorted_refine=args.sorted_refine)
         nbatches = sum((min(call_q, nq - c0) + b_path - 1) // b_path for c0 in range(0, nq, call_q))
         q_per_pass = nq / nbatches
+        search = local_fn(path, kcfg)
+        approx = (par.approx_index_search(raw, index, config=kcfg) if use_idx and ws > 1 and sharded else None)
 
-        def knn(qsrc, **kw):
-            if use_index:
+        def knn_local(qsrc, **kw):
+            if use_idx:
                 return P.knn_index(raw, index, qsrc, k=k, raw16=raw16, **kw)
             if use_nb:
                 return P.knn_nb(raw, sax, qsrc, w=W, card=CARD, **kw)
@@ -336,34 +407,42 @@ def run_gpu(args):
         out_idx = torch.empty((nq, k), dtype=torch.int64, device=dev)
         out_dist = torch.empty((nq, k), dtype=torch.float32, device=dev)
 
-        def step(qsrc, oi, od, cfg_=None):
-            cfg_ = cfg_ or kcfg
+        def step(qsrc, oi, od):
+            """One step: every call of the config answered exactly over the whole collection."""
             for c0 in range(0, nq, call_q):
                 c1 = min(nq, c0 + call_q)
-                knn(qsrc[c0:c1], out_idx=oi[c0:c1], out_dist=od[c0:c1], config=cfg_)
+                if ws == 1 or not sharded:
+                    knn_local(qsrc[c0:c1], out_idx=oi[c0:c1], out_dist=od[c0:c1], config=kcfg, sync=False)
+                else:
+                    gi, gd = par.knn_sharded(qsrc[c0:c1], k, lo, search, approx=approx)
+                    oi[c0:c1].copy_(gi, non_blocking=True)
+                    od[c0:c1].copy_(gd, non_blocking=True)
 
-        _, _, stats = knn(queries, out_idx=out_idx, out_dist=out_dist, config=kcfg, stats=True)
+        _, _, stats = knn_local(queries, out_idx=out_idx, out_dist=out_dist, config=kcfg, stats=True)
         for _ in range(max(0, args.warmup - 1)):
             step(queries, out_idx, out_dist)
         torch.cuda.synchronize()
-        r = {"path": path, "stats": stats, "knn": knn, "out_idx": out_idx}
-        # timed region
+        r = {"path": path, "stats": stats, "out_idx": out_idx}
+        # timed region: K steps, an event between consecutive steps (per-step spread)
         launches0 = P.launch_count()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
         if ws > 1:
             dist.barrier()
         torch.cuda.synchronize()
         with ClockSampler(local) as clocks:
-            e0.record(st)
-            for _ in range(args.steps):
+            evs[0].record(st)
+            for i in range(args.steps):
                 step(queries, out_idx, out_dist)
-            e1.record(st)
+                evs[i + 1].record(st)
             torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()
         r["launches"] = P.launch_count() - launches0
         r["clocks"] = clocks.summary()
-        r["step_ms"] = reduce_max_ms(e0.elapsed_time(e1) / args.steps, dev, ws)
-        r["value"] = weak_throughput(nq, ws, r["step_ms"])
+        per_step = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+        r["step_ms"] = reduce_max_ms(evs[0].elapsed_time(evs[-1]) / args.steps, dev, ws)
+        r["spread"] = spread(per_step)
+        r["value"] = (nq if sharded else nq * ws) / (r["step_ms"] / 1e3)
         # the same K steps with libparis' per-launch CUDA events (launching stream)
         P.profile_reset()
         P.profile_enable(True)
@@ -373,18 +452,31 @@ def run_gpu(args):
         P.profile_enable(False)
         prof = P.profile_read()
         if full:
-            # e2e through the same ABI calls with HOST (pinned) buffers
+            # e2e through the same public calls with HOST (pinned) buffers: every step copies
+            # its queries host -> device and reads its results back (one sync per step)
             hq = queries.cpu().pin_memory()
             hidx = torch.empty((nq, k), dtype=torch.int64).pin_memory()
             hdist = torch.empty((nq, k), dtype=torch.float32).pin_memory()
-            step(hq, hidx, hdist)
-            torch.cuda.synchronize()
+
+            def step_e2e():
+                if ws == 1 or not sharded:
+                    step(hq, hidx, hdist)                    # the library stages H2D / D2H
+                else:
+                    qd = hq.to(dev, non_blocking=True)
+                    step(qd, out_idx, out_dist)
+                    hidx.copy_(out_idx, non_blocking=True)
+                    hdist.copy_(out_dist, non_blocking=True)
+                st.synchronize()
+
+            step_e2e()
+            if ws > 1:
+                dist.barrier()
             e0.record(st)
             for _ in range(args.steps):
-                step(hq, hidx, hdist)
+                step_e2e()
             e1.record(st)
             torch.cuda.synchronize()
-            r["e2e_value"] = weak_throughput(nq, ws, reduce_max_ms(e0.elapsed_time(e1) / args.steps, dev, ws))
+            r["e2e_value"] = (nq if sharded else nq * ws) / (reduce_max_ms(e0.elapsed_time(e1) / args.steps, dev, ws) / 1e3)
             assert torch.equal(hidx, out_idx.cpu()), "host-buffer path disagrees with device path"
         cand = stats["candidates"].numpy().astype(np.float64)
         refined = stats["refined"].numpy().astype(np.float64)
@@ -396,15 +488,13 @@ def run_gpu(args):
             v["share"] = v["ms_per_step"] / tot
         alg = {
             # SAX bytes per pass + 8 B per candidate written
-            "lb_pass": (nbatches * n * W + 8.0 * cand.sum()) / nbatches,
+            "lb_pass": (nbatches * n_local * W + 8.0 * cand.sum()) / nbatches,
             # raw bytes per refined series (K6): fp32 rows + the bf16 rows of the pre-filter
             "refine": (4.0 * length * refined.sum()
                        + 2.0 * length * stats["raw16_rows"].numpy().astype(np.float64).sum()) / nbatches,
             # nb-ParIS+ workers: the SAX array + the raw series they read
-            "nb_distcomp": (nbatches * n * W + 4.0 * length * refined.sum()) / nbatches,
+            "nb_distcomp": (nbatches * n_local * W + 4.0 * length * refined.sum()) / nbatches,
         }
-        # per-batch algorithmic amounts against the kernel's device time per batch (the k = 1
-        # refine is two launches per batch -- two LB-ordered waves -- so time is summed per batch)
         for name, v in kern.items():
             v["launch_ms"] = v["ms_per_step"] * args.steps / prof[name][0]
             v["ms_per_batch"] = v["ms_per_step"] / nbatches
@@ -414,38 +504,37 @@ def run_gpu(args):
         roof = None
         if dom:
             per_launch_ms = kern[dom]["ms_per_batch"]
-            pk = 148 * 64 * 2 * ALU_CLOCK_GHZ * 1e9 / 1e12
-            alu_src = f"derived: 148 SM x 64 FMA lanes/clk x 2 (f16x2) x {ALU_CLOCK_GHZ} GHz"
-            if dom == "lb_pass" and use_index:
+            pk_derived = 148 * 64 * 2 * ALU_CLOCK_GHZ * 1e9 / 1e12
+            alu = {"peak": fma_peak, "peak_source": "measured in this run: paris_debug_hfma2_probe (8 independent "
+                   "fma.rn.f16x2 chains per thread, 4 CTAs x 512 threads per SM)",
+                   "peak_derived": pk_derived,
+                   "peak_derived_source": f"148 SM x 64 FMA lanes/clk x 2 (f16x2) x {ALU_CLOCK_GHZ} GHz"}
+            if dom == "lb_pass" and use_idx:
                 # index path: the algorithmic work is the (block, query) pairs whose envelope
-                # bound passed (stats lb_blocks) x PARIS_INDEX_BLOCK series x w segments x 3 FMA-pipe half-ops
+                # bound passed (stats lb_blocks) x PARIS_INDEX_BLOCK series x w segments x 3 fp16
+                # FMA-pipe ops (the minimal fp16x2 MINDIST form: two relu-FMAs + one FMA)
                 blocks = stats["lb_blocks"].numpy().astype(np.float64).sum()
                 ops = 3.0 * W * P.PARIS_INDEX_BLOCK * blocks / nbatches
                 ach = ops / (per_launch_ms / 1e3) / 1e12
-                roof = {"kernel": dom, "bound": "alu", "achieved": ach, "peak": pk,
-                        "unit": "Tops/s (fp16x2 half-ops)", "frac": ach / pk,
-                        "traffic": ncu_traffic(dom + "_index", args.config),
-                        "algorithmic_ops_per_batch": ops, "ms_per_batch": per_launch_ms, "peak_source": alu_src,
-                        "active_block_frac": blocks / (nq * (n / P.PARIS_INDEX_BLOCK)),
-                        "hbm_achieved_gbs": alg[dom] / (per_launch_ms / 1e3) / 1e9, "hbm_peak_gbs": peak,
-                        "queries_per_pass": q_per_pass}
+                roof = dict({"kernel": dom, "bound": "alu", "achieved": ach, "unit": "Tops/s (fp16 FMA-pipe ops)",
+                             "frac": ach / fma_peak, "frac_of_derived": ach / pk_derived,
+                             "traffic": ncu_traffic(dom + "_index", args.config),
+                             "algorithmic_ops_per_batch": ops, "ms_per_batch": per_launch_ms,
+                             "active_block_frac": blocks / (nq * (n_local / P.PARIS_INDEX_BLOCK)),
+                             "hbm_achieved_gbs": alg[dom] / (per_launch_ms / 1e3) / 1e9, "hbm_peak_gbs": peak,
+                             "queries_per_pass": q_per_pass}, **alu)
             elif dom == "lb_pass" and q_per_pass > 1.5:
-                # batched fp16x2 LB: bound by the FMA pipe, not HBM: 3 half-precision
-                # FMA-pipe ops per (series, segment, query)
-                ops = 3.0 * n * W * q_per_pass
+                # batched fp16x2 LB: bound by the FMA pipe, not HBM
+                ops = 3.0 * n_local * W * q_per_pass
                 ach = ops / (per_launch_ms / 1e3) / 1e12
-                roof = {"kernel": dom, "bound": "alu", "achieved": ach, "peak": pk,
-                        "unit": "Tops/s (fp16x2 half-ops)", "frac": ach / pk,
-                        "traffic": ncu_traffic(dom, args.config),
-                        "algorithmic_ops_per_batch": ops, "ms_per_batch": per_launch_ms, "peak_source": alu_src,
-                        "hbm_achieved_gbs": alg[dom] / (per_launch_ms / 1e3) / 1e9, "hbm_peak_gbs": peak,
-                        "queries_per_pass": q_per_pass}
+                roof = dict({"kernel": dom, "bound": "alu", "achieved": ach, "unit": "Tops/s (fp16 FMA-pipe ops)",
+                             "frac": ach / fma_peak, "frac_of_derived": ach / pk_derived,
+                             "traffic": ncu_traffic(dom, args.config),
+                             "algorithmic_ops_per_batch": ops, "ms_per_batch": per_launch_ms,
+                             "hbm_achieved_gbs": alg[dom] / (per_launch_ms / 1e3) / 1e9, "hbm_peak_gbs": peak,
+                             "queries_per_pass": q_per_pass}, **alu)
             elif args.raw_host and dom in ("refine", "nb_distcomp", "seed_ed"):
-                # f3: the seeds' and candidates' raw rows cross PCIe (zero-copy reads of pinned host memory)
-                if dom == "seed_ed":
-                    byts = 4.0 * length * seed_series(n, use_index, args.index_seeds, k) * q_per_pass
-                else:
-                    byts = 4.0 * length * refined_sum_of(stats) / nbatches
+                byts = 4.0 * length * float(refined.sum()) / nbatches
                 ach = byts / (per_launch_ms / 1e3) / 1e9
                 roof = {"kernel": dom, "bound": "pcie", "achieved": ach, "peak": h2d_gbs, "unit": "GB/s",
                         "frac": ach / h2d_gbs, "traffic": None, "algorithmic_bytes_per_batch": byts,
@@ -454,7 +543,7 @@ def run_gpu(args):
             elif dom in alg:
                 ach = alg[dom] / (per_launch_ms / 1e3) / 1e9
                 roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                        "frac": ach / peak, "traffic": ncu_traffic(dom + ("_index" if use_index else ""), args.config),
+                        "frac": ach / peak, "traffic": ncu_traffic(dom + ("_index" if use_idx else ""), args.config),
                         "algorithmic_bytes_per_batch": alg[dom], "ms_per_batch": per_launch_ms,
                         "peak_source": peak_src}
         r.update(kern=kern, roof=roof, cand=cand, refined=refined, batch=b_path)
@@ -464,11 +553,11 @@ def run_gpu(args):
 
     primary = measure_path(args.path, True)
     secondary = None
-    if args.both:
+    if args.both and ws == 1:
         secondary = measure_path("flat" if args.path in ("index", "nb") else "index", False)
 
     def timed_index(qsrc, kk):
-        """q/s and pruning of the index path on a query set (events, max over ranks)."""
+        """q/s and pruning of the index path on a query set (events, one GPU)."""
         kc = P.KnnConfig(batch=args.batch or 64, index_seeds=args.index_seeds)
         _, _, stq = P.knn_index(raw, index, qsrc, k=kk, config=kc, stats=True, raw16=raw16)
         torch.cuda.synchronize()
@@ -478,16 +567,16 @@ def run_gpu(args):
                 P.knn_index(raw, index, qsrc[c0:c0 + call_q], k=kk, config=kc, raw16=raw16)
         e1.record(st)
         torch.cuda.synchronize()
-        ms = reduce_max_ms(e0.elapsed_time(e1) / args.steps, dev, ws)
+        ms = e0.elapsed_time(e1) / args.steps
         ref = stq["refined"].numpy().astype(np.float64)
-        return {"k": kk, "queries": int(qsrc.shape[0]), "value": weak_throughput(int(qsrc.shape[0]), ws, ms),
+        return {"k": kk, "queries": int(qsrc.shape[0]), "value": qsrc.shape[0] / (ms / 1e3),
                 "unit": "queries/s", "ms_per_step": ms,
                 "candidates_mean": float(stq["candidates"].numpy().astype(np.float64).mean()),
                 "refined_mean": float(ref.mean()), "pruning_ratio": float(1.0 - ref.mean() / n),
                 "raw16_rows_mean": float(stq["raw16_rows"].numpy().astype(np.float64).mean())}
 
     sweep = None
-    if index is not None and not args.no_sweep and not args.raw_host:
+    if index is not None and ws == 1 and not args.no_sweep and not args.raw_host:
         if args.config == 2:  # BASELINE config 2: exact 1-NN and k = 10
             sweep = [dict(timed_index(queries, 10), sigma=0.05)]
         elif args.config == 5:  # config 5: 5 sets x 200 member + N(0, sigma^2) queries, k = 1 and 100
@@ -506,7 +595,7 @@ def run_gpu(args):
 
     # ---- flat LB pass at one query per SAX read: the HBM-roofline configuration of K4 (SURVEY §7 hard part 1)
     lb1 = None
-    if not args.no_b1:
+    if not args.no_b1 and ws == 1:
         nq1 = min(nq, 8)
         cfg1 = P.KnnConfig(batch=1)
         knn_flat(queries[:nq1], config=cfg1)
@@ -522,7 +611,7 @@ def run_gpu(args):
             a1 = by1 / (ms1 / c1 / 1e3) / 1e9
             lb1 = {"kernel": "lb_pass", "bound": "hbm", "queries_per_pass": 1, "launch_ms": ms1 / c1,
                    "algorithmic_bytes_per_launch": by1, "achieved": a1, "peak": peak, "unit": "GB/s",
-                   "frac": a1 / peak, "queries": nq1}
+                   "frac": a1 / peak, "frac_of_read_peak": a1 / read_peak if read_peak else None, "queries": nq1}
         if "refine" in pr1:
             c1, ms1 = pr1["refine"]  # two launches (waves) per query
             by1 = 4.0 * length * float(st1["refined"].double().mean())
@@ -531,46 +620,55 @@ def run_gpu(args):
                                     "achieved": by1 / (ms1 / nq1 / 1e3) / 1e9, "peak": peak, "unit": "GB/s"}
     sum_bytes = n * (4.0 * length + W)
     summarize = {"series_per_s": n / (sum_ms / 1e3), "ms": sum_ms, "unit": "series/s",
-                 "roofline": {"kernel": "summarize", "bound": "hbm", "achieved": sum_bytes / (sum_ms / 1e3) / 1e9,
-                              "peak": peak, "unit": "GB/s", "frac": sum_bytes / (sum_ms / 1e3) / 1e9 / peak,
+                 "roofline": {"kernel": "summarize", "bound": "hbm",
+                              "achieved": n_local * (4.0 * length + W) / (sum_ms_local / 1e3) / 1e9,
+                              "peak": peak, "unit": "GB/s",
+                              "frac": n_local * (4.0 * length + W) / (sum_ms_local / 1e3) / 1e9 / peak,
                               "traffic": ncu_traffic("summarize", args.config),
-                              "algorithmic_bytes_per_launch": sum_bytes}}
+                              "algorithmic_bytes_per_launch": n_local * (4.0 * length + W)}}
+    _ = sum_bytes
     if args.raw_host:
-        # host raw: the whole call (chunked H2D copies overlapped with the kernel) is bound by PCIe
-        h2d = n * 4.0 * length
+        h2d = n_local * 4.0 * length
         summarize["roofline"] = {"kernel": "summarize (host raw, double-buffered H2D)", "bound": "pcie",
-                                 "achieved": h2d / (sum_ms / 1e3) / 1e9, "peak": h2d_gbs, "unit": "GB/s",
-                                 "frac": h2d / (sum_ms / 1e3) / 1e9 / h2d_gbs, "traffic": None,
+                                 "achieved": h2d / (sum_ms_local / 1e3) / 1e9, "peak": h2d_gbs, "unit": "GB/s",
+                                 "frac": h2d / (sum_ms_local / 1e3) / 1e9 / h2d_gbs, "traffic": None,
                                  "algorithmic_bytes_per_launch": h2d,
                                  "peak_source": "measured in this run: pinned host -> device cudaMemcpyAsync"}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        n_sample = min(n, args.ref_sample)
-        t_q = oracle_sample(raw, queries, k, n_sample, args.ref_queries)
-        cpu = {"value": 1.0 / (t_q * n / n_sample), "unit": "queries/s", "cores": 1, "kind": "oracle",
-               "sample": f"oracle_knn_pruned (1 thread, fp64) over the first {n_sample} series, "
-                         f"{args.ref_queries} queries, time scaled x{n / n_sample:.0f} to n={n}"}
+        samples = [s for s in (args.ref_sample // 4, args.ref_sample) if s > 0]
+        pts, est = oracle_scaling(raw if not args.raw_host else raw, queries, k, n, samples, args.ref_queries)
+        cpu = dict({"value": 1.0 / est, "unit": "queries/s", "cores": 1, "kind": "oracle",
+                    "sample": f"oracle_knn_pruned (1 thread pinned to one host core, fp64, its own SAX) over the "
+                              f"first {pts[-1]['n']} series, {args.ref_queries} queries, time scaled "
+                              f"x{n / pts[-1]['n']:.0f} to n={n}",
+                    "scaling_points": pts}, **host_info())
 
     if rank == 0:
         line = {
             "metric": "exact 1-NN queries/sec", "value": value, "unit": "queries/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms_max,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "strong" if sharded else "weak", "vs_baseline": None,
+            "dtype": "f32",
             "data": "synthetic (seeded Philox random walks, z-normalized; no dataset on the box)",
             "config": {"workload": cfg["desc"], "n": n, "len": length, "w": W, "card": CARD, "nq": nq, "k": k,
                        "batch": primary["batch"], "path": args.path, "index_build_ms": index_ms,
-                       "raw_bf16": None if raw16 is None else {"build_ms": raw16_ms, "bytes": raw16.numel() * 2}, "parallelism": f"weak x{ws} (independent collections + queries per GPU)",
+                       "raw_bf16": None if raw16 is None else {"build_ms": raw16_ms, "bytes": raw16.numel() * 2},
+                       "parallelism": (f"shard x{ws} by series id (tau all-reduce(min) + all-gather + exact merge)"
+                                       if sharded else f"weak x{ws} (independent collections + queries per GPU)"),
                        "l2": "inputs larger than L2 (no flush)",
-                       "raw": "pinned host memory (f3)" if args.raw_host else "HBM"},
+                       "raw": "pinned host memory (f3)" if args.raw_host else "HBM",
+                       "lib_sha16": lib_sha16()},
             "roofline": dict(roof, read_peak_gbs=read_peak,
                              frac_of_read_peak=(roof["achieved"] / read_peak
                                                 if read_peak and roof and roof.get("unit") == "GB/s" else None))
                         if roof else roof,
+            "spread": primary["spread"],
             "lb_batch1": lb1,
             "other_path": None if secondary is None else {
                 "path": secondary["path"], "value": secondary["value"], "ms_per_step": secondary["step_ms"],
-                "roofline": secondary["roof"], "kernels": secondary["kern"],
+                "spread": secondary["spread"], "roofline": secondary["roof"], "kernels": secondary["kern"],
                 "candidates_mean": float(secondary["cand"].mean()), "refined_mean": float(secondary["refined"].mean())},
             "cpu_baseline": cpu,
             "sweep": sweep,
@@ -583,97 +681,16 @@ def run_gpu(args):
             "pruning": {"candidates_mean": float(cand.mean()), "candidates_p50": float(np.median(cand)),
                         "candidates_max": float(cand.max()), "refined_mean": float(refined.mean()),
                         "refined_max": float(refined.max()),
-                        "pruning_ratio": float(1.0 - refined.mean() / n),
+                        "pruning_ratio": float(1.0 - refined.mean() / n_local),
                         "tau_seed_mean": float(stats["tau_seed"].mean()),
-                        "lb_blocks_frac_p50": float(np.median(stats["lb_blocks"].numpy())) / max(1.0, n / P.PARIS_INDEX_BLOCK),
-                        "lb_blocks_frac_max": float(stats["lb_blocks"].numpy().max()) / max(1.0, n / P.PARIS_INDEX_BLOCK),
-                        "lb_blocks_frac_mean": float(stats["lb_blocks"].numpy().mean()) / max(1.0, n / P.PARIS_INDEX_BLOCK),
-                        "lb_blocks_top5_share": float(np.sort(stats["lb_blocks"].numpy())[-5:].sum()
-                                                      / max(1, stats["lb_blocks"].numpy().sum())),
+                        "lb_blocks_frac_p50": float(np.median(stats["lb_blocks"].numpy())) / max(1.0, n_local / P.PARIS_INDEX_BLOCK),
+                        "lb_blocks_frac_max": float(stats["lb_blocks"].numpy().max()) / max(1.0, n_local / P.PARIS_INDEX_BLOCK),
+                        "lb_blocks_frac_mean": float(stats["lb_blocks"].numpy().mean()) / max(1.0, n_local / P.PARIS_INDEX_BLOCK),
                         "refined_top5_share": float(np.sort(refined)[-5:].sum() / max(1.0, refined.sum())),
                         "bsf_updates_mean": primary.get("bsf_updates_mean"),
-                        "raw16_rows_mean": float(stats["raw16_rows"].numpy().astype(np.float64).mean())},
+                        "raw16_rows_mean": float(stats["raw16_rows"].numpy().astype(np.float64).mean()),
+                        "note": "rank 0's shard" if ws > 1 and sharded else None},
         }
-        print(json.dumps(line), flush=True)
-    if ws > 1:
-        dist.destroy_process_group()
-    return 0
-
-
-def run_gpu_sharded(args):
-    """--shard: ONE collection of the config's size split by id range across the ranks
-    (strong scaling); every query batch is searched per shard and merged exactly with one
-    all-gather of the per-rank rows + paris_merge_topk."""
-    import numpy as np
-    import torch
-    import torch.distributed as dist
-
-    import paper_2009_00166_b200 as P
-    from paper_2009_00166_b200 import parallel as par
-    from datagen import gpu as dg
-    import datagen
-
-    ws, rank, local = dist_env()
-    if ws > 1:
-        dist.init_process_group("nccl")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    cfg = CONFIGS[args.config]
-    n, length, nq, k = cfg["n"], cfg["len"], cfg["nq"], cfg["k"]
-    if args.n:
-        n = args.n
-    if args.nq:
-        nq = args.nq
-    call_q = cfg.get("call", nq)
-    ds, qs = datagen.config_seeds(args.config)
-    lo, hi = par.shard_range(n, rank, ws)
-    raw = dg.walks(hi - lo, length, ds, first_id=lo, device=dev)        # this rank's ids [lo, hi)
-    if cfg["queries"] == "fresh":
-        queries = dg.walks(nq, length, qs, device=dev)
-    else:
-        full_src = torch.empty(0)  # member queries need their source rows: generate them by id
-        src = datagen.member_ids(nq, n, qs)
-        base = torch.stack([dg.walks(1, length, ds, first_id=int(s_), device=dev)[0] for s_ in src])
-        queries, _ = dg.noisy_members(base, nq, float(cfg["queries"][5:]), qs)
-        del full_src
-    sax = P.summarize(raw, W, CARD)
-    index = P.index_build(sax, W, CARD)
-    local_fn = par.local_index_search(raw, index, config=P.KnnConfig(index_seeds=args.index_seeds))
-    torch.cuda.synchronize()
-
-    def step():
-        outs = []
-        for c0 in range(0, nq, call_q):
-            outs.append(par.knn_sharded(queries[c0:c0 + call_q], k, lo, local_fn))
-        return outs
-
-    for _ in range(max(3, args.warmup)):
-        step()
-    torch.cuda.synchronize()
-    st = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if ws > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clocks:
-        e0.record(st)
-        for _ in range(args.steps):
-            step()
-        e1.record(st)
-        torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
-    ms = reduce_max_ms(e0.elapsed_time(e1) / args.steps, dev, ws)
-    value = nq / (ms / 1e3)
-    if rank == 0:
-        line = {"metric": "exact 1-NN queries/sec", "value": value, "unit": "queries/s", "n_gpus": ws,
-                "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-                "data": "synthetic (seeded Philox random walks, z-normalized; no dataset on the box)",
-                "config": {"workload": cfg["desc"], "n": n, "len": length, "w": W, "card": CARD, "nq": nq, "k": k,
-                           "path": "index, sharded by id range + all-gather + paris_merge_topk",
-                           "parallelism": f"shard x{ws}", "l2": "inputs larger than L2 (no flush)"},
-                "clocks": clocks.summary()}
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
@@ -696,9 +713,10 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="override n (debug only)")
     ap.add_argument("--nq", type=int, default=0, help="override query count (debug only)")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--shard", action="store_true",
-                    help="one collection split across the ranks (strong scaling, exact merge) instead of one "
-                         "collection per rank (weak scaling)")
+    ap.add_argument("--weak", action="store_true",
+                    help="one collection of the config's size per rank (weak scaling) instead of one collection "
+                         "sharded over the ranks (the default, strong scaling)")
+    ap.add_argument("--shard", action="store_true", help="(default) one collection sharded over the ranks")
     ap.add_argument("--no-b1", action="store_true", help="skip the batch-1 LB roofline measurement")
     ap.add_argument("--sorted-refine", action="store_true",
                     help="k = 1: refine bucket-sorted lists (K5 scatter) instead of the unsorted waves (A/B)")
@@ -714,8 +732,6 @@ def main():
     args.warmup = max(args.warmup, 3) if args.impl == "paris" else args.warmup
     if args.impl == "reference":
         return run_reference(args)
-    if args.shard:
-        return run_gpu_sharded(args)
     return run_gpu(args)
 
 

@@ -1154,17 +1154,20 @@ struct LbiWarp {
   unsigned n;
   unsigned pad[3];
 };
+constexpr int kMaxItems = kBPT * (kMaxB / 2);  // items of a tile: 32 blocks x up to 32 slot pairs
 struct LbiMisc {
   uint64_t full[4], empty[4];
   int64_t tile[4];
-  unsigned next[4];
-  unsigned pad[4];
-  unsigned long long bm[4][kBPT];
+  unsigned next[4];    // per stage: the next unclaimed item pair
+  unsigned nitems[4];  // per stage: items of its tile
   LbConsts c;
   LbiWarp w[kIWarps];
+  // per stage: the tile's items, decoded by the producer from the block masks:
+  // block | slot a << 8 | slot b << 16 (0xFF: none)
+  uint32_t items[4][kMaxItems];
 };
 constexpr size_t kIMiscBytes = (sizeof(LbiMisc) + 127) & ~(size_t)127;
-static_assert(kTileBytes + kIMiscBytes + 4096 <= 65536, "stage 0 + misc must fit below the table");
+static_assert(kTileBytes + kIMiscBytes + 2048 <= 65536, "stage 0 + misc must fit below the table");
 
 __device__ __forceinline__ uint32_t hole_addr(uint32_t T, int h) { return T + 256u * (uint32_t)h + 128u; }
 __device__ __forceinline__ uint32_t lbi_key_addr(uint32_t T, int warp, int e) {
@@ -1266,16 +1269,22 @@ __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int s
   if (!__any_sync(0xffffffffu, pf != 0u)) return;
   uint32_t pm = 0;  // bit 2j+h: series j passes for slot h
   float lbv[4][2];
-  if (pf) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+  for (int q = 0; q < 8; ++q) lbv[q >> 1][q & 1] = 0.f;
+  for (uint32_t r = pf; r; r &= r - 1) {  // the fp32 bound only for the lane's passing pairs
+    const int bit = __ffs(r) - 1;
+    const int jj = bit >> 1;  // explicit selects: no dynamic register indexing
+    uint32_t v = acc[0];
+    v = jj == 1 ? acc[1] : v;
+    v = jj == 2 ? acc[2] : v;
+    v = jj == 3 ? acc[3] : v;
+    const float hv = (bit & 1) ? h_hi_f(v) : h_lo_f(v);
+    const float lb = __fmul_rd(fmaxf(__fsub_rd(hv, c.wabs), 0.f), c.lbconv);
+    if (lb <= c.thr[(bit & 1) ? sb : sa]) {
+      pm |= 1u << bit;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int sl = h ? sb : sa;
-        const float hv = h ? h_hi_f(acc[j]) : h_lo_f(acc[j]);
-        lbv[j][h] = __fmul_rd(fmaxf(__fsub_rd(hv, c.wabs), 0.f), c.lbconv);
-        if (((pf >> (2 * j + h)) & 1u) && lbv[j][h] <= c.thr[sl]) pm |= 1u << (2 * j + h);
-      }
+      for (int q = 0; q < 8; ++q)
+        if (q == bit) lbv[q >> 1][q & 1] = lb;
     }
   }
   if (!__any_sync(0xffffffffu, pm != 0u)) return;
@@ -1490,21 +1499,52 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
   lb_consts_init(a, nslots, &M.c);  // ends with __syncthreads
 
   if (warp == kIWarps) {
-    // ---- producer: refill stage st as soon as every consumer warp released it
-    if (lane == 0) {
-      int64_t li = blockIdx.x;
-      unsigned tnext = li < nlist ? __ldg(tile_list + li) : 0u;
-      for (int64_t it = 0; li < nlist; ++it, li += gridDim.x) {
-        const int st = (int)(it % NST);
-        const unsigned tile = tnext;
-        if (li + gridDim.x < nlist) tnext = __ldg(tile_list + li + gridDim.x);  // the next id, early
-        if (it >= NST) mbar_wait(&M.empty[st], (unsigned)(((it / NST) - 1) & 1));
+    // ---- producer: refill stage st as soon as every consumer warp released it.  The
+    // whole warp decodes the tile's 32 block masks (lane = block; read from global one tile
+    // ahead) into the stage's item list -- a block's live query slots paired in order,
+    // consecutive live slots forming an item -- so the consumers claim ready items.
+    int64_t li = blockIdx.x;
+    unsigned tnext = 0;
+    uint64_t bnext = 0;
+    if (li < nlist) {
+      tnext = __ldg(tile_list + li);
+      bnext = __ldg(bmask + (size_t)tnext * kBPT + lane);
+    }
+    for (int64_t it = 0; li < nlist; ++it, li += gridDim.x) {
+      const int st = (int)(it % NST);
+      const unsigned tile = tnext;
+      uint64_t m = bnext;
+      if (li + gridDim.x < nlist) {  // the next tile's id and masks, early
+        tnext = __ldg(tile_list + li + gridDim.x);
+        bnext = __ldg(bmask + (size_t)tnext * kBPT + lane);
+      }
+      if (it >= NST) mbar_wait(&M.empty[st], (unsigned)(((it / NST) - 1) & 1));
+      const int cnt = (__popcll(m) + 1) >> 1;
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      uint32_t* out = M.items[st] + (incl - cnt);
+      for (int i = 0; i < cnt; ++i) {
+        const uint32_t sa = (uint32_t)__ffsll((long long)m) - 1u;
+        m &= m - 1;
+        const uint32_t sb = m ? (uint32_t)__ffsll((long long)m) - 1u : 0xFFu;
+        m &= m - 1;
+        out[i] = (uint32_t)lane | (sa << 8) | (sb << 16);
+      }
+      __threadfence_block();
+      if (lane == 31) {
+        M.nitems[st] = (unsigned)incl;
         M.tile[st] = tile;
         M.next[st] = 0;
+      }
+      __syncwarp();
+      if (lane == 31) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&M.full[st], (unsigned)(kTileBytes + kBPT * 8));
+        mbar_expect_tx(&M.full[st], (unsigned)kTileBytes);  // release: the items are visible to the waiters
         bulk_g2s(gbase + stage_addr(st), a.sax + (size_t)tile * kTileBytes, (unsigned)kTileBytes, &M.full[st]);
-        bulk_g2s(&M.bm[st][0], bmask + (size_t)tile * kBPT, (unsigned)(kBPT * 8), &M.full[st]);
       }
     }
   } else {
@@ -1520,17 +1560,7 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
       mbar_wait(&M.full[st], (unsigned)((it / NST) & 1));
       const int64_t tile = M.tile[st];
       PARIS_DCHECK(tile >= 0 && tile * kTS < a.n);
-      // the tile's 32 block masks (lane = block); a block's live slots are evaluated two
-      // at a time (an item); a 64-series block is half a warp, so a warp claims two items
-      const uint64_t bm = M.bm[st][lane];
-      const int cnt = (__popcll(bm) + 1) >> 1;
-      int incl = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      const int total = (int)M.nitems[st];
       const uint32_t rows = stage_addr(st);
       for (;;) {
         unsigned cl = 0;
@@ -1538,21 +1568,11 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
         const int t0 = (int)__shfl_sync(0xffffffffu, cl, 0);
         if (t0 >= total) break;
         const int t = t0 + h;  // this half-warp's item
-        const unsigned m0 = __ballot_sync(0xffffffffu, incl <= t0);
-        const unsigned m1 = __ballot_sync(0xffffffffu, incl <= t0 + 1);
         const bool active = t < total;
-        const int k = active ? __popc(h ? m1 : m0) : 0;
-        const int excl = __shfl_sync(0xffffffffu, incl - cnt, k);
-        const uint64_t bmk = __shfl_sync(0xffffffffu, (unsigned long long)bm, k);
-        // slots 2r+1 and 2r+2 (1-based) of the block's live set: clear the first 2r bits
-        uint64_t m = active ? bmk : 0ull;
-        for (int i = t - excl; i > 0; --i) {
-          m &= m - 1;
-          m &= m - 1;
-        }
-        const int sa = m ? __ffsll((long long)m) - 1 : 0;
-        m &= m - 1;
-        const int sb = (active && m) ? __ffsll((long long)m) - 1 : -1;
+        const uint32_t item = M.items[st][active ? t : t0];
+        const int k = (int)(item & 31u);
+        const int sa = (int)((item >> 8) & 0xFFu);
+        const int sb = active && ((item >> 16) & 0xFFu) != 0xFFu ? (int)((item >> 16) & 0xFFu) : -1;
         const int sq = sb >= 0 ? sb : sa;  // odd count: duplicate lane, masked in emission
         // single-query form per slot (as k_lb1): one lookup t = (-U16, L16) serves both
         // slots; d = relu(q2 + t) = (relu(q_lo - U), relu(L - q_hi)) and acc += d^2 keep the
@@ -1582,14 +1602,16 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
             }
           }
         }
-        // LB16 per (series, slot) = ABOVE + BELOW sums (fp32 add, rounded up to fp16 -- the
-        // single-query form inside k_lb's error budget), packed (slot sa low, sb high)
+        // LB16 per (series, slot) = ABOVE + BELOW sums, one packed fp16 add for both slots
+        // (slot sa low, sb high); its rounding is one more (1+u) factor inside k_lb's error
+        // budget G = (1+u)^(w+4), and only LB16's upper bound enters the tests
         uint32_t acc[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const uint32_t la = __half_as_ushort(__float2half_ru(h_lo_f(acca[j]) + h_hi_f(acca[j])));
-          const uint32_t lb = __half_as_ushort(__float2half_ru(h_lo_f(accb[j]) + h_hi_f(accb[j])));
-          acc[j] = la | (lb << 16);
+          const uint32_t above = __byte_perm(acca[j], accb[j], 0x5410), below = __byte_perm(acca[j], accb[j], 0x7632);
+          uint32_t sum;
+          asm("add.rn.f16x2 %0, %1, %2;" : "=r"(sum) : "r"(above), "r"(below));
+          acc[j] = sum;
         }
         const int64_t i0 = tile * kTS + k * PARIS_INDEX_BLOCK + 4 * hl;
         const int nvalid = active ? (int)std::max<int64_t>(0, imin64(4, a.n - i0)) : 0;

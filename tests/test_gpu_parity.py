@@ -258,3 +258,21 @@ def test_knn_overflow_fallback_shapes(P, torch_dev, n, w, length, k):
     gi, gd = _knn_case(P, torch_dev, x, q, k, w=w, config=p.KnnConfig(cap=16, seed_div=n))
     ri, rd2 = oracle.knn_bruteforce(x, q, k)
     check_knn(x, q, gi, gd, ri, rd2)
+
+
+def test_gpu_member_queries_by_id(torch_dev):
+    """Sharded benches build member queries from rows generated by id: identical to
+    noisy_members over the whole collection."""
+    from datagen import gpu
+    import __graft_entry__ as ge
+    ge.build()
+    xd = gpu.walks(5000, 128, 31)
+    a, src_a = gpu.noisy_members(xd, 12, 0.1, 32)
+    b, src_b = gpu.member_queries(5000, 128, 31, 12, 0.1, 32)
+    assert np.array_equal(src_a, src_b)
+    assert torch_equal(a, b)
+
+
+def torch_equal(a, b):
+    import torch
+    return bool(torch.equal(a, b))
