@@ -65,6 +65,31 @@ int paris_summarize(const float* raw, int64_t n, int32_t len, int32_t w, int32_t
                     uint8_t* out_sax, void* stream);
 
 /*
+ * paris_summarize_file -- paris_summarize of a raw collection stored in a FILE (the paper's
+ * setting: raw data on disk, index construction reading it sequentially):
+ * n rows of len fp32 starting at byte `offset` of `path`.  A reader thread preads 256 MB
+ * chunks into three pinned host buffers while the calling thread copies each chunk to a
+ * device staging buffer and summarizes it (the Coordinator's double buffer); direct_io != 0
+ * asks for O_DIRECT (the disk's own bandwidth, no page cache; needs offset % 4096 == 0,
+ * else buffered reads).  out_bf16 (optional, device [n][len] bf16 bits, len % 8 == 0): the
+ * bf16 copy of paris_raw_bf16 built from the same staged chunks.  Returns once the whole
+ * file has been read (results valid when `stream` completes).  PARIS_EINVAL for an
+ * unreadable or short file.
+ */
+int paris_summarize_file(const char* path, int64_t offset, int64_t n, int32_t len, int32_t w, int32_t card,
+                         uint8_t* out_sax, uint16_t* out_bf16, int32_t direct_io, void* stream);
+
+/*
+ * paris_map_raw_file / paris_unmap_raw_file -- map `bytes` of a raw file (from a page-aligned
+ * `offset`) read-only and register the mapping with CUDA (cudaHostRegisterReadOnly; its
+ * pages are pinned, so the file must fit in host RAM): *out_ptr is then a host raw pointer
+ * the k-NN calls accept -- the candidates' rows are read straight from the
+ * file's pages over PCIe (the RDC workers' random reads of the raw file).
+ */
+int paris_map_raw_file(const char* path, int64_t offset, int64_t bytes, void** out_ptr);
+int paris_unmap_raw_file(void* ptr, int64_t bytes);
+
+/*
  * paris_knn_exact -- exact k-NN under Euclidean distance (k-NN per
  * S:406-414) following ParIS+ ExactSearch (Alg9):
  *   1. BSF seed (approximate search analog, R8): the lower bound over

@@ -76,6 +76,12 @@ def load():
         P, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
         lib.paris_summarize.argtypes = [P, i64, i32, i32, i32, P, P]
         lib.paris_summarize.restype = ctypes.c_int
+        lib.paris_summarize_file.argtypes = [ctypes.c_char_p, i64, i64, i32, i32, i32, P, P, i32, P]
+        lib.paris_summarize_file.restype = ctypes.c_int
+        lib.paris_map_raw_file.argtypes = [ctypes.c_char_p, i64, i64, ctypes.POINTER(ctypes.c_void_p)]
+        lib.paris_map_raw_file.restype = ctypes.c_int
+        lib.paris_unmap_raw_file.argtypes = [P, i64]
+        lib.paris_unmap_raw_file.restype = ctypes.c_int
         lib.paris_knn_exact.argtypes = [P, P, i64, P, i32, i32, P, P, i32, i32, i32, P]
         lib.paris_knn_exact.restype = ctypes.c_int
         lib.paris_knn_exact_ex.argtypes = [P, P, i64, P, i32, i32, P, P, i32, i32, i32, P,
@@ -178,6 +184,48 @@ def summarize(raw: torch.Tensor, w: int = 16, card: int = 256, out: torch.Tensor
         raise ValueError("out must be uint8 with n*w elements")
     _check(lib.paris_summarize(raw.data_ptr(), n, length, w, card, out.data_ptr(), _stream(stream)))
     return out
+
+
+def summarize_file(path: str, n: int, length: int, w: int = 16, card: int = 256, offset: int = 0,
+                   out: torch.Tensor | None = None, bf16: bool = False, direct_io: bool = False, stream=None):
+    """paris_summarize_file: PAA + iSAX of n rows of `length` fp32 stored in a file (from byte
+    `offset`) -> uint8 [w][n] on the current CUDA device; with bf16=True also the [n][len]
+    bf16 copy (paris_raw_bf16 of the same rows).  Returns sax, or (sax, raw16)."""
+    lib = load()
+    if out is None:
+        out = torch.empty((w, n), dtype=torch.uint8, device="cuda")
+    _need_cuda(out, "out")
+    r16 = torch.empty((n, length), dtype=torch.int16, device=out.device) if bf16 else None
+    _check(lib.paris_summarize_file(os.fsencode(path), int(offset), int(n), int(length), int(w), int(card),
+                                    out.data_ptr(), r16.data_ptr() if bf16 else None, 1 if direct_io else 0,
+                                    _stream(stream)))
+    return (out, r16) if bf16 else out
+
+
+class MappedRaw:
+    """A raw file mapped read-only and registered with CUDA (paris_map_raw_file): `.tensor` is
+    a [n][len] fp32 host tensor the k-NN calls accept as raw (pinned).  close() unmaps."""
+
+    def __init__(self, path: str, n: int, length: int, offset: int = 0):
+        lib = load()
+        self.bytes = int(n) * int(length) * 4
+        ptr = ctypes.c_void_p()
+        _check(lib.paris_map_raw_file(os.fsencode(path), int(offset), self.bytes, ctypes.byref(ptr)))
+        self.ptr = ptr.value
+        buf = (ctypes.c_char * self.bytes).from_address(self.ptr)
+        self.tensor = torch.frombuffer(buf, dtype=torch.float32).view(n, length)
+
+    def close(self):
+        if self.ptr:
+            self.tensor = None
+            load().paris_unmap_raw_file(self.ptr, self.bytes)
+            self.ptr = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
 
 
 PARIS_INDEX_BLOCK = 64

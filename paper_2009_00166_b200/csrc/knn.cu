@@ -1217,11 +1217,6 @@ __device__ void lbi_flush(LbiWarp& wb, uint32_t T, int warp, int nslots, const L
   __syncwarp();
   const int m = (int)wb.n;
   if (m == 0) return;
-  for (int b = lane; b < nslots; b += 32) {
-    const unsigned k = wb.cnt[b];
-    wb.cnt[b] = k ? atomicAdd(&a.count[b], k) : 0u;
-  }
-  __syncwarp();
   static_assert(kWBI == 64, "two entries per lane");
   uint64_t key[2];
   uint32_t id[2];
@@ -1232,7 +1227,14 @@ __device__ void lbi_flush(LbiWarp& wb, uint32_t T, int warp, int nslots, const L
     key[r] = e < m ? lds_u64(lbi_key_addr(T, warp, e)) : kNoKey;
     sl[r] = e < m ? wb.slot[e] : 0;
     id[r] = e < m ? __ldg(a.perm + key_id(key[r])) : 0u;
+    if (e < m) atomicAdd(&wb.cnt[sl[r]], 1u);  // per-slot counts, here rather than per emission
   }
+  __syncwarp();
+  for (int b = lane; b < nslots; b += 32) {
+    const unsigned k = wb.cnt[b];
+    wb.cnt[b] = k ? atomicAdd(&a.count[b], k) : 0u;
+  }
+  __syncwarp();
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
     if (lane + 32 * r >= m) continue;
@@ -1289,13 +1291,7 @@ __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int s
   }
   if (!__any_sync(0xffffffffu, pm != 0u)) return;
   const int cntl = __popc(pm);
-  int incl = cntl;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  const int total = (int)__reduce_add_sync(0xffffffffu, (unsigned)cntl);
   if ((int)wb.n + total > kWBI) lbi_flush<HC>(wb, T, warp, nslots, c, a, hist16);
   if (total > kWBI) {  // degenerate (e.g. tau = inf): straight to global memory
 #pragma unroll
@@ -1311,7 +1307,9 @@ __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int s
     }
     return;
   }
-  int pos = (int)wb.n + incl - cntl;
+  // a lane's entries at consecutive positions reserved with one shared atomic (per-slot
+  // counts are taken at flush time)
+  int pos = cntl ? (int)atomicAdd(&wb.n, (unsigned)cntl) : 0;
   for (uint32_t r = pm; r; r &= r - 1) {
     const int bit = __ffs(r) - 1;
     const int j = bit >> 1, sl = (bit & 1) ? sb : sa;
@@ -1324,20 +1322,6 @@ __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int s
     wb.slot[pos] = (uint8_t)sl;
     ++pos;
   }
-  // per-slot counts: summed over each half-warp (its item has slots sa, sb), one shared
-  // atomic per (half, slot) instead of one per candidate
-  int na = __popc(pm & 0x55u), nbb = __popc(pm & 0xAAu);
-#pragma unroll
-  for (int o = 8; o > 0; o >>= 1) {
-    na += __shfl_xor_sync(0xffffffffu, na, o);
-    nbb += __shfl_xor_sync(0xffffffffu, nbb, o);
-  }
-  if ((lane & 15) == 0) {
-    if (na) atomicAdd(&wb.cnt[sa], (unsigned)na);
-    if (nbb) atomicAdd(&wb.cnt[sb], (unsigned)nbb);
-  }
-  __syncwarp();
-  if (lane == 31) wb.n += total;
   __syncwarp();
 }
 

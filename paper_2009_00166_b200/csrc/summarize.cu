@@ -660,6 +660,17 @@ __global__ void __launch_bounds__(256) k_raw_bf16(const float4* __restrict__ raw
 }  // namespace
 }  // namespace paris
 
+namespace paris {
+int raw_bf16_launch(const float* raw, int64_t n, int len, uint16_t* out, cudaStream_t st) {
+  const int64_t n8 = n * (int64_t)len / 8;
+  const int grid = (int)std::min<int64_t>((n8 + 255) / 256, (int64_t)sm_count() * 16);
+  PARIS_CHECK_LAUNCH(PARIS_LAUNCH("raw_bf16", k_raw_bf16, grid, 256, 0, st, reinterpret_cast<const float4*>(raw), n8,
+                                  reinterpret_cast<uint4*>(out)),
+                     "raw_bf16 launch");
+  return PARIS_OK;
+}
+}  // namespace paris
+
 extern "C" int paris_raw_bf16(const float* raw, int64_t n, int32_t len, uint16_t* out, void* stream) {
   if (!raw || !out || n < 1 || len < 8 || (len % 8) || (reinterpret_cast<uintptr_t>(raw) & 15) ||
       (reinterpret_cast<uintptr_t>(out) & 15)) {
@@ -667,15 +678,202 @@ extern "C" int paris_raw_bf16(const float* raw, int64_t n, int32_t len, uint16_t
                      (long long)n, len);
     return PARIS_EINVAL;
   }
-  const int64_t n8 = n * (int64_t)len / 8;
-  const int grid = (int)std::min<int64_t>((n8 + 255) / 256, (int64_t)paris::sm_count() * 16);
-  PARIS_CHECK_LAUNCH(PARIS_LAUNCH("raw_bf16", paris::k_raw_bf16, grid, 256, 0, (cudaStream_t)stream,
-                                  reinterpret_cast<const float4*>(raw), n8, reinterpret_cast<uint4*>(out)),
-                     "raw_bf16 launch");
-  return PARIS_OK;
+  return paris::raw_bf16_launch(raw, n, len, out, (cudaStream_t)stream);
 }
 
 extern "C" int paris_summarize(const float* raw, int64_t n, int32_t len, int32_t w, int32_t card,
                                uint8_t* out_sax, void* stream) {
   return paris::summarize_impl(raw, n, len, w, card, out_sax, (cudaStream_t)stream);
+}
+
+// ---------------------------------------------------------------- raw data in a file (f3)
+// The paper's setting: the raw collection is a file on disk and index construction reads
+// it sequentially (IndexBulkLoading's Coordinator fills one half of the double-buffered
+// raw data buffer while the workers summarize the other).  Here a
+// reader thread preads chunks into three pinned host buffers; the calling thread copies
+// each chunk to a device staging buffer (copy stream) and summarizes it there (plus,
+// optionally, its bf16 copy for paris_knn_index_x); a pinned buffer is re-read only once
+// its copy completed.  O_DIRECT (page-cache bypass: the disk's own bandwidth) when the
+// file system allows it, buffered reads otherwise.
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <condition_variable>
+#include <mutex>
+#include <thread>
+
+namespace paris {
+int raw_bf16_launch(const float* raw, int64_t n, int len, uint16_t* out, cudaStream_t st);
+
+static int summarize_file_impl(const char* path, int64_t offset, int64_t n, int len, int w, int card,
+                               uint8_t* out_sax, uint16_t* out_bf16, int direct_io, cudaStream_t st) {
+  const CardTables* tab = device_tables(card);
+  if (!tab) return PARIS_ECONFIG;
+  const size_t row = (size_t)len * 4;
+  size_t cbytes = kHostChunkBytes;
+  if (const char* ev = getenv("PARIS_HOST_CHUNK_BYTES")) {  // test hook: force many chunks
+    const long long v = atoll(ev);
+    if (v > 0) cbytes = (size_t)v;
+  }
+  int64_t chunk = std::max<int64_t>(16, ((int64_t)(cbytes / row)) / 16 * 16);
+  chunk = std::min<int64_t>(chunk, (n + 15) / 16 * 16);
+  const size_t cb = (size_t)chunk * row;
+  int fd = -1;
+  bool odirect = false;
+  if (direct_io && (offset % 4096) == 0 && (cb % 4096) == 0) {
+    fd = open(path, O_RDONLY | O_DIRECT);
+    odirect = fd >= 0;
+  }
+  if (fd < 0) fd = open(path, O_RDONLY);
+  if (fd < 0) {
+    set_error("paris_summarize_file: cannot open %s", path);
+    return PARIS_EINVAL;
+  }
+  struct stat sb;
+  if (fstat(fd, &sb) != 0 || (int64_t)sb.st_size < offset + n * (int64_t)row) {
+    close(fd);
+    set_error("paris_summarize_file: %s holds fewer than n=%lld rows of %d floats after offset %lld", path,
+              (long long)n, len, (long long)offset);
+    return PARIS_EINVAL;
+  }
+  if (!odirect) posix_fadvise(fd, offset, n * (int64_t)row, POSIX_FADV_SEQUENTIAL);
+  constexpr int NB = 3;  // pinned read buffers: the reader runs up to two chunks ahead
+  void* hb[NB] = {nullptr, nullptr, nullptr};
+  float* db[2] = {nullptr, nullptr};
+  cudaStream_t cs = nullptr;
+  cudaEvent_t copied[NB] = {nullptr, nullptr, nullptr}, dcopied[2] = {nullptr, nullptr},
+              consumed[2] = {nullptr, nullptr};
+  cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+  for (int i = 0; i < NB && e == cudaSuccess; ++i) {
+    e = cudaHostAlloc(&hb[i], cb, cudaHostAllocDefault);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming);
+  }
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    e = cudaEventCreateWithFlags(&consumed[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&dcopied[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaMallocAsync((void**)&db[i], cb, st);
+  }
+  if (e == cudaSuccess) e = cudaEventRecord(consumed[0], st);
+  if (e == cudaSuccess) e = cudaEventRecord(consumed[1], st);
+  const int64_t nchunks = (n + chunk - 1) / chunk;
+  // reader thread: chunk c into hb[c % NB] once the H2D copy of chunk c - NB is done
+  std::mutex mu;
+  std::condition_variable cv;
+  int64_t ready = 0;       // chunks read
+  bool failed = false;
+  std::thread reader;
+  if (e == cudaSuccess) {
+    reader = std::thread([&]() {
+      for (int64_t c = 0; c < nchunks; ++c) {
+        {
+          std::lock_guard<std::mutex> lk(mu);
+          if (failed) return;  // the consumer gave up
+        }
+        if (c >= NB && cudaEventSynchronize(copied[c % NB]) != cudaSuccess) { std::lock_guard<std::mutex> lk(mu); failed = true; cv.notify_all(); return; }
+        const size_t want = (size_t)std::min<int64_t>(chunk, n - c * chunk) * row;
+        const size_t rd = odirect ? ((want + 4095) & ~(size_t)4095) : want;  // O_DIRECT: whole blocks
+        size_t got = 0;
+        while (got < want) {
+          const ssize_t r = pread(fd, (char*)hb[c % NB] + got, rd - got, offset + (off_t)(c * chunk * row + got));
+          if (r <= 0) { std::lock_guard<std::mutex> lk(mu); failed = true; cv.notify_all(); return; }
+          got += (size_t)r;
+        }
+        std::lock_guard<std::mutex> lk(mu);
+        ready = c + 1;
+        cv.notify_all();
+      }
+    });
+  }
+  int rc = PARIS_OK;
+  for (int64_t c = 0; c < nchunks && e == cudaSuccess && rc == PARIS_OK; ++c) {
+    {
+      std::unique_lock<std::mutex> lk(mu);
+      cv.wait(lk, [&] { return ready > c || failed; });
+      if (failed) { rc = PARIS_EINVAL; set_error("paris_summarize_file: read of %s failed", path); break; }
+    }
+    const int b = (int)(c & 1), h = (int)(c % NB);
+    const int64_t c0 = c * chunk, m = std::min<int64_t>(chunk, n - c0);
+    e = cudaStreamWaitEvent(cs, consumed[b], 0);  // the kernels of chunk c-2 are done with db[b]
+    if (e == cudaSuccess) e = cudaMemcpyAsync(db[b], hb[h], (size_t)m * row, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess) e = cudaEventRecord(copied[h], cs);
+    if (e == cudaSuccess) e = cudaEventRecord(dcopied[b], cs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, dcopied[b], 0);
+    if (e == cudaSuccess) rc = summarize_device(db[b], m, len, w, card, out_sax + c0, n, tab, st);
+    if (e == cudaSuccess && rc == PARIS_OK && out_bf16) rc = raw_bf16_launch(db[b], m, len, out_bf16 + (size_t)c0 * len, st);
+    if (e == cudaSuccess && rc == PARIS_OK) e = cudaEventRecord(consumed[b], st);
+  }
+  if (reader.joinable()) {
+    if (e != cudaSuccess || rc != PARIS_OK) {  // let the reader finish its waits, then stop it
+      std::lock_guard<std::mutex> lk(mu);
+      failed = true;
+    }
+    reader.join();
+  }
+  if (e != cudaSuccess && rc == PARIS_OK) rc = cuda_error(e, "paris_summarize_file");
+  cudaStreamSynchronize(cs);  // the pinned buffers are freed below
+  for (int i = 0; i < NB; ++i) {
+    if (hb[i]) cudaFreeHost(hb[i]);
+    if (copied[i]) cudaEventDestroy(copied[i]);
+  }
+  for (int i = 0; i < 2; ++i) {
+    if (db[i]) cudaFreeAsync(db[i], st);
+    if (consumed[i]) cudaEventDestroy(consumed[i]);
+    if (dcopied[i]) cudaEventDestroy(dcopied[i]);
+  }
+  if (cs) cudaStreamDestroy(cs);
+  close(fd);
+  return rc;
+}
+}  // namespace paris
+
+extern "C" int paris_summarize_file(const char* path, int64_t offset, int64_t n, int32_t len, int32_t w, int32_t card,
+                                    uint8_t* out_sax, uint16_t* out_bf16, int32_t direct_io, void* stream) {
+  if (!path || !out_sax || n < 1 || n >= (int64_t(1) << 31) || offset < 0) {
+    paris::set_error("paris_summarize_file: bad arguments");
+    return PARIS_EINVAL;
+  }
+  if (len < 4 || len > 4096 || (len % 4) || w < 1 || w > 64 || (len % w) || (out_bf16 && (len % 8))) {
+    paris::set_error("paris_summarize_file: unsupported (len=%d, w=%d)", len, w);
+    return PARIS_ECONFIG;
+  }
+  paris::retain_pool();
+  return paris::summarize_file_impl(path, offset, n, len, w, card, out_sax, out_bf16, direct_io, (cudaStream_t)stream);
+}
+
+// A raw file mapped read-only and registered with CUDA (its pages pinned): the exact
+// search then reads the candidates' rows straight from it (zero-copy over PCIe), the
+// RDC workers' random reads of the raw file.  Needs the file in host RAM.
+extern "C" int paris_map_raw_file(const char* path, int64_t offset, int64_t bytes, void** out_ptr) {
+  if (!path || !out_ptr || bytes <= 0 || offset < 0 || (offset % 4096)) {
+    paris::set_error("paris_map_raw_file: bad arguments (offset must be page aligned)");
+    return PARIS_EINVAL;
+  }
+  const int fd = open(path, O_RDONLY);
+  if (fd < 0) {
+    paris::set_error("paris_map_raw_file: cannot open %s", path);
+    return PARIS_EINVAL;
+  }
+  void* p = mmap(nullptr, (size_t)bytes, PROT_READ, MAP_SHARED | MAP_POPULATE, fd, offset);
+  close(fd);
+  if (p == MAP_FAILED) {
+    paris::set_error("paris_map_raw_file: mmap of %lld bytes failed", (long long)bytes);
+    return PARIS_ENOMEM;
+  }
+  const cudaError_t e = cudaHostRegister(p, (size_t)bytes, cudaHostRegisterMapped | cudaHostRegisterReadOnly);
+  if (e != cudaSuccess) {
+    munmap(p, (size_t)bytes);
+    return paris::cuda_error(e, "paris_map_raw_file: cudaHostRegister");
+  }
+  *out_ptr = p;
+  return PARIS_OK;
+}
+
+extern "C" int paris_unmap_raw_file(void* ptr, int64_t bytes) {
+  if (!ptr || bytes <= 0) return PARIS_EINVAL;
+  cudaHostUnregister(ptr);
+  munmap(ptr, (size_t)bytes);
+  cudaGetLastError();
+  return PARIS_OK;
 }

@@ -48,6 +48,14 @@ def test_argument_validation_without_gpu(lib):
     assert so.paris_knn_exact(addr, addr, 5, addr, 1, 6, addr, addr, 256, 16, 256, None) == lib.PARIS_EINVAL
     assert so.paris_knn_exact(addr, addr, 5000, addr, 1, 2000, addr, addr, 256, 16, 256, None) == lib.PARIS_EINVAL
     assert so.paris_knn_exact(addr, addr, 5, addr, 1, 0, addr, addr, 256, 16, 256, None) == lib.PARIS_EINVAL
+    # approximate search: same size checks
+    assert so.paris_knn_approx(addr, addr, 5, addr, 1, 6, addr, addr, 256, 16, 256, None, None) == lib.PARIS_EINVAL
+    # file-backed raw: null path, unsupported shape, unaligned mapping offset
+    assert so.paris_summarize_file(None, 0, 10, 256, 16, 256, addr, None, 0, None) == lib.PARIS_EINVAL
+    assert so.paris_summarize_file(b"/tmp/x", 0, 10, 256, 15, 256, addr, None, 0, None) == lib.PARIS_ECONFIG
+    out = ctypes.c_void_p()
+    assert so.paris_map_raw_file(b"/tmp/x", 17, 4096, ctypes.byref(out)) == lib.PARIS_EINVAL
+    assert so.paris_map_raw_file(b"/nonexistent/raw.f32", 0, 4096, ctypes.byref(out)) == lib.PARIS_EINVAL
 
 
 @pytest.mark.parametrize("card", [2, 4, 8, 16, 32, 64, 128, 256])

@@ -147,3 +147,44 @@ def test_knn_index_pinned_raw_bf16(P, k):
     check_knn(x, q, hi.cpu().numpy(), hd.cpu().numpy(), ri, rd2)
     if k == 1:
         assert st["refined"].float().mean().item() < 50   # fp32 rows read per query
+
+
+@pytest.mark.parametrize("direct_io", [False, True])
+def test_summarize_file_and_mapped_search(P, small_chunks, tmp_path, direct_io):
+    """Raw data in a FILE (the paper's disk setting): paris_summarize_file (pread reader thread,
+    pinned triple buffer, many chunks, O_DIRECT or buffered) gives the device path's SAX array
+    and bf16 copy bit for bit; the file mapped with paris_map_raw_file serves the exact search
+    (zero-copy candidate rows), equal to the oracle."""
+    import torch
+    n, length = 3 * 1024 + 48, 256
+    x = datagen.random_walks(n, length, 3131)
+    q = datagen.random_walks(5, length, 3132)
+    q[2] = x[n - 7]
+    path = tmp_path / "raw.f32"
+    header = 4096
+    with open(path, "wb") as f:
+        f.write(b"\0" * header)
+        f.write(np.ascontiguousarray(x).tobytes())
+    xd = torch.from_numpy(x).cuda()
+    ref_sax = P.summarize(xd, 16, 256)
+    ref16 = P.raw_bf16(xd)
+    sax, r16 = P.summarize_file(str(path), n, length, 16, 256, offset=header, bf16=True, direct_io=direct_io)
+    torch.cuda.synchronize()
+    assert torch.equal(sax, ref_sax)
+    assert torch.equal(r16, ref16)
+    bad, _, _ = sax_mismatches(x, sax.cpu().numpy(), 16, 256)
+    assert len(bad) == 0
+    idx = P.index_build(sax, 16, 256)
+    with P.MappedRaw(str(path), n, length, offset=header) as m:
+        assert m.tensor.is_pinned()
+        for k, raw16 in ((1, r16), (1, None), (4, None)):
+            gi, gd = P.knn_index(m.tensor, idx, torch.from_numpy(q).cuda(), k=k, raw16=raw16)
+            ri, rd2 = oracle.knn_bruteforce(x, q, k)
+            check_knn(x, q, gi.cpu().numpy(), gd.cpu().numpy(), ri, rd2)
+    with pytest.raises(P.ParisError):
+        P.summarize_file(str(path), n + 1000, length, 16, 256, offset=header)   # short file
+
+
+def test_summarize_file_rejects_missing(P):
+    with pytest.raises(P.ParisError):
+        P.summarize_file("/nonexistent/raw.f32", 100, 256)
