@@ -2395,6 +2395,156 @@ k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
   if (threadIdx.x < nb && s_r16[threadIdx.x]) atomicAdd(&a.refined16[threadIdx.x], s_r16[threadIdx.x]);
 }
 
+// k = 1 with the bf16 pre-filter, lane per candidate (the default index-path refine when
+// a bf16 copy is given): a warp walks its share of the query's unsorted list as
+// k_refine1u does (same waves, same rotation, same LB <= BSF test), but queues the
+// keys that pass in shared memory and takes them 32 at a time, ONE CANDIDATE PER LANE:
+// each lane streams its own bf16 row (8 x 16-byte loads in flight per lane, 32 rows per
+// warp -- no cross-lane reduction), sums D^2 = ||q - x~||^2 sequentially in fp32 and drops
+// the candidate once the pre-filter's lower bound (1 - rho) D - rho ||q|| (bf16_lb; D may
+// be a partial sum: the bound grows with D) exceeds the live BSF -- after every 64 points.
+// The few survivors get their exact fp32 distance warp-cooperatively (refine_group, U rows
+// in flight), which lowers the BSF.  Error bound of a lane's sequential fp32 sum of len
+// terms: e <= (len + 8) 2^-24, doubled as in bf16_lb's margin.
+#ifndef PARIS_REFQ_CTAS
+#define PARIS_REFQ_CTAS 4
+#endif
+constexpr int kRefQCtas = PARIS_REFQ_CTAS;
+constexpr int kRefQLen = 256;  // longest row of the lane-per-candidate form (query staged in shared memory)
+
+template <int NC, int U>
+__global__ void __launch_bounds__(kRefThreads, kRefQCtas)
+k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
+  __shared__ unsigned s_refined[kMaxB], s_cnt[kMaxB], s_cut[kMaxB], s_r16[kMaxB];
+  __shared__ float s_scale[kMaxB];
+  __shared__ uint64_t s_queue[kRefWarps][64];
+  __shared__ __align__(16) float s_qv[kRefWarps][kRefQLen];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x < kMaxB) {
+    const bool on = threadIdx.x < nb;
+    s_refined[threadIdx.x] = 0;
+    s_r16[threadIdx.x] = 0;
+    s_cnt[threadIdx.x] = on ? (unsigned)imin64((int64_t)a.count[threadIdx.x], a.cap) : 0u;
+    s_cut[threadIdx.x] = on ? cut[threadIdx.x * kNB] : 0u;
+    s_scale[threadIdx.x] = on ? bin_scale(__uint_as_float(a.thr_seed[threadIdx.x])) : 0.f;
+  }
+  __syncthreads();
+  const unsigned gw = blockIdx.x * kRefWarps + warp, GW = gridDim.x * kRefWarps;
+  const int nh = a.len >> 3;  // uint4 (8 bf16) per row
+  const float e2 = 2.f * (float)(a.len + 8) * 5.9604644775390625e-08f;      // lane-sequential sums
+  const float e2w = 2.f * (float)((a.len >> 5) + 8) * 5.9604644775390625e-08f;  // warp-tree sums
+  uint64_t* queue = s_queue[warp];
+  const float4* sq4 = reinterpret_cast<const float4*>(s_qv[warp]);
+  for (int b = 0; b < nb; ++b) {
+    const unsigned cnt = s_cnt[b];
+    const unsigned nchunk = (cnt + 31) / 32;
+    const unsigned first = (gw + (unsigned)b * 613u) % GW;  // rotate: spread small lists over all warps
+    if (first >= nchunk) continue;
+    const float scale = s_scale[b];
+    const int cutb = (int)s_cut[b];
+    const uint64_t* list = a.sorted + (size_t)b * a.cap;
+    const float4* qv = reinterpret_cast<const float4*>(a.queries + (size_t)b * a.len);
+    unsigned long long* bp = a.best + (size_t)b * kPadU64;
+    unsigned nref = 0, nref16 = 0;
+    uint64_t cur = kNoKey;
+    __syncwarp();
+    float qs = 0.f;  // the query in shared memory (broadcast reads) and qn_hi >= ||q||
+    for (int f = lane; f < (a.len >> 2); f += 32) {
+      const float4 v = __ldg(qv + f);
+      reinterpret_cast<float4*>(s_qv[warp])[f] = v;
+      qs = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, qs))));
+    }
+    const float qn_hi = __fsqrt_ru(__fmul_ru(warp_sum(qs), 1.f + e2w));
+    __syncwarp();
+    int qn = 0;  // queued keys
+
+    // the queued keys [0, m) one per lane: bf16 pre-filter, then the survivors exactly
+    auto drain = [&](int m) {
+      cur = min(cur, ld_relaxed_u64(bp));
+      float thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
+      const uint64_t key = lane < m ? queue[lane] : kNoKey;
+      bool live = lane < m && key_val(key) <= thr;
+      nref16 += __popc(__ballot_sync(0xffffffffu, live));
+      const uint4* row = reinterpret_cast<const uint4*>(a.raw16 + (size_t)key_id(key) * a.len);
+      float s2 = 0.f;
+      for (int c0 = 0; c0 < nh; c0 += 8) {
+        uint4 h[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          h[u] = (live && c0 + u < nh) ? ld_stream_u4(row + c0 + u) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (c0 + u >= nh) break;
+          const float4 q0 = sq4[2 * (c0 + u)], q1 = sq4[2 * (c0 + u) + 1];
+          const float qq[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+          const uint32_t w4[4] = {h[u].x, h[u].y, h[u].z, h[u].w};
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float d = __uint_as_float((e & 1) ? (w4[e >> 1] & 0xFFFF0000u) : (w4[e >> 1] << 16)) - qq[e];
+            s2 = fmaf(d, d, s2);
+          }
+        }
+        if (live && c0 + 8 < nh) {  // early abandoning on the partial sum
+          const float lb = bf16_lb(s2, qn_hi, e2);
+          if (lb > 0.f && __fmul_rd(lb, lb) > thr) live = false;
+        }
+      }
+      if (live) {
+        const float lb = bf16_lb(s2, qn_hi, e2);
+        if (lb > 0.f && __fmul_rd(lb, lb) > thr) live = false;
+      }
+      unsigned m2 = __ballot_sync(0xffffffffu, live);
+      while (m2) {  // survivors: exact fp32 distance, U rows in flight per warp
+        uint64_t ks[U];
+        bool lv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int src = m2 ? __ffs(m2) - 1 : 0;
+          const bool has = m2 != 0u;
+          m2 &= m2 - 1;
+          ks[u] = __shfl_sync(0xffffffffu, key, src);
+          lv[u] = has && key_val(ks[u]) <= thr;
+        }
+        refine_group<NC, U>(a, qv, ks, lv, thr, cur, bp, nref);
+        thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
+      }
+    };
+
+    uint64_t knext = (first * 32 + lane < cnt) ? __ldg(list + first * 32 + lane) : kNoKey;
+    for (unsigned ch = first; ch < nchunk; ch += GW) {
+      const unsigned i = ch * 32 + lane;
+      const uint64_t k0 = knext;
+      {
+        const unsigned in = (ch + GW) * 32 + lane;
+        knext = (ch + GW < nchunk && in < cnt) ? __ldg(list + in) : kNoKey;
+      }
+      cur = min(cur, ld_relaxed_u64(bp));
+      const float thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
+      const float lb0 = key_val(k0);
+      const int bin = lb_bin(lb0, scale);
+      const bool pass = i < cnt && (wave == 0 ? bin <= cutb : bin > cutb) && lb0 <= thr;
+      const unsigned m = __ballot_sync(0xffffffffu, pass);
+      if (pass) queue[qn + __popc(m & ((1u << lane) - 1u))] = k0;
+      qn += __popc(m);
+      __syncwarp();
+      if (qn >= 32) {
+        drain(32);
+        __syncwarp();
+        if (lane < qn - 32) queue[lane] = queue[32 + lane];  // the rest to the front
+        qn -= 32;
+        __syncwarp();
+      }
+    }
+    if (qn > 0) drain(qn);
+    __syncwarp();
+    if (lane == 0 && nref) atomicAdd(&s_refined[b], nref);
+    if (lane == 0 && nref16) atomicAdd(&s_r16[b], nref16);
+  }
+  __syncthreads();
+  if (threadIdx.x < nb && s_refined[threadIdx.x]) atomicAdd(&a.refined[threadIdx.x], s_refined[threadIdx.x]);
+  if (threadIdx.x < nb && s_r16[threadIdx.x]) atomicAdd(&a.refined16[threadIdx.x], s_r16[threadIdx.x]);
+}
+
 // ---------------------------------------------------------------- K6, k > 1 (append, then select)
 // The query-wide threshold from the refined-distance histogram: at least k distinct
 // refined series have fp32 d^2 < (t + 2) / scale for the first bin t where the count
@@ -3388,6 +3538,12 @@ cudaError_t launch_refine1(const RefineArgs& ra, int nb, int64_t max_work, cudaS
 
 template <int NC, int U>
 cudaError_t launch_refine1u(const RefineArgs& ra, int nb, int wave, const unsigned* cut, cudaStream_t st) {
+  if constexpr (NC <= 2) {
+    if (ra.raw16 && !getenv("PARIS_REF16_WARP")) {  // lane per candidate (env: A/B of the warp form)
+      const int grid = sms() * kRefQCtas;
+      return PARIS_LAUNCH("refine", (k_refine1q<NC, U>), grid, kRefThreads, 0, st, ra, nb, wave, cut);
+    }
+  }
   if (ra.raw16) {
     const int grid = sms() * (NC <= 2 ? kRefU16Ctas : 2);
     return PARIS_LAUNCH("refine", (k_refine1u<NC, U, true>), grid, kRefThreads, 0, st, ra, nb, wave, cut);
