@@ -240,7 +240,7 @@ def run_reference(args):
             "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": sec_per_query * nq * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg["desc"], "n": n, "len": length, "w": W, "card": CARD, "nq": nq, "k": k},
+            "config": {"workload": cfg["desc"] + ("" if args.sigma is None else f" [queries: sigma = {args.sigma}]"), "n": n, "len": length, "w": W, "card": CARD, "nq": nq, "k": k},
             "cpu_baseline": dict({"value": value, "unit": "queries/s", "cores": 1, "kind": "oracle", "sample": sample},
                                  **host_info()),
             "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -283,6 +283,8 @@ def run_gpu(args):
     t0 = time.time()
     raw = dg.walks(n_local, length, ds, first_id=lo, device=dev)          # this rank's ids [lo, hi)
     sigma = None if cfg["queries"] == "fresh" else float(cfg["queries"][5:])
+    if args.sigma is not None and sigma is not None:
+        sigma = args.sigma  # query hardness override (C2 / C5 member + N(0, sigma^2) queries)
     if sigma is None:
         queries = dg.walks(nq, length, qs, device=dev)
     elif sharded and ws > 1:
@@ -652,7 +654,7 @@ def run_gpu(args):
             "higher_is_better": True, "scaling": "strong" if sharded else "weak", "vs_baseline": None,
             "dtype": "f32",
             "data": "synthetic (seeded Philox random walks, z-normalized; no dataset on the box)",
-            "config": {"workload": cfg["desc"], "n": n, "len": length, "w": W, "card": CARD, "nq": nq, "k": k,
+            "config": {"workload": cfg["desc"] + ("" if args.sigma is None else f" [queries: sigma = {args.sigma}]"), "n": n, "len": length, "w": W, "card": CARD, "nq": nq, "k": k,
                        "batch": primary["batch"], "path": args.path, "index_build_ms": index_ms,
                        "raw_bf16": None if raw16 is None else {"build_ms": raw16_ms, "bytes": raw16.numel() * 2},
                        "parallelism": (f"shard x{ws} by series id (tau all-reduce(min) + all-gather + exact merge)"
@@ -726,6 +728,8 @@ def main():
     ap.add_argument("--no-sweep", action="store_true", help="skip the C2 k=10 / C5 sigma x k sweeps")
     ap.add_argument("--raw-host", action="store_true",
                     help="f3: keep the raw collection in pinned host memory (SAX/index in HBM)")
+    ap.add_argument("--sigma", type=float, default=None,
+                    help="C2/C5: noise of the member queries (hardness; default the config's 0.05)")
     ap.add_argument("--ref-sample", type=int, default=2_000_000)
     ap.add_argument("--ref-queries", type=int, default=4)
     args = ap.parse_args()

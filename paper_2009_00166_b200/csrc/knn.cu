@@ -1623,38 +1623,49 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
 
 // ---------------------------------------------------------------- K4, one query per pass
 // B = 1 (flat path): the pass is one lookup + two FMAs per (series, segment), so
-// it is fed by plain 16-byte loads at high occupancy rather than the TMA ring
-// (whose 16 row copies per tile cap delivery near 2.7 TB/s): a thread owns 16
-// consecutive series (one uint4 per segment row, 256 B in flight), the region
-// table (-U16, L16) is replicated 32x in shared memory (conflict-free lookups),
-// and the single-query fp16x2 form accumulates (ABOVE, BELOW) per series.
-constexpr int kLb1Threads = 256;
+// it is fed by plain 8-byte loads at high occupancy rather than the TMA ring (whose 16
+// row copies per tile cap delivery near 2.7 TB/s): one CTA of 24 warps per SM, a thread
+// owns SPT consecutive series (one uint2 / uint4 per segment row), and the single-query
+// fp16x2 form accumulates (ABOVE, BELOW) per series.  The region table (-U16, L16) is
+// replicated 32x (entry c of lane l at T + 256c + 4l, T a 64 KB boundary of dynamic
+// shared memory): ONE byte permute {lane*4, symbol, T bits 16..31} is a lookup's whole
+// address, so a (series, segment) costs PRMT + LDS + 2 HFMA2.
+constexpr int kLb1Threads = 768;
 #ifndef PARIS_LB1_SPT
 #define PARIS_LB1_SPT 8
 #endif
 
 // SPT series per thread: 16 (one uint4 per row) or 8 (one uint2 per row, fewer
-// registers -> more resident warps).
+// registers).
 template <int SPT>
-__global__ void __launch_bounds__(kLb1Threads, SPT == 16 ? 2 : SPT == 8 ? 3 : 4)
+__global__ void __launch_bounds__(kLb1Threads, 1)
 k_lb1(LbArgs a) {
-  __shared__ uint32_t s_tab[kMaxCard * 32];
+  extern __shared__ __align__(128) uint8_t dsm1[];
   __shared__ uint32_t s_qd[kTW];
   __shared__ LbConsts s_c;
   __shared__ WarpBuf s_wb[kLb1Threads / 32];
   __shared__ unsigned s_hist[kNB];
+  const uint32_t S0 = smem_u32(dsm1);
+  const uint32_t T = (S0 + 0xFFFFu) & ~0xFFFFu;
+  {
+    uint32_t dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    if (T + 65536u > S0 + dyn) __trap();  // launch config inconsistent with the layout
+  }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   WarpBuf& wb = s_wb[warp];
   for (int b = lane; b < kMaxB; b += 32) wb.cnt[b] = 0;
   if (lane == 0) wb.n = 0;
   for (int i = tid; i < kNB; i += kLb1Threads) s_hist[i] = 0;
-  for (int i = tid; i < kMaxCard * 32; i += kLb1Threads) s_tab[i] = a.tab->lu16p[i >> 5];
+  for (int i = tid; i < kMaxCard * 32; i += kLb1Threads)
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(T + 256u * (uint32_t)(i >> 5) + 4u * (uint32_t)(i & 31)),
+                 "r"(a.tab->lu16p[i >> 5]) : "memory");
   if (tid < kTW) {
     const uint2 v = a.g_q16[tid];  // pair layout, slot 0 = low halves
     s_qd[tid] = (v.x & 0xFFFFu) | (v.y << 16);
   }
   lb_consts_init(a, 1, &s_c);  // ends with __syncthreads
-  const uint32_t* tabl = s_tab + lane;
+  const uint32_t lanebase = T | ((uint32_t)lane * 4u);  // bytes {lane * 4, 0, T bits 16-31}
   const int64_t n = a.n;
   const int64_t ngroups = n / SPT;  // n % 16 == 0 (tiled-path condition)
   for (int64_t g = (int64_t)blockIdx.x * kLb1Threads + tid; g - lane < ngroups;
@@ -1682,7 +1693,9 @@ k_lb1(LbArgs a) {
         const uint32_t qd = s_qd[s];
 #pragma unroll
         for (int j = 0; j < SPT; ++j) {
-          const uint32_t t = tabl[__byte_perm(wd[s][j >> 2], 0, 0x4440 | (j & 3)) * 32];
+          uint32_t t;
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(t)
+                       : "r"(__byte_perm(wd[s][j >> 2], lanebase, 0x7604u | ((uint32_t)(j & 3) << 4))));
           const uint32_t d = h2_fma_relu(qd, kHalf2One, t);
           acc[j] = h2_fma(d, d, acc[j]);
         }
@@ -2395,22 +2408,23 @@ k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
   if (threadIdx.x < nb && s_r16[threadIdx.x]) atomicAdd(&a.refined16[threadIdx.x], s_r16[threadIdx.x]);
 }
 
-// k = 1 with the bf16 pre-filter, lane per candidate (the default index-path refine when
-// a bf16 copy is given): a warp walks its share of the query's unsorted list as
-// k_refine1u does (same waves, same rotation, same LB <= BSF test), but queues the
-// keys that pass in shared memory and takes them 32 at a time, ONE CANDIDATE PER LANE:
-// each lane streams its own bf16 row (8 x 16-byte loads in flight per lane, 32 rows per
-// warp -- no cross-lane reduction), sums D^2 = ||q - x~||^2 sequentially in fp32 and drops
-// the candidate once the pre-filter's lower bound (1 - rho) D - rho ||q|| (bf16_lb; D may
-// be a partial sum: the bound grows with D) exceeds the live BSF -- after every 64 points.
-// The few survivors get their exact fp32 distance warp-cooperatively (refine_group, U rows
-// in flight), which lowers the BSF.  Error bound of a lane's sequential fp32 sum of len
-// terms: e <= (len + 8) 2^-24, doubled as in bf16_lb's margin.
+// k = 1 with the bf16 pre-filter (the default index-path refine when a bf16 copy is
+// given), eight lanes per candidate: a warp walks its share of the query's unsorted list
+// as k_refine1u does (same waves, same rotation, same LB <= BSF test) but queues
+// the keys that pass in shared memory and drains them 8 at a time -- an octet of lanes per
+// candidate, two candidates per octet, so each lane has 8 independent 16-byte loads in
+// flight and every load instruction touches four whole 128-byte lines (4 KB of bf16 rows
+// in flight per warp).  D^2 = ||q - x~||^2 is summed per lane in two fp32 chains and
+// reduced over the octet; a candidate whose pre-filter bound (1 - rho) D - rho ||q||
+// (bf16_lb) exceeds the live BSF is dropped, the few survivors get their exact fp32
+// distance warp-cooperatively (refine_group, U rows in flight), which lowers the BSF.
+// Error bound of the octet sum: <= (len/16 + 8) 2^-24 relative (two chains of len/16
+// terms, one add, a 3-level tree), doubled as in bf16_lb's margin.
 #ifndef PARIS_REFQ_CTAS
-#define PARIS_REFQ_CTAS 4
+#define PARIS_REFQ_CTAS 3
 #endif
 constexpr int kRefQCtas = PARIS_REFQ_CTAS;
-constexpr int kRefQLen = 256;  // longest row of the lane-per-candidate form (query staged in shared memory)
+constexpr int kRefQLen = 256;  // longest row of the octet form (query staged in shared memory)
 
 template <int NC, int U>
 __global__ void __launch_bounds__(kRefThreads, kRefQCtas)
@@ -2420,6 +2434,7 @@ k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
   __shared__ uint64_t s_queue[kRefWarps][64];
   __shared__ __align__(16) float s_qv[kRefWarps][kRefQLen];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int oct = lane >> 3, sub = lane & 7;
   if (threadIdx.x < kMaxB) {
     const bool on = threadIdx.x < nb;
     s_refined[threadIdx.x] = 0;
@@ -2431,7 +2446,8 @@ k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
   __syncthreads();
   const unsigned gw = blockIdx.x * kRefWarps + warp, GW = gridDim.x * kRefWarps;
   const int nh = a.len >> 3;  // uint4 (8 bf16) per row
-  const float e2 = 2.f * (float)(a.len + 8) * 5.9604644775390625e-08f;      // lane-sequential sums
+  const int nper = (nh + 7) >> 3;  // uint4 per lane of an octet
+  const float e2 = 2.f * (float)((a.len >> 4) + 8) * 5.9604644775390625e-08f;   // octet sums
   const float e2w = 2.f * (float)((a.len >> 5) + 8) * 5.9604644775390625e-08f;  // warp-tree sums
   uint64_t* queue = s_queue[warp];
   const float4* sq4 = reinterpret_cast<const float4*>(s_qv[warp]);
@@ -2448,7 +2464,7 @@ k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     unsigned nref = 0, nref16 = 0;
     uint64_t cur = kNoKey;
     __syncwarp();
-    float qs = 0.f;  // the query in shared memory (broadcast reads) and qn_hi >= ||q||
+    float qs = 0.f;  // the query in shared memory and qn_hi >= ||q||
     for (int f = lane; f < (a.len >> 2); f += 32) {
       const float4 v = __ldg(qv + f);
       reinterpret_cast<float4*>(s_qv[warp])[f] = v;
@@ -2458,55 +2474,80 @@ k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     __syncwarp();
     int qn = 0;  // queued keys
 
-    // the queued keys [0, m) one per lane: bf16 pre-filter, then the survivors exactly
+    // the queued keys [0, m): octet o takes keys 8r + o and 8r + 4 + o of round r
     auto drain = [&](int m) {
-      cur = min(cur, ld_relaxed_u64(bp));
-      float thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
-      const uint64_t key = lane < m ? queue[lane] : kNoKey;
-      bool live = lane < m && key_val(key) <= thr;
-      nref16 += __popc(__ballot_sync(0xffffffffu, live));
-      const uint4* row = reinterpret_cast<const uint4*>(a.raw16 + (size_t)key_id(key) * a.len);
-      float s2 = 0.f;
-      for (int c0 = 0; c0 < nh; c0 += 8) {
-        uint4 h[8];
+      for (int r0 = 0; r0 < m; r0 += 8) {
+        cur = min(cur, ld_relaxed_u64(bp));
+        float thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
+        uint64_t key[2];
+        bool live[2];
+        const uint4* row[2];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          h[u] = (live && c0 + u < nh) ? ld_stream_u4(row + c0 + u) : make_uint4(0u, 0u, 0u, 0u);
+        for (int c = 0; c < 2; ++c) {
+          const int e = r0 + 4 * c + oct;
+          key[c] = e < m ? queue[e] : kNoKey;
+          live[c] = e < m && key_val(key[c]) <= thr;
+          row[c] = reinterpret_cast<const uint4*>(a.raw16 + (size_t)key_id(key[c]) * a.len);
+        }
+        nref16 += __popc(__ballot_sync(0xffffffffu, sub == 0 && live[0])) +
+                  __popc(__ballot_sync(0xffffffffu, sub == 0 && live[1]));
+        float s2[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+        for (int i0 = 0; i0 < nper; i0 += 4) {
+          uint4 h[2][4];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (c0 + u >= nh) break;
-          const float4 q0 = sq4[2 * (c0 + u)], q1 = sq4[2 * (c0 + u) + 1];
-          const float qq[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-          const uint32_t w4[4] = {h[u].x, h[u].y, h[u].z, h[u].w};
+          for (int c = 0; c < 2; ++c)
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const float d = __uint_as_float((e & 1) ? (w4[e >> 1] & 0xFFFF0000u) : (w4[e >> 1] << 16)) - qq[e];
-            s2 = fmaf(d, d, s2);
+            for (int i = 0; i < 4; ++i) {
+              const int f = sub + 8 * (i0 + i);
+              h[c][i] = (live[c] && i0 + i < nper && f < nh) ? ld_stream_u4(row[c] + f) : make_uint4(0u, 0u, 0u, 0u);
+            }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int f = sub + 8 * (i0 + i);
+            if (i0 + i >= nper || f >= nh) break;
+            const float4 q0 = sq4[2 * f], q1 = sq4[2 * f + 1];
+            const float qq[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              const uint32_t w4[4] = {h[c][i].x, h[c][i].y, h[c][i].z, h[c][i].w};
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const float d = __uint_as_float((e & 1) ? (w4[e >> 1] & 0xFFFF0000u) : (w4[e >> 1] << 16)) - qq[e];
+                s2[c][e & 1] = fmaf(d, d, s2[c][e & 1]);
+              }
+            }
           }
         }
-        if (live && c0 + 8 < nh) {  // early abandoning on the partial sum
-          const float lb = bf16_lb(s2, qn_hi, e2);
-          if (lb > 0.f && __fmul_rd(lb, lb) > thr) live = false;
-        }
-      }
-      if (live) {
-        const float lb = bf16_lb(s2, qn_hi, e2);
-        if (lb > 0.f && __fmul_rd(lb, lb) > thr) live = false;
-      }
-      unsigned m2 = __ballot_sync(0xffffffffu, live);
-      while (m2) {  // survivors: exact fp32 distance, U rows in flight per warp
-        uint64_t ks[U];
-        bool lv[U];
+        bool keep[2];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int src = m2 ? __ffs(m2) - 1 : 0;
-          const bool has = m2 != 0u;
-          m2 &= m2 - 1;
-          ks[u] = __shfl_sync(0xffffffffu, key, src);
-          lv[u] = has && key_val(ks[u]) <= thr;
+        for (int c = 0; c < 2; ++c) {
+          float v = s2[c][0] + s2[c][1];
+          v += __shfl_xor_sync(0xffffffffu, v, 4);
+          v += __shfl_xor_sync(0xffffffffu, v, 2);
+          v += __shfl_xor_sync(0xffffffffu, v, 1);
+          const float lb = bf16_lb(v, qn_hi, e2);
+          keep[c] = live[c] && !(lb > 0.f && __fmul_rd(lb, lb) > thr);
         }
-        refine_group<NC, U>(a, qv, ks, lv, thr, cur, bp, nref);
-        thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
+        // survivors (octet leaders' bits): exact fp32 distance, U rows in flight per warp
+        unsigned m2 = __ballot_sync(0xffffffffu, sub == 0 && keep[0]);
+        unsigned m3 = __ballot_sync(0xffffffffu, sub == 0 && keep[1]);
+        while (m2 | m3) {
+          uint64_t ks[U];
+          bool lv[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const bool from2 = m2 != 0u;
+            const unsigned mm = from2 ? m2 : m3;
+            const int src = mm ? __ffs(mm) - 1 : 0;
+            const bool has = mm != 0u;
+            if (from2) m2 &= m2 - 1; else m3 &= m3 - 1;
+            const uint64_t k0 = __shfl_sync(0xffffffffu, key[0], src), k1 = __shfl_sync(0xffffffffu, key[1], src);
+            ks[u] = from2 ? k0 : k1;
+            lv[u] = has && key_val(ks[u]) <= thr;
+          }
+          refine_group<NC, U>(a, qv, ks, lv, thr, cur, bp, nref);
+          thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
+        }
       }
     };
 
@@ -3490,7 +3531,18 @@ cudaError_t launch_nb(const Plan& p, const float* raw, const uint8_t* sax, const
 cudaError_t launch_lb1(const Plan& p, const uint8_t* sax, const CardTables* tab, const Ws& ws, cudaStream_t st,
                        int64_t cap) {
   constexpr int SPT = PARIS_LB1_SPT;
-  const int occ = cached_per_device((const void*)k_lb1<SPT>, [](int) { return occupancy(k_lb1<SPT>, kLb1Threads, 0); });
+  // dynamic shared memory: up to the 64 KB-aligned 64 KB table above the static arrays
+  const int smem1 = cached_per_device((const void*)k_lb1<SPT>, [](int dev) {
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, k_lb1<SPT>) != cudaSuccess) return 0;
+    const int v = optin - (int)fa.sharedSizeBytes;
+    if (cudaFuncSetAttribute(k_lb1<SPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, v) != cudaSuccess) return 0;
+    return v;
+  });
+  if (smem1 <= 0) return cudaErrorInvalidConfiguration;
+  const int occ = 1;
   LbArgs la;
   la.sax = sax; la.n = p.n; la.w = p.w; la.seglen_f = (float)(p.len / p.w); la.tab = tab;
   la.g_q = ws.g_q; la.g_q16 = ws.g_q16; la.nb = 1; la.thr = ws.thr_seed; la.count = ws.count;
@@ -3499,7 +3551,7 @@ cudaError_t launch_lb1(const Plan& p, const uint8_t* sax, const CardTables* tab,
   const int64_t ngroups = p.n / SPT;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((ngroups + kLb1Threads - 1) / kLb1Threads,
                                                               (int64_t)sms() * occ));
-  return PARIS_LAUNCH("lb_pass", k_lb1<SPT>, grid, kLb1Threads, 0, st, la);
+  return PARIS_LAUNCH("lb_pass", k_lb1<SPT>, grid, kLb1Threads, smem1, st, la);
 }
 
 template <int MODE>

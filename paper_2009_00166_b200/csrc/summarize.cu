@@ -855,16 +855,33 @@ extern "C" int paris_map_raw_file(const char* path, int64_t offset, int64_t byte
     paris::set_error("paris_map_raw_file: cannot open %s", path);
     return PARIS_EINVAL;
   }
+  // a read-only shared mapping registered read-only (the page cache's own pages); where the
+  // driver refuses that, a private writable mapping (pinning copies each page once)
   void* p = mmap(nullptr, (size_t)bytes, PROT_READ, MAP_SHARED | MAP_POPULATE, fd, offset);
+  cudaError_t e = cudaErrorInvalidValue;
+  if (p != MAP_FAILED) {
+    e = cudaHostRegister(p, (size_t)bytes, cudaHostRegisterMapped | cudaHostRegisterReadOnly);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      munmap(p, (size_t)bytes);
+      p = MAP_FAILED;
+    }
+  }
+  if (p == MAP_FAILED) {
+    p = mmap(nullptr, (size_t)bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_POPULATE, fd, offset);
+    if (p != MAP_FAILED) {
+      e = cudaHostRegister(p, (size_t)bytes, cudaHostRegisterMapped);
+      if (e != cudaSuccess) {
+        munmap(p, (size_t)bytes);
+        p = MAP_FAILED;
+      }
+    }
+  }
   close(fd);
   if (p == MAP_FAILED) {
+    if (e != cudaSuccess) return paris::cuda_error(e, "paris_map_raw_file: cudaHostRegister");
     paris::set_error("paris_map_raw_file: mmap of %lld bytes failed", (long long)bytes);
     return PARIS_ENOMEM;
-  }
-  const cudaError_t e = cudaHostRegister(p, (size_t)bytes, cudaHostRegisterMapped | cudaHostRegisterReadOnly);
-  if (e != cudaSuccess) {
-    munmap(p, (size_t)bytes);
-    return paris::cuda_error(e, "paris_map_raw_file: cudaHostRegister");
   }
   *out_ptr = p;
   return PARIS_OK;
