@@ -281,45 +281,56 @@ def run_gpu(args):
     n_local = hi - lo
 
     t0 = time.time()
-    raw = dg.walks(n_local, length, ds, first_id=lo, device=dev)          # this rank's ids [lo, hi)
+    use_index = args.path == "index"
+    want16 = not args.no_raw16 and (use_index or args.both)
     sigma = None if cfg["queries"] == "fresh" else float(cfg["queries"][5:])
     if args.sigma is not None and sigma is not None:
         sigma = args.sigma  # query hardness override (C2 / C5 member + N(0, sigma^2) queries)
-    if sigma is None:
-        queries = dg.walks(nq, length, qs, device=dev)
-    elif sharded and ws > 1:
-        queries, _ = dg.member_queries(n, length, ds, nq, sigma, qs, device=dev)   # same on every rank
-    else:
-        queries, _ = dg.noisy_members(raw, nq, sigma, qs)
-    sax = torch.empty((W, n_local), dtype=torch.uint8, device=dev)
-    torch.cuda.synchronize()
-    log(f"rank {rank}: generated ids [{lo}, {hi}) of n={n} len={length} nq={nq} in {time.time() - t0:.1f}s")
-    h2d_gbs = None
-    use_index = args.path == "index"
-    # the bf16 copy of raw for the index path's refinement pre-filter (paris_raw_bf16), built once
-    raw16, raw16_ms = None, None
-    if not args.no_raw16 and (use_index or args.both):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        raw16 = P.raw_bf16(raw)
-        e1.record()
-        torch.cuda.synchronize()
-        raw16_ms = e0.elapsed_time(e1)
-    if args.raw_host:
-        # f3: the raw collection lives in pinned host memory (not in HBM); summarize streams
-        # it through the double-buffered H2D pipeline, the refinement reads candidates' rows
-        # through the host mapping.  Only SAX (+ index, + the bf16 copy) stays in HBM.
-        t1 = time.time()
-        raw_h = torch.empty((n_local, length), dtype=torch.float32, pin_memory=True)
-        step_rows = 1 << 20
-        for r0 in range(0, n_local, step_rows):
-            raw_h[r0:r0 + step_rows].copy_(raw[r0:r0 + step_rows])
-        torch.cuda.synchronize()
-        del raw
+    raw16, raw16_ms, h2d_gbs, mapped, file_info = None, None, None, None, None
+    if args.raw_host or args.raw_file:
+        # f3: the raw collection lives OUTSIDE HBM -- in pinned host memory (--raw-host) or in a
+        # file on the local disk (--raw-file), generated in chunks on the GPU so that
+        # collections beyond HBM fit; only SAX, the index and the bf16 copy stay in HBM.
+        chunk_rows = 1 << 22
+        buf = torch.empty((min(chunk_rows, n_local), length), dtype=torch.float32, device=dev)
+        if want16:
+            raw16 = torch.empty((n_local, length), dtype=torch.int16, device=dev)
+        if args.raw_host:
+            raw_h = torch.empty((n_local, length), dtype=torch.float32, pin_memory=True)
+            for r0 in range(0, n_local, chunk_rows):
+                m = min(chunk_rows, n_local - r0)
+                dg.walks(m, length, ds, first_id=lo + r0, out=buf[:m])
+                raw_h[r0:r0 + m].copy_(buf[:m])
+                if want16:
+                    raw16[r0:r0 + m].copy_(P.raw_bf16(buf[:m]))
+            raw = raw_h
+        else:
+            path = args.raw_file
+            hbuf = torch.empty((min(chunk_rows, n_local), length), dtype=torch.float32, pin_memory=True)
+            with open(path, "wb") as f:
+                for r0 in range(0, n_local, chunk_rows):
+                    m = min(chunk_rows, n_local - r0)
+                    dg.walks(m, length, ds, first_id=lo + r0, out=buf[:m])
+                    hbuf[:m].copy_(buf[:m])
+                    f.write(hbuf[:m].numpy().tobytes())
+                f.flush()
+                os.fsync(f.fileno())
+            del hbuf
+            try:  # drop the file's pages: summarize_file then reads the disk, not the page cache
+                with open("/proc/sys/vm/drop_caches", "w") as dc:
+                    dc.write("1")
+                dropped = True
+            except OSError:
+                dropped = False
+            file_info = {"path": path, "bytes": os.path.getsize(path), "page_cache_dropped": dropped}
+        del buf
         torch.cuda.empty_cache()
-        raw = raw_h
+        if sigma is None:
+            queries = dg.walks(nq, length, qs, device=dev)
+        else:
+            queries, _ = dg.member_queries(n, length, ds, nq, sigma, qs, device=dev)
         tmp = torch.empty(1 << 28, dtype=torch.float32, device=dev)        # the PCIe roofline
-        src = raw.view(-1)[:1 << 28]
+        src = torch.empty(1 << 28, dtype=torch.float32, pin_memory=True)
         tmp.copy_(src, non_blocking=True)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -328,11 +339,47 @@ def run_gpu(args):
         e1.record()
         torch.cuda.synchronize()
         h2d_gbs = 3 * 4.0 * (1 << 28) / (e0.elapsed_time(e1) / 1e3) / 1e9
-        del tmp
-        log(f"rank {rank}: raw moved to pinned host memory in {time.time() - t1:.1f}s; H2D copy {h2d_gbs:.1f} GB/s")
+        del tmp, src
+        log(f"rank {rank}: raw outside HBM ({'pinned host' if args.raw_host else 'file'}) in {time.time() - t0:.1f}s; "
+            f"H2D copy {h2d_gbs:.1f} GB/s")
+    else:
+        raw = dg.walks(n_local, length, ds, first_id=lo, device=dev)          # this rank's ids [lo, hi)
+        if sigma is None:
+            queries = dg.walks(nq, length, qs, device=dev)
+        elif sharded and ws > 1:
+            queries, _ = dg.member_queries(n, length, ds, nq, sigma, qs, device=dev)   # same on every rank
+        else:
+            queries, _ = dg.noisy_members(raw, nq, sigma, qs)
+        # the bf16 copy of raw for the index path's refinement pre-filter (paris_raw_bf16), built once
+        if want16:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            raw16 = P.raw_bf16(raw)
+            e1.record()
+            torch.cuda.synchronize()
+            raw16_ms = e0.elapsed_time(e1)
+    sax = torch.empty((W, n_local), dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+    log(f"rank {rank}: generated ids [{lo}, {hi}) of n={n} len={length} nq={nq} in {time.time() - t0:.1f}s")
+    if args.raw_file:
+        # summarize from the file (the paper's index construction from disk: pread reader thread,
+        # O_DIRECT, pinned triple buffer), timed once; then the file mapped for the search
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t1 = time.time()
+        e0.record()
+        P.summarize_file(args.raw_file, n_local, length, W, CARD, out=sax, direct_io=True)
+        e1.record()
+        torch.cuda.synchronize()
+        file_info.update(summarize_wall_s=time.time() - t1, summarize_ms=e0.elapsed_time(e1),
+                         read_gbs=file_info["bytes"] / (time.time() - t1) / 1e9)
+        mapped = P.MappedRaw(args.raw_file, n_local, length)
+        raw = mapped.tensor
+        log(f"rank {rank}: summarized {file_info['bytes'] / 1e9:.1f} GB from the file in "
+            f"{file_info['summarize_wall_s']:.1f} s ({file_info['read_gbs']:.2f} GB/s); file mapped")
     st = torch.cuda.current_stream()
 
-    # ---- summarize (rows a1-a2): warmup + timed (each rank its shard; whole job = n / max)
+    # ---- summarize (rows a1-a2): warmup + timed (each rank its shard; whole job = n / max);
+    # with --raw-file the timed passes summarize the mapped (RAM-resident) file
     for _ in range(args.warmup):
         P.summarize(raw, W, CARD, out=sax)
     torch.cuda.synchronize()
@@ -359,7 +406,7 @@ def run_gpu(args):
     peak, peak_src = measured_peaks()
     # read-only streaming peak and the fp16x2 FMA-pipe peak, measured here
     read_peak = None
-    if not args.raw_host:
+    if not (args.raw_host or args.raw_file):
         probe = raw if raw.numel() * 4 >= (8 << 30) else torch.empty(8 << 30, dtype=torch.uint8, device=dev)
         P.debug_read_probe(probe)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -535,7 +582,7 @@ def run_gpu(args):
                              "algorithmic_ops_per_batch": ops, "ms_per_batch": per_launch_ms,
                              "hbm_achieved_gbs": alg[dom] / (per_launch_ms / 1e3) / 1e9, "hbm_peak_gbs": peak,
                              "queries_per_pass": q_per_pass}, **alu)
-            elif args.raw_host and dom in ("refine", "nb_distcomp", "seed_ed"):
+            elif (args.raw_host or args.raw_file) and dom in ("refine", "nb_distcomp", "seed_ed"):
                 byts = 4.0 * length * float(refined.sum()) / nbatches
                 ach = byts / (per_launch_ms / 1e3) / 1e9
                 roof = {"kernel": dom, "bound": "pcie", "achieved": ach, "peak": h2d_gbs, "unit": "GB/s",
@@ -578,7 +625,7 @@ def run_gpu(args):
                 "raw16_rows_mean": float(stq["raw16_rows"].numpy().astype(np.float64).mean())}
 
     sweep = None
-    if index is not None and ws == 1 and not args.no_sweep and not args.raw_host:
+    if index is not None and ws == 1 and not args.no_sweep and not (args.raw_host or args.raw_file):
         if args.config == 2:  # BASELINE config 2: exact 1-NN and k = 10
             sweep = [dict(timed_index(queries, 10), sigma=0.05)]
         elif args.config == 5:  # config 5: 5 sets x 200 member + N(0, sigma^2) queries, k = 1 and 100
@@ -629,7 +676,7 @@ def run_gpu(args):
                               "traffic": ncu_traffic("summarize", args.config),
                               "algorithmic_bytes_per_launch": n_local * (4.0 * length + W)}}
     _ = sum_bytes
-    if args.raw_host:
+    if args.raw_host or args.raw_file:
         h2d = n_local * 4.0 * length
         summarize["roofline"] = {"kernel": "summarize (host raw, double-buffered H2D)", "bound": "pcie",
                                  "achieved": h2d / (sum_ms_local / 1e3) / 1e9, "peak": h2d_gbs, "unit": "GB/s",
@@ -660,7 +707,9 @@ def run_gpu(args):
                        "parallelism": (f"shard x{ws} by series id (tau all-reduce(min) + all-gather + exact merge)"
                                        if sharded else f"weak x{ws} (independent collections + queries per GPU)"),
                        "l2": "inputs larger than L2 (no flush)",
-                       "raw": "pinned host memory (f3)" if args.raw_host else "HBM",
+                       "raw": ("pinned host memory (f3)" if args.raw_host else
+                               f"file {args.raw_file} (f3; mapped for the search)" if args.raw_file else "HBM"),
+                       "raw_file": file_info,
                        "lib_sha16": lib_sha16()},
             "roofline": dict(roof, read_peak_gbs=read_peak,
                              frac_of_read_peak=(roof["achieved"] / read_peak
@@ -694,6 +743,9 @@ def run_gpu(args):
                         "note": "rank 0's shard" if ws > 1 and sharded else None},
         }
         print(json.dumps(line), flush=True)
+    if mapped is not None:
+        raw = None
+        mapped.close()
     if ws > 1:
         dist.destroy_process_group()
     return 0
@@ -728,6 +780,9 @@ def main():
     ap.add_argument("--no-sweep", action="store_true", help="skip the C2 k=10 / C5 sigma x k sweeps")
     ap.add_argument("--raw-host", action="store_true",
                     help="f3: keep the raw collection in pinned host memory (SAX/index in HBM)")
+    ap.add_argument("--raw-file", default=None,
+                    help="f3: write the raw collection to this file, summarize it from disk (O_DIRECT), search "
+                         "with the file mapped (SAX/index/bf16 copy in HBM)")
     ap.add_argument("--sigma", type=float, default=None,
                     help="C2/C5: noise of the member queries (hardness; default the config's 0.05)")
     ap.add_argument("--ref-sample", type=int, default=2_000_000)

@@ -34,12 +34,13 @@ extern "C" {
 #endif
 
 #define PARIS_OK 0
-#define PARIS_EINVAL (-1)  /* null pointer, n < 1, nq < 0, k < 1, k > n, k > PARIS_MAX_K */
+#define PARIS_EINVAL (-1)  /* null pointer, n < 1, nq < 0, k < 1, k > n (approximate search: k > PARIS_MAX_K) */
 #define PARIS_ECONFIG (-2) /* unsupported (len, w, card) -- see the list above */
 #define PARIS_ECUDA (-3)   /* a CUDA launch/runtime error; details in paris_last_error() */
 #define PARIS_ENOMEM (-4)  /* scratch allocation failed */
 
-#define PARIS_MAX_K 1024
+#define PARIS_MAX_K 1024  /* largest k of the pruned search; 1024 < k <= n: every series' distance
+                              is computed and the keys sorted (no pruning can pay there) */
 #define PARIS_INDEX_BLOCK 64  /* series per envelope block of the index (paris_index_build) */
 #define PARIS_INDEX_TILE 2048 /* series per tile of the index's tile-major sorted SAX array   */
 

@@ -31,7 +31,7 @@ for _k in ("PARIS_REFQ_CTAS", "PARIS_REFU_CTAS", "PARIS_REFU_U", "PARIS_REFU16_C
         FLAGS = FLAGS + [f"-D{_k}={int(os.environ[_k])}"]
 if os.environ.get("PARIS_DEBUG"):  # device bounds checks (PARIS_DCHECK) -- debugging builds only
     FLAGS = FLAGS + ["-DPARIS_DEBUG_CHECKS"]
-SOURCES = ["runtime.cu", "summarize.cu", "knn.cu", "index.cu", "merge.cu"]
+SOURCES = ["runtime.cu", "summarize.cu", "knn.cu", "index.cu", "merge.cu", "select.cu"]
 HEADERS = ["runtime.cuh"]
 
 

@@ -34,6 +34,8 @@
 namespace paris {
 
 int summarize_impl(const float*, int64_t, int, int, int, uint8_t*, cudaStream_t);
+int knn_large_k(const float* raw, int64_t n, int len, const float* queries, int nq, int k, int64_t* out_idx,
+                float* out_dist, cudaStream_t st);
 
 namespace {
 
@@ -1269,58 +1271,34 @@ __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int s
   if (nvalid < 4) pf &= (1u << (2 * nvalid)) - 1u;
   if (sb < 0) pf &= 0x55u;
   if (!__any_sync(0xffffffffu, pf != 0u)) return;
-  uint32_t pm = 0;  // bit 2j+h: series j passes for slot h
-  float lbv[4][2];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) lbv[q >> 1][q & 1] = 0.f;
-  for (uint32_t r = pf; r; r &= r - 1) {  // the fp32 bound only for the lane's passing pairs
-    const int bit = __ffs(r) - 1;
-    const int jj = bit >> 1;  // explicit selects: no dynamic register indexing
-    uint32_t v = acc[0];
-    v = jj == 1 ? acc[1] : v;
-    v = jj == 2 ? acc[2] : v;
-    v = jj == 3 ? acc[3] : v;
-    const float hv = (bit & 1) ? h_hi_f(v) : h_lo_f(v);
-    const float lb = __fmul_rd(fmaxf(__fsub_rd(hv, c.wabs), 0.f), c.lbconv);
-    if (lb <= c.thr[(bit & 1) ? sb : sa]) {
-      pm |= 1u << bit;
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (q == bit) lbv[q >> 1][q & 1] = lb;
-    }
-  }
-  if (!__any_sync(0xffffffffu, pm != 0u)) return;
-  const int cntl = __popc(pm);
-  const int total = (int)__reduce_add_sync(0xffffffffu, (unsigned)cntl);
+  // room for every pair that passed the fp16 test (an upper bound of the appends)
+  const int total = (int)__reduce_add_sync(0xffffffffu, (unsigned)__popc(pf));
   if ((int)wb.n + total > kWBI) lbi_flush<HC>(wb, T, warp, nslots, c, a, hist16);
-  if (total > kWBI) {  // degenerate (e.g. tau = inf): straight to global memory
-#pragma unroll
-    for (int bit = 0; bit < 8; ++bit) {
-      if (!((pm >> bit) & 1u)) continue;
-      const int j = bit >> 1, sl = (bit & 1) ? sb : sa;
-      const unsigned pos = atomicAdd(&a.count[sl], 1u);
-      if ((int64_t)pos < a.cap) {
-        a.cand[(size_t)sl * a.cap + pos] = make_key(lbv[j][bit & 1], __ldg(a.perm + i0 + j));
-        const int fb = lb_bin(lbv[j][bit & 1], c.scale[sl]);
-        atomicAdd(&a.hist[sl * kNB + (HC ? (fb | 7) : fb)], 1u);
-      }
-    }
-    return;
-  }
-  // a lane's entries at consecutive positions reserved with one shared atomic (per-slot
-  // counts are taken at flush time)
-  int pos = cntl ? (int)atomicAdd(&wb.n, (unsigned)cntl) : 0;
-  for (uint32_t r = pm; r; r &= r - 1) {
+  const bool direct = total > kWBI;  // degenerate (e.g. tau = inf): straight to global memory
+  for (uint32_t r = pf; r; r &= r - 1) {  // the rigorous fp32 bound only for the passing pairs
     const int bit = __ffs(r) - 1;
     const int j = bit >> 1, sl = (bit & 1) ? sb : sa;
-    PARIS_DCHECK(i0 + j < a.n && pos < kWBI && sl >= 0);
-    float lv = 0.f;  // lbv[j][bit & 1] without dynamic register indexing
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      if (q == bit) lv = lbv[q >> 1][q & 1];
-    sts_u64(lbi_key_addr(T, warp, pos), make_key(lv, (uint32_t)(i0 + j)));  // sorted position
-    wb.slot[pos] = (uint8_t)sl;
-    ++pos;
+    uint32_t v = acc[0];  // acc[j]: explicit selects, no dynamic register indexing
+    v = j == 1 ? acc[1] : v;
+    v = j == 2 ? acc[2] : v;
+    v = j == 3 ? acc[3] : v;
+    const float hv = (bit & 1) ? h_hi_f(v) : h_lo_f(v);
+    const float lb = __fmul_rd(fmaxf(__fsub_rd(hv, c.wabs), 0.f), c.lbconv);
+    if (!(lb <= c.thr[sl])) continue;
+    if (direct) {
+      const unsigned pos = atomicAdd(&a.count[sl], 1u);
+      if ((int64_t)pos < a.cap) {
+        a.cand[(size_t)sl * a.cap + pos] = make_key(lb, __ldg(a.perm + i0 + j));
+        const int fb = lb_bin(lb, c.scale[sl]);
+        atomicAdd(&a.hist[sl * kNB + (HC ? (fb | 7) : fb)], 1u);
+      }
+    } else {
+      // staged as (LB, sorted position); per-slot counts and ids are resolved at flush time
+      const int pos = (int)atomicAdd(&wb.n, 1u);
+      PARIS_DCHECK(i0 + j < a.n && pos < kWBI && sl >= 0);
+      sts_u64(lbi_key_addr(T, warp, pos), make_key(lb, (uint32_t)(i0 + j)));
+      wb.slot[pos] = (uint8_t)sl;
+    }
   }
   __syncwarp();
 }
@@ -3940,11 +3918,14 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
     set_error("paris_knn_exact: null pointer");
     return PARIS_EINVAL;
   }
-  if (n < 1 || n >= (int64_t(1) << 31) || nq < 0 || k < 1 || k > n || k > PARIS_MAX_K) {
-    set_error("paris_knn_exact: bad sizes n=%lld nq=%d k=%d (need 1<=k<=min(n,%d), n<2^31)",
+  // k <= n; k beyond PARIS_MAX_K takes the full-sort path (knn_large_k), except for
+  // the approximate search, whose answer is the seeds' top-k
+  if (n < 1 || n >= (int64_t(1) << 31) || nq < 0 || k < 1 || k > n || (approx && k > PARIS_MAX_K)) {
+    set_error("paris_knn_exact: bad sizes n=%lld nq=%d k=%d (need 1<=k<=n, n<2^31; approximate: k<=%d)",
               (long long)n, nq, k, PARIS_MAX_K);
     return PARIS_EINVAL;
   }
+  const bool large_k = k > PARIS_MAX_K;
   if (len < 4 || len > 4096 || (len % 4) || w < 1 || w > kMaxW || (len % w)) {
     set_error("paris_knn_exact: unsupported (len=%d, w=%d)", len, w);
     return PARIS_ECONFIG;
@@ -4065,13 +4046,13 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   const size_t qbytes = (size_t)nq * len * 4, ibytes = (size_t)nq * k * 8, dbytes = (size_t)nq * k * 4;
   const size_t cbytes = (size_t)nq * 4 * 5;
   auto up = [](size_t v) { return (v + 255) & ~(size_t)255; };
-  const size_t wsb = up(ws_layout(p, p.cap, nullptr, nullptr));
+  const size_t wsb = large_k ? 0 : up(ws_layout(p, p.cap, nullptr, nullptr));
   const size_t total = wsb + up(qbytes) + up(ibytes) + up(dbytes) + up(cbytes);
   void* wsh = nullptr;
   char* base = (char*)ws_acquire(total, st, &wsh, nullptr);
   if (!base) return PARIS_ENOMEM;
   Ws ws;
-  ws_layout(p, p.cap, &ws, base);
+  if (!large_k) ws_layout(p, p.cap, &ws, base);
   char* cur = base + wsb;
   float* sq = (float*)cur; cur += up(qbytes);
   int64_t* sidx = (int64_t*)cur; cur += up(ibytes);
@@ -4102,7 +4083,10 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   // (device outputs) instead of the approximate search -- measures the LB pass under an
   // ideal BSF; results stay exact for any seed
   const bool seed_from_out = cfg && cfg->reserved[3] == 1 && !hi && !hd;
-  for (int q0 = 0; q0 < nq && rc == PARIS_OK; q0 += p.B) {
+  if (large_k && rc == PARIS_OK) {
+    rc = knn_large_k(raw, n, len, d_q, nq, k, d_idx, d_dist, st);  // every series refined (no pruning)
+  }
+  for (int q0 = 0; q0 < nq && rc == PARIS_OK && !large_k; q0 += p.B) {
     const int nb = std::min(p.B, nq - q0);
     rc = run_batch(p, raw, sax, d_q + (size_t)q0 * len, nb, q0, p.cap, tab, ws, d_idx, d_dist,
                    all_count, all_refined, all_tau, all_blocks, all_extra, st, /*rescan=*/seed_from_out);
@@ -4129,6 +4113,7 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
     if (e != cudaSuccess) rc = cuda_error(e, "paris_knn_exact stats D2H");
     if (rc == PARIS_OK) {
       for (int q = 0; q < nq; ++q) {
+        if (large_k) h_count[q] = h_ref[q] = (unsigned)n;
         if (stats->candidates) stats->candidates[q] = h_count[q];
         if (stats->refined) stats->refined[q] = h_ref[q];
         if (stats->tau_seed) stats->tau_seed[q] = h_tau[q];

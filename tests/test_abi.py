@@ -46,7 +46,8 @@ def test_argument_validation_without_gpu(lib):
     assert so.paris_summarize(addr, 10, 256, 16, 100, addr, None) == lib.PARIS_ECONFIG
     # k > n -> EINVAL
     assert so.paris_knn_exact(addr, addr, 5, addr, 1, 6, addr, addr, 256, 16, 256, None) == lib.PARIS_EINVAL
-    assert so.paris_knn_exact(addr, addr, 5000, addr, 1, 2000, addr, addr, 256, 16, 256, None) == lib.PARIS_EINVAL
+    assert so.paris_knn_exact(addr, addr, 5000, addr, 1, 6000, addr, addr, 256, 16, 256, None) == lib.PARIS_EINVAL
+    assert so.paris_knn_approx(addr, addr, 5000, addr, 1, 2000, addr, addr, 256, 16, 256, None, None) == lib.PARIS_EINVAL
     assert so.paris_knn_exact(addr, addr, 5, addr, 1, 0, addr, addr, 256, 16, 256, None) == lib.PARIS_EINVAL
     # approximate search: same size checks
     assert so.paris_knn_approx(addr, addr, 5, addr, 1, 6, addr, addr, 256, 16, 256, None, None) == lib.PARIS_EINVAL

@@ -276,3 +276,18 @@ def test_gpu_member_queries_by_id(torch_dev):
 def torch_equal(a, b):
     import torch
     return bool(torch.equal(a, b))
+
+
+@pytest.mark.parametrize("k", [1025, 3000, 5003])
+def test_knn_large_k_full_sort(P, torch_dev, k):
+    """k beyond PARIS_MAX_K up to k = n: every series' distance, keys sorted --
+    equal to brute force (k = n is the full sort), on the flat and index paths."""
+    import torch
+    n = 5003
+    x = datagen.random_walks(n, 128, 8100)
+    q = datagen.random_walks(3, 128, 8101)
+    q[1] = x[4000]
+    gi, gd = _knn_case(P, torch_dev, x, q, k, w=16)
+    ri, rd2 = oracle.knn_bruteforce(x, q, k)
+    check_knn(x, q, gi, gd, ri, rd2)
+    assert gi[1, 0] == 4000
