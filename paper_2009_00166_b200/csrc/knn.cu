@@ -2282,6 +2282,7 @@ k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
   constexpr int kPF = kPFMul * U;  // bf16 pre-filter rows per warp step
   __shared__ unsigned s_refined[kMaxB], s_cnt[kMaxB], s_cut[kMaxB], s_r16[kMaxB];
   __shared__ float s_scale[kMaxB];
+  __shared__ unsigned s_pre[kMaxB + 1];  // 32-key chunks of the queries before query b
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x < kMaxB) {
     const bool on = threadIdx.x < nb;
@@ -2292,11 +2293,22 @@ k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     s_scale[threadIdx.x] = on ? bin_scale(__uint_as_float(a.thr_seed[threadIdx.x])) : 0.f;
   }
   __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned c = 0;
+    for (int b = 0; b < nb; ++b) { s_pre[b] = c; c += (s_cnt[b] + 31) / 32; }
+    s_pre[nb] = c;
+  }
+  __syncthreads();
   const unsigned gw = blockIdx.x * kRefWarps + warp, GW = gridDim.x * kRefWarps;
-  for (int b = 0; b < nb; ++b) {
+  // the batch's chunks, all queries concatenated, cut into GW contiguous ranges (k_refine1q)
+  const uint64_t C = s_pre[nb];
+  const unsigned c_lo = (unsigned)((uint64_t)gw * C / GW), c_hi = (unsigned)((uint64_t)(gw + 1) * C / GW);
+  int b = 0;
+  while (b < nb && s_pre[b + 1] <= c_lo) ++b;
+  for (; b < nb && s_pre[b] < c_hi; ++b) {
     const unsigned cnt = s_cnt[b];
-    const unsigned nchunk = (cnt + 31) / 32;
-    const unsigned first = (gw + (unsigned)b * 613u) % GW;  // rotate: spread small lists over all warps
+    const unsigned first = max(c_lo, s_pre[b]) - s_pre[b];         // this warp's chunks of query b
+    const unsigned nchunk = min(c_hi, s_pre[b + 1]) - s_pre[b];    // [first, nchunk)  // rotate: spread small lists over all warps
     if (first >= nchunk) continue;
     const float scale = s_scale[b];
     const int cutb = (int)s_cut[b];
@@ -2317,12 +2329,12 @@ k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     }
     // the next chunk's keys are loaded while this chunk is processed
     uint64_t knext = (first * 32 + lane < cnt) ? __ldg(list + first * 32 + lane) : kNoKey;
-    for (unsigned ch = first; ch < nchunk; ch += GW) {
+    for (unsigned ch = first; ch < nchunk; ++ch) {
       const unsigned i = ch * 32 + lane;
       const uint64_t k0 = knext;
       {
-        const unsigned in = (ch + GW) * 32 + lane;
-        knext = (ch + GW < nchunk && in < cnt) ? __ldg(list + in) : kNoKey;
+        const unsigned in = (ch + 1) * 32 + lane;
+        knext = (ch + 1 < nchunk && in < cnt) ? __ldg(list + in) : kNoKey;
       }
       cur = min(cur, ld_relaxed_u64(bp));
       float thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
@@ -2409,6 +2421,7 @@ __global__ void __launch_bounds__(kRefThreads, kRefQCtas)
 k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
   __shared__ unsigned s_refined[kMaxB], s_cnt[kMaxB], s_cut[kMaxB], s_r16[kMaxB];
   __shared__ float s_scale[kMaxB];
+  __shared__ unsigned s_pre[kMaxB + 1];  // 32-key chunks of the queries before query b
   __shared__ uint64_t s_queue[kRefWarps][64];
   __shared__ __align__(16) float s_qv[kRefWarps][kRefQLen];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -2422,17 +2435,30 @@ k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     s_scale[threadIdx.x] = on ? bin_scale(__uint_as_float(a.thr_seed[threadIdx.x])) : 0.f;
   }
   __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned c = 0;
+    for (int b = 0; b < nb; ++b) { s_pre[b] = c; c += (s_cnt[b] + 31) / 32; }
+    s_pre[nb] = c;
+  }
+  __syncthreads();
   const unsigned gw = blockIdx.x * kRefWarps + warp, GW = gridDim.x * kRefWarps;
+  // the batch's chunks, all queries concatenated, cut into GW contiguous ranges: a warp
+  // works through one or two queries' candidates (balanced by candidate count, few
+  // per-query setups)
+  const uint64_t C = s_pre[nb];
+  const unsigned c_lo = (unsigned)((uint64_t)gw * C / GW), c_hi = (unsigned)((uint64_t)(gw + 1) * C / GW);
   const int nh = a.len >> 3;  // uint4 (8 bf16) per row
   const int nper = (nh + 7) >> 3;  // uint4 per lane of an octet
   const float e2 = 2.f * (float)((a.len >> 4) + 8) * 5.9604644775390625e-08f;   // octet sums
   const float e2w = 2.f * (float)((a.len >> 5) + 8) * 5.9604644775390625e-08f;  // warp-tree sums
   uint64_t* queue = s_queue[warp];
   const float4* sq4 = reinterpret_cast<const float4*>(s_qv[warp]);
-  for (int b = 0; b < nb; ++b) {
+  int b = 0;
+  while (b < nb && s_pre[b + 1] <= c_lo) ++b;
+  for (; b < nb && s_pre[b] < c_hi; ++b) {
     const unsigned cnt = s_cnt[b];
-    const unsigned nchunk = (cnt + 31) / 32;
-    const unsigned first = (gw + (unsigned)b * 613u) % GW;  // rotate: spread small lists over all warps
+    const unsigned first = max(c_lo, s_pre[b]) - s_pre[b];         // this warp's chunks of query b
+    const unsigned nchunk = min(c_hi, s_pre[b + 1]) - s_pre[b];    // [first, nchunk)
     if (first >= nchunk) continue;
     const float scale = s_scale[b];
     const int cutb = (int)s_cut[b];
@@ -2530,12 +2556,12 @@ k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     };
 
     uint64_t knext = (first * 32 + lane < cnt) ? __ldg(list + first * 32 + lane) : kNoKey;
-    for (unsigned ch = first; ch < nchunk; ch += GW) {
+    for (unsigned ch = first; ch < nchunk; ++ch) {
       const unsigned i = ch * 32 + lane;
       const uint64_t k0 = knext;
       {
-        const unsigned in = (ch + GW) * 32 + lane;
-        knext = (ch + GW < nchunk && in < cnt) ? __ldg(list + in) : kNoKey;
+        const unsigned in = (ch + 1) * 32 + lane;
+        knext = (ch + 1 < nchunk && in < cnt) ? __ldg(list + in) : kNoKey;
       }
       cur = min(cur, ld_relaxed_u64(bp));
       const float thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
@@ -2676,6 +2702,7 @@ k_refine_kx(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut, ui
             unsigned* __restrict__ res_cnt) {
   __shared__ unsigned s_refined[kMaxB], s_cnt[kMaxB], s_cut[kMaxB];
   __shared__ float s_scale[kMaxB];
+  __shared__ unsigned s_pre[kMaxB + 1];  // 32-key chunks of the queries before query b
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x < kMaxB) {
     const bool on = threadIdx.x < nb;
@@ -2685,11 +2712,22 @@ k_refine_kx(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut, ui
     s_scale[threadIdx.x] = on ? bin_scale(__uint_as_float(a.thr_seed[threadIdx.x])) : 0.f;
   }
   __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned c = 0;
+    for (int b = 0; b < nb; ++b) { s_pre[b] = c; c += (s_cnt[b] + 31) / 32; }
+    s_pre[nb] = c;
+  }
+  __syncthreads();
   const unsigned gw = blockIdx.x * kRefWarps + warp, GW = gridDim.x * kRefWarps;
-  for (int b = 0; b < nb; ++b) {
+  // the batch's chunks, all queries concatenated, cut into GW contiguous ranges (k_refine1q)
+  const uint64_t C = s_pre[nb];
+  const unsigned c_lo = (unsigned)((uint64_t)gw * C / GW), c_hi = (unsigned)((uint64_t)(gw + 1) * C / GW);
+  int b = 0;
+  while (b < nb && s_pre[b + 1] <= c_lo) ++b;
+  for (; b < nb && s_pre[b] < c_hi; ++b) {
     const unsigned cnt = s_cnt[b];
-    const unsigned nchunk = (cnt + 31) / 32;
-    const unsigned first = (gw + (unsigned)b * 613u) % GW;
+    const unsigned first = max(c_lo, s_pre[b]) - s_pre[b];         // this warp's chunks of query b
+    const unsigned nchunk = min(c_hi, s_pre[b + 1]) - s_pre[b];    // [first, nchunk)
     if (first >= nchunk) continue;
     const float scale = s_scale[b];
     const int cutb = (int)s_cut[b];
@@ -2700,12 +2738,12 @@ k_refine_kx(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut, ui
     // wave B starts from the threshold wave A's results imply
     if (wave == 1 && scale > 0.f) hist_threshold(a, b, scale);
     uint64_t knext = (first * 32 + lane < cnt) ? __ldg(list + first * 32 + lane) : kNoKey;
-    for (unsigned ch = first; ch < nchunk; ch += GW) {
+    for (unsigned ch = first; ch < nchunk; ++ch) {
       const unsigned i = ch * 32 + lane;
       const uint64_t k0 = knext;
       {
-        const unsigned in = (ch + GW) * 32 + lane;
-        knext = (ch + GW < nchunk && in < cnt) ? __ldg(list + in) : kNoKey;
+        const unsigned in = (ch + 1) * 32 + lane;
+        knext = (ch + 1 < nchunk && in < cnt) ? __ldg(list + in) : kNoKey;
       }
       float thr = __uint_as_float(ld_relaxed_u32(&a.thr[b * kPadU32]));
       const float lb0 = key_val(k0);
