@@ -2242,6 +2242,10 @@ k_refine1(RefineArgs a, int nb) {
 #define PARIS_REFU_CTAS 6
 #endif
 constexpr int kRefUCtas = PARIS_REFU_CTAS;
+#ifndef PARIS_REF_RUN
+#define PARIS_REF_RUN 8
+#endif
+constexpr uint64_t kRefRun = PARIS_REF_RUN;  // consecutive 32-key chunks a refine warp takes at a time
 #ifndef PARIS_REFU_U
 #define PARIS_REFU_U 2
 #endif
@@ -2300,12 +2304,13 @@ k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
   }
   __syncthreads();
   const unsigned gw = blockIdx.x * kRefWarps + warp, GW = gridDim.x * kRefWarps;
-  // the batch's chunks, all queries concatenated, cut into GW contiguous ranges (k_refine1q)
+  // the batch's chunks, all queries concatenated, dealt in runs of kRefRun (k_refine1q)
   const uint64_t C = s_pre[nb];
-  const unsigned c_lo = (unsigned)((uint64_t)gw * C / GW), c_hi = (unsigned)((uint64_t)(gw + 1) * C / GW);
-  int b = 0;
-  while (b < nb && s_pre[b + 1] <= c_lo) ++b;
-  for (; b < nb && s_pre[b] < c_hi; ++b) {
+  int b0 = 0;
+  for (uint64_t run = gw; run * kRefRun < C; run += GW) {
+  const unsigned c_lo = (unsigned)(run * kRefRun), c_hi = (unsigned)min(C, run * kRefRun + kRefRun);
+  while (b0 < nb && s_pre[b0 + 1] <= c_lo) ++b0;
+  for (int b = b0; b < nb && s_pre[b] < c_hi; ++b) {
     const unsigned cnt = s_cnt[b];
     const unsigned first = max(c_lo, s_pre[b]) - s_pre[b];         // this warp's chunks of query b
     const unsigned nchunk = min(c_hi, s_pre[b + 1]) - s_pre[b];    // [first, nchunk)  // rotate: spread small lists over all warps
@@ -2393,6 +2398,7 @@ k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     if (lane == 0 && nref) atomicAdd(&s_refined[b], nref);
     if (lane == 0 && nref16) atomicAdd(&s_r16[b], nref16);
   }
+  }  // runs
   __syncthreads();
   if (threadIdx.x < nb && s_refined[threadIdx.x]) atomicAdd(&a.refined[threadIdx.x], s_refined[threadIdx.x]);
   if (threadIdx.x < nb && s_r16[threadIdx.x]) atomicAdd(&a.refined16[threadIdx.x], s_r16[threadIdx.x]);
@@ -2442,20 +2448,22 @@ k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
   }
   __syncthreads();
   const unsigned gw = blockIdx.x * kRefWarps + warp, GW = gridDim.x * kRefWarps;
-  // the batch's chunks, all queries concatenated, cut into GW contiguous ranges: a warp
-  // works through one or two queries' candidates (balanced by candidate count, few
-  // per-query setups)
+  // the batch's chunks, all queries concatenated, dealt to the warps in runs of kRefRun
+  // consecutive chunks, round-robin: a warp sees every part of the batch (balanced: the
+  // share of candidates that pass the BSF test varies a lot between queries) but sets up
+  // a query only once per run instead of once per query (C / (GW kRefRun) runs per warp)
   const uint64_t C = s_pre[nb];
-  const unsigned c_lo = (unsigned)((uint64_t)gw * C / GW), c_hi = (unsigned)((uint64_t)(gw + 1) * C / GW);
   const int nh = a.len >> 3;  // uint4 (8 bf16) per row
   const int nper = (nh + 7) >> 3;  // uint4 per lane of an octet
   const float e2 = 2.f * (float)((a.len >> 4) + 8) * 5.9604644775390625e-08f;   // octet sums
   const float e2w = 2.f * (float)((a.len >> 5) + 8) * 5.9604644775390625e-08f;  // warp-tree sums
   uint64_t* queue = s_queue[warp];
   const float4* sq4 = reinterpret_cast<const float4*>(s_qv[warp]);
-  int b = 0;
-  while (b < nb && s_pre[b + 1] <= c_lo) ++b;
-  for (; b < nb && s_pre[b] < c_hi; ++b) {
+  int b0 = 0;
+  for (uint64_t run = gw; run * kRefRun < C; run += GW) {
+  const unsigned c_lo = (unsigned)(run * kRefRun), c_hi = (unsigned)min(C, run * kRefRun + kRefRun);
+  while (b0 < nb && s_pre[b0 + 1] <= c_lo) ++b0;
+  for (int b = b0; b < nb && s_pre[b] < c_hi; ++b) {
     const unsigned cnt = s_cnt[b];
     const unsigned first = max(c_lo, s_pre[b]) - s_pre[b];         // this warp's chunks of query b
     const unsigned nchunk = min(c_hi, s_pre[b + 1]) - s_pre[b];    // [first, nchunk)
@@ -2585,6 +2593,7 @@ k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     if (lane == 0 && nref) atomicAdd(&s_refined[b], nref);
     if (lane == 0 && nref16) atomicAdd(&s_r16[b], nref16);
   }
+  }  // runs
   __syncthreads();
   if (threadIdx.x < nb && s_refined[threadIdx.x]) atomicAdd(&a.refined[threadIdx.x], s_refined[threadIdx.x]);
   if (threadIdx.x < nb && s_r16[threadIdx.x]) atomicAdd(&a.refined16[threadIdx.x], s_r16[threadIdx.x]);
@@ -2719,12 +2728,13 @@ k_refine_kx(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut, ui
   }
   __syncthreads();
   const unsigned gw = blockIdx.x * kRefWarps + warp, GW = gridDim.x * kRefWarps;
-  // the batch's chunks, all queries concatenated, cut into GW contiguous ranges (k_refine1q)
+  // the batch's chunks, all queries concatenated, dealt in runs of kRefRun (k_refine1q)
   const uint64_t C = s_pre[nb];
-  const unsigned c_lo = (unsigned)((uint64_t)gw * C / GW), c_hi = (unsigned)((uint64_t)(gw + 1) * C / GW);
-  int b = 0;
-  while (b < nb && s_pre[b + 1] <= c_lo) ++b;
-  for (; b < nb && s_pre[b] < c_hi; ++b) {
+  int b0 = 0;
+  for (uint64_t run = gw; run * kRefRun < C; run += GW) {
+  const unsigned c_lo = (unsigned)(run * kRefRun), c_hi = (unsigned)min(C, run * kRefRun + kRefRun);
+  while (b0 < nb && s_pre[b0 + 1] <= c_lo) ++b0;
+  for (int b = b0; b < nb && s_pre[b] < c_hi; ++b) {
     const unsigned cnt = s_cnt[b];
     const unsigned first = max(c_lo, s_pre[b]) - s_pre[b];         // this warp's chunks of query b
     const unsigned nchunk = min(c_hi, s_pre[b + 1]) - s_pre[b];    // [first, nchunk)
@@ -2770,6 +2780,7 @@ k_refine_kx(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut, ui
     }
     if (lane == 0 && nref) atomicAdd(&s_refined[b], nref);
   }
+  }  // runs
   __syncthreads();
   if (threadIdx.x < nb && s_refined[threadIdx.x]) atomicAdd(&a.refined[threadIdx.x], s_refined[threadIdx.x]);
 }
