@@ -2242,10 +2242,6 @@ k_refine1(RefineArgs a, int nb) {
 #define PARIS_REFU_CTAS 6
 #endif
 constexpr int kRefUCtas = PARIS_REFU_CTAS;
-#ifndef PARIS_REF_RUN
-#define PARIS_REF_RUN 8
-#endif
-constexpr uint64_t kRefRun = PARIS_REF_RUN;  // consecutive 32-key chunks a refine warp takes at a time
 #ifndef PARIS_REFU_U
 #define PARIS_REFU_U 2
 #endif
@@ -2286,7 +2282,6 @@ k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
   constexpr int kPF = kPFMul * U;  // bf16 pre-filter rows per warp step
   __shared__ unsigned s_refined[kMaxB], s_cnt[kMaxB], s_cut[kMaxB], s_r16[kMaxB];
   __shared__ float s_scale[kMaxB];
-  __shared__ unsigned s_pre[kMaxB + 1];  // 32-key chunks of the queries before query b
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x < kMaxB) {
     const bool on = threadIdx.x < nb;
@@ -2297,23 +2292,11 @@ k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     s_scale[threadIdx.x] = on ? bin_scale(__uint_as_float(a.thr_seed[threadIdx.x])) : 0.f;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned c = 0;
-    for (int b = 0; b < nb; ++b) { s_pre[b] = c; c += (s_cnt[b] + 31) / 32; }
-    s_pre[nb] = c;
-  }
-  __syncthreads();
   const unsigned gw = blockIdx.x * kRefWarps + warp, GW = gridDim.x * kRefWarps;
-  // the batch's chunks, all queries concatenated, dealt in runs of kRefRun (k_refine1q)
-  const uint64_t C = s_pre[nb];
-  int b0 = 0;
-  for (uint64_t run = gw; run * kRefRun < C; run += GW) {
-  const unsigned c_lo = (unsigned)(run * kRefRun), c_hi = (unsigned)min(C, run * kRefRun + kRefRun);
-  while (b0 < nb && s_pre[b0 + 1] <= c_lo) ++b0;
-  for (int b = b0; b < nb && s_pre[b] < c_hi; ++b) {
+  for (int b = 0; b < nb; ++b) {
     const unsigned cnt = s_cnt[b];
-    const unsigned first = max(c_lo, s_pre[b]) - s_pre[b];         // this warp's chunks of query b
-    const unsigned nchunk = min(c_hi, s_pre[b + 1]) - s_pre[b];    // [first, nchunk)  // rotate: spread small lists over all warps
+    const unsigned nchunk = (cnt + 31) / 32;
+    const unsigned first = (gw + (unsigned)b * 613u) % GW;  // rotate: spread small lists over all warps
     if (first >= nchunk) continue;
     const float scale = s_scale[b];
     const int cutb = (int)s_cut[b];
@@ -2334,12 +2317,12 @@ k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     }
     // the next chunk's keys are loaded while this chunk is processed
     uint64_t knext = (first * 32 + lane < cnt) ? __ldg(list + first * 32 + lane) : kNoKey;
-    for (unsigned ch = first; ch < nchunk; ++ch) {
+    for (unsigned ch = first; ch < nchunk; ch += GW) {
       const unsigned i = ch * 32 + lane;
       const uint64_t k0 = knext;
       {
-        const unsigned in = (ch + 1) * 32 + lane;
-        knext = (ch + 1 < nchunk && in < cnt) ? __ldg(list + in) : kNoKey;
+        const unsigned in = (ch + GW) * 32 + lane;
+        knext = (ch + GW < nchunk && in < cnt) ? __ldg(list + in) : kNoKey;
       }
       cur = min(cur, ld_relaxed_u64(bp));
       float thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
@@ -2398,7 +2381,6 @@ k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     if (lane == 0 && nref) atomicAdd(&s_refined[b], nref);
     if (lane == 0 && nref16) atomicAdd(&s_r16[b], nref16);
   }
-  }  // runs
   __syncthreads();
   if (threadIdx.x < nb && s_refined[threadIdx.x]) atomicAdd(&a.refined[threadIdx.x], s_refined[threadIdx.x]);
   if (threadIdx.x < nb && s_r16[threadIdx.x]) atomicAdd(&a.refined16[threadIdx.x], s_r16[threadIdx.x]);
@@ -2420,16 +2402,15 @@ k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
 #define PARIS_REFQ_CTAS 3
 #endif
 constexpr int kRefQCtas = PARIS_REFQ_CTAS;
-constexpr int kRefQLen = 256;  // longest row of the octet form (query staged in shared memory)
+constexpr int kRefQLen = 256;  // longest row of the octet form
 
 template <int NC, int U>
 __global__ void __launch_bounds__(kRefThreads, kRefQCtas)
 k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
   __shared__ unsigned s_refined[kMaxB], s_cnt[kMaxB], s_cut[kMaxB], s_r16[kMaxB];
   __shared__ float s_scale[kMaxB];
-  __shared__ unsigned s_pre[kMaxB + 1];  // 32-key chunks of the queries before query b
   __shared__ uint64_t s_queue[kRefWarps][64];
-  __shared__ __align__(16) float s_qv[kRefWarps][kRefQLen];
+  __shared__ float s_qn[kMaxB];  // per query: qn_hi >= ||q||
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int oct = lane >> 3, sub = lane & 7;
   if (threadIdx.x < kMaxB) {
@@ -2440,33 +2421,27 @@ k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     s_cut[threadIdx.x] = on ? cut[threadIdx.x * kNB] : 0u;
     s_scale[threadIdx.x] = on ? bin_scale(__uint_as_float(a.thr_seed[threadIdx.x])) : 0.f;
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned c = 0;
-    for (int b = 0; b < nb; ++b) { s_pre[b] = c; c += (s_cnt[b] + 31) / 32; }
-    s_pre[nb] = c;
+  const float e2w = 2.f * (float)((a.len >> 5) + 8) * 5.9604644775390625e-08f;  // warp-tree sums
+  for (int b = warp; b < nb; b += kRefWarps) {  // the query norms, once per CTA
+    const float4* qv = reinterpret_cast<const float4*>(a.queries + (size_t)b * a.len);
+    float qs = 0.f;
+    for (int f = lane; f < (a.len >> 2); f += 32) {
+      const float4 v = __ldg(qv + f);
+      qs = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, qs))));
+    }
+    qs = warp_sum(qs);
+    if (lane == 0) s_qn[b] = __fsqrt_ru(__fmul_ru(qs, 1.f + e2w));
   }
   __syncthreads();
   const unsigned gw = blockIdx.x * kRefWarps + warp, GW = gridDim.x * kRefWarps;
-  // the batch's chunks, all queries concatenated, dealt to the warps in runs of kRefRun
-  // consecutive chunks, round-robin: a warp sees every part of the batch (balanced: the
-  // share of candidates that pass the BSF test varies a lot between queries) but sets up
-  // a query only once per run instead of once per query (C / (GW kRefRun) runs per warp)
-  const uint64_t C = s_pre[nb];
   const int nh = a.len >> 3;  // uint4 (8 bf16) per row
   const int nper = (nh + 7) >> 3;  // uint4 per lane of an octet
   const float e2 = 2.f * (float)((a.len >> 4) + 8) * 5.9604644775390625e-08f;   // octet sums
-  const float e2w = 2.f * (float)((a.len >> 5) + 8) * 5.9604644775390625e-08f;  // warp-tree sums
   uint64_t* queue = s_queue[warp];
-  const float4* sq4 = reinterpret_cast<const float4*>(s_qv[warp]);
-  int b0 = 0;
-  for (uint64_t run = gw; run * kRefRun < C; run += GW) {
-  const unsigned c_lo = (unsigned)(run * kRefRun), c_hi = (unsigned)min(C, run * kRefRun + kRefRun);
-  while (b0 < nb && s_pre[b0 + 1] <= c_lo) ++b0;
-  for (int b = b0; b < nb && s_pre[b] < c_hi; ++b) {
+  for (int b = 0; b < nb; ++b) {
     const unsigned cnt = s_cnt[b];
-    const unsigned first = max(c_lo, s_pre[b]) - s_pre[b];         // this warp's chunks of query b
-    const unsigned nchunk = min(c_hi, s_pre[b + 1]) - s_pre[b];    // [first, nchunk)
+    const unsigned nchunk = (cnt + 31) / 32;
+    const unsigned first = (gw + (unsigned)b * 613u) % GW;  // rotate: spread small lists over all warps
     if (first >= nchunk) continue;
     const float scale = s_scale[b];
     const int cutb = (int)s_cut[b];
@@ -2475,15 +2450,7 @@ k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     unsigned long long* bp = a.best + (size_t)b * kPadU64;
     unsigned nref = 0, nref16 = 0;
     uint64_t cur = kNoKey;
-    __syncwarp();
-    float qs = 0.f;  // the query in shared memory and qn_hi >= ||q||
-    for (int f = lane; f < (a.len >> 2); f += 32) {
-      const float4 v = __ldg(qv + f);
-      reinterpret_cast<float4*>(s_qv[warp])[f] = v;
-      qs = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, qs))));
-    }
-    const float qn_hi = __fsqrt_ru(__fmul_ru(warp_sum(qs), 1.f + e2w));
-    __syncwarp();
+    const float qn_hi = s_qn[b];
     int qn = 0;  // queued keys
 
     // the queued keys [0, m): octet o takes keys 8r + o and 8r + 4 + o of round r
@@ -2517,7 +2484,7 @@ k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
           for (int i = 0; i < 4; ++i) {
             const int f = sub + 8 * (i0 + i);
             if (i0 + i >= nper || f >= nh) break;
-            const float4 q0 = sq4[2 * f], q1 = sq4[2 * f + 1];
+            const float4 q0 = __ldg(qv + 2 * f), q1 = __ldg(qv + 2 * f + 1);  // L1-resident query
             const float qq[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
@@ -2564,12 +2531,12 @@ k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     };
 
     uint64_t knext = (first * 32 + lane < cnt) ? __ldg(list + first * 32 + lane) : kNoKey;
-    for (unsigned ch = first; ch < nchunk; ++ch) {
+    for (unsigned ch = first; ch < nchunk; ch += GW) {
       const unsigned i = ch * 32 + lane;
       const uint64_t k0 = knext;
       {
-        const unsigned in = (ch + 1) * 32 + lane;
-        knext = (ch + 1 < nchunk && in < cnt) ? __ldg(list + in) : kNoKey;
+        const unsigned in = (ch + GW) * 32 + lane;
+        knext = (ch + GW < nchunk && in < cnt) ? __ldg(list + in) : kNoKey;
       }
       cur = min(cur, ld_relaxed_u64(bp));
       const float thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
@@ -2593,7 +2560,6 @@ k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     if (lane == 0 && nref) atomicAdd(&s_refined[b], nref);
     if (lane == 0 && nref16) atomicAdd(&s_r16[b], nref16);
   }
-  }  // runs
   __syncthreads();
   if (threadIdx.x < nb && s_refined[threadIdx.x]) atomicAdd(&a.refined[threadIdx.x], s_refined[threadIdx.x]);
   if (threadIdx.x < nb && s_r16[threadIdx.x]) atomicAdd(&a.refined16[threadIdx.x], s_r16[threadIdx.x]);
@@ -2711,7 +2677,6 @@ k_refine_kx(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut, ui
             unsigned* __restrict__ res_cnt) {
   __shared__ unsigned s_refined[kMaxB], s_cnt[kMaxB], s_cut[kMaxB];
   __shared__ float s_scale[kMaxB];
-  __shared__ unsigned s_pre[kMaxB + 1];  // 32-key chunks of the queries before query b
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x < kMaxB) {
     const bool on = threadIdx.x < nb;
@@ -2721,23 +2686,11 @@ k_refine_kx(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut, ui
     s_scale[threadIdx.x] = on ? bin_scale(__uint_as_float(a.thr_seed[threadIdx.x])) : 0.f;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned c = 0;
-    for (int b = 0; b < nb; ++b) { s_pre[b] = c; c += (s_cnt[b] + 31) / 32; }
-    s_pre[nb] = c;
-  }
-  __syncthreads();
   const unsigned gw = blockIdx.x * kRefWarps + warp, GW = gridDim.x * kRefWarps;
-  // the batch's chunks, all queries concatenated, dealt in runs of kRefRun (k_refine1q)
-  const uint64_t C = s_pre[nb];
-  int b0 = 0;
-  for (uint64_t run = gw; run * kRefRun < C; run += GW) {
-  const unsigned c_lo = (unsigned)(run * kRefRun), c_hi = (unsigned)min(C, run * kRefRun + kRefRun);
-  while (b0 < nb && s_pre[b0 + 1] <= c_lo) ++b0;
-  for (int b = b0; b < nb && s_pre[b] < c_hi; ++b) {
+  for (int b = 0; b < nb; ++b) {
     const unsigned cnt = s_cnt[b];
-    const unsigned first = max(c_lo, s_pre[b]) - s_pre[b];         // this warp's chunks of query b
-    const unsigned nchunk = min(c_hi, s_pre[b + 1]) - s_pre[b];    // [first, nchunk)
+    const unsigned nchunk = (cnt + 31) / 32;
+    const unsigned first = (gw + (unsigned)b * 613u) % GW;
     if (first >= nchunk) continue;
     const float scale = s_scale[b];
     const int cutb = (int)s_cut[b];
@@ -2748,12 +2701,12 @@ k_refine_kx(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut, ui
     // wave B starts from the threshold wave A's results imply
     if (wave == 1 && scale > 0.f) hist_threshold(a, b, scale);
     uint64_t knext = (first * 32 + lane < cnt) ? __ldg(list + first * 32 + lane) : kNoKey;
-    for (unsigned ch = first; ch < nchunk; ++ch) {
+    for (unsigned ch = first; ch < nchunk; ch += GW) {
       const unsigned i = ch * 32 + lane;
       const uint64_t k0 = knext;
       {
-        const unsigned in = (ch + 1) * 32 + lane;
-        knext = (ch + 1 < nchunk && in < cnt) ? __ldg(list + in) : kNoKey;
+        const unsigned in = (ch + GW) * 32 + lane;
+        knext = (ch + GW < nchunk && in < cnt) ? __ldg(list + in) : kNoKey;
       }
       float thr = __uint_as_float(ld_relaxed_u32(&a.thr[b * kPadU32]));
       const float lb0 = key_val(k0);
@@ -2780,7 +2733,6 @@ k_refine_kx(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut, ui
     }
     if (lane == 0 && nref) atomicAdd(&s_refined[b], nref);
   }
-  }  // runs
   __syncthreads();
   if (threadIdx.x < nb && s_refined[threadIdx.x]) atomicAdd(&a.refined[threadIdx.x], s_refined[threadIdx.x]);
 }
