@@ -358,6 +358,14 @@ def run_gpu(args):
             e1.record()
             torch.cuda.synchronize()
             raw16_ms = e0.elapsed_time(e1)
+    paa16, paa_ms = None, None
+    if args.paa and use_index and not (args.raw_host or args.raw_file):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        paa16 = P.paa_f16(raw, args.paa)
+        e1.record()
+        torch.cuda.synchronize()
+        paa_ms = e0.elapsed_time(e1)
     sax = torch.empty((W, n_local), dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
     log(f"rank {rank}: generated ids [{lo}, {hi}) of n={n} len={length} nq={nq} in {time.time() - t0:.1f}s")
@@ -428,7 +436,7 @@ def run_gpu(args):
 
     def local_fn(path, kcfg):
         if path == "index":
-            return par.local_index_search(raw, index, config=kcfg, raw16=raw16)
+            return par.local_index_search(raw, index, config=kcfg, raw16=raw16, paa16=paa16)
         if path == "nb":
             return lambda qq, kk, tau_in=None: P.knn_nb(raw, sax, qq, w=W, card=CARD, config=kcfg)
         return par.local_flat_search(raw, sax, W, CARD, config=kcfg)
@@ -448,7 +456,7 @@ def run_gpu(args):
 
         def knn_local(qsrc, **kw):
             if use_idx:
-                return P.knn_index(raw, index, qsrc, k=k, raw16=raw16, **kw)
+                return P.knn_index(raw, index, qsrc, k=k, raw16=raw16, paa16=paa16, **kw)
             if use_nb:
                 return P.knn_nb(raw, sax, qsrc, w=W, card=CARD, **kw)
             return P.knn_exact(raw, sax, qsrc, k=k, w=W, card=CARD, **kw)
@@ -540,7 +548,8 @@ def run_gpu(args):
             "lb_pass": (nbatches * n_local * W + 8.0 * cand.sum()) / nbatches,
             # raw bytes per refined series (K6): fp32 rows + the bf16 rows of the pre-filter
             "refine": (4.0 * length * refined.sum()
-                       + 2.0 * length * stats["raw16_rows"].numpy().astype(np.float64).sum()) / nbatches,
+                       + 2.0 * length * stats["raw16_rows"].numpy().astype(np.float64).sum()
+                       + 2.0 * (args.paa or 0) * stats["paa_rows"].numpy().astype(np.float64).sum()) / nbatches,
             # nb-ParIS+ workers: the SAX array + the raw series they read
             "nb_distcomp": (nbatches * n_local * W + 4.0 * length * refined.sum()) / nbatches,
         }
@@ -608,12 +617,12 @@ def run_gpu(args):
     def timed_index(qsrc, kk):
         """q/s and pruning of the index path on a query set (events, one GPU)."""
         kc = P.KnnConfig(batch=args.batch or 64, index_seeds=args.index_seeds)
-        _, _, stq = P.knn_index(raw, index, qsrc, k=kk, config=kc, stats=True, raw16=raw16)
+        _, _, stq = P.knn_index(raw, index, qsrc, k=kk, config=kc, stats=True, raw16=raw16, paa16=paa16)
         torch.cuda.synchronize()
         e0.record(st)
         for _ in range(args.steps):
             for c0 in range(0, qsrc.shape[0], call_q):
-                P.knn_index(raw, index, qsrc[c0:c0 + call_q], k=kk, config=kc, raw16=raw16)
+                P.knn_index(raw, index, qsrc[c0:c0 + call_q], k=kk, config=kc, raw16=raw16, paa16=paa16)
         e1.record(st)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / args.steps
@@ -704,6 +713,7 @@ def run_gpu(args):
             "config": {"workload": cfg["desc"] + ("" if args.sigma is None else f" [queries: sigma = {args.sigma}]"), "n": n, "len": length, "w": W, "card": CARD, "nq": nq, "k": k,
                        "batch": primary["batch"], "path": args.path, "index_build_ms": index_ms,
                        "raw_bf16": None if raw16 is None else {"build_ms": raw16_ms, "bytes": raw16.numel() * 2},
+                       "paa_f16": None if paa16 is None else {"w2": args.paa, "build_ms": paa_ms, "bytes": paa16.numel() * 2},
                        "parallelism": (f"shard x{ws} by series id (tau all-reduce(min) + all-gather + exact merge)"
                                        if sharded else f"weak x{ws} (independent collections + queries per GPU)"),
                        "l2": "inputs larger than L2 (no flush)",
@@ -740,6 +750,7 @@ def run_gpu(args):
                         "refined_top5_share": float(np.sort(refined)[-5:].sum() / max(1.0, refined.sum())),
                         "bsf_updates_mean": primary.get("bsf_updates_mean"),
                         "raw16_rows_mean": float(stats["raw16_rows"].numpy().astype(np.float64).mean()),
+                        "paa_rows_mean": float(stats["paa_rows"].numpy().astype(np.float64).mean()),
                         "note": "rank 0's shard" if ws > 1 and sharded else None},
         }
         print(json.dumps(line), flush=True)
@@ -777,6 +788,9 @@ def main():
     ap.add_argument("--raw16", action="store_true", help="(default) index path with the bf16 refinement "
                     "pre-filter (paris_raw_bf16 + paris_knn_index_x)")
     ap.add_argument("--no-raw16", action="store_true", help="index path without the bf16 pre-filter")
+    ap.add_argument("--paa", type=int, default=0, choices=[0, 32, 64],
+                    help="index path: the fp16 PAA pre-filter at this many segments (paris_paa_f16 + "
+                         "paris_knn_index_aux); 0 = off")
     ap.add_argument("--no-sweep", action="store_true", help="skip the C2 k=10 / C5 sigma x k sweeps")
     ap.add_argument("--raw-host", action="store_true",
                     help="f3: keep the raw collection in pinned host memory (SAX/index in HBM)")

@@ -187,6 +187,7 @@ typedef struct paris_knn_stats {
   int64_t* bsf_updates; /* paris_knn_nb: updates of the workers' private BSF copies   */
   int64_t* raw16_rows;  /* paris_knn_index_x: bf16 rows read by the refinement pre-filter
                            (refined = the fp32 rows read after it)                     */
+  int64_t* paa_rows;    /* paris_knn_index_aux: fp16 PAA rows read by the PAA pre-filter */
 } paris_knn_stats;
 
 /* Same as paris_knn_exact with tunables and optional stats (either may be NULL). */
@@ -259,6 +260,37 @@ int paris_knn_index_x(const float* raw, const uint16_t* raw_bf16, const uint8_t*
                       const paris_knn_config* config, paris_knn_stats* stats);
 
 /*
+ * paris_paa_f16 -- the PAA of every raw series at w2 segments (w2 | len, w2 % 8 == 0,
+ * w2 <= 256), each mean computed in fp64 and rounded to nearest fp16 (|mean| >= 65000 -> NaN,
+ * which disables the filter for that series): out device [n][w2] fp16 bits, 16-byte aligned
+ * (a B200 addition, not in the paper: 2 w2 bytes per series -- 128 B at w2 = 64 against 1 KB of
+ * raw -- for the PAA pre-filter of paris_knn_index_aux).  Asynchronous on `stream`.
+ */
+int paris_paa_f16(const float* raw, int64_t n, int32_t len, int32_t w2, uint16_t* out, void* stream);
+
+/* Refinement pre-filters for paris_knn_index_aux (NULL members = off). */
+typedef struct paris_refine_aux {
+  const uint16_t* raw_bf16; /* [n][len] bf16 copy of raw (paris_raw_bf16), or NULL                */
+  const uint16_t* paa16;    /* [n][w2] fp16 PAA of raw (paris_paa_f16), or NULL                     */
+  int32_t w2;               /* segments of paa16: 32 or 64 (w2 | len)                              */
+  int32_t reserved;
+} paris_refine_aux;
+
+/*
+ * paris_knn_index_aux -- paris_knn_index_ex with refinement pre-filters (k = 1, len <= 256):
+ * a candidate that passes the LB test against the live BSF first meets the PAA lower bound
+ * ED(q, x) >= sqrt(len/w2) ||PAA_w2(q) - PAA_w2(x)|| (Keogh's PAA bound; the fp16 rounding of
+ * the stored PAA bounded rigorously) -- the w2 > w resolution prunes most of the
+ * candidates the iSAX bound let through, reading 2 w2 bytes instead of the raw row -- then, if
+ * given, the bf16 bound of paris_knn_index_x, then the exact fp32 distance.  Same exact
+ * results as paris_knn_index; k > 1 ignores the filters.  Stats: paa_rows.
+ */
+int paris_knn_index_aux(const float* raw, const uint8_t* sax_sorted, const uint32_t* perm, const uint8_t* env, int64_t n,
+                        const float* queries, int32_t nq, int32_t k, int64_t* out_idx, float* out_dist, int32_t len,
+                        int32_t w, int32_t card, void* stream, const paris_refine_aux* aux,
+                        const paris_knn_config* config, paris_knn_stats* stats);
+
+/*
  * paris_knn_nb -- exact 1-NN with nb-ParIS+ (Alg7-Alg8,
  * P:1158-1246): the same seed as paris_knn_exact (approximate search analog),
  * then SAX is split into contiguous parts, one per DistComp worker (a warp);
@@ -293,7 +325,8 @@ void paris_release_workspace(void);
 const char* paris_last_error(void);
 
 /* ABI version (major*100 + minor). */
-int32_t paris_version(void);  /* 106: asynchronous k-NN calls, device-side overflow, paris_release_workspace,
+int32_t paris_version(void);  /* 107: paris_paa_f16, paris_knn_index_aux (PAA pre-filter);
+                                 106: asynchronous k-NN calls, device-side overflow, paris_release_workspace,
                                  paris_knn_approx / paris_knn_index_approx, paris_knn_config.tau_in */
 
 /* Test hook: the library's own fp64 breakpoints cut_1..cut_{card-1} (R2) into

@@ -13,7 +13,7 @@ from ._binding import (  # noqa: F401
     PARIS_EINVAL, PARIS_ECONFIG, PARIS_ECUDA, PARIS_ENOMEM, PARIS_MAX_K,
     ParisError, KnnConfig, Index, PARIS_INDEX_BLOCK, PARIS_INDEX_TILE, library_path, load, summarize, knn_exact,
     summarize_file, MappedRaw,
-    index_build, knn_index, knn_nb, knn_approx, merge_topk, last_error, raw_bf16, release_workspace,
+    index_build, knn_index, knn_nb, knn_approx, merge_topk, last_error, raw_bf16, paa_f16, release_workspace,
     profile_enable, profile_reset, profile_read, launch_count, version, debug_cuts, debug_half_dir, debug_read_probe,
     debug_hfma2_probe, symbols,
 )

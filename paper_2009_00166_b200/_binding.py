@@ -38,7 +38,13 @@ class _Config(ctypes.Structure):
 class _Stats(ctypes.Structure):
     _fields_ = [("candidates", ctypes.c_void_p), ("refined", ctypes.c_void_p),
                 ("tau_seed", ctypes.c_void_p), ("lb_blocks", ctypes.c_void_p),
-                ("bsf_updates", ctypes.c_void_p), ("raw16_rows", ctypes.c_void_p)]
+                ("bsf_updates", ctypes.c_void_p), ("raw16_rows", ctypes.c_void_p),
+                ("paa_rows", ctypes.c_void_p)]
+
+
+class _Aux(ctypes.Structure):
+    _fields_ = [("raw_bf16", ctypes.c_void_p), ("paa16", ctypes.c_void_p), ("w2", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
 
 class _KProf(ctypes.Structure):
@@ -95,6 +101,11 @@ def load():
         lib.paris_knn_index_x.argtypes = [P, P, P, P, P, i64, P, i32, i32, P, P, i32, i32, i32, P,
                                           ctypes.POINTER(_Config), ctypes.POINTER(_Stats)]
         lib.paris_knn_index_x.restype = ctypes.c_int
+        lib.paris_knn_index_aux.argtypes = [P, P, P, P, i64, P, i32, i32, P, P, i32, i32, i32, P,
+                                            ctypes.POINTER(_Aux), ctypes.POINTER(_Config), ctypes.POINTER(_Stats)]
+        lib.paris_knn_index_aux.restype = ctypes.c_int
+        lib.paris_paa_f16.argtypes = [P, i64, i32, i32, P, P]
+        lib.paris_paa_f16.restype = ctypes.c_int
         lib.paris_raw_bf16.argtypes = [P, i64, i32, P, P]
         lib.paris_raw_bf16.restype = ctypes.c_int
         lib.paris_knn_index.argtypes = [P, P, P, P, i64, P, i32, i32, P, P, i32, i32, i32, P]
@@ -270,15 +281,28 @@ def raw_bf16(raw: torch.Tensor, stream=None) -> torch.Tensor:
     return out
 
 
+def paa_f16(raw: torch.Tensor, w2: int = 64, stream=None) -> torch.Tensor:
+    """fp16 PAA of every row of raw at w2 segments (paris_paa_f16) -> int16 bits [n][w2] (CUDA):
+    the PAA refinement pre-filter of knn_index(..., paa16=...)."""
+    lib = load()
+    _need_cuda(raw, "raw")
+    if raw.dtype != torch.float32 or raw.dim() != 2:
+        raise ValueError("raw must be [n][len] float32")
+    out = torch.empty((raw.shape[0], w2), dtype=torch.int16, device=raw.device)
+    _check(lib.paris_paa_f16(raw.data_ptr(), raw.shape[0], raw.shape[1], w2, out.data_ptr(), _stream(stream)))
+    return out
+
+
 def knn_index(raw: torch.Tensor, index: Index, queries: torch.Tensor, k: int = 1,
               out_idx: torch.Tensor | None = None, out_dist: torch.Tensor | None = None, stream=None,
               config: KnnConfig | None = None, stats: bool = False, raw16: torch.Tensor | None = None,
-              sync: bool | None = None):
-    """Exact k-NN over an Index (paris_knn_index); same results as knn_exact.  raw16: the
-    bf16 copy of raw (raw_bf16) -> the refinement pre-filter (paris_knn_index_x)."""
+              sync: bool | None = None, paa16: torch.Tensor | None = None):
+    """Exact k-NN over an Index (paris_knn_index); same results as knn_exact.  Refinement
+    pre-filters: raw16 = the bf16 copy of raw (raw_bf16, paris_knn_index_x); paa16 = the fp16
+    PAA of raw (paa_f16, paris_knn_index_aux)."""
     return knn_exact(raw, index.sax_sorted, queries, k=k, w=index.w, card=index.card, out_idx=out_idx,
                      out_dist=out_dist, stream=stream, config=config, stats=stats, _index=index, _raw16=raw16,
-                     sync=sync)
+                     sync=sync, _paa16=paa16)
 
 
 def knn_nb(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, w: int = 16, card: int = 256,
@@ -339,7 +363,8 @@ def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: in
               w: int = 16, card: int = 256, out_idx: torch.Tensor | None = None,
               out_dist: torch.Tensor | None = None, stream=None,
               config: KnnConfig | None = None, stats: bool = False, _index: Index | None = None,
-              _nb: bool = False, _raw16: torch.Tensor | None = None, sync: bool | None = None):
+              _nb: bool = False, _raw16: torch.Tensor | None = None, sync: bool | None = None,
+              _paa16: torch.Tensor | None = None):
     """Exact k-NN of every query (rows of `queries`, CUDA or host) over raw/sax.
 
     sax (and the index) are CUDA tensors; raw is CUDA or pinned host memory (the
@@ -380,9 +405,10 @@ def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: in
     if stats:
         arrays = (torch.zeros(nq, dtype=torch.int64), torch.zeros(nq, dtype=torch.int64),
                   torch.zeros(nq, dtype=torch.float32), torch.zeros(nq, dtype=torch.int64),
-                  torch.zeros(nq, dtype=torch.int64), torch.zeros(nq, dtype=torch.int64))
+                  torch.zeros(nq, dtype=torch.int64), torch.zeros(nq, dtype=torch.int64),
+                  torch.zeros(nq, dtype=torch.int64))
         st = _Stats(arrays[0].data_ptr(), arrays[1].data_ptr(), arrays[2].data_ptr(), arrays[3].data_ptr(),
-                    arrays[4].data_ptr(), arrays[5].data_ptr())
+                    arrays[4].data_ptr(), arrays[5].data_ptr(), arrays[6].data_ptr())
     if _nb:
         if k != 1:
             raise ValueError("knn_nb answers 1-NN (nb-ParIS+, Alg7-8)")
@@ -394,6 +420,17 @@ def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: in
                                     out_idx.data_ptr(), out_dist.data_ptr(), length, w, card,
                                     _stream(stream), ctypes.byref(cfg) if cfg else None,
                                     ctypes.byref(st) if st else None)
+    elif _paa16 is not None:
+        _need_cuda(_paa16, "paa16")
+        if _paa16.dim() != 2 or _paa16.shape[0] != n or _paa16.element_size() != 2:
+            raise ValueError("paa16 must be the [n][w2] 16-bit PAA of raw (paa_f16)")
+        if _raw16 is not None:
+            _need_cuda(_raw16, "raw16")
+        aux = _Aux(_raw16.data_ptr() if _raw16 is not None else None, _paa16.data_ptr(), int(_paa16.shape[1]), 0)
+        rc = lib.paris_knn_index_aux(raw.data_ptr(), sax.data_ptr(), _index.perm.data_ptr(), _index.env.data_ptr(), n,
+                                     queries.data_ptr(), nq, k, out_idx.data_ptr(), out_dist.data_ptr(), length, w,
+                                     card, _stream(stream), ctypes.byref(aux), ctypes.byref(cfg) if cfg else None,
+                                     ctypes.byref(st) if st else None)
     elif _raw16 is not None:
         _need_cuda(_raw16, "raw16")
         if _raw16.shape != raw.shape or _raw16.element_size() != 2:
@@ -420,7 +457,7 @@ def knn_exact(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, k: in
     if stats:
         return out_idx, out_dist, {"candidates": arrays[0], "refined": arrays[1],
                                    "tau_seed": arrays[2], "lb_blocks": arrays[3], "bsf_updates": arrays[4],
-                                   "raw16_rows": arrays[5]}
+                                   "raw16_rows": arrays[5], "paa_rows": arrays[6]}
     return out_idx, out_dist
 
 

@@ -1937,6 +1937,9 @@ struct RefineArgs {
   const uint16_t* raw16 = nullptr;  // optional bf16 copy of raw [n][len] (paris_raw_bf16): pre-filter
   unsigned* refined16 = nullptr;    // per query: bf16 rows read by the pre-filter
   unsigned* ghist = nullptr;        // k > 1: per query, histogram of refined exact d^2 (kNB bins of tau_seed^2)
+  const __half* paa16 = nullptr;    // optional [n][w2] fp16 PAA of raw (paris_paa_f16): the PAA pre-filter
+  int w2 = 0;
+  unsigned* paa_rows = nullptr;     // per query of the batch: PAA rows read (accumulated over the call)
 };
 
 // One warp step: up to kU candidates (indices i0 + u*stride) against the live
@@ -2404,25 +2407,34 @@ k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
 constexpr int kRefQCtas = PARIS_REFQ_CTAS;
 constexpr int kRefQLen = 256;  // longest row of the octet form
 
-template <int NC, int U>
+// W2 > 0: the PAA pre-filter first (paris_paa_f16): per candidate its fp16 PAA row (2 W2
+// bytes, an octet of lanes reading one 16-byte piece each), the rigorous PAA lower bound
+// sqrt(len/W2) ((1 - rho16) D~ - (rho16 + 2^-23) ||q_p|| - sqrt(W2) 2^-24) with
+// D~ = ||q_p - x~_p|| (Keogh's PAA bound; fp16 rounding bounded as the bf16
+// one); survivors go on to the bf16 stage (if a.raw16) or straight to the
+// exact fp32 distance.
+template <int NC, int U, int W2, bool R16>
 __global__ void __launch_bounds__(kRefThreads, kRefQCtas)
 k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
-  __shared__ unsigned s_refined[kMaxB], s_cnt[kMaxB], s_cut[kMaxB], s_r16[kMaxB];
+  __shared__ unsigned s_refined[kMaxB], s_cnt[kMaxB], s_cut[kMaxB], s_r16[kMaxB], s_paa[kMaxB];
   __shared__ float s_scale[kMaxB];
   __shared__ uint64_t s_queue[kRefWarps][64];
   __shared__ float s_qn[kMaxB];  // per query: qn_hi >= ||q||
+  __shared__ float s_qp[W2 > 0 ? kMaxB : 1][W2 > 0 ? W2 : 1];  // per query: its PAA-W2 (fp32 of the fp64 means)
+  __shared__ float s_qpn[kMaxB];  // per query: >= ||q_p||
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int oct = lane >> 3, sub = lane & 7;
   if (threadIdx.x < kMaxB) {
     const bool on = threadIdx.x < nb;
     s_refined[threadIdx.x] = 0;
     s_r16[threadIdx.x] = 0;
+    s_paa[threadIdx.x] = 0;
     s_cnt[threadIdx.x] = on ? (unsigned)imin64((int64_t)a.count[threadIdx.x], a.cap) : 0u;
     s_cut[threadIdx.x] = on ? cut[threadIdx.x * kNB] : 0u;
     s_scale[threadIdx.x] = on ? bin_scale(__uint_as_float(a.thr_seed[threadIdx.x])) : 0.f;
   }
   const float e2w = 2.f * (float)((a.len >> 5) + 8) * 5.9604644775390625e-08f;  // warp-tree sums
-  for (int b = warp; b < nb; b += kRefWarps) {  // the query norms, once per CTA
+  for (int b = warp; b < nb; b += kRefWarps) {  // the query norms (and PAA), once per CTA
     const float4* qv = reinterpret_cast<const float4*>(a.queries + (size_t)b * a.len);
     float qs = 0.f;
     for (int f = lane; f < (a.len >> 2); f += 32) {
@@ -2431,6 +2443,19 @@ k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     }
     qs = warp_sum(qs);
     if (lane == 0) s_qn[b] = __fsqrt_ru(__fmul_ru(qs, 1.f + e2w));
+    if (W2 > 0) {
+      const int sl = a.len / W2;
+      float pn = 0.f;
+      for (int sg = lane; sg < W2; sg += 32) {
+        double m = 0.0;
+        for (int j = 0; j < sl; ++j) m += (double)a.queries[(size_t)b * a.len + (size_t)sg * sl + j];
+        const float v = (float)(m / (double)sl);
+        s_qp[W2 > 0 ? b : 0][W2 > 0 ? sg : 0] = v;
+        pn = fmaf(v, v, pn);
+      }
+      pn = warp_sum(pn);
+      if (lane == 0) s_qpn[b] = __fsqrt_ru(__fmul_ru(pn, 1.f + e2w));
+    }
   }
   __syncthreads();
   const unsigned gw = blockIdx.x * kRefWarps + warp, GW = gridDim.x * kRefWarps;
@@ -2453,8 +2478,109 @@ k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     const float qn_hi = s_qn[b];
     int qn = 0;  // queued keys
 
+    // W2 > 0: the PAA stage over the queued keys [0, m) (m <= 32): octet o takes keys
+    // o + 4i, i < 8 (each lane one 16-byte piece of every row: 8 loads in flight); the
+    // survivors are compacted to the front of the queue
+    unsigned npaa = 0;
+    float qpl[W2 > 0 ? W2 / 8 : 1];  // this lane's query PAA values (segments sub*W2/8 ..)
+    if (W2 > 0) {
+#pragma unroll
+      for (int e = 0; e < (W2 > 0 ? W2 / 8 : 1); ++e) qpl[e] = s_qp[W2 > 0 ? b : 0][W2 > 0 ? sub * (W2 / 8) + e : 0];
+    }
+    const float qpn_hi = W2 > 0 ? s_qpn[b] : 0.f;
+    auto paa_stage = [&](int m) -> int {
+      constexpr int EPL = W2 > 0 ? W2 / 8 : 1;  // fp16 values per lane of a row
+      cur = min(cur, ld_relaxed_u64(bp));
+      const float thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
+      const float e2p = 2.f * (float)(EPL + 8) * 5.9604644775390625e-08f;    // lane chain + octet tree
+      constexpr float rho16 = 4.8875808715820312e-04f;  // 2^-11 (1 + 2^-10), rounded up
+      constexpr float one_m_rho16 = 0.99951171875f;     // 1 - 2^-11 (1 + 2^-10), rounded down
+      const float qterm = __fmul_ru(rho16 + 1.1920928955078125e-07f, qpn_hi);   // (rho16 + 2^-23) ||q_p||
+      const float slack = __fmul_ru(sqrtf((float)W2) * 1.0001f, 5.9604644775390625e-08f);  // sqrt(W2) 2^-24
+      const float scale2 = __fdiv_rd((float)a.len, (float)(W2 > 0 ? W2 : 1));
+      // all keys first (the survivors are compacted over the same queue entries)
+      uint64_t key[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int e = oct + 4 * i;
+        key[i] = e < m ? queue[e] : kNoKey;
+      }
+      __syncwarp();
+      int nout = 0;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {  // 4 rows per octet at a time (registers)
+        bool keep[4];
+        uint32_t pw[4][EPL / 2 > 0 ? EPL / 2 : 1];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int e = oct + 4 * (4 * half + i);
+          const uint64_t kk = key[4 * half + i];
+          keep[i] = e < m && key_val(kk) <= thr;
+          const __half* row = a.paa16 + (size_t)key_id(kk) * W2 + sub * EPL;
+          if (EPL == 8) {
+            const uint4 v = keep[i] ? ld_stream_u4(reinterpret_cast<const uint4*>(row)) : make_uint4(0u, 0u, 0u, 0u);
+            pw[i][0] = v.x; pw[i][EPL / 2 > 1 ? 1 : 0] = v.y; pw[i][EPL / 2 > 2 ? 2 : 0] = v.z; pw[i][EPL / 2 > 3 ? 3 : 0] = v.w;
+          } else if (EPL == 4) {
+            uint2 v = make_uint2(0u, 0u);
+            if (keep[i]) v = __ldcs(reinterpret_cast<const uint2*>(row));
+            pw[i][0] = v.x; pw[i][EPL / 2 > 1 ? 1 : 0] = v.y;
+          } else {
+            pw[i][0] = keep[i] ? __ldcs(reinterpret_cast<const uint32_t*>(row)) : 0u;
+          }
+          npaa += __popc(__ballot_sync(0xffffffffu, sub == 0 && keep[i]));
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          float acc = 0.f;
+#pragma unroll
+          for (int e = 0; e < EPL; ++e) {
+            const uint32_t w = pw[i][e >> 1];
+            const float x = __half2float(__ushort_as_half((unsigned short)((e & 1) ? (w >> 16) : (w & 0xFFFFu))));
+            const float d = x - qpl[e];
+            acc = fmaf(d, d, acc);
+          }
+          acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+          acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+          acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+          const float D = __fsqrt_rd(__fmul_rd(acc, 1.f - e2p));
+          const float Dp = __fsub_rd(__fsub_rd(__fmul_rd(one_m_rho16, D), qterm), slack);
+          const float lb2 = Dp > 0.f ? __fmul_rd(scale2, __fmul_rd(Dp, Dp)) : 0.f;
+          const bool kp = keep[i] && !(lb2 > thr);  // NaN (a PAA beyond fp16): no pruning
+          const unsigned mk = __ballot_sync(0xffffffffu, sub == 0 && kp);
+          if (sub == 0 && kp) queue[nout + __popc(mk & ((1u << lane) - 1u))] = key[4 * half + i];
+          nout += __popc(mk);
+        }
+      }
+      __syncwarp();
+      return nout;
+    };
+
     // the queued keys [0, m): octet o takes keys 8r + o and 8r + 4 + o of round r
     auto drain = [&](int m) {
+      if (W2 > 0) {
+        m = paa_stage(m);
+        if (!R16) {  // PAA survivors straight to the exact distance, U rows in flight
+          cur = min(cur, ld_relaxed_u64(bp));
+          float thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
+          const uint64_t kl = lane < m ? queue[lane] : kNoKey;
+          unsigned m2 = __ballot_sync(0xffffffffu, lane < m && key_val(kl) <= thr);
+          while (m2) {
+            uint64_t ks[U];
+            bool lv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int src = m2 ? __ffs(m2) - 1 : 0;
+              const bool has = m2 != 0u;
+              m2 &= m2 - 1;
+              ks[u] = __shfl_sync(0xffffffffu, kl, src);
+              lv[u] = has && key_val(ks[u]) <= thr;
+            }
+            refine_group<NC, U>(a, qv, ks, lv, thr, cur, bp, nref);
+            thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
+          }
+          return;
+        }
+      }
       for (int r0 = 0; r0 < m; r0 += 8) {
         cur = min(cur, ld_relaxed_u64(bp));
         float thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
@@ -2559,10 +2685,13 @@ k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     __syncwarp();
     if (lane == 0 && nref) atomicAdd(&s_refined[b], nref);
     if (lane == 0 && nref16) atomicAdd(&s_r16[b], nref16);
+    if (W2 > 0 && lane == 0 && npaa) atomicAdd(&s_paa[b], npaa);
   }
   __syncthreads();
   if (threadIdx.x < nb && s_refined[threadIdx.x]) atomicAdd(&a.refined[threadIdx.x], s_refined[threadIdx.x]);
   if (threadIdx.x < nb && s_r16[threadIdx.x]) atomicAdd(&a.refined16[threadIdx.x], s_r16[threadIdx.x]);
+  if (W2 > 0 && threadIdx.x < nb && s_paa[threadIdx.x] && a.paa_rows)
+    atomicAdd(&a.paa_rows[threadIdx.x], s_paa[threadIdx.x]);
 }
 
 // ---------------------------------------------------------------- K6, k > 1 (append, then select)
@@ -3360,6 +3489,8 @@ struct Plan {
   const uint16_t* raw16 = nullptr;  // optional bf16 copy of raw: refine pre-filter (k = 1)
   bool raw_host = false;            // raw in pinned host memory (f3)
   int fbL = 0;                      // overflow fallback: warps of its grid (= lists per query for k > 1)
+  const __half* paa16 = nullptr;    // optional fp16 PAA of raw: refine pre-filter (k = 1)
+  int w2 = 0;
   const float* tau_in = nullptr;    // external per-query bound of the k-th NN distance (device)
   bool approx = false;              // paris_knn_approx: the seeds' top-k only
 };
@@ -3570,10 +3701,16 @@ cudaError_t launch_refine1(const RefineArgs& ra, int nb, int64_t max_work, cudaS
 template <int NC, int U>
 cudaError_t launch_refine1u(const RefineArgs& ra, int nb, int wave, const unsigned* cut, cudaStream_t st) {
   if constexpr (NC <= 2) {
-    if (ra.raw16 && !getenv("PARIS_REF16_WARP")) {  // lane per candidate (env: A/B of the warp form)
-      const int grid = sms() * kRefQCtas;
-      return PARIS_LAUNCH("refine", (k_refine1q<NC, U>), grid, kRefThreads, 0, st, ra, nb, wave, cut);
+    const int grid = sms() * kRefQCtas;
+    if (ra.paa16) {  // the PAA pre-filter (then the bf16 one, if given)
+      if (ra.w2 == 32)
+        return ra.raw16 ? PARIS_LAUNCH("refine", (k_refine1q<NC, U, 32, true>), grid, kRefThreads, 0, st, ra, nb, wave, cut)
+                        : PARIS_LAUNCH("refine", (k_refine1q<NC, U, 32, false>), grid, kRefThreads, 0, st, ra, nb, wave, cut);
+      return ra.raw16 ? PARIS_LAUNCH("refine", (k_refine1q<NC, U, 64, true>), grid, kRefThreads, 0, st, ra, nb, wave, cut)
+                      : PARIS_LAUNCH("refine", (k_refine1q<NC, U, 64, false>), grid, kRefThreads, 0, st, ra, nb, wave, cut);
     }
+    if (ra.raw16 && !getenv("PARIS_REF16_WARP"))  // octets per candidate (env: A/B of the warp form)
+      return PARIS_LAUNCH("refine", (k_refine1q<NC, U, 0, true>), grid, kRefThreads, 0, st, ra, nb, wave, cut);
   }
   if (ra.raw16) {
     const int grid = sms() * (NC <= 2 ? kRefU16Ctas : 2);
@@ -3668,7 +3805,7 @@ int launch_fallback(const Plan& p, const float* raw, const uint8_t* sax, const f
 int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* qbatch, int nb, int q0,
               int64_t cap, const CardTables* tab, const Ws& ws, int64_t* d_idx, float* d_dist,
               unsigned* all_count, unsigned* all_refined, float* all_tau, unsigned* all_blocks,
-              unsigned* all_extra, cudaStream_t st, bool rescan = false) {
+              unsigned* all_extra, cudaStream_t st, bool rescan = false, unsigned* all_paa = nullptr) {
   const int P = pairs_for(nb);
   cudaError_t e = cudaMemsetAsync(ws.zero_block, 0, ws.zero_bytes, st);
   if (e != cudaSuccess) return cuda_error(e, "memset scratch");
@@ -3767,6 +3904,9 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
   ra.raw16 = (p.k == 1 && (p.raw_host || p.len >= kRaw16MinLen)) ? p.raw16 : nullptr;
   ra.refined16 = ws.updates;
   ra.ghist = ws.ghist;
+  ra.paa16 = p.k == 1 ? p.paa16 : nullptr;
+  ra.w2 = p.w2;
+  ra.paa_rows = all_paa ? all_paa + q0 : nullptr;
   dim3 g((unsigned)p.XB, (unsigned)nb);
   if (p.k == 1) {
     cudaError_t e1 = cudaSuccess;
@@ -3901,7 +4041,7 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
              int64_t* out_idx, float* out_dist, int len, int w, int card, cudaStream_t st,
              const paris_knn_config* cfg, paris_knn_stats* stats, const uint32_t* perm = nullptr,
              const uint8_t* env = nullptr, bool nb_mode = false, const uint16_t* raw16 = nullptr,
-             bool approx = false) {
+             bool approx = false, const uint16_t* paa16 = nullptr, int w2 = 0) {
   if (nb_mode && (k != 1 || w != kTW || n % 4 != 0)) {
     set_error("paris_knn_nb: needs k == 1, w == 16, n %% 4 == 0 (k=%d, w=%d, n=%lld)", k, w, (long long)n);
     return k != 1 ? PARIS_EINVAL : PARIS_ECONFIG;
@@ -3987,6 +4127,18 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
     }
     p.raw16 = raw16;
   }
+  if (paa16) {
+    if (w2 != 32 && w2 != 64) {
+      set_error("paris_knn_index_aux: paa16 needs w2 in {32, 64} (got %d)", w2);
+      return PARIS_ECONFIG;
+    }
+    if ((len % w2) || is_host_ptr(paa16) || (reinterpret_cast<uintptr_t>(paa16) & 15)) {
+      set_error("paris_knn_index_aux: paa16 must be 16-byte aligned device memory and w2 | len");
+      return PARIS_EINVAL;
+    }
+    p.paa16 = reinterpret_cast<const __half*>(paa16);
+    p.w2 = w2;
+  }
   p.raw_host = raw_host;
   p.approx = approx;
   if (cfg && cfg->tau_in && !approx && !nb_mode) {
@@ -4045,7 +4197,7 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   const bool hq = is_host_ptr(queries), hi = is_host_ptr(out_idx), hd = is_host_ptr(out_dist);
   cudaError_t e;
   const size_t qbytes = (size_t)nq * len * 4, ibytes = (size_t)nq * k * 8, dbytes = (size_t)nq * k * 4;
-  const size_t cbytes = (size_t)nq * 4 * 5;
+  const size_t cbytes = (size_t)nq * 4 * 6;
   auto up = [](size_t v) { return (v + 255) & ~(size_t)255; };
   const size_t wsb = large_k ? 0 : up(ws_layout(p, p.cap, nullptr, nullptr));
   const size_t total = wsb + up(qbytes) + up(ibytes) + up(dbytes) + up(cbytes);
@@ -4063,6 +4215,7 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   float* all_tau = (float*)(all_refined + nq);
   unsigned* all_blocks = (unsigned*)(all_tau + nq);
   unsigned* all_extra = all_blocks + nq;  // nb: BSF-copy updates; index + bf16: pre-filter rows
+  unsigned* all_paa = all_extra + nq;     // index + PAA pre-filter: PAA rows read
   const float* d_q = queries;
   int64_t* d_idx = hi ? sidx : out_idx;
   float* d_dist = hd ? sdist : out_dist;
@@ -4090,7 +4243,7 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   for (int q0 = 0; q0 < nq && rc == PARIS_OK && !large_k; q0 += p.B) {
     const int nb = std::min(p.B, nq - q0);
     rc = run_batch(p, raw, sax, d_q + (size_t)q0 * len, nb, q0, p.cap, tab, ws, d_idx, d_dist,
-                   all_count, all_refined, all_tau, all_blocks, all_extra, st, /*rescan=*/seed_from_out);
+                   all_count, all_refined, all_tau, all_blocks, all_extra, st, /*rescan=*/seed_from_out, all_paa);
   }
   // no synchronization: a query whose candidate buffer overflowed was completed on the
   // device (k_fallback); host outputs are copied back stream-ordered
@@ -4103,13 +4256,14 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
     if (e != cudaSuccess) rc = cuda_error(e, "D2H out_dist");
   }
   if (rc == PARIS_OK && stats) {  // measurement path: read the counters (synchronizes)
-    std::vector<unsigned> h_count(nq), h_ref(nq), h_blk(nq), h_ext(nq);
+    std::vector<unsigned> h_count(nq), h_ref(nq), h_blk(nq), h_ext(nq), h_paa(nq);
     std::vector<float> h_tau(nq);
     e = cudaMemcpyAsync(h_count.data(), all_count, (size_t)nq * 4, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(h_ref.data(), all_refined, (size_t)nq * 4, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(h_tau.data(), all_tau, (size_t)nq * 4, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(h_blk.data(), all_blocks, (size_t)nq * 4, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(h_ext.data(), all_extra, (size_t)nq * 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h_paa.data(), all_paa, (size_t)nq * 4, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) rc = cuda_error(e, "paris_knn_exact stats D2H");
     if (rc == PARIS_OK) {
@@ -4121,6 +4275,7 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
         if (stats->lb_blocks) stats->lb_blocks[q] = p.nb ? 0 : h_blk[q];
         if (stats->bsf_updates) stats->bsf_updates[q] = p.nb ? h_ext[q] : 0;
         if (stats->raw16_rows) stats->raw16_rows[q] = p.nb ? 0 : h_ext[q];
+        if (stats->paa_rows) stats->paa_rows[q] = h_paa[q];
       }
     }
   }
@@ -4167,6 +4322,15 @@ int paris_knn_index_ex(const float* raw, const uint8_t* sax_sorted, const uint32
                        const paris_knn_config* config, paris_knn_stats* stats) {
   return paris::knn_impl(raw, sax_sorted, n, queries, nq, k, out_idx, out_dist, len, w, card,
                          (cudaStream_t)stream, config, stats, perm, env);
+}
+
+int paris_knn_index_aux(const float* raw, const uint8_t* sax_sorted, const uint32_t* perm, const uint8_t* env, int64_t n,
+                        const float* queries, int32_t nq, int32_t k, int64_t* out_idx, float* out_dist, int32_t len,
+                        int32_t w, int32_t card, void* stream, const paris_refine_aux* aux,
+                        const paris_knn_config* config, paris_knn_stats* stats) {
+  return paris::knn_impl(raw, sax_sorted, n, queries, nq, k, out_idx, out_dist, len, w, card, (cudaStream_t)stream,
+                         config, stats, perm, env, false, aux ? aux->raw_bf16 : nullptr, false,
+                         aux ? aux->paa16 : nullptr, aux ? aux->w2 : 0);
 }
 
 int paris_knn_approx(const float* raw, const uint8_t* sax, int64_t n, const float* queries, int32_t nq, int32_t k,

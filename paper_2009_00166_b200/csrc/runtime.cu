@@ -478,7 +478,7 @@ int paris_debug_read_probe(const void* p, int64_t bytes, void* stream) {
 
 const char* paris_last_error(void) { return paris::g_err.c_str(); }
 
-int32_t paris_version(void) { return 106; }
+int32_t paris_version(void) { return 107; }
 
 void paris_release_workspace(void) { paris::ws_free_all(); }
 

@@ -17,6 +17,7 @@
 #include "runtime.cuh"
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -644,6 +645,26 @@ int summarize_impl(const float* raw, int64_t n, int len, int w, int card, uint8_
 
 namespace paris {
 namespace {
+// PAA with w2 segments (seglen = len / w2), each mean in fp64 then rounded to nearest fp16
+// (through fp32: |x - fl16(x)| <= 2^-11 (1 + 2^-10) |fl16(x)| + 2^-24);
+// a mean beyond the fp16 range is stored as NaN -- the refine then never prunes on it.
+// Warp per series: lane l owns segments l, l + 32, ...
+__global__ void __launch_bounds__(256) k_paa16(const float* __restrict__ raw, int64_t n, int len, int w2,
+                                              __half* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int seglen = len / w2;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const float* x = raw + (size_t)i * len;
+    for (int s = lane; s < w2; s += 32) {
+      double acc = 0.0;
+      for (int j = 0; j < seglen; ++j) acc += (double)__ldcs(x + (size_t)s * seglen + j);
+      const double m = acc / (double)seglen;
+      out[(size_t)i * w2 + s] = fabs(m) < 65000.0 ? __float2half_rn((float)m) : __ushort_as_half((unsigned short)0x7E00u);
+    }
+  }
+}
+
 // fp32 -> bf16 (round to nearest even), 8 values per thread-iteration
 __global__ void __launch_bounds__(256) k_raw_bf16(const float4* __restrict__ raw, int64_t n8,
                                                   uint4* __restrict__ out) {
@@ -670,6 +691,20 @@ int raw_bf16_launch(const float* raw, int64_t n, int len, uint16_t* out, cudaStr
   return PARIS_OK;
 }
 }  // namespace paris
+
+extern "C" int paris_paa_f16(const float* raw, int64_t n, int32_t len, int32_t w2, uint16_t* out, void* stream) {
+  if (!raw || !out || n < 1 || len < 4 || w2 < 1 || w2 > 256 || (len % w2) || (reinterpret_cast<uintptr_t>(out) & 15) ||
+      (w2 % 8)) {
+    paris::set_error("paris_paa_f16: bad arguments (n=%lld len=%d w2=%d; w2 | len, w2 %% 8 == 0, w2 <= 256)",
+                     (long long)n, len, w2);
+    return PARIS_EINVAL;
+  }
+  const int grid = (int)std::min<int64_t>((n + 7) / 8, (int64_t)paris::sm_count() * 16);
+  PARIS_CHECK_LAUNCH(PARIS_LAUNCH("paa_f16", paris::k_paa16, grid, 256, 0, (cudaStream_t)stream, raw, n, len, w2,
+                                  reinterpret_cast<__half*>(out)),
+                     "paa_f16 launch");
+  return PARIS_OK;
+}
 
 extern "C" int paris_raw_bf16(const float* raw, int64_t n, int32_t len, uint16_t* out, void* stream) {
   if (!raw || !out || n < 1 || len < 8 || (len % 8) || (reinterpret_cast<uintptr_t>(raw) & 15) ||

@@ -78,14 +78,14 @@ def knn_sharded(queries: torch.Tensor, k: int, shard_base: int, local, group=Non
     return merge(all_dst.contiguous(), all_idx.contiguous())
 
 
-def local_index_search(raw_shard: torch.Tensor, index, config=None, raw16=None):
-    """`local` for knn_sharded over a shard indexed with paris_index_build (with the bf16
-    refinement pre-filter when raw16 is given, as the single-GPU bench path)."""
+def local_index_search(raw_shard: torch.Tensor, index, config=None, raw16=None, paa16=None):
+    """`local` for knn_sharded over a shard indexed with paris_index_build (with the bf16 / PAA
+    refinement pre-filters when given, as the single-GPU bench path)."""
     def run(queries, k, tau_in=None):
         cfg = config
         if tau_in is not None:
             cfg = dataclasses.replace(config or B.KnnConfig(), tau_in=tau_in)
-        return B.knn_index(raw_shard, index, queries, k=k, config=cfg, raw16=raw16)
+        return B.knn_index(raw_shard, index, queries, k=k, config=cfg, raw16=raw16, paa16=paa16)
     return run
 
 

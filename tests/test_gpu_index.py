@@ -216,3 +216,51 @@ def test_knn_overflow_fallback_mixed(P, k):
     check_knn(x, q, fi.cpu().numpy(), fd.cpu().numpy(), ri, rd2)
     cap = 65536
     assert (st["candidates"].numpy()[flood] > cap).all(), "the flooded queries did not overflow"
+
+
+@pytest.mark.parametrize("scale,shift,w2,with16,length", [(1.0, 0.0, 64, False, 256), (1.0, 0.0, 32, False, 256),
+                                                         (1.0, 0.0, 64, True, 256), (1.0, 0.0, 32, False, 128),
+                                                         (1e4, 3e4, 64, False, 256), (1e-4, 0.0, 64, True, 256)])
+def test_knn_index_paa_prefilter(P, scale, shift, w2, with16, length):
+    """paris_knn_index_aux: the fp16 PAA pre-filter (then optionally the bf16 one) only drops
+    candidates whose rigorous PAA lower bound exceeds the BSF -> results identical to the
+    unfiltered index search and to the oracle: z-normalized data, data far from unit scale
+    (PAA means beyond the fp16 range are stored as NaN: no pruning on them), tiny scale
+    (fp16 subnormals), near-member queries, exact duplicates (ties)."""
+    import torch
+    n, nq = 40_000, 40
+    x = datagen.random_walks(n, length, 800 + w2) * np.float32(scale) + np.float32(shift)
+    q = datagen.random_walks(nq, length, 801 + w2) * np.float32(scale) + np.float32(shift)
+    rng = np.random.default_rng(6)
+    q[:6] = x[[3, 3000, 39_999, 20_000, 77, 5]] + (1e-3 * scale * rng.standard_normal((6, length))).astype(np.float32)
+    x[9] = x[3]                                          # duplicate of a near-member's source (tie)
+    xd = torch.from_numpy(x).cuda()
+    sax = P.summarize(xd, 16, 256)
+    idx = P.index_build(sax, 16, 256)
+    paa = P.paa_f16(xd, w2)
+    r16 = P.raw_bf16(xd) if with16 else None
+    qd = torch.from_numpy(q).cuda()
+    gi, gd, st = P.knn_index(xd, idx, qd, k=1, paa16=paa, raw16=r16, stats=True)
+    hi, hd = P.knn_index(xd, idx, qd, k=1)
+    assert torch.equal(gi, hi) and torch.equal(gd, hd)
+    ri, rd2 = oracle.knn_bruteforce(x, q, 1)
+    check_knn(x, q, gi.cpu().numpy(), gd.cpu().numpy(), ri, rd2)
+    assert gi[0, 0].item() == 3                          # tie with id 9: the lower id
+    assert st["paa_rows"].sum() > 0
+    if scale == 1.0:
+        _, _, st0 = P.knn_index(xd, idx, qd, k=1, stats=True)
+        assert st["refined"].sum() < st0["refined"].sum()  # fp32 rows actually skipped
+
+
+def test_paa_f16_definition(P):
+    """paris_paa_f16 = the fp64 segment means rounded to nearest fp16 (NaN beyond the fp16 range)."""
+    import torch
+    x = (torch.randn(2000, 256, device="cuda", dtype=torch.float64) * 3).float()
+    x[7] *= 1e5
+    for w2 in (32, 64):
+        got = P.paa_f16(x, w2).view(torch.float16).float().cpu().numpy()
+        m = x.double().view(2000, w2, -1).mean(-1).cpu().numpy()
+        ref = m.astype(np.float32).astype(np.float16).astype(np.float32)
+        ok = np.abs(m) < 65000
+        assert np.array_equal(got[ok], ref[ok])
+        assert np.isnan(got[~ok]).all() and (~ok).any()
