@@ -359,6 +359,8 @@ def run_gpu(args):
             torch.cuda.synchronize()
             raw16_ms = e0.elapsed_time(e1)
     paa16, paa_ms = None, None
+    if args.paa < 0:
+        args.paa = min(64, length // 4) if length % 32 == 0 and length >= 128 else 0
     if args.paa and use_index and not (args.raw_host or args.raw_file):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -788,9 +790,9 @@ def main():
     ap.add_argument("--raw16", action="store_true", help="(default) index path with the bf16 refinement "
                     "pre-filter (paris_raw_bf16 + paris_knn_index_x)")
     ap.add_argument("--no-raw16", action="store_true", help="index path without the bf16 pre-filter")
-    ap.add_argument("--paa", type=int, default=0, choices=[0, 32, 64],
+    ap.add_argument("--paa", type=int, default=-1, choices=[-1, 0, 32, 64],
                     help="index path: the fp16 PAA pre-filter at this many segments (paris_paa_f16 + "
-                         "paris_knn_index_aux); 0 = off")
+                         "paris_knn_index_aux); -1 (default) = len/4 capped at 64, 0 = off")
     ap.add_argument("--no-sweep", action="store_true", help="skip the C2 k=10 / C5 sigma x k sweeps")
     ap.add_argument("--raw-host", action="store_true",
                     help="f3: keep the raw collection in pinned host memory (SAX/index in HBM)")

@@ -1940,6 +1940,7 @@ struct RefineArgs {
   const __half* paa16 = nullptr;    // optional [n][w2] fp16 PAA of raw (paris_paa_f16): the PAA pre-filter
   int w2 = 0;
   unsigned* paa_rows = nullptr;     // per query of the batch: PAA rows read (accumulated over the call)
+  const float* qaux = nullptr;      // [nb][kQAux] query constants (k_qaux), octet refine
 };
 
 // One warp step: up to kU candidates (indices i0 + u*stride) against the live
@@ -2406,6 +2407,39 @@ k_refine1u(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
 #endif
 constexpr int kRefQCtas = PARIS_REFQ_CTAS;
 constexpr int kRefQLen = 256;  // longest row of the octet form
+constexpr int kQAux = 80;      // floats per query of the refine's query constants (k_qaux)
+
+// Per query of a batch, once: qn_hi >= ||q|| (warp-tree fp32 sum, rounded up with its
+// margin), and for the PAA pre-filter the query's PAA at w2 segments (fp64 means rounded
+// to fp32) and qpn_hi >= ||PAA_w2(q)||: out[b * kQAux + {0, 1, 16 + s}].  A warp per query.
+__global__ void __launch_bounds__(32) k_qaux(const float* __restrict__ queries, int len, int w2,
+                                             float* __restrict__ out) {
+  const int b = blockIdx.x, lane = threadIdx.x;
+  const float e2w = 2.f * (float)((len >> 5) + 8) * 5.9604644775390625e-08f;
+  const float4* qv = reinterpret_cast<const float4*>(queries + (size_t)b * len);
+  float qs = 0.f;
+  for (int f = lane; f < (len >> 2); f += 32) {
+    const float4 v = __ldg(qv + f);
+    qs = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, qs))));
+  }
+  qs = warp_sum(qs);
+  float pn = 0.f;
+  if (w2 > 0) {
+    const int sl = len / w2;
+    for (int sg = lane; sg < w2; sg += 32) {
+      double m = 0.0;
+      for (int j = 0; j < sl; ++j) m += (double)queries[(size_t)b * len + (size_t)sg * sl + j];
+      const float v = (float)(m / (double)sl);
+      out[b * kQAux + 16 + sg] = v;
+      pn = fmaf(v, v, pn);
+    }
+    pn = warp_sum(pn);
+  }
+  if (lane == 0) {
+    out[b * kQAux + 0] = __fsqrt_ru(__fmul_ru(qs, 1.f + e2w));
+    out[b * kQAux + 1] = __fsqrt_ru(__fmul_ru(pn, 1.f + e2w));
+  }
+}
 
 // W2 > 0: the PAA pre-filter first (paris_paa_f16): per candidate its fp16 PAA row (2 W2
 // bytes, an octet of lanes reading one 16-byte piece each), the rigorous PAA lower bound
@@ -2419,9 +2453,7 @@ k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
   __shared__ unsigned s_refined[kMaxB], s_cnt[kMaxB], s_cut[kMaxB], s_r16[kMaxB], s_paa[kMaxB];
   __shared__ float s_scale[kMaxB];
   __shared__ uint64_t s_queue[kRefWarps][64];
-  __shared__ float s_qn[kMaxB];  // per query: qn_hi >= ||q||
-  __shared__ float s_qp[W2 > 0 ? kMaxB : 1][W2 > 0 ? W2 : 1];  // per query: its PAA-W2 (fp32 of the fp64 means)
-  __shared__ float s_qpn[kMaxB];  // per query: >= ||q_p||
+
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int oct = lane >> 3, sub = lane & 7;
   if (threadIdx.x < kMaxB) {
@@ -2432,30 +2464,6 @@ k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     s_cnt[threadIdx.x] = on ? (unsigned)imin64((int64_t)a.count[threadIdx.x], a.cap) : 0u;
     s_cut[threadIdx.x] = on ? cut[threadIdx.x * kNB] : 0u;
     s_scale[threadIdx.x] = on ? bin_scale(__uint_as_float(a.thr_seed[threadIdx.x])) : 0.f;
-  }
-  const float e2w = 2.f * (float)((a.len >> 5) + 8) * 5.9604644775390625e-08f;  // warp-tree sums
-  for (int b = warp; b < nb; b += kRefWarps) {  // the query norms (and PAA), once per CTA
-    const float4* qv = reinterpret_cast<const float4*>(a.queries + (size_t)b * a.len);
-    float qs = 0.f;
-    for (int f = lane; f < (a.len >> 2); f += 32) {
-      const float4 v = __ldg(qv + f);
-      qs = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, qs))));
-    }
-    qs = warp_sum(qs);
-    if (lane == 0) s_qn[b] = __fsqrt_ru(__fmul_ru(qs, 1.f + e2w));
-    if (W2 > 0) {
-      const int sl = a.len / W2;
-      float pn = 0.f;
-      for (int sg = lane; sg < W2; sg += 32) {
-        double m = 0.0;
-        for (int j = 0; j < sl; ++j) m += (double)a.queries[(size_t)b * a.len + (size_t)sg * sl + j];
-        const float v = (float)(m / (double)sl);
-        s_qp[W2 > 0 ? b : 0][W2 > 0 ? sg : 0] = v;
-        pn = fmaf(v, v, pn);
-      }
-      pn = warp_sum(pn);
-      if (lane == 0) s_qpn[b] = __fsqrt_ru(__fmul_ru(pn, 1.f + e2w));
-    }
   }
   __syncthreads();
   const unsigned gw = blockIdx.x * kRefWarps + warp, GW = gridDim.x * kRefWarps;
@@ -2475,7 +2483,8 @@ k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     unsigned long long* bp = a.best + (size_t)b * kPadU64;
     unsigned nref = 0, nref16 = 0;
     uint64_t cur = kNoKey;
-    const float qn_hi = s_qn[b];
+    const float* qx = a.qaux + (size_t)b * kQAux;  // k_qaux: ||q||, ||PAA(q)||, PAA(q)
+    const float qn_hi = __ldg(qx);
     int qn = 0;  // queued keys
 
     // W2 > 0: the PAA stage over the queued keys [0, m) (m <= 32): octet o takes keys
@@ -2485,9 +2494,9 @@ k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     float qpl[W2 > 0 ? W2 / 8 : 1];  // this lane's query PAA values (segments sub*W2/8 ..)
     if (W2 > 0) {
 #pragma unroll
-      for (int e = 0; e < (W2 > 0 ? W2 / 8 : 1); ++e) qpl[e] = s_qp[W2 > 0 ? b : 0][W2 > 0 ? sub * (W2 / 8) + e : 0];
+      for (int e = 0; e < (W2 > 0 ? W2 / 8 : 1); ++e) qpl[e] = __ldg(qx + 16 + sub * (W2 / 8) + e);
     }
-    const float qpn_hi = W2 > 0 ? s_qpn[b] : 0.f;
+    const float qpn_hi = W2 > 0 ? __ldg(qx + 1) : 0.f;
     auto paa_stage = [&](int m) -> int {
       constexpr int EPL = W2 > 0 ? W2 / 8 : 1;  // fp16 values per lane of a row
       cur = min(cur, ld_relaxed_u64(bp));
@@ -3461,6 +3470,7 @@ struct Ws {
   unsigned* tile_list;   // index mode: live tiles
   unsigned* fb_refined;  // overflow fallback: rows refined per query
   uint64_t* fb_lists;    // overflow fallback, k > 1: [B][fbL][k] warp lists
+  float* qaux;           // [B][80] per-query refine constants (k_qaux)
   size_t zero_bytes;
   unsigned long long* best;
   uint64_t* cand;
@@ -3743,6 +3753,7 @@ size_t ws_layout(const Plan& p, int64_t cap, Ws* ws, char* base) {
   const size_t o_sorted = take(need_sorted ? sizeof(uint64_t) * B * (size_t)cap : 8);
   const size_t o_lists = take(p.k > 1 && p.sorted_refine ? sizeof(uint64_t) * B * (size_t)p.XB * p.k : 8);
   const size_t o_fbl = take(p.k > 1 ? sizeof(uint64_t) * B * (size_t)p.fbL * p.k : 8);
+  const size_t o_qaux = take(sizeof(float) * B * 80);
   const int64_t ntiles = (p.n + kTS - 1) / kTS;
   const size_t o_bmask = take(p.perm ? sizeof(unsigned long long) * (size_t)ntiles * kBPT : 8);
   const size_t o_tlist = take(p.perm ? sizeof(unsigned) * (size_t)ntiles : 8);
@@ -3771,6 +3782,7 @@ size_t ws_layout(const Plan& p, int64_t cap, Ws* ws, char* base) {
   ws->sorted = (uint64_t*)(c + o_sorted);
   ws->lists = (uint64_t*)(c + o_lists);
   ws->fb_lists = (uint64_t*)(c + o_fbl);
+  ws->qaux = (float*)(c + o_qaux);
   ws->bmask = (unsigned long long*)(c + o_bmask);
   ws->tile_list = (unsigned*)(c + o_tlist);
   return off;
@@ -3907,6 +3919,10 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
   ra.paa16 = p.k == 1 ? p.paa16 : nullptr;
   ra.w2 = p.w2;
   ra.paa_rows = all_paa ? all_paa + q0 : nullptr;
+  ra.qaux = ws.qaux;
+  if (p.k == 1 && (ra.raw16 || ra.paa16) && p.len <= kRefQLen)  // the octet refine's query constants
+    PARIS_CHECK_LAUNCH(PARIS_LAUNCH("qprep", k_qaux, nb, 32, 0, st, qbatch, p.len, ra.paa16 ? p.w2 : 0, ws.qaux),
+                       "qaux launch");
   dim3 g((unsigned)p.XB, (unsigned)nb);
   if (p.k == 1) {
     cudaError_t e1 = cudaSuccess;
