@@ -632,6 +632,7 @@ def run_gpu(args):
         return {"k": kk, "queries": int(qsrc.shape[0]), "value": qsrc.shape[0] / (ms / 1e3),
                 "unit": "queries/s", "ms_per_step": ms,
                 "candidates_mean": float(stq["candidates"].numpy().astype(np.float64).mean()),
+                "candidates_max": float(stq["candidates"].numpy().astype(np.float64).max()),
                 "refined_mean": float(ref.mean()), "pruning_ratio": float(1.0 - ref.mean() / n),
                 "raw16_rows_mean": float(stq["raw16_rows"].numpy().astype(np.float64).mean())}
 

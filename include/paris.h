@@ -167,7 +167,8 @@ typedef struct paris_knn_config {
                            (device outputs; experiments with an ideal BSF);
                            [4] > 0: candidate-buffer capacity per query (test hook: forces the
                            overflow fallback; default max(65536, n/32 | n/16 for k > 1) grown
-                           to a 2 GB budget per candidate array) */
+                           to a budget per candidate array of 1/8 of the free device memory,
+                           clamped to [2, 16] GB) */
   const float* tau_in;  /* optional DEVICE [nq]: per query, an upper bound of its k-th NN
                            distance from outside the call (+inf = none) -- e.g. the minimum
                            over the shards of a sharded collection of their approximate

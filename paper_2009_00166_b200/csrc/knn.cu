@@ -2441,6 +2441,80 @@ __global__ void __launch_bounds__(32) k_qaux(const float* __restrict__ queries, 
   }
 }
 
+// The PAA pre-filter over a warp's queued keys [0, m) (m <= 32; every lane calls it):
+// octet o (lanes 8o..8o+7) takes keys o + 4i, i < 8, each lane one 2*W2/8-byte piece of the
+// row (4 rows per octet in flight at a time); keys whose LB <= thr and whose rigorous PAA
+// bound does not exceed thr are compacted to the front of the queue; returns
+// their count.  npaa counts the PAA rows read.  qpl: this lane's W2/8 query PAA values.
+template <int W2>
+__device__ __forceinline__ int paa_filter_queue(const RefineArgs& a, uint64_t* queue, int m, float thr,
+                                                const float (&qpl)[W2 > 0 ? W2 / 8 : 1], float qpn_hi,
+                                                unsigned& npaa) {
+  constexpr int EPL = W2 > 0 ? W2 / 8 : 1;  // fp16 values per lane of a row
+  const int lane = threadIdx.x & 31, oct = lane >> 3, sub = lane & 7;
+  const float e2p = 2.f * (float)(EPL + 8) * 5.9604644775390625e-08f;    // lane chain + octet tree
+  constexpr float rho16 = 4.8875808715820312e-04f;  // 2^-11 (1 + 2^-10), rounded up
+  constexpr float one_m_rho16 = 0.99951171875f;     // 1 - 2^-11 (1 + 2^-10), rounded down
+  const float qterm = __fmul_ru(rho16 + 1.1920928955078125e-07f, qpn_hi);   // (rho16 + 2^-23) ||q_p||
+  const float slack = __fmul_ru(sqrtf((float)W2) * 1.0001f, 5.9604644775390625e-08f);  // sqrt(W2) 2^-24
+  const float scale2 = __fdiv_rd((float)a.len, (float)(W2 > 0 ? W2 : 1));
+  // all keys first (the survivors are compacted over the same queue entries)
+  uint64_t key[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int e = oct + 4 * i;
+    key[i] = e < m ? queue[e] : kNoKey;
+  }
+  __syncwarp();
+  int nout = 0;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {  // 4 rows per octet at a time (registers)
+    bool keep[4];
+    uint32_t pw[4][EPL / 2 > 0 ? EPL / 2 : 1];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = oct + 4 * (4 * half + i);
+      const uint64_t kk = key[4 * half + i];
+      keep[i] = e < m && key_val(kk) <= thr;
+      const __half* row = a.paa16 + (size_t)key_id(kk) * W2 + sub * EPL;
+      if (EPL == 8) {
+        const uint4 v = keep[i] ? ld_stream_u4(reinterpret_cast<const uint4*>(row)) : make_uint4(0u, 0u, 0u, 0u);
+        pw[i][0] = v.x; pw[i][EPL / 2 > 1 ? 1 : 0] = v.y; pw[i][EPL / 2 > 2 ? 2 : 0] = v.z; pw[i][EPL / 2 > 3 ? 3 : 0] = v.w;
+      } else if (EPL == 4) {
+        uint2 v = make_uint2(0u, 0u);
+        if (keep[i]) v = __ldcs(reinterpret_cast<const uint2*>(row));
+        pw[i][0] = v.x; pw[i][EPL / 2 > 1 ? 1 : 0] = v.y;
+      } else {
+        pw[i][0] = keep[i] ? __ldcs(reinterpret_cast<const uint32_t*>(row)) : 0u;
+      }
+      npaa += __popc(__ballot_sync(0xffffffffu, sub == 0 && keep[i]));
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float acc = 0.f;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        const uint32_t w = pw[i][e >> 1];
+        const float x = __half2float(__ushort_as_half((unsigned short)((e & 1) ? (w >> 16) : (w & 0xFFFFu))));
+        const float d = x - qpl[e];
+        acc = fmaf(d, d, acc);
+      }
+      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      const float D = __fsqrt_rd(__fmul_rd(acc, 1.f - e2p));
+      const float Dp = __fsub_rd(__fsub_rd(__fmul_rd(one_m_rho16, D), qterm), slack);
+      const float lb2 = Dp > 0.f ? __fmul_rd(scale2, __fmul_rd(Dp, Dp)) : 0.f;
+      const bool kp = keep[i] && !(lb2 > thr);  // NaN (a PAA beyond fp16): no pruning
+      const unsigned mk = __ballot_sync(0xffffffffu, sub == 0 && kp);
+      if (sub == 0 && kp) queue[nout + __popc(mk & ((1u << lane) - 1u))] = key[4 * half + i];
+      nout += __popc(mk);
+    }
+  }
+  __syncwarp();
+  return nout;
+}
+
 // W2 > 0: the PAA pre-filter first (paris_paa_f16): per candidate its fp16 PAA row (2 W2
 // bytes, an octet of lanes reading one 16-byte piece each), the rigorous PAA lower bound
 // sqrt(len/W2) ((1 - rho16) D~ - (rho16 + 2^-23) ||q_p|| - sqrt(W2) 2^-24) with
@@ -2498,70 +2572,9 @@ k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     }
     const float qpn_hi = W2 > 0 ? __ldg(qx + 1) : 0.f;
     auto paa_stage = [&](int m) -> int {
-      constexpr int EPL = W2 > 0 ? W2 / 8 : 1;  // fp16 values per lane of a row
       cur = min(cur, ld_relaxed_u64(bp));
       const float thr = (cur == kNoKey) ? INFINITY : __fmul_ru(key_val(cur), a.d2up);
-      const float e2p = 2.f * (float)(EPL + 8) * 5.9604644775390625e-08f;    // lane chain + octet tree
-      constexpr float rho16 = 4.8875808715820312e-04f;  // 2^-11 (1 + 2^-10), rounded up
-      constexpr float one_m_rho16 = 0.99951171875f;     // 1 - 2^-11 (1 + 2^-10), rounded down
-      const float qterm = __fmul_ru(rho16 + 1.1920928955078125e-07f, qpn_hi);   // (rho16 + 2^-23) ||q_p||
-      const float slack = __fmul_ru(sqrtf((float)W2) * 1.0001f, 5.9604644775390625e-08f);  // sqrt(W2) 2^-24
-      const float scale2 = __fdiv_rd((float)a.len, (float)(W2 > 0 ? W2 : 1));
-      // all keys first (the survivors are compacted over the same queue entries)
-      uint64_t key[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int e = oct + 4 * i;
-        key[i] = e < m ? queue[e] : kNoKey;
-      }
-      __syncwarp();
-      int nout = 0;
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {  // 4 rows per octet at a time (registers)
-        bool keep[4];
-        uint32_t pw[4][EPL / 2 > 0 ? EPL / 2 : 1];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int e = oct + 4 * (4 * half + i);
-          const uint64_t kk = key[4 * half + i];
-          keep[i] = e < m && key_val(kk) <= thr;
-          const __half* row = a.paa16 + (size_t)key_id(kk) * W2 + sub * EPL;
-          if (EPL == 8) {
-            const uint4 v = keep[i] ? ld_stream_u4(reinterpret_cast<const uint4*>(row)) : make_uint4(0u, 0u, 0u, 0u);
-            pw[i][0] = v.x; pw[i][EPL / 2 > 1 ? 1 : 0] = v.y; pw[i][EPL / 2 > 2 ? 2 : 0] = v.z; pw[i][EPL / 2 > 3 ? 3 : 0] = v.w;
-          } else if (EPL == 4) {
-            uint2 v = make_uint2(0u, 0u);
-            if (keep[i]) v = __ldcs(reinterpret_cast<const uint2*>(row));
-            pw[i][0] = v.x; pw[i][EPL / 2 > 1 ? 1 : 0] = v.y;
-          } else {
-            pw[i][0] = keep[i] ? __ldcs(reinterpret_cast<const uint32_t*>(row)) : 0u;
-          }
-          npaa += __popc(__ballot_sync(0xffffffffu, sub == 0 && keep[i]));
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          float acc = 0.f;
-#pragma unroll
-          for (int e = 0; e < EPL; ++e) {
-            const uint32_t w = pw[i][e >> 1];
-            const float x = __half2float(__ushort_as_half((unsigned short)((e & 1) ? (w >> 16) : (w & 0xFFFFu))));
-            const float d = x - qpl[e];
-            acc = fmaf(d, d, acc);
-          }
-          acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-          acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-          acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-          const float D = __fsqrt_rd(__fmul_rd(acc, 1.f - e2p));
-          const float Dp = __fsub_rd(__fsub_rd(__fmul_rd(one_m_rho16, D), qterm), slack);
-          const float lb2 = Dp > 0.f ? __fmul_rd(scale2, __fmul_rd(Dp, Dp)) : 0.f;
-          const bool kp = keep[i] && !(lb2 > thr);  // NaN (a PAA beyond fp16): no pruning
-          const unsigned mk = __ballot_sync(0xffffffffu, sub == 0 && kp);
-          if (sub == 0 && kp) queue[nout + __popc(mk & ((1u << lane) - 1u))] = key[4 * half + i];
-          nout += __popc(mk);
-        }
-      }
-      __syncwarp();
-      return nout;
+      return paa_filter_queue<W2>(a, queue, m, thr, qpl, qpn_hi, npaa);
     };
 
     // the queued keys [0, m): octet o takes keys 8r + o and 8r + 4 + o of round r
@@ -2809,22 +2822,25 @@ __device__ __forceinline__ int refine_group_k(const RefineArgs& a, const float4*
 // (d^2, id) keys to the query's result list, and lowers the threshold from the
 // query-wide histogram after every 16 rows it completed.  k_select_topk then picks
 // the exact top-k of the results.
-template <int NC, int U>
-__global__ void __launch_bounds__(kRefThreads, NC <= 2 ? kRefUCtas : 2)
+template <int NC, int U, int W2 = 0>
+__global__ void __launch_bounds__(kRefThreads, W2 > 0 ? 4 : (NC <= 2 ? kRefUCtas : 2))
 k_refine_kx(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut, uint64_t* __restrict__ res,
             unsigned* __restrict__ res_cnt) {
-  __shared__ unsigned s_refined[kMaxB], s_cnt[kMaxB], s_cut[kMaxB];
+  __shared__ unsigned s_refined[kMaxB], s_cnt[kMaxB], s_cut[kMaxB], s_paa[kMaxB];
+  __shared__ uint64_t s_queue[W2 > 0 ? kRefWarps : 1][32];
   __shared__ float s_scale[kMaxB];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x < kMaxB) {
     const bool on = threadIdx.x < nb;
     s_refined[threadIdx.x] = 0;
+    s_paa[threadIdx.x] = 0;
     s_cnt[threadIdx.x] = on ? (unsigned)imin64((int64_t)a.count[threadIdx.x], a.cap) : 0u;
     s_cut[threadIdx.x] = on ? cut[threadIdx.x * kNB] : 0u;
     s_scale[threadIdx.x] = on ? bin_scale(__uint_as_float(a.thr_seed[threadIdx.x])) : 0.f;
   }
   __syncthreads();
   const unsigned gw = blockIdx.x * kRefWarps + warp, GW = gridDim.x * kRefWarps;
+  const int sub = lane & 7;
   for (int b = 0; b < nb; ++b) {
     const unsigned cnt = s_cnt[b];
     const unsigned nchunk = (cnt + 31) / 32;
@@ -2834,8 +2850,16 @@ k_refine_kx(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut, ui
     const int cutb = (int)s_cut[b];
     const uint64_t* list = a.sorted + (size_t)b * a.cap;
     const float4* qv = reinterpret_cast<const float4*>(a.queries + (size_t)b * a.len);
-    unsigned nref = 0;
+    unsigned nref = 0, npaa = 0;
     int since = 0;
+    float qpl[W2 > 0 ? W2 / 8 : 1];  // this lane's query PAA values (the PAA pre-filter)
+    float qpn_hi = 0.f;
+    if (W2 > 0) {
+      const float* qx = a.qaux + (size_t)b * kQAux;
+#pragma unroll
+      for (int e = 0; e < (W2 > 0 ? W2 / 8 : 1); ++e) qpl[e] = __ldg(qx + 16 + sub * (W2 / 8) + e);
+      qpn_hi = __ldg(qx + 1);
+    }
     // wave B starts from the threshold wave A's results imply
     if (wave == 1 && scale > 0.f) hist_threshold(a, b, scale);
     uint64_t knext = (first * 32 + lane < cnt) ? __ldg(list + first * 32 + lane) : kNoKey;
@@ -2851,6 +2875,16 @@ k_refine_kx(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut, ui
       const int bin = lb_bin(lb0, scale);
       const bool mine = i < cnt && (wave == 0 ? bin <= cutb : bin > cutb);
       unsigned m = __ballot_sync(0xffffffffu, mine && lb0 <= thr);
+      uint64_t kq = k0;  // the candidates' keys, one per lane (compacted by the PAA stage)
+      if (W2 > 0 && m) {
+        uint64_t* queue = s_queue[W2 > 0 ? warp : 0];
+        if (mine && lb0 <= thr) queue[__popc(m & ((1u << lane) - 1u))] = k0;
+        __syncwarp();
+        const int nk = paa_filter_queue<W2>(a, queue, __popc(m), thr, qpl, qpn_hi, npaa);
+        kq = lane < nk ? queue[lane] : kNoKey;
+        m = nk >= 32 ? 0xffffffffu : ((1u << nk) - 1u);
+        __syncwarp();
+      }
       while (m) {
         uint64_t key[U];
         bool live[U];
@@ -2859,7 +2893,7 @@ k_refine_kx(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut, ui
           const int src = m ? __ffs(m) - 1 : 0;
           const bool has = m != 0u;
           m &= m - 1;
-          key[u] = __shfl_sync(0xffffffffu, k0, src);
+          key[u] = __shfl_sync(0xffffffffu, kq, src);
           live[u] = has && key_val(key[u]) <= thr;
         }
         since += refine_group_k<NC, U>(a, qv, b, scale, key, live, thr, res, res_cnt, nref);
@@ -2870,9 +2904,12 @@ k_refine_kx(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut, ui
       }
     }
     if (lane == 0 && nref) atomicAdd(&s_refined[b], nref);
+    if (W2 > 0 && lane == 0 && npaa) atomicAdd(&s_paa[b], npaa);
   }
   __syncthreads();
   if (threadIdx.x < nb && s_refined[threadIdx.x]) atomicAdd(&a.refined[threadIdx.x], s_refined[threadIdx.x]);
+  if (W2 > 0 && threadIdx.x < nb && s_paa[threadIdx.x] && a.paa_rows)
+    atomicAdd(&a.paa_rows[threadIdx.x], s_paa[threadIdx.x]);
 }
 
 // Exact top-k of a query's result list: every true top-k member is there (its exact
@@ -3916,11 +3953,11 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
   ra.raw16 = (p.k == 1 && (p.raw_host || p.len >= kRaw16MinLen)) ? p.raw16 : nullptr;
   ra.refined16 = ws.updates;
   ra.ghist = ws.ghist;
-  ra.paa16 = p.k == 1 ? p.paa16 : nullptr;
+  ra.paa16 = (p.k == 1 || !p.sorted_refine) && p.len <= kRefQLen ? p.paa16 : nullptr;
   ra.w2 = p.w2;
   ra.paa_rows = all_paa ? all_paa + q0 : nullptr;
   ra.qaux = ws.qaux;
-  if (p.k == 1 && (ra.raw16 || ra.paa16) && p.len <= kRefQLen)  // the octet refine's query constants
+  if ((ra.raw16 || ra.paa16) && p.len <= kRefQLen)  // the octet / PAA refine's query constants
     PARIS_CHECK_LAUNCH(PARIS_LAUNCH("qprep", k_qaux, nb, 32, 0, st, qbatch, p.len, ra.paa16 ? p.w2 : 0, ws.qaux),
                        "qaux launch");
   dim3 g((unsigned)p.XB, (unsigned)nb);
@@ -3964,10 +4001,22 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
     cudaError_t e1 = cudaSuccess;
     const int NC = p.len <= 128 ? 1 : p.len <= 256 ? 2 : p.len <= 512 ? 4 : p.len <= 1024 ? 8 : 32;
     for (int wv = 0; wv < 2 && e1 == cudaSuccess; ++wv) {
-      const int grid = sms() * (NC <= 2 ? kRefUCtas : 2);
+      const int grid = sms() * (NC <= 2 ? (ra.paa16 ? 4 : kRefUCtas) : 2);
       switch (NC) {
-        case 1: e1 = PARIS_LAUNCH("refine", (k_refine_kx<1, kRefUU * 2>), grid, kRefThreads, 0, st, ra, nb, wv, ws.cursor, ws.sorted, res_cnt); break;
-        case 2: e1 = PARIS_LAUNCH("refine", (k_refine_kx<2, kRefUU>), grid, kRefThreads, 0, st, ra, nb, wv, ws.cursor, ws.sorted, res_cnt); break;
+        case 1:
+          if (ra.paa16)
+            e1 = PARIS_LAUNCH("refine", (k_refine_kx<1, kRefUU * 2, 32>), grid, kRefThreads, 0, st, ra, nb, wv, ws.cursor, ws.sorted, res_cnt);
+          else
+            e1 = PARIS_LAUNCH("refine", (k_refine_kx<1, kRefUU * 2>), grid, kRefThreads, 0, st, ra, nb, wv, ws.cursor, ws.sorted, res_cnt);
+          break;
+        case 2:
+          if (ra.paa16 && ra.w2 == 64)
+            e1 = PARIS_LAUNCH("refine", (k_refine_kx<2, kRefUU, 64>), grid, kRefThreads, 0, st, ra, nb, wv, ws.cursor, ws.sorted, res_cnt);
+          else if (ra.paa16)
+            e1 = PARIS_LAUNCH("refine", (k_refine_kx<2, kRefUU, 32>), grid, kRefThreads, 0, st, ra, nb, wv, ws.cursor, ws.sorted, res_cnt);
+          else
+            e1 = PARIS_LAUNCH("refine", (k_refine_kx<2, kRefUU>), grid, kRefThreads, 0, st, ra, nb, wv, ws.cursor, ws.sorted, res_cnt);
+          break;
         case 4: e1 = PARIS_LAUNCH("refine", (k_refine_kx<4, 1>), grid, kRefThreads, 0, st, ra, nb, wv, ws.cursor, ws.sorted, res_cnt); break;
         case 8: e1 = PARIS_LAUNCH("refine", (k_refine_kx<8, 1>), grid, kRefThreads, 0, st, ra, nb, wv, ws.cursor, ws.sorted, res_cnt); break;
         default: e1 = PARIS_LAUNCH("refine", (k_refine_kx<32, 1>), grid, kRefThreads, 0, st, ra, nb, wv, ws.cursor, ws.sorted, res_cnt); break;
@@ -4172,12 +4221,16 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   // queries (C5 sigma = 0.2, k = 100: ~670 K of 2e7), so n/16 -- an overflow costs a
   // per-query re-scan
   // candidate buffer per query: at least max(65536, n/32) (n/16 for k > 1), grown to a
-  // 2 GB budget per candidate array when that is larger (hard queries -- C3: up to 24% of
-  // n -- then stay on the regular path instead of the overflow fallback)
+  // budget per candidate array of 1/8 of the free device memory, clamped to [2, 16] GB
+  // (hard queries -- C3: up to 24% of n; C5 k = 100: more -- then stay on the regular
+  // path instead of the overflow fallback)
   {
     const int Bq = 2 * pairs_for(p.B);
     const int64_t floor_cap = std::max<int64_t>(65536, k > 1 ? n / 16 : n / 32);
-    const int64_t budget = (int64_t)(2ll << 30) / (8ll * Bq);
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); fr = 0; }
+    const int64_t bud_bytes = std::min<int64_t>(16ll << 30, std::max<int64_t>(2ll << 30, (int64_t)(fr / 8)));
+    const int64_t budget = bud_bytes / (8ll * Bq);
     p.cap = (nb_mode || approx) ? 1 : std::min<int64_t>(n, std::max(floor_cap, budget));
     if (cfg && cfg->reserved[4] > 0 && !nb_mode && !approx) p.cap = std::min<int64_t>(n, cfg->reserved[4]);  // test hook
   }

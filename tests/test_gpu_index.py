@@ -264,3 +264,27 @@ def test_paa_f16_definition(P):
         ok = np.abs(m) < 65000
         assert np.array_equal(got[ok], ref[ok])
         assert np.isnan(got[~ok]).all() and (~ok).any()
+
+
+@pytest.mark.parametrize("k,w2,length", [(4, 64, 256), (100, 64, 256), (10, 32, 128)])
+def test_knn_index_paa_prefilter_k(P, k, w2, length):
+    """k > 1 with the PAA pre-filter (k_refine_kx): each candidate below the live k-th
+    threshold meets the PAA bound before its raw row -- the exact top-k, equal to the
+    unfiltered search and to the oracle (member queries, ties)."""
+    import torch
+    n, nq = 30_000 + 16, 20
+    x = datagen.random_walks(n, length, 900 + k)
+    q = datagen.random_walks(nq, length, 901 + k)
+    q[:3] = x[[11, 29_000, 500]]
+    x[12] = x[11]                                      # a tie at distance 0
+    xd = torch.from_numpy(x).cuda()
+    sax = P.summarize(xd, 16, 256)
+    idx = P.index_build(sax, 16, 256)
+    paa = P.paa_f16(xd, w2)
+    qd = torch.from_numpy(q).cuda()
+    gi, gd, st = P.knn_index(xd, idx, qd, k=k, paa16=paa, stats=True)
+    hi, hd, st0 = P.knn_index(xd, idx, qd, k=k, stats=True)
+    assert torch.equal(gi, hi) and torch.equal(gd, hd)
+    ri, rd2 = oracle.knn_bruteforce(x, q, k)
+    check_knn(x, q, gi.cpu().numpy(), gd.cpu().numpy(), ri, rd2)
+    assert st["paa_rows"].sum() > 0 and st["refined"].sum() < st0["refined"].sum()
