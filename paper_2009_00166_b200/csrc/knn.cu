@@ -4229,7 +4229,9 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
     const int64_t floor_cap = std::max<int64_t>(65536, k > 1 ? n / 16 : n / 32);
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); fr = 0; }
-    const int64_t bud_bytes = std::min<int64_t>(16ll << 30, std::max<int64_t>(2ll << 30, (int64_t)(fr / 8)));
+    // (whole GB: the workspace the first call allocates barely moves the budget of the next)
+    const int64_t bud_bytes =
+        std::min<int64_t>(16ll << 30, std::max<int64_t>(2ll << 30, (int64_t)(fr / 8) & ~((1ll << 30) - 1)));
     const int64_t budget = bud_bytes / (8ll * Bq);
     p.cap = (nb_mode || approx) ? 1 : std::min<int64_t>(n, std::max(floor_cap, budget));
     if (cfg && cfg->reserved[4] > 0 && !nb_mode && !approx) p.cap = std::min<int64_t>(n, cfg->reserved[4]);  // test hook

@@ -2,9 +2,10 @@
 the CPU oracle answers one by one: the oracle's LB-pruned exact scan (itself pinned to brute
 force) over the full collection, on the oracle's own SAX (independent of the CUDA summarize).
 
-* C4 (1e8 x 256): exactly the bench's default call -- ``knn_index(..., raw16=raw_bf16(raw))``,
-  k = 1, all 100 queries in ONE call (a 64-query pass and a 36-query pass, the bf16 refinement
-  pre-filter, the 2048-series leaf seed) -- queries sampled from both passes; the flat path too.
+* C4 (1e8 x 256): exactly the bench's default call -- ``knn_index(..., raw16=raw_bf16(raw),
+  paa16=paa_f16(raw, 64))``, k = 1, all 100 queries in ONE call (a 64-query pass and a 36-query
+  pass, the PAA and bf16 refinement pre-filters, the 2048-series leaf seed) -- queries sampled
+  from both passes; the flat path too.
 * C5 (2e7 x 256): the query-hardness sweep's k = 100 mode at sigma = 0.2 and sigma = 0.01
   (bench.py's query sets), index path with the bf16 copy passed as the bench does, and flat.
 * C3 (1e7 x 128): calls of 64 queries (BASELINE config 3), two calls, queries from both.
@@ -70,9 +71,10 @@ def test_c4_bench_call_parity(P):
     sax = P.summarize(raw, 16, 256)
     idx = P.index_build(sax, 16, 256)
     raw16 = P.raw_bf16(raw)
-    gi, gd, st = P.knn_index(raw, idx, q, k=1, raw16=raw16, stats=True)    # one call: 64 + 36
-    assert st["raw16_rows"].sum() > 0, "the bf16 pre-filter did not run"
-    del raw16, idx
+    paa16 = P.paa_f16(raw, 64)
+    gi, gd, st = P.knn_index(raw, idx, q, k=1, raw16=raw16, paa16=paa16, stats=True)    # one call: 64 + 36
+    assert st["paa_rows"].sum() > 0, "the PAA pre-filter did not run"
+    del raw16, paa16, idx
     gi_f, gd_f = P.knn_exact(raw, sax, q[:32], k=1)     # flat path: two 16-query passes
     del sax
     torch.cuda.empty_cache()
@@ -101,12 +103,13 @@ def test_c5_k100_hardness_parity(P):
     idx = P.index_build(sax, 16, 256)
     raw16 = P.raw_bf16(raw)
     sets = {}
+    paa16 = P.paa_f16(raw, 64)
     for si, sig in ((0, 0.01), (4, 0.2)):
         q, _ = dg.noisy_members(raw, 200, sig, qs + 101 * (si + 1))
-        gi, gd = P.knn_index(raw, idx, q, k=100, raw16=raw16)           # all 200: 4 passes
+        gi, gd = P.knn_index(raw, idx, q, k=100, raw16=raw16, paa16=paa16)   # all 200: 4 passes
         fi, fd = P.knn_exact(raw, sax, q[:2], k=100)
         sets[sig] = (q.cpu().numpy(), gi.cpu().numpy(), gd.cpu().numpy(), fi.cpu().numpy(), fd.cpu().numpy())
-    del raw16, idx, sax
+    del raw16, paa16, idx, sax
     torch.cuda.empty_cache()
     x = raw.cpu().numpy()
     del raw
@@ -130,13 +133,14 @@ def test_c3_calls_of_64_parity(P):
     sax = P.summarize(raw, 16, 256)
     idx = P.index_build(sax, 16, 256)
     raw16 = P.raw_bf16(raw)
-    out = [P.knn_index(raw, idx, q[c:c + 64], k=1, raw16=raw16) for c in (0, 64)]
+    paa16 = P.paa_f16(raw, 32)                       # bench.py's default at len 128
+    out = [P.knn_index(raw, idx, q[c:c + 64], k=1, raw16=raw16, paa16=paa16) for c in (0, 64)]
     fl = [P.knn_exact(raw, sax, q[c:c + 64], k=1) for c in (0, 64)]
     gi = torch.cat([o[0] for o in out]).cpu().numpy()
     gd = torch.cat([o[1] for o in out]).cpu().numpy()
     fi = torch.cat([o[0] for o in fl]).cpu().numpy()
     fd = torch.cat([o[1] for o in fl]).cpu().numpy()
-    del raw16, idx, sax
+    del raw16, paa16, idx, sax
     torch.cuda.empty_cache()
     x = raw.cpu().numpy()
     del raw
@@ -165,9 +169,10 @@ def test_c1_c2_parity(P, config):
     sax = P.summarize(raw, 16, 256)
     idx = P.index_build(sax, 16, 256)
     raw16 = P.raw_bf16(raw)
-    gi, gd = P.knn_index(raw, idx, q, k=1, raw16=raw16)
+    paa16 = P.paa_f16(raw, 64)
+    gi, gd = P.knn_index(raw, idx, q, k=1, raw16=raw16, paa16=paa16)
     fi, fd = P.knn_exact(raw, sax, q, k=1)
-    ti, td = P.knn_index(raw, idx, q, k=10)
+    ti, td = P.knn_index(raw, idx, q, k=10, paa16=paa16)
     x = raw.cpu().numpy()
     qh = q.cpu().numpy()
     rows = np.arange(0, nq, nq // 10)
