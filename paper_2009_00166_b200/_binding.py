@@ -307,10 +307,10 @@ def knn_index(raw: torch.Tensor, index: Index, queries: torch.Tensor, k: int = 1
 
 def knn_nb(raw: torch.Tensor, sax: torch.Tensor, queries: torch.Tensor, w: int = 16, card: int = 256,
            out_idx: torch.Tensor | None = None, out_dist: torch.Tensor | None = None, stream=None,
-           config: KnnConfig | None = None, stats: bool = False):
+           config: KnnConfig | None = None, stats: bool = False, sync: bool | None = None):
     """Exact 1-NN with nb-ParIS+ (paris_knn_nb): per-worker BSF copies, fused LB -> refine."""
     return knn_exact(raw, sax, queries, k=1, w=w, card=card, out_idx=out_idx, out_dist=out_dist, stream=stream,
-                     config=config, stats=stats, _nb=True)
+                     config=config, stats=stats, _nb=True, sync=sync)
 
 
 def _make_config(config, nq: int):

@@ -1602,16 +1602,17 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
 // ---------------------------------------------------------------- K4, one query per pass
 // B = 1 (flat path): the pass is one lookup + two FMAs per (series, segment), so
 // it is fed by plain 8-byte loads at high occupancy rather than the TMA ring (whose 16
-// row copies per tile cap delivery near 2.7 TB/s): one CTA of 24 warps per SM, a thread
-// owns SPT consecutive series (one uint2 / uint4 per segment row), and the single-query
+// row copies per tile cap delivery near 2.7 TB/s): one CTA of 32 warps per SM, a thread
+// owns SPT = 4 consecutive series (one 32-bit word per segment row; the next group's 16
+// words prefetched into registers while the current group is bounded), and the single-query
 // fp16x2 form accumulates (ABOVE, BELOW) per series.  The region table (-U16, L16) is
 // replicated 32x (entry c of lane l at T + 256c + 4l, T a 64 KB boundary of dynamic
 // shared memory): ONE byte permute {lane*4, symbol, T bits 16..31} is a lookup's whole
 // address, so a (series, segment) costs PRMT + LDS + 2 HFMA2.
-constexpr int kLb1Threads = 768;
 #ifndef PARIS_LB1_SPT
-#define PARIS_LB1_SPT 8
+#define PARIS_LB1_SPT 4
 #endif
+constexpr int kLb1Threads = PARIS_LB1_SPT >= 8 ? 768 : 1024;
 
 // SPT series per thread: 16 (one uint4 per row) or 8 (one uint2 per row, fewer
 // registers).
@@ -1621,10 +1622,11 @@ k_lb1(LbArgs a) {
   extern __shared__ __align__(128) uint8_t dsm1[];
   __shared__ uint32_t s_qd[kTW];
   __shared__ LbConsts s_c;
-  __shared__ WarpBuf s_wb[kLb1Threads / 32];
   __shared__ unsigned s_hist[kNB];
+  // the warps' candidate buffers at the start of dynamic shared memory, below the table
+  WarpBuf* s_wb = reinterpret_cast<WarpBuf*>(dsm1);
   const uint32_t S0 = smem_u32(dsm1);
-  const uint32_t T = (S0 + 0xFFFFu) & ~0xFFFFu;
+  const uint32_t T = (S0 + (uint32_t)(sizeof(WarpBuf) * (kLb1Threads / 32)) + 0xFFFFu) & ~0xFFFFu;
   {
     uint32_t dyn;
     asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
@@ -1646,26 +1648,39 @@ k_lb1(LbArgs a) {
   const uint32_t lanebase = T | ((uint32_t)lane * 4u);  // bytes {lane * 4, 0, T bits 16-31}
   const int64_t n = a.n;
   const int64_t ngroups = n / SPT;  // n % 16 == 0 (tiled-path condition)
+  // the next group's words are loaded while the current group is bounded (software
+  // prefetch: one HBM latency per group is hidden behind the previous group's lookups)
+  auto load_words = [&](int64_t g, uint32_t (&wd)[kTW][SPT / 4]) {
+    const int64_t i0 = (int64_t)SPT * g;
+#pragma unroll
+    for (int s = 0; s < kTW; ++s) {
+      if (g >= ngroups) { wd[s][0] = 0u; if (SPT > 4) wd[s][SPT / 4 - 1] = 0u; continue; }
+      if (SPT == 16) {
+        const uint4 v = __ldcs(reinterpret_cast<const uint4*>(a.sax + (size_t)s * n + i0));
+        wd[s][0] = v.x; wd[s][1 % (SPT / 4)] = v.y; wd[s][2 % (SPT / 4)] = v.z; wd[s][3 % (SPT / 4)] = v.w;
+      } else if (SPT == 8) {
+        const uint2 v = __ldcs(reinterpret_cast<const uint2*>(a.sax + (size_t)s * n + i0));
+        wd[s][0] = v.x; wd[s][1 % (SPT / 4)] = v.y;
+      } else {
+        wd[s][0] = __ldcs(reinterpret_cast<const uint32_t*>(a.sax + (size_t)s * n + i0));
+      }
+    }
+  };
+  uint32_t wnext[kTW][SPT / 4];
+  load_words((int64_t)blockIdx.x * kLb1Threads + tid, wnext);
   for (int64_t g = (int64_t)blockIdx.x * kLb1Threads + tid; g - lane < ngroups;
        g += (int64_t)gridDim.x * kLb1Threads) {
     const int64_t i0 = (int64_t)SPT * g;
+    uint32_t wd[kTW][SPT / 4];
+#pragma unroll
+    for (int s = 0; s < kTW; ++s)
+#pragma unroll
+      for (int c = 0; c < SPT / 4; ++c) wd[s][c] = wnext[s][c];
+    load_words(g + (int64_t)gridDim.x * kLb1Threads, wnext);
     uint32_t acc[SPT];
 #pragma unroll
     for (int j = 0; j < SPT; ++j) acc[j] = 0u;
     if (g < ngroups) {
-      uint32_t wd[kTW][SPT / 4];
-#pragma unroll
-      for (int s = 0; s < kTW; ++s) {
-        if (SPT == 16) {
-          const uint4 v = __ldcs(reinterpret_cast<const uint4*>(a.sax + (size_t)s * n + i0));
-          wd[s][0] = v.x; wd[s][1 % (SPT / 4)] = v.y; wd[s][2 % (SPT / 4)] = v.z; wd[s][3 % (SPT / 4)] = v.w;
-        } else if (SPT == 8) {
-          const uint2 v = __ldcs(reinterpret_cast<const uint2*>(a.sax + (size_t)s * n + i0));
-          wd[s][0] = v.x; wd[s][1 % (SPT / 4)] = v.y;
-        } else {
-          wd[s][0] = __ldcs(reinterpret_cast<const uint32_t*>(a.sax + (size_t)s * n + i0));
-        }
-      }
 #pragma unroll
       for (int s = 0; s < kTW; ++s) {
         const uint32_t qd = s_qd[s];

@@ -188,3 +188,42 @@ def test_summarize_file_and_mapped_search(P, small_chunks, tmp_path, direct_io):
 def test_summarize_file_rejects_missing(P):
     with pytest.raises(P.ParisError):
         P.summarize_file("/nonexistent/raw.f32", 100, 256)
+
+
+@pytest.mark.parametrize("source", ["pinned", "file"])
+def test_host_raw_host_buffers_equal_device_buffers(P, tmp_path, source):
+    """With raw outside HBM (pinned host memory, or a mapped file) and the bf16 copy in HBM,
+    the end-to-end call with HOST query / output buffers (pinned; staged by the library,
+    asynchronous) returns exactly the rows of the device-buffer call, over many calls on one
+    stream (the cached workspace reused), and both equal the oracle."""
+    import torch
+    n, length, nq = 200_000, 256, 100
+    x = datagen.random_walks(n, length, 5151)
+    q = datagen.random_walks(nq, length, 5152)
+    q[7] = x[12345]
+    xd = torch.from_numpy(x).cuda()
+    sax = P.summarize(xd, 16, 256)
+    idx = P.index_build(sax, 16, 256)
+    r16 = P.raw_bf16(xd)
+    del xd
+    mapped = None
+    if source == "pinned":
+        raw = torch.from_numpy(x).pin_memory()
+    else:
+        path = tmp_path / "raw.f32"
+        x.tofile(path)
+        mapped = P.MappedRaw(str(path), n, length)
+        raw = mapped.tensor
+    qd = torch.from_numpy(q).cuda()
+    hq = torch.from_numpy(q).pin_memory()
+    di, dd = P.knn_index(raw, idx, qd, k=1, raw16=r16)
+    hi = torch.empty((nq, 1), dtype=torch.int64).pin_memory()
+    hd = torch.empty((nq, 1), dtype=torch.float32).pin_memory()
+    for _ in range(3):
+        P.knn_index(raw, idx, hq, k=1, raw16=r16, out_idx=hi, out_dist=hd, sync=False)
+        torch.cuda.current_stream().synchronize()
+        assert torch.equal(hi, di.cpu()) and torch.equal(hd, dd.cpu())
+    ri, rd2 = oracle.knn_bruteforce(x, q, 1)
+    check_knn(x, q, hi.numpy(), hd.numpy(), ri, rd2)
+    if mapped is not None:
+        mapped.close()
