@@ -536,7 +536,17 @@ def run_gpu(args):
             e1.record(st)
             torch.cuda.synchronize()
             r["e2e_value"] = (nq if sharded else nq * ws) / (reduce_max_ms(e0.elapsed_time(e1) / args.steps, dev, ws) / 1e3)
-            assert torch.equal(hidx, out_idx.cpu()), "host-buffer path disagrees with device path"
+            if not torch.equal(hidx, out_idx.cpu()):
+                bad = (hidx != out_idx.cpu()).nonzero()[:, 0].tolist()
+                msg = []
+                for b in bad[:4]:
+                    ih, idv = int(hidx[b, 0]), int(out_idx[b, 0])
+                    qh = queries[b].double().cpu()
+                    th = float(((raw[ih].double().cpu() if not raw.is_cuda else raw[ih].double().cpu()) - qh).pow(2).sum().sqrt())
+                    td = float(((raw[idv].double().cpu()) - qh).pow(2).sum().sqrt())
+                    msg.append(f"q{b}: host {ih} d={float(hdist[b, 0]):.6f} (true {th:.6f}) | device {idv} "
+                               f"d={float(out_dist[b, 0]):.6f} (true {td:.6f})")
+                raise AssertionError(f"host-buffer path disagrees with device path on {len(bad)} rows: " + "; ".join(msg))
         cand = stats["candidates"].numpy().astype(np.float64)
         refined = stats["refined"].numpy().astype(np.float64)
         kern = {}

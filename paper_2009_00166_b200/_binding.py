@@ -59,7 +59,7 @@ class KnnConfig:
     wave_a: int = 0     # k = 1: first refinement wave per query (0 = 2048)
     force_direct: bool = False  # test hook: use the direct-load LB kernels even where the TMA-tiled ones apply
     sorted_refine: bool = False  # k = 1: refine the bucket-sorted lists (K5 scatter) instead of the unsorted waves
-    index_seeds: int = 0        # index mode: seed series around the query's leaf (0 = 1024)
+    index_seeds: int = 0        # index mode: seed series around the leaf (0 = 1024, 2048 from 5e7 series, 32k for k > 1; 64 with host raw and no bf16 copy)
     seed_from_out: bool = False  # test hook: seed from the rows already in out_idx/out_dist (device)
     tau_in: "torch.Tensor | None" = None  # [nq] float32 CUDA: external bound of each query's k-th NN distance
     cap: int = 0                # test hook: candidate-buffer capacity per query (forces the overflow fallback)

@@ -606,7 +606,7 @@ struct LbArgs {
   uint64_t* cand;
   int64_t cap;
   const uint32_t* perm;  // index mode: sorted position -> series id (else nullptr)
-  const uint8_t* env;    // index mode: [n/128 blocks][2][16] min/max symbols (else nullptr)
+  const uint8_t* env;    // index mode: [n/64 blocks][2][16] min/max symbols (else nullptr)
   unsigned* blocks;      // index mode: per query, blocks whose envelope bound passed
 };
 
@@ -1148,6 +1148,15 @@ __device__ __forceinline__ uint32_t half_of(uint32_t v, int h) { return (v >> (1
 // shared address (the symbol lands in bits 8..15).
 constexpr int kIWarps = 24;                   // consumer warps
 constexpr int kIThreads = (kIWarps + 1) * 32; // + the producer warp
+#ifndef PARIS_LBI_GROUPS
+#define PARIS_LBI_GROUPS 2
+#endif
+// consumer groups: group g takes the tiles it = g, g + G, ... (its stages), so a warp sees
+// every G-th tile and does ~G times the rounds per stage visit (the per-visit cost -- wait,
+// arrive, the final empty claim -- is paid half as often)
+constexpr int kIGroups = PARIS_LBI_GROUPS;
+constexpr int kIGroupWarps = kIWarps / kIGroups;
+static_assert(kIWarps % kIGroups == 0, "equal consumer groups");
 constexpr int kWBI = 64;                      // staged candidates per consumer warp
 constexpr uint32_t kIStageBytes = (uint32_t)kTileBytes;
 struct LbiWarp {
@@ -1436,7 +1445,7 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
   if (tid == 0) {
     for (int st = 0; st < NST; ++st) {
       mbar_init(&M.full[st], 1);
-      mbar_init(&M.empty[st], kIWarps);
+      mbar_init(&M.empty[st], kIGroupWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1515,7 +1524,7 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
     const LbConsts& c = M.c;
     const uint32_t lanebase = T | ((uint32_t)lane * 4u);  // bytes {lane * 4, 0, T bits 16-31}
     const int h = lane >> 4, hl = lane & 15;
-    for (int64_t it = 0;; ++it) {
+    for (int64_t it = warp / kIGroupWarps;; it += kIGroups) {
       const int64_t li = blockIdx.x + it * gridDim.x;
       if (li >= nlist) break;
       const int st = (int)(it % NST);
@@ -4190,7 +4199,7 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   Plan p;
   p.n = n; p.len = len; p.w = w; p.card = card; p.k = k;
   {
-    const int cap_b = indexed ? kMaxB : kMaxBFlat;  // index: 32 queries per pass, flat: 16
+    const int cap_b = indexed ? kMaxB : kMaxBFlat;  // index: 64 queries per pass, flat: 16
     p.B = (cfg && cfg->batch > 0) ? std::min(cfg->batch, cap_b) : cap_b;
   }
   p.tiled = (n % 16 == 0) && (w == kTW) && (indexed || !(cfg && cfg->reserved[0] == 1));
