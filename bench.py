@@ -311,6 +311,8 @@ def run_gpu(args):
                 for r0 in range(0, n_local, chunk_rows):
                     m = min(chunk_rows, n_local - r0)
                     dg.walks(m, length, ds, first_id=lo + r0, out=buf[:m])
+                    if want16:
+                        raw16[r0:r0 + m].copy_(P.raw_bf16(buf[:m]))
                     hbuf[:m].copy_(buf[:m])
                     f.write(hbuf[:m].numpy().tobytes())
                 f.flush()
