@@ -45,6 +45,20 @@ W, CARD = 16, 256
 ALU_CLOCK_GHZ = 1.965  # B200 clocks.max.sm (B200_PROFILING.md)
 
 
+
+def workload_desc(cfg, args):
+    """The config's workload line plus every override this run applied (n, raw placement, sigma)."""
+    extra = []
+    if getattr(args, "n", None):
+        extra.append(f"n = {args.n:.3g} series (override)")
+    if getattr(args, "raw_host", False):
+        extra.append("raw in pinned host memory, SAX/index/bf16 copy in HBM (f3)")
+    if getattr(args, "raw_file", None):
+        extra.append(f"raw in a file on local disk ({args.raw_file}), mapped for the search (f3)")
+    if args.sigma is not None:
+        extra.append(f"queries: sigma = {args.sigma}")
+    return cfg["desc"] + (" [" + "; ".join(extra) + "]" if extra else "")
+
 def log(*a):
     print("[bench]", *a, file=sys.stderr, flush=True)
 
@@ -240,7 +254,7 @@ def run_reference(args):
             "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": sec_per_query * nq * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg["desc"] + ("" if args.sigma is None else f" [queries: sigma = {args.sigma}]"), "n": n, "len": length, "w": W, "card": CARD, "nq": nq, "k": k},
+            "config": {"workload": workload_desc(cfg, args), "n": n, "len": length, "w": W, "card": CARD, "nq": nq, "k": k},
             "cpu_baseline": dict({"value": value, "unit": "queries/s", "cores": 1, "kind": "oracle", "sample": sample},
                                  **host_info()),
             "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -725,7 +739,7 @@ def run_gpu(args):
             "higher_is_better": True, "scaling": "strong" if sharded else "weak", "vs_baseline": None,
             "dtype": "f32",
             "data": "synthetic (seeded Philox random walks, z-normalized; no dataset on the box)",
-            "config": {"workload": cfg["desc"] + ("" if args.sigma is None else f" [queries: sigma = {args.sigma}]"), "n": n, "len": length, "w": W, "card": CARD, "nq": nq, "k": k,
+            "config": {"workload": workload_desc(cfg, args), "n": n, "len": length, "w": W, "card": CARD, "nq": nq, "k": k,
                        "batch": primary["batch"], "path": args.path, "index_build_ms": index_ms,
                        "raw_bf16": None if raw16 is None else {"build_ms": raw16_ms, "bytes": raw16.numel() * 2},
                        "paa_f16": None if paa16 is None else {"w2": args.paa, "build_ms": paa_ms, "bytes": paa16.numel() * 2},
