@@ -1490,6 +1490,13 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
         bnext = __ldg(bmask + (size_t)tnext * kBPT + lane);
       }
       if (it >= NST) mbar_wait(&M.empty[st], (unsigned)(((it / NST) - 1) & 1));
+      // the copy first, the item decode while it is in flight: its complete_tx may land
+      // before the expect_tx below (the tx-count goes transiently negative), but the
+      // phase cannot complete before that arrival
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        bulk_g2s(gbase + stage_addr(st), a.sax + (size_t)tile * kTileBytes, (unsigned)kTileBytes, &M.full[st]);
+      }
       const int cnt = (__popcll(m) + 1) >> 1;
       int incl = cnt;
 #pragma unroll
@@ -1512,11 +1519,7 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
         M.next[st] = 0;
       }
       __syncwarp();
-      if (lane == 31) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&M.full[st], (unsigned)kTileBytes);  // release: the items are visible to the waiters
-        bulk_g2s(gbase + stage_addr(st), a.sax + (size_t)tile * kTileBytes, (unsigned)kTileBytes, &M.full[st]);
-      }
+      if (lane == 31) mbar_expect_tx(&M.full[st], (unsigned)kTileBytes);  // release: the items are visible
     }
   } else {
     // ---- consumers
@@ -1721,6 +1724,187 @@ k_lb1(LbArgs a) {
   __syncthreads();
   for (int i = tid; i < kNB; i += kLb1Threads)
     if (s_hist[i]) atomicAdd(&a.hist[i], s_hist[i]);
+}
+
+// ---------------------------------------------------------------- K4, one query per pass (TMA ring)
+// k_lb1t: the B = 1 pass as a producer/consumer stream.  One warp issues the 16 row
+// copies (2 KB each, cp.async.bulk) of a 2048-series tile into a 4-stage ring; 16
+// consumer warps own 4 series per thread, copy their 16 segment words to registers
+// (conflict-free 32-bit loads), release the stage at once (so the producer refills it
+// while they compute) and bound the words with the single-query fp16 form (PRMT + LDS +
+// 2 HFMA2 per (series, segment), the region table replicated 32x as in k_lb1).  The
+// (ABOVE, BELOW) halves of two series are summed by one packed fp16 add (one more (1+u)
+// factor inside G, as k_lbi); candidates are staged per warp in the table's holes.
+// No global address arithmetic per load (k_lb1 spent about half its issue slots on it).
+// Shared plan (S0 = dynamic base, T = the 64 KB boundary above stage 0 + misc):
+//   [S0, S0 + 32K) stage 0 | misc | [T, T + 64K) table + holes | T + 64K: stages 1..3
+//   holes 0..31: warp w's staged keys in holes 2w, 2w + 1 (16 keys each); 64..71: the
+//   256-bin LB histogram.
+constexpr int kL1Warps = 16;                      // 512 consumer threads x 4 series = one tile
+constexpr int kL1Threads = (kL1Warps + 1) * 32;  // + the producer warp
+constexpr int kL1Stages = 4;
+constexpr int kL1WB = 32;                         // staged keys per consumer warp
+struct Lb1Misc {
+  uint64_t full[kL1Stages], empty[kL1Stages];
+  LbConsts c;
+  uint32_t qd[kTW];
+  unsigned wn[kL1Warps];
+};
+static_assert(kTileBytes + sizeof(Lb1Misc) + 2048 <= 65536, "stage 0 + misc below the table");
+
+__device__ __forceinline__ uint32_t l1_key_addr(uint32_t T, int warp, int e) {
+  return T + 256u * (uint32_t)(2 * warp + (e >> 4)) + 128u + 8u * (uint32_t)(e & 15);
+}
+__device__ __forceinline__ uint32_t l1_hist_addr(uint32_t T, int bin) {
+  return T + 256u * (uint32_t)(64 + (bin >> 5)) + 128u + 4u * (uint32_t)(bin & 31);
+}
+
+__device__ void lb1t_flush(uint32_t T, int warp, unsigned& wn, const LbConsts& c, const LbArgs& a) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  const int m = (int)wn;
+  if (m == 0) return;
+  unsigned base = 0;
+  if (lane == 0) base = atomicAdd(&a.count[0], (unsigned)m);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (lane < m) {
+    const uint64_t key = lds_u64(l1_key_addr(T, warp, lane));
+    if ((int64_t)base + lane < a.cap) {
+      a.cand[(size_t)base + lane] = key;
+      atoms_add(l1_hist_addr(T, lb_bin(key_val(key), c.scale[0])), 1u);
+    }
+  }
+  __syncwarp();
+  if (lane == 0) wn = 0;
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kL1Threads, 1)
+k_lb1t(LbArgs a) {
+  extern __shared__ __align__(128) uint8_t dsm[];
+  const uint32_t S0 = smem_u32(dsm);
+  const uint32_t T = (S0 + (uint32_t)(kTileBytes + sizeof(Lb1Misc)) + 0xFFFFu) & ~0xFFFFu;
+  uint8_t* const gbase = dsm - S0;
+  Lb1Misc& M = *reinterpret_cast<Lb1Misc*>(dsm + kTileBytes);
+  auto stage_addr = [&](int st) -> uint32_t {
+    return st == 0 ? S0 : T + 65536u + (uint32_t)(st - 1) * (uint32_t)kTileBytes;
+  };
+  {
+    uint32_t dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    if (T + 65536u + (uint32_t)(kL1Stages - 1) * (uint32_t)kTileBytes > S0 + dyn) __trap();
+  }
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t n = a.n;
+  const int64_t ntiles = (n + kTS - 1) / kTS;
+  if (tid == 0) {
+    for (int st = 0; st < kL1Stages; ++st) {
+      mbar_init(&M.full[st], 1);
+      mbar_init(&M.empty[st], kL1Warps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = tid; i < kMaxCard * 32; i += kL1Threads)
+    sts_u32(T + 256u * (uint32_t)(i >> 5) + 4u * (uint32_t)(i & 31), a.tab->lu16p[i >> 5]);
+  for (int i = tid; i < kNB; i += kL1Threads) sts_u32(l1_hist_addr(T, i), 0u);
+  if (tid < kTW) {
+    const uint2 v = a.g_q16[tid];  // pair layout, slot 0 = low halves: half2(q_lo16, -q_hi16)
+    M.qd[tid] = (v.x & 0xFFFFu) | (v.y << 16);
+  }
+  if (tid < kL1Warps) M.wn[tid] = 0;
+  lb_consts_init(a, 1, &M.c);  // ends with __syncthreads
+
+  if (warp == kL1Warps) {
+    // ---- producer: 16 row copies per tile into the stage the consumers released
+    int64_t it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int st = (int)(it % kL1Stages);
+      if (it >= kL1Stages) mbar_wait(&M.empty[st], (unsigned)(((it / kL1Stages) - 1) & 1));
+      const int64_t base = tile * kTS;
+      const unsigned bytes = (unsigned)imin64(kTS, n - base);  // n % 16 == 0: a multiple of 16
+      if (lane == 0) mbar_expect_tx(&M.full[st], bytes * (unsigned)kTW);
+      __syncwarp();
+      if (lane < kTW)
+        bulk_g2s(gbase + stage_addr(st) + (uint32_t)lane * (uint32_t)kTS, a.sax + (size_t)lane * n + base, bytes,
+                 &M.full[st]);
+    }
+  } else {
+    // ---- consumers: thread t owns series 4t .. 4t+3 of every tile of this CTA
+    const LbConsts& c = M.c;
+    const uint32_t lanebase = T | ((uint32_t)lane * 4u);  // bytes {lane * 4, -, T bits 16-31}
+    const uint32_t T2 = (c.T16[0] & 0xFFFFu) * 0x10001u;  // slot 0's threshold in both halves
+    const float thr = c.thr[0];
+    uint32_t qd[kTW];
+#pragma unroll
+    for (int s = 0; s < kTW; ++s) qd[s] = M.qd[s];
+    int64_t it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int st = (int)(it % kL1Stages);
+      mbar_wait(&M.full[st], (unsigned)((it / kL1Stages) & 1));
+      const uint32_t* rows = reinterpret_cast<const uint32_t*>(gbase + stage_addr(st)) + tid;
+      uint32_t wd[kTW];
+#pragma unroll
+      for (int s = 0; s < kTW; ++s) wd[s] = rows[s * (kTS / 4)];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&M.empty[st]);  // the words are in registers: refill now
+      uint32_t acc[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int s = 0; s < kTW; ++s) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t t = lds_u32(__byte_perm(wd[s], lanebase, 0x7604u | ((uint32_t)j << 4)));
+          const uint32_t d = h2_fma_relu(qd[s], kHalf2One, t);
+          acc[j] = h2_fma(d, d, acc[j]);
+        }
+      }
+      // LB16 of series (0, 1) and (2, 3): ABOVE + BELOW in one packed add each
+      uint32_t s01, s23;
+      asm("add.rn.f16x2 %0, %1, %2;" : "=r"(s01) : "r"(__byte_perm(acc[0], acc[1], 0x5410)),
+          "r"(__byte_perm(acc[0], acc[1], 0x7632)));
+      asm("add.rn.f16x2 %0, %1, %2;" : "=r"(s23) : "r"(__byte_perm(acc[2], acc[3], 0x5410)),
+          "r"(__byte_perm(acc[2], acc[3], 0x7632)));
+      const int64_t i0 = tile * kTS + 4 * (int64_t)tid;
+      uint32_t pf = h2_le_bits(s01, T2) | (h2_le_bits(s23, T2) << 2);
+      if (i0 >= n) pf = 0u;  // a partial last tile (n % 16 == 0: whole groups of 4)
+      if (!__any_sync(0xffffffffu, pf != 0u)) continue;
+      // rigorous fp32 bounds for the pairs that passed the fp16 test (rare)
+      float lbv[4];
+      unsigned m = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t v = j < 2 ? s01 : s23;
+        const float hv = (j & 1) ? h_hi_f(v) : h_lo_f(v);
+        lbv[j] = __fmul_rd(fmaxf(__fsub_rd(hv, c.wabs), 0.f), c.lbconv);
+        if (((pf >> j) & 1u) && lbv[j] <= thr) m |= 1u << j;
+      }
+      const int total = (int)__reduce_add_sync(0xffffffffu, (unsigned)__popc(m));
+      if (total == 0) continue;
+      if ((int)M.wn[warp] + total > kL1WB) lb1t_flush(T, warp, M.wn[warp], c, a);
+      if (total > kL1WB) {  // degenerate (e.g. tau = inf): straight to global memory
+        for (unsigned r = m; r; r &= r - 1) {
+          const int j = __ffs(r) - 1;
+          const unsigned pos = atomicAdd(&a.count[0], 1u);
+          if ((int64_t)pos < a.cap) {
+            a.cand[pos] = make_key(lbv[j], (uint32_t)(i0 + j));
+            atoms_add(l1_hist_addr(T, lb_bin(lbv[j], c.scale[0])), 1u);
+          }
+        }
+      } else {
+        for (unsigned r = m; r; r &= r - 1) {
+          const int j = __ffs(r) - 1;
+          const int pos = (int)atomicAdd(&M.wn[warp], 1u);
+          sts_u64(l1_key_addr(T, warp, pos), make_key(lbv[j], (uint32_t)(i0 + j)));
+        }
+      }
+      __syncwarp();
+    }
+    lb1t_flush(T, warp, M.wn[warp], c, a);
+  }
+  __syncthreads();
+  for (int i = tid; i < kNB; i += kL1Threads) {
+    const uint32_t v = lds_u32(l1_hist_addr(T, i));
+    if (v) atomicAdd(&a.hist[i], v);
+  }
 }
 
 // ---------------------------------------------------------------- f2: nb-ParIS+
@@ -3711,6 +3895,26 @@ cudaError_t launch_nb(const Plan& p, const float* raw, const uint8_t* sax, const
 
 cudaError_t launch_lb1(const Plan& p, const uint8_t* sax, const CardTables* tab, const Ws& ws, cudaStream_t st,
                        int64_t cap) {
+  static const bool old_form = getenv("PARIS_LB1_OLD") != nullptr;  // A/B: the register-prefetch k_lb1
+  if (!old_form) {
+    const int smemt = cached_per_device((const void*)k_lb1t, [](int dev) {
+      int optin = 0;
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+      cudaFuncAttributes fa;
+      if (cudaFuncGetAttributes(&fa, k_lb1t) != cudaSuccess) return 0;
+      const int v = optin - (int)fa.sharedSizeBytes;
+      if (cudaFuncSetAttribute(k_lb1t, cudaFuncAttributeMaxDynamicSharedMemorySize, v) != cudaSuccess) return 0;
+      return v;
+    });
+    if (smemt <= 0) return cudaErrorInvalidConfiguration;
+    LbArgs la;
+    la.sax = sax; la.n = p.n; la.w = p.w; la.seglen_f = (float)(p.len / p.w); la.tab = tab;
+    la.g_q = ws.g_q; la.g_q16 = ws.g_q16; la.nb = 1; la.thr = ws.thr_seed; la.count = ws.count;
+    la.hist = ws.hist; la.cand = ws.cand; la.cap = cap; la.perm = nullptr; la.env = nullptr;
+    la.blocks = ws.blocks;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms(), (p.n + kTS - 1) / kTS));
+    return PARIS_LAUNCH("lb_pass", k_lb1t, grid, kL1Threads, smemt, st, la);
+  }
   constexpr int SPT = PARIS_LB1_SPT;
   // dynamic shared memory: up to the 64 KB-aligned 64 KB table above the static arrays
   const int smem1 = cached_per_device((const void*)k_lb1<SPT>, [](int dev) {

@@ -161,6 +161,24 @@ def test_knn_host_buffers_and_batches(P, torch_dev):
         check_knn(x, q, gi, gd, ri, rd2)
 
 
+@pytest.mark.parametrize("n", [16, 2048, 2064, 9 * 2048 + 400, 150_000])
+def test_knn_batch1_tiled_pass(P, torch_dev, n):
+    """One query per SAX pass on the tiled layout (k_lb1t: TMA ring of 2048-series tiles,
+    ragged last tile): k = 1 and k = 9 against the oracle, member queries (LB = 0
+    candidates in the last tile) and a capacity small enough to overflow."""
+    import paper_2009_00166_b200 as p
+    x = datagen.random_walks(n, 256, 77 + n)
+    q = np.concatenate([datagen.random_walks(4, 256, 78 + n), x[[n - 1, n // 2]]])
+    for k in (1, 9):
+        kk = min(k, n)
+        ri, rd2 = oracle.knn_bruteforce(x, q, kk)
+        gi, gd = _knn_case(P, torch_dev, x, q, kk, config=p.KnnConfig(batch=1))
+        check_knn(x, q, gi, gd, ri, rd2)
+        if n >= 2048:
+            gi, gd = _knn_case(P, torch_dev, x, q, kk, config=p.KnnConfig(batch=1, seed_div=n, cap=64))
+            check_knn(x, q, gi, gd, ri, rd2)
+
+
 def test_knn_pruned_oracle_and_stats(P, torch_dev):
     """Larger n against the oracle's LB-pruned scan (itself pinned to brute force)."""
     torch, dev = torch_dev
