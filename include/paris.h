@@ -326,7 +326,8 @@ void paris_release_workspace(void);
 const char* paris_last_error(void);
 
 /* ABI version (major*100 + minor). */
-int32_t paris_version(void);  /* 107: paris_paa_f16, paris_knn_index_aux (PAA pre-filter);
+int32_t paris_version(void);  /* 108: paris_debug_set_variant (tuning A/B hook);
+                                 107: paris_paa_f16, paris_knn_index_aux (PAA pre-filter);
                                  106: asynchronous k-NN calls, device-side overflow, paris_release_workspace,
                                  paris_knn_approx / paris_knn_index_approx, paris_knn_config.tau_in */
 
@@ -343,6 +344,14 @@ int paris_debug_read_probe(const void* p, int64_t bytes, void* stream);
  * threads, each thread `iters` x 8 independent fma.rn.f16x2 (2 fp16 FMAs each); bench.py
  * times it for the batched LB's "alu" roofline denominator.  Asynchronous on `stream`. */
 int paris_debug_hfma2_probe(int32_t iters, int32_t blocks_per_sm, void* stream);
+
+/* Tuning hook (A/B of kernel variants inside one process; results are identical, only
+ * the speed differs): key 0 = consumer warps of the index LB pass (24 (default) or 30),
+ * key 1 = batch-1 flat LB (0: register-prefetch k_lb1,
+ * 1 (default): TMA ring k_lb1t), key 2 = pre-filtered k = 1 refine (0: k_refine1q, a warp per
+ * (query, chunk run); 1 (default): k_refine1m, one chunk stream over the batch).  Returns the previous value, -1 for an unknown key.
+ * Process-global; not synchronized with calls in flight on other host threads. */
+int32_t paris_debug_set_variant(int32_t key, int32_t value);
 
 /* Test hook: IEEE binary16 bits of v rounded toward -inf (dir < 0) or +inf
  * (dir > 0) -- the directed rounding behind the batched fp16 lower bound. */

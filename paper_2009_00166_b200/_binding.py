@@ -133,6 +133,8 @@ def load():
         lib.paris_debug_read_probe.restype = ctypes.c_int
         lib.paris_debug_hfma2_probe.argtypes = [i32, i32, P]
         lib.paris_debug_hfma2_probe.restype = ctypes.c_int
+        lib.paris_debug_set_variant.argtypes = [i32, i32]
+        lib.paris_debug_set_variant.restype = i32
         lib.paris_debug_half_dir.argtypes = [ctypes.c_double, i32]
         lib.paris_debug_half_dir.restype = ctypes.c_uint16
         _lib = lib
@@ -514,6 +516,11 @@ def debug_hfma2_probe(iters: int, blocks_per_sm: int = 4, stream=None) -> float:
     import torch as _t
     sms = _t.cuda.get_device_properties(_t.cuda.current_device()).multi_processor_count
     return float(sms) * blocks_per_sm * 512 * iters * 8 * 2
+
+
+def debug_set_variant(key: int, value: int) -> int:
+    """Tuning hook (paris_debug_set_variant): A/B of kernel variants, identical results."""
+    return int(load().paris_debug_set_variant(int(key), int(value)))
 
 
 def debug_half_dir(v: float, direction: int) -> int:

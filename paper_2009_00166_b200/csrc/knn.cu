@@ -1141,13 +1141,11 @@ __device__ __forceinline__ uint32_t half_of(uint32_t v, int h) { return (v >> (1
 //                                            two copies (bytes 0..63 for half-warp 0, 64..127
 //                                            for half-warp 1: 16-byte broadcast loads of two
 //                                            different slots never share a bank)
-//                            holes  64..159  per-warp candidate keys (kWBI per warp)
-//                            holes 160..223  coarse LB histograms (HC), a slot per hole
+//                            holes  64..183  per-warp candidate keys (kWBI per warp, NW <= 30)
+//                            holes 192..255  coarse LB histograms (HC), a slot per hole
 //   [T + 64K, ...)         ring stages 1 .. NST-1, then the 16-bit histograms (!HC)
 // One byte permute of a SAX word with {lane * 4, -, T bits 16..31} is a lookup's whole
 // shared address (the symbol lands in bits 8..15).
-constexpr int kIWarps = 24;                   // consumer warps
-constexpr int kIThreads = (kIWarps + 1) * 32; // + the producer warp
 #ifndef PARIS_LBI_GROUPS
 #define PARIS_LBI_GROUPS 2
 #endif
@@ -1155,8 +1153,14 @@ constexpr int kIThreads = (kIWarps + 1) * 32; // + the producer warp
 // every G-th tile and does ~G times the rounds per stage visit (the per-visit cost -- wait,
 // arrive, the final empty claim -- is paid half as often)
 constexpr int kIGroups = PARIS_LBI_GROUPS;
-constexpr int kIGroupWarps = kIWarps / kIGroups;
-static_assert(kIWarps % kIGroups == 0, "equal consumer groups");
+// one producer warp per consumer group (when the ring's stages split evenly over the
+// groups): a group's refills never wait behind another group's slow tile
+constexpr int kIProd = kIGroups;
+// NW consumer warps (a template parameter of k_lbi: 24 by default, 30 = 1024 threads at
+// <= 64 registers, paris_debug_set_variant key 0)
+template <int NW>
+constexpr int lbi_threads() { return (NW + kIProd) * 32; }
+constexpr int kIHistHole = 192;
 constexpr int kWBI = 64;                      // staged candidates per consumer warp
 constexpr uint32_t kIStageBytes = (uint32_t)kTileBytes;
 struct LbiWarp {
@@ -1166,19 +1170,22 @@ struct LbiWarp {
   unsigned pad[3];
 };
 constexpr int kMaxItems = kBPT * (kMaxB / 2);  // items of a tile: 32 blocks x up to 32 slot pairs
+template <int NW>
 struct LbiMisc {
   uint64_t full[4], empty[4];
   int64_t tile[4];
   unsigned next[4];    // per stage: the next unclaimed item pair
   unsigned nitems[4];  // per stage: items of its tile
   LbConsts c;
-  LbiWarp w[kIWarps];
+  LbiWarp w[NW];
   // per stage: the tile's items, decoded by the producer from the block masks:
   // block | slot a << 8 | slot b << 16 (0xFF: none)
   uint32_t items[4][kMaxItems];
 };
-constexpr size_t kIMiscBytes = (sizeof(LbiMisc) + 127) & ~(size_t)127;
-static_assert(kTileBytes + kIMiscBytes + 2048 <= 65536, "stage 0 + misc must fit below the table");
+template <int NW>
+constexpr size_t lbi_misc_bytes() { return (sizeof(LbiMisc<NW>) + 127) & ~(size_t)127; }
+static_assert(kTileBytes + lbi_misc_bytes<30>() + 2048 <= 65536, "stage 0 + misc must fit below the table");
+static_assert(64 + 4 * 30 <= kIHistHole, "key holes below the histogram holes");
 
 __device__ __forceinline__ uint32_t hole_addr(uint32_t T, int h) { return T + 256u * (uint32_t)h + 128u; }
 __device__ __forceinline__ uint32_t lbi_key_addr(uint32_t T, int warp, int e) {
@@ -1214,7 +1221,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // the packed 16-bit form at hist16 (hist16_add).
 template <bool HC>
 __device__ __forceinline__ void lbi_hist(uint32_t T, unsigned* hist16, int b, int bin, unsigned* g_hist) {
-  if (HC) atoms_add(hole_addr(T, 160 + b) + 4u * (uint32_t)(bin >> 3), 1u);
+  if (HC) atoms_add(hole_addr(T, kIHistHole + b) + 4u * (uint32_t)(bin >> 3), 1u);
   else hist16_add(hist16, b * kNB + bin, g_hist);
 }
 
@@ -1417,16 +1424,18 @@ k_blkmask(LbArgs a, unsigned long long* __restrict__ bmask, unsigned* __restrict
 // HC: coarse LB histograms (the k = 1 / k > 1 refine waves only need a quantile of
 // them) in the table's holes and a 4-stage ring; !HC (the opt-in bucket-sorted walk,
 // whose scatter needs exact bins): 16-bit 256-bin histograms and 3 stages.
-template <int P, bool HC>
-__global__ void __launch_bounds__(kIThreads, 1)
+template <int P, bool HC, int NW>
+__global__ void __launch_bounds__(lbi_threads<NW>(), 1)
 k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __restrict__ tile_list,
       const unsigned* __restrict__ tile_count) {
   constexpr int NST = HC ? 4 : 3;
   extern __shared__ __align__(128) uint8_t dsm[];
   const uint32_t S0 = smem_u32(dsm);
-  const uint32_t T = (S0 + (uint32_t)(kTileBytes + kIMiscBytes) + 0xFFFFu) & ~0xFFFFu;  // the table
+  constexpr int kIWarps = NW, kIGroupWarps = NW / kIGroups, kIThreads = lbi_threads<NW>();
+  static_assert(NW % kIGroups == 0, "equal consumer groups");
+  const uint32_t T = (S0 + (uint32_t)(kTileBytes + lbi_misc_bytes<NW>()) + 0xFFFFu) & ~0xFFFFu;  // the table
   uint8_t* const gbase = dsm - S0;  // generic pointer of shared address x: gbase + x
-  LbiMisc& M = *reinterpret_cast<LbiMisc*>(dsm + kTileBytes);
+  LbiMisc<NW>& M = *reinterpret_cast<LbiMisc<NW>*>(dsm + kTileBytes);
   unsigned* hist16 = reinterpret_cast<unsigned*>(gbase + T + 65536u + (uint32_t)(NST - 1) * kIStageBytes);
   auto stage_addr = [&](int st) -> uint32_t {
     return st == 0 ? S0 : T + 65536u + (uint32_t)(st - 1) * kIStageBytes;
@@ -1459,7 +1468,7 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
     sts_u32(hole_addr(T, b) + 64u + 4u * (uint32_t)sg, qw);
   }
   if (HC) {
-    for (int i = tid; i < nslots * kNBC; i += kIThreads) sts_u32(hole_addr(T, 160 + i / kNBC) + 4u * (uint32_t)(i % kNBC), 0u);
+    for (int i = tid; i < nslots * kNBC; i += kIThreads) sts_u32(hole_addr(T, kIHistHole + i / kNBC) + 4u * (uint32_t)(i % kNBC), 0u);
   } else {
     for (int i = tid; i < nslots * kNB / 2; i += kIThreads) hist16[i] = 0;
   }
@@ -1469,24 +1478,29 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
   }
   lb_consts_init(a, nslots, &M.c);  // ends with __syncthreads
 
-  if (warp == kIWarps) {
-    // ---- producer: refill stage st as soon as every consumer warp released it.  The
-    // whole warp decodes the tile's 32 block masks (lane = block; read from global one tile
-    // ahead) into the stage's item list -- a block's live query slots paired in order,
-    // consecutive live slots forming an item -- so the consumers claim ready items.
-    int64_t li = blockIdx.x;
+  if (warp >= kIWarps) {
+    // ---- producers: refill stage st as soon as every consumer warp of its group released
+    // it.  The whole warp decodes the tile's 32 block masks (lane = block; read from global
+    // one tile ahead) into the stage's item list -- a block's live query slots paired in
+    // order, consecutive live slots forming an item -- so the consumers claim ready items.
+    // With NST % groups == 0 producer p serves group p's stages (tiles it = p, p + NP, ..).
+    constexpr int NP = (NST % kIGroups == 0) ? kIGroups : 1;
+    const int pi = warp - kIWarps;
+    if (pi >= NP) goto lbi_done;
+    int64_t li = blockIdx.x + (int64_t)pi * gridDim.x;
+    const int64_t lstep = (int64_t)NP * gridDim.x;
     unsigned tnext = 0;
     uint64_t bnext = 0;
     if (li < nlist) {
       tnext = __ldg(tile_list + li);
       bnext = __ldg(bmask + (size_t)tnext * kBPT + lane);
     }
-    for (int64_t it = 0; li < nlist; ++it, li += gridDim.x) {
+    for (int64_t it = pi; li < nlist; it += NP, li += lstep) {
       const int st = (int)(it % NST);
       const unsigned tile = tnext;
       uint64_t m = bnext;
-      if (li + gridDim.x < nlist) {  // the next tile's id and masks, early
-        tnext = __ldg(tile_list + li + gridDim.x);
+      if (li + lstep < nlist) {  // the next tile's id and masks, early
+        tnext = __ldg(tile_list + li + lstep);
         bnext = __ldg(bmask + (size_t)tnext * kBPT + lane);
       }
       if (it >= NST) mbar_wait(&M.empty[st], (unsigned)(((it / NST) - 1) & 1));
@@ -1597,10 +1611,11 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
     }
     lbi_flush<HC>(wb, T, warp, nslots, c, a, hist16);
   }
+lbi_done:
   __syncthreads();
   if (HC) {
     for (int i = tid; i < nslots * kNBC; i += kIThreads) {
-      const uint32_t v = lds_u32(hole_addr(T, 160 + i / kNBC) + 4u * (uint32_t)(i % kNBC));
+      const uint32_t v = lds_u32(hole_addr(T, kIHistHole + i / kNBC) + 4u * (uint32_t)(i % kNBC));
       if (v) atomicAdd(&a.hist[(i / kNBC) * kNB + (i % kNBC) * 8 + 7], v);
     }
   } else {
@@ -2924,6 +2939,307 @@ k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     atomicAdd(&a.paa_rows[threadIdx.x], s_paa[threadIdx.x]);
 }
 
+// k = 1 index-path refine with the PAA pre-filter (and the bf16 one if R16) over ONE
+// stream of candidate chunks: the batch's unsorted lists concatenated (chunk c of query b
+// at s_off[b] + c), warp w takes chunks w, w + GW, ... -- every query's chunks spread over
+// all warps (balanced per query, as the rotated interleave of k_refine1q), but a warp never
+// restarts per query: the per-query constants (PAA of q, ||q||, ||PAA(q)||, wave cut, bin
+// scale) sit in shared memory for the whole batch, queued keys carry their query, and the
+// queue is drained only when full (k_refine1q paid a setup, a key-prefetch miss and a
+// partial drain -- three dependent memory round trips -- per (warp, query) with ~1.3
+// chunks each at C4).  Same tests in the same arithmetic: LB <= BSF, the PAA
+// bound, the bf16 bound, exact fp32 distance with early abandoning; only the order in
+// which candidates are refined differs (the result is the unique minimum (d^2, id) key).
+#ifndef PARIS_REFM_CTAS
+#define PARIS_REFM_CTAS 3
+#endif
+constexpr int kRefMCtas = PARIS_REFM_CTAS;
+#ifndef PARIS_REFM_KP
+#define PARIS_REFM_KP 1
+#endif
+constexpr int kRefMKP = PARIS_REFM_KP;  // chunks of keys in flight per warp
+#ifndef PARIS_REFM_H
+#define PARIS_REFM_H 2
+#endif
+constexpr int kRefMH = PARIS_REFM_H;    // bf16 stage: 16-byte pieces per candidate in flight
+template <int NC, int U, int W2, bool R16>
+__global__ void __launch_bounds__(kRefThreads, kRefMCtas)
+k_refine1m(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
+  static_assert(W2 == 32 || W2 == 64, "PAA pre-filter widths");
+  constexpr int EPL = W2 / 8;  // fp16 PAA values per lane of a row (an octet per row)
+  __shared__ unsigned s_off[kMaxB + 1];
+  __shared__ unsigned s_cnt[kMaxB], s_cut[kMaxB], s_refined[kMaxB], s_r16[kMaxB], s_paa[kMaxB];
+  __shared__ float s_scale[kMaxB], s_qn[kMaxB], s_qpn[kMaxB];
+  __shared__ __align__(16) float s_qp[kMaxB * W2];
+  __shared__ uint64_t s_queue[kRefWarps][64];
+  __shared__ uint8_t s_qb[kRefWarps][64];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int oct = lane >> 3, sub = lane & 7;
+  if (tid < kMaxB) {
+    const bool on = tid < nb;
+    s_refined[tid] = 0;
+    s_r16[tid] = 0;
+    s_paa[tid] = 0;
+    s_cnt[tid] = on ? (unsigned)imin64((int64_t)a.count[tid], a.cap) : 0u;
+    s_cut[tid] = on ? cut[tid * kNB] : 0u;
+    s_scale[tid] = on ? bin_scale(__uint_as_float(a.thr_seed[tid])) : 0.f;
+    s_qn[tid] = on ? a.qaux[tid * kQAux] : 0.f;
+    s_qpn[tid] = on ? a.qaux[tid * kQAux + 1] : 0.f;
+  }
+  for (int i = tid; i < nb * W2; i += kRefThreads) s_qp[i] = a.qaux[(i / W2) * kQAux + 16 + i % W2];
+  __syncthreads();
+  if (warp == 0) {  // chunk offsets: an exclusive scan of ceil(cnt / 32) over the queries
+    unsigned run = 0;
+    for (int b0 = 0; b0 < nb; b0 += 32) {
+      const int b = b0 + lane;
+      const unsigned c = b < nb ? (s_cnt[b] + 31u) / 32u : 0u;
+      unsigned incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      if (b < nb) s_off[b] = run + incl - c;
+      run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) s_off[nb] = run;
+  }
+  __syncthreads();
+  const unsigned TC = s_off[nb];
+  const unsigned gw = blockIdx.x * kRefWarps + warp, GW = gridDim.x * kRefWarps;
+  const int nh = a.len >> 3;       // uint4 (8 bf16) per row
+  const int nper = (nh + 7) >> 3;  // uint4 per lane of an octet
+  const float e2 = 2.f * (float)((a.len >> 4) + 8) * 5.9604644775390625e-08f;  // octet sums (bf16)
+  const float e2p = 2.f * (float)(EPL + 8) * 5.9604644775390625e-08f;          // octet sums (PAA)
+  constexpr float rho16 = 4.8875808715820312e-04f;  // 2^-11 (1 + 2^-10), rounded up
+  constexpr float one_m_rho16 = 0.99951171875f;     // 1 - 2^-11 (1 + 2^-10), rounded down
+  const float slack = __fmul_ru(sqrtf((float)W2) * 1.0001f, 5.9604644775390625e-08f);  // sqrt(W2) 2^-24
+  const float scale2 = __fdiv_rd((float)a.len, (float)W2);
+  uint64_t* queue = s_queue[warp];
+  uint8_t* qb = s_qb[warp];
+  auto thr_of = [&](uint64_t bsf) { return bsf == kNoKey ? INFINITY : __fmul_ru(key_val(bsf), a.d2up); };
+  // the query owning chunk gc: the last b with s_off[b] <= gc (empty queries share offsets)
+  auto chunk_query = [&](unsigned gc) -> int {
+    int lo = 0, hi = nb;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_off[mid] <= gc) lo = mid; else hi = mid;
+    }
+    return lo;
+  };
+  // exact fp32 distance of one queued survivor (warp-cooperative, early abandoning)
+  auto refine_one = [&](uint64_t key, int b) {
+    uint64_t ks[1] = {key};
+    const uint64_t bsf = ld_relaxed_u64(a.best + (size_t)b * kPadU64);
+    bool lv[1] = {key_val(key) <= thr_of(bsf)};
+    if (!lv[0]) return;
+    uint64_t cur = bsf;
+    unsigned nr = 0;
+    refine_group<NC, 1>(a, reinterpret_cast<const float4*>(a.queries + (size_t)b * a.len), ks, lv, thr_of(bsf), cur,
+                        a.best + (size_t)b * kPadU64, nr);
+    if (lane == 0 && nr) atomicAdd(&s_refined[b], nr);
+  };
+  // the queued entries [0, m): the PAA stage (octet o: entries o + 4i, i < 8, in two halves of
+  // four rows in flight), survivors compacted to the front; then bf16 (R16) and exact fp32
+  auto drain = [&](int m) {
+    uint64_t key[8];
+    int kb[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int e = oct + 4 * i;
+      key[i] = e < m ? queue[e] : kNoKey;
+      kb[i] = e < m ? (int)qb[e] : 0;
+    }
+    __syncwarp();
+    int nout = 0;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      bool keep[4];
+      float thr[4];
+      uint32_t pw[4][EPL / 2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int e = oct + 4 * (4 * half + i);
+        const uint64_t kk = key[4 * half + i];
+        const int b = kb[4 * half + i];
+        thr[i] = e < m ? thr_of(ld_relaxed_u64(a.best + (size_t)b * kPadU64)) : 0.f;
+        const __half* row = a.paa16 + (size_t)key_id(kk) * W2 + sub * EPL;
+        keep[i] = e < m;
+        if (EPL == 8) {
+          const uint4 v = keep[i] ? ld_stream_u4(reinterpret_cast<const uint4*>(row)) : make_uint4(0u, 0u, 0u, 0u);
+          pw[i][0] = v.x; pw[i][EPL / 2 > 1 ? 1 : 0] = v.y; pw[i][EPL / 2 > 2 ? 2 : 0] = v.z; pw[i][EPL / 2 > 3 ? 3 : 0] = v.w;
+        } else {
+          uint2 v = make_uint2(0u, 0u);
+          if (keep[i]) v = __ldcs(reinterpret_cast<const uint2*>(row));
+          pw[i][0] = v.x; pw[i][EPL / 2 > 1 ? 1 : 0] = v.y;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int b = kb[4 * half + i];
+        if (sub == 0 && keep[i]) atomicAdd(&s_paa[b], 1u);  // rows read
+        keep[i] = keep[i] && key_val(key[4 * half + i]) <= thr[i];
+        const float4* qp4 = reinterpret_cast<const float4*>(s_qp + b * W2 + sub * EPL);
+        float acc = 0.f;
+#pragma unroll
+        for (int e4 = 0; e4 < EPL / 4; ++e4) {
+          const float4 q = qp4[e4];
+          const float qq[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+          for (int e1 = 0; e1 < 4; ++e1) {
+            const int e = 4 * e4 + e1;
+            const uint32_t w = pw[i][e >> 1];
+            const float x = __half2float(__ushort_as_half((unsigned short)((e & 1) ? (w >> 16) : (w & 0xFFFFu))));
+            const float d = x - qq[e1];
+            acc = fmaf(d, d, acc);
+          }
+        }
+        acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        const float qterm = __fmul_ru(rho16 + 1.1920928955078125e-07f, s_qpn[b]);  // (rho16 + 2^-23) ||q_p||
+        const float D = __fsqrt_rd(__fmul_rd(acc, 1.f - e2p));
+        const float Dp = __fsub_rd(__fsub_rd(__fmul_rd(one_m_rho16, D), qterm), slack);
+        const float lb2 = Dp > 0.f ? __fmul_rd(scale2, __fmul_rd(Dp, Dp)) : 0.f;
+        const bool kp = keep[i] && !(lb2 > thr[i]);  // NaN (a PAA beyond fp16): no pruning
+        const unsigned mk = __ballot_sync(0xffffffffu, sub == 0 && kp);
+        if (sub == 0 && kp) {
+          const int at = nout + __popc(mk & ((1u << lane) - 1u));
+          queue[at] = key[4 * half + i];
+          qb[at] = (uint8_t)b;
+        }
+        nout += __popc(mk);
+      }
+    }
+    __syncwarp();
+    if (!R16) {
+      for (int e = 0; e < nout; ++e) refine_one(queue[e], qb[e]);
+      __syncwarp();
+      return;
+    }
+    // bf16 stage over the PAA survivors: octet o takes entries r0 + o and r0 + 4 + o
+    for (int r0 = 0; r0 < nout; r0 += 8) {
+      uint64_t kc[2];
+      int bc[2];
+      bool live[2];
+      float thr[2];
+      const uint4* row[2];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int e = r0 + 4 * c + oct;
+        kc[c] = e < nout ? queue[e] : kNoKey;
+        bc[c] = e < nout ? (int)qb[e] : 0;
+        thr[c] = e < nout ? thr_of(ld_relaxed_u64(a.best + (size_t)bc[c] * kPadU64)) : 0.f;
+        live[c] = e < nout;
+        row[c] = reinterpret_cast<const uint4*>(a.raw16 + (size_t)key_id(kc[c]) * a.len);
+      }
+      float s2[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+      for (int i0 = 0; i0 < nper; i0 += kRefMH) {  // kRefMH uint4 per candidate in flight (registers)
+        uint4 h[2][kRefMH];
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int i = 0; i < kRefMH; ++i) {
+            const int f = sub + 8 * (i0 + i);
+            h[c][i] = (live[c] && i0 + i < nper && f < nh) ? ld_stream_u4(row[c] + f) : make_uint4(0u, 0u, 0u, 0u);
+          }
+#pragma unroll
+        for (int i = 0; i < kRefMH; ++i) {
+          const int f = sub + 8 * (i0 + i);
+          if (i0 + i >= nper || f >= nh) break;
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const float4* qv = reinterpret_cast<const float4*>(a.queries + (size_t)bc[c] * a.len);
+            const float4 q0 = __ldg(qv + 2 * f), q1 = __ldg(qv + 2 * f + 1);  // L1-resident queries
+            const float qq[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+            const uint32_t w4[4] = {h[c][i].x, h[c][i].y, h[c][i].z, h[c][i].w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float d = __uint_as_float((e & 1) ? (w4[e >> 1] & 0xFFFF0000u) : (w4[e >> 1] << 16)) - qq[e];
+              s2[c][e & 1] = fmaf(d, d, s2[c][e & 1]);
+            }
+          }
+        }
+      }
+      bool keep[2];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        live[c] = live[c] && key_val(kc[c]) <= thr[c];
+        if (sub == 0 && live[c]) atomicAdd(&s_r16[bc[c]], 1u);
+        float v = s2[c][0] + s2[c][1];
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        const float lb = bf16_lb(v, s_qn[bc[c]], e2);
+        keep[c] = live[c] && !(lb > 0.f && __fmul_rd(lb, lb) > thr[c]);
+      }
+      // survivors (octet leaders' bits): exact fp32 distance, one row at a time
+      unsigned m2 = __ballot_sync(0xffffffffu, sub == 0 && keep[0]);
+      unsigned m3 = __ballot_sync(0xffffffffu, sub == 0 && keep[1]);
+      while (m2 | m3) {
+        const bool from2 = m2 != 0u;
+        const int src = __ffs(from2 ? m2 : m3) - 1;
+        if (from2) m2 &= m2 - 1; else m3 &= m3 - 1;
+        const uint64_t k = __shfl_sync(0xffffffffu, from2 ? kc[0] : kc[1], src);
+        const int b = __shfl_sync(0xffffffffu, from2 ? bc[0] : bc[1], src);
+        refine_one(k, b);
+      }
+    }
+    __syncwarp();
+  };
+
+  int qn = 0;
+  // the chunk stream: the keys of the next kRefMKP chunks in flight (a register ring of
+  // (query, key)), the query's BSF word read one chunk ahead
+  auto fetch = [&](unsigned gc, int& b, uint64_t& k) {
+    if (gc >= TC) { b = 0; k = kNoKey; return; }
+    b = chunk_query(gc);
+    const unsigned i = (gc - s_off[b]) * 32u + lane;
+    k = i < s_cnt[b] ? __ldg(a.sorted + (size_t)b * a.cap + i) : kNoKey;
+  };
+  int rb[kRefMKP];
+  uint64_t rk[kRefMKP];
+#pragma unroll
+  for (int r = 0; r < kRefMKP; ++r) fetch(gw + (unsigned)r * GW, rb[r], rk[r]);
+  uint64_t bsfn = ld_relaxed_u64(a.best + (size_t)rb[0] * kPadU64);
+  for (unsigned gc = gw; gc < TC; gc += GW) {
+    const int b = rb[0];
+    const uint64_t k0 = rk[0], bsf = bsfn;
+#pragma unroll
+    for (int r = 0; r + 1 < kRefMKP; ++r) { rb[r] = rb[r + 1]; rk[r] = rk[r + 1]; }
+    fetch(gc + (unsigned)kRefMKP * GW, rb[kRefMKP - 1], rk[kRefMKP - 1]);
+    bsfn = ld_relaxed_u64(a.best + (size_t)rb[0] * kPadU64);
+    const float thr = thr_of(bsf);
+    const float lb0 = key_val(k0);
+    const int bin = lb_bin(lb0, s_scale[b]);
+    const int cutb = (int)s_cut[b];
+    const bool pass = k0 != kNoKey && (wave == 0 ? bin <= cutb : bin > cutb) && lb0 <= thr;
+    const unsigned m = __ballot_sync(0xffffffffu, pass);
+    if (pass) {
+      const int at = qn + __popc(m & ((1u << lane) - 1u));
+      queue[at] = k0;
+      qb[at] = (uint8_t)b;
+    }
+    qn += __popc(m);
+    __syncwarp();
+    if (qn >= 32) {
+      drain(32);
+      __syncwarp();
+      if (lane < qn - 32) {
+        queue[lane] = queue[32 + lane];  // the rest to the front
+        qb[lane] = qb[32 + lane];
+      }
+      qn -= 32;
+      __syncwarp();
+    }
+  }
+  if (qn > 0) drain(qn);
+  __syncthreads();
+  if (tid < nb && s_refined[tid]) atomicAdd(&a.refined[tid], s_refined[tid]);
+  if (R16 && tid < nb && s_r16[tid]) atomicAdd(&a.refined16[tid], s_r16[tid]);
+  if (tid < nb && s_paa[tid] && a.paa_rows) atomicAdd(&a.paa_rows[tid], s_paa[tid]);
+}
+
 // ---------------------------------------------------------------- K6, k > 1 (append, then select)
 // The query-wide threshold from the refined-distance histogram: at least k distinct
 // refined series have fp32 d^2 < (t + 2) / scale for the first bin t where the count
@@ -3819,26 +4135,32 @@ cudaError_t launch_lbt(const Plan& p, const uint8_t* sax, int nb, const CardTabl
                       ws.seed_ids, p.S);
 }
 
-// dynamic shared memory of k_lbi<P, HC>: everything the device allows a CTA beyond the
+// dynamic shared memory of k_lbi<P, HC, S1>: everything the device allows a CTA beyond the
 // kernel's static shared memory (the kernel checks its layout fits)
-template <int P, bool HC>
+template <int P, bool HC, int NW>
 int lbi_smem() {
-  return cached_per_device((const void*)k_lbi<P, HC>, [](int dev) {
+  return cached_per_device((const void*)k_lbi<P, HC, NW>, [](int dev) {
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, k_lbi<P, HC>) != cudaSuccess) return 0;
+    if (cudaFuncGetAttributes(&fa, k_lbi<P, HC, NW>) != cudaSuccess) return 0;
     const int v = optin - (int)fa.sharedSizeBytes;
-    if (cudaFuncSetAttribute(k_lbi<P, HC>, cudaFuncAttributeMaxDynamicSharedMemorySize, v) != cudaSuccess) return 0;
+    if (cudaFuncSetAttribute(k_lbi<P, HC, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, v) != cudaSuccess) return 0;
     return v;
   });
+}
+
+template <int P, bool HC, int NW>
+cudaError_t launch_lbi_pass(int grid, cudaStream_t st, const LbArgs& la, const Ws& ws) {
+  const int smem = lbi_smem<P, HC, NW>();
+  if (smem <= 0) return cudaErrorInvalidConfiguration;
+  return PARIS_LAUNCH("lb_pass", (k_lbi<P, HC, NW>), grid, lbi_threads<NW>(), smem, st, la, ws.bmask,
+                      ws.tile_list, ws.tile_count);
 }
 
 template <int P>
 cudaError_t launch_index_lb(const Plan& p, const uint8_t* sax, int nb, const CardTables* tab, const Ws& ws,
                             cudaStream_t st, int64_t cap) {
-  const int smem = p.sorted_refine ? lbi_smem<P, false>() : lbi_smem<P, true>();
-  if (smem <= 0) return cudaErrorInvalidConfiguration;
   LbArgs la;
   la.sax = sax; la.n = p.n; la.w = p.w; la.seglen_f = (float)(p.len / p.w); la.tab = tab;
   la.g_q = ws.g_q; la.g_q16 = ws.g_q16; la.nb = nb; la.thr = ws.thr_seed; la.count = ws.count;
@@ -3850,11 +4172,10 @@ cudaError_t launch_index_lb(const Plan& p, const uint8_t* sax, int nb, const Car
                                ws.tile_count, ws.blocks);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(sms(), ntiles);
+  const bool w30 = g_variant[0] == 30;  // tuning: 30 consumer warps (1024 threads) instead of 24
   if (!p.sorted_refine)  // coarse histograms suffice for the wave cut (no bucket sort): 4 ring stages
-    return PARIS_LAUNCH("lb_pass", (k_lbi<P, true>), grid, kIThreads, smem, st, la, ws.bmask, ws.tile_list,
-                        ws.tile_count);
-  return PARIS_LAUNCH("lb_pass", (k_lbi<P, false>), grid, kIThreads, smem, st, la, ws.bmask, ws.tile_list,
-                      ws.tile_count);
+    return w30 ? launch_lbi_pass<P, true, 30>(grid, st, la, ws) : launch_lbi_pass<P, true, 24>(grid, st, la, ws);
+  return w30 ? launch_lbi_pass<P, false, 30>(grid, st, la, ws) : launch_lbi_pass<P, false, 24>(grid, st, la, ws);
 }
 
 cudaError_t dispatch_index_lb(int nb, const Plan& p, const uint8_t* sax, const CardTables* tab, const Ws& ws,
@@ -3895,7 +4216,7 @@ cudaError_t launch_nb(const Plan& p, const float* raw, const uint8_t* sax, const
 
 cudaError_t launch_lb1(const Plan& p, const uint8_t* sax, const CardTables* tab, const Ws& ws, cudaStream_t st,
                        int64_t cap) {
-  static const bool old_form = getenv("PARIS_LB1_OLD") != nullptr;  // A/B: the register-prefetch k_lb1
+  const bool old_form = g_variant[1] == 0;  // A/B: the register-prefetch k_lb1
   if (!old_form) {
     const int smemt = cached_per_device((const void*)k_lb1t, [](int dev) {
       int optin = 0;
@@ -3973,19 +4294,36 @@ cudaError_t launch_refine1(const RefineArgs& ra, int nb, int64_t max_work, cudaS
   return PARIS_LAUNCH("refine", (k_refine1<NC, U>), grid, kRefThreads, 0, st, ra, nb);
 }
 
+// the octet-form refine (k_refine1q) when a pre-filter copy is given; cudaErrorNotSupported
+// otherwise (the caller falls back to k_refine1u)
+template <int NC, int U>
+cudaError_t launch_refine1q(const RefineArgs& ra, int nb, int wave, const unsigned* cut, cudaStream_t st, int grid) {
+  if (ra.paa16) {  // the PAA pre-filter (then the bf16 one, if given)
+    if (ra.w2 == 32)
+      return ra.raw16 ? PARIS_LAUNCH("refine", (k_refine1q<NC, U, 32, true>), grid, kRefThreads, 0, st, ra, nb, wave, cut)
+                      : PARIS_LAUNCH("refine", (k_refine1q<NC, U, 32, false>), grid, kRefThreads, 0, st, ra, nb, wave, cut);
+    return ra.raw16 ? PARIS_LAUNCH("refine", (k_refine1q<NC, U, 64, true>), grid, kRefThreads, 0, st, ra, nb, wave, cut)
+                    : PARIS_LAUNCH("refine", (k_refine1q<NC, U, 64, false>), grid, kRefThreads, 0, st, ra, nb, wave, cut);
+  }
+  if (ra.raw16 && !getenv("PARIS_REF16_WARP"))  // octets per candidate (env: A/B of the warp form)
+    return PARIS_LAUNCH("refine", (k_refine1q<NC, U, 0, true>), grid, kRefThreads, 0, st, ra, nb, wave, cut);
+  return cudaErrorNotSupported;
+}
+
 template <int NC, int U>
 cudaError_t launch_refine1u(const RefineArgs& ra, int nb, int wave, const unsigned* cut, cudaStream_t st) {
   if constexpr (NC <= 2) {
-    const int grid = sms() * kRefQCtas;
-    if (ra.paa16) {  // the PAA pre-filter (then the bf16 one, if given)
+    if (ra.paa16 && g_variant[2] == 1) {  // one chunk stream over the batch (k_refine1m)
+      const int gridm = sms() * kRefMCtas;
       if (ra.w2 == 32)
-        return ra.raw16 ? PARIS_LAUNCH("refine", (k_refine1q<NC, U, 32, true>), grid, kRefThreads, 0, st, ra, nb, wave, cut)
-                        : PARIS_LAUNCH("refine", (k_refine1q<NC, U, 32, false>), grid, kRefThreads, 0, st, ra, nb, wave, cut);
-      return ra.raw16 ? PARIS_LAUNCH("refine", (k_refine1q<NC, U, 64, true>), grid, kRefThreads, 0, st, ra, nb, wave, cut)
-                      : PARIS_LAUNCH("refine", (k_refine1q<NC, U, 64, false>), grid, kRefThreads, 0, st, ra, nb, wave, cut);
+        return ra.raw16 ? PARIS_LAUNCH("refine", (k_refine1m<NC, U, 32, true>), gridm, kRefThreads, 0, st, ra, nb, wave, cut)
+                        : PARIS_LAUNCH("refine", (k_refine1m<NC, U, 32, false>), gridm, kRefThreads, 0, st, ra, nb, wave, cut);
+      return ra.raw16 ? PARIS_LAUNCH("refine", (k_refine1m<NC, U, 64, true>), gridm, kRefThreads, 0, st, ra, nb, wave, cut)
+                      : PARIS_LAUNCH("refine", (k_refine1m<NC, U, 64, false>), gridm, kRefThreads, 0, st, ra, nb, wave, cut);
     }
-    if (ra.raw16 && !getenv("PARIS_REF16_WARP"))  // octets per candidate (env: A/B of the warp form)
-      return PARIS_LAUNCH("refine", (k_refine1q<NC, U, 0, true>), grid, kRefThreads, 0, st, ra, nb, wave, cut);
+    const int grid = sms() * kRefQCtas;
+    const cudaError_t e = launch_refine1q<NC, U>(ra, nb, wave, cut, st, grid);
+    if (e != cudaErrorNotSupported) return e;
   }
   if (ra.raw16) {
     const int grid = sms() * (NC <= 2 ? kRefU16Ctas : 2);

@@ -77,6 +77,8 @@ void retain_pool();
 
 // SM count of the current device (cached per device; thread-safe).
 int device_sms();
+// tuning variants (paris_debug_set_variant): [0] index LB item form, [1] batch-1 LB kernel
+extern int g_variant[4];
 
 // Per-(key, device) one-time setup -- e.g. cudaFuncSetAttribute of a kernel -- run under
 // a lock, so a concurrent first caller waits until it is done; cached only on success.

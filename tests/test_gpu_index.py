@@ -288,3 +288,37 @@ def test_knn_index_paa_prefilter_k(P, k, w2, length):
     ri, rd2 = oracle.knn_bruteforce(x, q, k)
     check_knn(x, q, gi.cpu().numpy(), gd.cpu().numpy(), ri, rd2)
     assert st["paa_rows"].sum() > 0 and st["refined"].sum() < st0["refined"].sum()
+
+
+@pytest.mark.parametrize("key,values", [(0, (24, 30)), (1, (0, 1)), (2, (0, 1))])
+def test_kernel_variants_identical(P, key, values):
+    """Tuning variants (paris_debug_set_variant): the index LB pass at 24 and 30 consumer warps,
+    the batch-1 flat LB as k_lb1 / k_lb1t, and the pre-filtered refine with and without its
+    loads pipelined, return identical rows, equal to the oracle's."""
+    import torch
+    n = 70_000
+    x = datagen.random_walks(n, 256, 610)
+    q = datagen.random_walks(40, 256, 611)
+    q[3] = x[n - 5]
+    xd = torch.from_numpy(x).cuda()
+    qd = torch.from_numpy(q).cuda()
+    sax = P.summarize(xd, 16, 256)
+    idx = P.index_build(sax, 16, 256) if key != 1 else None
+    r16, p16 = (P.raw_bf16(xd), P.paa_f16(xd, 64)) if key == 2 else (None, None)
+    ri, rd2 = oracle.knn_bruteforce(x, q, 1 if key == 2 else 4)
+    outs = []
+    old = P.debug_set_variant(key, values[0])
+    try:
+        for v in values:
+            P.debug_set_variant(key, v)
+            if key == 0:
+                gi, gd = P.knn_index(xd, idx, qd, k=4)
+            elif key == 2:
+                gi, gd = P.knn_index(xd, idx, qd, k=1, raw16=r16, paa16=p16)
+            else:
+                gi, gd = P.knn_exact(xd, sax, qd, k=4, config=P.KnnConfig(batch=1))
+            check_knn(x, q, gi.cpu().numpy(), gd.cpu().numpy(), ri, rd2)
+            outs.append((gi.cpu(), gd.cpu()))
+    finally:
+        P.debug_set_variant(key, old)
+    assert all(torch.equal(o[0], outs[0][0]) and torch.equal(o[1], outs[0][1]) for o in outs)
