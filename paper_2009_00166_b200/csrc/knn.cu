@@ -1601,6 +1601,16 @@ k_lbi(LbArgs a, const unsigned long long* __restrict__ bmask, const unsigned* __
           asm("add.rn.f16x2 %0, %1, %2;" : "=r"(sum) : "r"(above), "r"(below));
           acc[j] = sum;
         }
+        // fast test: the packed minimum of the four series' (LB16 sa, LB16 sb) against the
+        // item's thresholds (a missing sb or an inactive half-warp never passes); almost every
+        // item stops here.  Series past n (last tile) may pass it: lbi_emit masks them.
+        {
+          const uint32_t Tp = active ? (half_of(c.T16[sa >> 1], sa & 1) |
+                                        ((sb >= 0 ? half_of(c.T16[sb >> 1], sb & 1) : (uint32_t)kHalfNeg1) << 16))
+                                     : (kHalfNeg1 | (kHalfNeg1 << 16));
+          const uint32_t mn = h2_min(h2_min(acc[0], acc[1]), h2_min(acc[2], acc[3]));
+          if (!__any_sync(0xffffffffu, h2_le_bits(mn, Tp) != 0u)) continue;
+        }
         const int64_t i0 = tile * kTS + k * PARIS_INDEX_BLOCK + 4 * hl;
         const int nvalid = active ? (int)std::max<int64_t>(0, imin64(4, a.n - i0)) : 0;
         PARIS_DCHECK(k < kBPT && sa >= 0 && sa < nslots && sb < nslots);
@@ -2955,7 +2965,7 @@ k_refine1q(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
 #endif
 constexpr int kRefMCtas = PARIS_REFM_CTAS;
 #ifndef PARIS_REFM_KP
-#define PARIS_REFM_KP 1
+#define PARIS_REFM_KP 2
 #endif
 constexpr int kRefMKP = PARIS_REFM_KP;  // chunks of keys in flight per warp
 #ifndef PARIS_REFM_H
