@@ -71,28 +71,55 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms while running."""
+    """SM clocks + throttle reasons sampled while running: in-process NVML (nvidia_ml_py) every
+    20 ms -- the first sample at entry -- so even a short timed region is covered and no
+    nvidia-smi process (whose NVML start-up stalled the GPU for 10-70 ms under the timed
+    region of the many-call C3 step) runs beside it; nvidia-smi every 200 ms only when NVML
+    is unavailable."""
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
         self.rows = []
         self._stop = threading.Event()
+        self._nvml = None
+        try:
+            if os.environ.get("BENCH_CLOCKS") == "smi":
+                raise RuntimeError("nvidia-smi sampling requested")
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            bits = [getattr(pynvml, "nvmlClocksThrottleReason" + n) for n in
+                    ("HwSlowdown", "HwThermalSlowdown", "SwThermalSlowdown", "SwPowerCap")]
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self._nvml = (pynvml, h, bits, mx)
+        except Exception:
+            self._nvml = None
         self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _sample_nvml(self):
+        pynvml, h, bits, mx = self._nvml
+        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+        r = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        self.rows.append([str(sm), str(mx), ""] + ["Active" if (r & b) else "Not Active" for b in bits])
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([c.strip() for c in out.split(",")])
+                if self._nvml:
+                    self._sample_nvml()
+                else:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([c.strip() for c in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.02 if self._nvml else 0.2)
 
     def __enter__(self):
         self._t.start()
@@ -104,14 +131,14 @@ class ClockSampler:
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"], "samples": 0}
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
+        reasons = sorted({self.NAMES[i] for r in self.rows for i in range(4)
                           if len(r) > 3 + i and r[3 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows),
+                "source": "nvml (in-process)" if self._nvml else "nvidia-smi"}
 
 
 def rank_seeds(config: int, rank: int):

@@ -228,18 +228,31 @@ template <int P>
 __device__ void query_prep(const float* __restrict__ queries, int nb, int len, int w,
                            float2* s_q, uint2* s_q16, float2* g_q, uint2* g_q16) {
   const int seglen = len / w;
+  // one thread per (slot, segment) in use (the rest zeroed apart); the fp64 sum runs over
+  // the segment's points in order (float4 loads when aligned: same order, same result)
   for (int i = threadIdx.x; i < 2 * P * kMaxW; i += blockDim.x) {
-    const int b = i / kMaxW, s = i % kMaxW;
-    float2 v = make_float2(0.f, 0.f);
-    if (b < nb && s < w) {
-      const float* x = queries + (size_t)b * len + (size_t)s * seglen;
-      double acc = 0.0;
-      for (int j = 0; j < seglen; ++j) acc += (double)x[j];
-      const double paa = acc / (double)seglen;
-      v = make_float2(__double2float_rd(paa), __double2float_ru(paa));
+    if (i / kMaxW >= nb || i % kMaxW >= w) {
+      s_q[i] = make_float2(0.f, 0.f);
+      if (g_q) g_q[i] = make_float2(0.f, 0.f);
     }
-    s_q[i] = v;
-    if (g_q) g_q[i] = v;
+  }
+  const bool v4 = (seglen % 4 == 0) && ((reinterpret_cast<uintptr_t>(queries) & 15u) == 0) && (len % 4 == 0);
+  for (int i = threadIdx.x; i < nb * w; i += blockDim.x) {
+    const int b = i / w, s = i % w;
+    const float* x = queries + (size_t)b * len + (size_t)s * seglen;
+    double acc = 0.0;
+    if (v4) {
+      for (int j = 0; j < seglen; j += 4) {
+        const float4 f = __ldg(reinterpret_cast<const float4*>(x + j));
+        acc += (double)f.x; acc += (double)f.y; acc += (double)f.z; acc += (double)f.w;
+      }
+    } else {
+      for (int j = 0; j < seglen; ++j) acc += (double)x[j];
+    }
+    const double paa = acc / (double)seglen;
+    const float2 v = make_float2(__double2float_rd(paa), __double2float_ru(paa));
+    s_q[b * kMaxW + s] = v;
+    if (g_q) g_q[b * kMaxW + s] = v;
   }
   __syncthreads();
   for (int i = threadIdx.x; i < P * kMaxW; i += blockDim.x) {
@@ -1325,7 +1338,7 @@ __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int s
 template <int P>
 __global__ void __launch_bounds__(256)
 k_blkmask(LbArgs a, unsigned long long* __restrict__ bmask, unsigned* __restrict__ tile_list,
-          unsigned* __restrict__ tile_count, unsigned* __restrict__ blocks) {
+          unsigned* __restrict__ tile_count, unsigned* __restrict__ blocks, unsigned* __restrict__ tile_claim) {
   // the envelope bound in the same packed fp16 pair form (and error budget, k_lb)
   // as the series bound: per segment the region [L16[min], U16[max]], two query
   // slots per instruction; a block is live for slot b iff its fp16 bound <= T16[b]
@@ -1342,8 +1355,18 @@ k_blkmask(LbArgs a, unsigned long long* __restrict__ bmask, unsigned* __restrict
   const int64_t nblocks = (a.n + PARIS_INDEX_BLOCK - 1) / PARIS_INDEX_BLOCK;
   const int64_t ntiles = (a.n + kTS - 1) / kTS;
   static_assert(kBPT == 32, "a warp step bounds the 32 blocks of one tile");
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + tid) >> 5, GW = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t g = gw; g < ntiles; g += GW) {
+  // a warp's first tile is its own index; later tiles are claimed one at a time from a
+  // global counter (the work per tile varies with the pairs its envelope leaves live; a
+  // static split left warps idle at the end), the next claim in flight while the current
+  // tile is bounded
+  const unsigned GW = (gridDim.x * blockDim.x) >> 5;
+  unsigned gnext = (blockIdx.x * blockDim.x + tid) >> 5;
+  for (;;) {
+    const int64_t g = gnext;
+    if (g >= ntiles) break;
+    unsigned cl = 0;
+    if (lane == 0) cl = atomicAdd(tile_claim, 1u);
+    gnext = GW + __shfl_sync(0xffffffffu, cl, 0);
     const int64_t blk = 32 * g + lane;
     const bool valid = blk < nblocks;
     uint4 mn = make_uint4(~0u, ~0u, ~0u, ~0u), mx = make_uint4(0u, 0u, 0u, 0u);  // neutral for padding
@@ -4035,6 +4058,7 @@ struct Ws {
   unsigned* refined;
   unsigned* blocks;      // index mode: blocks whose envelope bound passed, per query
   unsigned* tile_count;  // index mode: live tiles listed
+  unsigned* tile_claim;  // index mode: the block pass's next unclaimed tile
   unsigned* updates;     // nb mode: V_bsf updates per query
   unsigned* ghist;       // k > 1: refined-distance histograms [B][kNB]
   unsigned long long* bmask;  // index mode: [ntiles*32] per-block live query-slot masks
@@ -4179,7 +4203,7 @@ cudaError_t launch_index_lb(const Plan& p, const uint8_t* sax, int nb, const Car
   const int64_t ntiles = (p.n + kTS - 1) / kTS;
   const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms() * kBmCtas, (ntiles + 7) / 8));
   cudaError_t e = PARIS_LAUNCH("lb_blocks", k_blkmask<P>, bgrid, 256, 0, st, la, ws.bmask, ws.tile_list,
-                               ws.tile_count, ws.blocks);
+                               ws.tile_count, ws.blocks, ws.tile_claim);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(sms(), ntiles);
   const bool w30 = g_variant[0] == 30;  // tuning: 30 consumer warps (1024 threads) instead of 24
@@ -4286,12 +4310,12 @@ constexpr size_t qprep_smem(int P) { return (size_t)3 * P * kMaxW * 8; }  // <= 
 
 cudaError_t launch_qprep(int nb, const Plan& p, const float* qb, const Ws& ws, cudaStream_t st) {
   switch (pairs_for(nb)) {
-    case 1: return PARIS_LAUNCH("qprep", k_qprep<1>, 1, 256, qprep_smem(1), st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
-    case 2: return PARIS_LAUNCH("qprep", k_qprep<2>, 1, 256, qprep_smem(2), st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
-    case 4: return PARIS_LAUNCH("qprep", k_qprep<4>, 1, 256, qprep_smem(4), st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
-    case 8: return PARIS_LAUNCH("qprep", k_qprep<8>, 1, 256, qprep_smem(8), st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
-    case 16: return PARIS_LAUNCH("qprep", k_qprep<16>, 1, 256, qprep_smem(16), st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
-    default: return PARIS_LAUNCH("qprep", k_qprep<32>, 1, 256, qprep_smem(32), st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
+    case 1: return PARIS_LAUNCH("qprep", k_qprep<1>, 1, 1024, qprep_smem(1), st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
+    case 2: return PARIS_LAUNCH("qprep", k_qprep<2>, 1, 1024, qprep_smem(2), st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
+    case 4: return PARIS_LAUNCH("qprep", k_qprep<4>, 1, 1024, qprep_smem(4), st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
+    case 8: return PARIS_LAUNCH("qprep", k_qprep<8>, 1, 1024, qprep_smem(8), st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
+    case 16: return PARIS_LAUNCH("qprep", k_qprep<16>, 1, 1024, qprep_smem(16), st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
+    default: return PARIS_LAUNCH("qprep", k_qprep<32>, 1, 1024, qprep_smem(32), st, qb, nb, p.len, p.w, ws.g_q, ws.g_q16);
   }
 }
 
@@ -4353,9 +4377,9 @@ size_t ws_layout(const Plan& p, int64_t cap, Ws* ws, char* base) {
   const size_t o_q16 = take(sizeof(uint2) * (B / 2) * kMaxW);
   const size_t o_sid = take(sizeof(int) * B * p.S);
   const size_t o_skey = take(sizeof(uint64_t) * B * p.S);
-  // zeroed per batch: thr_seed | count | hist | cursor | refined | blocks | tile_count | updates
+  // zeroed per batch: thr_seed | count | hist | cursor | refined | blocks | tile_count | tile_claim | updates
   //                   | fb_refined | (k > 1) ghist
-  const size_t zb = sizeof(unsigned) * (B + B + B * kNB + B * kNB + B + B + 1 + B + B + (p.k > 1 ? B * kNB + 4 : 0));
+  const size_t zb = sizeof(unsigned) * (B + B + B * kNB + B * kNB + B + B + 2 + B + B + (p.k > 1 ? B * kNB + 4 : 0));
   const size_t o_zero = take(zb);
   const size_t o_best = take(sizeof(unsigned long long) * B * kPadU64);
   const size_t o_thr = take(sizeof(unsigned) * B * kPadU32);
@@ -4387,7 +4411,8 @@ size_t ws_layout(const Plan& p, int64_t cap, Ws* ws, char* base) {
   ws->refined = ws->cursor + B * kNB;
   ws->blocks = ws->refined + B;
   ws->tile_count = ws->blocks + B;
-  ws->updates = ws->tile_count + 1;
+  ws->tile_claim = ws->tile_count + 1;
+  ws->updates = ws->tile_claim + 1;
   ws->fb_refined = ws->updates + B;
   ws->ghist = p.k > 1 ? (unsigned*)(((uintptr_t)(ws->fb_refined + B) + 15) & ~(uintptr_t)15) : nullptr;
   ws->best = (unsigned long long*)(c + o_best);
@@ -4491,6 +4516,28 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
     const int grid = (int)std::min<int64_t>(sms(), (p.n + kTS - 1) / kTS);
     if (p.perm) {
       PARIS_CHECK_LAUNCH(dispatch_index_lb(nb, p, sax, tab, ws, st, cap), "lb_pass launch");
+      if (const char* bpath = getenv("PARIS_DEBUG_BMASK")) {  // tuning aid: block-mask statistics
+        const int64_t ntl = (p.n + kTS - 1) / kTS;
+        std::vector<unsigned long long> hm((size_t)ntl * kBPT);
+        cudaMemcpyAsync(hm.data(), ws.bmask, hm.size() * 8, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        long long bits = 0, pair_items = 0, fixed_pairs = 0, fixed_quads = 0, live_blocks = 0;
+        for (unsigned long long m : hm) {
+          const int c = __builtin_popcountll(m);
+          bits += c;
+          pair_items += (c + 1) / 2;
+          fixed_pairs += __builtin_popcountll((m | (m >> 1)) & 0x5555555555555555ull);
+          const unsigned long long q2 = m | (m >> 1), q4 = q2 | (q2 >> 2);
+          fixed_quads += __builtin_popcountll(q4 & 0x1111111111111111ull);
+          live_blocks += c > 0;
+        }
+        if (FILE* f = fopen(bpath, "a")) {
+          fprintf(f, "{\"nb\": %d, \"blocks\": %lld, \"live_blocks\": %lld, \"live_bits\": %lld, "
+                     "\"pair_items\": %lld, \"fixed_pair_items\": %lld, \"fixed_quad_items\": %lld}\n",
+                  nb, (long long)hm.size(), live_blocks, bits, pair_items, fixed_pairs, fixed_quads);
+          fclose(f);
+        }
+      }
       if (getenv("PARIS_DEBUG_TILES")) {  // debugging aid: live tiles streamed by this batch
         unsigned tc = 0;
         cudaMemcpyAsync(&tc, ws.tile_count, 4, cudaMemcpyDeviceToHost, st);
