@@ -3019,7 +3019,15 @@ k_refine1m(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     s_qn[tid] = on ? a.qaux[tid * kQAux] : 0.f;
     s_qpn[tid] = on ? a.qaux[tid * kQAux + 1] : 0.f;
   }
-  for (int i = tid; i < nb * W2; i += kRefThreads) s_qp[i] = a.qaux[(i / W2) * kQAux + 16 + i % W2];
+  // the query PAA stored so that the eight lanes of an octet (one 128-bit load phase) read
+  // eight consecutive float4: segment 8 sub + 4 e4 + e1 (lane sub, its float4 e4) at
+  // float4 e4 * 8 + sub of the query's row (a plain row put lanes sub and sub + 4 on the
+  // same banks)
+  for (int i = tid; i < nb * W2; i += kRefThreads) {
+    const int b = i / W2, sg = i % W2;
+    const int sub_ = sg / EPL, e4 = (sg % EPL) / 4, e1 = sg % 4;
+    s_qp[b * W2 + (e4 * 8 + sub_) * 4 + e1] = a.qaux[b * kQAux + 16 + sg];
+  }
   __syncthreads();
   if (warp == 0) {  // chunk offsets: an exclusive scan of ceil(cnt / 32) over the queries
     unsigned run = 0;
@@ -3112,11 +3120,11 @@ k_refine1m(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
         const int b = kb[4 * half + i];
         if (sub == 0 && keep[i]) atomicAdd(&s_paa[b], 1u);  // rows read
         keep[i] = keep[i] && key_val(key[4 * half + i]) <= thr[i];
-        const float4* qp4 = reinterpret_cast<const float4*>(s_qp + b * W2 + sub * EPL);
+        const float4* qp4 = reinterpret_cast<const float4*>(s_qp + b * W2) + sub;
         float acc = 0.f;
 #pragma unroll
         for (int e4 = 0; e4 < EPL / 4; ++e4) {
-          const float4 q = qp4[e4];
+          const float4 q = qp4[8 * e4];
           const float qq[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
           for (int e1 = 0; e1 < 4; ++e1) {
