@@ -3006,6 +3006,7 @@ k_refine1m(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
   __shared__ __align__(16) float s_qp[kMaxB * W2];
   __shared__ uint64_t s_queue[kRefWarps][64];
   __shared__ uint8_t s_qb[kRefWarps][64];
+  __shared__ float s_qt[kRefWarps][64];  // the query's pruning threshold when the key was queued
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int oct = lane >> 3, sub = lane & 7;
   if (tid < kMaxB) {
@@ -3058,6 +3059,7 @@ k_refine1m(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
   const float scale2 = __fdiv_rd((float)a.len, (float)W2);
   uint64_t* queue = s_queue[warp];
   uint8_t* qb = s_qb[warp];
+  float* qt = s_qt[warp];
   auto thr_of = [&](uint64_t bsf) { return bsf == kNoKey ? INFINITY : __fmul_ru(key_val(bsf), a.d2up); };
   // the query owning chunk gc: the last b with s_off[b] <= gc (empty queries share offsets)
   auto chunk_query = [&](unsigned gc) -> int {
@@ -3085,11 +3087,13 @@ k_refine1m(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
   auto drain = [&](int m) {
     uint64_t key[8];
     int kb[8];
+    float kt[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int e = oct + 4 * i;
       key[i] = e < m ? queue[e] : kNoKey;
       kb[i] = e < m ? (int)qb[e] : 0;
+      kt[i] = e < m ? qt[e] : 0.f;
     }
     __syncwarp();
     int nout = 0;
@@ -3103,7 +3107,7 @@ k_refine1m(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
         const int e = oct + 4 * (4 * half + i);
         const uint64_t kk = key[4 * half + i];
         const int b = kb[4 * half + i];
-        thr[i] = e < m ? thr_of(ld_relaxed_u64(a.best + (size_t)b * kPadU64)) : 0.f;
+        thr[i] = kt[4 * half + i];  // as of the chunk scan (a stale bound only prunes less)
         const __half* row = a.paa16 + (size_t)key_id(kk) * W2 + sub * EPL;
         keep[i] = e < m;
         if (EPL == 8) {
@@ -3148,6 +3152,7 @@ k_refine1m(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
           const int at = nout + __popc(mk & ((1u << lane) - 1u));
           queue[at] = key[4 * half + i];
           qb[at] = (uint8_t)b;
+          qt[at] = thr[i];
         }
         nout += __popc(mk);
       }
@@ -3170,7 +3175,7 @@ k_refine1m(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
         const int e = r0 + 4 * c + oct;
         kc[c] = e < nout ? queue[e] : kNoKey;
         bc[c] = e < nout ? (int)qb[e] : 0;
-        thr[c] = e < nout ? thr_of(ld_relaxed_u64(a.best + (size_t)bc[c] * kPadU64)) : 0.f;
+        thr[c] = e < nout ? qt[e] : 0.f;
         live[c] = e < nout;
         row[c] = reinterpret_cast<const uint4*>(a.raw16 + (size_t)key_id(kc[c]) * a.len);
       }
@@ -3260,6 +3265,7 @@ k_refine1m(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
       const int at = qn + __popc(m & ((1u << lane) - 1u));
       queue[at] = k0;
       qb[at] = (uint8_t)b;
+      qt[at] = thr;
     }
     qn += __popc(m);
     __syncwarp();
@@ -3269,6 +3275,7 @@ k_refine1m(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
       if (lane < qn - 32) {
         queue[lane] = queue[32 + lane];  // the rest to the front
         qb[lane] = qb[32 + lane];
+        qt[lane] = qt[32 + lane];
       }
       qn -= 32;
       __syncwarp();
