@@ -27,7 +27,7 @@ if os.environ.get("PARIS_LB_NOMAX"):  # tuning experiments only (bit-identical L
     FLAGS = FLAGS + [f"-DPARIS_LB_NOMAX={int(os.environ['PARIS_LB_NOMAX'])}"]
 for _k in ("PARIS_LBI_GROUPS", "PARIS_REF_RUN", "PARIS_REFQ_CTAS", "PARIS_REFU_CTAS", "PARIS_REFU_U", "PARIS_REFU16_CTAS", "PARIS_REFU16_MUL", "PARIS_LBI_UNROLL",
            "PARIS_RAW16_MINLEN", "PARIS_LBI_THREADS", "PARIS_LBI_DYN", "PARIS_BM_CTAS", "PARIS_REFM_CTAS",
-           "PARIS_REFM_KP", "PARIS_REFM_H"):  # tuning experiments only
+           "PARIS_REFM_KP", "PARIS_REFM_H", "PARIS_REFM_ROWS"):  # tuning experiments only
     if os.environ.get(_k):
         FLAGS = FLAGS + [f"-D{_k}={int(os.environ[_k])}"]
 if os.environ.get("PARIS_DEBUG"):  # device bounds checks (PARIS_DCHECK) -- debugging builds only

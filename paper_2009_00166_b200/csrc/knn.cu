@@ -2995,6 +2995,10 @@ constexpr int kRefMKP = PARIS_REFM_KP;  // chunks of keys in flight per warp
 #define PARIS_REFM_H 2
 #endif
 constexpr int kRefMH = PARIS_REFM_H;    // bf16 stage: 16-byte pieces per candidate in flight
+#ifndef PARIS_REFM_ROWS
+#define PARIS_REFM_ROWS 4
+#endif
+constexpr int kRefMRows = PARIS_REFM_ROWS;  // PAA stage: rows per octet in flight (4 or 8)
 template <int NC, int U, int W2, bool R16>
 __global__ void __launch_bounds__(kRefThreads, kRefMCtas)
 k_refine1m(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
@@ -3098,16 +3102,16 @@ k_refine1m(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
     __syncwarp();
     int nout = 0;
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      bool keep[4];
-      float thr[4];
-      uint32_t pw[4][EPL / 2];
+    for (int half = 0; half < 8 / kRefMRows; ++half) {
+      bool keep[kRefMRows];
+      float thr[kRefMRows];
+      uint32_t pw[kRefMRows][EPL / 2];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int e = oct + 4 * (4 * half + i);
-        const uint64_t kk = key[4 * half + i];
-        const int b = kb[4 * half + i];
-        thr[i] = kt[4 * half + i];  // as of the chunk scan (a stale bound only prunes less)
+      for (int i = 0; i < kRefMRows; ++i) {
+        const int e = oct + 4 * (kRefMRows * half + i);
+        const uint64_t kk = key[kRefMRows * half + i];
+        const int b = kb[kRefMRows * half + i];
+        thr[i] = kt[kRefMRows * half + i];  // as of the chunk scan (a stale bound only prunes less)
         const __half* row = a.paa16 + (size_t)key_id(kk) * W2 + sub * EPL;
         keep[i] = e < m;
         if (EPL == 8) {
@@ -3120,10 +3124,10 @@ k_refine1m(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
         }
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int b = kb[4 * half + i];
+      for (int i = 0; i < kRefMRows; ++i) {
+        const int b = kb[kRefMRows * half + i];
         if (sub == 0 && keep[i]) atomicAdd(&s_paa[b], 1u);  // rows read
-        keep[i] = keep[i] && key_val(key[4 * half + i]) <= thr[i];
+        keep[i] = keep[i] && key_val(key[kRefMRows * half + i]) <= thr[i];
         const float4* qp4 = reinterpret_cast<const float4*>(s_qp + b * W2) + sub;
         float acc = 0.f;
 #pragma unroll
@@ -3150,7 +3154,7 @@ k_refine1m(RefineArgs a, int nb, int wave, const unsigned* __restrict__ cut) {
         const unsigned mk = __ballot_sync(0xffffffffu, sub == 0 && kp);
         if (sub == 0 && kp) {
           const int at = nout + __popc(mk & ((1u << lane) - 1u));
-          queue[at] = key[4 * half + i];
+          queue[at] = key[kRefMRows * half + i];
           qb[at] = (uint8_t)b;
           qt[at] = thr[i];
         }
