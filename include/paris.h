@@ -349,9 +349,21 @@ int paris_debug_hfma2_probe(int32_t iters, int32_t blocks_per_sm, void* stream);
  * the speed differs): key 0 = consumer warps of the index LB pass (24 (default) or 30),
  * key 1 = batch-1 flat LB (0: register-prefetch k_lb1,
  * 1 (default): TMA ring k_lb1t), key 2 = pre-filtered k = 1 refine (0: k_refine1q, a warp per
- * (query, chunk run); 1 (default): k_refine1m, one chunk stream over the batch).  Returns the previous value, -1 for an unknown key.
+ * (query, chunk run); 1 (default): k_refine1m, one chunk stream over the batch), key 3 = index LB pass
+ * (0: block pass + k_lbi; 1: the tensor-core filter k_gf, falling back to 0 per pass when a query PAA
+ * exceeds 16 in magnitude).  Returns the previous value, -1 for an unknown key.
  * Process-global; not synchronized with calls in flight on other host threads. */
 int32_t paris_debug_set_variant(int32_t key, int32_t value);
+
+/* Test hook for the tensor-core filter of the index LB pass (key 3 below; k_gf, DESIGN.md f1):
+ * the raw fp32 accumulators out[pos * 64 + slot] of the three tcgen05.mma per 128 series,
+ *   sum_j half(tabw[sym_j]).lo * B[slot][2j] + half(tabw[sym_j]).hi * B[slot][2j+1] + B[slot][32] + B[slot][33],
+ * for a caller-made symbol table tabw (256 words, half2) and B matrix (64 rows x 48 fp16,
+ * columns 34..47 zero) over the tile-major sorted SAX array of n series (w = 16).  All
+ * pointers device; out holds n * 64 floats.  swap_desc != 0 swaps the descriptor's leading /
+ * stride byte offsets (diagnosis).  Synchronizes `stream`. */
+int paris_debug_gf_mma(const uint8_t* sax_sorted, int64_t n, const uint32_t* tabw, const uint16_t* bmat, float* out,
+                       int32_t swap_desc, void* stream);
 
 /* Test hook: IEEE binary16 bits of v rounded toward -inf (dir < 0) or +inf
  * (dir > 0) -- the directed rounding behind the batched fp16 lower bound. */

@@ -14,6 +14,6 @@ from ._binding import (  # noqa: F401
     ParisError, KnnConfig, Index, PARIS_INDEX_BLOCK, PARIS_INDEX_TILE, library_path, load, summarize, knn_exact,
     summarize_file, MappedRaw,
     index_build, knn_index, knn_nb, knn_approx, merge_topk, last_error, raw_bf16, paa_f16, release_workspace,
-    profile_enable, profile_reset, profile_read, launch_count, version, debug_cuts, debug_half_dir, debug_read_probe, debug_set_variant,
+    profile_enable, profile_reset, profile_read, launch_count, version, debug_cuts, debug_half_dir, debug_read_probe, debug_set_variant, debug_gf_mma,
     debug_hfma2_probe, symbols,
 )

@@ -133,6 +133,8 @@ def load():
         lib.paris_debug_read_probe.restype = ctypes.c_int
         lib.paris_debug_hfma2_probe.argtypes = [i32, i32, P]
         lib.paris_debug_hfma2_probe.restype = ctypes.c_int
+        lib.paris_debug_gf_mma.argtypes = [P, i64, P, P, P, i32, P]
+        lib.paris_debug_gf_mma.restype = ctypes.c_int
         lib.paris_debug_set_variant.argtypes = [i32, i32]
         lib.paris_debug_set_variant.restype = i32
         lib.paris_debug_half_dir.argtypes = [ctypes.c_double, i32]
@@ -516,6 +518,15 @@ def debug_hfma2_probe(iters: int, blocks_per_sm: int = 4, stream=None) -> float:
     import torch as _t
     sms = _t.cuda.get_device_properties(_t.cuda.current_device()).multi_processor_count
     return float(sms) * blocks_per_sm * 512 * iters * 8 * 2
+
+
+def debug_gf_mma(sax_sorted, n: int, tabw, bmat, swap_desc: int = 0, stream=None):
+    """paris_debug_gf_mma: the tensor-core filter's raw accumulators, [n, 64] fp32 (device)."""
+    import torch as _t
+    out = _t.empty((int(n), 64), dtype=_t.float32, device=sax_sorted.device)
+    _check(load().paris_debug_gf_mma(sax_sorted.data_ptr(), int(n), tabw.data_ptr(), bmat.data_ptr(), out.data_ptr(),
+                                     int(swap_desc), _stream(stream)))
+    return out
 
 
 def debug_set_variant(key: int, value: int) -> int:

@@ -1338,7 +1338,9 @@ __device__ __forceinline__ void lbi_emit(const uint32_t (&acc)[4], int sa, int s
 template <int P>
 __global__ void __launch_bounds__(256)
 k_blkmask(LbArgs a, unsigned long long* __restrict__ bmask, unsigned* __restrict__ tile_list,
-          unsigned* __restrict__ tile_count, unsigned* __restrict__ blocks, unsigned* __restrict__ tile_claim) {
+          unsigned* __restrict__ tile_count, unsigned* __restrict__ blocks, unsigned* __restrict__ tile_claim,
+          const unsigned* __restrict__ skip_if) {
+  if (skip_if && *skip_if) return;  // the tensor-core filter (k_gf) took this pass: no tile is listed
   // the envelope bound in the same packed fp16 pair form (and error budget, k_lb)
   // as the series bound: per segment the region [L16[min], U16[max]], two query
   // slots per instruction; a block is live for slot b iff its fp16 bound <= T16[b]
@@ -4085,6 +4087,7 @@ struct Ws {
   unsigned* fb_refined;  // overflow fallback: rows refined per query
   uint64_t* fb_lists;    // overflow fallback, k > 1: [B][fbL][k] warp lists
   float* qaux;           // [B][80] per-query refine constants (k_qaux)
+  struct GfParams* gf;   // index mode: per-pass parameters of the tensor-core filter (k_gf)
   size_t zero_bytes;
   unsigned long long* best;
   uint64_t* cand;
@@ -4190,6 +4193,25 @@ cudaError_t launch_lbt(const Plan& p, const uint8_t* sax, int nb, const CardTabl
 
 // dynamic shared memory of k_lbi<P, HC, S1>: everything the device allows a CTA beyond the
 // kernel's static shared memory (the kernel checks its layout fits)
+#include "gfilter.cuh"
+
+static_assert(sizeof(GfParams) <= 8192, "GfParams fits its workspace slot");
+cudaError_t gf_attr() {
+  static int key;
+  return once_per_device(&key, [](int) {
+    return cudaFuncSetAttribute(k_gf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGfSmem);
+  });
+}
+cudaError_t launch_gf(const LbArgs& la, int card, GfParams* gp, cudaStream_t st) {
+  cudaError_t e = gf_attr();
+  if (e != cudaSuccess) return e;
+  e = PARIS_LAUNCH("lb_prep", k_gf_prep, 1, 256, 0, st, la, card, gp);
+  if (e != cudaSuccess) return e;
+  const int64_t nrounds = (la.n + kGfRound - 1) / kGfRound;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(device_sms(), (nrounds + kGfWG - 1) / kGfWG));
+  return PARIS_LAUNCH("lb_pass", k_gf, grid, kGfThreads, kGfSmem, st, la, gp, (float*)nullptr, 0);
+}
+
 template <int P, bool HC, int NW>
 int lbi_smem() {
   return cached_per_device((const void*)k_lbi<P, HC, NW>, [](int dev) {
@@ -4221,8 +4243,15 @@ cudaError_t launch_index_lb(const Plan& p, const uint8_t* sax, int nb, const Car
   la.blocks = ws.blocks;
   const int64_t ntiles = (p.n + kTS - 1) / kTS;
   const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms() * kBmCtas, (ntiles + 7) / 8));
+  const unsigned* skip_if = nullptr;
+  if (g_variant[3] == 1 && !p.sorted_refine && p.w == 16) {
+    // tensor-core filter pass; the block pass + k_lbi below run only if it declined (gf->ok == 0)
+    const cudaError_t eg = launch_gf(la, p.card, ws.gf, st);
+    if (eg != cudaSuccess) return eg;
+    skip_if = &ws.gf->ok;
+  }
   cudaError_t e = PARIS_LAUNCH("lb_blocks", k_blkmask<P>, bgrid, 256, 0, st, la, ws.bmask, ws.tile_list,
-                               ws.tile_count, ws.blocks, ws.tile_claim);
+                               ws.tile_count, ws.blocks, ws.tile_claim, skip_if);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(sms(), ntiles);
   const bool w30 = g_variant[0] == 30;  // tuning: 30 consumer warps (1024 threads) instead of 24
@@ -4413,6 +4442,7 @@ size_t ws_layout(const Plan& p, int64_t cap, Ws* ws, char* base) {
   const int64_t ntiles = (p.n + kTS - 1) / kTS;
   const size_t o_bmask = take(p.perm ? sizeof(unsigned long long) * (size_t)ntiles * kBPT : 8);
   const size_t o_tlist = take(p.perm ? sizeof(unsigned) * (size_t)ntiles : 8);
+  const size_t o_gf = take(8192);
   if (!base) return off;
   char* c = base;
   ws->base = base;
@@ -4442,6 +4472,7 @@ size_t ws_layout(const Plan& p, int64_t cap, Ws* ws, char* base) {
   ws->qaux = (float*)(c + o_qaux);
   ws->bmask = (unsigned long long*)(c + o_bmask);
   ws->tile_list = (unsigned*)(c + o_tlist);
+  ws->gf = (GfParams*)(c + o_gf);
   return off;
 }
 
@@ -4998,7 +5029,41 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
 
 }  // namespace paris
 
+namespace paris {
+
+// Debug: the raw accumulators of k_gf for a caller-made table and B matrix (tests the
+// tcgen05 unit, its descriptors and its accumulation error).  All pointers device.
+int debug_gf_mma(const uint8_t* sax_sorted, int64_t n, const uint32_t* tabw, const uint16_t* bmat, float* out,
+                 int swap_desc, cudaStream_t st) {
+  if (!sax_sorted || !tabw || !bmat || !out || n < 1) return PARIS_EINVAL;
+  const CardTables* tab = device_tables(256);
+  if (!tab) return PARIS_ECUDA;
+  GfParams* gp = nullptr;
+  if (cudaMalloc((void**)&gp, sizeof(GfParams)) != cudaSuccess) return PARIS_ENOMEM;
+  const unsigned one = 1u;
+  cudaMemcpyAsync(gp->tabw, tabw, sizeof(uint32_t) * kMaxCard, cudaMemcpyDeviceToDevice, st);
+  cudaMemcpyAsync(gp->B, bmat, sizeof(uint16_t) * kGfN * kGfK, cudaMemcpyDeviceToDevice, st);
+  cudaMemcpyAsync(&gp->ok, &one, sizeof(unsigned), cudaMemcpyHostToDevice, st);
+  LbArgs la{};
+  la.sax = sax_sorted; la.n = n; la.w = 16; la.seglen_f = 16.f; la.tab = tab; la.nb = 0;
+  cudaError_t e = gf_attr();
+  if (e == cudaSuccess) {
+    const int64_t nrounds = (n + kGfRound - 1) / kGfRound;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(device_sms(), (nrounds + kGfWG - 1) / kGfWG));
+    e = PARIS_LAUNCH("gf_debug", k_gf, grid, kGfThreads, kGfSmem, st, la, gp, out, swap_desc);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(gp);
+  return e == cudaSuccess ? PARIS_OK : cuda_error(e, "paris_debug_gf_mma");
+}
+}  // namespace paris
+
 extern "C" {
+int paris_debug_gf_mma(const uint8_t* sax_sorted, int64_t n, const uint32_t* tabw, const uint16_t* bmat, float* out,
+                       int32_t swap_desc, void* stream) {
+  return paris::debug_gf_mma(sax_sorted, n, tabw, bmat, out, swap_desc, (cudaStream_t)stream);
+}
+
 
 int paris_knn_exact(const float* raw, const uint8_t* sax, int64_t n, const float* queries, int32_t nq,
                     int32_t k, int64_t* out_idx, float* out_dist, int32_t len, int32_t w, int32_t card,

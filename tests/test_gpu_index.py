@@ -290,7 +290,7 @@ def test_knn_index_paa_prefilter_k(P, k, w2, length):
     assert st["paa_rows"].sum() > 0 and st["refined"].sum() < st0["refined"].sum()
 
 
-@pytest.mark.parametrize("key,values", [(0, (24, 30)), (1, (0, 1)), (2, (0, 1))])
+@pytest.mark.parametrize("key,values", [(0, (24, 30)), (1, (0, 1)), (2, (0, 1)), (3, (0, 1))])
 def test_kernel_variants_identical(P, key, values):
     """Tuning variants (paris_debug_set_variant): the index LB pass at 24 and 30 consumer warps,
     the batch-1 flat LB as k_lb1 / k_lb1t, and the pre-filtered refine with and without its
@@ -311,7 +311,7 @@ def test_kernel_variants_identical(P, key, values):
     try:
         for v in values:
             P.debug_set_variant(key, v)
-            if key == 0:
+            if key in (0, 3):
                 gi, gd = P.knn_index(xd, idx, qd, k=4)
             elif key == 2:
                 gi, gd = P.knn_index(xd, idx, qd, k=1, raw16=r16, paa16=p16)
