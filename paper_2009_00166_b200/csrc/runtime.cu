@@ -457,7 +457,7 @@ static struct VariantEnv {
 extern "C" {
 
 int32_t paris_debug_set_variant(int32_t key, int32_t value) {
-  if (key < 0 || key >= 3) return -1;
+  if (key < 0 || key >= 4) return -1;
   const int old = paris::g_variant[key];
   paris::g_variant[key] = value;
   return old;
