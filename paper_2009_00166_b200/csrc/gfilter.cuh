@@ -25,10 +25,14 @@
 
 constexpr int kGfN = 64;            // query columns per MMA (= kMaxB)
 constexpr int kGfK = 48;            // K: 16 x (c, g) + 16 for the per-query constant
-constexpr int kGfRound = 256;       // series per warpgroup round (two 128-row MMA tiles)
+constexpr int kGfRound = 128;       // series per warpgroup round (one 128-row MMA tile)
 constexpr int kGfWG = 4;            // warpgroups per CTA, each an independent pipeline
 constexpr int kGfThreads = 128 * kGfWG;
-constexpr int kGfStages = 2;        // SAX stages per warpgroup
+constexpr int kGfStages = 8;        // SAX stages per warpgroup (queued survivors read their symbols later)
+constexpr int kGfAhead = 3;         // rounds whose SAX copy is in flight
+constexpr int kGfKeep = 3;          // a survivor waits at most this many rounds in its warp's queue
+constexpr int kGfQ = 128;           // survivor queue entries per warp (ring)
+static_assert(kGfAhead + kGfKeep + 2 <= kGfStages, "a stage is refilled only after its queued survivors are done");
 constexpr uint32_t kGfStageBytes = 16 * kGfRound;
 constexpr uint32_t kGfASbo = 528;   // 8-row group stride of an A tile (conflict-free row stores)
 constexpr uint32_t kGfATile = 16 * kGfASbo;
@@ -230,16 +234,19 @@ k_gf_prep(LbArgs a, int card, GfParams* __restrict__ gp) {
 
 struct GfShared {
   uint64_t full[kGfWG][kGfStages];
-  uint64_t mma[kGfWG];
+  uint64_t mma[kGfWG][2];
+  uint64_t ready[kGfWG][2];
   uint32_t tmem_base;
   LbConsts c;
   float2 lu[kMaxCard];
   float2 q[kGfN * 16];
   unsigned hist[kGfN * kNBC];
+  uint32_t hq[kGfThreads / 32][kGfQ];
   WarpBuf wb[kGfThreads / 32];
 };
 constexpr size_t kGfSmem = 1024 /* alignment */ + kMaxCard * 128 /* table */ + kGfWG * kGfStages * kGfStageBytes +
                            kGfWG * 2 * kGfATile + kGfA2Bytes + kGfBBytes + sizeof(GfShared);
+static_assert(kGfSmem <= 227 * 1024, "k_gf shared memory");
 
 // Flush of a warp's staged candidates (keys hold sorted positions; ids through perm here).
 __device__ void gf_flush(WarpBuf& wb, int nslots, const LbConsts& c, const LbArgs& a, unsigned* s_hist) {
@@ -270,6 +277,14 @@ __device__ void gf_flush(WarpBuf& wb, int nslots, const LbConsts& c, const LbArg
 
 // a: index-mode LbArgs (a.sax = tile-major sorted SAX).  dump != nullptr (debug): the raw
 // accumulators, dump[pos * 64 + slot], and no candidate work.
+//
+// Four warpgroups per CTA, each its own pipeline over 128-series rounds: iteration i builds
+// the A tile of round i (a thread per series: 16 symbol bytes -> 16 table words -> 4 row
+// stores), one warpgroup barrier, one thread issues the three MMAs of round i into TMEM
+// buffer i & 1 and the SAX copy of round i + kGfAhead, and then the warpgroup reads the
+// accumulators of round i - 1 (its MMA was issued a whole iteration earlier): 64 sign bits
+// per series.  Survivors go to a per-warp queue (round, row, slot) and are bounded 32 at a
+// time (a lane each), at most kGfKeep rounds later -- their symbols are still in the ring.
 __global__ void __launch_bounds__(kGfThreads, 1)
 k_gf(LbArgs a, const GfParams* __restrict__ gp, float* __restrict__ dump, int swap_desc) {
   if (gp->ok == 0u) return;
@@ -290,7 +305,10 @@ k_gf(LbArgs a, const GfParams* __restrict__ gp, float* __restrict__ dump, int sw
   if (tid == 0) {
     for (int i = 0; i < kGfWG; ++i) {
       for (int s = 0; s < kGfStages; ++s) mbar_init(&M.full[i][s], 1);
-      mbar_init(&M.mma[i], 1);
+      mbar_init(&M.mma[i][0], 1);
+      mbar_init(&M.mma[i][1], 1);
+      mbar_init(&M.ready[i][0], 4);
+      mbar_init(&M.ready[i][1], 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -322,136 +340,160 @@ k_gf(LbArgs a, const GfParams* __restrict__ gp, float* __restrict__ dump, int sw
   tc_fence_after();
   const uint32_t tmem = M.tmem_base;
   WarpBuf& wb = M.wb[warp];
+  uint32_t* const hq = M.hq[warp];
   const LbConsts& c = M.c;
 
   const int64_t nrounds = (a.n + kGfRound - 1) / kGfRound;
   const int64_t gw = (int64_t)blockIdx.x * kGfWG + g, gstride = (int64_t)gridDim.x * kGfWG;
+  const int cnt = gw < nrounds ? (int)((nrounds - gw + gstride - 1) / gstride) : 0;  // this warpgroup's rounds
   const uint32_t my_stage0 = s_stage + (uint32_t)g * kGfStages * kGfStageBytes;
   const uint32_t my_A = s_A + (uint32_t)g * 2 * kGfATile;
-  const uint32_t my_tmem = tmem + (uint32_t)g * 128u;  // columns [128g, 128g + 128)
+  const uint32_t my_tmem = tmem + (uint32_t)g * 128u + ((uint32_t)(32 * (warp & 3)) << 16);
   constexpr uint32_t idesc = (1u << 4) | ((uint32_t)(kGfN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  constexpr int kRPT = kTS / kGfRound;  // rounds per index tile
 
-  auto issue_load = [&](int64_t round, int st) {
-    // 16 rows of 256 bytes of the tile-major array (whole tiles are allocated)
-    const uint8_t* src = a.sax + (size_t)(round / 8) * kTileBytes + (size_t)(round % 8) * kGfRound;
-    mbar_expect_tx(&M.full[g][st], kGfStageBytes);
-#pragma unroll 1
-    for (int s = 0; s < 16; ++s)
-      bulk_g2s(gbase + my_stage0 + (uint32_t)st * kGfStageBytes + (uint32_t)s * kGfRound, src + (size_t)s * kTS, kGfRound,
-               &M.full[g][st]);
+  // whole warp: lane 0 arms the stage's barrier, lanes 0..15 copy a 128-byte row each (the
+  // tile-major array is allocated in whole tiles)
+  auto issue_load = [&](int i) {
+    const int64_t round = gw + (int64_t)i * gstride;
+    const int st = i % kGfStages;
+    const uint8_t* src = a.sax + (size_t)(round / kRPT) * kTileBytes + (size_t)(round % kRPT) * kGfRound;
+    if (lane == 0) mbar_expect_tx(&M.full[g][st], kGfStageBytes);
+    __syncwarp();
+    if (lane < 16)
+      bulk_g2s(gbase + my_stage0 + (uint32_t)st * kGfStageBytes + (uint32_t)lane * kGfRound, src + (size_t)lane * kTS,
+               kGfRound, &M.full[g][st]);
   };
-  if (wt == 0) {
-    for (int s = 0; s < kGfStages; ++s)
-      if (gw + s * gstride < nrounds) issue_load(gw + s * gstride, s);
-  }
+  if ((warp & 3) == 0)
+    for (int i = 0; i < kGfAhead && i < cnt; ++i) issue_load(i);
 
-  int it = 0;
-  for (int64_t round = gw; round < nrounds; round += gstride, ++it) {
-    const int st = it % kGfStages;
-    const uint32_t stage = my_stage0 + (uint32_t)st * kGfStageBytes;
-    mbar_wait(&M.full[g][st], (unsigned)(it / kGfStages) & 1u);
-    // ---- A rows of series 2wt, 2wt + 1 of the round: the table words of their symbols
-    {
+  // survivor queue (ring of kGfQ entries): entry = round index << 11 | lane << 6 | slot
+  unsigned qhead = 0, qcount = 0;  // warp-uniform registers
+  auto drain = [&](unsigned take) {  // bound `take` <= 32 queued survivors, a lane each
+    const bool have = (unsigned)lane < take;
+    const uint32_t e = have ? hq[(qhead + (unsigned)lane) % kGfQ] : 0u;
+    const int b = (int)(e & 63u), ln = (int)((e >> 6) & 31u), ri = (int)(e >> 11);
+    const uint32_t stage = my_stage0 + (uint32_t)(ri % kGfStages) * kGfStageBytes + (uint32_t)(32 * (warp & 3) + ln);
+    float lbv = 0.f;
+    bool cand = false;
+    if (have) {
+      float acc = 0.f;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t sym = lds_u8(stage + (uint32_t)j * kGfRound);
+        const float2 lu = M.lu[sym];
+        const float2 q = M.q[b * 16 + j];
+        const float d = fmaxf(fmaxf(__fsub_rd(lu.x, q.y), __fsub_rd(q.x, lu.y)), 0.f);
+        acc = __fmaf_rd(d, d, acc);
+      }
+      lbv = __fmul_rd(acc, a.seglen_f);
+      cand = lbv <= c.thr[b];
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, cand);
+    if (bal) {
+      const int total = __popc(bal);
+      if (wb.n + total > kWB) gf_flush(wb, nslots, c, a, M.hist);
+      if (cand) {
+        const int64_t pos = (gw + (int64_t)ri * gstride) * kGfRound + 32 * (warp & 3) + ln;
+        const int e2 = wb.n + __popc(bal & ((1u << lane) - 1u));
+        wb.key[e2] = make_key(lbv, (uint32_t)pos);
+        wb.slot[e2] = (uint8_t)b;
+        atomicAdd(&wb.cnt[b], 1u);
+      }
+      __syncwarp();
+      if (lane == 0) wb.n += total;
+      __syncwarp();
+    }
+    qhead = (qhead + take) % kGfQ;
+    qcount -= take;
+  };
+
+  for (int i = 0; i <= cnt; ++i) {
+    if (i < cnt) {
+      const int st = i % kGfStages;
+      const uint32_t stage = my_stage0 + (uint32_t)st * kGfStageBytes + (uint32_t)wt;
+      mbar_wait(&M.full[g][st], (unsigned)(i / kGfStages) & 1u);
+      // ---- A row of series wt of the round: the table words of its symbols
       const uint32_t tl = s_tab + 4u * (uint32_t)lane;
-      const int r0 = 2 * (wt & 63);
-      const uint32_t rowa = my_A + (uint32_t)(wt >> 6) * kGfATile + (uint32_t)(r0 >> 3) * kGfASbo + (uint32_t)(r0 & 7) * 16u;
+      const uint32_t rowa = my_A + (uint32_t)(i & 1) * kGfATile + (uint32_t)(wt >> 3) * kGfASbo + (uint32_t)(wt & 7) * 16u;
 #pragma unroll
       for (int kc = 0; kc < 4; ++kc) {
-        uint32_t w0[4], w1[4];
+        uint32_t w0[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const uint32_t two = lds_u16(stage + (uint32_t)(4 * kc + e) * kGfRound + 2u * (uint32_t)wt);
-          w0[e] = lds_u32(tl + ((two & 0xFFu) << 7));
-          w1[e] = lds_u32(tl + ((two >> 8) << 7));
-        }
+        for (int e = 0; e < 4; ++e) w0[e] = lds_u32(tl + (lds_u8(stage + (uint32_t)(4 * kc + e) * kGfRound) << 7));
         sts_u4(rowa + (uint32_t)kc * 128u, w0[0], w0[1], w0[2], w0[3]);
-        sts_u4(rowa + (uint32_t)kc * 128u + 16u, w1[0], w1[1], w1[2], w1[3]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&M.ready[g][i & 1]);  // this warp: A(i) rows written, accumulators of round i - 2 read
+      if ((warp & 3) == (i & 3)) {
+        // this round's issuer (the warps take turns): all four warps ready -> the three MMAs of
+        // round i, then the SAX copy of round i + kGfAhead (into the stage of round
+        // i + kGfAhead - kGfStages: no warp holds a survivor that old)
+        mbar_wait(&M.ready[g][i & 1], (unsigned)(i >> 1) & 1u);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t At = my_A + (uint32_t)(i & 1) * kGfATile;
+          const uint32_t d = tmem + (uint32_t)g * 128u + (uint32_t)(i & 1) * kGfN;
+          const uint32_t la = swap_desc ? kGfASbo : 128u, sa = swap_desc ? 128u : kGfASbo;
+          const uint32_t lb = swap_desc ? kGfBSbo : 128u, sb = swap_desc ? 128u : kGfBSbo;
+          const uint32_t l2 = swap_desc ? kGfA2Sbo : 128u, s2 = swap_desc ? 128u : kGfA2Sbo;
+          tc_mma_f16(d, gf_desc(At, la, sa), gf_desc(s_B, lb, sb), idesc, 0u);
+          tc_mma_f16(d, gf_desc(At + 256u, la, sa), gf_desc(s_B + 256u, lb, sb), idesc, 1u);
+          tc_mma_f16(d, gf_desc(s_A2, l2, s2), gf_desc(s_B + 512u, lb, sb), idesc, 1u);
+          tc_commit(&M.mma[g][i & 1]);
+        }
+        __syncwarp();
+        if (i + kGfAhead < cnt) issue_load(i + kGfAhead);
       }
     }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    tc_fence_before();
-    wg_bar(1 + g);
-    if (wt == 0) {
-      tc_fence_after();
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const uint32_t At = my_A + (uint32_t)t * kGfATile;
-        const uint32_t d = my_tmem + (uint32_t)t * kGfN;
-        const uint32_t la = swap_desc ? kGfASbo : 128u, sa = swap_desc ? 128u : kGfASbo;
-        const uint32_t lb = swap_desc ? kGfBSbo : 128u, sb = swap_desc ? 128u : kGfBSbo;
-        const uint32_t l2 = swap_desc ? kGfA2Sbo : 128u, s2 = swap_desc ? 128u : kGfA2Sbo;
-        tc_mma_f16(d, gf_desc(At, la, sa), gf_desc(s_B, lb, sb), idesc, 0u);
-        tc_mma_f16(d, gf_desc(At + 256u, la, sa), gf_desc(s_B + 256u, lb, sb), idesc, 1u);
-        tc_mma_f16(d, gf_desc(s_A2, l2, s2), gf_desc(s_B + 512u, lb, sb), idesc, 1u);
-      }
-      tc_commit(&M.mma[g]);
-    }
-    mbar_wait(&M.mma[g], (unsigned)it & 1u);
+    if (i == 0) continue;
+    // ---- epilogue of round i - 1: the sign of each accumulator
+    const int ri = i - 1;
+    mbar_wait(&M.mma[g][ri & 1], (unsigned)(ri >> 1) & 1u);
     tc_fence_after();
-    // ---- epilogue: the sign of each accumulator
-#pragma unroll 1
-    for (int t = 0; t < 2; ++t) {
-      uint32_t v[64];
-      tc_ld64(my_tmem + (uint32_t)t * kGfN + ((uint32_t)(32 * (warp & 3)) << 16), v);
-      const int col = t * 128 + 32 * (warp & 3) + lane;  // series of the round
-      const int64_t pos = round * kGfRound + col;
-      if (dump) {
-        if (pos < a.n) {
+    uint32_t v[64];
+    tc_ld64(my_tmem + (uint32_t)(ri & 1) * kGfN, v);
+    const int64_t pos = (gw + (int64_t)ri * gstride) * kGfRound + 32 * (warp & 3) + lane;
+    if (dump) {
+      if (pos < a.n) {
 #pragma unroll
-          for (int i = 0; i < 64; ++i) dump[(size_t)pos * 64 + i] = __uint_as_float(v[i]);
-        }
-        continue;
+        for (int k = 0; k < 64; ++k) dump[(size_t)pos * 64 + k] = __uint_as_float(v[k]);
       }
-      uint32_t m0 = 0, m1 = 0;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) m0 = __funnelshift_l(v[i], m0, 1);
-#pragma unroll
-      for (int i = 32; i < 64; ++i) m1 = __funnelshift_l(v[i], m1, 1);
-      m0 = __brev(m0);  // bit i: slot i
-      m1 = __brev(m1);  // bit i: slot 32 + i
-      if (pos >= a.n) { m0 = 0; m1 = 0; }
-      // ---- survivors: rigorous fp32 MINDIST from the symbols, one per lane per turn
-      while (__any_sync(0xffffffffu, (m0 | m1) != 0u)) {
-        const bool have = (m0 | m1) != 0u;
-        int b = 0;
-        if (m0) { b = __ffs(m0) - 1; m0 &= m0 - 1; }
-        else if (m1) { b = 32 + __ffs(m1) - 1; m1 &= m1 - 1; }
-        float lbv = 0.f;
-        bool cand = false;
-        if (have && b < a.nb) {
-          float acc = 0.f;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const uint32_t sym = lds_u8(stage + (uint32_t)j * kGfRound + (uint32_t)col);
-            const float2 lu = M.lu[sym];
-            const float2 q = M.q[b * 16 + j];
-            const float d = fmaxf(fmaxf(__fsub_rd(lu.x, q.y), __fsub_rd(q.x, lu.y)), 0.f);
-            acc = __fmaf_rd(d, d, acc);
-          }
-          lbv = __fmul_rd(acc, a.seglen_f);
-          cand = lbv <= c.thr[b];
-        }
-        const unsigned bal = __ballot_sync(0xffffffffu, cand);
-        if (bal) {
-          const int total = __popc(bal);
-          if (wb.n + total > kWB) gf_flush(wb, nslots, c, a, M.hist);
-          if (cand) {
-            const int e = wb.n + __popc(bal & ((1u << lane) - 1u));
-            wb.key[e] = make_key(lbv, (uint32_t)pos);
-            wb.slot[e] = (uint8_t)b;
-            atomicAdd(&wb.cnt[b], 1u);
-          }
-          __syncwarp();
-          if (lane == 0) wb.n += total;
-          __syncwarp();
-        }
-      }
+      continue;
     }
-    tc_fence_before();
-    wg_bar(1 + g);  // every warp is done with the stage and the accumulators
-    if (wt == 0 && round + kGfStages * gstride < nrounds) issue_load(round + kGfStages * gstride, st);
+    uint32_t m0 = 0, m1 = 0;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) m0 = __funnelshift_l(v[k], m0, 1);
+#pragma unroll
+    for (int k = 32; k < 64; ++k) m1 = __funnelshift_l(v[k], m1, 1);
+    m0 = __brev(m0);  // bit k: slot k
+    m1 = __brev(m1);  // bit k: slot 32 + k
+    if (pos >= a.n) { m0 = 0; m1 = 0; }
+    // ---- queue the survivors, one per lane per turn
+    while (__any_sync(0xffffffffu, (m0 | m1) != 0u)) {
+      if (qcount + 32u > (unsigned)kGfQ) drain(32u);
+      const bool have = (m0 | m1) != 0u;
+      int b = 0;
+      if (m0) { b = __ffs(m0) - 1; m0 &= m0 - 1; }
+      else if (m1) { b = 32 + __ffs(m1) - 1; m1 &= m1 - 1; }
+      const bool keep = have && b < a.nb;
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (keep) hq[(qhead + qcount + (unsigned)__popc(bal & ((1u << lane) - 1u))) % kGfQ] = ((uint32_t)ri << 11) | ((uint32_t)lane << 6) | (uint32_t)b;
+      qcount += (unsigned)__popc(bal);
+      __syncwarp();
+    }
+    while (qcount >= 32u) drain(32u);
+    if (qcount) {
+      const int oldest = (int)(hq[qhead] >> 11);
+      if (oldest <= ri - kGfKeep + 1) drain(qcount);
+    }
   }
-  if (!dump) gf_flush(wb, nslots, c, a, M.hist);
+  if (!dump) {
+    while (qcount) drain(qcount < 32u ? qcount : 32u);
+    gf_flush(wb, nslots, c, a, M.hist);
+  }
   tc_fence_before();
   __syncthreads();
   if (!dump)
