@@ -492,7 +492,10 @@ def run_gpu(args):
         full=True also the end-to-end variant through host buffers and the clock record."""
         use_idx = path == "index"
         use_nb = path == "nb"
-        b_path = args.batch or (64 if use_idx else 16)  # the library's default queries per pass
+        gfv = P.debug_set_variant(3, 0)  # read the LB-pass variant (restored at once)
+        P.debug_set_variant(3, gfv)
+        gf_on = (gfv == 1) or (gfv == 2 and not use_idx)  # the pass runs through the tensor-core filter (k_gf)
+        b_path = args.batch or (64 if (use_idx or gf_on) else 16)  # the library's default queries per pass
         kcfg = P.KnnConfig(batch=b_path, index_seeds=args.index_seeds, sorted_refine=args.sorted_refine)
         nbatches = sum((min(call_q, nq - c0) + b_path - 1) // b_path for c0 in range(0, nq, call_q))
         q_per_pass = nq / nbatches
@@ -636,6 +639,21 @@ def run_gpu(args):
                              "active_block_frac": blocks / (nq * (n_local / P.PARIS_INDEX_BLOCK)),
                              "hbm_achieved_gbs": alg[dom] / (per_launch_ms / 1e3) / 1e9, "hbm_peak_gbs": peak,
                              "queries_per_pass": q_per_pass}, **alu)
+            elif dom == "lb_pass" and "lb_prep" in kern:
+                # the tensor-core filter (k_gf): the contraction itself is far from the tensor peak (K = 48);
+                # the pass is bound by the integer/ALU pipe -- per series 16 symbol extractions + 16 table
+                # address computations and one sign extraction per (series, slot of 64) -- against
+                # 148 SMs x 64 ALU-pipe lanes per clock (DESIGN.md f1, k_gf)
+                ops = n_local * (32.0 + 64.0)
+                pk_alu = 148 * 64 * ALU_CLOCK_GHZ * 1e9 / 1e12
+                ach = ops / (per_launch_ms / 1e3) / 1e12
+                roof = {"kernel": dom + " (k_gf)", "bound": "alu", "achieved": ach, "unit": "T lane-ops/s (ALU pipe)",
+                        "peak": pk_alu, "frac": ach / pk_alu,
+                        "peak_source": f"derived: 148 SM x 64 ALU-pipe lanes/clk x {ALU_CLOCK_GHZ} GHz",
+                        "traffic": None, "algorithmic_ops_per_batch": ops, "ms_per_batch": per_launch_ms,
+                        "tensor_tflops": 2.0 * n_local * 64 * 48 / (per_launch_ms / 1e3) / 1e12,
+                        "hbm_achieved_gbs": alg[dom] / (per_launch_ms / 1e3) / 1e9, "hbm_peak_gbs": peak,
+                        "queries_per_pass": q_per_pass}
             elif dom == "lb_pass" and q_per_pass > 1.5:
                 # batched fp16x2 LB: bound by the FMA pipe, not HBM
                 ops = 3.0 * n_local * W * q_per_pass

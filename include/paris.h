@@ -349,9 +349,11 @@ int paris_debug_hfma2_probe(int32_t iters, int32_t blocks_per_sm, void* stream);
  * the speed differs): key 0 = consumer warps of the index LB pass (24 (default) or 30),
  * key 1 = batch-1 flat LB (0: register-prefetch k_lb1,
  * 1 (default): TMA ring k_lb1t), key 2 = pre-filtered k = 1 refine (0: k_refine1q, a warp per
- * (query, chunk run); 1 (default): k_refine1m, one chunk stream over the batch), key 3 = index LB pass
- * (0: block pass + k_lbi; 1: the tensor-core filter k_gf, falling back to 0 per pass when a query PAA
- * exceeds 16 in magnitude).  Returns the previous value, -1 for an unknown key.
+ * (query, chunk run); 1 (default): k_refine1m, one chunk stream over the batch), key 3 = the LB pass as a
+ * tensor-core filter (k_gf: 64 query slots per pass, tcgen05.mma + the sign of the accumulators, fp32 MINDIST for
+ * the survivors; a pass falls back to the fp16 kernels when a query PAA exceeds 16 in magnitude): 2 (default) = on
+ * the flat path (paris_knn_exact; 2.6x at 1e8 x 256), 1 = on the index path too (slower there than the block pass +
+ * k_lbi), 0 = off.  Returns the previous value, -1 for an unknown key.
  * Process-global; not synchronized with calls in flight on other host threads. */
 int32_t paris_debug_set_variant(int32_t key, int32_t value);
 

@@ -275,7 +275,8 @@ __device__ void gf_flush(WarpBuf& wb, int nslots, const LbConsts& c, const LbArg
   __syncwarp();
 }
 
-// a: index-mode LbArgs (a.sax = tile-major sorted SAX).  dump != nullptr (debug): the raw
+// a: LbArgs of the index path (a.perm set, a.sax = tile-major sorted SAX) or of the flat path (a.perm null,
+// a.sax = [16][n], n % 16 == 0).  dump != nullptr (debug): the raw
 // accumulators, dump[pos * 64 + slot], and no candidate work.
 //
 // Four warpgroups per CTA, each its own pipeline over 128-series rounds: iteration i builds
@@ -357,12 +358,16 @@ k_gf(LbArgs a, const GfParams* __restrict__ gp, float* __restrict__ dump, int sw
   auto issue_load = [&](int i) {
     const int64_t round = gw + (int64_t)i * gstride;
     const int st = i % kGfStages;
-    const uint8_t* src = a.sax + (size_t)(round / kRPT) * kTileBytes + (size_t)(round % kRPT) * kGfRound;
-    if (lane == 0) mbar_expect_tx(&M.full[g][st], kGfStageBytes);
+    // index: tile-major [tile][16][2048] (whole tiles allocated); flat: [16][n]
+    const uint8_t* src = a.perm ? a.sax + (size_t)(round / kRPT) * kTileBytes + (size_t)(round % kRPT) * kGfRound
+                                : a.sax + (size_t)round * kGfRound;
+    const size_t rstride = a.perm ? (size_t)kTS : (size_t)a.n;
+    const unsigned bytes = a.perm ? (unsigned)kGfRound : (unsigned)imin64(kGfRound, a.n - round * kGfRound);
+    if (lane == 0) mbar_expect_tx(&M.full[g][st], bytes * 16u);
     __syncwarp();
     if (lane < 16)
-      bulk_g2s(gbase + my_stage0 + (uint32_t)st * kGfStageBytes + (uint32_t)lane * kGfRound, src + (size_t)lane * kTS,
-               kGfRound, &M.full[g][st]);
+      bulk_g2s(gbase + my_stage0 + (uint32_t)st * kGfStageBytes + (uint32_t)lane * kGfRound, src + (size_t)lane * rstride,
+               bytes, &M.full[g][st]);
   };
   if ((warp & 3) == 0)
     for (int i = 0; i < kGfAhead && i < cnt; ++i) issue_load(i);

@@ -621,6 +621,7 @@ struct LbArgs {
   const uint32_t* perm;  // index mode: sorted position -> series id (else nullptr)
   const uint8_t* env;    // index mode: [n/64 blocks][2][16] min/max symbols (else nullptr)
   unsigned* blocks;      // index mode: per query, blocks whose envelope bound passed
+  const unsigned* skip_if = nullptr;  // k_lbt<P, 1>: leave at once if *skip_if != 0 (k_gf took the pass)
 };
 
 struct LbConsts {
@@ -990,6 +991,7 @@ __device__ __forceinline__ void lbt_seg1(uint32_t word, const uint32_t* __restri
 template <int P, int MODE>
 __global__ void __launch_bounds__(kTThreads, 1)
 k_lbt(LbArgs a, int64_t nlim, int* __restrict__ seed_ids, int S) {
+  if (MODE == 1 && a.skip_if && *a.skip_if) return;
   constexpr int PP = P > 0 ? P : 1;
   extern __shared__ __align__(128) uint8_t dsm[];
   uint8_t* s_tiles = dsm;
@@ -4087,7 +4089,8 @@ struct Ws {
   unsigned* fb_refined;  // overflow fallback: rows refined per query
   uint64_t* fb_lists;    // overflow fallback, k > 1: [B][fbL][k] warp lists
   float* qaux;           // [B][80] per-query refine constants (k_qaux)
-  struct GfParams* gf;   // index mode: per-pass parameters of the tensor-core filter (k_gf)
+  struct GfParams* gf;   // per-pass parameters of the tensor-core filter (k_gf)
+  const unsigned* lb_skip_if = nullptr;  // flat path behind k_gf: the k_lbt passes run only if it declined
   size_t zero_bytes;
   unsigned long long* best;
   uint64_t* cand;
@@ -4120,6 +4123,7 @@ struct Plan {
   int w2 = 0;
   const float* tau_in = nullptr;    // external per-query bound of the k-th NN distance (device)
   bool approx = false;              // paris_knn_approx: the seeds' top-k only
+  bool gf = false;                  // LB pass through the tensor-core filter (variant key 3)
 };
 
 int pairs_for(int nb) { return nb <= 2 ? 1 : nb <= 4 ? 2 : nb <= 8 ? 4 : nb <= 16 ? 8 : nb <= 32 ? 16 : 32; }
@@ -4187,6 +4191,7 @@ cudaError_t launch_lbt(const Plan& p, const uint8_t* sax, int nb, const CardTabl
   la.g_q = ws.g_q; la.g_q16 = ws.g_q16; la.nb = nb; la.thr = ws.thr_seed; la.count = ws.count;
   la.hist = ws.hist; la.cand = ws.cand; la.cap = cap; la.perm = p.perm; la.env = p.env;
   la.blocks = ws.blocks;
+  la.skip_if = MODE == 1 ? ws.lb_skip_if : nullptr;
   return PARIS_LAUNCH(MODE ? "lb_pass" : "seed_lb", (k_lbt<P, MODE>), grid, kTThreads, kTSmem, st, la, nlim,
                       ws.seed_ids, p.S);
 }
@@ -4244,7 +4249,7 @@ cudaError_t launch_index_lb(const Plan& p, const uint8_t* sax, int nb, const Car
   const int64_t ntiles = (p.n + kTS - 1) / kTS;
   const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms() * kBmCtas, (ntiles + 7) / 8));
   const unsigned* skip_if = nullptr;
-  if (g_variant[3] == 1 && !p.sorted_refine && p.w == 16) {
+  if (p.gf) {
     // tensor-core filter pass; the block pass + k_lbi below run only if it declined (gf->ok == 0)
     const cudaError_t eg = launch_gf(la, p.card, ws.gf, st);
     if (eg != cudaSuccess) return eg;
@@ -4509,9 +4514,29 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
   const int P = pairs_for(nb);
   cudaError_t e = cudaMemsetAsync(ws.zero_block, 0, ws.zero_bytes, st);
   if (e != cudaSuccess) return cuda_error(e, "memset scratch");
+  // flat path behind the tensor-core filter: up to 64 slots per pass; query prep, the seed
+  // pass and (if the filter declines) the k_lbt pass run per sub-batch of 16 slots, each on
+  // its own slice of the scratch
+  const bool gf_flat = p.gf && !p.perm && nb > 8;
+  auto sub_ws = [&](int j0) {
+    Ws w2 = ws;
+    w2.g_q = ws.g_q + (size_t)j0 * kMaxW;
+    w2.g_q16 = ws.g_q16 + (size_t)(j0 / kMaxBFlat) * kMaxW * (kMaxBFlat / 2);
+    w2.seed_ids = ws.seed_ids + (size_t)j0 * p.S;
+    w2.thr_seed = ws.thr_seed + j0;
+    w2.count = ws.count + j0;
+    w2.hist = ws.hist + (size_t)j0 * kNB;
+    w2.cand = ws.cand + (size_t)j0 * cap;
+    w2.lb_skip_if = &ws.gf->ok;
+    return w2;
+  };
   if (rescan) {
     // query PAA (the direct LB kernels compute it in their seed prologue) + BSF from the first pass
-    if (p.tiled) PARIS_CHECK_LAUNCH(launch_qprep(nb, p, qbatch, ws, st), "qprep launch");
+    if (gf_flat) {
+      for (int j0 = 0; j0 < nb; j0 += kMaxBFlat)
+        PARIS_CHECK_LAUNCH(launch_qprep(std::min(kMaxBFlat, nb - j0), p, qbatch + (size_t)j0 * p.len, sub_ws(j0), st),
+                           "qprep launch");
+    } else if (p.tiled) PARIS_CHECK_LAUNCH(launch_qprep(nb, p, qbatch, ws, st), "qprep launch");
     else PARIS_CHECK_LAUNCH(dispatch_p(P, false, p, sax, qbatch, nb, tab, ws, st, cap), "seed_lb launch");
     PARIS_CHECK_LAUNCH(PARIS_LAUNCH("seed_select", k_seed_prev, 1, kMaxB, 0, st, d_idx, d_dist, nb, q0, p.k, p.d2up,
                                     ws.thr, ws.thr_seed, ws.best),
@@ -4522,6 +4547,13 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
       PARIS_CHECK_LAUNCH(PARIS_LAUNCH("seed_lb", k_approx_seed, nb, 32, 0, st, sax, p.perm, p.n, ws.g_q, tab, p.card,
                                       ws.seed_ids, p.S),
                          "approx seed launch");
+    } else if (gf_flat) {
+      for (int j0 = 0; j0 < nb; j0 += kMaxBFlat) {
+        const int nbj = std::min(kMaxBFlat, nb - j0);
+        const Ws w2 = sub_ws(j0);
+        PARIS_CHECK_LAUNCH(launch_qprep(nbj, p, qbatch + (size_t)j0 * p.len, w2, st), "qprep launch");
+        PARIS_CHECK_LAUNCH(dispatch_lbt<0>(nbj, p, sax, tab, w2, st, cap, p.ns, p.seed_grid), "seed_lb launch");
+      }
     } else if (p.tiled) {
       PARIS_CHECK_LAUNCH(launch_qprep(nb, p, qbatch, ws, st), "qprep launch");
       PARIS_CHECK_LAUNCH(dispatch_lbt<0>(nb, p, sax, tab, ws, st, cap, p.ns, p.seed_grid), "seed_lb launch");
@@ -4595,6 +4627,17 @@ int run_batch(const Plan& p, const float* raw, const uint8_t* sax, const float* 
         fprintf(stderr, "[paris] batch q0=%d nb=%d: %u of %lld tiles live\n", q0, nb, tc,
                 (long long)((p.n + kTS - 1) / kTS));
       }
+    }
+    else if (gf_flat) {
+      LbArgs la;
+      la.sax = sax; la.n = p.n; la.w = p.w; la.seglen_f = (float)(p.len / p.w); la.tab = tab;
+      la.g_q = ws.g_q; la.g_q16 = ws.g_q16; la.nb = nb; la.thr = ws.thr_seed; la.count = ws.count;
+      la.hist = ws.hist; la.cand = ws.cand; la.cap = cap; la.perm = nullptr; la.env = nullptr;
+      la.blocks = ws.blocks;
+      PARIS_CHECK_LAUNCH(launch_gf(la, p.card, ws.gf, st), "lb_pass launch");
+      for (int j0 = 0; j0 < nb; j0 += kMaxBFlat)  // only if the filter declined the pass
+        PARIS_CHECK_LAUNCH(dispatch_lbt<1>(std::min(kMaxBFlat, nb - j0), p, sax, tab, sub_ws(j0), st, cap, p.n, grid),
+                           "lb_pass launch");
     }
     else if (nb == 1) PARIS_CHECK_LAUNCH(launch_lb1(p, sax, tab, ws, st, cap), "lb_pass launch");
     else PARIS_CHECK_LAUNCH(dispatch_lbt<1>(nb, p, sax, tab, ws, st, cap, p.n, grid), "lb_pass launch");
@@ -4847,11 +4890,15 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
 
   Plan p;
   p.n = n; p.len = len; p.w = w; p.card = card; p.k = k;
+  p.tiled = (n % 16 == 0) && (w == kTW) && (indexed || !(cfg && cfg->reserved[0] == 1));
+  // tensor-core filter (variant key 3): 2 (default) = flat path only, 1 = index path too, 0 = off
+  p.gf = (g_variant[3] == 1 || (g_variant[3] == 2 && !indexed)) && p.tiled && !nb_mode && !approx &&
+         !(cfg && cfg->reserved[1] == 1);
   {
-    const int cap_b = indexed ? kMaxB : kMaxBFlat;  // index: 64 queries per pass, flat: 16
+    // index: 64 queries per pass; flat: 16 (k_lbt), 64 behind the tensor-core filter
+    const int cap_b = (indexed || p.gf) ? kMaxB : kMaxBFlat;
     p.B = (cfg && cfg->batch > 0) ? std::min(cfg->batch, cap_b) : cap_b;
   }
-  p.tiled = (n % 16 == 0) && (w == kTW) && (indexed || !(cfg && cfg->reserved[0] == 1));
   p.perm = perm;
   p.env = env;
   p.nb = nb_mode;
@@ -5046,6 +5093,7 @@ int debug_gf_mma(const uint8_t* sax_sorted, int64_t n, const uint32_t* tabw, con
   cudaMemcpyAsync(&gp->ok, &one, sizeof(unsigned), cudaMemcpyHostToDevice, st);
   LbArgs la{};
   la.sax = sax_sorted; la.n = n; la.w = 16; la.seglen_f = 16.f; la.tab = tab; la.nb = 0;
+  la.perm = reinterpret_cast<const uint32_t*>(sax_sorted);  // tile-major layout (never read: no candidates here)
   cudaError_t e = gf_attr();
   if (e == cudaSuccess) {
     const int64_t nrounds = (n + kGfRound - 1) / kGfRound;

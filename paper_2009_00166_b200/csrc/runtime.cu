@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(512) k_hfma2_probe(int iters, unsigned* out) {
   if (x == 0x9E3779B9u) out[0] = x;  // keeps the chains live; practically never taken
 }
 }  // namespace
-int g_variant[4] = {24, 1, 1, 0};
+int g_variant[4] = {24, 1, 1, 2};
 // PARIS_VARIANT="key=value,key=value" sets tuning variants at load time (profiling runs
 // of unmodified scripts); paris_debug_set_variant overrides them later
 static struct VariantEnv {

@@ -94,6 +94,46 @@ def test_knn_index_gf_parity(P, n, nq, k, card):
     assert c1 <= c0 * 1.01 + 16  # fp32 MINDIST is at least as tight as the fp16 one
 
 
+@pytest.mark.parametrize("n,nq,k", [(70_000, 40, 1), (50_000 + 16, 64, 3), (33_008, 100, 1), (20_000, 9, 5)])
+def test_knn_flat_gf_parity(P, n, nq, k):
+    """paris_knn_exact behind the filter: 64 query slots per pass of the flat [16][n] array
+    (seeds per 16-slot sub-batch), same rows as the default flat path and the oracle."""
+    import torch
+    x = datagen.random_walks(n, 256, 940 + k)
+    q = datagen.random_walks(nq, 256, 941 + k)
+    q[nq - 1] = x[7]
+    xd = torch.from_numpy(x).cuda()
+    qd = torch.from_numpy(q).cuda()
+    sax = P.summarize(xd, 16, 256)
+    ri, rd2 = oracle.knn_bruteforce(x, q, k)
+    old = P.debug_set_variant(3, 0)
+    try:
+        hi, hd, st0 = P.knn_exact(xd, sax, qd, k=k, stats=True)  # k_lbt, 16 slots per pass
+        P.debug_set_variant(3, 2)
+        gi, gd, st1 = P.knn_exact(xd, sax, qd, k=k, stats=True)  # k_gf, 64 slots per pass (the default)
+    finally:
+        P.debug_set_variant(3, old)
+    assert old == 2
+    check_knn(x, q, gi.cpu().numpy(), gd.cpu().numpy(), ri, rd2)
+    assert torch.equal(gi, hi) and torch.equal(gd, hd)
+    c0, c1 = int(st0["candidates"].sum()), int(st1["candidates"].sum())
+    print(f"flat candidates: k_lbt {c0}, k_gf {c1}")
+
+
+def test_knn_flat_gf_unnormalized_falls_back(P):
+    import torch
+    n = 40_000
+    x = datagen.random_walks(n, 256, 950)
+    q = datagen.random_walks(20, 256, 951)
+    q[17] = q[17] * 40.0 + 25.0
+    xd = torch.from_numpy(x).cuda()
+    qd = torch.from_numpy(q).cuda()
+    sax = P.summarize(xd, 16, 256)
+    ri, rd2 = oracle.knn_bruteforce(x, q, 2)
+    gi, gd = P.knn_exact(xd, sax, qd, k=2)  # the filter is the flat path's default
+    check_knn(x, q, gi.cpu().numpy(), gd.cpu().numpy(), ri, rd2)
+
+
 def test_knn_index_gf_unnormalized_falls_back(P):
     """Query PAA beyond +-16: the filter declines the pass and the block pass + k_lbi run."""
     import torch
