@@ -27,7 +27,8 @@ constexpr int kGfN = 64;            // query columns per MMA (= kMaxB)
 constexpr int kGfK = 48;            // K: 16 x (c, g) + 16 for the per-query constant
 constexpr int kGfRound = 128;       // series per warpgroup round (one 128-row MMA tile)
 constexpr int kGfWG = 4;            // warpgroups per CTA, each an independent pipeline
-constexpr int kGfThreads = 128 * kGfWG;
+constexpr int kGfWorkers = 128 * kGfWG;
+constexpr int kGfThreads = kGfWorkers + 32;  // + the issuing warp (MMAs, SAX copies)
 constexpr int kGfStages = 8;        // SAX stages per warpgroup (queued survivors read their symbols later)
 constexpr int kGfAhead = 3;         // rounds whose SAX copy is in flight
 constexpr int kGfKeep = 3;          // a survivor waits at most this many rounds in its warp's queue
@@ -98,6 +99,14 @@ __device__ __forceinline__ void tc_ld64(uint32_t taddr, uint32_t (&v)[64]) {
         "=r"(v[49]), "=r"(v[50]), "=r"(v[51]), "=r"(v[52]), "=r"(v[53]), "=r"(v[54]), "=r"(v[55]), "=r"(v[56]),
         "=r"(v[57]), "=r"(v[58]), "=r"(v[59]), "=r"(v[60]), "=r"(v[61]), "=r"(v[62]), "=r"(v[63])
       : "r"(taddr)
+      : "memory");
+}
+// one 2-D tile (box of the tensor map) global -> shared, completing on an mbarrier
+__device__ __forceinline__ void tma_tile_2d(uint32_t dst, const void* tmap, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(dst),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
 __device__ __forceinline__ void sts_u4(uint32_t addr, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
@@ -241,8 +250,8 @@ struct GfShared {
   float2 lu[kMaxCard];
   float2 q[kGfN * 16];
   unsigned hist[kGfN * kNBC];
-  uint32_t hq[kGfThreads / 32][kGfQ];
-  WarpBuf wb[kGfThreads / 32];
+  uint32_t hq[kGfWorkers / 32][kGfQ];
+  WarpBuf wb[kGfWorkers / 32];
 };
 constexpr size_t kGfSmem = 1024 /* alignment */ + kMaxCard * 128 /* table */ + kGfWG * kGfStages * kGfStageBytes +
                            kGfWG * 2 * kGfATile + kGfA2Bytes + kGfBBytes + sizeof(GfShared);
@@ -287,7 +296,8 @@ __device__ void gf_flush(WarpBuf& wb, int nslots, const LbConsts& c, const LbArg
 // per series.  Survivors go to a per-warp queue (round, row, slot) and are bounded 32 at a
 // time (a lane each), at most kGfKeep rounds later -- their symbols are still in the ring.
 __global__ void __launch_bounds__(kGfThreads, 1)
-k_gf(LbArgs a, const GfParams* __restrict__ gp, float* __restrict__ dump, int swap_desc) {
+k_gf(LbArgs a, const GfParams* __restrict__ gp, float* __restrict__ dump, int swap_desc,
+     const __grid_constant__ CUtensorMap tmap) {
   if (gp->ok == 0u) return;
   extern __shared__ uint8_t dsm_raw[];
   const uint32_t S0 = (smem_u32(dsm_raw) + 1023u) & ~1023u;
@@ -329,7 +339,7 @@ k_gf(LbArgs a, const GfParams* __restrict__ gp, float* __restrict__ dump, int sw
   for (int i = tid; i < kGfN * 16; i += kGfThreads)
     M.q[i] = (i >> 4) < a.nb ? a.g_q[(i >> 4) * kMaxW + (i & 15)] : make_float2(0.f, 0.f);
   for (int i = tid; i < kGfN * kNBC; i += kGfThreads) M.hist[i] = 0;
-  {
+  if (warp < kGfWorkers / 32) {
     WarpBuf& wb0 = M.wb[warp];
     for (int b = lane; b < kMaxB; b += 32) wb0.cnt[b] = 0;
     if (lane == 0) wb0.n = 0;
@@ -340,37 +350,69 @@ k_gf(LbArgs a, const GfParams* __restrict__ gp, float* __restrict__ dump, int sw
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = M.tmem_base;
+  const int64_t nrounds = (a.n + kGfRound - 1) / kGfRound;
+  const int64_t gstride = (int64_t)gridDim.x * kGfWG;
+  constexpr uint32_t idesc = (1u << 4) | ((uint32_t)(kGfN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  constexpr int kRPT = kTS / kGfRound;  // rounds per index tile
+
+  if (warp == kGfWorkers / 32) {
+    // ---- the issuing warp: for every warpgroup in turn, once its four warps have written the A
+    // tile of round i (and read the accumulators of round i - 2), the three MMAs of round i and
+    // the SAX copy of round i + kGfAhead (into the stage of round i + kGfAhead - kGfStages: no
+    // warp holds a survivor that old).  One 2-D tensor-map copy per stage: 16 rows x 128 bytes.
+    int cnts[kGfWG];
+    int cmax = 0;
+#pragma unroll
+    for (int gg = 0; gg < kGfWG; ++gg) {
+      const int64_t gw2 = (int64_t)blockIdx.x * kGfWG + gg;
+      cnts[gg] = gw2 < nrounds ? (int)((nrounds - gw2 + gstride - 1) / gstride) : 0;
+      cmax = cnts[gg] > cmax ? cnts[gg] : cmax;
+    }
+    auto load = [&](int gg, int i) {
+      const int64_t round = (int64_t)blockIdx.x * kGfWG + gg + (int64_t)i * gstride;
+      const int st = i % kGfStages;
+      // index: rows of [tile][16][2048] (whole tiles allocated); flat: [16][n], columns past n zero-filled
+      const int c0 = a.perm ? (int)(round % kRPT) * kGfRound : (int)(round * kGfRound);
+      const int c1 = a.perm ? (int)(round / kRPT) * 16 : 0;
+      mbar_expect_tx(&M.full[gg][st], kGfStageBytes);
+      tma_tile_2d(s_stage + (uint32_t)(gg * kGfStages + st) * kGfStageBytes, &tmap, c0, c1, &M.full[gg][st]);
+    };
+    if (lane == 0) {
+      for (int i = 0; i < kGfAhead; ++i)
+#pragma unroll
+        for (int gg = 0; gg < kGfWG; ++gg)
+          if (i < cnts[gg]) load(gg, i);
+    }
+    for (int i = 0; i < cmax; ++i) {
+#pragma unroll
+      for (int gg = 0; gg < kGfWG; ++gg) {
+        if (i >= cnts[gg]) continue;
+        mbar_wait(&M.ready[gg][i & 1], (unsigned)(i >> 1) & 1u);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t At = s_A + (uint32_t)(gg * 2 + (i & 1)) * kGfATile;
+          const uint32_t d = tmem + (uint32_t)gg * 128u + (uint32_t)(i & 1) * kGfN;
+          const uint32_t la = swap_desc ? kGfASbo : 128u, sa = swap_desc ? 128u : kGfASbo;
+          const uint32_t lb = swap_desc ? kGfBSbo : 128u, sb = swap_desc ? 128u : kGfBSbo;
+          const uint32_t l2 = swap_desc ? kGfA2Sbo : 128u, s2 = swap_desc ? 128u : kGfA2Sbo;
+          tc_mma_f16(d, gf_desc(At, la, sa), gf_desc(s_B, lb, sb), idesc, 0u);
+          tc_mma_f16(d, gf_desc(At + 256u, la, sa), gf_desc(s_B + 256u, lb, sb), idesc, 1u);
+          tc_mma_f16(d, gf_desc(s_A2, l2, s2), gf_desc(s_B + 512u, lb, sb), idesc, 1u);
+          tc_commit(&M.mma[gg][i & 1]);
+          if (i + kGfAhead < cnts[gg]) load(gg, i + kGfAhead);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
   WarpBuf& wb = M.wb[warp];
   uint32_t* const hq = M.hq[warp];
   const LbConsts& c = M.c;
-
-  const int64_t nrounds = (a.n + kGfRound - 1) / kGfRound;
-  const int64_t gw = (int64_t)blockIdx.x * kGfWG + g, gstride = (int64_t)gridDim.x * kGfWG;
+  const int64_t gw = (int64_t)blockIdx.x * kGfWG + g;
   const int cnt = gw < nrounds ? (int)((nrounds - gw + gstride - 1) / gstride) : 0;  // this warpgroup's rounds
   const uint32_t my_stage0 = s_stage + (uint32_t)g * kGfStages * kGfStageBytes;
   const uint32_t my_A = s_A + (uint32_t)g * 2 * kGfATile;
   const uint32_t my_tmem = tmem + (uint32_t)g * 128u + ((uint32_t)(32 * (warp & 3)) << 16);
-  constexpr uint32_t idesc = (1u << 4) | ((uint32_t)(kGfN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-  constexpr int kRPT = kTS / kGfRound;  // rounds per index tile
-
-  // whole warp: lane 0 arms the stage's barrier, lanes 0..15 copy a 128-byte row each (the
-  // tile-major array is allocated in whole tiles)
-  auto issue_load = [&](int i) {
-    const int64_t round = gw + (int64_t)i * gstride;
-    const int st = i % kGfStages;
-    // index: tile-major [tile][16][2048] (whole tiles allocated); flat: [16][n]
-    const uint8_t* src = a.perm ? a.sax + (size_t)(round / kRPT) * kTileBytes + (size_t)(round % kRPT) * kGfRound
-                                : a.sax + (size_t)round * kGfRound;
-    const size_t rstride = a.perm ? (size_t)kTS : (size_t)a.n;
-    const unsigned bytes = a.perm ? (unsigned)kGfRound : (unsigned)imin64(kGfRound, a.n - round * kGfRound);
-    if (lane == 0) mbar_expect_tx(&M.full[g][st], bytes * 16u);
-    __syncwarp();
-    if (lane < 16)
-      bulk_g2s(gbase + my_stage0 + (uint32_t)st * kGfStageBytes + (uint32_t)lane * kGfRound, src + (size_t)lane * rstride,
-               bytes, &M.full[g][st]);
-  };
-  if ((warp & 3) == 0)
-    for (int i = 0; i < kGfAhead && i < cnt; ++i) issue_load(i);
 
   // survivor queue (ring of kGfQ entries): entry = round index << 11 | lane << 6 | slot
   unsigned qhead = 0, qcount = 0;  // warp-uniform registers
@@ -432,26 +474,6 @@ k_gf(LbArgs a, const GfParams* __restrict__ gp, float* __restrict__ dump, int sw
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&M.ready[g][i & 1]);  // this warp: A(i) rows written, accumulators of round i - 2 read
-      if ((warp & 3) == (i & 3)) {
-        // this round's issuer (the warps take turns): all four warps ready -> the three MMAs of
-        // round i, then the SAX copy of round i + kGfAhead (into the stage of round
-        // i + kGfAhead - kGfStages: no warp holds a survivor that old)
-        mbar_wait(&M.ready[g][i & 1], (unsigned)(i >> 1) & 1u);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t At = my_A + (uint32_t)(i & 1) * kGfATile;
-          const uint32_t d = tmem + (uint32_t)g * 128u + (uint32_t)(i & 1) * kGfN;
-          const uint32_t la = swap_desc ? kGfASbo : 128u, sa = swap_desc ? 128u : kGfASbo;
-          const uint32_t lb = swap_desc ? kGfBSbo : 128u, sb = swap_desc ? 128u : kGfBSbo;
-          const uint32_t l2 = swap_desc ? kGfA2Sbo : 128u, s2 = swap_desc ? 128u : kGfA2Sbo;
-          tc_mma_f16(d, gf_desc(At, la, sa), gf_desc(s_B, lb, sb), idesc, 0u);
-          tc_mma_f16(d, gf_desc(At + 256u, la, sa), gf_desc(s_B + 256u, lb, sb), idesc, 1u);
-          tc_mma_f16(d, gf_desc(s_A2, l2, s2), gf_desc(s_B + 512u, lb, sb), idesc, 1u);
-          tc_commit(&M.mma[g][i & 1]);
-        }
-        __syncwarp();
-        if (i + kGfAhead < cnt) issue_load(i + kGfAhead);
-      }
     }
     if (i == 0) continue;
     // ---- epilogue of round i - 1: the sign of each accumulator
@@ -468,13 +490,19 @@ k_gf(LbArgs a, const GfParams* __restrict__ gp, float* __restrict__ dump, int sw
       }
       continue;
     }
-    uint32_t m0 = 0, m1 = 0;
+    uint32_t m0, m1;
+    {
+      uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;  // four independent chains of 16 sign bits
 #pragma unroll
-    for (int k = 0; k < 32; ++k) m0 = __funnelshift_l(v[k], m0, 1);
-#pragma unroll
-    for (int k = 32; k < 64; ++k) m1 = __funnelshift_l(v[k], m1, 1);
-    m0 = __brev(m0);  // bit k: slot k
-    m1 = __brev(m1);  // bit k: slot 32 + k
+      for (int k = 0; k < 16; ++k) {
+        c0 = __funnelshift_l(v[k], c0, 1);
+        c1 = __funnelshift_l(v[16 + k], c1, 1);
+        c2 = __funnelshift_l(v[32 + k], c2, 1);
+        c3 = __funnelshift_l(v[48 + k], c3, 1);
+      }
+      m0 = __brev((c0 << 16) | c1);  // bit k: slot k
+      m1 = __brev((c2 << 16) | c3);  // bit k: slot 32 + k
+    }
     if (pos >= a.n) { m0 = 0; m1 = 0; }
     // ---- queue the survivors, one per lane per turn
     while (__any_sync(0xffffffffu, (m0 | m1) != 0u)) {
@@ -499,6 +527,7 @@ k_gf(LbArgs a, const GfParams* __restrict__ gp, float* __restrict__ dump, int sw
     while (qcount) drain(qcount < 32u ? qcount : 32u);
     gf_flush(wb, nslots, c, a, M.hist);
   }
+  }  // worker warps
   tc_fence_before();
   __syncthreads();
   if (!dump)

@@ -26,6 +26,7 @@
 // d^2 scaled by d2up), so pruning never drops a series of the exact answer.
 #include "runtime.cuh"
 
+#include <cuda.h>
 #include <cuda_fp16.h>
 
 #include <algorithm>
@@ -4207,14 +4208,46 @@ cudaError_t gf_attr() {
     return cudaFuncSetAttribute(k_gf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGfSmem);
   });
 }
-cudaError_t launch_gf(const LbArgs& la, int card, GfParams* gp, cudaStream_t st) {
+// 2-D tensor map of the SAX array for k_gf's stage copies (box: 128 series x 16 segment rows).
+// Index layout: [tile][16][2048] seen as 16 * ntiles rows of 2048 bytes; flat layout: 16 rows of n bytes.
+cudaError_t gf_tensor_map(const LbArgs& la, CUtensorMap* tm) {
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode enc = []() -> Encode {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess ||
+        qr != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return (Encode)fn;
+  }();
+  if (!enc) return cudaErrorNotSupported;
+  const int64_t ntiles = (la.n + kTS - 1) / kTS;
+  cuuint64_t dims[2], strides[1];
+  if (la.perm) { dims[0] = kTS; dims[1] = (cuuint64_t)(16 * ntiles); strides[0] = kTS; }
+  else { dims[0] = (cuuint64_t)la.n; dims[1] = 16; strides[0] = (cuuint64_t)la.n; }
+  const cuuint32_t box[2] = {(cuuint32_t)kGfRound, 16u}, es[2] = {1u, 1u};
+  const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(la.sax), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+cudaError_t launch_gf_kernel(const char* name, const LbArgs& la, const GfParams* gp, float* dump, int swap_desc,
+                             cudaStream_t st) {
   cudaError_t e = gf_attr();
   if (e != cudaSuccess) return e;
-  e = PARIS_LAUNCH("lb_prep", k_gf_prep, 1, 256, 0, st, la, card, gp);
+  CUtensorMap tm;
+  e = gf_tensor_map(la, &tm);
   if (e != cudaSuccess) return e;
   const int64_t nrounds = (la.n + kGfRound - 1) / kGfRound;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(device_sms(), (nrounds + kGfWG - 1) / kGfWG));
-  return PARIS_LAUNCH("lb_pass", k_gf, grid, kGfThreads, kGfSmem, st, la, gp, (float*)nullptr, 0);
+  return PARIS_LAUNCH(name, k_gf, grid, kGfThreads, kGfSmem, st, la, gp, dump, swap_desc, tm);
+}
+cudaError_t launch_gf(const LbArgs& la, int card, GfParams* gp, cudaStream_t st) {
+  const cudaError_t e = PARIS_LAUNCH("lb_prep", k_gf_prep, 1, 256, 0, st, la, card, gp);
+  if (e != cudaSuccess) return e;
+  return launch_gf_kernel("lb_pass", la, gp, nullptr, 0, st);
 }
 
 template <int P, bool HC, int NW>
@@ -4893,7 +4926,7 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   p.tiled = (n % 16 == 0) && (w == kTW) && (indexed || !(cfg && cfg->reserved[0] == 1));
   // tensor-core filter (variant key 3): 2 (default) = flat path only, 1 = index path too, 0 = off
   p.gf = (g_variant[3] == 1 || (g_variant[3] == 2 && !indexed)) && p.tiled && !nb_mode && !approx &&
-         !(cfg && cfg->reserved[1] == 1);
+         !(cfg && cfg->reserved[1] == 1) && (reinterpret_cast<uintptr_t>(sax) & 15) == 0;
   {
     // index: 64 queries per pass; flat: 16 (k_lbt), 64 behind the tensor-core filter
     const int cap_b = (indexed || p.gf) ? kMaxB : kMaxBFlat;
@@ -5094,12 +5127,7 @@ int debug_gf_mma(const uint8_t* sax_sorted, int64_t n, const uint32_t* tabw, con
   LbArgs la{};
   la.sax = sax_sorted; la.n = n; la.w = 16; la.seglen_f = 16.f; la.tab = tab; la.nb = 0;
   la.perm = reinterpret_cast<const uint32_t*>(sax_sorted);  // tile-major layout (never read: no candidates here)
-  cudaError_t e = gf_attr();
-  if (e == cudaSuccess) {
-    const int64_t nrounds = (n + kGfRound - 1) / kGfRound;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(device_sms(), (nrounds + kGfWG - 1) / kGfWG));
-    e = PARIS_LAUNCH("gf_debug", k_gf, grid, kGfThreads, kGfSmem, st, la, gp, out, swap_desc);
-  }
+  cudaError_t e = launch_gf_kernel("gf_debug", la, gp, out, swap_desc, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   cudaFree(gp);
   return e == cudaSuccess ? PARIS_OK : cuda_error(e, "paris_debug_gf_mma");
