@@ -33,7 +33,7 @@ for _k in ("PARIS_LBI_GROUPS", "PARIS_REF_RUN", "PARIS_REFQ_CTAS", "PARIS_REFU_C
 if os.environ.get("PARIS_DEBUG"):  # device bounds checks (PARIS_DCHECK) -- debugging builds only
     FLAGS = FLAGS + ["-DPARIS_DEBUG_CHECKS"]
 SOURCES = ["runtime.cu", "summarize.cu", "knn.cu", "index.cu", "merge.cu", "select.cu"]
-HEADERS = ["runtime.cuh"]
+HEADERS = ["runtime.cuh", "gfilter.cuh"]
 
 
 def _newer(target: str, deps) -> bool:

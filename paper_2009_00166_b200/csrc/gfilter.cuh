@@ -28,7 +28,7 @@ constexpr int kGfK = 48;            // K: 16 x (c, g) + 16 for the per-query con
 constexpr int kGfRound = 128;       // series per warpgroup round (one 128-row MMA tile)
 constexpr int kGfWG = 4;            // warpgroups per CTA, each an independent pipeline
 constexpr int kGfWorkers = 128 * kGfWG;
-constexpr int kGfThreads = kGfWorkers + 32;  // + the issuing warp (MMAs, SAX copies)
+constexpr int kGfThreads = kGfWorkers + 32 * kGfWG;  // + an issuing warp per warpgroup (MMAs, SAX copies)
 constexpr int kGfStages = 8;        // SAX stages per warpgroup (queued survivors read their symbols later)
 constexpr int kGfAhead = 3;         // rounds whose SAX copy is in flight
 constexpr int kGfKeep = 3;          // a survivor waits at most this many rounds in its warp's queue
@@ -100,6 +100,16 @@ __device__ __forceinline__ void tc_ld64(uint32_t taddr, uint32_t (&v)[64]) {
         "=r"(v[57]), "=r"(v[58]), "=r"(v[59]), "=r"(v[60]), "=r"(v[61]), "=r"(v[62]), "=r"(v[63])
       : "r"(taddr)
       : "memory");
+}
+// non-blocking phase test of an mbarrier
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0u;
 }
 // one 2-D tile (box of the tensor map) global -> shared, completing on an mbarrier
 __device__ __forceinline__ void tma_tile_2d(uint32_t dst, const void* tmap, int c0, int c1, uint64_t* bar) {
@@ -355,21 +365,17 @@ k_gf(LbArgs a, const GfParams* __restrict__ gp, float* __restrict__ dump, int sw
   constexpr uint32_t idesc = (1u << 4) | ((uint32_t)(kGfN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   constexpr int kRPT = kTS / kGfRound;  // rounds per index tile
 
-  if (warp == kGfWorkers / 32) {
-    // ---- the issuing warp: for every warpgroup in turn, once its four warps have written the A
-    // tile of round i (and read the accumulators of round i - 2), the three MMAs of round i and
-    // the SAX copy of round i + kGfAhead (into the stage of round i + kGfAhead - kGfStages: no
-    // warp holds a survivor that old).  One 2-D tensor-map copy per stage: 16 rows x 128 bytes.
-    int cnts[kGfWG];
-    int cmax = 0;
-#pragma unroll
-    for (int gg = 0; gg < kGfWG; ++gg) {
-      const int64_t gw2 = (int64_t)blockIdx.x * kGfWG + gg;
-      cnts[gg] = gw2 < nrounds ? (int)((nrounds - gw2 + gstride - 1) / gstride) : 0;
-      cmax = cnts[gg] > cmax ? cnts[gg] : cmax;
-    }
-    auto load = [&](int gg, int i) {
-      const int64_t round = (int64_t)blockIdx.x * kGfWG + gg + (int64_t)i * gstride;
+  if (warp >= kGfWorkers / 32) {
+    // ---- the issuing warp of warpgroup gg: once the group's four warps have written the A tile
+    // of round i (and read the accumulators of round i - 2), the three MMAs of round i and the
+    // SAX copy of round i + kGfAhead (into the stage of round i + kGfAhead - kGfStages: no warp
+    // holds a survivor that old).  One 2-D tensor-map copy per stage: 16 rows x 128 bytes.  (One
+    // warp serving all four groups was the bottleneck: ~580 cycles per round served.)
+    const int gg = warp - kGfWorkers / 32;
+    const int64_t gw2 = (int64_t)blockIdx.x * kGfWG + gg;
+    const int cnt2 = gw2 < nrounds ? (int)((nrounds - gw2 + gstride - 1) / gstride) : 0;
+    auto load = [&](int i) {
+      const int64_t round = gw2 + (int64_t)i * gstride;
       const int st = i % kGfStages;
       // index: rows of [tile][16][2048] (whole tiles allocated); flat: [16][n], columns past n zero-filled
       const int c0 = a.perm ? (int)(round % kRPT) * kGfRound : (int)(round * kGfRound);
@@ -377,32 +383,26 @@ k_gf(LbArgs a, const GfParams* __restrict__ gp, float* __restrict__ dump, int sw
       mbar_expect_tx(&M.full[gg][st], kGfStageBytes);
       tma_tile_2d(s_stage + (uint32_t)(gg * kGfStages + st) * kGfStageBytes, &tmap, c0, c1, &M.full[gg][st]);
     };
-    if (lane == 0) {
-      for (int i = 0; i < kGfAhead; ++i)
-#pragma unroll
-        for (int gg = 0; gg < kGfWG; ++gg)
-          if (i < cnts[gg]) load(gg, i);
-    }
-    for (int i = 0; i < cmax; ++i) {
-#pragma unroll
-      for (int gg = 0; gg < kGfWG; ++gg) {
-        if (i >= cnts[gg]) continue;
-        mbar_wait(&M.ready[gg][i & 1], (unsigned)(i >> 1) & 1u);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t At = s_A + (uint32_t)(gg * 2 + (i & 1)) * kGfATile;
-          const uint32_t d = tmem + (uint32_t)gg * 128u + (uint32_t)(i & 1) * kGfN;
-          const uint32_t la = swap_desc ? kGfASbo : 128u, sa = swap_desc ? 128u : kGfASbo;
-          const uint32_t lb = swap_desc ? kGfBSbo : 128u, sb = swap_desc ? 128u : kGfBSbo;
-          const uint32_t l2 = swap_desc ? kGfA2Sbo : 128u, s2 = swap_desc ? 128u : kGfA2Sbo;
-          tc_mma_f16(d, gf_desc(At, la, sa), gf_desc(s_B, lb, sb), idesc, 0u);
-          tc_mma_f16(d, gf_desc(At + 256u, la, sa), gf_desc(s_B + 256u, lb, sb), idesc, 1u);
-          tc_mma_f16(d, gf_desc(s_A2, l2, s2), gf_desc(s_B + 512u, lb, sb), idesc, 1u);
-          tc_commit(&M.mma[gg][i & 1]);
-          if (i + kGfAhead < cnts[gg]) load(gg, i + kGfAhead);
-        }
-        __syncwarp();
+    const uint32_t la = swap_desc ? kGfASbo : 128u, sa = swap_desc ? 128u : kGfASbo;
+    const uint32_t lb = swap_desc ? kGfBSbo : 128u, sb = swap_desc ? 128u : kGfBSbo;
+    const uint32_t l2 = swap_desc ? kGfA2Sbo : 128u, s2 = swap_desc ? 128u : kGfA2Sbo;
+    const uint64_t dB0 = gf_desc(s_B, lb, sb), dB1 = gf_desc(s_B + 256u, lb, sb), dB2 = gf_desc(s_B + 512u, lb, sb);
+    const uint64_t dA2 = gf_desc(s_A2, l2, s2);
+    if (lane == 0)
+      for (int i = 0; i < kGfAhead && i < cnt2; ++i) load(i);
+    for (int i = 0; i < cnt2; ++i) {
+      mbar_wait(&M.ready[gg][i & 1], (unsigned)(i >> 1) & 1u);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t At = s_A + (uint32_t)(gg * 2 + (i & 1)) * kGfATile;
+        const uint32_t d = tmem + (uint32_t)gg * 128u + (uint32_t)(i & 1) * kGfN;
+        tc_mma_f16(d, gf_desc(At, la, sa), dB0, idesc, 0u);
+        tc_mma_f16(d, gf_desc(At + 256u, la, sa), dB1, idesc, 1u);
+        tc_mma_f16(d, dA2, dB2, idesc, 1u);
+        tc_commit(&M.mma[gg][i & 1]);
+        if (i + kGfAhead < cnt2) load(i + kGfAhead);
       }
+      __syncwarp();
     }
   } else {
   WarpBuf& wb = M.wb[warp];
@@ -517,11 +517,10 @@ k_gf(LbArgs a, const GfParams* __restrict__ gp, float* __restrict__ dump, int sw
       qcount += (unsigned)__popc(bal);
       __syncwarp();
     }
-    while (qcount >= 32u) drain(32u);
-    if (qcount) {
-      const int oldest = (int)(hq[qhead] >> 11);
-      if (oldest <= ri - kGfKeep + 1) drain(qcount);
-    }
+    // every warp bounds its queued survivors in the same rounds (every kGfKeep-th): a warp that
+    // drained alone held up its warpgroup's next MMA while the other three waited
+    if (ri % kGfKeep == kGfKeep - 1)
+      while (qcount) drain(qcount < 32u ? qcount : 32u);
   }
   if (!dump) {
     while (qcount) drain(qcount < 32u ? qcount : 32u);
