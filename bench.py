@@ -650,7 +650,8 @@ def run_gpu(args):
                 roof = {"kernel": dom + " (k_gf)", "bound": "alu", "achieved": ach, "unit": "T lane-ops/s (ALU pipe)",
                         "peak": pk_alu, "frac": ach / pk_alu,
                         "peak_source": f"derived: 148 SM x 64 ALU-pipe lanes/clk x {ALU_CLOCK_GHZ} GHz",
-                        "traffic": None, "algorithmic_ops_per_batch": ops, "ms_per_batch": per_launch_ms,
+                        "traffic": ncu_traffic("lb_pass_gf", args.config), "algorithmic_ops_per_batch": ops,
+                        "ms_per_batch": per_launch_ms,
                         "tensor_tflops": 2.0 * n_local * 64 * 48 / (per_launch_ms / 1e3) / 1e12,
                         "hbm_achieved_gbs": alg[dom] / (per_launch_ms / 1e3) / 1e9, "hbm_peak_gbs": peak,
                         "queries_per_pass": q_per_pass}

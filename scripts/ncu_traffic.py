@@ -31,7 +31,8 @@ def dram(rep):
 
 
 res = {"lib_sha16": sha, "C4": {}}
-for name, key in (("k_lbi", "lb_pass_index"), ("k_refine1m", "refine_index"), ("k_summarize_seg", "summarize")):
+for name, key in (("k_lbi", "lb_pass_index"), ("k_refine1m", "refine_index"), ("k_summarize_seg", "summarize"),
+                  ("k_gf", "lb_pass_gf")):
     v = dram(os.path.join(out_dir, f"full_c4_{name}.ncu-rep"))
     if v is not None:
         res["C4"][key] = v
