@@ -27,4 +27,8 @@ run(6000 * 16 + 48, 256, 3, 10, True)             # index, ragged last tile, k >
 run(40_000, 256, 33, 1, True)                     # index, two batches (32 + 1)
 run(70_000, 128, 2, 1000, True, P.KnnConfig(index_seeds=1), zero_q=True)   # index overflow re-scan
 run(70_000, 128, 2, 1000, False, P.KnnConfig(seed_div=70_000), zero_q=True)  # flat overflow re-scan
+run(4096 + 48, 256, 40, 2, False)                 # flat behind the tensor-core filter (k_gf), sub-batches 16+16+8
+P.debug_set_variant(3, 1)
+run(6000 * 16 + 48, 256, 40, 1, True)             # index path through k_gf
+P.debug_set_variant(3, 2)
 print("all ok")
