@@ -578,18 +578,20 @@ def run_gpu(args):
             # listed (a host-side stall of tens of ms -- another process, a page fault -- lands in one
             # of them; every step synchronizes, so the host is on the critical path here)
             reps, step_max = [], 0.0
-            for _rep in range(3):
-                if ws > 1:
-                    dist.barrier()
-                torch.cuda.synchronize()
-                e0.record(st)
-                for _ in range(args.steps):
-                    t0 = time.perf_counter()
-                    step_e2e()
-                    step_max = max(step_max, (time.perf_counter() - t0) * 1e3)
-                e1.record(st)
-                torch.cuda.synchronize()
-                reps.append(reduce_max_ms(e0.elapsed_time(e1) / args.steps, dev, ws))
+            with ClockSampler(local) as clocks_e2e:
+                for _rep in range(3):
+                    if ws > 1:
+                        dist.barrier()
+                    torch.cuda.synchronize()
+                    e0.record(st)
+                    for _ in range(args.steps):
+                        t0 = time.perf_counter()
+                        step_e2e()
+                        step_max = max(step_max, (time.perf_counter() - t0) * 1e3)
+                    e1.record(st)
+                    torch.cuda.synchronize()
+                    reps.append(reduce_max_ms(e0.elapsed_time(e1) / args.steps, dev, ws))
+            r["e2e_clocks"] = clocks_e2e.summary()
             r["e2e_reps_ms"] = reps
             r["e2e_step_max_ms"] = step_max
             r["e2e_value"] = (nq if sharded else nq * ws) / (sorted(reps)[1] / 1e3)
@@ -820,7 +822,7 @@ def run_gpu(args):
             "cpu_baseline": cpu,
             "sweep": sweep,
             "e2e": {"value": e2e_value, "unit": "queries/s", "ms_per_step_repetitions": primary.get("e2e_reps_ms"),
-                    "slowest_step_ms": primary.get("e2e_step_max_ms"), "h2d_bytes_per_step": nq * length * 4,
+                    "slowest_step_ms": primary.get("e2e_step_max_ms"), "clocks": primary.get("e2e_clocks"), "h2d_bytes_per_step": nq * length * 4,
                     "d2h_bytes_per_step": nq * k * 12},
             "gpu_launches": launches,
             "clocks": clocks,
