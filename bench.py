@@ -496,7 +496,8 @@ def run_gpu(args):
         P.debug_set_variant(3, gfv)
         gf_on = (gfv == 1) or (gfv == 2 and not use_idx)  # the pass runs through the tensor-core filter (k_gf)
         b_path = args.batch or (64 if (use_idx or gf_on) else 16)  # the library's default queries per pass
-        kcfg = P.KnnConfig(batch=b_path, index_seeds=args.index_seeds, sorted_refine=args.sorted_refine)
+        kcfg = P.KnnConfig(batch=b_path, index_seeds=args.index_seeds, sorted_refine=args.sorted_refine,
+                           seed_div=args.seed_div)
         nbatches = sum((min(call_q, nq - c0) + b_path - 1) // b_path for c0 in range(0, nq, call_q))
         q_per_pass = nq / nbatches
         search = local_fn(path, kcfg)
@@ -859,6 +860,7 @@ def main():
     ap.add_argument("--config", type=int, default=4, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="paris", choices=["paris", "reference"])
     ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--seed-div", type=int, default=0, help="flat path: seed sample = n / seed_div (0: the library default)")
     ap.add_argument("--index-seeds", type=int, default=0, help="index path: seed series around the leaf")
     ap.add_argument("--both", type=int, default=1, help="also time the other query path (reported as a sub-object)")
     ap.add_argument("--path", default="index", choices=["flat", "index", "nb"],
