@@ -258,7 +258,7 @@ struct GfShared {
   uint32_t tmem_base;
   LbConsts c;
   float2 lu[kMaxCard];
-  float2 q[kGfN * 16];
+  float2 q[kGfN * 17];  // row stride 17: lanes bounding different slots read different banks
   unsigned hist[kGfN * kNBC];
   uint32_t hq[kGfWorkers / 32][kGfQ];
   WarpBuf wb[kGfWorkers / 32];
@@ -347,7 +347,7 @@ k_gf(LbArgs a, const GfParams* __restrict__ gp, float* __restrict__ dump, int sw
   }
   for (int i = tid; i < kMaxCard; i += kGfThreads) M.lu[i] = a.tab->lu[i];
   for (int i = tid; i < kGfN * 16; i += kGfThreads)
-    M.q[i] = (i >> 4) < a.nb ? a.g_q[(i >> 4) * kMaxW + (i & 15)] : make_float2(0.f, 0.f);
+    M.q[(i >> 4) * 17 + (i & 15)] = (i >> 4) < a.nb ? a.g_q[(i >> 4) * kMaxW + (i & 15)] : make_float2(0.f, 0.f);
   for (int i = tid; i < kGfN * kNBC; i += kGfThreads) M.hist[i] = 0;
   if (warp < kGfWorkers / 32) {
     WarpBuf& wb0 = M.wb[warp];
@@ -429,7 +429,7 @@ k_gf(LbArgs a, const GfParams* __restrict__ gp, float* __restrict__ dump, int sw
       for (int j = 0; j < 16; ++j) {
         const uint32_t sym = lds_u8(stage + (uint32_t)j * kGfRound);
         const float2 lu = M.lu[sym];
-        const float2 q = M.q[b * 16 + j];
+        const float2 q = M.q[b * 17 + j];
         const float d = fmaxf(fmaxf(__fsub_rd(lu.x, q.y), __fsub_rd(q.x, lu.y)), 0.f);
         acc = __fmaf_rd(d, d, acc);
       }
