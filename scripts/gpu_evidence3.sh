@@ -5,7 +5,7 @@
 # roofline.traffic of this very build), then the default bench line, every config, the
 # reference arm and torchrun N=1 (sharded path).  OUT=gpurun_out/<tag>
 cd "$GRAFT_REPO_ROOT" || exit 1
-OUT=${OUT:-gpurun_out/ev5}
+OUT=${OUT:-gpurun_out/ev6}
 mkdir -p $OUT
 (free -g; nproc; lscpu | grep -i "model name"; nvidia-smi --query-gpu=name,clocks.max.sm --format=csv) > $OUT/box.txt 2>&1
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
