@@ -30,6 +30,8 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <chrono>
+#include <mutex>
 #include <vector>
 
 namespace paris {
@@ -4980,8 +4982,27 @@ int knn_impl(const float* raw, const uint8_t* sax, int64_t n, const float* queri
   {
     const int Bq = 2 * pairs_for(p.B);
     const int64_t floor_cap = std::max<int64_t>(65536, k > 1 ? n / 16 : n / 32);
-    size_t fr = 0, tot = 0;
-    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); fr = 0; }
+    // free device memory, sampled at most once per second per device: cudaMemGetInfo takes 0.08 ms
+    // at the median but 7 ms at p99 and up to 27 ms (scripts/exp_host_latency.py) -- a stall in
+    // every hundredth call of a synchronous caller
+    size_t fr = 0;
+    {
+      static std::mutex mu;
+      static size_t cached_free[64] = {0};
+      static std::chrono::steady_clock::time_point stamp[64];
+      int dev = 0;
+      cudaGetDevice(&dev);
+      dev = (dev >= 0 && dev < 64) ? dev : 0;
+      std::lock_guard<std::mutex> lk(mu);
+      const auto now = std::chrono::steady_clock::now();
+      if (cached_free[dev] == 0 || now - stamp[dev] > std::chrono::seconds(1)) {
+        size_t f2 = 0, tot = 0;
+        if (cudaMemGetInfo(&f2, &tot) != cudaSuccess) { cudaGetLastError(); f2 = 0; }
+        cached_free[dev] = f2;
+        stamp[dev] = now;
+      }
+      fr = cached_free[dev];
+    }
     // (whole GB: the workspace the first call allocates barely moves the budget of the next)
     const int64_t bud_bytes =
         std::min<int64_t>(16ll << 30, std::max<int64_t>(2ll << 30, (int64_t)(fr / 8) & ~((1ll << 30) - 1)));
